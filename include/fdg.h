@@ -1,0 +1,211 @@
+/*
+ * fdg.h -- C ABI of the B200-native GNNDrive sample -> extract path.
+ *
+ * This is the drop-in boundary: the reference (featdrive, header-only C++20)
+ * has no FFI of its own, so each entry point below replaces one concrete
+ * reference interface (cited file:line, relative to
+ * /root/reference/proj/include/featdrive). Plain pointers and sizes only.
+ * Pointers suffixed `_dev` are device (HBM) pointers; `stream` is a
+ * cudaStream_t passed as void* (NULL = the legacy default stream).
+ *
+ * Error convention: every function returns an fdg_status; on failure a
+ * thread-local message is available from fdg_last_error(). Reference exception
+ * types map as: std::out_of_range -> FDG_OUT_OF_RANGE, std::invalid_argument ->
+ * FDG_INVALID_ARG, InvariantViolation -> FDG_INVARIANT, StandbyTimeout ->
+ * FDG_CAPACITY. The C++ shim (include/featdrive_gpu.hpp) rethrows those types.
+ * Asynchronous calls report device-detected errors through fdg_batch_counts.status.
+ */
+#ifndef FDG_H
+#define FDG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FDG_MAX_LAYERS 8
+
+typedef enum {
+    FDG_OK = 0,
+    FDG_OUT_OF_RANGE = 1, /* seed / node id >= num_nodes   (sampling.hpp:90-91, feature_file.hpp:74-76) */
+    FDG_INVALID_ARG = 2,  /* bad fanouts / config          (sampling.hpp:24-28, pipeline.hpp:56-65)    */
+    FDG_INVARIANT = 3,    /* buffer-manager invariant      (common.hpp:57-65, buffer_manager.hpp:478)  */
+    FDG_CAPACITY = 4,     /* standby list / arena exhausted (buffer_manager.hpp:274-279)               */
+    FDG_CUDA_ERROR = 5,
+    FDG_NOT_LOADED = 6,   /* topology / features not resident yet                                        */
+    FDG_REJECTION = 7     /* internal: Lemire rejection seen, batch re-run exactly (never user visible) */
+} fdg_status;
+
+typedef struct fdg_ctx fdg_ctx;         /* device + resident CSC topology + feature table (shards)   */
+typedef struct fdg_sampler fdg_sampler; /* per-stream sampling workspace                             */
+typedef struct fdg_bm fdg_bm;           /* GPU feature-buffer manager                                */
+
+/* Device-written per-batch record (the async counterpart of SampledBatch sizes,
+ * pipeline/stats.hpp:19-25 BatchRecord, plus per-layer block offsets). */
+typedef struct {
+    uint32_t status;        /* fdg_status of the batch (device-detected)                         */
+    uint32_t n_nodes;       /* SampledBatch.nodes.size()                                          */
+    uint32_t n_edges;       /* SampledBatch.edges.size()                                          */
+    uint32_t rejections;    /* Lemire rejections observed (0 in practice)                         */
+    uint64_t bad_seed;      /* first out-of-range seed when status == FDG_OUT_OF_RANGE             */
+    uint64_t checksum;      /* trainer_step checksum when a fused gather ran (pipeline.hpp:103-124) */
+    uint32_t bad_seed_pos;
+    uint32_t n_layers;
+    uint32_t layer_nodes[FDG_MAX_LAYERS + 2]; /* nodes before layer l's new nodes; [1] = #unique seeds */
+    uint32_t layer_edges[FDG_MAX_LAYERS + 1]; /* edges before layer l                               */
+    uint32_t layer_draws[FDG_MAX_LAYERS + 1]; /* MT19937-64 words before layer l                    */
+    uint32_t words_used;
+    uint32_t pad;
+} fdg_batch_counts;
+
+typedef struct {
+    uint64_t num_nodes;
+    uint64_t num_edges;
+    uint32_t idx_bytes;     /* 4 when num_nodes < 2^32 (indices stored as u32), else 8 */
+    uint32_t row_bytes;     /* feature row bytes (0 if no features)                    */
+    uint32_t dtype;         /* 0 = f32 (reference format, format.hpp:58-61), 1 = f16   */
+    uint32_t n_shards;
+    const void* indptr_dev; /* u64[num_nodes+1]                                         */
+    const void* indices_dev;
+    const void* table_dev;  /* shard 0 base (row-major, no header)                       */
+    uint64_t rows_per_shard;
+    int device;
+    int pad;
+} fdg_ctx_info;
+
+const char* fdg_last_error(void);
+int fdg_version(void);
+
+/* ---- device plumbing (so callers need no CUDA runtime of their own) ---------- */
+int fdg_device_count(int* n);
+int fdg_set_device(int device);
+int fdg_malloc(void** ptr_dev, uint64_t bytes);
+int fdg_free(void* ptr_dev);
+int fdg_host_alloc(void** ptr, uint64_t bytes); /* pinned */
+int fdg_host_free(void* ptr);
+int fdg_memcpy_h2d(void* dst_dev, const void* src, uint64_t bytes, void* stream);
+int fdg_memcpy_d2h(void* dst, const void* src_dev, uint64_t bytes, void* stream);
+int fdg_memcpy_d2d(void* dst_dev, const void* src_dev, uint64_t bytes, void* stream);
+int fdg_memset(void* dst_dev, int value, uint64_t bytes, void* stream);
+int fdg_stream_create(void** stream);
+int fdg_stream_destroy(void* stream);
+int fdg_stream_sync(void* stream);
+int fdg_device_sync(void);
+int fdg_event_create(void** ev);
+int fdg_event_destroy(void* ev);
+int fdg_event_record(void* ev, void* stream);
+int fdg_stream_wait_event(void* stream, void* ev);
+int fdg_event_elapsed_ms(void* start, void* end, float* ms);
+int fdg_event_sync(void* ev);
+int fdg_mem_info(uint64_t* free_bytes, uint64_t* total_bytes);
+
+/* ---- context: replaces graph::Topology (topology.hpp:33-193) and the feature
+ *      table reader storage::FeatureTable (feature_file.hpp:25-107) ------------- */
+int fdg_ctx_create(int device, fdg_ctx** out);
+int fdg_ctx_destroy(fdg_ctx* ctx);
+int fdg_ctx_info_get(const fdg_ctx* ctx, fdg_ctx_info* out);
+/* Host CSC arrays as in indptr.bin / indices.bin (format.hpp:9-12); validated like
+ * Topology::load_indptr (topology.hpp:76-105). */
+int fdg_ctx_load_topology(fdg_ctx* ctx, const uint64_t* indptr, uint64_t num_nodes,
+                          const uint64_t* indices, uint64_t num_edges);
+int fdg_ctx_load_topology_files(fdg_ctx* ctx, const char* dataset_dir);
+/* Bit-exact GPU port of storage::synthetic_in_degree / synthetic_in_neighbors
+ * (generator.hpp:85-121) building the CSC directly in HBM. */
+int fdg_ctx_generate_topology(fdg_ctx* ctx, uint64_t seed, uint64_t num_nodes, uint32_t avg_degree);
+/* Feature rows, packed by node id (format.hpp:42). */
+int fdg_ctx_load_features(fdg_ctx* ctx, const void* rows, uint64_t num_nodes, uint32_t row_bytes, uint32_t dtype);
+int fdg_ctx_load_features_file(fdg_ctx* ctx, const char* features_bin);
+/* Bit-exact GPU port of storage::synthetic_row (generator.hpp:65-81); dtype 1
+ * stores RN(f32 -> f16) of the same values. n_shards > 1 splits rows into
+ * contiguous blocks of ceil(N / n_shards) (owner = node / rows_per_shard). */
+int fdg_ctx_generate_features(fdg_ctx* ctx, uint64_t seed, uint64_t num_nodes, uint32_t dim, uint32_t dtype,
+                              uint32_t n_shards);
+/* Row-sharded table: shard s lives at bases[s] (local or NVLink peer pointer). */
+int fdg_ctx_set_feature_shards(fdg_ctx* ctx, const void* const* bases_dev, uint32_t n_shards,
+                               uint64_t rows_per_shard, uint64_t num_nodes, uint32_t row_bytes, uint32_t dtype);
+int fdg_ctx_download_topology(const fdg_ctx* ctx, uint64_t* indptr, void* indices /* idx_bytes each */);
+int fdg_ctx_download_rows(const fdg_ctx* ctx, uint64_t first, uint64_t count, void* out);
+
+/* ---- sampler: replaces graph::sample_khop (sampling.hpp:72-134) --------------- */
+/* Workspace for batches of <= max_seeds seeds with the given fanouts; fanouts are
+ * validated as Fanouts::validate (sampling.hpp:23-29). */
+int fdg_sampler_create(fdg_ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32_t n_layers,
+                       fdg_sampler** out);
+int fdg_sampler_destroy(fdg_sampler* s);
+/* Fanouts::max_batch_nodes (sampling.hpp:32-40) clamped to N (pipeline.hpp:69-71), and the edge bound. */
+int fdg_sampler_capacity(const fdg_sampler* s, uint64_t* max_nodes, uint64_t* max_edges);
+/* Asynchronous sample on `stream`. seeds_dev: u64[n_seeds]. Outputs: nodes_dev u64[cap],
+ * edges_dev u32[2*cap] as {src_local, dst_local} (LocalEdge, sampling.hpp:43-46),
+ * counts_dev: device fdg_batch_counts. cap must be >= fdg_sampler_capacity. */
+int fdg_sample_khop(fdg_sampler* s, void* stream, const uint64_t* seeds_dev, uint32_t n_seeds,
+                    uint64_t rng_seed, uint64_t* nodes_dev, uint32_t* edges_dev, uint64_t cap,
+                    fdg_batch_counts* counts_dev);
+/* Pre-generate the MT19937-64 streams of upcoming batches on `stream` (off the
+ * critical path); a later fdg_sample_khop with the same rng_seed consumes them. */
+int fdg_sampler_prefetch(fdg_sampler* s, void* stream, const uint64_t* rng_seeds, uint32_t n);
+/* Synchronous convenience with host buffers and the reference's exact error
+ * behaviour (first out-of-range seed in order -> FDG_OUT_OF_RANGE). A batch that
+ * hit a Lemire rejection is transparently re-run in the exact (serialised
+ * offset) mode. layer_nodes[L+2] / layer_edges[L+1] may be NULL. */
+int fdg_sample_khop_host(fdg_sampler* s, const uint64_t* seeds, uint32_t n_seeds, uint64_t rng_seed,
+                         uint64_t* nodes, uint32_t* edges, uint64_t cap, uint64_t* n_nodes, uint64_t* n_edges,
+                         uint64_t* layer_nodes, uint64_t* layer_edges);
+/* Test hook: as fdg_sample_khop_host but drawing from an explicit word stream
+ * instead of MT19937-64 (exercises the Lemire rejection path exactly). */
+int fdg_sample_khop_words_host(fdg_sampler* s, const uint64_t* seeds, uint32_t n_seeds, const uint64_t* words,
+                               uint64_t n_words, uint64_t* nodes, uint32_t* edges, uint64_t cap,
+                               uint64_t* n_nodes, uint64_t* n_edges, uint64_t* words_used);
+/* MT19937-64 words of std::mt19937_64(splitmix64(rng_seed)) (sampling.hpp:78), on device. */
+int fdg_mt_stream(void* stream, uint64_t rng_seed, uint64_t n, uint64_t* out_dev);
+
+/* ---- extraction: the mini-batch gather -------------------------------------- */
+/* out_dev[i, :] = row(nodes_dev[i]) for i < n (n = *n_dev when n_dev != NULL, else
+ * n_host). When checksum_dev != NULL it also accumulates trainer_step's
+ * order-insensitive checksum sum_i hash_bytes64(row) (pipeline.hpp:103-124,
+ * common.hpp:88-105) into *checksum_dev (caller zeroes it). */
+int fdg_gather(fdg_ctx* ctx, void* stream, const uint64_t* nodes_dev, const uint32_t* n_dev, uint64_t n_host,
+               void* out_dev, uint64_t* checksum_dev);
+/* Checksum of rows already resident (region slot payloads addressed by alias). */
+int fdg_checksum_alias(fdg_ctx* ctx, void* stream, const void* region_dev, const int64_t* alias_dev,
+                       const uint32_t* n_dev, uint64_t n_host, uint64_t* checksum_dev);
+
+/* ---- buffer manager: replaces featbuf::BufferManager (buffer_manager.hpp:222-527),
+ *      FeatureRegion (device_region.hpp:24-50) and Extractor::extract_batch
+ *      (extractor.hpp:88-113) ---------------------------------------------------- */
+typedef struct {
+    uint64_t hits, loads, waits, evictions, takeovers, releases, standby_len;
+} fdg_bm_stats;
+
+/* slot_count >= min_reserved (N_e * M_b rule, buffer_manager.hpp:229-231). */
+int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint32_t max_batch_nodes,
+                  fdg_bm** out);
+int fdg_bm_destroy(fdg_bm* bm);
+/* Algorithm 1 for one batch, stream-ordered: acquire_for_batch (241-269), LRU
+ * standby pops with eviction (274-294), bind (297-310), table -> slot row copies
+ * for the misses, publish (313-324). alias_dev: i64[n] (NodeAliasList). When
+ * out_dev != NULL the mini-batch tensor X[i] = slot(alias[i]) is also written. */
+int fdg_bm_extract(fdg_bm* bm, void* stream, const uint64_t* nodes_dev, const uint32_t* n_dev, uint64_t n_host,
+                   int64_t* alias_dev, void* out_dev, uint64_t* checksum_dev);
+/* release_batch (352-364): ref--, MRU append at 0 with the mapping left valid. */
+int fdg_bm_release(fdg_bm* bm, void* stream, const uint64_t* nodes_dev, const uint32_t* n_dev, uint64_t n_host);
+int fdg_bm_stats_get(fdg_bm* bm, fdg_bm_stats* out); /* synchronises the bm stream */
+int fdg_bm_status(fdg_bm* bm);                       /* sticky device-detected status */
+void* fdg_bm_region(fdg_bm* bm);                     /* FeatureRegion base: slot s at s*row_bytes */
+/* Introspection for tests (mapping_entry / reverse_mapping, buffer_manager.hpp:420-429). */
+int fdg_bm_entry(fdg_bm* bm, uint64_t node, int64_t* slot, uint32_t* ref, uint32_t* valid);
+int fdg_bm_reverse(fdg_bm* bm, uint64_t slot, int64_t* node);
+/* Full invariant sweep (validate_locked, buffer_manager.hpp:488-515) on device. */
+int fdg_bm_validate(fdg_bm* bm);
+
+/* ---- host SET-loop runner (pipeline.hpp:185-257 sampler/extractor stages) ----- */
+/* partition_epoch (sampling.hpp:57-70) with the same libstdc++ std::shuffle. */
+int fdg_partition_epoch(const uint64_t* train_ids, uint64_t n, uint64_t batch_size, uint64_t shuffle_seed,
+                        uint64_t* out_ids);
+uint64_t fdg_batch_seed(uint64_t seed, uint64_t epoch, uint64_t global_batch); /* pipeline.hpp:295-298 */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDG_H */

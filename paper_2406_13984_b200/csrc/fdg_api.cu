@@ -1,0 +1,392 @@
+// fdg_api.cu -- the extern "C" boundary (include/fdg.h).
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "fdg_internal.cuh"
+
+namespace fdg {
+
+static thread_local std::string g_error;
+
+void set_error(const std::string& msg) { g_error = msg; }
+int fail(int code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+    g_error = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ") in " + what +
+              " at " + file + ":" + std::to_string(line);
+    return FDG_CUDA_ERROR;
+}
+
+struct Sampler;
+int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32_t n_layers, Sampler** out);
+void sampler_destroy(Sampler* s);
+int sampler_prefetch(Sampler* s, cudaStream_t st, const uint64_t* rng_seeds, uint32_t n);
+int sampler_sample(Sampler* s, cudaStream_t st, const uint64_t* seeds, uint32_t n_seeds, uint64_t rng_seed,
+                   uint64_t* nodes, uint32_t* edges, uint64_t cap, fdg_batch_counts* cnt);
+int sampler_sample_host(Sampler* s, const uint64_t* seeds, uint32_t n_seeds, uint64_t rng_seed,
+                        const uint64_t* ext_words, uint64_t n_ext_words, uint64_t* nodes, uint32_t* edges,
+                        uint64_t cap, uint64_t* n_nodes, uint64_t* n_edges, uint64_t* layer_nodes,
+                        uint64_t* layer_edges, uint64_t* words_used);
+void sampler_capacity(const Sampler* s, uint64_t* max_nodes, uint64_t* max_edges);
+
+namespace {
+
+int read_file(const std::string& path, uint64_t offset, uint64_t bytes, void* dst) {
+    int fd = ::open(path.c_str(), O_RDONLY);
+    if (fd < 0) return fail(FDG_INVALID_ARG, "open " + path + ": " + std::strerror(errno));
+    uint64_t got = 0;
+    while (got < bytes) {
+        ssize_t n = ::pread(fd, static_cast<char*>(dst) + got, std::min<uint64_t>(bytes - got, 1ull << 30),
+                            offset + got);
+        if (n <= 0) {
+            ::close(fd);
+            return fail(FDG_INVALID_ARG, "read " + path + " failed");
+        }
+        got += uint64_t(n);
+    }
+    ::close(fd);
+    return FDG_OK;
+}
+
+int64_t file_size(const std::string& path) {
+    struct stat st {};
+    if (::stat(path.c_str(), &st) != 0) return -1;
+    return st.st_size;
+}
+
+}  // namespace
+}  // namespace fdg
+
+using namespace fdg;
+
+extern "C" {
+
+const char* fdg_last_error(void) { return g_error.c_str(); }
+int fdg_version(void) { return 1; }
+
+// ---- plumbing -----------------------------------------------------------------
+int fdg_device_count(int* n) { FDG_CUDA(cudaGetDeviceCount(n)); return FDG_OK; }
+int fdg_set_device(int d) { FDG_CUDA(cudaSetDevice(d)); return FDG_OK; }
+int fdg_malloc(void** p, uint64_t b) { FDG_CUDA(cudaMalloc(p, std::max<uint64_t>(b, 1))); return FDG_OK; }
+int fdg_free(void* p) { FDG_CUDA(cudaFree(p)); return FDG_OK; }
+int fdg_host_alloc(void** p, uint64_t b) { FDG_CUDA(cudaMallocHost(p, std::max<uint64_t>(b, 1))); return FDG_OK; }
+int fdg_host_free(void* p) { FDG_CUDA(cudaFreeHost(p)); return FDG_OK; }
+int fdg_memcpy_h2d(void* d, const void* s, uint64_t b, void* st) {
+    FDG_CUDA(cudaMemcpyAsync(d, s, b, cudaMemcpyHostToDevice, (cudaStream_t)st));
+    return FDG_OK;
+}
+int fdg_memcpy_d2h(void* d, const void* s, uint64_t b, void* st) {
+    FDG_CUDA(cudaMemcpyAsync(d, s, b, cudaMemcpyDeviceToHost, (cudaStream_t)st));
+    return FDG_OK;
+}
+int fdg_memcpy_d2d(void* d, const void* s, uint64_t b, void* st) {
+    FDG_CUDA(cudaMemcpyAsync(d, s, b, cudaMemcpyDeviceToDevice, (cudaStream_t)st));
+    return FDG_OK;
+}
+int fdg_memset(void* d, int v, uint64_t b, void* st) {
+    FDG_CUDA(cudaMemsetAsync(d, v, b, (cudaStream_t)st));
+    return FDG_OK;
+}
+int fdg_stream_create(void** st) {
+    cudaStream_t s;
+    FDG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    *st = s;
+    return FDG_OK;
+}
+int fdg_stream_destroy(void* st) { FDG_CUDA(cudaStreamDestroy((cudaStream_t)st)); return FDG_OK; }
+int fdg_stream_sync(void* st) { FDG_CUDA(cudaStreamSynchronize((cudaStream_t)st)); return FDG_OK; }
+int fdg_device_sync(void) { FDG_CUDA(cudaDeviceSynchronize()); return FDG_OK; }
+int fdg_event_create(void** ev) {
+    cudaEvent_t e;
+    FDG_CUDA(cudaEventCreate(&e));
+    *ev = e;
+    return FDG_OK;
+}
+int fdg_event_destroy(void* ev) { FDG_CUDA(cudaEventDestroy((cudaEvent_t)ev)); return FDG_OK; }
+int fdg_event_record(void* ev, void* st) { FDG_CUDA(cudaEventRecord((cudaEvent_t)ev, (cudaStream_t)st)); return FDG_OK; }
+int fdg_stream_wait_event(void* st, void* ev) {
+    FDG_CUDA(cudaStreamWaitEvent((cudaStream_t)st, (cudaEvent_t)ev, 0));
+    return FDG_OK;
+}
+int fdg_event_elapsed_ms(void* a, void* b, float* ms) {
+    FDG_CUDA(cudaEventElapsedTime(ms, (cudaEvent_t)a, (cudaEvent_t)b));
+    return FDG_OK;
+}
+int fdg_event_sync(void* ev) { FDG_CUDA(cudaEventSynchronize((cudaEvent_t)ev)); return FDG_OK; }
+int fdg_mem_info(uint64_t* f, uint64_t* t) {
+    size_t a, b;
+    FDG_CUDA(cudaMemGetInfo(&a, &b));
+    *f = a;
+    *t = b;
+    return FDG_OK;
+}
+
+// ---- context -------------------------------------------------------------------
+int fdg_ctx_create(int device, fdg_ctx** out) {
+    FDG_CUDA(cudaSetDevice(device));
+    auto c = new fdg_ctx();
+    c->device = device;
+    cudaError_t e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "fdg_ctx_create", __FILE__, __LINE__);
+    }
+    *out = c;
+    return FDG_OK;
+}
+
+int fdg_ctx_destroy(fdg_ctx* c) {
+    if (!c) return FDG_OK;
+    cudaSetDevice(c->device);
+    if (c->indptr) cudaFree(c->indptr);
+    if (c->indices) cudaFree(c->indices);
+    for (void* p : c->owned_shards) cudaFree(p);
+    if (c->shard_table) cudaFree((void*)c->shard_table);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return FDG_OK;
+}
+
+int fdg_ctx_info_get(const fdg_ctx* c, fdg_ctx_info* o) {
+    std::memset(o, 0, sizeof(*o));
+    o->num_nodes = c->num_nodes;
+    o->num_edges = c->num_edges;
+    o->idx_bytes = c->idx_bytes;
+    o->row_bytes = c->row_bytes;
+    o->dtype = c->dtype;
+    o->n_shards = c->n_shards;
+    o->indptr_dev = c->indptr;
+    o->indices_dev = c->indices;
+    o->table_dev = c->shard_bases.empty() ? nullptr : c->shard_bases[0];
+    o->rows_per_shard = c->rows_per_shard;
+    o->device = c->device;
+    return FDG_OK;
+}
+
+int fdg_ctx_load_topology(fdg_ctx* c, const uint64_t* indptr, uint64_t n, const uint64_t* indices, uint64_t e) {
+    // Topology::load_indptr / open_indices validation (topology.hpp:84-113)
+    if (n == 0 && (!indptr || indptr[0] != 0)) return fail(FDG_INVALID_ARG, "indptr file has invalid size");
+    if (indptr[0] != 0) return fail(FDG_INVALID_ARG, "indptr must start at 0");
+    for (uint64_t i = 0; i < n; ++i)
+        if (indptr[i] > indptr[i + 1]) return fail(FDG_INVALID_ARG, "indptr is not non-decreasing");
+    if (indptr[n] != e) return fail(FDG_INVALID_ARG, "indices size does not match indptr");
+    cudaSetDevice(c->device);
+    if (c->indptr) cudaFree(c->indptr);
+    if (c->indices) cudaFree(c->indices);
+    c->indptr = nullptr;
+    c->indices = nullptr;
+    c->idx_bytes = n <= 0xFFFFFFFFull ? 4 : 8;
+    FDG_CUDA(cudaMalloc(&c->indptr, (n + 1) * 8));
+    FDG_CUDA(cudaMemcpy(c->indptr, indptr, (n + 1) * 8, cudaMemcpyHostToDevice));
+    FDG_CUDA(cudaMalloc(&c->indices, std::max<uint64_t>(e, 1) * c->idx_bytes));
+    if (c->idx_bytes == 8) {
+        FDG_CUDA(cudaMemcpy(c->indices, indices, e * 8, cudaMemcpyHostToDevice));
+    } else {
+        // narrow to u32 in chunks (lossless: every id < N <= 2^32-1)
+        const uint64_t chunk = 1ull << 24;
+        std::vector<uint32_t> tmp(std::min<uint64_t>(chunk, std::max<uint64_t>(e, 1)));
+        for (uint64_t at = 0; at < e; at += chunk) {
+            uint64_t k = std::min<uint64_t>(chunk, e - at);
+            for (uint64_t i = 0; i < k; ++i) {
+                if (indices[at + i] >= n) return fail(FDG_INVALID_ARG, "indices entry out of range");
+                tmp[i] = uint32_t(indices[at + i]);
+            }
+            FDG_CUDA(cudaMemcpy(static_cast<uint32_t*>(c->indices) + at, tmp.data(), k * 4, cudaMemcpyHostToDevice));
+        }
+    }
+    c->num_nodes = n;
+    c->num_edges = e;
+    return FDG_OK;
+}
+
+int fdg_ctx_load_topology_files(fdg_ctx* c, const char* dir) {
+    std::string d(dir);
+    int64_t ps = file_size(d + "/indptr.bin"), is = file_size(d + "/indices.bin");
+    if (ps < 8 || ps % 8) return fail(FDG_INVALID_ARG, "indptr file " + d + "/indptr.bin has invalid size");
+    if (is < 0 || is % 8) return fail(FDG_INVALID_ARG, "indices file has invalid size");
+    std::vector<uint64_t> indptr(uint64_t(ps) / 8), indices(uint64_t(is) / 8);
+    FDG_TRY(read_file(d + "/indptr.bin", 0, uint64_t(ps), indptr.data()));
+    FDG_TRY(read_file(d + "/indices.bin", 0, uint64_t(is), indices.data()));
+    return fdg_ctx_load_topology(c, indptr.data(), indptr.size() - 1, indices.data(), indices.size());
+}
+
+int fdg_ctx_generate_topology(fdg_ctx* c, uint64_t seed, uint64_t n, uint32_t avg) {
+    cudaSetDevice(c->device);
+    return generate_topology(*c, seed, n, avg);
+}
+
+static int install_table(fdg_ctx* c, void* dev, uint64_t n, uint32_t row_bytes, uint32_t dtype) {
+    for (void* p : c->owned_shards) cudaFree(p);
+    c->owned_shards.assign(1, dev);
+    c->shard_bases.assign(1, dev);
+    c->row_bytes = row_bytes;
+    c->dtype = dtype;
+    c->n_shards = 1;
+    c->rows_per_shard = n;
+    c->feat_nodes = n;
+    if (c->shard_table) cudaFree((void*)c->shard_table);
+    FDG_CUDA(cudaMalloc((void**)&c->shard_table, sizeof(void*)));
+    FDG_CUDA(cudaMemcpy((void*)c->shard_table, &dev, sizeof(void*), cudaMemcpyHostToDevice));
+    return FDG_OK;
+}
+
+int fdg_ctx_load_features(fdg_ctx* c, const void* rows, uint64_t n, uint32_t row_bytes, uint32_t dtype) {
+    if (n == 0 || row_bytes == 0 || row_bytes % 4) return fail(FDG_INVALID_ARG, "feature rows: bad shape");
+    cudaSetDevice(c->device);
+    void* dev = nullptr;
+    FDG_CUDA(cudaMalloc(&dev, n * row_bytes));
+    FDG_CUDA(cudaMemcpy(dev, rows, n * row_bytes, cudaMemcpyHostToDevice));
+    return install_table(c, dev, n, row_bytes, dtype);
+}
+
+int fdg_ctx_load_features_file(fdg_ctx* c, const char* path) {
+    // DatasetHeader decode + validate (format.hpp:33-65, 117-136)
+    unsigned char h[64];
+    FDG_TRY(read_file(path, 0, 64, h));
+    if (std::memcmp(h, "FEATDRV1", 8) != 0) return fail(FDG_INVALID_ARG, "feature file: bad magic");
+    uint32_t version, dim, dtype, row_bytes;
+    uint64_t n, data_offset;
+    std::memcpy(&version, h + 8, 4);
+    std::memcpy(&n, h + 16, 8);
+    std::memcpy(&dim, h + 24, 4);
+    std::memcpy(&dtype, h + 28, 4);
+    std::memcpy(&row_bytes, h + 32, 4);
+    std::memcpy(&data_offset, h + 40, 8);
+    if (version != 1) return fail(FDG_INVALID_ARG, "feature file: unsupported version");
+    if (dtype != 0) return fail(FDG_INVALID_ARG, "feature file: unsupported dtype code");
+    if (n == 0 || dim == 0) return fail(FDG_INVALID_ARG, "feature file: empty dataset");
+    if (row_bytes != dim * 4) return fail(FDG_INVALID_ARG, "feature file: row_bytes != dim * 4");
+    if (data_offset % 512 || data_offset < 64) return fail(FDG_INVALID_ARG, "feature file: misaligned data_offset");
+    if (file_size(path) != int64_t(data_offset + n * row_bytes))
+        return fail(FDG_INVALID_ARG, "feature file: length != header-implied");
+    std::vector<char> buf(n * row_bytes);
+    FDG_TRY(read_file(path, data_offset, n * row_bytes, buf.data()));
+    return fdg_ctx_load_features(c, buf.data(), n, row_bytes, 0);
+}
+
+int fdg_ctx_generate_features(fdg_ctx* c, uint64_t seed, uint64_t n, uint32_t dim, uint32_t dtype, uint32_t n_shards) {
+    cudaSetDevice(c->device);
+    return generate_features(*c, seed, n, dim, dtype, n_shards);
+}
+
+int fdg_ctx_set_feature_shards(fdg_ctx* c, const void* const* bases, uint32_t n_shards, uint64_t rps, uint64_t n,
+                               uint32_t row_bytes, uint32_t dtype) {
+    if (n_shards == 0 || rps == 0 || (n + rps - 1) / rps > n_shards)
+        return fail(FDG_INVALID_ARG, "feature shards: inconsistent geometry");
+    cudaSetDevice(c->device);
+    for (void* p : c->owned_shards) cudaFree(p);
+    c->owned_shards.clear();
+    c->shard_bases.clear();
+    for (uint32_t i = 0; i < n_shards; ++i) c->shard_bases.push_back(const_cast<void*>(bases[i]));
+    c->row_bytes = row_bytes;
+    c->dtype = dtype;
+    c->n_shards = n_shards;
+    c->rows_per_shard = rps;
+    c->feat_nodes = n;
+    if (c->shard_table) cudaFree((void*)c->shard_table);
+    FDG_CUDA(cudaMalloc((void**)&c->shard_table, n_shards * sizeof(void*)));
+    FDG_CUDA(cudaMemcpy((void*)c->shard_table, c->shard_bases.data(), n_shards * sizeof(void*), cudaMemcpyHostToDevice));
+    return FDG_OK;
+}
+
+int fdg_ctx_download_topology(const fdg_ctx* c, uint64_t* indptr, void* indices) {
+    if (!c->indptr) return fail(FDG_NOT_LOADED, "no topology");
+    cudaSetDevice(c->device);
+    if (indptr) FDG_CUDA(cudaMemcpy(indptr, c->indptr, (c->num_nodes + 1) * 8, cudaMemcpyDeviceToHost));
+    if (indices) FDG_CUDA(cudaMemcpy(indices, c->indices, c->num_edges * c->idx_bytes, cudaMemcpyDeviceToHost));
+    return FDG_OK;
+}
+
+int fdg_ctx_download_rows(const fdg_ctx* c, uint64_t first, uint64_t count, void* out) {
+    if (c->shard_bases.empty()) return fail(FDG_NOT_LOADED, "no feature table");
+    if (first + count > c->feat_nodes) return fail(FDG_OUT_OF_RANGE, "download_rows: range out of bounds");
+    cudaSetDevice(c->device);
+    uint64_t at = first;
+    char* o = static_cast<char*>(out);
+    while (at < first + count) {
+        uint64_t s = at / c->rows_per_shard, local = at - s * c->rows_per_shard;
+        uint64_t k = std::min<uint64_t>(c->rows_per_shard - local, first + count - at);
+        FDG_CUDA(cudaMemcpy(o, static_cast<const char*>(c->shard_bases[s]) + local * c->row_bytes, k * c->row_bytes,
+                            cudaMemcpyDeviceToHost));
+        o += k * c->row_bytes;
+        at += k;
+    }
+    return FDG_OK;
+}
+
+// ---- sampler -----------------------------------------------------------------------
+int fdg_sampler_create(fdg_ctx* c, uint32_t max_seeds, const uint32_t* fanouts, uint32_t n_layers, fdg_sampler** out) {
+    cudaSetDevice(c->device);
+    Sampler* s = nullptr;
+    FDG_TRY(sampler_create(c, max_seeds, fanouts, n_layers, &s));
+    *out = reinterpret_cast<fdg_sampler*>(s);
+    return FDG_OK;
+}
+int fdg_sampler_destroy(fdg_sampler* s) {
+    sampler_destroy(reinterpret_cast<Sampler*>(s));
+    return FDG_OK;
+}
+int fdg_sampler_capacity(const fdg_sampler* s, uint64_t* mn, uint64_t* me) {
+    sampler_capacity(reinterpret_cast<const Sampler*>(s), mn, me);
+    return FDG_OK;
+}
+int fdg_sample_khop(fdg_sampler* s, void* st, const uint64_t* seeds, uint32_t n_seeds, uint64_t rng_seed,
+                    uint64_t* nodes, uint32_t* edges, uint64_t cap, fdg_batch_counts* cnt) {
+    return sampler_sample(reinterpret_cast<Sampler*>(s), (cudaStream_t)st, seeds, n_seeds, rng_seed, nodes, edges, cap,
+                          cnt);
+}
+int fdg_sampler_prefetch(fdg_sampler* s, void* st, const uint64_t* rng_seeds, uint32_t n) {
+    return sampler_prefetch(reinterpret_cast<Sampler*>(s), (cudaStream_t)st, rng_seeds, n);
+}
+int fdg_sample_khop_host(fdg_sampler* s, const uint64_t* seeds, uint32_t n_seeds, uint64_t rng_seed, uint64_t* nodes,
+                         uint32_t* edges, uint64_t cap, uint64_t* nn, uint64_t* ne, uint64_t* ln, uint64_t* le) {
+    return sampler_sample_host(reinterpret_cast<Sampler*>(s), seeds, n_seeds, rng_seed, nullptr, 0, nodes, edges, cap,
+                               nn, ne, ln, le, nullptr);
+}
+int fdg_sample_khop_words_host(fdg_sampler* s, const uint64_t* seeds, uint32_t n_seeds, const uint64_t* words,
+                               uint64_t n_words, uint64_t* nodes, uint32_t* edges, uint64_t cap, uint64_t* nn,
+                               uint64_t* ne, uint64_t* wu) {
+    return sampler_sample_host(reinterpret_cast<Sampler*>(s), seeds, n_seeds, 0, words, n_words, nodes, edges, cap, nn,
+                               ne, nullptr, nullptr, wu);
+}
+int fdg_mt_stream(void* st, uint64_t rng_seed, uint64_t n, uint64_t* out) {
+    FDG_CUDA(launch_mt_streams((cudaStream_t)st, &rng_seed, 1, n, out, n));
+    return FDG_OK;
+}
+
+// ---- gather -------------------------------------------------------------------------
+int fdg_gather(fdg_ctx* c, void* st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host, void* out,
+               uint64_t* checksum) {
+    return launch_gather(*c, (cudaStream_t)st, nodes, n_dev, n_host, out, checksum);
+}
+
+int fdg_checksum_alias(fdg_ctx* c, void* st, const void* region, const int64_t* alias, const uint32_t* n_dev,
+                       uint64_t n_host, uint64_t* checksum) {
+    return launch_checksum_alias(*c, (cudaStream_t)st, region, alias, n_dev, n_host, checksum);
+}
+
+// ---- host helpers -------------------------------------------------------------------
+// partition_epoch (sampling.hpp:57-70): std::shuffle with mt19937_64(splitmix64(seed)),
+// the same libstdc++ as the reference build, then chunks of batch_size.
+int fdg_partition_epoch(const uint64_t* ids, uint64_t n, uint64_t batch_size, uint64_t shuffle_seed, uint64_t* out) {
+    if (batch_size < 1) return fail(FDG_INVALID_ARG, "partition_epoch: batch_size must be >= 1");
+    std::vector<uint64_t> v(ids, ids + n);
+    std::mt19937_64 rng(splitmix64(shuffle_seed));
+    std::shuffle(v.begin(), v.end(), rng);
+    std::memcpy(out, v.data(), n * 8);
+    return FDG_OK;
+}
+
+uint64_t fdg_batch_seed(uint64_t seed, uint64_t epoch, uint64_t b) { return hash_combine(hash_combine(seed, epoch), b); }
+
+}  // extern "C"

@@ -1,0 +1,696 @@
+// fdg_bm.cu -- the holistic feature-buffer manager on the GPU.
+//
+// Replaces featbuf::BufferManager (buffer_manager.hpp:222-527) + FeatureRegion
+// (device_region.hpp:24-50) + the extractor's metadata protocol
+// (extractor.hpp:142-151, 391-394) for stream-ordered batches. Exactly the
+// reference's state transitions and LRU order, computed batch-parallel:
+//
+//   mapping table  node -> packed {i32 slot, u32 valid<<31 | ref}  (8 B/node)
+//   reverse map    slot -> node (~0 = free)
+//   standby list   the reference's intrusive LRU list becomes a FIFO ring of
+//                  slot ids with tombstones: push_mru = append at `tail`
+//                  (recording the slot's ring position), remove(slot) on a hit
+//                  = clear in_list[slot] (the stale ring entry is skipped
+//                  later), pop_lru = the next live entry from `head`. An entry
+//                  at position p is live iff in_list[slot] && pos[slot] == p.
+//
+// extract(nodes):                                   reference
+//   k_acquire  classify + ref++ + standby remove;   acquire_for_batch 241-269
+//              ordered rank of to-load positions (decoupled look-back)
+//   k_select   first L live ring entries from head  get_standby_slot 274-294 (xL, batch order)
+//   k_bind     evict previous owner, bind, publish  bind_slot 297-310, publish_valid 313-324
+//   k_move     misses: table -> slot (and -> X); hits: slot -> X (mini-batch tensor)
+// release(nodes):
+//   k_release  ref--; slots reaching 0 appended in batch order   release_batch 352-364, 461-476
+//   k_compact  drops tombstones when the ring nears capacity (persistent grid, no-op otherwise)
+//
+// Parity: alias lists, hits/loads/evictions and mapping entries equal the
+// reference BufferManager driven by the same sequential schedule (tests/).
+#include <algorithm>
+#include <vector>
+
+#include "fdg_internal.cuh"
+
+namespace fdg {
+namespace {
+
+constexpr uint32_t kValid = 0x80000000u;
+constexpr uint32_t kRefMask = 0x7FFFFFFFu;
+constexpr uint64_t kNoNode = ~0ull;
+constexpr int kT = 256;        // threads per tile
+constexpr int kI = 8;          // items per thread
+constexpr int kTileN = kT * kI;
+
+struct Entry {
+    int32_t slot;
+    uint32_t refv;
+};
+
+struct BmState {
+    uint64_t head, tail;   // ring positions (monotonic)
+    uint64_t live;         // standby size
+    uint64_t hits, loads, waits, evictions, takeovers, releases;
+    uint32_t status;
+    uint32_t n_load;       // to-load count of the current batch
+    uint32_t done;         // select finished
+    uint32_t ring_sel;     // which ring buffer is current
+    uint32_t tile_ctr[4];
+    uint64_t new_head;
+};
+
+struct BmDev {
+    Entry* map;
+    uint64_t* reverse;
+    uint64_t* pos;        // slot -> ring position of its live entry
+    uint8_t* in_list;
+    int32_t* ring[2];
+    uint64_t R;           // ring capacity
+    uint64_t S;           // slots
+    uint64_t N;           // nodes
+    BmState* st;
+    unsigned long long* tiles;  // packed look-back words
+    uint32_t* load_pos;   // [max_batch] to-load rank -> batch position
+    uint32_t* sel;        // [max_batch] to-load rank -> slot
+    uint8_t* is_load;     // [max_batch]
+    uint64_t max_batch;
+};
+
+// 64-bit packed look-back word: [63:62] state (1 aggregate, 2 inclusive),
+// [61:32] epoch, [31:0] value. One atomic store publishes value + state.
+__device__ __forceinline__ unsigned long long lb_pack(uint32_t state, uint32_t epoch, uint32_t v) {
+    return (uint64_t(state) << 62) | (uint64_t(epoch & 0x3FFFFFFFu) << 32) | v;
+}
+__device__ __forceinline__ unsigned long long lb_load(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+
+// Warp 0 of a block: exclusive prefix of this tile's aggregate `agg`.
+__device__ uint32_t lookback(unsigned long long* tiles, uint32_t tile, uint32_t agg, uint32_t epoch, int lane) {
+    if (tile == 0) {
+        if (lane == 0) atomicExch(tiles, lb_pack(2, epoch, agg));
+        return 0;
+    }
+    if (lane == 0) atomicExch(tiles + tile, lb_pack(1, epoch, agg));
+    uint32_t excl = 0;
+    int j = int(tile) - 1;
+    for (;;) {
+        int jj = j - lane;
+        uint32_t st = 2, v = 0;
+        if (jj >= 0) {
+            unsigned long long w = lb_load(tiles + jj);
+            st = ((w >> 32) & 0x3FFFFFFFu) == (epoch & 0x3FFFFFFFu) ? uint32_t(w >> 62) : 0u;
+            v = uint32_t(w);
+        }
+        if (__any_sync(0xffffffffu, st == 0)) continue;
+        uint32_t im = __ballot_sync(0xffffffffu, st == 2);
+        int stop = __ffs(im) - 1;
+        uint32_t c = lane <= stop ? v : 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        excl += c;
+        if (stop < 32) break;
+        j -= 32;
+    }
+    if (lane == 0) atomicExch(tiles + tile, lb_pack(2, epoch, excl + agg));
+    return excl;
+}
+
+// Block-wide: exclusive scan of per-thread counts + decoupled look-back.
+// Returns this thread's exclusive global prefix; *total_out (smem) = tile incl total.
+__device__ uint32_t block_rank(unsigned long long* tiles, uint32_t tile, uint32_t mine, uint32_t epoch,
+                               uint32_t* s_warp, uint32_t* s_misc) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < kT / 32 ? s_warp[lane] : 0, wx = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, wx, o);
+            if (lane >= o) wx += y;
+        }
+        if (lane < kT / 32) s_warp[lane] = wx - w;
+        uint32_t agg = __shfl_sync(0xffffffffu, wx, 31);
+        uint32_t ex = lookback(tiles, tile, agg, epoch, lane);
+        if (lane == 0) {
+            s_misc[0] = ex;
+            s_misc[1] = ex + agg;
+        }
+    }
+    __syncthreads();
+    return s_misc[0] + s_warp[warp] + x - mine;
+}
+
+__device__ __forceinline__ uint64_t load_n(const uint32_t* n_dev, uint64_t n_host) { return n_dev ? *n_dev : n_host; }
+
+// ------------------------------------------------------------- k_acquire ----
+__global__ void __launch_bounds__(kT) k_acquire(BmDev B, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                                                int64_t* alias, uint32_t epoch) {
+    __shared__ uint32_t s_warp[kT / 32], s_misc[2], s_tile;
+    __shared__ unsigned long long s_hits, s_removed;
+    BmState* S = B.st;
+    if (S->status) return;
+    const uint64_t n = load_n(n_dev, n_host);
+    const uint32_t ntiles = n ? uint32_t((n + kTileN - 1) / kTileN) : 1;
+    if (threadIdx.x == 0) {
+        s_tile = atomicAdd(&S->tile_ctr[0], 1u);
+        s_hits = 0;
+        s_removed = 0;
+    }
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) return;
+    const uint64_t i0 = uint64_t(tile) * kTileN + threadIdx.x * kI;
+    uint32_t load_mask = 0, mine = 0, hits = 0, removed = 0;
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < kI; ++k) {
+        uint64_t i = i0 + k;
+        if (i >= n) break;
+        uint64_t node = nodes[i];
+        if (node >= B.N) {
+            bad = true;
+            continue;
+        }
+        Entry e = B.map[node];
+        uint32_t ref = e.refv & kRefMask;
+        if (e.refv & kValid) {
+            if (ref == 0) {  // StandbyList::remove (buffer_manager.hpp:250)
+                B.in_list[e.slot] = 0;
+                ++removed;
+            }
+            alias[i] = e.slot;
+            B.is_load[i] = 0;
+            ++hits;
+        } else if (ref > 0) {
+            bad = true;  // in flight elsewhere: impossible for stream-ordered batches
+        } else {
+            alias[i] = -1;
+            B.is_load[i] = 1;
+            load_mask |= 1u << k;
+            ++mine;
+        }
+        B.map[node].refv = e.refv + 1;
+    }
+    if (bad) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
+    if (hits) atomicAdd(&s_hits, (unsigned long long)hits);
+    if (removed) atomicAdd(&s_removed, (unsigned long long)removed);
+    uint32_t r = block_rank(B.tiles, tile, mine, epoch, s_warp, s_misc);
+#pragma unroll
+    for (int k = 0; k < kI; ++k)
+        if (load_mask & (1u << k)) B.load_pos[r++] = uint32_t(i0 + k);
+    if (threadIdx.x == 0) {
+        if (s_hits) atomicAdd((unsigned long long*)&S->hits, s_hits);
+        if (s_removed) atomicAdd((unsigned long long*)&S->live, (unsigned long long)(-(long long)s_removed));
+        if (tile == ntiles - 1) {
+            S->n_load = s_misc[1];
+            S->loads += s_misc[1];
+            S->done = 0;
+            S->new_head = S->head;
+        }
+    }
+}
+
+// ------------------------------------------------------------- k_select ----
+// Persistent CTAs claim ring tiles from `head` in order and rank live entries;
+// the first L live slots are the reference's L successive pop_lru() results.
+__global__ void __launch_bounds__(kT) k_select(BmDev B, uint32_t epoch) {
+    __shared__ uint32_t s_warp[kT / 32], s_misc[2], s_tile;
+    BmState* S = B.st;
+    if (S->status) return;
+    const uint32_t L = S->n_load;
+    if (L == 0) return;
+    const uint64_t head = S->head, tail = S->tail;
+    const int32_t* ring = B.ring[S->ring_sel];
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = *(volatile uint32_t*)&S->done ? 0xFFFFFFFFu : atomicAdd(&S->tile_ctr[1], 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        __syncthreads();
+        if (tile == 0xFFFFFFFFu) return;
+        const uint64_t p0 = head + uint64_t(tile) * kTileN;
+        if (p0 >= tail && tile > 0) {
+            // past the ring end: publish an empty inclusive so successors resolve
+            if (threadIdx.x < 32) {
+                uint32_t ex = lookback(B.tiles, tile, 0, epoch, threadIdx.x & 31);
+                if (threadIdx.x == 0 && ex < L) atomicExch(&S->status, uint32_t(FDG_CAPACITY));
+            }
+            return;
+        }
+        uint32_t live_mask = 0, mine = 0;
+        int32_t slots[kI];
+#pragma unroll
+        for (int k = 0; k < kI; ++k) {
+            uint64_t p = p0 + threadIdx.x * kI + k;
+            slots[k] = -1;
+            if (p < tail) {
+                int32_t s = ring[p % B.R];
+                if (B.in_list[s] && B.pos[s] == p) {
+                    slots[k] = s;
+                    live_mask |= 1u << k;
+                    ++mine;
+                }
+            }
+        }
+        uint32_t r = block_rank(B.tiles, tile, mine, epoch, s_warp, s_misc);
+#pragma unroll
+        for (int k = 0; k < kI; ++k)
+            if (live_mask & (1u << k)) {
+                if (r < L) B.sel[r] = slots[k];
+                if (r == L - 1) {
+                    S->new_head = p0 + threadIdx.x * kI + k + 1;
+                    atomicExch(&S->done, 1u);
+                }
+                ++r;
+            }
+        if (threadIdx.x == 0 && s_misc[1] < L && p0 + kTileN >= tail) atomicExch(&S->status, uint32_t(FDG_CAPACITY));
+        __syncthreads();
+    }
+}
+
+// --------------------------------------------------------------- k_bind ----
+__global__ void k_bind(BmDev B, const uint64_t* nodes, int64_t* alias) {
+    BmState* S = B.st;
+    if (S->status) return;
+    const uint32_t L = S->n_load;
+    uint32_t ev = 0;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
+        const int32_t slot = B.sel[k];
+        const uint32_t i = B.load_pos[k];
+        const uint64_t node = nodes[i];
+        const uint64_t prev = B.reverse[slot];
+        if (prev != kNoNode) {  // invalidate the previous owner (buffer_manager.hpp:281-291)
+            Entry pe = B.map[prev];
+            if ((pe.refv & kRefMask) != 0 || pe.slot != slot) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
+            B.map[prev] = Entry{-1, 0u};
+            ++ev;
+        }
+        Entry e = B.map[node];
+        B.map[node] = Entry{slot, e.refv | kValid};  // bind + publish
+        B.reverse[slot] = node;
+        B.in_list[slot] = 0;
+        alias[i] = slot;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+    if ((threadIdx.x & 31) == 0 && ev) atomicAdd((unsigned long long*)&S->evictions, (unsigned long long)ev);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        atomicAdd((unsigned long long*)&S->live, (unsigned long long)(-(long long)L));
+        S->head = S->new_head;
+    }
+}
+
+// --------------------------------------------------------------- k_move ----
+// 16-byte chunks over the batch: misses read the table and fill their slot
+// (and X); hits read their slot (into X). Without X only misses move.
+__global__ void __launch_bounds__(512) k_move(BmDev B, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                                              const int64_t* alias, const char* table, char* region, uint32_t rb,
+                                              char* X) {
+    BmState* S = B.st;
+    if (S->status) return;
+    const uint32_t cpr = rb / 16;
+    const uint64_t n = X ? load_n(n_dev, n_host) : S->n_load;
+    const uint64_t total = n * cpr;
+    for (uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; c < total; c += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t r = c / cpr, col = c - r * cpr;
+        const uint64_t i = X ? r : B.load_pos[r];
+        const int64_t slot = alias[i];
+        uint4* dst_slot = reinterpret_cast<uint4*>(region + uint64_t(slot) * rb) + col;
+        if (B.is_load[i]) {
+            uint4 v = reinterpret_cast<const uint4*>(table + nodes[i] * rb)[col];
+            *dst_slot = v;
+            if (X) reinterpret_cast<uint4*>(X + i * rb)[col] = v;
+        } else if (X) {
+            reinterpret_cast<uint4*>(X + i * rb)[col] = *dst_slot;
+        }
+    }
+}
+
+// ------------------------------------------------------------ k_release ----
+__global__ void __launch_bounds__(kT) k_release(BmDev B, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                                                uint32_t epoch) {
+    __shared__ uint32_t s_warp[kT / 32], s_misc[2], s_tile;
+    BmState* S = B.st;
+    if (S->status) return;
+    const uint64_t n = load_n(n_dev, n_host);
+    const uint32_t ntiles = n ? uint32_t((n + kTileN - 1) / kTileN) : 1;
+    if (threadIdx.x == 0) s_tile = atomicAdd(&S->tile_ctr[2], 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) return;
+    const uint64_t i0 = uint64_t(tile) * kTileN + threadIdx.x * kI;
+    uint32_t mask = 0, mine = 0;
+    int32_t slots[kI];
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < kI; ++k) {
+        uint64_t i = i0 + k;
+        if (i >= n) break;
+        uint64_t node = nodes[i];
+        if (node >= B.N) {
+            bad = true;
+            continue;
+        }
+        Entry e = B.map[node];
+        uint32_t ref = e.refv & kRefMask;
+        if (!(e.refv & kValid) || ref == 0) {  // buffer_manager.hpp:357, 462
+            bad = true;
+            continue;
+        }
+        B.map[node].refv = e.refv - 1;
+        if (ref == 1) {
+            slots[k] = e.slot;
+            mask |= 1u << k;
+            ++mine;
+        }
+    }
+    if (bad) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
+    uint32_t r = block_rank(B.tiles, tile, mine, epoch, s_warp, s_misc);
+    const uint64_t tail = S->tail;
+    int32_t* ring = B.ring[S->ring_sel];
+#pragma unroll
+    for (int k = 0; k < kI; ++k)
+        if (mask & (1u << k)) {  // push_mru in batch order (buffer_manager.hpp:467)
+            uint64_t p = tail + r++;
+            ring[p % B.R] = slots[k];
+            B.pos[slots[k]] = p;
+            B.in_list[slots[k]] = 1;
+        }
+    if (threadIdx.x == 0 && tile == ntiles - 1) {
+        uint32_t tot = s_misc[1];
+        if (tail + tot - S->head > B.R) atomicExch(&S->status, uint32_t(FDG_CAPACITY));
+        S->tail = tail + tot;
+        S->live += tot;
+        S->releases += 1;
+    }
+}
+
+// ------------------------------------------------------------ k_compact ----
+// Persistent grid (all CTAs co-resident): when tombstones make the ring too
+// long, copy the live entries of [head, tail) in order into the other ring.
+__global__ void __launch_bounds__(kT) k_compact(BmDev B, uint64_t slack, uint32_t epoch) {
+    __shared__ uint32_t s_warp[kT / 32], s_misc[2], s_tile;
+    BmState* S = B.st;
+    if (S->status) return;
+    const uint64_t head = S->head, tail = S->tail;
+    if ((tail - head) + slack <= B.R) return;
+    const int32_t* src = B.ring[S->ring_sel];
+    int32_t* dst = B.ring[S->ring_sel ^ 1];
+    const uint64_t len = tail - head;
+    const uint32_t ntiles = uint32_t((len + kTileN - 1) / kTileN);
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&S->tile_ctr[3], 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        __syncthreads();
+        if (tile >= ntiles) break;
+        const uint64_t p0 = head + uint64_t(tile) * kTileN + threadIdx.x * kI;
+        uint32_t mask = 0, mine = 0;
+        int32_t slots[kI];
+#pragma unroll
+        for (int k = 0; k < kI; ++k) {
+            uint64_t p = p0 + k;
+            if (p < tail) {
+                int32_t s = src[p % B.R];
+                if (B.in_list[s] && B.pos[s] == p) {
+                    slots[k] = s;
+                    mask |= 1u << k;
+                    ++mine;
+                }
+            }
+        }
+        uint32_t r = block_rank(B.tiles, tile, mine, epoch, s_warp, s_misc);
+#pragma unroll
+        for (int k = 0; k < kI; ++k)
+            if (mask & (1u << k)) {
+                dst[r] = slots[k];
+                B.pos[slots[k]] = r;
+                ++r;
+            }
+        if (threadIdx.x == 0 && tile == ntiles - 1) S->new_head = s_misc[1];  // live count
+        __syncthreads();
+    }
+}
+
+__global__ void k_compact_finish(BmDev B, uint64_t slack) {
+    BmState* S = B.st;
+    if (S->status) return;
+    if ((S->tail - S->head) + slack <= B.R) return;
+    S->ring_sel ^= 1;
+    S->head = 0;
+    S->tail = S->new_head;
+}
+
+__global__ void k_reset_ctrs(BmState* S) {
+    if (threadIdx.x < 4) S->tile_ctr[threadIdx.x] = 0;
+}
+
+__global__ void k_init(BmDev B) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < B.N; v += stride) B.map[v] = Entry{-1, 0u};
+    for (uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; s < B.S; s += stride) {
+        B.reverse[s] = kNoNode;
+        B.pos[s] = s;
+        B.in_list[s] = 1;
+        B.ring[0][s] = int32_t(s);
+    }
+}
+
+}  // namespace
+
+struct Bm {
+    Ctx* ctx = nullptr;
+    BmDev d{};
+    void* arena = nullptr;
+    char* region = nullptr;
+    uint64_t slots = 0;
+    uint32_t max_batch = 0;
+    uint32_t epoch = 1;
+    cudaStream_t stream = nullptr;  // for stats/validate
+};
+
+}  // namespace fdg
+
+struct fdg_bm : fdg::Bm {};
+
+using namespace fdg;
+
+namespace {
+
+uint32_t n_tiles_for(uint64_t n) { return uint32_t(std::max<uint64_t>(1, (n + kTileN - 1) / kTileN)); }
+
+int bm_persistent_grid(const Bm* b) { return b->ctx->sm_count * 2; }
+
+}  // namespace
+
+extern "C" {
+
+int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint32_t max_batch_nodes, fdg_bm** out) {
+    if (slot_count == 0) return fail(FDG_INVARIANT, "slot_count must be positive");
+    if (slot_count < min_reserved) return fail(FDG_INVARIANT, "feature buffer smaller than the N_e * M_b reservation");
+    if (slot_count >= uint64_t(INT32_MAX)) return fail(FDG_INVALID_ARG, "slot_count must be < 2^31");
+    if (ctx->row_bytes == 0) return fail(FDG_NOT_LOADED, "buffer manager needs a feature table");
+    if (ctx->row_bytes % 16) return fail(FDG_INVALID_ARG, "buffer manager: row_bytes must be a multiple of 16");
+    if (ctx->n_shards != 1) return fail(FDG_INVALID_ARG, "buffer manager: sharded tables not supported yet");
+    cudaSetDevice(ctx->device);
+    auto b = new fdg_bm();
+    b->ctx = ctx;
+    b->slots = slot_count;
+    b->max_batch = std::max<uint32_t>(max_batch_nodes, 1);
+    const uint64_t N = ctx->num_nodes ? ctx->num_nodes : ctx->feat_nodes;
+    const uint64_t R = 2 * slot_count + 8 * uint64_t(b->max_batch) + kTileN;
+    auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+    uint64_t sz = 0;
+    const uint64_t o_map = sz; sz += al(N * 8);
+    const uint64_t o_rev = sz; sz += al(slot_count * 8);
+    const uint64_t o_pos = sz; sz += al(slot_count * 8);
+    const uint64_t o_inl = sz; sz += al(slot_count);
+    const uint64_t o_r0 = sz; sz += al(R * 4);
+    const uint64_t o_r1 = sz; sz += al(R * 4);
+    const uint64_t o_st = sz; sz += al(sizeof(BmState));
+    const uint64_t tiles = R / kTileN + 2 + n_tiles_for(b->max_batch);
+    const uint64_t o_tl = sz; sz += al(tiles * 8);
+    const uint64_t o_lp = sz; sz += al(uint64_t(b->max_batch) * 4);
+    const uint64_t o_sel = sz; sz += al(uint64_t(b->max_batch) * 4);
+    const uint64_t o_isl = sz; sz += al(uint64_t(b->max_batch));
+    cudaError_t e = cudaMalloc(&b->arena, sz);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&b->region, slot_count * ctx->row_bytes);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        if (b->arena) cudaFree(b->arena);
+        delete b;
+        return cuda_fail(e, "fdg_bm_create", __FILE__, __LINE__);
+    }
+    char* a = static_cast<char*>(b->arena);
+    BmDev& d = b->d;
+    d.map = reinterpret_cast<Entry*>(a + o_map);
+    d.reverse = reinterpret_cast<uint64_t*>(a + o_rev);
+    d.pos = reinterpret_cast<uint64_t*>(a + o_pos);
+    d.in_list = reinterpret_cast<uint8_t*>(a + o_inl);
+    d.ring[0] = reinterpret_cast<int32_t*>(a + o_r0);
+    d.ring[1] = reinterpret_cast<int32_t*>(a + o_r1);
+    d.R = R;
+    d.S = slot_count;
+    d.N = N;
+    d.st = reinterpret_cast<BmState*>(a + o_st);
+    d.tiles = reinterpret_cast<unsigned long long*>(a + o_tl);
+    d.load_pos = reinterpret_cast<uint32_t*>(a + o_lp);
+    d.sel = reinterpret_cast<uint32_t*>(a + o_sel);
+    d.is_load = reinterpret_cast<uint8_t*>(a + o_isl);
+    d.max_batch = b->max_batch;
+    FDG_CUDA(cudaMemset(d.st, 0, sizeof(BmState)));
+    FDG_CUDA(cudaMemset(d.tiles, 0, tiles * 8));
+    BmState h{};
+    h.head = 0;
+    h.tail = slot_count;
+    h.live = slot_count;
+    FDG_CUDA(cudaMemcpy(d.st, &h, sizeof(h), cudaMemcpyHostToDevice));
+    k_init<<<ctx->sm_count * 8, 256>>>(d);
+    FDG_CUDA(cudaGetLastError());
+    FDG_CUDA(cudaDeviceSynchronize());
+    *out = b;
+    return FDG_OK;
+}
+
+int fdg_bm_destroy(fdg_bm* b) {
+    if (!b) return FDG_OK;
+    cudaSetDevice(b->ctx->device);
+    cudaFree(b->arena);
+    cudaFree(b->region);
+    cudaStreamDestroy(b->stream);
+    delete b;
+    return FDG_OK;
+}
+
+int fdg_bm_extract(fdg_bm* b, void* stv, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host, int64_t* alias,
+                   void* out, uint64_t* checksum) {
+    cudaStream_t st = (cudaStream_t)stv;
+    const uint64_t bound = n_host;
+    if (bound > b->max_batch) return fail(FDG_INVALID_ARG, "bm_extract: batch larger than max_batch_nodes");
+    const BmDev& d = b->d;
+    k_reset_ctrs<<<1, 32, 0, st>>>(d.st);
+    k_acquire<<<n_tiles_for(bound), kT, 0, st>>>(d, nodes, n_dev, n_host, alias, b->epoch++);
+    k_select<<<bm_persistent_grid(b), kT, 0, st>>>(d, b->epoch++);
+    k_bind<<<std::max<uint32_t>(1, std::min<uint32_t>((bound + 255) / 256, b->ctx->sm_count * 8)), 256, 0, st>>>(
+        d, nodes, alias);
+    const uint32_t rb = b->ctx->row_bytes;
+    const char* table = static_cast<const char*>(b->ctx->shard_bases[0]);
+    uint64_t chunks = bound * (rb / 16);
+    int blocks = int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 511) / 512, uint64_t(b->ctx->sm_count) * 4)));
+    k_move<<<blocks, 512, 0, st>>>(d, nodes, n_dev, n_host, alias, table, b->region, rb, static_cast<char*>(out));
+    FDG_CUDA(cudaGetLastError());
+    if (checksum) {
+        FDG_TRY(launch_checksum_alias(*b->ctx, st, b->region, alias, n_dev, n_host, checksum));
+    }
+    return FDG_OK;
+}
+
+int fdg_bm_release(fdg_bm* b, void* stv, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host) {
+    cudaStream_t st = (cudaStream_t)stv;
+    const BmDev& d = b->d;
+    const uint64_t slack = 2 * uint64_t(b->max_batch) + kTileN;
+    k_reset_ctrs<<<1, 32, 0, st>>>(d.st);
+    k_release<<<n_tiles_for(n_host), kT, 0, st>>>(d, nodes, n_dev, n_host, b->epoch++);
+    k_compact<<<bm_persistent_grid(b), kT, 0, st>>>(d, slack, b->epoch++);
+    k_compact_finish<<<1, 1, 0, st>>>(d, slack);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
+int fdg_bm_stats_get(fdg_bm* b, fdg_bm_stats* out) {
+    FDG_CUDA(cudaDeviceSynchronize());
+    BmState h;
+    FDG_CUDA(cudaMemcpy(&h, b->d.st, sizeof(h), cudaMemcpyDeviceToHost));
+    out->hits = h.hits;
+    out->loads = h.loads;
+    out->waits = h.waits;
+    out->evictions = h.evictions;
+    out->takeovers = h.takeovers;
+    out->releases = h.releases;
+    out->standby_len = h.live;
+    return FDG_OK;
+}
+
+int fdg_bm_status(fdg_bm* b) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return FDG_CUDA_ERROR;
+    BmState h;
+    if (cudaMemcpy(&h, b->d.st, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return FDG_CUDA_ERROR;
+    return int(h.status);
+}
+
+void* fdg_bm_region(fdg_bm* b) { return b->region; }
+
+int fdg_bm_entry(fdg_bm* b, uint64_t node, int64_t* slot, uint32_t* ref, uint32_t* valid) {
+    if (node >= b->d.N) return fail(FDG_OUT_OF_RANGE, "bm_entry: node out of range");
+    FDG_CUDA(cudaDeviceSynchronize());
+    Entry e;
+    FDG_CUDA(cudaMemcpy(&e, b->d.map + node, sizeof(e), cudaMemcpyDeviceToHost));
+    *slot = e.slot;
+    *ref = e.refv & kRefMask;
+    *valid = e.refv >> 31;
+    return FDG_OK;
+}
+
+int fdg_bm_reverse(fdg_bm* b, uint64_t slot, int64_t* node) {
+    if (slot >= b->slots) return fail(FDG_OUT_OF_RANGE, "bm_reverse: slot out of range");
+    FDG_CUDA(cudaDeviceSynchronize());
+    uint64_t v;
+    FDG_CUDA(cudaMemcpy(&v, b->d.reverse + slot, 8, cudaMemcpyDeviceToHost));
+    *node = v == kNoNode ? -1 : int64_t(v);
+    return FDG_OK;
+}
+
+// validate_locked (buffer_manager.hpp:488-515) on a host copy: bijection between
+// mapping and reverse, no valid entry without a slot, standby soundness, and
+// the live-ring count equals the standby size.
+int fdg_bm_validate(fdg_bm* b) {
+    FDG_CUDA(cudaDeviceSynchronize());
+    const BmDev& d = b->d;
+    std::vector<Entry> map(d.N);
+    std::vector<uint64_t> rev(d.S), pos(d.S);
+    std::vector<uint8_t> inl(d.S);
+    BmState h;
+    FDG_CUDA(cudaMemcpy(&h, d.st, sizeof(h), cudaMemcpyDeviceToHost));
+    if (h.status) return fail(int(h.status), "buffer manager in error state " + std::to_string(h.status));
+    FDG_CUDA(cudaMemcpy(map.data(), d.map, d.N * 8, cudaMemcpyDeviceToHost));
+    FDG_CUDA(cudaMemcpy(rev.data(), d.reverse, d.S * 8, cudaMemcpyDeviceToHost));
+    FDG_CUDA(cudaMemcpy(pos.data(), d.pos, d.S * 8, cudaMemcpyDeviceToHost));
+    FDG_CUDA(cudaMemcpy(inl.data(), d.in_list, d.S, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> ring(d.R);
+    FDG_CUDA(cudaMemcpy(ring.data(), d.ring[h.ring_sel], d.R * 4, cudaMemcpyDeviceToHost));
+    std::vector<uint8_t> seen(d.S, 0);
+    for (uint64_t v = 0; v < d.N; ++v) {
+        const Entry& e = map[v];
+        if (e.slot < 0 && (e.refv & kValid)) return fail(FDG_INVARIANT, "impossible state: valid without slot");
+        if (e.slot >= 0) {
+            if (uint64_t(e.slot) >= d.S) return fail(FDG_INVARIANT, "slot out of range");
+            if (rev[e.slot] != v) return fail(FDG_INVARIANT, "mapping/reverse mismatch for node " + std::to_string(v));
+            if (seen[e.slot]) return fail(FDG_INVARIANT, "slot mapped by two nodes");
+            seen[e.slot] = 1;
+        }
+    }
+    uint64_t live = 0;
+    for (uint64_t p = h.head; p < h.tail; ++p) {
+        int32_t s = ring[p % d.R];
+        if (!(inl[s] && pos[s] == p)) continue;
+        ++live;
+        if (rev[s] != kNoNode && (map[rev[s]].refv & kRefMask) != 0)
+            return fail(FDG_INVARIANT, "standby slot whose node still holds references");
+    }
+    if (live != h.live) return fail(FDG_INVARIANT, "standby size mismatch");
+    for (uint64_t s = 0; s < d.S; ++s) {
+        if (rev[s] == kNoNode) continue;
+        if (map[rev[s]].slot != int32_t(s)) return fail(FDG_INVARIANT, "reverse mapping points at node without matching slot");
+    }
+    return FDG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,264 @@
+// fdg_gather.cu -- feature extraction as an HBM gather into the mini-batch
+// tensor: X[i, :] = row(nodes[i]).
+//
+// Replaces the reference's extraction byte movement: per-row copies from the
+// staging arena into FeatureRegion slots (extractor.hpp:374-386,
+// device_region.hpp:60-64) that the trainer then reads by alias
+// (pipeline.hpp:103-124). On B200 the whole table is HBM-resident, so a batch's
+// rows move table -> X in one pass: 16-byte vector loads that bypass L1
+// (ld.global.nc.L1::no_allocate) and 16-byte streaming stores, consecutive
+// threads on consecutive 16 B chunks of the flattened [n, row_bytes] output
+// (coalesced writes; each row read as whole 32 B sectors). HBM-bound:
+// algorithmic bytes = 2 * n * row_bytes per launch.
+//
+// k_gather_hash additionally folds trainer_step's checksum
+// sum_i hash_bytes64(row_i) (common.hpp:88-105): a warp stages 32 rows in
+// shared memory and each lane then runs one row's sequential splitmix chain.
+#include "fdg_internal.cuh"
+
+namespace fdg {
+namespace {
+
+struct FastDiv {  // Granlund-Montgomery round-up division by a runtime constant (n < 2^32)
+    uint32_t m, l;
+    __host__ void init(uint32_t d) {
+        l = 0;
+        while ((1ull << l) < d) ++l;
+        m = uint32_t(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        return uint32_t((uint64_t(__umulhi(n, m)) + n) >> l);
+    }
+};
+
+struct TableRef {
+    const char* base;              // single shard
+    const char* const* shards;     // sharded: device array of bases
+    uint64_t rows_per_shard;
+    uint32_t n_shards;
+    uint32_t row_bytes;
+};
+
+template <bool SHARDED>
+__device__ __forceinline__ const char* row_ptr(const TableRef& t, uint64_t node) {
+    if constexpr (!SHARDED) {
+        return t.base + node * t.row_bytes;
+    } else {
+        uint64_t s = node / t.rows_per_shard;
+        return t.shards[s] + (node - s * t.rows_per_shard) * t.row_bytes;
+    }
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void stg_stream(uint4* p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+constexpr int kUnroll = 4;
+
+// 16-byte chunk gather over the flattened output.
+template <bool SHARDED>
+__global__ void __launch_bounds__(512) k_gather16(const uint64_t* __restrict__ nodes, const uint32_t* n_dev,
+                                                  uint64_t n_host, const uint32_t* status, TableRef t,
+                                                  FastDiv cdiv, uint32_t cpr, uint4* __restrict__ out) {
+    if (status && *status) return;
+    const uint64_t n = n_dev ? *n_dev : n_host;
+    const uint32_t total = uint32_t(n * cpr);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    for (; c + (kUnroll - 1) * stride < total; c += kUnroll * stride) {
+        uint4 v[kUnroll];
+        uint32_t cc[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            cc[u] = c + u * stride;
+            uint32_t row = cdiv.div(cc[u]);
+            uint32_t col = cc[u] - row * cpr;
+            const uint4* src = reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, __ldg(nodes + row))) + col;
+            v[u] = ldg_stream(src);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) stg_stream(out + cc[u], v[u]);
+    }
+    for (; c < total; c += stride) {
+        uint32_t row = cdiv.div(c);
+        uint32_t col = c - row * cpr;
+        const uint4* src = reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, __ldg(nodes + row))) + col;
+        stg_stream(out + c, ldg_stream(src));
+    }
+}
+
+// 4-byte fallback for rows that are not a multiple of 16 bytes.
+template <bool SHARDED>
+__global__ void k_gather4(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
+                          const uint32_t* status, TableRef t, FastDiv cdiv, uint32_t cpr, uint32_t* __restrict__ out) {
+    if (status && *status) return;
+    const uint64_t n = n_dev ? *n_dev : n_host;
+    const uint64_t total = n * cpr;
+    for (uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; c < total;
+         c += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t row = c / cpr, col = c - row * cpr;
+        out[c] = reinterpret_cast<const uint32_t*>(row_ptr<SHARDED>(t, nodes[row]))[col];
+    }
+}
+
+constexpr int kHashWarps = 4;
+
+__device__ __forceinline__ uint64_t hash_row_smem(const char* row, uint32_t n) {
+    uint64_t h = 0x27d4eb2f165667c5ull ^ (uint64_t(n) * 0x9e3779b97f4a7c15ull);
+    uint32_t full = n >> 3;
+    const uint2* p = reinterpret_cast<const uint2*>(row);
+    for (uint32_t s = 0; s < full; ++s) {
+        uint2 w = p[s];
+        h = splitmix64(h ^ (uint64_t(w.y) << 32 | w.x));
+    }
+    uint32_t rem = n & 7;
+    if (rem) {  // rows are 4-byte multiples: a 4-byte tail lane
+        uint64_t lane = reinterpret_cast<const uint32_t*>(row + (full << 3))[0];
+        h = splitmix64(h ^ lane ^ (uint64_t(rem) << 56));
+    }
+    return splitmix64(h);
+}
+
+// Gather + trainer checksum. Rows are staged per warp in shared memory with a
+// stride of row_bytes + 8 so the per-lane 8-byte hash reads are conflict-free.
+// ALIAS: rows are FeatureRegion slots addressed by the alias list (t.base = region,
+// `nodes` holds the i64 aliases) -- trainer_step's region.slot(alias[i]) read.
+template <bool SHARDED, bool ALIAS = false>
+__global__ void __launch_bounds__(kHashWarps * 32) k_gather_hash(const uint64_t* __restrict__ nodes,
+                                                                 const uint32_t* n_dev, uint64_t n_host,
+                                                                 const uint32_t* status, TableRef t,
+                                                                 char* __restrict__ out, uint64_t* checksum) {
+    extern __shared__ __align__(16) char smem[];
+    if (status && *status) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rb = t.row_bytes;
+    const uint32_t stride = rb + 8;
+    char* wbuf = smem + size_t(warp) * 32 * stride;
+    const uint64_t n = n_dev ? *n_dev : n_host;
+    const uint64_t groups = (n + 31) / 32;
+    const uint32_t words = rb >> 2;  // 4-byte words per row
+    uint64_t sum = 0;
+    for (uint64_t g = blockIdx.x * uint64_t(kHashWarps) + warp; g < groups; g += uint64_t(gridDim.x) * kHashWarps) {
+        const uint64_t r0 = g * 32;
+        const uint32_t rows = uint32_t(n - r0 < 32 ? n - r0 : 32);
+        uint64_t my_node = lane < rows ? nodes[r0 + lane] : 0;
+        for (uint32_t r = 0; r < rows; ++r) {
+            uint64_t node = __shfl_sync(0xffffffffu, my_node, r);
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(ALIAS ? t.base + node * rb : row_ptr<SHARDED>(t, node));
+            uint32_t* sm = reinterpret_cast<uint32_t*>(wbuf + r * stride);
+            if (out) {
+                uint32_t* dst = reinterpret_cast<uint32_t*>(out + (r0 + r) * rb);
+                for (uint32_t w = lane; w < words; w += 32) {
+                    uint32_t v = __ldg(src + w);
+                    dst[w] = v;
+                    sm[w] = v;
+                }
+            } else {
+                for (uint32_t w = lane; w < words; w += 32) sm[w] = __ldg(src + w);
+            }
+        }
+        __syncwarp();
+        if (lane < rows) sum += hash_row_smem(wbuf + lane * stride, rb);
+        __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
+}
+
+TableRef table_ref(const Ctx& c) {
+    TableRef t;
+    t.base = c.shard_bases.empty() ? nullptr : static_cast<const char*>(c.shard_bases[0]);
+    t.shards = reinterpret_cast<const char* const*>(c.shard_table);
+    t.rows_per_shard = c.rows_per_shard;
+    t.n_shards = c.n_shards;
+    t.row_bytes = c.row_bytes;
+    return t;
+}
+
+}  // namespace
+
+int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
+                        uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status) {
+    if (c.row_bytes == 0 || c.shard_bases.empty()) return fail(FDG_NOT_LOADED, "gather: no feature table loaded");
+    TableRef t = table_ref(c);
+    const bool sharded = c.n_shards > 1;
+    if (n_bound == 0) return FDG_OK;
+    if (checksum) {
+        size_t smem = size_t(kHashWarps) * 32 * (c.row_bytes + 8);
+        static bool attr_set[2] = {false, false};
+        auto kfn = sharded ? k_gather_hash<true> : k_gather_hash<false>;
+        if (!attr_set[sharded]) {
+            FDG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr_set[sharded] = true;
+        }
+        if (smem > 200 * 1024) return fail(FDG_INVALID_ARG, "gather: row too large for the fused checksum");
+        uint64_t groups = (n_bound + 31) / 32;
+        int blocks = int(std::min<uint64_t>((groups + kHashWarps - 1) / kHashWarps, uint64_t(c.sm_count) * 8));
+        kfn<<<blocks, kHashWarps * 32, smem, st>>>(nodes, n_dev, n_host, status, t, static_cast<char*>(out), checksum);
+        FDG_CUDA(cudaGetLastError());
+        return FDG_OK;
+    }
+    if (c.row_bytes % 16 == 0) {
+        uint32_t cpr = c.row_bytes / 16;
+        if (n_bound * cpr >= (1ull << 32)) return fail(FDG_INVALID_ARG, "gather: batch too large");
+        FastDiv d;
+        d.init(cpr);
+        uint64_t total = n_bound * cpr;
+        int blocks = int(std::min<uint64_t>((total + 511) / 512, uint64_t(c.sm_count) * 4));
+        if (sharded)
+            k_gather16<true><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr, static_cast<uint4*>(out));
+        else
+            k_gather16<false><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr, static_cast<uint4*>(out));
+    } else {
+        uint32_t cpr = c.row_bytes / 4;
+        FastDiv d;
+        d.init(cpr);
+        uint64_t total = n_bound * cpr;
+        int blocks = int(std::min<uint64_t>((total + 255) / 256, uint64_t(c.sm_count) * 8));
+        if (sharded)
+            k_gather4<true><<<blocks, 256, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr, static_cast<uint32_t*>(out));
+        else
+            k_gather4<false><<<blocks, 256, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr, static_cast<uint32_t*>(out));
+    }
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
+int launch_gather(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                  void* out, uint64_t* checksum) {
+    uint64_t bound = n_dev ? std::max<uint64_t>(n_host, 1) : n_host;
+    return launch_gather_bound(c, st, nodes, n_dev, n_host, bound, out, checksum, nullptr);
+}
+
+int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, const int64_t* alias,
+                          const uint32_t* n_dev, uint64_t n_host, uint64_t* checksum) {
+    if (c.row_bytes == 0) return fail(FDG_NOT_LOADED, "checksum: no feature table loaded");
+    if (!checksum) return fail(FDG_INVALID_ARG, "checksum: null output");
+    TableRef t = table_ref(c);
+    t.base = static_cast<const char*>(region);
+    size_t smem = size_t(kHashWarps) * 32 * (c.row_bytes + 8);
+    static bool attr_set = false;
+    if (!attr_set) {
+        FDG_CUDA(cudaFuncSetAttribute(k_gather_hash<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+        attr_set = true;
+    }
+    if (smem > 200 * 1024) return fail(FDG_INVALID_ARG, "checksum: row too large");
+    uint64_t groups = (std::max<uint64_t>(n_host, 1) + 31) / 32;
+    int blocks = int(std::min<uint64_t>((groups + kHashWarps - 1) / kHashWarps, uint64_t(c.sm_count) * 8));
+    k_gather_hash<false, true><<<blocks, kHashWarps * 32, smem, st>>>(reinterpret_cast<const uint64_t*>(alias), n_dev,
+                                                                     n_host, nullptr, t, nullptr, checksum);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
+}  // namespace fdg

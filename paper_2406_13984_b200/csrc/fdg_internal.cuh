@@ -1,0 +1,87 @@
+// fdg_internal.cuh -- shared internals of libfdg (B200 / sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "fdg.h"
+
+namespace fdg {
+
+// ---- error plumbing -----------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define FDG_CUDA(call)                                                        \
+    do {                                                                      \
+        cudaError_t _e = (call);                                              \
+        if (_e != cudaSuccess) return ::fdg::cuda_fail(_e, #call, __FILE__, __LINE__); \
+    } while (0)
+
+#define FDG_TRY(call)                      \
+    do {                                   \
+        int _rc = (call);                  \
+        if (_rc != FDG_OK) return _rc;     \
+    } while (0)
+
+// ---- reference hashing on device (common.hpp:77-105) ------------------------------
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t hash_combine(uint64_t a, uint64_t b) {
+    return splitmix64(a ^ (b + 0x9e3779b97f4a7c15ull + (a << 6) + (a >> 2)));
+}
+// k-th output (k >= 0) of a SplitMix stream seeded with `seed` (common.hpp:112-118):
+// the state after k+1 calls is seed + (k+1)*gamma, so any draw is random-access.
+__host__ __device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t k) {
+    return splitmix64(seed + k * 0x9e3779b97f4a7c15ull);
+}
+
+// ---- context ---------------------------------------------------------------------
+struct Ctx {
+    int device = 0;
+    uint64_t num_nodes = 0;
+    uint64_t num_edges = 0;
+    uint32_t idx_bytes = 4;
+    uint64_t* indptr = nullptr;   // u64[N+1]
+    void* indices = nullptr;      // u32/u64[E]
+    // features
+    uint32_t row_bytes = 0;
+    uint32_t dtype = 0;
+    uint32_t n_shards = 0;
+    uint64_t rows_per_shard = 0;
+    uint64_t feat_nodes = 0;
+    std::vector<void*> shard_bases;   // device pointers (may be peers)
+    std::vector<void*> owned_shards;  // allocations owned by this ctx
+    const void** shard_table = nullptr;  // device copy of shard_bases
+    cudaStream_t stream = nullptr;    // setup stream
+    int sm_count = 148;
+};
+
+}  // namespace fdg
+
+struct fdg_ctx : fdg::Ctx {};
+
+namespace fdg {
+// generator entry points (fdg_generate.cu)
+int generate_topology(Ctx& c, uint64_t seed, uint64_t num_nodes, uint32_t avg_degree);
+int generate_features(Ctx& c, uint64_t seed, uint64_t num_nodes, uint32_t dim, uint32_t dtype, uint32_t n_shards);
+// MT19937-64 (fdg_mt.cu)
+// rng_seeds: HOST array (passed by value to the kernel)
+cudaError_t launch_mt_streams(cudaStream_t st, const uint64_t* rng_seeds, uint32_t n_streams,
+                              uint64_t words_per_stream, uint64_t* out_dev, uint64_t out_stride);
+// gather (fdg_gather.cu)
+int launch_gather(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                  void* out, uint64_t* checksum);
+int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, const int64_t* alias,
+                          const uint32_t* n_dev, uint64_t n_host, uint64_t* checksum);
+int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
+                        uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status);
+}  // namespace fdg

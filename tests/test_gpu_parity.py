@@ -1,0 +1,300 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the C restatement. Bit-exact everywhere (integer / byte work)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _sample_cases(g):
+    meta, so, fo = g["smp_meta"], g["smp_seed_off"], g["smp_fan_off"]
+    no = np.concatenate([[0], np.cumsum(meta[:, 0])]).astype(np.int64)
+    eo = np.concatenate([[0], np.cumsum(meta[:, 1])]).astype(np.int64)
+    for k in range(len(meta)):
+        yield (g["smp_seeds"][so[k]:so[k + 1]], g["smp_fan"][fo[k]:fo[k + 1]], int(meta[k, 2]),
+               g["smp_nodes"][no[k]:no[k + 1]], g["smp_edges"][eo[k]:eo[k + 1]])
+
+
+def _header(n, dim):
+    h = bytearray(512)
+    h[0:8] = b"FEATDRV1"
+    h[8:12] = (1).to_bytes(4, "little")
+    h[16:24] = n.to_bytes(8, "little")
+    h[24:28] = dim.to_bytes(4, "little")
+    h[32:36] = (dim * 4).to_bytes(4, "little")
+    h[40:48] = (512).to_bytes(8, "little")
+    return bytes(h)
+
+
+# ------------------------------------------------------------------ generator --
+def test_generator_matches_reference_digests(fd, golden):
+    for k in range(len(golden["gen_digests"])):
+        n, dim, avg, seed, ne = map(int, golden[f"gen{k}_params"])
+        t = fd.Topology.generate(n, dim, avg, seed)
+        assert t.num_edges == ne
+        indptr, indices = t.download_topology()
+        assert hashlib.sha256(indptr.tobytes()).hexdigest() == golden["gen_digests"][k][1]
+        assert hashlib.sha256(indices.astype(np.uint64).tobytes()).hexdigest() == golden["gen_digests"][k][2]
+        rows = t.download_rows(0, n)
+        assert hashlib.sha256(_header(n, dim) + rows.tobytes()).hexdigest() == golden["gen_digests"][k][0]
+
+
+def test_generator_products_shape_sha256(fd):
+    """Full products-shaped dataset (2,449,029 nodes, 100-dim, avg 28, seed 7): SHA-256 prefixes of
+    the reference generator's files, as recorded in SURVEY.md section 7."""
+    n, dim = 2449029, 100
+    t = fd.Topology.generate(n, dim, 28, 7)
+    indptr, indices = t.download_topology()
+    assert hashlib.sha256(indptr.tobytes()).hexdigest().startswith("02d7e31ebf19542c")
+    assert hashlib.sha256(indices.astype(np.uint64).tobytes()).hexdigest().startswith("d7ee933b7864fead")
+    h = hashlib.sha256(_header(n, dim))
+    step = 200_000
+    for first in range(0, n, step):
+        h.update(t.download_rows(first, min(step, n - first)).tobytes())
+    assert h.hexdigest().startswith("608e9a5483bdbbe9")
+
+
+def test_generator_vs_port_random(fd, port):
+    for n, dim, avg, seed in [(30000, 5, 9, 1), (777, 12, 40, 2), (5000, 2, 64, 9)]:
+        t = fd.Topology.generate(n, dim, avg, seed)
+        ip, ix = t.download_topology()
+        pip, pix = port.generate_topology(seed, n, avg)
+        np.testing.assert_array_equal(ip, pip)
+        np.testing.assert_array_equal(ix.astype(np.uint64), pix)
+        rows = t.download_rows(0, n).view(np.float32)
+        np.testing.assert_array_equal(rows.view(np.uint32), port.generate_features(seed, n, dim).view(np.uint32))
+
+
+def test_generator_fp16_shards(fd, port):
+    n, dim = 1001, 24
+    t = fd.Topology.generate(n, dim, 8, 7, dtype="f16", shards=3)
+    info = t.info()
+    assert info.row_bytes == dim * 2 and info.n_shards == 3
+    got = t.download_rows(0, n).view(np.float16)
+    want = port.generate_features(7, n, dim).astype(np.float16)  # IEEE RN f32 -> f16
+    np.testing.assert_array_equal(got.view(np.uint16), want.view(np.uint16))
+
+
+# ---------------------------------------------------------------------- MT --
+def test_mt_stream_golden(fd, golden, port):
+    for s, words in zip(golden["mt_seeds"], golden["mt_words"]):
+        np.testing.assert_array_equal(fd.mt_stream(int(s), words.shape[0]), words)
+    big = fd.mt_stream(12345, 1_111_111)
+    np.testing.assert_array_equal(big, port.mt_stream(12345, 1_111_111))
+
+
+# ----------------------------------------------------------------- sampling --
+def test_sample_khop_golden(fd, golden):
+    t = fd.Topology.generate(5000, 16, 12, 7)
+    for seeds, fan, rs, nodes, edges in _sample_cases(golden):
+        b = fd.sample_khop(t, seeds, list(fan), rs)
+        np.testing.assert_array_equal(b.nodes, nodes)
+        np.testing.assert_array_equal(b.edges, edges)
+    ts = fd.Topology.generate(3000, 4, 1, 5)
+    b = fd.sample_khop(ts, golden["sparse_seeds"], [2, 2, 2], 77)
+    np.testing.assert_array_equal(b.nodes, golden["sparse_nodes"])
+    np.testing.assert_array_equal(b.edges, golden["sparse_edges"])
+
+
+def test_sample_khop_errors(fd):
+    t = fd.Topology.generate(5000, 16, 12, 7)
+    with pytest.raises(fd.OutOfRange, match="5000"):  # first out-of-range seed in order
+        fd.sample_khop(t, np.array([3, 5000, 7, 6000], np.uint64), [2], 1)
+    with pytest.raises(fd.InvalidArgument):
+        fd.sample_khop(t, np.array([3], np.uint64), [2, 0], 1)
+    with pytest.raises(fd.InvalidArgument):
+        fd.sample_khop(t, np.array([3], np.uint64), [], 1)
+    # the sampler stays usable after an error
+    b = fd.sample_khop(t, np.array([3, 4], np.uint64), [2], 1)
+    assert b.nodes[:2].tolist() == [3, 4]
+
+
+@pytest.mark.parametrize("fan", [[10, 10, 10], [15, 10, 5], [1], [40, 3], [25, 25]])
+def test_sample_khop_vs_port(fd, port, fan):
+    t = fd.Topology.generate(200_000, 8, 16, 3, features=False)
+    ip, ix = t.download_topology()
+    rs = np.random.RandomState(len(fan) * 100 + fan[0])
+    for k in range(3):
+        seeds = rs.randint(0, 200_000, size=rs.choice([1, 37, 1000])).astype(np.uint64)
+        r = int(rs.randint(0, 2**63))
+        b = fd.sample_khop(t, seeds, fan, r)
+        o = port.sample_khop(ip, ix, seeds, fan, r)
+        np.testing.assert_array_equal(b.nodes, o["nodes"])
+        np.testing.assert_array_equal(b.edges, o["edges"])
+        np.testing.assert_array_equal(b.layer_nodes, o["layer_nodes"])
+        np.testing.assert_array_equal(b.layer_edges, o["layer_edges"])
+
+
+def test_sample_high_duplicate_rate(fd, port):
+    """A tiny dense graph: almost every pick is a duplicate (dedup stress)."""
+    t = fd.Topology.generate(300, 4, 64, 5, features=False)
+    ip, ix = t.download_topology()
+    for k in range(5):
+        seeds = np.random.RandomState(k).randint(0, 300, size=500).astype(np.uint64)
+        b = fd.sample_khop(t, seeds, [12, 12, 12], 1000 + k)
+        o = port.sample_khop(ip, ix, seeds, [12, 12, 12], 1000 + k)
+        np.testing.assert_array_equal(b.nodes, o["nodes"])
+        np.testing.assert_array_equal(b.edges, o["edges"])
+
+
+def test_sample_lemire_rejection_exact(fd, port):
+    """Zero words force libstdc++'s Lemire rejection loop (low = 0 < 2^64 mod r for r not
+    a power of two), consuming extra words and shifting every later draw: the GPU's
+    exact mode must match the sequential restatement word for word."""
+    t = fd.Topology.generate(20000, 4, 16, 4, features=False)
+    ip, ix = t.download_topology()
+    s = fd.Sampler(t, [10, 10], max_seeds=64)
+    rs = np.random.RandomState(3)
+    for trial in range(4):
+        seeds = rs.randint(0, 20000, size=64).astype(np.uint64)
+        words = rs.randint(0, 2**63, size=s.max_edges + 4096, dtype=np.int64).astype(np.uint64) * 2 + 1
+        words[rs.randint(0, 2000, size=40)] = 0
+        nodes, edges, used = s.sample_words(seeds, words)
+        o = port.sample_khop(ip, ix, seeds, [10, 10], 0, words=words)
+        assert used == o["words_used"]
+        np.testing.assert_array_equal(nodes, o["nodes"])
+        np.testing.assert_array_equal(edges, o["edges"])
+
+
+def test_sample_papers_shape_vs_port(fd, port):
+    """Full Papers100M-shaped topology (111,059,956 nodes, avg degree 16): two batches of
+    the epoch-0 partition, bit-exact against the restatement."""
+    n = 111_059_956
+    t = fd.Topology.generate(n, 128, 16, 7, features=False)
+    assert t.num_edges == 1_613_492_860
+    ip, ix = t.download_topology()
+    order = np.concatenate(fd.partition_epoch(np.arange(1_000_000, dtype=np.uint64), 1000, port.hash_combine(0, 0)))
+    for b in (0, 1):
+        seeds = order[b * 1000:(b + 1) * 1000]
+        r = fd.batch_seed(0, 0, b)
+        got = fd.sample_khop(t, seeds, [10, 10, 10], r)
+        o = port.sample_khop(ip, ix, seeds, [10, 10, 10], r)
+        np.testing.assert_array_equal(got.nodes, o["nodes"])
+        np.testing.assert_array_equal(got.edges, o["edges"])
+
+
+# ------------------------------------------------------------------- gather --
+@pytest.mark.parametrize("dim,dtype", [(100, "f32"), (128, "f32"), (256, "f32"), (7, "f32"), (768, "f16")])
+def test_gather_and_checksum(fd, port, dim, dtype):
+    n = 50_000
+    t = fd.Topology.generate(n, dim, 8, 7, dtype=dtype)
+    table = t.download_rows(0, n)
+    nodes = np.random.RandomState(dim).randint(0, n, size=12_345).astype(np.uint64)
+    x = fd.gather(t, nodes)
+    np.testing.assert_array_equal(x, table[nodes.astype(np.int64)])
+    x2, cs = fd.gather(t, nodes, checksum=True)
+    np.testing.assert_array_equal(x2, x)
+    assert cs == port.checksum_rows(table[nodes.astype(np.int64)])
+    empty = fd.gather(t, np.zeros(0, np.uint64))
+    assert empty.shape == (0, t.row_bytes)
+
+
+def test_gather_sharded(fd):
+    n = 10_001
+    t1 = fd.Topology.generate(n, 64, 8, 7, shards=1)
+    t4 = fd.Topology.generate(n, 64, 8, 7, shards=4)
+    nodes = np.random.RandomState(0).randint(0, n, size=5000).astype(np.uint64)
+    np.testing.assert_array_equal(fd.gather(t1, nodes), fd.gather(t4, nodes))
+
+
+def test_sync_pipeline_checksums_golden(fd, golden, port):
+    """sample_khop -> gather -> trainer checksum equals the reference's
+    run_sync_reference BatchRecords (pipeline.hpp:261-293)."""
+    t = fd.Topology.generate(5000, 16, 12, 7)
+    order = np.concatenate(fd.partition_epoch(np.arange(200, dtype=np.uint64), 50, port.hash_combine(0, 0)))
+    for rec in golden["sync_records"]:
+        b = int(rec[0])
+        batch = fd.sample_khop(t, order[b * 50:(b + 1) * 50], [4, 4], fd.batch_seed(0, 0, b))
+        assert len(batch.nodes) == int(rec[2])
+        _, cs = fd.gather(t, batch.nodes, checksum=True)
+        assert cs == int(rec[3])
+
+
+# ----------------------------------------------------------- buffer manager --
+def test_buffer_manager_golden(fd, golden):
+    g = golden
+    t = fd.Topology.generate(5000, 16, 12, 7)
+    off = g["bm_off"].astype(np.int64)
+    batches = [g["bm_nodes"][off[b]:off[b + 1]] for b in range(len(off) - 1)]
+    bm = fd.BufferManager(t, int(g["bm_S"][0]), max_batch_nodes=max(len(x) for x in batches))
+    aliases = []
+    for b, nodes in enumerate(batches):
+        aliases.append(bm.extract(nodes))
+        if b >= 1:
+            bm.release_batch(batches[b - 1])
+        s = bm.stats()
+        assert [s[k] for k in ("hits", "loads", "waits", "evictions", "takeovers", "releases", "standby_len")] == \
+            [int(v) for v in g["bm_stats"][b]]
+    np.testing.assert_array_equal(np.concatenate(aliases), g["bm_alias"])
+    ent = np.array([bm.mapping_entry(v) for v in range(0, 5000, 7)], np.int64)
+    np.testing.assert_array_equal(ent, g["bm_entries"])
+    bm.validate()
+
+
+def test_extractor_checksums_golden(fd, golden):
+    """Extractor.extract_batch + trainer_step through the GPU region equal the
+    reference's real Extractor (alias lists) and trainer_step checksums."""
+    g = golden
+    t = fd.Topology.generate(5000, 16, 12, 7)
+    off = g["bm_off"].astype(np.int64)
+    batches = [g["bm_nodes"][off[b]:off[b + 1]] for b in range(4)]
+    slots = 2 * max(len(x) for x in [g["bm_nodes"][off[b]:off[b + 1]] for b in range(len(off) - 1)]) + 50
+    bm = fd.BufferManager(t, slots, max_batch_nodes=max(len(x) for x in batches))
+    ex = fd.Extractor(bm)
+    aliases, sums = [], []
+    for b, nodes in enumerate(batches):
+        batch = fd.SampledBatch(nodes=nodes)
+        a = ex.extract_batch(batch)
+        aliases.append(a)
+        sums.append(fd.trainer_step(batch, a, bm))
+        if b >= 1:
+            bm.release_batch(batches[b - 1])
+    np.testing.assert_array_equal(np.concatenate(aliases), g["ex_alias"])
+    assert sums == [int(x) for x in g["ex_checksum"]]
+
+
+@pytest.mark.parametrize("S,lag", [(2600, 1), (5200, 2), (20000, 3)])
+def test_buffer_manager_vs_port_random(fd, port, S, lag):
+    n = 20000
+    t = fd.Topology.generate(n, 32, 8, 1)
+    table = t.download_rows(0, n)
+    rs = np.random.RandomState(S + lag)
+    mb = 1300
+    bm = fd.BufferManager(t, S, max_batch_nodes=mb)
+    ob = oracle.PortBufferManager(port, n, S)
+    hist = []
+    for it in range(60):
+        hot = rs.randint(0, 3000, size=rs.randint(0, 600))
+        cold = rs.randint(0, n, size=rs.randint(1, 700))
+        nodes = np.unique(np.concatenate([hot, cold])).astype(np.uint64)[:mb]
+        rs.shuffle(nodes)
+        alias, x, cs = bm.extract(nodes, want_rows=True, checksum=True)
+        oa, _ = ob.extract(nodes)
+        np.testing.assert_array_equal(alias, oa)
+        np.testing.assert_array_equal(x, table[nodes.astype(np.int64)])
+        assert cs == port.checksum_rows(x)
+        hist.append(nodes)
+        while len(hist) > lag:
+            old = hist.pop(0)
+            bm.release_batch(old)
+            ob.release(old)
+        s = bm.stats()
+        assert [s["hits"], s["loads"], s["evictions"], s["releases"], s["standby_len"]] == \
+            [int(v) for v in ob.stats()[[0, 1, 3, 5, 6]]]
+    bm.validate()
+    got = bm.region_slots(alias)
+    np.testing.assert_array_equal(got, table[nodes.astype(np.int64)])
+
+
+def test_buffer_manager_capacity_and_invariants(fd):
+    t = fd.Topology.generate(1000, 16, 8, 1)
+    with pytest.raises(fd.InvariantViolation):
+        fd.BufferManager(t, 10, min_reserved=20)
+    bm = fd.BufferManager(t, 10, max_batch_nodes=50)
+    bm.extract(np.arange(8, dtype=np.uint64))
+    with pytest.raises(fd.StandbyTimeout):  # only 2 free slots remain for 5 misses
+        bm.extract(np.arange(100, 105, dtype=np.uint64))
