@@ -255,6 +255,9 @@ class Ref:
         L.fdref_run_epoch.restype = i64
         L.fdref_run_epoch.argtypes = [C.c_char_p, vp, u64, u64, u64, u64, vp, u32, C.c_int, u32, u32,
                                       vp, u64, vp]
+        L.fdref_gen_indptr.argtypes = [u64, u64, u32, u32, vp]
+        L.fdref_gen_indices.argtypes = [u64, u64, u32, u32, vp, vp]
+        L.fdref_gen_features.argtypes = [u64, u64, u32, u32, vp]
         L.fdref_bench_sample_extract.restype = C.c_double
         L.fdref_bench_sample_extract.argtypes = [vp, vp, u32, vp, u64, u64, vp, u32, u64, u64, u64, u32,
                                                  vp, vp]
@@ -302,6 +305,46 @@ class Ref:
         ne = np.zeros(1, np.uint64)
         self.check(self.lib.fdref_generate_dataset(out_dir.encode(), num_nodes, dim, avg, seed, _p(ne)))
         return int(ne[0])
+
+    def stage_dataset(self, out_dir, num_nodes, dim, avg, seed, threads, features=True):
+        """Reference generator run multi-threaded straight into indptr.bin / indices.bin
+        under out_dir (a tmpfs such as /dev/shm keeps it in RAM). Returns (features
+        array in host memory or None, num_edges). The feature file itself is not
+        written: the CPU baseline extracts from host memory (SSD staging is out of scope)."""
+        os.makedirs(out_dir, exist_ok=True)
+        indptr = np.lib.format.open_memmap(os.path.join(out_dir, "indptr.npy"), mode="w+", dtype=np.uint64,
+                                           shape=(num_nodes + 1,))
+        self.lib.fdref_gen_indptr(seed, num_nodes, avg, threads, _p(indptr))
+        ne = int(indptr[-1])
+        indptr.tofile(os.path.join(out_dir, "indptr.bin"))
+        del indptr
+        os.remove(os.path.join(out_dir, "indptr.npy"))
+        ip = np.fromfile(os.path.join(out_dir, "indptr.bin"), np.uint64)
+        indices = np.memmap(os.path.join(out_dir, "indices.bin"), mode="w+", dtype=np.uint64, shape=(max(ne, 1),))
+        self.lib.fdref_gen_indices(seed, num_nodes, avg, threads, _p(ip), _p(indices))
+        indices.flush()
+        del indices
+        if ne == 0:
+            open(os.path.join(out_dir, "indices.bin"), "wb").close()
+        feats = None
+        if features:
+            feats = np.empty((num_nodes, dim), np.float32)
+            self.lib.fdref_gen_features(seed, num_nodes, dim, threads, _p(feats))
+        return feats, ne
+
+    def bench_sample_extract(self, topo, table, seeds, n_batches, batch_size, fanouts, seed, epoch, first_batch,
+                             threads):
+        table = np.ascontiguousarray(table)
+        rb = table.shape[1] * table.itemsize
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        f = np.ascontiguousarray(fanouts, np.uint32)
+        cs = np.zeros(n_batches, np.uint64)
+        nc = np.zeros(n_batches, np.uint64)
+        secs = self.lib.fdref_bench_sample_extract(topo.h, _p(table), rb, _p(seeds), n_batches, batch_size, _p(f),
+                                                   len(f), seed, epoch, first_batch, threads, _p(cs), _p(nc))
+        if secs < 0:
+            raise OracleError(9, self.err())
+        return secs, cs, nc
 
     def partition_epoch(self, ids, batch, shuffle_seed):
         ids = np.ascontiguousarray(ids, np.uint64)

@@ -121,6 +121,48 @@ int fdref_generate_dataset(const char* dir, uint64_t num_nodes, uint32_t dim, ui
     });
 }
 
+// Multi-threaded driver over the reference's per-node generator functions (all
+// pure functions of (seed, node), generator.hpp:65-121), filling caller memory
+// (e.g. numpy memmaps of indptr.bin / indices.bin in /dev/shm). Byte-identical to
+// create_synthetic_dataset's files; used to stage Papers-scale CPU baselines.
+extern "C++" template <typename Fn>
+void parallel_nodes(uint64_t n, uint32_t threads, Fn&& fn) {
+    std::vector<std::thread> pool;
+    std::atomic<uint64_t> next{0};
+    const uint64_t chunk = 1 << 14;
+    for (uint32_t t = 0; t < std::max<uint32_t>(threads, 1); ++t)
+        pool.emplace_back([&] {
+            for (;;) {
+                uint64_t lo = next.fetch_add(chunk);
+                if (lo >= n) return;
+                uint64_t hi = std::min(n, lo + chunk);
+                for (uint64_t v = lo; v < hi; ++v) fn(v);
+            }
+        });
+    for (auto& th : pool) th.join();
+}
+
+void fdref_gen_indptr(uint64_t seed, uint64_t n, uint32_t avg, uint32_t threads, uint64_t* indptr) {
+    parallel_nodes(n, threads, [&](uint64_t v) { indptr[v + 1] = storage::synthetic_in_degree(seed, v, avg, n); });
+    indptr[0] = 0;
+    for (uint64_t v = 0; v < n; ++v) indptr[v + 1] += indptr[v];
+}
+
+void fdref_gen_indices(uint64_t seed, uint64_t n, uint32_t avg, uint32_t threads, const uint64_t* indptr,
+                       uint64_t* indices) {
+    parallel_nodes(n, threads, [&](uint64_t v) {
+        auto nb = storage::synthetic_in_neighbors(seed, v, avg, n);
+        std::memcpy(indices + indptr[v], nb.data(), nb.size() * 8);
+    });
+}
+
+void fdref_gen_features(uint64_t seed, uint64_t n, uint32_t dim, uint32_t threads, void* out) {
+    parallel_nodes(n, threads, [&](uint64_t v) {
+        storage::synthetic_row(seed, v, dim,
+                               std::span<std::byte>(static_cast<std::byte*>(out) + v * dim * 4ull, dim * 4ull));
+    });
+}
+
 // ---- graph (graph/topology.hpp, graph/sampling.hpp) ------------------------
 void* fdref_topology_open(const char* dir) {
     try {

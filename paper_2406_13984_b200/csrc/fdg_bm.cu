@@ -105,7 +105,7 @@ __device__ uint32_t lookback(unsigned long long* tiles, uint32_t tile, uint32_t 
         }
         if (__any_sync(0xffffffffu, st == 0)) continue;
         uint32_t im = __ballot_sync(0xffffffffu, st == 2);
-        int stop = __ffs(im) - 1;
+        int stop = im ? __ffs(im) - 1 : 32;  // nearest inclusive predecessor in this window
         uint32_t c = lane <= stop ? v : 0;
 #pragma unroll
         for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -237,14 +237,10 @@ __global__ void __launch_bounds__(kT) k_select(BmDev B, uint32_t epoch) {
         __syncthreads();
         if (tile == 0xFFFFFFFFu) return;
         const uint64_t p0 = head + uint64_t(tile) * kTileN;
-        if (p0 >= tail && tile > 0) {
-            // past the ring end: publish an empty inclusive so successors resolve
-            if (threadIdx.x < 32) {
-                uint32_t ex = lookback(B.tiles, tile, 0, epoch, threadIdx.x & 31);
-                if (threadIdx.x == 0 && ex < L) atomicExch(&S->status, uint32_t(FDG_CAPACITY));
-            }
-            return;
-        }
+        // Past the ring end: nothing to rank (the tile holding tail-1 -- or tile 0 of
+        // an empty ring -- reports a short standby list). No look-back slot is used,
+        // so tile ids stay within the tiles array.
+        if (p0 >= tail && tile > 0) return;
         uint32_t live_mask = 0, mine = 0;
         int32_t slots[kI];
 #pragma unroll

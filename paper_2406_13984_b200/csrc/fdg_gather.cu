@@ -111,6 +111,11 @@ __global__ void k_gather4(const uint64_t* __restrict__ nodes, const uint32_t* n_
 
 constexpr int kHashWarps = 4;
 
+__host__ __device__ __forceinline__ uint32_t hash_stride(uint32_t rb) {
+    uint32_t s = (rb + 7) & ~7u;
+    return ((s >> 3) & 1) ? s : s + 8;
+}
+
 __device__ __forceinline__ uint64_t hash_row_smem(const char* row, uint32_t n) {
     uint64_t h = 0x27d4eb2f165667c5ull ^ (uint64_t(n) * 0x9e3779b97f4a7c15ull);
     uint32_t full = n >> 3;
@@ -128,7 +133,8 @@ __device__ __forceinline__ uint64_t hash_row_smem(const char* row, uint32_t n) {
 }
 
 // Gather + trainer checksum. Rows are staged per warp in shared memory with a
-// stride of row_bytes + 8 so the per-lane 8-byte hash reads are conflict-free.
+// stride (hash_stride) that is 8-byte aligned and an odd number of 8-byte words, so
+// the per-lane 8-byte hash reads of 16 lanes hit 16 distinct bank pairs.
 // ALIAS: rows are FeatureRegion slots addressed by the alias list (t.base = region,
 // `nodes` holds the i64 aliases) -- trainer_step's region.slot(alias[i]) read.
 template <bool SHARDED, bool ALIAS = false>
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(kHashWarps * 32) k_gather_hash(const uint64_t*
     if (status && *status) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rb = t.row_bytes;
-    const uint32_t stride = rb + 8;
+    const uint32_t stride = hash_stride(rb);
     char* wbuf = smem + size_t(warp) * 32 * stride;
     const uint64_t n = n_dev ? *n_dev : n_host;
     const uint64_t groups = (n + 31) / 32;
@@ -193,7 +199,7 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
     const bool sharded = c.n_shards > 1;
     if (n_bound == 0) return FDG_OK;
     if (checksum) {
-        size_t smem = size_t(kHashWarps) * 32 * (c.row_bytes + 8);
+        size_t smem = size_t(kHashWarps) * 32 * hash_stride(c.row_bytes);
         static bool attr_set[2] = {false, false};
         auto kfn = sharded ? k_gather_hash<true> : k_gather_hash<false>;
         if (!attr_set[sharded]) {
@@ -245,7 +251,7 @@ int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, con
     if (!checksum) return fail(FDG_INVALID_ARG, "checksum: null output");
     TableRef t = table_ref(c);
     t.base = static_cast<const char*>(region);
-    size_t smem = size_t(kHashWarps) * 32 * (c.row_bytes + 8);
+    size_t smem = size_t(kHashWarps) * 32 * hash_stride(c.row_bytes);
     static bool attr_set = false;
     if (!attr_set) {
         FDG_CUDA(cudaFuncSetAttribute(k_gather_hash<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

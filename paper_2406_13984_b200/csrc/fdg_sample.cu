@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kScanThreads) k_intern(Work<IdT> W, uint32_t q
                 }
                 if (__any_sync(0xffffffffu, st == 0)) continue;
                 uint32_t im = __ballot_sync(0xffffffffu, st == 2);
-                int stop = __ffs(im) - 1;  // nearest inclusive predecessor (always exists: jj < 0 counts)
+                int stop = im ? __ffs(im) - 1 : 32;  // nearest inclusive predecessor in this window
                 __threadfence();
                 Tri v{0, 0, 0};
                 if (lane < stop) {
