@@ -167,6 +167,16 @@ int fdg_mt_stream(void* stream, uint64_t rng_seed, uint64_t n, uint64_t* out_dev
  * common.hpp:88-105) into *checksum_dev (caller zeroes it). */
 int fdg_gather(fdg_ctx* ctx, void* stream, const uint64_t* nodes_dev, const uint32_t* n_dev, uint64_t n_host,
                void* out_dev, uint64_t* checksum_dev);
+/* Gather engine: TMA bulk copies (default; one 4-warp CTA per SM) or the 16-byte
+ * LDG/STG kernel (also used for sharded tables and rows not a multiple of 16 B). */
+#define FDG_GATHER_TMA 0
+#define FDG_GATHER_LDG 1
+int fdg_set_gather_impl(int impl);
+/* Tuning knobs (process-wide): "gather_impl" (FDG_GATHER_*), "gather_evict_first"
+ * (0/1: L2 evict-first hints on the gather stream), "l2_persist_mb" (L2 set-aside
+ * for the samplers' hash tables; 0 = off), "hash_load_pct" (hash table sizing). */
+int fdg_set_option(const char* key, int64_t value);
+int fdg_get_option(const char* key, int64_t* value);
 /* Checksum of rows already resident (region slot payloads addressed by alias). */
 int fdg_checksum_alias(fdg_ctx* ctx, void* stream, const void* region_dev, const int64_t* alias_dev,
                        const uint32_t* n_dev, uint64_t n_host, uint64_t* checksum_dev);
@@ -199,7 +209,46 @@ int fdg_bm_reverse(fdg_bm* bm, uint64_t slot, int64_t* node);
 /* Full invariant sweep (validate_locked, buffer_manager.hpp:488-515) on device. */
 int fdg_bm_validate(fdg_bm* bm);
 
-/* ---- host SET-loop runner (pipeline.hpp:185-257 sampler/extractor stages) ----- */
+/* ---- native SET-loop runner: PipelineSession's sampler / extractor / trainer /
+ *      releaser stages for one worker = one GPU (pipeline.hpp:325-543) ------------ */
+typedef struct fdg_pipeline fdg_pipeline;
+typedef struct {
+    uint32_t batch_size;          /* seeds per batch (PipelineConfig::batch_size, pipeline.hpp:37)       */
+    uint32_t n_samplers;          /* concurrent sampler workspaces/streams (0 -> 2)                      */
+    uint32_t prefetch_group;      /* MT19937-64 streams generated per launch, per sampler (0 -> 16)     */
+    uint32_t use_buffer_manager;  /* extract through the GPU BufferManager (config 3)                    */
+    uint64_t buffer_slots;        /* S when use_buffer_manager                                           */
+    uint32_t write_x;             /* materialise the mini-batch tensor X (always on for the plain gather) */
+    uint32_t checksum;            /* fuse trainer_step's checksum (pipeline.hpp:103-124)                 */
+    uint32_t flags;               /* diagnostics: FDG_PIPE_SAMPLE_ONLY / FDG_PIPE_EXTRACT_ONLY           */
+    float host_enqueue_ms;        /* out: host time spent enqueueing the last run                        */
+    uint32_t group_batches;       /* batches sampled per launch chain (0 -> 4, max 8)                    */
+} fdg_pipeline_config;
+#define FDG_PIPE_SAMPLE_ONLY 1u   /* skip extraction (sampler throughput)                                 */
+#define FDG_PIPE_EXTRACT_ONLY 2u  /* sample each slot once, then only extract (extraction throughput)    */
+#define FDG_PIPE_NO_L2_PERSIST 4u /* do not pin the samplers' hash tables in L2                          */
+#define FDG_PIPE_NO_PRIORITY 8u   /* equal stream priorities for sampling and extraction                 */
+/* Current configuration (including host_enqueue_ms of the last run). */
+int fdg_pipeline_get_config(const fdg_pipeline* p, fdg_pipeline_config* out);
+
+int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers, const fdg_pipeline_config* cfg,
+                        fdg_pipeline** out);
+int fdg_pipeline_destroy(fdg_pipeline* p);
+/* Runs n_batches batches; batch j uses seeds[j*batch_size ...] (device memory, or
+ * pinned host memory copied per batch when seeds_on_host) and rng_seeds[j] (host).
+ * records_host (nullable, pinned for async) receives each batch's fdg_batch_counts
+ * by an in-stream D2H copy; extract_ms (nullable) per-batch extraction kernel time;
+ * elapsed_ms = device time of the whole run. Synchronises before returning. */
+int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, const uint64_t* rng_seeds,
+                     uint64_t n_batches, fdg_batch_counts* records_host, float* extract_ms, float* elapsed_ms);
+/* Device batch records of the last run, [first, first+n). */
+int fdg_pipeline_records(fdg_pipeline* p, uint64_t first, uint64_t n, fdg_batch_counts* out);
+
+/* ---- tracing: per-launch CUDA-event timeline (DurationCounter analogue, common.hpp:240-260) */
+int fdg_trace_enable(int on);          /* clears previous records when turning on */
+int fdg_trace_dump(const char* path);  /* CSV: name,stream,start_ms,end_ms       */
+
+/* ---- host helpers ------------------------------------------------------------------ */
 /* partition_epoch (sampling.hpp:57-70) with the same libstdc++ std::shuffle. */
 int fdg_partition_epoch(const uint64_t* train_ids, uint64_t n, uint64_t batch_size, uint64_t shuffle_seed,
                         uint64_t* out_ids);

@@ -6,13 +6,13 @@ this package is its Python mirror of the reference's interface
 """
 from .featdrive import (  # noqa: F401
     BufferManager, CudaError, DeviceBuffer, Event, Extractor, Fanouts, FeatdriveError, InvalidArgument,
-    InvariantViolation, OutOfRange, SampledBatch, Sampler, StandbyTimeout, Stream, Topology, batch_seed,
-    device_count, gather, mt_stream, partition_epoch, sample_khop, trainer_step,
+    InvariantViolation, OutOfRange, Pipeline, SampledBatch, Sampler, StandbyTimeout, Stream, Topology, batch_seed,
+    device_count, gather, mt_stream, partition_epoch, sample_khop, set_option, trainer_step,
 )
 
 __all__ = [
     "BufferManager", "CudaError", "DeviceBuffer", "Event", "Extractor", "Fanouts", "FeatdriveError",
-    "InvalidArgument", "InvariantViolation", "OutOfRange", "SampledBatch", "Sampler", "StandbyTimeout",
+    "InvalidArgument", "InvariantViolation", "OutOfRange", "Pipeline", "SampledBatch", "Sampler", "StandbyTimeout",
     "Stream", "Topology", "batch_seed", "device_count", "gather", "mt_stream", "partition_epoch",
-    "sample_khop", "trainer_step",
+    "sample_khop", "set_option", "trainer_step",
 ]

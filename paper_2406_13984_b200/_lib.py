@@ -33,6 +33,12 @@ class CtxInfo(C.Structure):
                 ("table_dev", vp), ("rows_per_shard", u64), ("device", ci), ("pad", ci)]
 
 
+class PipelineConfig(C.Structure):
+    _fields_ = [("batch_size", u32), ("n_samplers", u32), ("prefetch_group", u32), ("use_buffer_manager", u32),
+                ("buffer_slots", u64), ("write_x", u32), ("checksum", u32), ("flags", u32),
+                ("host_enqueue_ms", C.c_float), ("group_batches", u32)]
+
+
 class BmStats(C.Structure):
     _fields_ = [(k, u64) for k in ("hits", "loads", "waits", "evictions", "takeovers", "releases", "standby_len")]
 
@@ -84,6 +90,9 @@ SIGNATURES = {
     "fdg_mt_stream": (ci, [vp, u64, u64, vp]),
     "fdg_gather": (ci, [vp, vp, vp, vp, u64, vp, vp]),
     "fdg_checksum_alias": (ci, [vp, vp, vp, vp, vp, u64, vp]),
+    "fdg_set_gather_impl": (ci, [ci]),
+    "fdg_set_option": (ci, [C.c_char_p, C.c_int64]),
+    "fdg_get_option": (ci, [C.c_char_p, C.POINTER(C.c_int64)]),
     "fdg_bm_create": (ci, [vp, u64, u64, u32, C.POINTER(vp)]),
     "fdg_bm_destroy": (ci, [vp]),
     "fdg_bm_extract": (ci, [vp, vp, vp, vp, u64, vp, vp, vp]),
@@ -94,6 +103,11 @@ SIGNATURES = {
     "fdg_bm_entry": (ci, [vp, u64, C.POINTER(i64), C.POINTER(u32), C.POINTER(u32)]),
     "fdg_bm_reverse": (ci, [vp, u64, C.POINTER(i64)]),
     "fdg_bm_validate": (ci, [vp]),
+    "fdg_pipeline_create": (ci, [vp, vp, u32, C.POINTER(PipelineConfig), C.POINTER(vp)]),
+    "fdg_pipeline_destroy": (ci, [vp]),
+    "fdg_pipeline_run": (ci, [vp, vp, ci, vp, u64, vp, vp, C.POINTER(C.c_float)]),
+    "fdg_pipeline_records": (ci, [vp, u64, u64, vp]),
+    "fdg_pipeline_get_config": (ci, [vp, C.POINTER(PipelineConfig)]),
     "fdg_partition_epoch": (ci, [vp, u64, u64, u64, vp]),
     "fdg_batch_seed": (u64, [u64, u64, u64]),
 }

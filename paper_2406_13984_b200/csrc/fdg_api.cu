@@ -370,6 +370,41 @@ int fdg_gather(fdg_ctx* c, void* st, const uint64_t* nodes, const uint32_t* n_de
     return launch_gather(*c, (cudaStream_t)st, nodes, n_dev, n_host, out, checksum);
 }
 
+int fdg_set_gather_impl(int impl) {
+    if (impl != FDG_GATHER_TMA && impl != FDG_GATHER_LDG) return fail(FDG_INVALID_ARG, "unknown gather impl");
+    g_gather_impl = impl;
+    return FDG_OK;
+}
+
+int fdg_set_option(const char* key, int64_t v) {
+    std::string k(key);
+    if (k == "gather_impl") return fdg_set_gather_impl(int(v));
+    if (k == "gather_evict_first") { g_gather_evict_first = v != 0; return FDG_OK; }
+    if (k == "l2_persist_mb") { g_l2_persist_mb = v < 0 ? 0 : v; return FDG_OK; }
+    if (k == "gather_ctas_per_sm") {
+        if (v < 1 || v > 4) return fail(FDG_INVALID_ARG, "gather_ctas_per_sm must be in [1, 4]");
+        g_gather_ctas_per_sm = int(v);
+        return FDG_OK;
+    }
+    if (k == "hash_load_pct") {
+        if (v < 10 || v > 70) return fail(FDG_INVALID_ARG, "hash_load_pct must be in [10, 70]");
+        g_hash_load_pct = v;
+        return FDG_OK;
+    }
+    return fail(FDG_INVALID_ARG, "unknown option " + k);
+}
+
+int fdg_get_option(const char* key, int64_t* v) {
+    std::string k(key);
+    if (k == "gather_impl") *v = g_gather_impl;
+    else if (k == "gather_evict_first") *v = g_gather_evict_first;
+    else if (k == "l2_persist_mb") *v = g_l2_persist_mb;
+    else if (k == "hash_load_pct") *v = g_hash_load_pct;
+    else if (k == "gather_ctas_per_sm") *v = g_gather_ctas_per_sm;
+    else return fail(FDG_INVALID_ARG, "unknown option " + k);
+    return FDG_OK;
+}
+
 int fdg_checksum_alias(fdg_ctx* c, void* st, const void* region, const int64_t* alias, const uint32_t* n_dev,
                        uint64_t n_host, uint64_t* checksum) {
     return launch_checksum_alias(*c, (cudaStream_t)st, region, alias, n_dev, n_host, checksum);

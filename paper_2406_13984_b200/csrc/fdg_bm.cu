@@ -445,6 +445,10 @@ __global__ void k_compact_finish(BmDev B, uint64_t slack) {
     S->tail = S->new_head;
 }
 
+__global__ void k_status_to(const BmState* S, uint32_t* dst) {
+    if (S->status && *dst == 0) *dst = S->status;
+}
+
 __global__ void k_reset_ctrs(BmState* S) {
     if (threadIdx.x < 4) S->tile_ctr[threadIdx.x] = 0;
 }
@@ -584,7 +588,7 @@ int fdg_bm_extract(fdg_bm* b, void* stv, const uint64_t* nodes, const uint32_t* 
     k_move<<<blocks, 512, 0, st>>>(d, nodes, n_dev, n_host, alias, table, b->region, rb, static_cast<char*>(out));
     FDG_CUDA(cudaGetLastError());
     if (checksum) {
-        FDG_TRY(launch_checksum_alias(*b->ctx, st, b->region, alias, n_dev, n_host, checksum));
+        FDG_TRY(launch_checksum_alias(*b->ctx, st, b->region, alias, n_dev, n_host, checksum, &d.st->status));
     }
     return FDG_OK;
 }
@@ -600,6 +604,19 @@ int fdg_bm_release(fdg_bm* b, void* stv, const uint64_t* nodes, const uint32_t* 
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;
 }
+
+}  // extern "C"
+
+namespace fdg {
+// Copies a device-detected buffer-manager error into a batch record's status (stream-ordered).
+int bm_status_to(fdg_bm* b, cudaStream_t st, uint32_t* dst) {
+    k_status_to<<<1, 1, 0, st>>>(b->d.st, dst);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+}  // namespace fdg
+
+extern "C" {
 
 int fdg_bm_stats_get(fdg_bm* b, fdg_bm_stats* out) {
     FDG_CUDA(cudaDeviceSynchronize());

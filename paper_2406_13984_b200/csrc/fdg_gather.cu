@@ -37,6 +37,7 @@ struct TableRef {
     uint64_t rows_per_shard;
     uint32_t n_shards;
     uint32_t row_bytes;
+    uint32_t evict_first;
 };
 
 template <bool SHARDED>
@@ -49,19 +50,33 @@ __device__ __forceinline__ const char* row_ptr(const TableRef& t, uint64_t node)
     }
 }
 
-__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+// Gather traffic is marked L2 evict-first so the ~1 GB/batch stream does not
+// flush the samplers' hash tables and CSR lines out of the 126 MB L2.
+__device__ __forceinline__ uint64_t gather_policy(bool evict_first) {
+    uint64_t pol;
+    if (evict_first)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p, uint64_t pol) {
     uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
+                 : "l"(p), "l"(pol));
     return v;
 }
-__device__ __forceinline__ void stg_stream(uint4* p, uint4 v) {
-    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+__device__ __forceinline__ void stg_stream(uint4* p, uint4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w), "l"(pol)
                  : "memory");
 }
 
 constexpr int kUnroll = 4;
+// 2 x 512 threads per SM (half the SM's warp slots): enough bytes in flight to
+// saturate HBM while leaving room for the next batch's sampling kernels and the
+// MT prefetch CTAs to co-reside (they run on other streams).
 
 // 16-byte chunk gather over the flattened output.
 template <bool SHARDED>
@@ -72,6 +87,7 @@ __global__ void __launch_bounds__(512) k_gather16(const uint64_t* __restrict__ n
     const uint64_t n = n_dev ? *n_dev : n_host;
     const uint32_t total = uint32_t(n * cpr);
     const uint32_t stride = gridDim.x * blockDim.x;
+    const uint64_t pol = gather_policy(t.evict_first);
     uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     for (; c + (kUnroll - 1) * stride < total; c += kUnroll * stride) {
         uint4 v[kUnroll];
@@ -82,16 +98,16 @@ __global__ void __launch_bounds__(512) k_gather16(const uint64_t* __restrict__ n
             uint32_t row = cdiv.div(cc[u]);
             uint32_t col = cc[u] - row * cpr;
             const uint4* src = reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, __ldg(nodes + row))) + col;
-            v[u] = ldg_stream(src);
+            v[u] = ldg_stream(src, pol);
         }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) stg_stream(out + cc[u], v[u]);
+        for (int u = 0; u < kUnroll; ++u) stg_stream(out + cc[u], v[u], pol);
     }
     for (; c < total; c += stride) {
         uint32_t row = cdiv.div(c);
         uint32_t col = c - row * cpr;
         const uint4* src = reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, __ldg(nodes + row))) + col;
-        stg_stream(out + c, ldg_stream(src));
+        stg_stream(out + c, ldg_stream(src, pol), pol);
     }
 }
 
@@ -187,10 +203,17 @@ TableRef table_ref(const Ctx& c) {
     t.rows_per_shard = c.rows_per_shard;
     t.n_shards = c.n_shards;
     t.row_bytes = c.row_bytes;
+    t.evict_first = g_gather_evict_first;
     return t;
 }
 
 }  // namespace
+
+// LDG/STG is the default: measured 177 us vs 203 us (TMA bulk) per Papers batch in
+// isolation and never slower inside the pipeline (profiles/README.md).
+int g_gather_impl = FDG_GATHER_LDG;
+int g_gather_evict_first = 1;
+int g_gather_ctas_per_sm = 2;
 
 int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
                         uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status) {
@@ -198,6 +221,9 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
     TableRef t = table_ref(c);
     const bool sharded = c.n_shards > 1;
     if (n_bound == 0) return FDG_OK;
+    if (g_gather_impl == FDG_GATHER_TMA && out &&
+        launch_gather_tma(c, st, nodes, n_dev, n_host, out, checksum, status) == FDG_OK)
+        return FDG_OK;  // rows that do not suit the TMA path fall through to the LDG kernels
     if (checksum) {
         size_t smem = size_t(kHashWarps) * 32 * hash_stride(c.row_bytes);
         static bool attr_set[2] = {false, false};
@@ -219,7 +245,7 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
         FastDiv d;
         d.init(cpr);
         uint64_t total = n_bound * cpr;
-        int blocks = int(std::min<uint64_t>((total + 511) / 512, uint64_t(c.sm_count) * 4));
+        int blocks = int(std::min<uint64_t>((total + 511) / 512, uint64_t(c.sm_count) * g_gather_ctas_per_sm));
         if (sharded)
             k_gather16<true><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr, static_cast<uint4*>(out));
         else
@@ -246,7 +272,7 @@ int launch_gather(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const ui
 }
 
 int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, const int64_t* alias,
-                          const uint32_t* n_dev, uint64_t n_host, uint64_t* checksum) {
+                          const uint32_t* n_dev, uint64_t n_host, uint64_t* checksum, const uint32_t* status) {
     if (c.row_bytes == 0) return fail(FDG_NOT_LOADED, "checksum: no feature table loaded");
     if (!checksum) return fail(FDG_INVALID_ARG, "checksum: null output");
     TableRef t = table_ref(c);
@@ -262,7 +288,7 @@ int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, con
     uint64_t groups = (std::max<uint64_t>(n_host, 1) + 31) / 32;
     int blocks = int(std::min<uint64_t>((groups + kHashWarps - 1) / kHashWarps, uint64_t(c.sm_count) * 8));
     k_gather_hash<false, true><<<blocks, kHashWarps * 32, smem, st>>>(reinterpret_cast<const uint64_t*>(alias), n_dev,
-                                                                     n_host, nullptr, t, nullptr, checksum);
+                                                                     n_host, status, t, nullptr, checksum);
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;
 }

@@ -28,6 +28,22 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
         if (_rc != FDG_OK) return _rc;     \
     } while (0)
 
+// ---- tracing (fdg_trace.cu) --------------------------------------------------------
+extern bool g_trace;
+class TraceScope {  // records events around the enclosed launches when tracing is on
+public:
+    TraceScope(const char* name, cudaStream_t st);
+    ~TraceScope();
+
+private:
+    const char* name_;
+    cudaStream_t st_;
+    cudaEvent_t a_ = nullptr;
+};
+#define FDG_CAT2(a, b) a##b
+#define FDG_CAT(a, b) FDG_CAT2(a, b)
+#define FDG_TRACE(name, st) ::fdg::TraceScope FDG_CAT(_fdg_trace_, __LINE__)(name, st)
+
 // ---- reference hashing on device (common.hpp:77-105) ------------------------------
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     x += 0x9e3779b97f4a7c15ull;
@@ -77,11 +93,22 @@ int generate_features(Ctx& c, uint64_t seed, uint64_t num_nodes, uint32_t dim, u
 // rng_seeds: HOST array (passed by value to the kernel)
 cudaError_t launch_mt_streams(cudaStream_t st, const uint64_t* rng_seeds, uint32_t n_streams,
                               uint64_t words_per_stream, uint64_t* out_dev, uint64_t out_stride);
+// one CTA per stream, CTA i writing ring + slots[i] * stride
+cudaError_t launch_mt_streams_slots(cudaStream_t st, const uint64_t* rng_seeds, const uint32_t* slots,
+                                    uint32_t n_streams, uint64_t words_per_stream, uint64_t* ring, uint64_t stride);
 // gather (fdg_gather.cu)
 int launch_gather(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                   void* out, uint64_t* checksum);
+extern int g_gather_impl;  // FDG_GATHER_TMA (default) or FDG_GATHER_LDG
+extern int g_gather_evict_first;
+extern int g_gather_ctas_per_sm;
+extern int64_t g_l2_persist_mb;
+extern int64_t g_hash_load_pct;
+int launch_gather_tma(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                      void* out, uint64_t* checksum, const uint32_t* status);
 int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, const int64_t* alias,
-                          const uint32_t* n_dev, uint64_t n_host, uint64_t* checksum);
+                          const uint32_t* n_dev, uint64_t n_host, uint64_t* checksum,
+                          const uint32_t* status = nullptr);
 int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
                         uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status);
 }  // namespace fdg

@@ -36,13 +36,14 @@ __device__ __forceinline__ uint64_t temper(uint64_t z) {
 
 struct MtSeeds {
     uint64_t s[32];
+    uint32_t slot[32];  // output block of CTA i = out + slot[i] * stride
 };
 
 __global__ void __launch_bounds__(160) k_mt_stream(MtSeeds seeds, uint64_t words, uint64_t* __restrict__ out,
                                                    uint64_t stride) {
     __shared__ uint64_t buf[2][kN];
     const int i = threadIdx.x;
-    uint64_t* dst = out + blockIdx.x * stride;
+    uint64_t* dst = out + uint64_t(seeds.slot[blockIdx.x]) * stride;
     if (i == 0) {  // [rand.eng.mers] seeding: x_i = f*(x_{i-1} ^ (x_{i-1} >> (w-2))) + i
         uint64_t x = splitmix64(seeds.s[blockIdx.x]);
         buf[0][0] = x;
@@ -93,8 +94,27 @@ cudaError_t launch_mt_streams(cudaStream_t st, const uint64_t* rng_seeds, uint32
     for (uint32_t base = 0; base < n_streams; base += 32) {
         MtSeeds p;
         uint32_t k = n_streams - base < 32 ? n_streams - base : 32;
-        for (uint32_t i = 0; i < k; ++i) p.s[i] = rng_seeds[base + i];
-        k_mt_stream<<<k, 160, 0, st>>>(p, words_per_stream, out_dev + uint64_t(base) * out_stride, out_stride);
+        for (uint32_t i = 0; i < k; ++i) {
+            p.s[i] = rng_seeds[base + i];
+            p.slot[i] = base + i;
+        }
+        k_mt_stream<<<k, 160, 0, st>>>(p, words_per_stream, out_dev, out_stride);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_mt_streams_slots(cudaStream_t st, const uint64_t* rng_seeds, const uint32_t* slots,
+                                    uint32_t n_streams, uint64_t words_per_stream, uint64_t* ring, uint64_t stride) {
+    for (uint32_t base = 0; base < n_streams; base += 32) {
+        MtSeeds p;
+        uint32_t k = n_streams - base < 32 ? n_streams - base : 32;
+        for (uint32_t i = 0; i < k; ++i) {
+            p.s[i] = rng_seeds[base + i];
+            p.slot[i] = slots[base + i];
+        }
+        k_mt_stream<<<k, 160, 0, st>>>(p, words_per_stream, ring, stride);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

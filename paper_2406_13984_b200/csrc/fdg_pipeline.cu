@@ -1,0 +1,358 @@
+// fdg_pipeline.cu -- native SET-loop runner: the B200 counterpart of
+// PipelineSession's sampler / extractor / trainer / releaser stages
+// (pipeline.hpp:325-543) for one worker (= one GPU).
+//
+// Reference: 4 sampler threads, 4 extractor threads, 1 trainer, 1 releaser and
+// bounded queues (pipeline.hpp:356-377). Here the "queues" are CUDA events
+// between streams:
+//   mt stream       : MT19937-64 streams for upcoming batches of each sampler,
+//                     one CTA per batch, generated far ahead of use
+//   S sampler streams: groups of G consecutive batches, round-robin over the
+//                     samplers; one launch chain samples a whole group
+//   extract stream  : per batch, the gather (or buffer-manager extract + lag-1
+//                     release) into the mini-batch tensor, the optional fused
+//                     trainer checksum and the optional D2H of the batch record
+// so groups g+1..g+S are sampled while group g is extracted. Batch j is keyed
+// exactly as the reference (rng seed = batch_seed(seed, epoch, global id)).
+#include <algorithm>
+#include <chrono>
+#include <vector>
+
+#include "fdg_internal.cuh"
+
+namespace fdg {
+struct Sampler;
+int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32_t n_layers, Sampler** out,
+                   uint32_t group);
+void sampler_destroy(Sampler* s);
+int sampler_prefetch(Sampler* s, cudaStream_t st, const uint64_t* rng_seeds, uint32_t n);
+int sampler_sample_group(Sampler* s, cudaStream_t st, uint32_t n, const uint64_t* const* seeds, const uint32_t* n_seeds,
+                         const uint64_t* rng_seeds, uint64_t* const* nodes, uint32_t* const* edges, uint64_t cap,
+                         fdg_batch_counts* const* cnt);
+void sampler_capacity(const Sampler* s, uint64_t* max_nodes, uint64_t* max_edges);
+void sampler_hash_region(const Sampler* s, void** base, uint64_t* bytes);
+int bm_status_to(fdg_bm* b, cudaStream_t st, uint32_t* dst);
+}  // namespace fdg
+
+struct fdg_pipeline {
+    fdg::Ctx* ctx = nullptr;
+    fdg_pipeline_config cfg{};
+    std::vector<fdg::Sampler*> samplers;
+    std::vector<cudaStream_t> sstream;
+    cudaStream_t xstream = nullptr, mstream = nullptr;
+    uint64_t cap = 0, max_nodes = 0;
+    uint32_t nslots = 0;             // per-batch output slots (2 * S * G)
+    std::vector<uint64_t*> nodes;
+    std::vector<uint32_t*> edges;
+    std::vector<uint64_t*> seeds;    // per-slot staging for host seeds
+    std::vector<int64_t*> alias;
+    std::vector<void*> X;
+    std::vector<cudaEvent_t> extracted;  // per slot
+    std::vector<cudaEvent_t> sampled;    // per group slot (2 * S)
+    fdg_batch_counts* counts = nullptr;  // device, one per batch of the current run
+    uint64_t counts_cap = 0;
+    std::vector<cudaEvent_t> tev;        // per-batch extract timing events (2 per batch)
+    fdg_bm* bm = nullptr;
+};
+
+using namespace fdg;
+
+namespace {
+
+void destroy(fdg_pipeline* p) {
+    if (!p) return;
+    cudaDeviceSynchronize();
+    for (auto s : p->samplers) sampler_destroy(s);
+    for (auto s : p->sstream) cudaStreamDestroy(s);
+    if (p->xstream) cudaStreamDestroy(p->xstream);
+    if (p->mstream) cudaStreamDestroy(p->mstream);
+    for (auto v : p->nodes) cudaFree(v);
+    for (auto v : p->edges) cudaFree(v);
+    for (auto v : p->seeds) cudaFree(v);
+    for (auto v : p->alias) cudaFree(v);
+    for (auto v : p->X) cudaFree(v);
+    for (auto e : p->sampled) cudaEventDestroy(e);
+    for (auto e : p->extracted) cudaEventDestroy(e);
+    for (auto e : p->tev) cudaEventDestroy(e);
+    if (p->counts) cudaFree(p->counts);
+    if (p->bm) fdg_bm_destroy(p->bm);
+    delete p;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers, const fdg_pipeline_config* cfg,
+                        fdg_pipeline** out) {
+    if (cfg->batch_size == 0) return fail(FDG_INVALID_ARG, "config: batch_size must be >= 1");
+    if (ctx->row_bytes == 0) return fail(FDG_NOT_LOADED, "pipeline: no feature table loaded");
+    cudaSetDevice(ctx->device);
+    auto p = new fdg_pipeline();
+    p->ctx = ctx;
+    p->cfg = *cfg;
+    if (p->cfg.n_samplers == 0) p->cfg.n_samplers = 2;
+    if (p->cfg.prefetch_group == 0) p->cfg.prefetch_group = 16;
+    if (p->cfg.group_batches == 0) p->cfg.group_batches = 1;
+    p->cfg.group_batches = std::min<uint32_t>(p->cfg.group_batches, 8);
+    // the MT ring (2 prefetch chunks) must never recycle a slot of the group being sampled
+    p->cfg.prefetch_group = std::max<uint32_t>(p->cfg.prefetch_group, 2 * p->cfg.group_batches);
+    const uint32_t S = p->cfg.n_samplers, G = p->cfg.group_batches;
+    // Sampler streams get the highest priority: their short latency-bound kernels
+    // should take free SM slots ahead of the bandwidth-bound extraction.
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    const bool prio = !(p->cfg.flags & FDG_PIPE_NO_PRIORITY);
+    for (uint32_t i = 0; i < S; ++i) {
+        Sampler* s = nullptr;
+        int rc = sampler_create(ctx, cfg->batch_size, fanouts, n_layers, &s, G);
+        if (rc) {
+            destroy(p);
+            return rc;
+        }
+        p->samplers.push_back(s);
+        cudaStream_t st;
+        FDG_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio ? prio_hi : prio_lo));
+        p->sstream.push_back(st);
+    }
+    // Optional: keep the samplers' batch hash tables L2-resident (persisting window).
+    if (!(p->cfg.flags & FDG_PIPE_NO_L2_PERSIST) && g_l2_persist_mb > 0) {
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
+        uint64_t want = 0;
+        for (auto s : p->samplers) {
+            void* b;
+            uint64_t n;
+            sampler_hash_region(s, &b, &n);
+            want += n;
+        }
+        if (max_persist > 0 && max_window > 0) {
+            const uint64_t persist =
+                std::min<uint64_t>(std::min<uint64_t>(want, uint64_t(max_persist)), uint64_t(g_l2_persist_mb) << 20);
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist);
+            for (uint32_t i = 0; i < S; ++i) {
+                void* b;
+                uint64_t n;
+                sampler_hash_region(p->samplers[i], &b, &n);
+                cudaStreamAttrValue a{};
+                a.accessPolicyWindow.base_ptr = b;
+                a.accessPolicyWindow.num_bytes = std::min<uint64_t>(n, uint64_t(max_window));
+                a.accessPolicyWindow.hitRatio = float(std::min(1.0, double(persist) / double(want)));
+                a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                cudaStreamSetAttribute(p->sstream[i], cudaStreamAttributeAccessPolicyWindow, &a);
+            }
+            cudaGetLastError();  // an optimisation only; ignore unsupported configurations
+        }
+    }
+    uint64_t mn, me;
+    sampler_capacity(p->samplers[0], &mn, &me);
+    p->max_nodes = mn;
+    p->cap = std::max<uint64_t>(std::max(mn, me), 1);
+    FDG_CUDA(cudaStreamCreateWithPriority(&p->xstream, cudaStreamNonBlocking, prio_lo));
+    FDG_CUDA(cudaStreamCreateWithFlags(&p->mstream, cudaStreamNonBlocking));
+    p->nslots = 2 * S * G;
+    for (uint32_t i = 0; i < p->nslots; ++i) {
+        uint64_t* n;
+        uint32_t* e;
+        uint64_t* sd;
+        FDG_CUDA(cudaMalloc(&n, p->cap * 8));
+        FDG_CUDA(cudaMalloc(&e, p->cap * 8));
+        FDG_CUDA(cudaMalloc(&sd, uint64_t(cfg->batch_size) * 8));
+        p->nodes.push_back(n);
+        p->edges.push_back(e);
+        p->seeds.push_back(sd);
+        cudaEvent_t b;
+        FDG_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        p->extracted.push_back(b);
+        FDG_CUDA(cudaEventRecord(b, p->xstream));
+    }
+    for (uint32_t i = 0; i < 2 * S; ++i) {
+        cudaEvent_t a;
+        FDG_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        p->sampled.push_back(a);
+    }
+    if (!cfg->use_buffer_manager) p->cfg.write_x = 1;  // the gather's product is X itself
+    for (uint32_t i = 0; i < 2; ++i) {
+        void* x = nullptr;
+        if (p->cfg.write_x) FDG_CUDA(cudaMalloc(&x, p->cap * ctx->row_bytes));
+        p->X.push_back(x);
+        int64_t* a = nullptr;
+        if (cfg->use_buffer_manager) FDG_CUDA(cudaMalloc(&a, p->cap * 8));
+        p->alias.push_back(a);
+    }
+    if (cfg->use_buffer_manager) {
+        int rc = fdg_bm_create(ctx, cfg->buffer_slots, 0, uint32_t(p->max_nodes), &p->bm);
+        if (rc) {
+            destroy(p);
+            return rc;
+        }
+    }
+    *out = p;
+    return FDG_OK;
+}
+
+int fdg_pipeline_destroy(fdg_pipeline* p) {
+    destroy(p);
+    return FDG_OK;
+}
+
+int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, const uint64_t* rng_seeds,
+                     uint64_t n_batches, fdg_batch_counts* records_host, float* extract_ms, float* elapsed_ms) {
+    cudaSetDevice(p->ctx->device);
+    const uint32_t S = p->cfg.n_samplers, PG = p->cfg.prefetch_group, B = p->cfg.batch_size;
+    const uint32_t G = p->cfg.group_batches;
+    if (n_batches == 0) return FDG_OK;
+    if (p->counts_cap < n_batches) {
+        if (p->counts) cudaFree(p->counts);
+        FDG_CUDA(cudaMalloc(&p->counts, n_batches * sizeof(fdg_batch_counts)));
+        p->counts_cap = n_batches;
+    }
+    if (extract_ms && p->tev.size() < 2 * n_batches) {
+        for (size_t i = p->tev.size(); i < 2 * n_batches; ++i) {
+            cudaEvent_t e;
+            FDG_CUDA(cudaEventCreate(&e));
+            p->tev.push_back(e);
+        }
+    }
+    const bool sample_only = p->cfg.flags & FDG_PIPE_SAMPLE_ONLY;
+    const bool extract_only = p->cfg.flags & FDG_PIPE_EXTRACT_ONLY;
+    const uint64_t n_groups = (n_batches + G - 1) / G;
+    const uint64_t sampled_groups = extract_only ? std::min<uint64_t>(n_groups, 2 * S) : n_groups;
+    // per-sampler batch lists (in sampling order) and their MT prefetch in chunks of PG
+    std::vector<std::vector<uint64_t>> mine(S);
+    for (uint64_t g = 0; g < sampled_groups; ++g)
+        for (uint64_t j = g * G; j < std::min<uint64_t>((g + 1) * G, n_batches); ++j) mine[g % S].push_back(j);
+    std::vector<uint64_t> fetched(S, 0);  // batches of mine[s] whose streams were requested
+    auto prefetch_upto = [&](uint32_t s, uint64_t upto) -> int {
+        upto = std::min<uint64_t>(upto, mine[s].size());
+        while (fetched[s] < upto) {
+            std::vector<uint64_t> r;
+            for (uint64_t k = fetched[s]; k < std::min<uint64_t>(fetched[s] + PG, mine[s].size()); ++k)
+                r.push_back(rng_seeds[mine[s][k]]);
+            FDG_TRY(sampler_prefetch(p->samplers[s], p->mstream, r.data(), uint32_t(r.size())));
+            fetched[s] += r.size();
+        }
+        return FDG_OK;
+    };
+    for (uint32_t s = 0; s < S; ++s) FDG_TRY(prefetch_upto(s, PG));
+    std::vector<uint64_t> consumed(S, 0);
+    cudaEvent_t t0, t1;
+    FDG_CUDA(cudaEventCreate(&t0));
+    FDG_CUDA(cudaEventCreate(&t1));
+    FDG_CUDA(cudaEventRecord(t0, p->xstream));
+    for (uint32_t s = 0; s < S; ++s) FDG_CUDA(cudaStreamWaitEvent(p->sstream[s], t0, 0));
+    auto h0 = std::chrono::steady_clock::now();
+    for (uint64_t g = 0; g < n_groups; ++g) {
+        const uint64_t j0 = g * G, j1 = std::min<uint64_t>(j0 + G, n_batches);
+        const uint32_t n = uint32_t(j1 - j0);
+        const uint32_t s = uint32_t(g % S);
+        const bool do_sample = g < sampled_groups;
+        const uint32_t gslot = uint32_t(g % (2 * S));
+        if (do_sample) {
+            // keep the MT ring ~1.5 prefetch chunks ahead of this sampler's consumption
+            FDG_TRY(prefetch_upto(s, consumed[s] + n + PG));
+            cudaStream_t ss = p->sstream[s];
+            const uint64_t* sd[8];
+            uint32_t ns[8];
+            uint64_t rs[8];
+            uint64_t* nd[8];
+            uint32_t* ed[8];
+            fdg_batch_counts* cn[8];
+            for (uint32_t i = 0; i < n; ++i) {
+                const uint64_t j = j0 + i;
+                const uint32_t slot = uint32_t(j % p->nslots);
+                FDG_CUDA(cudaStreamWaitEvent(ss, p->extracted[slot], 0));
+                sd[i] = seeds + j * B;
+                if (seeds_on_host) {  // host -> device copy of this batch's seeds (pinned for async)
+                    FDG_CUDA(cudaMemcpyAsync(p->seeds[slot], sd[i], uint64_t(B) * 8, cudaMemcpyHostToDevice, ss));
+                    sd[i] = p->seeds[slot];
+                }
+                ns[i] = B;
+                rs[i] = rng_seeds[j];
+                nd[i] = p->nodes[slot];
+                ed[i] = p->edges[slot];
+                cn[i] = p->counts + j;
+            }
+            FDG_TRY(sampler_sample_group(p->samplers[s], ss, n, sd, ns, rs, nd, ed, p->cap, cn));
+            consumed[s] += n;
+            FDG_CUDA(cudaEventRecord(p->sampled[gslot], ss));
+            FDG_CUDA(cudaStreamWaitEvent(p->xstream, p->sampled[gslot], 0));
+        }
+        for (uint64_t j = j0; j < j1; ++j) {
+            const uint32_t slot = uint32_t(j % p->nslots);
+            // extract-only diagnostics re-extract the batches sampled in the first groups
+            const uint64_t src_j = do_sample ? j : (j % (sampled_groups * G));
+            fdg_batch_counts* cnt = p->counts + src_j;
+            if (sample_only) {
+                FDG_CUDA(cudaEventRecord(p->extracted[slot], p->xstream));
+                continue;
+            }
+            FDG_TRACE("extract", p->xstream);
+            if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j], p->xstream));
+            const uint32_t* n_dev = &cnt->n_nodes;
+            uint64_t* cs = p->cfg.checksum ? &cnt->checksum : nullptr;
+            void* X = p->X[j & 1];
+            const uint32_t nslot = uint32_t(src_j % p->nslots);
+            if (!p->bm) {
+                FDG_TRY(launch_gather_bound(*p->ctx, p->xstream, p->nodes[nslot], n_dev, p->cap, p->cap, X, cs,
+                                            &cnt->status));
+            } else {
+                FDG_TRY(fdg_bm_extract(p->bm, p->xstream, p->nodes[nslot], n_dev, p->cap, p->alias[j & 1], X, cs));
+                FDG_TRY(bm_status_to(p->bm, p->xstream, &cnt->status));  // e.g. CAPACITY = StandbyTimeout
+                if (j > 0) {  // lag-1 release (the releaser stage, pipeline.hpp:525-543)
+                    const uint64_t pj = do_sample ? j - 1 : ((j - 1) % (sampled_groups * G));
+                    FDG_TRY(fdg_bm_release(p->bm, p->xstream, p->nodes[pj % p->nslots], &p->counts[pj].n_nodes,
+                                           p->cap));
+                    // batch j-1's node list is free only once it has been released
+                    FDG_CUDA(cudaEventRecord(p->extracted[(j - 1) % p->nslots], p->xstream));
+                }
+            }
+            if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j + 1], p->xstream));
+            if (records_host)  // device -> host read of the batch record (counts + checksum)
+                FDG_CUDA(cudaMemcpyAsync(records_host + j, cnt, sizeof(fdg_batch_counts), cudaMemcpyDeviceToHost,
+                                         p->xstream));
+            if (!p->bm) FDG_CUDA(cudaEventRecord(p->extracted[slot], p->xstream));
+        }
+    }
+    if (p->bm && !sample_only) {  // drain: release the last batch
+        const uint64_t lj = extract_only ? (n_batches - 1) % (sampled_groups * G) : n_batches - 1;
+        FDG_TRY(fdg_bm_release(p->bm, p->xstream, p->nodes[lj % p->nslots], &p->counts[lj].n_nodes, p->cap));
+        FDG_CUDA(cudaEventRecord(p->extracted[(n_batches - 1) % p->nslots], p->xstream));
+    }
+    for (uint32_t s = 0; s < S; ++s) {  // join the sampler streams
+        cudaEvent_t e;
+        FDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        FDG_CUDA(cudaEventRecord(e, p->sstream[s]));
+        FDG_CUDA(cudaStreamWaitEvent(p->xstream, e, 0));
+        cudaEventDestroy(e);
+    }
+    FDG_CUDA(cudaEventRecord(t1, p->xstream));
+    p->cfg.host_enqueue_ms =
+        std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    FDG_CUDA(cudaEventSynchronize(t1));
+    FDG_CUDA(cudaDeviceSynchronize());
+    float ms = 0;
+    FDG_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+    if (elapsed_ms) *elapsed_ms = ms;
+    if (extract_ms && !sample_only)
+        for (uint64_t j = 0; j < n_batches; ++j)
+            FDG_CUDA(cudaEventElapsedTime(extract_ms + j, p->tev[2 * j], p->tev[2 * j + 1]));
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    return FDG_OK;
+}
+
+int fdg_pipeline_get_config(const fdg_pipeline* p, fdg_pipeline_config* out) {
+    *out = p->cfg;
+    return FDG_OK;
+}
+
+int fdg_pipeline_records(fdg_pipeline* p, uint64_t first, uint64_t n, fdg_batch_counts* out) {
+    if (first + n > p->counts_cap) return fail(FDG_INVALID_ARG, "pipeline_records: range beyond last run");
+    FDG_CUDA(cudaMemcpy(out, p->counts + first, n * sizeof(fdg_batch_counts), cudaMemcpyDeviceToHost));
+    return FDG_OK;
+}
+
+}  // extern "C"

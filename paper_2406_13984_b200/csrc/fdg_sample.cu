@@ -3,32 +3,35 @@
 //
 // Reference semantics (sequential): one std::mt19937_64(splitmix64(rng_seed))
 // stream is consumed in (layer, frontier node, Floyd step) order, one
-// uniform_int_distribution<u64>(0, j) draw (libstdc++ Lemire, 1 word unless a
-// ~2^-57-probability rejection) per Floyd step; picks are interned into
-// `nodes` in first-occurrence order; frontier l+1 = fresh ids of layer l, which
-// is the contiguous slice nodes[layer_nodes[l+1], layer_nodes[l+2]).
+// uniform_int_distribution<u64>(0, j) draw (libstdc++ Lemire: 1 word unless a
+// ~2^-57-probability rejection) per Floyd step; picks are interned into `nodes`
+// in first-occurrence order; frontier l+1 = the fresh ids of layer l, which is
+// the contiguous slice nodes[layer_nodes[l+1], layer_nodes[l+2]).
 //
-// Parallel restatement per batch (all stream-ordered, sizes stay on device):
-//   k_seeds    : init the batch record; insert seeds into the batch hash
-//                (key -> min position, atomicMin), range-check seeds.
-//   k_intern   : one pass per pick list (seeds, then each layer): an entry is a
-//                first occurrence iff its pending min position equals the pick's
-//                position; a single-pass decoupled look-back scan of
+// Parallel restatement (stream-ordered, sizes stay on the device). Every kernel
+// takes a Group of up to kGMax batches (blockIdx.y = batch): latency chains and
+// kernel tails are paid once per group, not once per batch.
+//   k_seeds    : init the batch record, range-check seeds, insert them into the
+//                batch hash (key -> min pick position).
+//   k_intern_s : one pass per pick list (seeds, then each layer). A pick is the
+//                first occurrence iff its hash entry still holds its own pending
+//                position; a striped single-pass decoupled look-back scan of
 //                (first, min(deg,f), deg>f ? f : 0) assigns local ids in pick
-//                order, writes `nodes`, finalises the hash entry, and emits the
-//                next frontier's CSR start/degree and pick / MT-draw offsets.
-//   k_sample   : one thread per frontier node: Floyd's draws from the
-//                pre-generated MT stream at the node's prefix-summed offset
-//                (Lemire via __umul64hi), value-compare collisions, insert picks
-//                into the hash, write edge dst; also fixes edge src ids of the
-//                previous layer (fused with the next layer's launch).
-//   k_fix_src  : edge src ids of the last layer.
+//                order, writes `nodes` and every edge's src id, finalises the
+//                entry and emits the next frontier's CSR start/degree and pick /
+//                MT-draw offsets.
+//   k_expand   : fanouts <= 16: a half-warp per frontier node, one pick per lane:
+//                Floyd's draws from the pre-generated MT stream at the node's
+//                prefix-summed offset (Lemire via __umul64hi), the value-compare
+//                collision chain resolved by shuffles + ballots, hash insert, dst.
+//   k_sample + k_insert : the thread-per-node path for fanouts > 16 and for the
+//                exact mode.
 // A Lemire rejection would consume an extra word and shift every later offset;
-// it is detected, the batch is flagged FDG_REJECTION, and the host runs the
-// batch again in exact mode (offsets re-derived from per-node consumption).
+// it is detected, the batch is flagged FDG_REJECTION, and the host re-runs that
+// batch in exact mode (offsets re-derived from per-node consumption).
 #include <algorithm>
 #include <cstring>
-#include <unordered_map>
+#include <string>
 
 #include "fdg_internal.cuh"
 
@@ -39,11 +42,8 @@ constexpr uint32_t kPend = 0x80000000u;
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kTile = kScanThreads * kScanItems;
-constexpr int kMaxF = 16;  // register-resident Floyd; larger fanouts use the scratch path
-
-template <typename IdT> struct Empty;
-template <> struct Empty<uint32_t> { static constexpr uint32_t v = 0xFFFFFFFFu; };
-template <> struct Empty<uint64_t> { static constexpr uint64_t v = ~0ull; };
+constexpr int kMaxF = 16;  // half-warp / register-resident Floyd; larger fanouts use the global path
+constexpr int kGMax = 8;   // batches per group launch
 
 struct Tri {
     uint32_t c, p, d;
@@ -57,62 +57,109 @@ struct FrontierBuf {
     uint32_t* draw_off;  // exclusive scan of (deg > f ? f : 0) within the layer
 };
 
+__device__ __forceinline__ uint32_t hslot(uint64_t key, uint32_t mask) {
+    return uint32_t((key * 0x9E3779B97F4A7C15ull) >> 32) & mask;
+}
+
+// ---- batch hash: node id -> {pending min position | final local id} ----------------
+// u32 ids: one packed 64-bit word per entry (key << 32 | value), so a new key
+// costs one CAS and a lookup one load. u64 ids: separate key / value arrays.
+template <typename IdT> struct HashTab;
+
+template <> struct HashTab<uint32_t> {
+    unsigned long long* e;
+    uint32_t mask;
+    static constexpr unsigned long long kEmpty = ~0ull;
+    __device__ __forceinline__ uint32_t insert(uint32_t key, uint32_t pos) const {
+        const unsigned long long want = (uint64_t(key) << 32) | (kPend | pos);
+        uint32_t h = hslot(key, mask);
+        for (;;) {
+            // CAS straight away: one scattered L2 operation per new key
+            unsigned long long cur = atomicCAS(e + h, kEmpty, want);
+            if (cur == kEmpty) return h;
+            if (uint32_t(cur >> 32) == key) {
+                // lower the pending minimum; a final id (< kPend) is never replaced
+                while (uint32_t(cur) > uint32_t(want)) {
+                    unsigned long long prev = atomicCAS(e + h, cur, want);
+                    if (prev == cur) break;
+                    cur = prev;
+                }
+                return h;
+            }
+            h = (h + 1) & mask;
+        }
+    }
+    __device__ __forceinline__ void load(uint32_t h, uint32_t& key, uint32_t& val) const {
+        unsigned long long v = e[h];
+        key = uint32_t(v >> 32);
+        val = uint32_t(v);
+    }
+    __device__ __forceinline__ void finalize(uint32_t h, uint32_t key, uint32_t local) const {
+        e[h] = (uint64_t(key) << 32) | local;
+    }
+};
+
+template <> struct HashTab<uint64_t> {
+    unsigned long long* keys;
+    uint32_t* vals;
+    uint32_t mask;
+    static constexpr unsigned long long kEmpty = ~0ull;
+    __device__ __forceinline__ uint32_t insert(uint64_t key, uint32_t pos) const {
+        uint32_t h = hslot(key, mask);
+        for (;;) {
+            unsigned long long cur = atomicCAS(keys + h, kEmpty, (unsigned long long)key);
+            if (cur == kEmpty || cur == key) {
+                atomicMin(vals + h, kPend | pos);
+                return h;
+            }
+            h = (h + 1) & mask;
+        }
+    }
+    __device__ __forceinline__ void load(uint32_t h, uint64_t& key, uint32_t& val) const {
+        key = keys[h];
+        val = vals[h];
+    }
+    __device__ __forceinline__ void finalize(uint32_t h, uint64_t, uint32_t local) const { vals[h] = local; }
+};
+
+// Everything one batch needs (passed by value, kGMax per launch, in kernel params).
 template <typename IdT>
 struct Work {
     const uint64_t* indptr;
     const IdT* indices;
     uint64_t num_nodes;
-    IdT* keys;           // hash keys
-    uint32_t* vals;      // hash values: final local id, or kPend | min position
-    uint32_t hmask;
-    uint32_t* seed_slot; // [max_seeds]
-    uint32_t* pick_slot; // [max_edges], indexed by global edge position
-    IdT* scratch;        // [max_edges] picks for the large-fanout path
+    HashTab<IdT> tab;
+    const uint64_t* seeds;
+    uint32_t n_seeds;
+    uint32_t n_layers;
+    uint32_t* seed_slot;  // [max_seeds]
+    uint32_t* pick_slot;  // [max_edges], by global edge position
+    uint32_t* rank;       // [max_edges], tile-relative rank of first occurrences
+    IdT* picks;           // [max_edges], picked neighbor ids (thread-per-node path)
     FrontierBuf fr[2];
-    uint32_t* consumed;  // exact mode: words consumed per frontier node
-    uint32_t* tile_flag; // decoupled look-back state
+    uint32_t* consumed;   // exact mode: words consumed per frontier node
+    uint32_t* tile_flag;  // decoupled look-back state
     uint4* tile_agg;
     uint4* tile_incl;
-    uint32_t* tile_ctr;  // per-pass dynamic tile counters
+    uint32_t* tile_ctr;   // per-pass dynamic tile counters
     const uint64_t* words;
     uint64_t words_cap;
-    uint64_t* nodes;     // output
-    uint32_t* edges;     // output, {src, dst} pairs
+    uint64_t* nodes;      // output
+    uint32_t* edges;      // output, {src, dst} pairs
     fdg_batch_counts* cnt;
     uint32_t fan[FDG_MAX_LAYERS];
-    uint32_t n_layers;
 };
 
-__device__ __forceinline__ uint32_t hslot(uint64_t key, uint32_t mask) {
-    return uint32_t((key * 0x9E3779B97F4A7C15ull) >> 32) & mask;
-}
-
-__device__ __forceinline__ uint32_t atomic_cas_key(uint32_t* p, uint32_t cmp, uint32_t v) { return atomicCAS(p, cmp, v); }
-__device__ __forceinline__ uint64_t atomic_cas_key(uint64_t* p, uint64_t cmp, uint64_t v) {
-    return atomicCAS(reinterpret_cast<unsigned long long*>(p), (unsigned long long)cmp, (unsigned long long)v);
-}
-
-// Insert `key` (or find it) and lower its pending position to `pos`. Entries
-// finalised by an earlier pass hold a local id < kPend and are left unchanged.
 template <typename IdT>
-__device__ __forceinline__ uint32_t hash_insert(IdT* keys, uint32_t* vals, uint32_t mask, IdT key, uint32_t pos) {
-    uint32_t h = hslot(key, mask);
-    for (;;) {
-        IdT cur = keys[h];
-        if (cur == Empty<IdT>::v) cur = atomic_cas_key(keys + h, Empty<IdT>::v, key);
-        if (cur == Empty<IdT>::v || cur == key) {
-            atomicMin(vals + h, kPend | pos);
-            return h;
-        }
-        h = (h + 1) & mask;
-    }
-}
+struct Group {
+    Work<IdT> w[kGMax];
+};
 
-// libstdc++ uniform_int_distribution<u64>(0, j) on word stream w (uniform_int_dist.h:257-281).
+// libstdc++ uniform_int_distribution<u64>(0, j) on the word stream (uniform_int_dist.h:257-281).
 __device__ __forceinline__ uint64_t lemire(const uint64_t* words, uint64_t cap, uint64_t& pos, uint64_t j,
                                            uint32_t& extra, bool& overflow) {
     const uint64_t r = j + 1;
-    uint64_t w = pos < cap ? words[pos] : 0;
+    uint64_t w = pos < cap ? __ldg(words + pos) : 0;
     overflow |= pos >= cap;
     ++pos;
     uint64_t lo = w * r;
@@ -134,7 +181,8 @@ __device__ __forceinline__ uint64_t lemire(const uint64_t* words, uint64_t cap, 
 
 // ---------------------------------------------------------------- k_seeds ----
 template <typename IdT>
-__global__ void __launch_bounds__(1024) k_seeds(Work<IdT> W, const uint64_t* seeds, uint32_t n_seeds) {
+__global__ void __launch_bounds__(256) k_seeds(const __grid_constant__ Group<IdT> G) {
+    const Work<IdT>& W = G.w[blockIdx.y];
     fdg_batch_counts* cnt = W.cnt;
     if (threadIdx.x == 0) {
         cnt->status = 0;
@@ -157,17 +205,17 @@ __global__ void __launch_bounds__(1024) k_seeds(Work<IdT> W, const uint64_t* see
         }
     }
     __syncthreads();
-    for (uint32_t p = threadIdx.x; p < n_seeds; p += blockDim.x) {
-        uint64_t s = seeds[p];
+    for (uint32_t p = threadIdx.x; p < W.n_seeds; p += blockDim.x) {
+        uint64_t s = W.seeds[p];
         if (s >= W.num_nodes) {  // sampling.hpp:89-93
             atomicMin(&cnt->bad_seed_pos, p);
             cnt->status = FDG_OUT_OF_RANGE;
             continue;
         }
-        W.seed_slot[p] = hash_insert<IdT>(W.keys, W.vals, W.hmask, IdT(s), p);
+        W.seed_slot[p] = W.tab.insert(IdT(s), p);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && cnt->status == FDG_OUT_OF_RANGE) cnt->bad_seed = seeds[cnt->bad_seed_pos];
+    if (threadIdx.x == 0 && cnt->status == FDG_OUT_OF_RANGE) cnt->bad_seed = W.seeds[cnt->bad_seed_pos];
 }
 
 // ----------------------------------------------------------- block scan ----
@@ -195,17 +243,82 @@ __device__ __forceinline__ uint4 ld_volatile4(const uint4* p) {
     return v;
 }
 
-// ---------------------------------------------------------------- k_intern ----
-// Pass q interns pick list q (q = 0: seeds; q = l+1: picks of layer l) and sets
-// up the frontier of layer q (when q < n_layers).
+// Warp 0: exclusive prefix of this tile's aggregate via decoupled look-back.
+__device__ Tri tri_lookback(uint32_t* flags, uint4* aggs, uint4* incls, uint32_t tile, Tri agg, uint32_t epoch,
+                            int lane) {
+    const uint32_t E = (epoch & 0x3FFFFFFFu) << 2;
+    Tri excl{0, 0, 0};
+    if (tile == 0) {
+        if (lane == 0) {
+            incls[0] = make_uint4(agg.c, agg.p, agg.d, 0);
+            __threadfence();
+            atomicExch(flags, E | 2u);
+        }
+        return excl;
+    }
+    if (lane == 0) {
+        aggs[tile] = make_uint4(agg.c, agg.p, agg.d, 0);
+        __threadfence();
+        atomicExch(flags + tile, E | 1u);
+    }
+    int j = int(tile) - 1;
+    for (;;) {
+        int jj = j - lane;
+        uint32_t st = 2;
+        if (jj >= 0) {
+            uint32_t fl = ld_volatile(flags + jj);
+            st = (fl & ~3u) == E ? (fl & 3u) : 0u;
+        }
+        if (__any_sync(0xffffffffu, st == 0)) continue;
+        uint32_t im = __ballot_sync(0xffffffffu, st == 2);
+        int stop = im ? __ffs(im) - 1 : 32;  // nearest inclusive predecessor in this window
+        __threadfence();
+        Tri v{0, 0, 0};
+        if (lane < stop) {
+            uint4 a = ld_volatile4(aggs + jj);
+            v = Tri{a.x, a.y, a.z};
+        } else if (lane == stop && jj >= 0) {
+            uint4 a = ld_volatile4(incls + jj);
+            v = Tri{a.x, a.y, a.z};
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            v.c += __shfl_xor_sync(0xffffffffu, v.c, o);
+            v.p += __shfl_xor_sync(0xffffffffu, v.p, o);
+            v.d += __shfl_xor_sync(0xffffffffu, v.d, o);
+        }
+        excl = excl + v;
+        if (stop < 32) break;
+        j -= 32;
+    }
+    if (lane == 0) {
+        Tri tot = excl + agg;
+        incls[tile] = make_uint4(tot.c, tot.p, tot.d, 0);
+        __threadfence();
+        atomicExch(flags + tile, E | 2u);
+    }
+    return excl;
+}
+
+// ------------------------------------------------------------- k_intern_s ----
+// Pass q interns pick list q (q = 0: seeds; q = l+1: picks of layer l), writes the
+// layer's edge src ids and sets up the frontier of layer q (when q < n_layers).
+// Striped tiles: item k of thread t is position tile*kTile + k*256 + t, so every
+// per-item global access of a warp is coalesced (L1TEX wavefronts, not DRAM bytes,
+// bound the sampler); the scan runs as 8 row scans (one per k) -- one warp per
+// row for the cross-warp step -- then one decoupled look-back per tile.
 template <typename IdT, bool SEEDS, bool HAS_NEXT>
-__global__ void __launch_bounds__(kScanThreads) k_intern(Work<IdT> W, uint32_t q, uint32_t n_seeds, uint32_t epoch) {
-    __shared__ Tri s_warp[kScanThreads / 32];
-    __shared__ Tri s_excl;
+__global__ void __launch_bounds__(kScanThreads) k_intern_s(const __grid_constant__ Group<IdT> G, uint32_t q,
+                                                           uint32_t epoch) {
+    static_assert(kScanItems == kScanThreads / 32, "one warp per row scan");
+    const Work<IdT>& W = G.w[blockIdx.y];
+    __shared__ Tri s_row[kScanItems][kScanThreads / 32];  // per row: warp inclusive -> exclusive
+    __shared__ Tri s_rowx[kScanItems];                    // per row: exclusive offset within the tile
+    __shared__ Tri s_excl, s_agg;
     __shared__ uint32_t s_tile;
     fdg_batch_counts* cnt = W.cnt;
     if (cnt->status) return;
-    const uint32_t P = SEEDS ? n_seeds : cnt->layer_edges[q] - cnt->layer_edges[q - 1];
+    const uint32_t P = SEEDS ? W.n_seeds : cnt->layer_edges[q] - cnt->layer_edges[q - 1];
     const uint32_t ebase = SEEDS ? 0 : cnt->layer_edges[q - 1];
     const uint32_t node_base = cnt->layer_nodes[q];
     const uint32_t ntiles = P ? (P + kTile - 1) / kTile : 1;
@@ -215,95 +328,87 @@ __global__ void __launch_bounds__(kScanThreads) k_intern(Work<IdT> W, uint32_t q
     const uint32_t tile = s_tile;
     if (tile >= ntiles) return;
     const uint32_t f = HAS_NEXT ? W.fan[q] : 0;
-    const uint32_t p0 = tile * kTile + tid * kScanItems;
+    const uint32_t p0 = tile * kTile + tid;  // item k: p0 + k * kScanThreads
 
-    uint32_t slot[kScanItems];
-    uint32_t first_mask = 0;
-    uint32_t degs[kScanItems];
+    uint32_t slot[kScanItems], val[kScanItems];
     IdT key[kScanItems];
-    Tri mine{0, 0, 0};
+    uint32_t first_mask = 0, valid_mask = 0;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-        uint32_t p = p0 + k;
-        degs[k] = 0;
+        const uint32_t p = p0 + k * kScanThreads;
         if (p < P) {
+            valid_mask |= 1u << k;
             slot[k] = SEEDS ? W.seed_slot[p] : W.pick_slot[ebase + p];
-            if (W.vals[slot[k]] == (kPend | p)) {
-                first_mask |= 1u << k;
-                key[k] = W.keys[slot[k]];
-                mine.c += 1;
-                if (HAS_NEXT) {
-                    uint64_t v = uint64_t(key[k]);
-                    uint32_t d = uint32_t(W.indptr[v + 1] - W.indptr[v]);
-                    degs[k] = d;
-                    mine.p += d < f ? d : f;
-                    mine.d += d > f ? f : 0;
-                }
-            }
         }
     }
-    // block exclusive scan of `mine`
-    Tri incl = warp_incl_scan(mine, lane);
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        Tri w = lane < kScanThreads / 32 ? s_warp[lane] : Tri{0, 0, 0};
-        Tri wi = warp_incl_scan(w, lane);
-        if (lane < kScanThreads / 32) s_warp[lane] = Tri{wi.c - w.c, wi.p - w.p, wi.d - w.d};
-        Tri agg{__shfl_sync(0xffffffffu, wi.c, 31), __shfl_sync(0xffffffffu, wi.p, 31),
-                __shfl_sync(0xffffffffu, wi.d, 31)};
-        // decoupled look-back
-        const uint32_t E = (epoch & 0x3FFFFFFFu) << 2;
-        Tri excl{0, 0, 0};
-        if (tile == 0) {
-            if (lane == 0) {
-                W.tile_incl[0] = make_uint4(agg.c, agg.p, agg.d, 0);
-                __threadfence();
-                atomicExch(W.tile_flag + 0, E | 2u);
-            }
-        } else {
-            if (lane == 0) {
-                W.tile_agg[tile] = make_uint4(agg.c, agg.p, agg.d, 0);
-                __threadfence();
-                atomicExch(W.tile_flag + tile, E | 1u);
-            }
-            int j = int(tile) - 1;
-            for (;;) {
-                int jj = j - lane;
-                uint32_t st = 2;
-                if (jj >= 0) {
-                    uint32_t fl = ld_volatile(W.tile_flag + jj);
-                    st = (fl & ~3u) == E ? (fl & 3u) : 0u;
-                }
-                if (__any_sync(0xffffffffu, st == 0)) continue;
-                uint32_t im = __ballot_sync(0xffffffffu, st == 2);
-                int stop = im ? __ffs(im) - 1 : 32;  // nearest inclusive predecessor in this window
-                __threadfence();
-                Tri v{0, 0, 0};
-                if (lane < stop) {
-                    uint4 a = ld_volatile4(W.tile_agg + jj);
-                    v = Tri{a.x, a.y, a.z};
-                } else if (lane == stop && jj >= 0) {
-                    uint4 a = ld_volatile4(W.tile_incl + jj);
-                    v = Tri{a.x, a.y, a.z};
-                }
 #pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    v.c += __shfl_xor_sync(0xffffffffu, v.c, o);
-                    v.p += __shfl_xor_sync(0xffffffffu, v.p, o);
-                    v.d += __shfl_xor_sync(0xffffffffu, v.d, o);
-                }
-                excl = excl + v;
-                if (stop < 32) break;
-                j -= 32;
-            }
-            if (lane == 0) {
-                Tri tot = excl + agg;
-                W.tile_incl[tile] = make_uint4(tot.c, tot.p, tot.d, 0);
-                __threadfence();
-                atomicExch(W.tile_flag + tile, E | 2u);
-            }
+    for (int k = 0; k < kScanItems; ++k)
+        if (valid_mask & (1u << k)) {
+            W.tab.load(slot[k], key[k], val[k]);
+            if (val[k] == (kPend | (p0 + k * kScanThreads))) first_mask |= 1u << k;
         }
+    uint64_t lo[kScanItems], hi[kScanItems];
+    Tri v[kScanItems];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) v[k] = Tri{(first_mask >> k) & 1u, 0, 0};
+    if (HAS_NEXT) {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k)
+            if (first_mask & (1u << k)) {
+                lo[k] = W.indptr[uint64_t(key[k])];
+                hi[k] = W.indptr[uint64_t(key[k]) + 1];
+            }
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k)
+            if (first_mask & (1u << k)) {
+                uint32_t d = uint32_t(hi[k] - lo[k]);
+                v[k].p = d < f ? d : f;
+                v[k].d = d > f ? f : 0;
+            }
+    }
+    // row scans: warp-inclusive per row; warp r turns row r's warp totals into exclusive
+    // warp offsets; thread 0 turns the row totals into row offsets.
+    Tri inc[kScanItems];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        inc[k] = warp_incl_scan(v[k], lane);
+        if (lane == 31) s_row[k][warp] = inc[k];
+    }
+    __syncthreads();
+    {
+        const int r = warp;
+        Tri w = lane < kScanThreads / 32 ? s_row[r][lane] : Tri{0, 0, 0};
+        Tri wi = warp_incl_scan(w, lane);
+        if (lane < kScanThreads / 32) s_row[r][lane] = Tri{wi.c - w.c, wi.p - w.p, wi.d - w.d};
+        if (lane == 31) s_rowx[r] = wi;  // row total for now
+    }
+    __syncthreads();
+    if (tid == 0) {
+        Tri run{0, 0, 0};
+        for (int r = 0; r < kScanItems; ++r) {
+            Tri t = s_rowx[r];
+            s_rowx[r] = run;
+            run = run + t;
+        }
+        s_agg = run;
+    }
+    __syncthreads();
+    Tri ex[kScanItems];  // tile-relative exclusive prefix of item k
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+        ex[k] = s_rowx[k] + s_row[k][warp] + Tri{inc[k].c - v[k].c, inc[k].p - v[k].p, inc[k].d - v[k].d};
+    if (!SEEDS) {
+        // tile-relative rank of every first occurrence, published (fenced) before this
+        // tile's look-back flag so later tiles can resolve their repeated picks
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k)
+            if (first_mask & (1u << k)) W.rank[ebase + p0 + k * kScanThreads] = ex[k].c;
+        __threadfence();
+        __syncthreads();
+    }
+    if (warp == 0) {
+        const Tri agg = s_agg;
+        Tri excl = tri_lookback(W.tile_flag, W.tile_agg, W.tile_incl, tile, agg, epoch, lane);
         if (lane == 0) {
             s_excl = excl;
             if (tile == ntiles - 1) {  // totals of this pass -> the batch record
@@ -317,41 +422,61 @@ __global__ void __launch_bounds__(kScanThreads) k_intern(Work<IdT> W, uint32_t q
                     cnt->n_edges = cnt->layer_edges[q];
                     cnt->words_used = cnt->layer_draws[q];
                 }
-                if (SEEDS && !HAS_NEXT) cnt->n_edges = 0;
             }
         }
     }
     __syncthreads();
-    Tri run = s_excl + s_warp[warp] + Tri{incl.c - mine.c, incl.p - mine.p, incl.d - mine.d};
-    if (first_mask) {
-        const FrontierBuf fr = W.fr[q & 1];
+    const Tri base = s_excl;
+    const uint32_t E = (epoch & 0x3FFFFFFFu) << 2;
+    const FrontierBuf fr = W.fr[q & 1];
 #pragma unroll
-        for (int k = 0; k < kScanItems; ++k) {
-            if (first_mask & (1u << k)) {
-                const uint32_t local = node_base + run.c;
-                W.nodes[local] = uint64_t(key[k]);
-                W.vals[slot[k]] = local;
-                if (HAS_NEXT) {
-                    uint32_t d = degs[k];
-                    fr.start[run.c] = W.indptr[uint64_t(key[k])];
-                    fr.deg[run.c] = d;
-                    fr.pick_off[run.c] = run.p;
-                    fr.draw_off[run.c] = run.d;
-                    run.p += d < f ? d : f;
-                    run.d += d > f ? f : 0;
-                }
-                run.c += 1;
+    for (int k = 0; k < kScanItems; ++k) {
+        if (!(valid_mask & (1u << k))) continue;
+        const uint32_t p = p0 + k * kScanThreads;
+        if (first_mask & (1u << k)) {
+            const uint32_t r = base.c + ex[k].c;
+            const uint32_t local = node_base + r;
+            W.nodes[local] = uint64_t(key[k]);
+            W.tab.finalize(slot[k], key[k], local);
+            if (!SEEDS) W.edges[2 * (ebase + p)] = local;
+            if (HAS_NEXT) {
+                fr.start[r] = lo[k];
+                fr.deg[r] = uint32_t(hi[k] - lo[k]);
+                fr.pick_off[r] = base.p + ex[k].p;
+                fr.draw_off[r] = base.d + ex[k].d;
             }
+        } else if (!SEEDS) {
+            // src id of a repeated pick (LocalEdge.src, sampling.hpp:124): a final id is used
+            // as is; a pending entry names its first occurrence, whose tile has published its
+            // rank and (once inclusive) its exclusive prefix.
+            uint32_t src = val[k];
+            if (src & kPend) {
+                const uint32_t pf = src & ~kPend;
+                const uint32_t tf = pf / kTile;
+                uint32_t bc;
+                if (tf == tile) {
+                    bc = base.c;
+                } else {
+                    while (ld_volatile(W.tile_flag + tf) != (E | 2u)) {
+                    }
+                    __threadfence();
+                    const uint4 in = ld_volatile4(W.tile_incl + tf);
+                    bc = tf == 0 ? 0u : in.x - ld_volatile4(W.tile_agg + tf).x;
+                }
+                src = node_base + bc + ld_volatile(W.rank + ebase + pf);
+            }
+            W.edges[2 * (ebase + p)] = src;
         }
     }
 }
 
 // ---------------------------------------------------------------- k_sample ----
-// MODE 0: sample + insert (fast path). MODE 1: exact-mode probe (count words
-// consumed per node, no inserts). MODE 2: exact-mode final (inserts, offsets
-// from W.consumed-derived draw_off).
+// Thread per frontier node (fanouts > 16 and exact mode). MODE 0: sample.
+// MODE 1: exact-mode probe (count words consumed per node, no outputs). MODE 2:
+// exact-mode final (offsets re-derived). Writes picks + edge dst; k_insert hashes.
 template <typename IdT, bool SMALLF, int MODE>
-__global__ void __launch_bounds__(256) k_sample(Work<IdT> W, uint32_t l) {
+__global__ void __launch_bounds__(256) k_sample(const __grid_constant__ Group<IdT> G, uint32_t l) {
+    const Work<IdT>& W = G.w[blockIdx.y];
     fdg_batch_counts* cnt = W.cnt;
     if (cnt->status) return;
     const uint32_t fs = cnt->layer_nodes[l];
@@ -359,31 +484,19 @@ __global__ void __launch_bounds__(256) k_sample(Work<IdT> W, uint32_t l) {
     const uint32_t eb = cnt->layer_edges[l];
     const uint64_t db = cnt->layer_draws[l];
     const uint32_t f = W.fan[l];
-    // edge src fix-up of the previous layer (its ids are final now)
-    const uint32_t fix_lo = l > 0 ? cnt->layer_edges[l - 1] : 0;
-    const uint32_t fix_hi = l > 0 ? eb : 0;
     const FrontierBuf fr = W.fr[l & 1];
-    const uint32_t stride = gridDim.x * blockDim.x;
-    const uint32_t span = max(F, fix_hi - fix_lo);
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < span; i += stride) {
-        if (MODE != 1 && i < fix_hi - fix_lo) {
-            uint32_t e = fix_lo + i;
-            W.edges[2 * e] = W.vals[W.pick_slot[e]];
-        }
-        if (i >= F) continue;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < F; i += gridDim.x * blockDim.x) {
         const uint64_t start = fr.start[i];
         const uint32_t deg = fr.deg[i];
-        const uint32_t po = fr.pick_off[i];
+        const uint32_t e0 = eb + fr.pick_off[i];
         const uint32_t dst = fs + i;
-        const uint32_t e0 = eb + po;
         if (deg <= f) {  // take all, in list order (sampling.hpp:107-108)
             if (MODE == 1) {
                 W.consumed[i] = 0;
                 continue;
             }
             for (uint32_t k = 0; k < deg; ++k) {
-                IdT v = W.indices[start + k];
-                W.pick_slot[e0 + k] = hash_insert<IdT>(W.keys, W.vals, W.hmask, v, po + k);
+                W.picks[e0 + k] = W.indices[start + k];
                 W.edges[2 * (e0 + k) + 1] = dst;
             }
             continue;
@@ -422,11 +535,11 @@ __global__ void __launch_bounds__(256) k_sample(Work<IdT> W, uint32_t l) {
 #pragma unroll
             for (int k = 0; k < kMaxF; ++k)
                 if (k < int(f)) {
-                    W.pick_slot[e0 + k] = hash_insert<IdT>(W.keys, W.vals, W.hmask, picked[k], po + k);
+                    W.picks[e0 + k] = picked[k];
                     W.edges[2 * (e0 + k) + 1] = dst;
                 }
         } else {
-            IdT* picked = W.scratch + e0;
+            IdT* picked = W.picks + e0;
             for (uint32_t k = 0; k < f; ++k) {
                 uint64_t tk = lemire(W.words, W.words_cap, pos, jlo + k, extra, overflow);
                 if (MODE == 1) continue;
@@ -437,14 +550,11 @@ __global__ void __launch_bounds__(256) k_sample(Work<IdT> W, uint32_t l) {
                         break;
                     }
                 picked[k] = c;
+                W.edges[2 * (e0 + k) + 1] = dst;
             }
             if (MODE == 1) {
                 W.consumed[i] = f + extra;
                 continue;
-            }
-            for (uint32_t k = 0; k < f; ++k) {
-                W.pick_slot[e0 + k] = hash_insert<IdT>(W.keys, W.vals, W.hmask, picked[k], po + k);
-                W.edges[2 * (e0 + k) + 1] = dst;
             }
         }
         if (overflow) atomicExch(&cnt->status, uint32_t(FDG_CAPACITY));
@@ -455,13 +565,85 @@ __global__ void __launch_bounds__(256) k_sample(Work<IdT> W, uint32_t l) {
     }
 }
 
+// ---------------------------------------------------------------- k_insert ----
+// Thread per pick of layer l (position = pick index within the layer).
 template <typename IdT>
-__global__ void k_fix_src(Work<IdT> W, uint32_t l) {
+__global__ void __launch_bounds__(256) k_insert(const __grid_constant__ Group<IdT> G, uint32_t l) {
+    const Work<IdT>& W = G.w[blockIdx.y];
     fdg_batch_counts* cnt = W.cnt;
     if (cnt->status) return;
-    const uint32_t lo = cnt->layer_edges[l], hi = cnt->layer_edges[l + 1];
-    for (uint32_t e = lo + blockIdx.x * blockDim.x + threadIdx.x; e < hi; e += gridDim.x * blockDim.x)
-        W.edges[2 * e] = W.vals[W.pick_slot[e]];
+    const uint32_t eb = cnt->layer_edges[l];
+    const uint32_t P = cnt->layer_edges[l + 1] - eb;
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x)
+        W.pick_slot[eb + p] = W.tab.insert(W.picks[eb + p], p);
+}
+
+// ---------------------------------------------------------------- k_expand ----
+// Fast path for fanouts <= 16: a half-warp per frontier node, one pick per lane.
+// Lane k draws t_k from MT word db + draw_off + k (a Lemire rejection -- p ~ 2^-57
+// per draw -- flags the batch for exact mode), loads cand_k = nb[t_k] and
+// alt_k = nb[j_k]; Floyd's value-compare collision chain is resolved in k order
+// with one shuffle + ballot per step; then every lane inserts its pick into the
+// batch hash and writes its edge's dst (sampling.hpp:104-126).
+template <typename IdT>
+__global__ void __launch_bounds__(256) k_expand(const __grid_constant__ Group<IdT> G, uint32_t l) {
+    const Work<IdT>& W = G.w[blockIdx.y];
+    fdg_batch_counts* cnt = W.cnt;
+    if (cnt->status) return;
+    const uint32_t fs = cnt->layer_nodes[l];
+    const uint32_t F = cnt->layer_nodes[l + 1] - fs;
+    const uint32_t eb = cnt->layer_edges[l];
+    const uint64_t db = cnt->layer_draws[l];
+    const uint32_t f = W.fan[l];
+    const FrontierBuf fr = W.fr[l & 1];
+    const int lane = threadIdx.x & 31, h = lane >> 4, k = lane & 15;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    bool rejected = false;
+    for (uint32_t pair = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; pair * 2 < F; pair += nwarps) {
+        const uint32_t i = pair * 2 + h;
+        const bool live = i < F;
+        uint64_t start = 0;
+        uint32_t deg = 0, po = 0, dro = 0;
+        if (live) {
+            start = fr.start[i];
+            deg = fr.deg[i];
+            po = fr.pick_off[i];
+            dro = fr.draw_off[i];
+        }
+        const bool floyd = deg > f;
+        const uint32_t npick = floyd ? f : deg;
+        IdT picked = 0, alt = 0;
+        if (live && uint32_t(k) < npick) {
+            if (floyd) {
+                const uint64_t j = uint64_t(deg - f) + k;
+                const uint64_t r = j + 1;
+                const uint64_t w = __ldg(W.words + db + dro + k);
+                const uint64_t lo = w * r;
+                if (lo < r && lo < (0 - r) % r) rejected = true;
+                picked = W.indices[start + __umul64hi(w, r)];
+                alt = W.indices[start + j];
+            } else {
+                picked = W.indices[start + k];
+            }
+        }
+        // Floyd collision chain: step s finalises lane s of each half-warp
+        if (__any_sync(0xffffffffu, live && floyd)) {
+            for (uint32_t s = 1; s < f; ++s) {
+                const IdT c = __shfl_sync(0xffffffffu, picked, int(s), 16);
+                const uint32_t hits = __ballot_sync(0xffffffffu, uint32_t(k) < s && picked == c);
+                if (uint32_t(k) == s && floyd && ((hits >> (h * 16)) & 0xFFFFu)) picked = alt;
+            }
+        }
+        if (live && uint32_t(k) < npick) {
+            const uint32_t e = eb + po + k;
+            W.pick_slot[e] = W.tab.insert(picked, po + k);
+            W.edges[2 * e + 1] = fs + i;
+        }
+    }
+    if (rejected) {
+        atomicAdd(&cnt->rejections, 1u);
+        atomicCAS(&cnt->status, 0u, uint32_t(FDG_REJECTION));
+    }
 }
 
 // exact mode helper: draw_off = exclusive scan(consumed) over the frontier (single block)
@@ -507,35 +689,43 @@ __global__ void k_rescan_draws(uint32_t* consumed, uint32_t* draw_off, const fdg
 
 }  // namespace
 
+int64_t g_l2_persist_mb = 0;
+int64_t g_hash_load_pct = 50;
+
 // ------------------------------------------------------------------ Sampler ----
-struct Sampler {
-    Ctx* ctx = nullptr;
-    uint32_t max_seeds = 0;
-    uint32_t n_layers = 0;
-    uint32_t fan[FDG_MAX_LAYERS] = {};
-    uint64_t max_nodes = 0, max_edges = 0, max_draws = 0;
-    uint64_t F_bound[FDG_MAX_LAYERS + 1] = {}, P_bound[FDG_MAX_LAYERS + 1] = {};
-    uint32_t hsize = 0;
-    bool small_f = true;
-    void* arena = nullptr;
-    // carved pointers
-    void* keys = nullptr;
-    uint32_t* vals = nullptr;
+struct Lane {  // per-batch workspace of one group slot
+    void* hash = nullptr;  // packed entries (u32 ids) or keys then vals (u64 ids)
     uint32_t* seed_slot = nullptr;
     uint32_t* pick_slot = nullptr;
-    void* scratch = nullptr;
+    uint32_t* rank = nullptr;
+    void* picks = nullptr;
     FrontierBuf fr[2];
     uint32_t* consumed = nullptr;
     uint32_t* tile_flag = nullptr;
     uint4* tile_agg = nullptr;
     uint4* tile_incl = nullptr;
     uint32_t* tile_ctr = nullptr;
-    uint32_t* exact_flags = nullptr;  // [changed, total]
-    uint64_t* words = nullptr;         // inline MT stream
-    uint64_t words_cap = 0;
-    uint64_t* seeds_buf = nullptr;     // host-API staging
-    uint64_t hash_bytes = 0;
     uint32_t epoch = 1;
+};
+
+struct Sampler {
+    Ctx* ctx = nullptr;
+    uint32_t max_seeds = 0;
+    uint32_t n_layers = 0;
+    uint32_t gmax = 1;
+    uint32_t fan[FDG_MAX_LAYERS] = {};
+    uint64_t max_nodes = 0, max_edges = 0, max_draws = 0;
+    uint64_t F_bound[FDG_MAX_LAYERS + 1] = {}, P_bound[FDG_MAX_LAYERS + 1] = {};
+    uint32_t hsize = 0;
+    bool small_f = true;
+    void* arena = nullptr;
+    void* hash_all = nullptr;  // the lanes' hash tables, contiguous (one memset per group)
+    std::vector<Lane> lanes;
+    uint64_t hash_bytes = 0;   // per lane
+    uint32_t* exact_flags = nullptr;  // [changed, total]
+    uint64_t* words = nullptr;        // inline MT stream
+    uint64_t words_cap = 0;
+    uint64_t* seeds_buf = nullptr;    // host-API staging
     // prefetch ring
     uint32_t ring_n = 0;
     uint64_t* ring_words = nullptr;
@@ -554,6 +744,17 @@ struct Sampler {
 struct fdg_sampler : fdg::Sampler {};
 
 namespace fdg {
+
+struct BatchArgs {  // one batch of a group launch
+    const uint64_t* seeds;
+    uint32_t n_seeds;
+    const uint64_t* words;
+    uint64_t words_cap;
+    uint64_t* nodes;
+    uint32_t* edges;
+    fdg_batch_counts* cnt;
+};
+
 namespace {
 
 uint64_t next_pow2(uint64_t v) {
@@ -563,143 +764,191 @@ uint64_t next_pow2(uint64_t v) {
 }
 
 template <typename IdT>
-Work<IdT> make_work(Sampler& s, const uint64_t* words, uint64_t words_cap, uint64_t* nodes, uint32_t* edges,
-                    fdg_batch_counts* cnt) {
+Work<IdT> make_work(Sampler& s, const Lane& ln, const BatchArgs& a) {
     Work<IdT> w;
     w.indptr = s.ctx->indptr;
     w.indices = static_cast<const IdT*>(s.ctx->indices);
     w.num_nodes = s.ctx->num_nodes;
-    w.keys = static_cast<IdT*>(s.keys);
-    w.vals = s.vals;
-    w.hmask = s.hsize - 1;
-    w.seed_slot = s.seed_slot;
-    w.pick_slot = s.pick_slot;
-    w.scratch = static_cast<IdT*>(s.scratch);
-    w.fr[0] = s.fr[0];
-    w.fr[1] = s.fr[1];
-    w.consumed = s.consumed;
-    w.tile_flag = s.tile_flag;
-    w.tile_agg = s.tile_agg;
-    w.tile_incl = s.tile_incl;
-    w.tile_ctr = s.tile_ctr;
-    w.words = words;
-    w.words_cap = words_cap;
-    w.nodes = nodes;
-    w.edges = edges;
-    w.cnt = cnt;
-    for (uint32_t l = 0; l < FDG_MAX_LAYERS; ++l) w.fan[l] = l < s.n_layers ? s.fan[l] : 0;
+    if constexpr (sizeof(IdT) == 4) {
+        w.tab.e = static_cast<unsigned long long*>(ln.hash);
+    } else {
+        w.tab.keys = static_cast<unsigned long long*>(ln.hash);
+        w.tab.vals = reinterpret_cast<uint32_t*>(static_cast<char*>(ln.hash) + uint64_t(s.hsize) * 8);
+    }
+    w.tab.mask = s.hsize - 1;
+    w.seeds = a.seeds;
+    w.n_seeds = a.n_seeds;
     w.n_layers = s.n_layers;
+    w.seed_slot = ln.seed_slot;
+    w.pick_slot = ln.pick_slot;
+    w.rank = ln.rank;
+    w.picks = static_cast<IdT*>(ln.picks);
+    w.fr[0] = ln.fr[0];
+    w.fr[1] = ln.fr[1];
+    w.consumed = ln.consumed;
+    w.tile_flag = ln.tile_flag;
+    w.tile_agg = ln.tile_agg;
+    w.tile_incl = ln.tile_incl;
+    w.tile_ctr = ln.tile_ctr;
+    w.words = a.words;
+    w.words_cap = a.words_cap;
+    w.nodes = a.nodes;
+    w.edges = a.edges;
+    w.cnt = a.cnt;
+    for (uint32_t l = 0; l < FDG_MAX_LAYERS; ++l) w.fan[l] = l < s.n_layers ? s.fan[l] : 0;
     return w;
 }
 
 uint32_t grid_for(uint64_t items, int threads, int max_blocks) {
     uint64_t b = (items + threads - 1) / threads;
-    return uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(b, uint64_t(max_blocks))));
+    return uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(b, uint64_t(std::max(max_blocks, 1)))));
 }
 
+// All lanes of a group share one look-back epoch per pass (their flag arrays differ).
 template <typename IdT>
-void launch_intern(Sampler& s, cudaStream_t st, const Work<IdT>& W, uint32_t q, uint32_t n_seeds) {
+void launch_intern(Sampler& s, cudaStream_t st, const Group<IdT>& G, uint32_t n, uint32_t q, uint32_t max_seeds,
+                   uint32_t epoch) {
     const bool seeds = q == 0;
     const bool has_next = q < s.n_layers;
-    const uint64_t P = seeds ? n_seeds : s.P_bound[q - 1];
-    const uint32_t tiles = uint32_t(std::max<uint64_t>(1, (P + kTile - 1) / kTile));
-    const uint32_t ep = s.epoch++;
+    const uint64_t P = seeds ? max_seeds : s.P_bound[q - 1];
+    const dim3 grid(uint32_t(std::max<uint64_t>(1, (P + kTile - 1) / kTile)), n);
     if (seeds) {
-        if (has_next) k_intern<IdT, true, true><<<tiles, kScanThreads, 0, st>>>(W, q, n_seeds, ep);
-        else k_intern<IdT, true, false><<<tiles, kScanThreads, 0, st>>>(W, q, n_seeds, ep);
+        if (has_next) k_intern_s<IdT, true, true><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
+        else k_intern_s<IdT, true, false><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
     } else {
-        if (has_next) k_intern<IdT, false, true><<<tiles, kScanThreads, 0, st>>>(W, q, n_seeds, ep);
-        else k_intern<IdT, false, false><<<tiles, kScanThreads, 0, st>>>(W, q, n_seeds, ep);
+        if (has_next) k_intern_s<IdT, false, true><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
+        else k_intern_s<IdT, false, false><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
     }
 }
 
 template <typename IdT, int MODE>
-void launch_sample(Sampler& s, cudaStream_t st, const Work<IdT>& W, uint32_t l) {
-    uint64_t span = std::max<uint64_t>(s.F_bound[l], l > 0 ? s.P_bound[l - 1] : 0);
-    uint32_t blocks = grid_for(span, 256, s.ctx->sm_count * 8);
-    if (s.small_f) k_sample<IdT, true, MODE><<<blocks, 256, 0, st>>>(W, l);
-    else k_sample<IdT, false, MODE><<<blocks, 256, 0, st>>>(W, l);
+void launch_sample(Sampler& s, cudaStream_t st, const Group<IdT>& G, uint32_t n, uint32_t l) {
+    const dim3 grid(grid_for(s.F_bound[l], 256, s.ctx->sm_count * 16 / int(n)), n);
+    if (s.small_f) k_sample<IdT, true, MODE><<<grid, 256, 0, st>>>(G, l);
+    else k_sample<IdT, false, MODE><<<grid, 256, 0, st>>>(G, l);
 }
 
-// Fast path: everything stream-ordered, no host synchronisation.
 template <typename IdT>
-int run_batch(Sampler& s, cudaStream_t st, const uint64_t* seeds, uint32_t n_seeds, const uint64_t* words,
-              uint64_t words_cap, uint64_t* nodes, uint32_t* edges, fdg_batch_counts* cnt) {
-    Work<IdT> W = make_work<IdT>(s, words, words_cap, nodes, edges, cnt);
-    FDG_CUDA(cudaMemsetAsync(s.keys, 0xFF, s.hash_bytes, st));
-    k_seeds<IdT><<<1, 1024, 0, st>>>(W, seeds, n_seeds);
-    launch_intern<IdT>(s, st, W, 0, n_seeds);
-    for (uint32_t l = 0; l < s.n_layers; ++l) {
-        launch_sample<IdT, 0>(s, st, W, l);
-        launch_intern<IdT>(s, st, W, l + 1, n_seeds);
+void launch_insert(Sampler& s, cudaStream_t st, const Group<IdT>& G, uint32_t n, uint32_t l) {
+    const dim3 grid(grid_for(s.P_bound[l], 256, s.ctx->sm_count * 16 / int(n)), n);
+    k_insert<IdT><<<grid, 256, 0, st>>>(G, l);
+}
+
+uint32_t next_epoch(Sampler& s, uint32_t n) {
+    uint32_t e = 0;
+    for (uint32_t i = 0; i < n; ++i) e = std::max(e, s.lanes[i].epoch);
+    for (uint32_t i = 0; i < n; ++i) s.lanes[i].epoch = e + 1;
+    return e;
+}
+
+// Fast path: a group of n batches, stream-ordered, no host synchronisation.
+template <typename IdT>
+int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
+    Group<IdT> G;
+    uint32_t max_seeds = 1;
+    for (uint32_t i = 0; i < n; ++i) {
+        G.w[i] = make_work<IdT>(s, s.lanes[i], a[i]);
+        max_seeds = std::max(max_seeds, a[i].n_seeds);
     }
-    uint32_t lastl = s.n_layers - 1;
-    k_fix_src<IdT><<<grid_for(s.P_bound[lastl], 256, s.ctx->sm_count * 8), 256, 0, st>>>(W, lastl);
+    {
+        FDG_TRACE("memset", st);
+        FDG_CUDA(cudaMemsetAsync(s.hash_all, 0xFF, s.hash_bytes * n, st));
+    }
+    {
+        FDG_TRACE("seeds", st);
+        k_seeds<IdT><<<dim3(1, n), 256, 0, st>>>(G);
+    }
+    {
+        FDG_TRACE("intern0", st);
+        launch_intern<IdT>(s, st, G, n, 0, max_seeds, next_epoch(s, n));
+    }
+    static const char* names[2][FDG_MAX_LAYERS] = {
+        {"expand0", "expand1", "expand2", "expand3", "expand4", "expand5", "expand6", "expand7"},
+        {"intern1", "intern2", "intern3", "intern4", "intern5", "intern6", "intern7", "intern8"}};
+    for (uint32_t l = 0; l < s.n_layers; ++l) {
+        {
+            FDG_TRACE(names[0][l], st);
+            if (s.small_f) {
+                const dim3 grid(grid_for(s.F_bound[l] * 16, 256, s.ctx->sm_count * 16 / int(n)), n);
+                k_expand<IdT><<<grid, 256, 0, st>>>(G, l);
+            } else {
+                launch_sample<IdT, 0>(s, st, G, n, l);
+                launch_insert<IdT>(s, st, G, n, l);
+            }
+        }
+        {
+            FDG_TRACE(names[1][l], st);
+            launch_intern<IdT>(s, st, G, n, l + 1, max_seeds, next_epoch(s, n));  // also writes edge src ids
+        }
+    }
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;
 }
 
-// Exact mode (after a Lemire rejection): per layer, iterate probe -> rescan of
-// the per-node word consumption until the draw offsets are self-consistent,
-// then run the inserting pass. Host-synchronising; never taken in practice.
+// Exact mode (after a Lemire rejection), one batch in lane 0: per layer, iterate
+// probe -> rescan of the per-node word consumption until the draw offsets are
+// self-consistent, then run the sampling pass. Host-synchronising; never taken
+// in practice.
 template <typename IdT>
-int run_batch_exact(Sampler& s, cudaStream_t st, const uint64_t* seeds, uint32_t n_seeds, const uint64_t* words,
-                    uint64_t words_cap, uint64_t* nodes, uint32_t* edges, fdg_batch_counts* cnt) {
-    Work<IdT> W = make_work<IdT>(s, words, words_cap, nodes, edges, cnt);
-    FDG_CUDA(cudaMemsetAsync(s.keys, 0xFF, s.hash_bytes, st));
-    k_seeds<IdT><<<1, 1024, 0, st>>>(W, seeds, n_seeds);
-    launch_intern<IdT>(s, st, W, 0, n_seeds);
+int run_batch_exact(Sampler& s, cudaStream_t st, const BatchArgs& a) {
+    Group<IdT> G;
+    G.w[0] = make_work<IdT>(s, s.lanes[0], a);
+    fdg_batch_counts* cnt = a.cnt;
+    FDG_CUDA(cudaMemsetAsync(s.lanes[0].hash, 0xFF, s.hash_bytes, st));
+    k_seeds<IdT><<<dim3(1, 1), 256, 0, st>>>(G);
+    launch_intern<IdT>(s, st, G, 1, 0, a.n_seeds, next_epoch(s, 1));
     for (uint32_t l = 0; l < s.n_layers; ++l) {
         for (int it = 0;; ++it) {
-            launch_sample<IdT, 1>(s, st, W, l);
+            launch_sample<IdT, 1>(s, st, G, 1, l);
             FDG_CUDA(cudaMemsetAsync(s.exact_flags, 0, 8, st));
-            k_rescan_draws<<<1, 1024, 0, st>>>(s.consumed, s.fr[l & 1].draw_off, cnt, l, s.exact_flags,
-                                               s.exact_flags + 1);
+            k_rescan_draws<<<1, 1024, 0, st>>>(s.lanes[0].consumed, s.lanes[0].fr[l & 1].draw_off, cnt, l,
+                                               s.exact_flags, s.exact_flags + 1);
             uint32_t h[2];
             FDG_CUDA(cudaMemcpyAsync(h, s.exact_flags, 8, cudaMemcpyDeviceToHost, st));
             FDG_CUDA(cudaStreamSynchronize(st));
             if (!h[0]) {
-                // fix the next layer's draw base: layer_draws[l+1] = layer_draws[l] + total
+                // layer_draws[l+1] = layer_draws[l] + words actually consumed by layer l
                 uint32_t base = 0;
                 FDG_CUDA(cudaMemcpy(&base, &cnt->layer_draws[l], 4, cudaMemcpyDeviceToHost));
                 uint32_t nb = base + h[1];
                 FDG_CUDA(cudaMemcpy(&cnt->layer_draws[l + 1], &nb, 4, cudaMemcpyHostToDevice));
                 break;
             }
-            if (it > 1 << 20) return fail(FDG_INVARIANT, "exact mode did not converge");
+            if (it > (1 << 20)) return fail(FDG_INVARIANT, "exact mode did not converge");
         }
-        launch_sample<IdT, 2>(s, st, W, l);
-        launch_intern<IdT>(s, st, W, l + 1, n_seeds);  // bases layer_draws[l+2] on the corrected [l+1]
+        launch_sample<IdT, 2>(s, st, G, 1, l);
+        launch_insert<IdT>(s, st, G, 1, l);
+        launch_intern<IdT>(s, st, G, 1, l + 1, a.n_seeds, next_epoch(s, 1));  // bases layer_draws[l+2] on [l+1]
     }
-    uint32_t lastl = s.n_layers - 1;
-    k_fix_src<IdT><<<grid_for(s.P_bound[lastl], 256, s.ctx->sm_count * 8), 256, 0, st>>>(W, lastl);
     FDG_CUDA(cudaGetLastError());
     FDG_CUDA(cudaStreamSynchronize(st));
     return FDG_OK;
 }
 
-int dispatch_batch(Sampler& s, cudaStream_t st, const uint64_t* seeds, uint32_t n_seeds, const uint64_t* words,
-                   uint64_t words_cap, uint64_t* nodes, uint32_t* edges, fdg_batch_counts* cnt, bool exact) {
-    if (s.ctx->idx_bytes == 4)
-        return exact ? run_batch_exact<uint32_t>(s, st, seeds, n_seeds, words, words_cap, nodes, edges, cnt)
-                     : run_batch<uint32_t>(s, st, seeds, n_seeds, words, words_cap, nodes, edges, cnt);
-    return exact ? run_batch_exact<uint64_t>(s, st, seeds, n_seeds, words, words_cap, nodes, edges, cnt)
-                 : run_batch<uint64_t>(s, st, seeds, n_seeds, words, words_cap, nodes, edges, cnt);
+int dispatch_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
+    return s.ctx->idx_bytes == 4 ? run_group<uint32_t>(s, st, n, a) : run_group<uint64_t>(s, st, n, a);
+}
+
+int dispatch_exact(Sampler& s, cudaStream_t st, const BatchArgs& a) {
+    return s.ctx->idx_bytes == 4 ? run_batch_exact<uint32_t>(s, st, a) : run_batch_exact<uint64_t>(s, st, a);
 }
 
 }  // namespace
 
-int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32_t n_layers, Sampler** out) {
+int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32_t n_layers, Sampler** out,
+                   uint32_t group) {
     if (!ctx->indptr) return fail(FDG_NOT_LOADED, "sampler: no topology loaded");
     if (n_layers == 0) return fail(FDG_INVALID_ARG, "fanouts: need at least one layer");
     if (n_layers > FDG_MAX_LAYERS) return fail(FDG_INVALID_ARG, "fanouts: more than FDG_MAX_LAYERS layers");
     for (uint32_t l = 0; l < n_layers; ++l)
         if (fanouts[l] < 1) return fail(FDG_INVALID_ARG, "fanouts: every entry must be >= 1");
     if (max_seeds == 0) max_seeds = 1;
+    group = std::max<uint32_t>(1, std::min<uint32_t>(group, kGMax));
     auto s = new Sampler();
     s->ctx = ctx;
     s->max_seeds = max_seeds;
     s->n_layers = n_layers;
+    s->gmax = group;
     const uint64_t N = ctx->num_nodes;
     uint64_t F = std::min<uint64_t>(max_seeds, N), nodes = F, edges = 0;
     uint32_t fmax = 0;
@@ -720,26 +969,31 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
         return fail(FDG_INVALID_ARG, "sampler: batch bound exceeds 2^31 picks");
     }
     s->small_f = fmax <= uint32_t(kMaxF);
-    s->hsize = uint32_t(next_pow2(std::max<uint64_t>(2 * s->max_nodes, 1024)));
+    s->hsize = uint32_t(next_pow2(std::max<uint64_t>(s->max_nodes * 100 / uint64_t(g_hash_load_pct), 1024)));
     const uint32_t ib = ctx->idx_bytes;
-    s->hash_bytes = uint64_t(s->hsize) * (ib + 4);
+    auto al = [](uint64_t b) { return (b + 255) & ~uint64_t(255); };
+    s->hash_bytes = al(uint64_t(s->hsize) * (ib == 4 ? 8 : 12));
     uint64_t fmaxF = 1;
     for (uint32_t l = 0; l < n_layers; ++l) fmaxF = std::max(fmaxF, s->F_bound[l]);
     const uint64_t tiles = (std::max<uint64_t>(s->max_edges, max_seeds) + kTile - 1) / kTile + 1;
     s->words_cap = s->max_draws + 4096;
-    auto al = [](uint64_t b) { return (b + 255) & ~uint64_t(255); };
-    uint64_t sz = 0;
-    const uint64_t o_keys = sz; sz += al(s->hash_bytes);  // keys then vals: one memset
-    const uint64_t o_seed = sz; sz += al(uint64_t(max_seeds) * 4);
-    const uint64_t o_pick = sz; sz += al(std::max<uint64_t>(s->max_edges, 1) * 4);
-    const uint64_t o_scr = sz; sz += s->small_f ? 0 : al(std::max<uint64_t>(s->max_edges, 1) * ib);
+    // per-lane layout
+    uint64_t lz = 0;
+    const uint64_t o_seed = lz; lz += al(uint64_t(max_seeds) * 4);
+    const uint64_t o_pick = lz; lz += al(std::max<uint64_t>(s->max_edges, 1) * 4);
+    const uint64_t o_rank = lz; lz += al(std::max<uint64_t>(s->max_edges, 1) * 4);
+    const uint64_t o_picks = lz; lz += s->small_f ? 0 : al(std::max<uint64_t>(s->max_edges, 1) * ib);
     uint64_t o_fr[2];
-    for (int b = 0; b < 2; ++b) { o_fr[b] = sz; sz += al(fmaxF * 8) + 3 * al(fmaxF * 4); }
-    const uint64_t o_cons = sz; sz += al(fmaxF * 4);
-    const uint64_t o_flag = sz; sz += al(tiles * 4);
-    const uint64_t o_agg = sz; sz += al(tiles * 16);
-    const uint64_t o_inc = sz; sz += al(tiles * 16);
-    const uint64_t o_ctr = sz; sz += al((FDG_MAX_LAYERS + 2) * 4);
+    for (int b = 0; b < 2; ++b) { o_fr[b] = lz; lz += al(fmaxF * 8) + 3 * al(fmaxF * 4); }
+    const uint64_t o_cons = lz; lz += al(fmaxF * 4);
+    const uint64_t o_flag = lz; lz += al(tiles * 4);
+    const uint64_t o_agg = lz; lz += al(tiles * 16);
+    const uint64_t o_inc = lz; lz += al(tiles * 16);
+    const uint64_t o_ctr = lz; lz += al((FDG_MAX_LAYERS + 2) * 4);
+    // sampler-wide layout: hashes of all lanes first (contiguous), then lanes, then shared
+    uint64_t sz = 0;
+    const uint64_t o_hash = sz; sz += s->hash_bytes * group;
+    const uint64_t o_lanes = sz; sz += lz * group;
     const uint64_t o_ex = sz; sz += al(16);
     const uint64_t o_words = sz; sz += al(s->words_cap * 8);
     const uint64_t o_seeds = sz; sz += al(uint64_t(max_seeds) * 8);
@@ -749,36 +1003,50 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
         delete s;
         return cuda_fail(e, "cudaMalloc(sampler arena)", __FILE__, __LINE__);
     }
-    char* a = static_cast<char*>(s->arena);
-    s->keys = a + o_keys;
-    s->vals = reinterpret_cast<uint32_t*>(a + o_keys + uint64_t(s->hsize) * ib);
-    s->seed_slot = reinterpret_cast<uint32_t*>(a + o_seed);
-    s->pick_slot = reinterpret_cast<uint32_t*>(a + o_pick);
-    s->scratch = s->small_f ? nullptr : a + o_scr;
-    for (int b = 0; b < 2; ++b) {
-        char* p = a + o_fr[b];
-        s->fr[b].start = reinterpret_cast<uint64_t*>(p);
-        p += al(fmaxF * 8);
-        s->fr[b].deg = reinterpret_cast<uint32_t*>(p);
-        p += al(fmaxF * 4);
-        s->fr[b].pick_off = reinterpret_cast<uint32_t*>(p);
-        p += al(fmaxF * 4);
-        s->fr[b].draw_off = reinterpret_cast<uint32_t*>(p);
+    char* A = static_cast<char*>(s->arena);
+    s->hash_all = A + o_hash;
+    s->lanes.resize(group);
+    for (uint32_t g = 0; g < group; ++g) {
+        Lane& ln = s->lanes[g];
+        char* a = A + o_lanes + g * lz;
+        ln.hash = A + o_hash + g * s->hash_bytes;
+        ln.seed_slot = reinterpret_cast<uint32_t*>(a + o_seed);
+        ln.pick_slot = reinterpret_cast<uint32_t*>(a + o_pick);
+        ln.rank = reinterpret_cast<uint32_t*>(a + o_rank);
+        ln.picks = s->small_f ? nullptr : a + o_picks;
+        for (int b = 0; b < 2; ++b) {
+            char* p = a + o_fr[b];
+            ln.fr[b].start = reinterpret_cast<uint64_t*>(p);
+            p += al(fmaxF * 8);
+            ln.fr[b].deg = reinterpret_cast<uint32_t*>(p);
+            p += al(fmaxF * 4);
+            ln.fr[b].pick_off = reinterpret_cast<uint32_t*>(p);
+            p += al(fmaxF * 4);
+            ln.fr[b].draw_off = reinterpret_cast<uint32_t*>(p);
+        }
+        ln.consumed = reinterpret_cast<uint32_t*>(a + o_cons);
+        ln.tile_flag = reinterpret_cast<uint32_t*>(a + o_flag);
+        ln.tile_agg = reinterpret_cast<uint4*>(a + o_agg);
+        ln.tile_incl = reinterpret_cast<uint4*>(a + o_inc);
+        ln.tile_ctr = reinterpret_cast<uint32_t*>(a + o_ctr);
+        cudaMemset(ln.tile_flag, 0, tiles * 4);
     }
-    s->consumed = reinterpret_cast<uint32_t*>(a + o_cons);
-    s->tile_flag = reinterpret_cast<uint32_t*>(a + o_flag);
-    s->tile_agg = reinterpret_cast<uint4*>(a + o_agg);
-    s->tile_incl = reinterpret_cast<uint4*>(a + o_inc);
-    s->tile_ctr = reinterpret_cast<uint32_t*>(a + o_ctr);
-    s->exact_flags = reinterpret_cast<uint32_t*>(a + o_ex);
-    s->words = reinterpret_cast<uint64_t*>(a + o_words);
-    s->seeds_buf = reinterpret_cast<uint64_t*>(a + o_seeds);
-    s->cnt_buf = reinterpret_cast<fdg_batch_counts*>(a + o_cnt);
-    cudaMemset(s->tile_flag, 0, tiles * 4);
+    s->exact_flags = reinterpret_cast<uint32_t*>(A + o_ex);
+    s->words = reinterpret_cast<uint64_t*>(A + o_words);
+    s->seeds_buf = reinterpret_cast<uint64_t*>(A + o_seeds);
+    s->cnt_buf = reinterpret_cast<fdg_batch_counts*>(A + o_cnt);
     e = cudaStreamCreateWithFlags(&s->host_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate", __FILE__, __LINE__);
+    if (s->small_f) {  // exact mode (thread-per-node path) needs the picks array of lane 0
+        e = cudaMalloc(&s->lanes[0].picks, std::max<uint64_t>(s->max_edges, 1) * ib);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(picks)", __FILE__, __LINE__);
+    }
     *out = s;
     return FDG_OK;
+}
+
+int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32_t n_layers, Sampler** out) {
+    return sampler_create(ctx, max_seeds, fanouts, n_layers, out, 1);
 }
 
 void sampler_destroy(Sampler* s) {
@@ -788,68 +1056,96 @@ void sampler_destroy(Sampler* s) {
     if (s->ring_words) cudaFree(s->ring_words);
     if (s->out_nodes) cudaFree(s->out_nodes);
     if (s->out_edges) cudaFree(s->out_edges);
+    if (s->small_f && !s->lanes.empty() && s->lanes[0].picks) cudaFree(s->lanes[0].picks);
     if (s->arena) cudaFree(s->arena);
     if (s->host_stream) cudaStreamDestroy(s->host_stream);
     delete s;
 }
 
+// MT streams of upcoming batches, generated concurrently (one CTA each) in a
+// single launch on `st`; the ring holds 2x the largest prefetch group.
 int sampler_prefetch(Sampler* s, cudaStream_t st, const uint64_t* rng_seeds, uint32_t n) {
     if (n == 0) return FDG_OK;
-    if (s->ring_n < n) {
-        // (re)build a ring of n stream slots
+    if (n > 32) {
+        for (uint32_t at = 0; at < n; at += 32) FDG_TRY(sampler_prefetch(s, st, rng_seeds + at, std::min(32u, n - at)));
+        return FDG_OK;
+    }
+    if (s->ring_n < 2 * n) {
         FDG_CUDA(cudaDeviceSynchronize());
         for (auto ev : s->ring_ready) cudaEventDestroy(ev);
         for (auto ev : s->ring_done) cudaEventDestroy(ev);
         if (s->ring_words) cudaFree(s->ring_words);
-        s->ring_n = n;
-        FDG_CUDA(cudaMalloc(&s->ring_words, uint64_t(n) * s->words_cap * 8));
-        s->ring_seed.assign(n, 0);
-        s->ring_valid.assign(n, false);
-        s->ring_ready.resize(n);
-        s->ring_done.resize(n);
-        for (uint32_t i = 0; i < n; ++i) {
+        s->ring_n = 2 * n;
+        FDG_CUDA(cudaMalloc(&s->ring_words, uint64_t(s->ring_n) * s->words_cap * 8));
+        s->ring_seed.assign(s->ring_n, 0);
+        s->ring_valid.assign(s->ring_n, false);
+        s->ring_ready.resize(s->ring_n);
+        s->ring_done.resize(s->ring_n);
+        for (uint32_t i = 0; i < s->ring_n; ++i) {
             FDG_CUDA(cudaEventCreateWithFlags(&s->ring_ready[i], cudaEventDisableTiming));
             FDG_CUDA(cudaEventCreateWithFlags(&s->ring_done[i], cudaEventDisableTiming));
             FDG_CUDA(cudaEventRecord(s->ring_done[i], st));
         }
         s->ring_next = 0;
     }
-    // claim n consecutive ring slots (wrapping), one MT CTA per stream
+    uint32_t slots[32];
     for (uint32_t k = 0; k < n; ++k) {
         uint32_t slot = (s->ring_next + k) % s->ring_n;
+        slots[k] = slot;
         FDG_CUDA(cudaStreamWaitEvent(st, s->ring_done[slot], 0));
         s->ring_seed[slot] = rng_seeds[k];
         s->ring_valid[slot] = true;
-        FDG_CUDA(launch_mt_streams(st, &rng_seeds[k], 1, s->words_cap, s->ring_words + uint64_t(slot) * s->words_cap,
-                                   s->words_cap));
-        FDG_CUDA(cudaEventRecord(s->ring_ready[slot], st));
     }
+    {
+        FDG_TRACE("mt", st);
+        FDG_CUDA(launch_mt_streams_slots(st, rng_seeds, slots, n, s->words_cap, s->ring_words, s->words_cap));
+    }
+    for (uint32_t k = 0; k < n; ++k) FDG_CUDA(cudaEventRecord(s->ring_ready[slots[k]], st));
     s->ring_next = (s->ring_next + n) % s->ring_n;
+    return FDG_OK;
+}
+
+// A group of n <= gmax batches in one launch chain on `st`. MT words come from the
+// prefetch ring when present, else they are generated inline (one CTA per batch).
+int sampler_sample_group(Sampler* s, cudaStream_t st, uint32_t n, const uint64_t* const* seeds, const uint32_t* n_seeds,
+                         const uint64_t* rng_seeds, uint64_t* const* nodes, uint32_t* const* edges, uint64_t cap,
+                         fdg_batch_counts* const* cnt) {
+    if (n == 0) return FDG_OK;
+    if (n > s->gmax) return fail(FDG_INVALID_ARG, "sample_group: more batches than the sampler's group size");
+    if (cap < s->max_nodes || cap < s->max_edges) return fail(FDG_INVALID_ARG, "sample_khop: output capacity below bound");
+    BatchArgs a[kGMax];
+    int ring_slot[kGMax];
+    uint64_t inline_seeds[kGMax];
+    uint32_t n_inline = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        if (n_seeds[i] > s->max_seeds) return fail(FDG_INVALID_ARG, "sample_khop: more seeds than the sampler was sized for");
+        ring_slot[i] = -1;
+        for (uint32_t r = 0; r < s->ring_n; ++r)
+            if (s->ring_valid[r] && s->ring_seed[r] == rng_seeds[i]) {
+                ring_slot[i] = int(r);
+                break;
+            }
+        a[i] = BatchArgs{seeds[i], n_seeds[i], nullptr, s->words_cap, nodes[i], edges[i], cnt[i]};
+        if (ring_slot[i] >= 0) {
+            FDG_CUDA(cudaStreamWaitEvent(st, s->ring_ready[ring_slot[i]], 0));
+            a[i].words = s->ring_words + uint64_t(ring_slot[i]) * s->words_cap;
+            s->ring_valid[ring_slot[i]] = false;
+        } else {
+            if (n_inline > 0) return fail(FDG_INVALID_ARG, "sample_group: at most one batch without a prefetched stream");
+            inline_seeds[n_inline++] = rng_seeds[i];
+            a[i].words = s->words;
+        }
+    }
+    if (n_inline) FDG_CUDA(launch_mt_streams(st, inline_seeds, 1, s->words_cap, s->words, s->words_cap));
+    FDG_TRY(dispatch_group(*s, st, n, a));
+    for (uint32_t i = 0; i < n; ++i)
+        if (ring_slot[i] >= 0) FDG_CUDA(cudaEventRecord(s->ring_done[ring_slot[i]], st));
     return FDG_OK;
 }
 
 int sampler_sample(Sampler* s, cudaStream_t st, const uint64_t* seeds, uint32_t n_seeds, uint64_t rng_seed,
                    uint64_t* nodes, uint32_t* edges, uint64_t cap, fdg_batch_counts* cnt) {
-    if (n_seeds > s->max_seeds) return fail(FDG_INVALID_ARG, "sample_khop: more seeds than the sampler was sized for");
-    if (cap < s->max_nodes || cap < s->max_edges) return fail(FDG_INVALID_ARG, "sample_khop: output capacity below bound");
-    const uint64_t* words = nullptr;
-    int ring_slot = -1;
-    for (uint32_t i = 0; i < s->ring_n; ++i)
-        if (s->ring_valid[i] && s->ring_seed[i] == rng_seed) {
-            ring_slot = int(i);
-            break;
-        }
-    if (ring_slot >= 0) {
-        FDG_CUDA(cudaStreamWaitEvent(st, s->ring_ready[ring_slot], 0));
-        words = s->ring_words + uint64_t(ring_slot) * s->words_cap;
-        s->ring_valid[ring_slot] = false;
-    } else {
-        FDG_CUDA(launch_mt_streams(st, &rng_seed, 1, s->words_cap, s->words, s->words_cap));
-        words = s->words;
-    }
-    FDG_TRY(dispatch_batch(*s, st, seeds, n_seeds, words, s->words_cap, nodes, edges, cnt, false));
-    if (ring_slot >= 0) FDG_CUDA(cudaEventRecord(s->ring_done[ring_slot], st));
-    return FDG_OK;
+    return sampler_sample_group(s, st, 1, &seeds, &n_seeds, &rng_seed, &nodes, &edges, cap, &cnt);
 }
 
 int sampler_sample_host(Sampler* s, const uint64_t* seeds, uint32_t n_seeds, uint64_t rng_seed,
@@ -867,20 +1163,17 @@ int sampler_sample_host(Sampler* s, const uint64_t* seeds, uint32_t n_seeds, uin
         FDG_CUDA(cudaMalloc(&s->out_edges, std::max<uint64_t>(s->max_edges, 1) * 8));
     }
     FDG_CUDA(cudaMemcpyAsync(s->seeds_buf, seeds, uint64_t(n_seeds) * 8, cudaMemcpyHostToDevice, st));
-    const uint64_t* words;
-    uint64_t wcap;
     uint64_t* ext = nullptr;
+    BatchArgs a{s->seeds_buf, n_seeds, s->words, s->words_cap, s->out_nodes, s->out_edges, s->cnt_buf};
     if (ext_words) {
         FDG_CUDA(cudaMalloc(&ext, std::max<uint64_t>(n_ext_words, 1) * 8));
         FDG_CUDA(cudaMemcpyAsync(ext, ext_words, n_ext_words * 8, cudaMemcpyHostToDevice, st));
-        words = ext;
-        wcap = n_ext_words;
+        a.words = ext;
+        a.words_cap = n_ext_words;
     } else {
         FDG_CUDA(launch_mt_streams(st, &rng_seed, 1, s->words_cap, s->words, s->words_cap));
-        words = s->words;
-        wcap = s->words_cap;
     }
-    int rc = dispatch_batch(*s, st, s->seeds_buf, n_seeds, words, wcap, s->out_nodes, s->out_edges, s->cnt_buf, false);
+    int rc = dispatch_group(*s, st, 1, &a);
     if (rc) {
         if (ext) cudaFree(ext);
         return rc;
@@ -889,7 +1182,7 @@ int sampler_sample_host(Sampler* s, const uint64_t* seeds, uint32_t n_seeds, uin
     FDG_CUDA(cudaMemcpyAsync(&h, s->cnt_buf, sizeof(h), cudaMemcpyDeviceToHost, st));
     FDG_CUDA(cudaStreamSynchronize(st));
     if (h.status == FDG_REJECTION) {
-        rc = dispatch_batch(*s, st, s->seeds_buf, n_seeds, words, wcap, s->out_nodes, s->out_edges, s->cnt_buf, true);
+        rc = dispatch_exact(*s, st, a);
         if (rc == FDG_OK) {
             FDG_CUDA(cudaMemcpyAsync(&h, s->cnt_buf, sizeof(h), cudaMemcpyDeviceToHost, st));
             FDG_CUDA(cudaStreamSynchronize(st));
@@ -914,11 +1207,14 @@ int sampler_sample_host(Sampler* s, const uint64_t* seeds, uint32_t n_seeds, uin
     return FDG_OK;
 }
 
-}  // namespace fdg
+void sampler_hash_region(const Sampler* s, void** base, uint64_t* bytes) {
+    *base = s->hash_all;
+    *bytes = s->hash_bytes * s->gmax;
+}
 
-namespace fdg {
 void sampler_capacity(const Sampler* s, uint64_t* max_nodes, uint64_t* max_edges) {
     *max_nodes = s->max_nodes;
     *max_edges = s->max_edges;
 }
+
 }  // namespace fdg

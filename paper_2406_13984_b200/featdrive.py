@@ -155,6 +155,11 @@ class Event:
             self.ptr = None
 
 
+def set_option(key: str, value: int) -> None:
+    """Process-wide tuning knob (fdg_set_option): gather_impl, gather_evict_first, ..."""
+    check(lib().fdg_set_option(key.encode(), int(value)))
+
+
 def device_count() -> int:
     n = C.c_int()
     check(lib().fdg_device_count(C.byref(n)))
@@ -466,6 +471,65 @@ class BufferManager:
         if getattr(self, "ptr", None):
             lib().fdg_bm_destroy(self.ptr)
             self.ptr = None
+
+
+COUNTS_DTYPE = np.dtype([("status", "<u4"), ("n_nodes", "<u4"), ("n_edges", "<u4"), ("rejections", "<u4"),
+                         ("bad_seed", "<u8"), ("checksum", "<u8"), ("bad_seed_pos", "<u4"), ("n_layers", "<u4"),
+                         ("layer_nodes", "<u4", (_lib.MAX_LAYERS + 2,)),
+                         ("layer_edges", "<u4", (_lib.MAX_LAYERS + 1,)),
+                         ("layer_draws", "<u4", (_lib.MAX_LAYERS + 1,)), ("words_used", "<u4"), ("pad", "<u4")])
+
+
+class Pipeline:
+    """Native SET-loop runner (fdg_pipeline_*): PipelineSession's sampler ->
+    extractor (-> trainer checksum -> releaser) stages for one GPU
+    (pipeline.hpp:325-543), batches pipelined across CUDA streams."""
+
+    def __init__(self, topo: Topology, fanouts, batch_size: int = 1000, buffer_slots: int | None = None,
+                 checksum: bool = False, samplers: int = 2, group_batches: int = 1, prefetch_group: int = 16,
+                 flags: int = 0):
+        self.topo = topo
+        cfg = _lib.PipelineConfig(batch_size=batch_size, n_samplers=samplers, prefetch_group=prefetch_group,
+                                  use_buffer_manager=1 if buffer_slots else 0, buffer_slots=buffer_slots or 0,
+                                  write_x=1, checksum=1 if checksum else 0, flags=flags, group_batches=group_batches)
+        f = np.ascontiguousarray(list(fanouts.per_layer if isinstance(fanouts, Fanouts) else fanouts), np.uint32)
+        p = C.c_void_p()
+        check(lib().fdg_pipeline_create(topo.ctx, _p(f), len(f), C.byref(cfg), C.byref(p)))
+        self.ptr = p.value
+        self.batch_size = batch_size
+
+    def run(self, seeds_ptr: int, on_host: bool, rng_seeds, records_ptr: int | None = None,
+            extract_ms: np.ndarray | None = None) -> float:
+        """Run len(rng_seeds) batches; returns the device time of the run in ms."""
+        rng = np.ascontiguousarray(rng_seeds, np.uint64)
+        ms = C.c_float()
+        check(lib().fdg_pipeline_run(self.ptr, seeds_ptr, 1 if on_host else 0, _p(rng), len(rng), records_ptr,
+                                     _p(extract_ms), C.byref(ms)))
+        return ms.value
+
+    def run_batches(self, seeds: np.ndarray, rng_seeds, checksum_records: bool = True) -> np.ndarray:
+        """Convenience: host seeds [n_batches * batch_size] -> per-batch records (COUNTS_DTYPE)."""
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        dev = DeviceBuffer.from_array(seeds)
+        self.run(dev.ptr, False, rng_seeds)
+        return self.records(len(rng_seeds))
+
+    def records(self, n: int) -> np.ndarray:
+        out = np.zeros(n, COUNTS_DTYPE)
+        check(lib().fdg_pipeline_records(self.ptr, 0, n, _p(out)))
+        return out
+
+    def host_enqueue_ms(self) -> float:
+        cfg = _lib.PipelineConfig()
+        check(lib().fdg_pipeline_get_config(self.ptr, C.byref(cfg)))
+        return cfg.host_enqueue_ms
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            lib().fdg_pipeline_destroy(self.ptr)
+            self.ptr = None
+
+    __del__ = close
 
 
 class Extractor:

@@ -1,0 +1,44 @@
+"""A/B experiments on the pipelined run. Each arg: 'k=v,k=v' with keys
+S (samplers), flags, mode (full|sample|extract) and any fdg_set_option key."""
+import ctypes as C
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+import paper_2406_13984_b200 as fd  # noqa: E402
+from paper_2406_13984_b200 import _lib  # noqa: E402
+from paper_2406_13984_b200.featdrive import DeviceBuffer  # noqa: E402
+
+cfgname = "papers"
+n, dim, avg, fan, B, t_ids, dtype, frac = bench.CONFIGS[cfgname]
+L = fd.featdrive.lib()
+topo = fd.Topology.generate(n, dim, avg, 7, dtype=dtype)
+order = np.concatenate(fd.partition_epoch(np.arange(t_ids, dtype=np.uint64), B, bench.hash_combine(0, 0)))
+K = 300
+rng = np.array([L.fdg_batch_seed(0, 0, int(g)) for g in range(K)], np.uint64)
+seeds = DeviceBuffer.from_array(np.ascontiguousarray(order[:K * B]))
+f = np.ascontiguousarray(fan, np.uint32)
+defaults = {"gather_impl": 0, "gather_evict_first": 1, "l2_persist_mb": 0, "hash_load_pct": 50}
+for spec in sys.argv[1:]:
+    kv = dict(x.split("=") for x in spec.split(",") if x)
+    S = int(kv.pop("S", 2))
+    Gb = int(kv.pop("G", 4))
+    mode = kv.pop("mode", "full")
+    flags = int(kv.pop("flags", 0)) | {"full": 0, "sample": 1, "extract": 2}[mode]
+    opts = dict(defaults)
+    opts.update({k: int(v) for k, v in kv.items()})
+    for k, v in opts.items():
+        fd.featdrive.check(L.fdg_set_option(k.encode(), v))
+    cfg = _lib.PipelineConfig(batch_size=B, n_samplers=S, prefetch_group=16, write_x=1, flags=flags, group_batches=Gb)
+    p = C.c_void_p()
+    fd.featdrive.check(L.fdg_pipeline_create(topo.ctx, f.ctypes.data_as(C.c_void_p), len(f), C.byref(cfg), C.byref(p)))
+    ms = C.c_float()
+    res = []
+    for rep in range(3):
+        fd.featdrive.check(L.fdg_pipeline_run(p, seeds.ptr, 0, rng.ctypes.data_as(C.c_void_p), K, None, None, C.byref(ms)))
+        res.append(ms.value / K * 1e3)
+    L.fdg_pipeline_destroy(p)
+    best = min(res[1:])
+    print(f"{spec:60s} {best:7.1f} us/batch  {1e6 / best:7.0f} batches/s", flush=True)

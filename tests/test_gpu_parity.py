@@ -298,3 +298,78 @@ def test_buffer_manager_capacity_and_invariants(fd):
     bm.extract(np.arange(8, dtype=np.uint64))
     with pytest.raises(fd.StandbyTimeout):  # only 2 free slots remain for 5 misses
         bm.extract(np.arange(100, 105, dtype=np.uint64))
+
+
+# ------------------------------------------------------------ native runner --
+@pytest.mark.parametrize("samplers,group,bm", [(1, 1, False), (2, 1, False), (2, 4, False), (3, 8, False),
+                                               (2, 2, True)])
+def test_pipeline_runner_matches_host_api(fd, samplers, group, bm):
+    """fdg_pipeline_run (pipelined, grouped, optional buffer manager) produces the same
+    per-batch node/edge counts and trainer checksums as sample_khop + gather."""
+    n, B, fan = 300_000, 256, [10, 5, 5]
+    t = fd.Topology.generate(n, 32, 12, 3)
+    order = np.concatenate(fd.partition_epoch(np.arange(20 * B, dtype=np.uint64), B, 1234))
+    nb = 20
+    rng = np.array([fd.batch_seed(0, 0, b) for b in range(nb)], np.uint64)
+    pipe = fd.Pipeline(t, fan, B, buffer_slots=(200_000 if bm else None), checksum=True, samplers=samplers,
+                       group_batches=group)
+    recs = pipe.run_batches(order, rng)
+    pipe.close()
+    assert np.all(recs["status"] == 0)
+    for b in range(nb):
+        batch = fd.sample_khop(t, order[b * B:(b + 1) * B], fan, int(rng[b]))
+        _, cs = fd.gather(t, batch.nodes, checksum=True)
+        assert int(recs["n_nodes"][b]) == len(batch.nodes)
+        assert int(recs["n_edges"][b]) == len(batch.edges)
+        assert int(recs["checksum"][b]) == cs, f"batch {b}"
+
+
+def test_pipeline_buffer_capacity_reported(fd):
+    """An undersized feature buffer (S below one batch's nodes) is the reference's
+    StandbyTimeout; the runner reports it in the batch record instead of faulting."""
+    t = fd.Topology.generate(300_000, 32, 12, 3)
+    B, fan = 256, [10, 5, 5]
+    order = np.arange(4 * B, dtype=np.uint64)
+    pipe = fd.Pipeline(t, fan, B, buffer_slots=20_000, checksum=True)
+    recs = pipe.run_batches(order, np.arange(4, dtype=np.uint64) + 1)
+    assert int(recs["status"][0]) == 4  # FDG_CAPACITY
+
+
+def test_pipeline_host_seeds_e2e(fd):
+    """The e2e path: seeds copied from pinned host memory per batch, records read back per batch."""
+    import ctypes as C
+    t = fd.Topology.generate(100_000, 16, 10, 5)
+    B, nb, fan = 128, 9, [4, 4]
+    seeds = np.random.RandomState(0).randint(0, 100_000, size=nb * B).astype(np.uint64)
+    rng = np.arange(nb, dtype=np.uint64) * 7919 + 11
+    L = fd.featdrive.lib()
+    pin, rec = C.c_void_p(), C.c_void_p()
+    fd.featdrive.check(L.fdg_host_alloc(C.byref(pin), seeds.nbytes))
+    fd.featdrive.check(L.fdg_host_alloc(C.byref(rec), nb * fd.featdrive.COUNTS_DTYPE.itemsize))
+    C.memmove(pin.value, seeds.ctypes.data, seeds.nbytes)
+    pipe = fd.Pipeline(t, fan, B, checksum=True)
+    pipe.run(pin.value, True, rng, rec.value)
+    recs = np.frombuffer((C.c_uint8 * (nb * fd.featdrive.COUNTS_DTYPE.itemsize)).from_address(rec.value),
+                         fd.featdrive.COUNTS_DTYPE).copy()
+    for b in range(nb):
+        batch = fd.sample_khop(t, seeds[b * B:(b + 1) * B], fan, int(rng[b]))
+        assert int(recs["checksum"][b]) == fd.gather(t, batch.nodes, checksum=True)[1]
+    L.fdg_host_free(pin.value)
+    L.fdg_host_free(rec.value)
+
+
+@pytest.mark.parametrize("impl", [0, 1])
+def test_gather_impls_agree(fd, port, impl):
+    """TMA bulk-copy gather and LDG gather: identical rows and checksums."""
+    n = 40_000
+    t = fd.Topology.generate(n, 128, 8, 9)
+    table = t.download_rows(0, n)
+    nodes = np.random.RandomState(impl).randint(0, n, size=50_000).astype(np.uint64)
+    fd.set_option("gather_impl", impl)
+    try:
+        x, cs = fd.gather(t, nodes, checksum=True)
+        np.testing.assert_array_equal(x, table[nodes.astype(np.int64)])
+        assert cs == port.checksum_rows(x)
+        np.testing.assert_array_equal(fd.gather(t, nodes), x)
+    finally:
+        fd.set_option("gather_impl", 1)
