@@ -125,6 +125,73 @@ __global__ void k_gather4(const uint64_t* __restrict__ nodes, const uint32_t* n_
     }
 }
 
+// Gather + trainer checksum for rows that are a multiple of 16 bytes. A warp owns
+// groups of 32 rows (one hashing lane per row) and walks them in 128-byte
+// chunks: lanes load the 32 rows' chunk with coalesced 16-byte loads (8 lanes per
+// 128-byte line), write it to X and stage it in shared memory at a 144-byte row
+// stride, then each lane folds its row's 16 8-byte lanes into its splitmix chain
+// from conflict-free 16-byte shared loads. 16 warps per SM keep ~64 KB of rows in
+// flight while the hash chains of other warps run (hash_bytes64, common.hpp:88-105).
+constexpr int kH16Warps = 8;
+constexpr int kH16Stride = 144;
+
+template <bool SHARDED, bool ALIAS>
+__global__ void __launch_bounds__(kH16Warps * 32, 2)
+    k_gather_hash16(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
+                    const uint32_t* status, TableRef t, char* __restrict__ out, uint64_t* checksum) {
+    __shared__ __align__(16) char smem[kH16Warps][32 * kH16Stride];
+    if (status && *status) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    char* wbuf = smem[warp];
+    const uint32_t rb = t.row_bytes;
+    const uint64_t n = n_dev ? *n_dev : n_host;
+    const uint64_t groups = (n + 31) / 32;
+    const uint64_t pol = gather_policy(t.evict_first);
+    uint64_t sum = 0;
+    for (uint64_t g = blockIdx.x * uint64_t(kH16Warps) + warp; g < groups; g += uint64_t(gridDim.x) * kH16Warps) {
+        const uint64_t r0 = g * 32;
+        const uint32_t rows = uint32_t(n - r0 < 32 ? n - r0 : 32);
+        const uint64_t my_node = lane < int(rows) ? nodes[r0 + lane] : 0;
+        uint64_t h = 0x27d4eb2f165667c5ull ^ (uint64_t(rb) * 0x9e3779b97f4a7c15ull);
+        for (uint32_t c0 = 0; c0 < rb; c0 += 128) {
+            const uint32_t parts = (rb - c0 < 128 ? rb - c0 : 128) >> 4;
+            const uint32_t part = lane & 7;
+            uint4 v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t r = k * 4 + (lane >> 3);
+                const uint64_t node = __shfl_sync(0xffffffffu, my_node, int(r));
+                if (r < rows && part < parts) {
+                    const char* src = ALIAS ? t.base + node * rb : row_ptr<SHARDED>(t, node);
+                    v[k] = ldg_stream(reinterpret_cast<const uint4*>(src + c0) + part, pol);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t r = k * 4 + (lane >> 3);
+                if (r < rows && part < parts) {
+                    if (out) stg_stream(reinterpret_cast<uint4*>(out + (r0 + r) * rb + c0) + part, v[k], pol);
+                    *reinterpret_cast<uint4*>(wbuf + r * kH16Stride + part * 16) = v[k];
+                }
+            }
+            __syncwarp();
+            if (lane < int(rows)) {
+                const uint4* p = reinterpret_cast<const uint4*>(wbuf + lane * kH16Stride);
+                for (uint32_t s = 0; s < parts; ++s) {
+                    const uint4 w = p[s];
+                    h = splitmix64(h ^ (uint64_t(w.y) << 32 | w.x));
+                    h = splitmix64(h ^ (uint64_t(w.w) << 32 | w.z));
+                }
+            }
+            __syncwarp();
+        }
+        if (lane < int(rows)) sum += splitmix64(h);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
+}
+
 constexpr int kHashWarps = 4;
 
 __host__ __device__ __forceinline__ uint32_t hash_stride(uint32_t rb) {
@@ -224,6 +291,18 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
     if (g_gather_impl == FDG_GATHER_TMA && out &&
         launch_gather_tma(c, st, nodes, n_dev, n_host, out, checksum, status) == FDG_OK)
         return FDG_OK;  // rows that do not suit the TMA path fall through to the LDG kernels
+    if (checksum && c.row_bytes % 16 == 0) {
+        uint64_t groups = (n_bound + 31) / 32;
+        int blocks = int(std::min<uint64_t>((groups + kH16Warps - 1) / kH16Warps, uint64_t(c.sm_count) * 2));
+        if (sharded)
+            k_gather_hash16<true, false><<<blocks, kH16Warps * 32, 0, st>>>(nodes, n_dev, n_host, status, t,
+                                                                          static_cast<char*>(out), checksum);
+        else
+            k_gather_hash16<false, false><<<blocks, kH16Warps * 32, 0, st>>>(nodes, n_dev, n_host, status, t,
+                                                                           static_cast<char*>(out), checksum);
+        FDG_CUDA(cudaGetLastError());
+        return FDG_OK;
+    }
     if (checksum) {
         size_t smem = size_t(kHashWarps) * 32 * hash_stride(c.row_bytes);
         static bool attr_set[2] = {false, false};
@@ -277,6 +356,14 @@ int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, con
     if (!checksum) return fail(FDG_INVALID_ARG, "checksum: null output");
     TableRef t = table_ref(c);
     t.base = static_cast<const char*>(region);
+    if (c.row_bytes % 16 == 0) {
+        uint64_t groups = (std::max<uint64_t>(n_host, 1) + 31) / 32;
+        int blocks = int(std::min<uint64_t>((groups + kH16Warps - 1) / kH16Warps, uint64_t(c.sm_count) * 2));
+        k_gather_hash16<false, true><<<blocks, kH16Warps * 32, 0, st>>>(reinterpret_cast<const uint64_t*>(alias),
+                                                                       n_dev, n_host, status, t, nullptr, checksum);
+        FDG_CUDA(cudaGetLastError());
+        return FDG_OK;
+    }
     size_t smem = size_t(kHashWarps) * 32 * hash_stride(c.row_bytes);
     static bool attr_set = false;
     if (!attr_set) {
