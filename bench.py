@@ -260,13 +260,18 @@ def run_ours(args):
     from paper_2406_13984_b200.featdrive import DeviceBuffer
 
     dist = Dist()
-    dev = dist.local
+    from paper_2406_13984_b200 import dist as fdist
+    dev = fdist.local_device(dist.local)
     L = fd.featdrive.lib()
     fd.featdrive.check(L.fdg_set_device(dev))
     cfg = args.config
     n, dim, avg, fan, B, t_ids, dtype, frac = CONFIGS[cfg]
     t0 = time.time()
-    topo = fd.Topology.generate(n, dim, avg, GEN_SEED, dtype=dtype, device=dev)
+    shard = args.shard and dist.world > 1
+    topo = fd.Topology.generate(n, dim, avg, GEN_SEED, dtype=dtype, device=dev, features=not shard)
+    sharded = None
+    if shard:  # row-sharded table: own rows generated locally, peers' rows read over NVLink (IPC)
+        sharded = fdist.ShardedFeatures(topo, dist.rank, dist.world, GEN_SEED, n, dim, dtype)
     info = topo.info()
     rb = info.row_bytes
     log(f"[rank {dist.rank}] generated {cfg} in HBM: {info.num_edges} edges, {rb} B rows, {time.time() - t0:.1f}s")
@@ -283,7 +288,7 @@ def run_ours(args):
         return np.ascontiguousarray(np.concatenate([order[g * B:(g + 1) * B] for g in ids_]))
 
     bm_slots = int(n * frac) if frac else None
-    pipe = Pipeline(fd, topo, fan, B, bm_slots=bm_slots, checksum=False, samplers=args.samplers)
+    pipe = Pipeline(fd, topo, fan, B, bm_slots=bm_slots, checksum=False, samplers=args.samplers, group=args.group)
     # ---------------- device-resident timed region ----------------
     warm_dev = DeviceBuffer.from_array(seeds_for(ids_warm))
     timed_dev = DeviceBuffer.from_array(seeds_for(ids))
@@ -308,7 +313,7 @@ def run_ours(args):
     # ---------------- end to end through the C ABI with host buffers ----------------
     # every step: H2D of the batch's seeds from pinned memory, sample, extract with the
     # fused trainer checksum, D2H of the batch record (counts + checksum) into pinned memory.
-    e2e = Pipeline(fd, topo, fan, B, bm_slots=bm_slots, checksum=True, samplers=args.samplers)
+    e2e = Pipeline(fd, topo, fan, B, bm_slots=bm_slots, checksum=True, samplers=args.samplers, group=args.group)
     csz = counts_dtype().itemsize
     pins = []
 
@@ -343,7 +348,8 @@ def run_ours(args):
         "dtype": "u64", "data": "synthetic (bit-exact GPU port of the reference generator, seed 7)",
         "config": {"workload": DESCR[cfg], "config": cfg, "nodes": n, "edges": int(info.num_edges),
                    "row_bytes": rb, "fanouts": fan, "batch": B, "global_batch": B * dist.world,
-                   "parallelism": f"dp{dist.world} (replicated CSR + table)",
+                   "parallelism": (f"dp{dist.world} (replicated CSR, table row-sharded over NVLink P2P)" if shard
+                                   else f"dp{dist.world} (replicated CSR + table)"),
                    "l2_policy": "inputs > L2 (57 GB table, ~0.5 GB X per batch); no flush",
                    "mean_nodes_per_batch": float(n_nodes.mean()), "samplers": args.samplers,
                    "buffer_slots": bm_slots},
@@ -368,6 +374,9 @@ def run_ours(args):
             line["cpu_baseline"] = {"value": None, "error": repr(e)}
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
+    dist.barrier()  # peers' shards stay mapped until every rank is done
+    if sharded:
+        sharded.close()
     dist.close()
 
 
@@ -433,6 +442,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="papers", choices=sorted(CONFIGS))
     ap.add_argument("--samplers", type=int, default=2)
+    ap.add_argument("--group", type=int, default=1, help="batches sampled per launch chain")
+    ap.add_argument("--shard", action="store_true",
+                    help="N>1: row-shard the feature table across GPUs (remote rows over NVLink P2P)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-batches", type=int, default=0)
     args = ap.parse_args()

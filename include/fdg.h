@@ -126,6 +126,19 @@ int fdg_ctx_generate_features(fdg_ctx* ctx, uint64_t seed, uint64_t num_nodes, u
 int fdg_ctx_set_feature_shards(fdg_ctx* ctx, const void* const* bases_dev, uint32_t n_shards,
                                uint64_t rows_per_shard, uint64_t num_nodes, uint32_t row_bytes, uint32_t dtype);
 int fdg_ctx_download_topology(const fdg_ctx* ctx, uint64_t* indptr, void* indices /* idx_bytes each */);
+
+/* ---- multi-GPU: one process per GPU, row-sharded feature table read over NVLink ----
+ * Rank r generates only its block of rows (owner = node / ceil(N / n_shards)) into a
+ * fresh allocation owned by the context, exports it with a CUDA IPC handle, opens
+ * the peers' handles, and installs all bases with fdg_ctx_set_feature_shards; the
+ * gather then loads remote rows directly through the peer mappings (one-sided, no
+ * collective). */
+int fdg_ctx_generate_feature_shard(fdg_ctx* ctx, uint64_t seed, uint64_t num_nodes, uint32_t dim, uint32_t dtype,
+                                   uint32_t shard, uint32_t n_shards, void** base_dev);
+#define FDG_IPC_HANDLE_BYTES 64
+int fdg_ipc_get_handle(const void* base_dev, unsigned char* handle /* FDG_IPC_HANDLE_BYTES */);
+int fdg_ipc_open_handle(const unsigned char* handle, void** base_dev);
+int fdg_ipc_close_handle(void* base_dev);
 int fdg_ctx_download_rows(const fdg_ctx* ctx, uint64_t first, uint64_t count, void* out);
 
 /* ---- sampler: replaces graph::sample_khop (sampling.hpp:72-134) --------------- */

@@ -79,6 +79,10 @@ SIGNATURES = {
     "fdg_ctx_generate_features": (ci, [vp, u64, u64, u32, u32, u32]),
     "fdg_ctx_set_feature_shards": (ci, [vp, vp, u32, u64, u64, u32, u32]),
     "fdg_ctx_download_topology": (ci, [vp, vp, vp]),
+    "fdg_ctx_generate_feature_shard": (ci, [vp, u64, u64, u32, u32, u32, u32, C.POINTER(vp)]),
+    "fdg_ipc_get_handle": (ci, [vp, vp]),
+    "fdg_ipc_open_handle": (ci, [vp, C.POINTER(vp)]),
+    "fdg_ipc_close_handle": (ci, [vp]),
     "fdg_ctx_download_rows": (ci, [vp, u64, u64, vp]),
     "fdg_sampler_create": (ci, [vp, u32, vp, u32, C.POINTER(vp)]),
     "fdg_sampler_destroy": (ci, [vp]),

@@ -284,8 +284,7 @@ int fdg_ctx_set_feature_shards(fdg_ctx* c, const void* const* bases, uint32_t n_
     if (n_shards == 0 || rps == 0 || (n + rps - 1) / rps > n_shards)
         return fail(FDG_INVALID_ARG, "feature shards: inconsistent geometry");
     cudaSetDevice(c->device);
-    for (void* p : c->owned_shards) cudaFree(p);
-    c->owned_shards.clear();
+    // allocations owned by the context (e.g. this rank's shard) stay alive until destroy
     c->shard_bases.clear();
     for (uint32_t i = 0; i < n_shards; ++i) c->shard_bases.push_back(const_cast<void*>(bases[i]));
     c->row_bytes = row_bytes;
@@ -296,6 +295,33 @@ int fdg_ctx_set_feature_shards(fdg_ctx* c, const void* const* bases, uint32_t n_
     if (c->shard_table) cudaFree((void*)c->shard_table);
     FDG_CUDA(cudaMalloc((void**)&c->shard_table, n_shards * sizeof(void*)));
     FDG_CUDA(cudaMemcpy((void*)c->shard_table, c->shard_bases.data(), n_shards * sizeof(void*), cudaMemcpyHostToDevice));
+    return FDG_OK;
+}
+
+int fdg_ctx_generate_feature_shard(fdg_ctx* c, uint64_t seed, uint64_t n, uint32_t dim, uint32_t dtype, uint32_t shard,
+                                   uint32_t n_shards, void** base) {
+    cudaSetDevice(c->device);
+    return generate_feature_shard(*c, seed, n, dim, dtype, shard, n_shards, base);
+}
+
+int fdg_ipc_get_handle(const void* base, unsigned char* handle) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == FDG_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    FDG_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(base)));
+    std::memcpy(handle, &h, sizeof(h));
+    return FDG_OK;
+}
+
+int fdg_ipc_open_handle(const unsigned char* handle, void** base) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    // lazy peer enablement: remote rows are then read over NVLink by ordinary loads
+    FDG_CUDA(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess));
+    return FDG_OK;
+}
+
+int fdg_ipc_close_handle(void* base) {
+    FDG_CUDA(cudaIpcCloseMemHandle(base));
     return FDG_OK;
 }
 

@@ -179,6 +179,31 @@ int generate_topology(Ctx& c, uint64_t seed, uint64_t n, uint32_t avg) {
     return FDG_OK;
 }
 
+int generate_feature_shard(Ctx& c, uint64_t seed, uint64_t n, uint32_t dim, uint32_t dtype, uint32_t shard,
+                           uint32_t n_shards, void** base) {
+    if (n == 0 || dim == 0 || n_shards == 0 || shard >= n_shards)
+        return fail(FDG_INVALID_ARG, "generate_feature_shard: bad geometry");
+    if (dtype > 1) return fail(FDG_INVALID_ARG, "generate_feature_shard: dtype must be 0 (f32) or 1 (f16)");
+    const uint32_t row_bytes = dim * (dtype == 0 ? 4 : 2);
+    const uint64_t rps = (n + n_shards - 1) / n_shards;
+    const uint64_t first = uint64_t(shard) * rps;
+    const uint64_t count = first < n ? std::min<uint64_t>(rps, n - first) : 0;
+    void* p = nullptr;
+    FDG_CUDA(cudaMalloc(&p, std::max<uint64_t>(count, 1) * row_bytes));
+    c.owned_shards.push_back(p);
+    if (count) {
+        int blocks = int(std::min<uint64_t>((count + 7) / 8, uint64_t(c.sm_count) * 16));
+        if (dtype == 0)
+            k_rows<float><<<blocks, 256, 0, c.stream>>>(seed, first, count, dim, (float*)p);
+        else
+            k_rows<__half><<<blocks, 256, 0, c.stream>>>(seed, first, count, dim, (__half*)p);
+        FDG_CUDA(cudaGetLastError());
+    }
+    FDG_CUDA(cudaStreamSynchronize(c.stream));
+    *base = p;
+    return FDG_OK;
+}
+
 int generate_features(Ctx& c, uint64_t seed, uint64_t n, uint32_t dim, uint32_t dtype, uint32_t n_shards) {
     if (n == 0 || dim == 0) return fail(FDG_INVALID_ARG, "generate_features: empty table");
     if (dtype > 1) return fail(FDG_INVALID_ARG, "generate_features: dtype must be 0 (f32) or 1 (f16)");

@@ -89,6 +89,8 @@ namespace fdg {
 // generator entry points (fdg_generate.cu)
 int generate_topology(Ctx& c, uint64_t seed, uint64_t num_nodes, uint32_t avg_degree);
 int generate_features(Ctx& c, uint64_t seed, uint64_t num_nodes, uint32_t dim, uint32_t dtype, uint32_t n_shards);
+int generate_feature_shard(Ctx& c, uint64_t seed, uint64_t n, uint32_t dim, uint32_t dtype, uint32_t shard,
+                           uint32_t n_shards, void** base);
 // MT19937-64 (fdg_mt.cu)
 // rng_seeds: HOST array (passed by value to the kernel)
 cudaError_t launch_mt_streams(cudaStream_t st, const uint64_t* rng_seeds, uint32_t n_streams,

@@ -1,0 +1,96 @@
+"""Multi-GPU plumbing: one process per GPU (torchrun), batches split into contiguous
+segments like PipelineSession::run_epoch_multi (pipeline.hpp:185-203), and an
+optional row-sharded feature table whose remote rows the gather reads through
+CUDA IPC peer mappings over NVLink (no collective on the data path).
+
+torch.distributed is used only as the control plane (barriers, max-over-ranks
+timing, IPC handle exchange); the data path is libfdg.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import featdrive as fdm
+
+
+def segment(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous chunk range of `rank`; sizes differ by at most one (pipeline.hpp:192-203)."""
+    base, rem = divmod(total, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def shard_geometry(num_nodes: int, n_shards: int) -> tuple[int, list[tuple[int, int]]]:
+    """Row blocks of ceil(N / n_shards): owner(node) = node // rows_per_shard."""
+    rps = -(-num_nodes // n_shards)
+    return rps, [(min(s * rps, num_nodes), min((s + 1) * rps, num_nodes)) for s in range(n_shards)]
+
+
+def exchange_handles(my_handle: bytes, rank: int, world: int, allgather) -> list[bytes]:
+    """All ranks' IPC handles in rank order; `allgather(obj) -> list` is e.g.
+    torch.distributed.all_gather_object over a gloo group."""
+    got = allgather(bytes(my_handle))
+    if len(got) != world or bytes(got[rank]) != bytes(my_handle):
+        raise fdm.InvariantViolation("IPC handle exchange returned an inconsistent view")
+    return [bytes(h) for h in got]
+
+
+def torch_allgather(group=None):
+    import torch.distributed as dist
+
+    def ag(obj):
+        out = [None] * dist.get_world_size(group)
+        dist.all_gather_object(out, obj, group=group)
+        return out
+
+    return ag
+
+
+class ShardedFeatures:
+    """This rank's shard of the synthetic table + the peers' shards mapped over IPC."""
+
+    def __init__(self, topo: fdm.Topology, rank: int, world: int, seed: int, num_nodes: int, dim: int,
+                 dtype: str = "f32", allgather=None):
+        L = fdm.lib()
+        self.topo, self.rank, self.world = topo, rank, world
+        base = C.c_void_p()
+        dt = 0 if dtype == "f32" else 1
+        fdm.check(L.fdg_ctx_generate_feature_shard(topo.ctx, seed, num_nodes, dim, dt, rank, world, C.byref(base)))
+        h = (C.c_ubyte * 64)()
+        fdm.check(L.fdg_ipc_get_handle(base.value, h))
+        handles = exchange_handles(bytes(h), rank, world, allgather or torch_allgather())
+        self.opened = []
+        bases = []
+        for r, hb in enumerate(handles):
+            if r == rank:
+                bases.append(base.value)
+                continue
+            p = C.c_void_p()
+            fdm.check(L.fdg_ipc_open_handle((C.c_ubyte * 64).from_buffer_copy(hb), C.byref(p)))
+            self.opened.append(p.value)
+            bases.append(p.value)
+        rps, _ = shard_geometry(num_nodes, world)
+        arr = (C.c_void_p * world)(*bases)
+        row_bytes = dim * (4 if dt == 0 else 2)
+        fdm.check(L.fdg_ctx_set_feature_shards(topo.ctx, C.cast(arr, C.c_void_p), world, rps, num_nodes, row_bytes,
+                                               dt))
+        self.rows_per_shard = rps
+
+    def close(self):
+        L = fdm.lib()
+        for p in self.opened:
+            L.fdg_ipc_close_handle(p)
+        self.opened = []
+
+
+def local_device(local_rank: int) -> int:
+    """GPU of this process (several ranks may share one GPU in tests)."""
+    n = fdm.device_count()
+    return local_rank % max(n, 1)
+
+
+def rank_batches(n_batches: int, world: int, rank: int) -> np.ndarray:
+    lo, hi = segment(n_batches, world, rank)
+    return np.arange(lo, hi, dtype=np.int64)

@@ -1,0 +1,91 @@
+"""Multi-process (world_size 2, gloo) coverage of the N>1 host logic on CPU, and the
+IPC row-sharded gather with two processes on one GPU."""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    from paper_2406_13984_b200 import dist as fdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # contiguous segments of the epoch's batches, as PipelineSession::run_epoch_multi
+        lo, hi = fdist.segment(1001, world, rank)
+        segs = [None] * world
+        dist.all_gather_object(segs, (lo, hi))
+        # IPC handle exchange protocol (fake 64-byte handles)
+        mine = bytes([rank + 1]) * 64
+        handles = fdist.exchange_handles(mine, rank, world, fdist.torch_allgather())
+        # bench's max-over-ranks timing reduction
+        os.environ["WORLD_SIZE"], os.environ["RANK"], os.environ["LOCAL_RANK"] = str(world), str(rank), str(rank)
+        import bench
+        d = bench.Dist.__new__(bench.Dist)
+        d.world, d.rank, d.local, d.dist = world, rank, rank, dist
+        mx = d.reduce(float(10 + rank), "max")
+        sm = d.reduce(1.0, "sum")
+        q.put((rank, segs, [h[0] for h in handles], mx, sm))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_host_logic():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    (r0, segs0, h0, mx0, sm0), (r1, segs1, h1, mx1, sm1) = res
+    assert segs0 == segs1 == [(0, 501), (501, 1001)]  # contiguous, sizes differ by <= 1
+    assert h0 == h1 == [1, 2]
+    assert mx0 == mx1 == 11.0 and sm0 == sm1 == 2.0
+
+
+def test_shard_geometry_and_segments():
+    sys.path.insert(0, ROOT)
+    from paper_2406_13984_b200 import dist as fdist
+    rps, blocks = fdist.shard_geometry(10_001, 4)
+    assert rps == 2501 and blocks[-1] == (7503, 10_001)
+    owner = np.arange(10_001) // rps
+    for s, (lo, hi) in enumerate(blocks):
+        assert np.all(owner[lo:hi] == s)
+    for world in (1, 2, 3, 8):
+        covered = np.concatenate([fdist.rank_batches(1000, world, r) for r in range(world)])
+        np.testing.assert_array_equal(covered, np.arange(1000))
+
+
+@pytest.mark.gpu
+def test_two_process_ipc_sharded_gather():
+    """Two ranks (torchrun, one GPU): each generates its half of the table, the halves
+    are exchanged over CUDA IPC, and every rank's sharded gather equals the rows of
+    the full single-process table."""
+    port = _free_port()
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port),
+                          os.path.join(ROOT, "tests", "mp_shard_check.py")],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert out.stdout.count("shard-ok") == 2
