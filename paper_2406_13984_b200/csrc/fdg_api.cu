@@ -407,11 +407,17 @@ int fdg_set_option(const char* key, int64_t v) {
     if (k == "gather_impl") return fdg_set_gather_impl(int(v));
     if (k == "gather_evict_first") { g_gather_evict_first = v != 0; return FDG_OK; }
     if (k == "l2_persist_mb") { g_l2_persist_mb = v < 0 ? 0 : v; return FDG_OK; }
+    if (k == "sampler_ctas_per_sm") {
+        if (v < 1 || v > 64) return fail(FDG_INVALID_ARG, "sampler_ctas_per_sm must be in [1, 64]");
+        g_sampler_ctas_per_sm = v;
+        return FDG_OK;
+    }
     if (k == "gather_ctas_per_sm") {
         if (v < 1 || v > 4) return fail(FDG_INVALID_ARG, "gather_ctas_per_sm must be in [1, 4]");
         g_gather_ctas_per_sm = int(v);
         return FDG_OK;
     }
+    if (k == "hash_clear") { g_hash_clear = v != 0; return FDG_OK; }
     if (k == "hash_load_pct") {
         if (v < 10 || v > 70) return fail(FDG_INVALID_ARG, "hash_load_pct must be in [10, 70]");
         g_hash_load_pct = v;
@@ -427,6 +433,8 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "l2_persist_mb") *v = g_l2_persist_mb;
     else if (k == "hash_load_pct") *v = g_hash_load_pct;
     else if (k == "gather_ctas_per_sm") *v = g_gather_ctas_per_sm;
+    else if (k == "sampler_ctas_per_sm") *v = g_sampler_ctas_per_sm;
+    else if (k == "hash_clear") *v = g_hash_clear;
     else return fail(FDG_INVALID_ARG, "unknown option " + k);
     return FDG_OK;
 }

@@ -106,6 +106,8 @@ extern int g_gather_evict_first;
 extern int g_gather_ctas_per_sm;
 extern int64_t g_l2_persist_mb;
 extern int64_t g_hash_load_pct;
+extern int64_t g_sampler_ctas_per_sm;
+extern int64_t g_hash_clear;  // 1: clear batch hash tables with a fill kernel, 0: cudaMemsetAsync
 int launch_gather_tma(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                       void* out, uint64_t* checksum, const uint32_t* status);
 int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, const int64_t* alias,

@@ -14,8 +14,11 @@
 //                     trainer checksum and the optional D2H of the batch record
 // so groups g+1..g+S are sampled while group g is extracted. Batch j is keyed
 // exactly as the reference (rng seed = batch_seed(seed, epoch, global id)).
+#include <cuda_profiler_api.h>
+
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <vector>
 
 #include "fdg_internal.cuh"
@@ -39,7 +42,8 @@ struct fdg_pipeline {
     fdg_pipeline_config cfg{};
     std::vector<fdg::Sampler*> samplers;
     std::vector<cudaStream_t> sstream;
-    cudaStream_t xstream = nullptr, mstream = nullptr;
+    std::vector<cudaStream_t> mstream;   // per-sampler MT prefetch streams
+    cudaStream_t xstream = nullptr;
     uint64_t cap = 0, max_nodes = 0;
     uint32_t nslots = 0;             // per-batch output slots (2 * S * G)
     std::vector<uint64_t*> nodes;
@@ -65,7 +69,7 @@ void destroy(fdg_pipeline* p) {
     for (auto s : p->samplers) sampler_destroy(s);
     for (auto s : p->sstream) cudaStreamDestroy(s);
     if (p->xstream) cudaStreamDestroy(p->xstream);
-    if (p->mstream) cudaStreamDestroy(p->mstream);
+    for (auto s : p->mstream) cudaStreamDestroy(s);
     for (auto v : p->nodes) cudaFree(v);
     for (auto v : p->edges) cudaFree(v);
     for (auto v : p->seeds) cudaFree(v);
@@ -151,7 +155,12 @@ int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers
     p->max_nodes = mn;
     p->cap = std::max<uint64_t>(std::max(mn, me), 1);
     FDG_CUDA(cudaStreamCreateWithPriority(&p->xstream, cudaStreamNonBlocking, prio_lo));
-    FDG_CUDA(cudaStreamCreateWithFlags(&p->mstream, cudaStreamNonBlocking));
+    // one MT stream per sampler: prefetch launches of different samplers overlap
+    for (uint32_t i = 0; i < S; ++i) {
+        cudaStream_t st;
+        FDG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        p->mstream.push_back(st);
+    }
     p->nslots = 2 * S * G;
     for (uint32_t i = 0; i < p->nslots; ++i) {
         uint64_t* n;
@@ -231,13 +240,20 @@ int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, 
             std::vector<uint64_t> r;
             for (uint64_t k = fetched[s]; k < std::min<uint64_t>(fetched[s] + PG, mine[s].size()); ++k)
                 r.push_back(rng_seeds[mine[s][k]]);
-            FDG_TRY(sampler_prefetch(p->samplers[s], p->mstream, r.data(), uint32_t(r.size())));
+            FDG_TRY(sampler_prefetch(p->samplers[s], p->mstream[s], r.data(), uint32_t(r.size())));
             fetched[s] += r.size();
         }
         return FDG_OK;
     };
     for (uint32_t s = 0; s < S; ++s) FDG_TRY(prefetch_upto(s, PG));
     std::vector<uint64_t> consumed(S, 0);
+    // FDG_PROFILE_RANGE=1: bracket the run for ncu range replay (concurrent kernels
+    // profiled together: --replay-mode app-range --profile-from-start off)
+    static const bool prof_range = std::getenv("FDG_PROFILE_RANGE") != nullptr;
+    if (prof_range) {
+        FDG_CUDA(cudaDeviceSynchronize());
+        cudaProfilerStart();
+    }
     cudaEvent_t t0, t1;
     FDG_CUDA(cudaEventCreate(&t0));
     FDG_CUDA(cudaEventCreate(&t1));
@@ -333,6 +349,7 @@ int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, 
         std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - h0).count();
     FDG_CUDA(cudaEventSynchronize(t1));
     FDG_CUDA(cudaDeviceSynchronize());
+    if (prof_range) cudaProfilerStop();
     float ms = 0;
     FDG_CUDA(cudaEventElapsedTime(&ms, t0, t1));
     if (elapsed_ms) *elapsed_ms = ms;

@@ -308,25 +308,42 @@ __device__ Tri tri_lookback(uint32_t* flags, uint4* aggs, uint4* incls, uint32_t
 // bound the sampler); the scan runs as 8 row scans (one per k) -- one warp per
 // row for the cross-warp step -- then one decoupled look-back per tile.
 template <typename IdT, bool SEEDS, bool HAS_NEXT>
+__device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint32_t epoch, uint32_t tile,
+                                            uint32_t P, uint32_t ntiles);
+
+// Persistent: a capped number of CTAs claim tiles in order (keeps SM slots free
+// for the concurrently running gather; look-back needs only claim order).
+template <typename IdT, bool SEEDS, bool HAS_NEXT>
 __global__ void __launch_bounds__(kScanThreads) k_intern_s(const __grid_constant__ Group<IdT> G, uint32_t q,
                                                            uint32_t epoch) {
-    static_assert(kScanItems == kScanThreads / 32, "one warp per row scan");
     const Work<IdT>& W = G.w[blockIdx.y];
-    __shared__ Tri s_row[kScanItems][kScanThreads / 32];  // per row: warp inclusive -> exclusive
-    __shared__ Tri s_rowx[kScanItems];                    // per row: exclusive offset within the tile
-    __shared__ Tri s_excl, s_agg;
     __shared__ uint32_t s_tile;
     fdg_batch_counts* cnt = W.cnt;
     if (cnt->status) return;
     const uint32_t P = SEEDS ? W.n_seeds : cnt->layer_edges[q] - cnt->layer_edges[q - 1];
+    const uint32_t ntiles = P ? (P + kTile - 1) / kTile : 1;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(W.tile_ctr + q, 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        __syncthreads();
+        if (tile >= ntiles) return;
+        intern_tile<IdT, SEEDS, HAS_NEXT>(W, q, epoch, tile, P, ntiles);
+        __syncthreads();
+    }
+}
+
+template <typename IdT, bool SEEDS, bool HAS_NEXT>
+__device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint32_t epoch, uint32_t tile,
+                                            uint32_t P, uint32_t ntiles) {
+    static_assert(kScanItems == kScanThreads / 32, "one warp per row scan");
+    __shared__ Tri s_row[kScanItems][kScanThreads / 32];  // per row: warp inclusive -> exclusive
+    __shared__ Tri s_rowx[kScanItems];                    // per row: exclusive offset within the tile
+    __shared__ Tri s_excl, s_agg;
+    fdg_batch_counts* cnt = W.cnt;
     const uint32_t ebase = SEEDS ? 0 : cnt->layer_edges[q - 1];
     const uint32_t node_base = cnt->layer_nodes[q];
-    const uint32_t ntiles = P ? (P + kTile - 1) / kTile : 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(W.tile_ctr + q, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    if (tile >= ntiles) return;
     const uint32_t f = HAS_NEXT ? W.fan[q] : 0;
     const uint32_t p0 = tile * kTile + tid;  // item k: p0 + k * kScanThreads
 
@@ -437,7 +454,7 @@ __global__ void __launch_bounds__(kScanThreads) k_intern_s(const __grid_constant
             const uint32_t r = base.c + ex[k].c;
             const uint32_t local = node_base + r;
             W.nodes[local] = uint64_t(key[k]);
-            W.tab.finalize(slot[k], key[k], local);
+            if (HAS_NEXT) W.tab.finalize(slot[k], key[k], local);  // no later pass reads the last layer's entries
             if (!SEEDS) W.edges[2 * (ebase + p)] = local;
             if (HAS_NEXT) {
                 fr.start[r] = lo[k];
@@ -691,6 +708,26 @@ __global__ void k_rescan_draws(uint32_t* consumed, uint32_t* draw_off, const fdg
 
 int64_t g_l2_persist_mb = 0;
 int64_t g_hash_load_pct = 50;
+int64_t g_sampler_ctas_per_sm = 16;
+int64_t g_hash_clear = 1;
+
+namespace {
+// Fill `n16` 16-byte words with all-ones (the empty hash entry), grid-stride.
+__global__ void __launch_bounds__(512) k_fill_ones(uint4* p, uint64_t n16) {
+    const uint4 v = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16; i += uint64_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+}  // namespace
+
+cudaError_t clear_hash(void* base, uint64_t bytes, int sm_count, cudaStream_t st) {
+    if (!g_hash_clear || (bytes & 15) || (uintptr_t(base) & 15)) return cudaMemsetAsync(base, 0xFF, bytes, st);
+    const uint64_t n16 = bytes / 16;
+    const uint64_t want = (n16 + 511) / 512;
+    const int grid = int(std::min<uint64_t>(want, uint64_t(sm_count) * 4));
+    k_fill_ones<<<std::max(grid, 1), 512, 0, st>>>((uint4*)base, n16);
+    return cudaGetLastError();
+}
 
 // ------------------------------------------------------------------ Sampler ----
 struct Lane {  // per-batch workspace of one group slot
@@ -811,7 +848,9 @@ void launch_intern(Sampler& s, cudaStream_t st, const Group<IdT>& G, uint32_t n,
     const bool seeds = q == 0;
     const bool has_next = q < s.n_layers;
     const uint64_t P = seeds ? max_seeds : s.P_bound[q - 1];
-    const dim3 grid(uint32_t(std::max<uint64_t>(1, (P + kTile - 1) / kTile)), n);
+    const uint64_t tiles = std::max<uint64_t>(1, (P + kTile - 1) / kTile);
+    const uint64_t cap = std::max<uint64_t>(1, uint64_t(s.ctx->sm_count) * g_sampler_ctas_per_sm / n);
+    const dim3 grid(uint32_t(std::min(tiles, cap)), n);
     if (seeds) {
         if (has_next) k_intern_s<IdT, true, true><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
         else k_intern_s<IdT, true, false><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
@@ -852,7 +891,7 @@ int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
     }
     {
         FDG_TRACE("memset", st);
-        FDG_CUDA(cudaMemsetAsync(s.hash_all, 0xFF, s.hash_bytes * n, st));
+        FDG_CUDA(clear_hash(s.hash_all, s.hash_bytes * n, s.ctx->sm_count, st));
     }
     {
         FDG_TRACE("seeds", st);
@@ -869,7 +908,7 @@ int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
         {
             FDG_TRACE(names[0][l], st);
             if (s.small_f) {
-                const dim3 grid(grid_for(s.F_bound[l] * 16, 256, s.ctx->sm_count * 16 / int(n)), n);
+                const dim3 grid(grid_for(s.F_bound[l] * 16, 256, int(s.ctx->sm_count * g_sampler_ctas_per_sm / n)), n);
                 k_expand<IdT><<<grid, 256, 0, st>>>(G, l);
             } else {
                 launch_sample<IdT, 0>(s, st, G, n, l);

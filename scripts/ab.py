@@ -20,11 +20,12 @@ K = 300
 rng = np.array([L.fdg_batch_seed(0, 0, int(g)) for g in range(K)], np.uint64)
 seeds = DeviceBuffer.from_array(np.ascontiguousarray(order[:K * B]))
 f = np.ascontiguousarray(fan, np.uint32)
-defaults = {"gather_impl": 0, "gather_evict_first": 1, "l2_persist_mb": 0, "hash_load_pct": 50}
+defaults = {"gather_impl": 1, "gather_evict_first": 1, "l2_persist_mb": 0, "hash_load_pct": 50,
+            "hash_clear": 1, "sampler_ctas_per_sm": 16, "gather_ctas_per_sm": 2}
 for spec in sys.argv[1:]:
     kv = dict(x.split("=") for x in spec.split(",") if x)
     S = int(kv.pop("S", 2))
-    Gb = int(kv.pop("G", 4))
+    Gb = int(kv.pop("G", 1))
     mode = kv.pop("mode", "full")
     flags = int(kv.pop("flags", 0)) | {"full": 0, "sample": 1, "extract": 2}[mode]
     opts = dict(defaults)
