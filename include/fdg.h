@@ -184,6 +184,7 @@ int fdg_gather(fdg_ctx* ctx, void* stream, const uint64_t* nodes_dev, const uint
  * LDG/STG kernel (also used for sharded tables and rows not a multiple of 16 B). */
 #define FDG_GATHER_TMA 0
 #define FDG_GATHER_LDG 1
+#define FDG_GATHER_TMA_WS 2 /* warp-specialised TMA: producer warp + consumer (hashing) warps */
 int fdg_set_gather_impl(int impl);
 /* Tuning knobs (process-wide): "gather_impl" (FDG_GATHER_*), "gather_evict_first"
  * (0/1: L2 evict-first hints on the gather stream), "l2_persist_mb" (L2 set-aside
@@ -256,6 +257,10 @@ int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, 
                      uint64_t n_batches, fdg_batch_counts* records_host, float* extract_ms, float* elapsed_ms);
 /* Device batch records of the last run, [first, first+n). */
 int fdg_pipeline_records(fdg_pipeline* p, uint64_t first, uint64_t n, fdg_batch_counts* out);
+/* Extraction intervals of the last run (which must have passed extract_ms): start/end of
+ * batch j's extraction launches in ms from the start of the run (one device timeline, so
+ * launches alternating over the two extraction streams can be unioned). */
+int fdg_pipeline_extract_times(fdg_pipeline* p, uint64_t first, uint64_t n, float* start_ms, float* end_ms);
 
 /* ---- tracing: per-launch CUDA-event timeline (DurationCounter analogue, common.hpp:240-260) */
 int fdg_trace_enable(int on);          /* clears previous records when turning on */

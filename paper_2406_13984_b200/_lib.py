@@ -111,6 +111,7 @@ SIGNATURES = {
     "fdg_pipeline_destroy": (ci, [vp]),
     "fdg_pipeline_run": (ci, [vp, vp, ci, vp, u64, vp, vp, C.POINTER(C.c_float)]),
     "fdg_pipeline_records": (ci, [vp, u64, u64, vp]),
+    "fdg_pipeline_extract_times": (ci, [vp, u64, u64, vp, vp]),
     "fdg_pipeline_get_config": (ci, [vp, C.POINTER(PipelineConfig)]),
     "fdg_partition_epoch": (ci, [vp, u64, u64, u64, vp]),
     "fdg_batch_seed": (u64, [u64, u64, u64]),

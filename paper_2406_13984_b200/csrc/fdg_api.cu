@@ -397,7 +397,8 @@ int fdg_gather(fdg_ctx* c, void* st, const uint64_t* nodes, const uint32_t* n_de
 }
 
 int fdg_set_gather_impl(int impl) {
-    if (impl != FDG_GATHER_TMA && impl != FDG_GATHER_LDG) return fail(FDG_INVALID_ARG, "unknown gather impl");
+    if (impl != FDG_GATHER_TMA && impl != FDG_GATHER_LDG && impl != FDG_GATHER_TMA_WS)
+        return fail(FDG_INVALID_ARG, "unknown gather impl");
     g_gather_impl = impl;
     return FDG_OK;
 }
@@ -418,6 +419,25 @@ int fdg_set_option(const char* key, int64_t v) {
         return FDG_OK;
     }
     if (k == "hash_clear") { g_hash_clear = v != 0; return FDG_OK; }
+    if (k == "hash_keep") { g_hash_keep = v != 0; return FDG_OK; }
+    if (k == "gather_dynamic") { g_gather_dynamic = v != 0; return FDG_OK; }
+    if (k == "hash_kernel") { g_hash_kernel = v; return FDG_OK; }
+    if (k == "checksum_impl") {
+        if (v < -1 || v > FDG_GATHER_TMA_WS) return fail(FDG_INVALID_ARG, "checksum_impl must be -1 or a gather impl");
+        g_checksum_impl = v;
+        return FDG_OK;
+    }
+    if (k == "ws_stg") { g_ws_stg = v != 0; return FDG_OK; }
+    if (k == "ws_hashers") {
+        if (v < 1 || v > 31) return fail(FDG_INVALID_ARG, "ws_hashers must be in [1, 31]");
+        g_ws_hashers = int(v);
+        return FDG_OK;
+    }
+    if (k == "extract_streams") {
+        if (v < 1 || v > 2) return fail(FDG_INVALID_ARG, "extract_streams must be 1 or 2");
+        g_extract_streams = v;
+        return FDG_OK;
+    }
     if (k == "hash_load_pct") {
         if (v < 10 || v > 70) return fail(FDG_INVALID_ARG, "hash_load_pct must be in [10, 70]");
         g_hash_load_pct = v;
@@ -435,6 +455,13 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "gather_ctas_per_sm") *v = g_gather_ctas_per_sm;
     else if (k == "sampler_ctas_per_sm") *v = g_sampler_ctas_per_sm;
     else if (k == "hash_clear") *v = g_hash_clear;
+    else if (k == "hash_keep") *v = g_hash_keep;
+    else if (k == "gather_dynamic") *v = g_gather_dynamic;
+    else if (k == "hash_kernel") *v = g_hash_kernel;
+    else if (k == "checksum_impl") *v = g_checksum_impl;
+    else if (k == "ws_hashers") *v = g_ws_hashers;
+    else if (k == "ws_stg") *v = g_ws_stg;
+    else if (k == "extract_streams") *v = g_extract_streams;
     else return fail(FDG_INVALID_ARG, "unknown option " + k);
     return FDG_OK;
 }

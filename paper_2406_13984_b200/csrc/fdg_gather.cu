@@ -14,6 +14,9 @@
 // k_gather_hash additionally folds trainer_step's checksum
 // sum_i hash_bytes64(row_i) (common.hpp:88-105): a warp stages 32 rows in
 // shared memory and each lane then runs one row's sequential splitmix chain.
+#include <algorithm>
+#include <atomic>
+
 #include "fdg_internal.cuh"
 
 namespace fdg {
@@ -111,6 +114,79 @@ __global__ void __launch_bounds__(512) k_gather16(const uint64_t* __restrict__ n
     }
 }
 
+// Dynamically scheduled variant: CTAs claim units of kUnroll * 512 * kDynIters
+// chunks (64 KB) from a per-launch counter, so CTAs that become resident late
+// (the SMs are shared with the samplers' kernels) take less of the work instead
+// of stretching the launch. The last CTA to finish resets the counter pair.
+constexpr int kDynIters = 2;
+constexpr uint32_t kDynRing = 64;
+__device__ uint32_t g_dyn_ctr[2 * kDynRing];
+
+// Counter pair for one dynamically scheduled launch (a ring, so launches in flight
+// on different streams never share one). nullptr on failure.
+uint32_t* dyn_counter() {
+    static uint32_t* ring = nullptr;
+    static std::atomic<uint32_t> next{0};
+    if (!ring && cudaGetSymbolAddress((void**)&ring, g_dyn_ctr) != cudaSuccess) return nullptr;
+    return ring + 2 * (next.fetch_add(1) % kDynRing);
+}
+
+template <bool SHARDED>
+__global__ void __launch_bounds__(512) k_gather16_dyn(const uint64_t* __restrict__ nodes, const uint32_t* n_dev,
+                                                      uint64_t n_host, const uint32_t* status, TableRef t,
+                                                      FastDiv cdiv, uint32_t cpr, uint4* __restrict__ out,
+                                                      uint32_t* ctr) {
+    __shared__ uint32_t s_unit;
+    const bool skip = status && *status;
+    const uint64_t n = skip ? 0 : (n_dev ? *n_dev : n_host);
+    const uint32_t total = uint32_t(n * cpr);
+    constexpr uint32_t kStep = kUnroll * 512;
+    constexpr uint32_t kUnit = kStep * kDynIters;
+    const uint64_t pol = gather_policy(t.evict_first);
+    for (;;) {
+        if (threadIdx.x == 0) s_unit = atomicAdd(ctr, 1u);
+        __syncthreads();
+        const uint64_t u0l = uint64_t(s_unit) * kUnit;
+        __syncthreads();
+        if (u0l >= total) break;
+        const uint32_t u0 = uint32_t(u0l), u1 = uint32_t(min(uint64_t(total), u0l + kUnit));
+#pragma unroll 1
+        for (uint32_t b = u0; b < u1; b += kStep) {
+            if (b + kStep <= u1) {
+                uint4 v[kUnroll];
+                uint32_t cc[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    cc[u] = b + u * 512 + threadIdx.x;
+                    uint32_t row = cdiv.div(cc[u]);
+                    uint32_t col = cc[u] - row * cpr;
+                    v[u] = ldg_stream(reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, __ldg(nodes + row))) + col,
+                                      pol);
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) stg_stream(out + cc[u], v[u], pol);
+            } else {
+                for (uint32_t c = b + threadIdx.x; c < u1; c += 512) {
+                    uint32_t row = cdiv.div(c);
+                    uint32_t col = c - row * cpr;
+                    stg_stream(out + c,
+                               ldg_stream(reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, __ldg(nodes + row))) + col,
+                                          pol),
+                               pol);
+                }
+            }
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // every CTA has claimed past the end
+            ctr[0] = 0;
+            ctr[1] = 0;
+            __threadfence();
+        }
+    }
+}
+
 // 4-byte fallback for rows that are not a multiple of 16 bytes.
 template <bool SHARDED>
 __global__ void k_gather4(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
@@ -190,6 +266,167 @@ __global__ void __launch_bounds__(kH16Warps * 32, 2)
 #pragma unroll
     for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
+}
+
+// Warp-specialised gather + checksum (LDG): Wc copy warps move 32-row groups
+// table -> X with coalesced 16-byte loads/stores (the flattened (row, part) items
+// of a group are contiguous in X) and stage each group in a shared-memory slot; Wh
+// hash warps fold the staged rows into trainer_step's checksum, two groups per
+// warp so every lane runs two independent splitmix chains (hash_bytes64 is a
+// serial chain per row, common.hpp:88-105: ILP comes from rows, not words).
+// Groups are striped statically over CTAs (group = blockIdx.x + k * gridDim.x).
+// Slot hand-off uses monotonic sequence words in shared memory (filled[s] = k + 1
+// after group k is staged, freed[s] = k + 1 after it is hashed): with many copy
+// warps sharing the ring, a waiter can be several laps ahead, which an mbarrier's
+// phase parity cannot tell apart.
+constexpr int kWsCopyWarps = 20, kWsHashWarps = 4, kWsBatch = 8;
+
+__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
+                 : "=r"(v)
+                 : "r"(uint32_t(__cvta_generic_to_shared(p)))
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(uint32_t(__cvta_generic_to_shared(p))), "r"(v)
+                 : "memory");
+}
+// lane 0 polls; the warp leaves together (syncwarp orders the other lanes after it)
+__device__ __forceinline__ void wait_seq(const uint32_t* p, uint32_t want) {
+    if ((threadIdx.x & 31) == 0)
+        while (int32_t(ld_acquire_cta(p) - want) < 0) __nanosleep(20);
+    __syncwarp();
+}
+
+template <bool SHARDED, bool ALIAS>
+__global__ void __launch_bounds__((kWsCopyWarps + kWsHashWarps) * 32, 1)
+    k_gather_hash_ws(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
+                     const uint32_t* status, TableRef t, char* __restrict__ out, uint64_t* checksum, uint32_t D) {
+    extern __shared__ __align__(16) char ws_smem[];
+    const uint32_t rb = t.row_bytes, rstride = rb + 16, cpr = rb >> 4;
+    const uint32_t slot_bytes = 32 * rstride;
+    uint32_t* filled = reinterpret_cast<uint32_t*>(ws_smem + size_t(D) * slot_bytes);
+    uint32_t* freed = filled + D;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool skip = status && *status;
+    const uint64_t n = skip ? 0 : (n_dev ? *n_dev : n_host);
+    const uint64_t groups = (n + 31) / 32;
+    const uint64_t nk = blockIdx.x < groups ? (groups - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    for (uint32_t d = threadIdx.x; d < D; d += blockDim.x) {
+        filled[d] = 0;
+        freed[d] = 0;
+    }
+    __syncthreads();
+    const uint64_t pol = gather_policy(t.evict_first);
+    if (warp < kWsCopyWarps) {  // ---- copy warps
+        uint64_t k = warp;
+        uint64_t my_node = 0;
+        if (k < nk) {
+            const uint64_t r = (blockIdx.x + k * gridDim.x) * 32 + lane;
+            my_node = r < n ? nodes[r] : 0;
+        }
+        for (; k < nk; k += kWsCopyWarps) {
+            const uint64_t g = blockIdx.x + k * gridDim.x;
+            const uint32_t rows = uint32_t(n - g * 32 < 32 ? n - g * 32 : 32);
+            const uint64_t nk2 = k + kWsCopyWarps;  // next group's node ids load under this group
+            uint64_t next_node = 0;
+            if (nk2 < nk) {
+                const uint64_t r = (blockIdx.x + nk2 * gridDim.x) * 32 + lane;
+                next_node = r < n ? nodes[r] : 0;
+            }
+            const uint32_t s = uint32_t(k % D);
+            char* slot = ws_smem + size_t(s) * slot_bytes;
+            const uint32_t items = rows * cpr;
+            bool waited = false;
+            for (uint32_t i0 = 0; i0 < items; i0 += 32 * kWsBatch) {
+                uint4 v[kWsBatch];
+#pragma unroll
+                for (int j = 0; j < kWsBatch; ++j) {
+                    const uint32_t i = i0 + j * 32 + lane;
+                    const uint32_t r = i / cpr;
+                    const uint64_t node = __shfl_sync(0xffffffffu, my_node, int(r < 32 ? r : 0));
+                    if (i < items) {
+                        const char* src = ALIAS ? t.base + node * rb : row_ptr<SHARDED>(t, node);
+                        v[j] = ldg_stream(reinterpret_cast<const uint4*>(src) + (i - r * cpr), pol);
+                    }
+                }
+                if (!waited) {  // group k - D (the slot's previous tenant) has been hashed
+                    if (k >= D) wait_seq(&freed[s], uint32_t(k - D + 1));
+                    waited = true;
+                }
+#pragma unroll
+                for (int j = 0; j < kWsBatch; ++j) {
+                    const uint32_t i = i0 + j * 32 + lane;
+                    if (i < items) {
+                        const uint32_t r = i / cpr, p = i - r * cpr;
+                        if (!ALIAS && out) stg_stream(reinterpret_cast<uint4*>(out + g * 32 * rb) + i, v[j], pol);
+                        *reinterpret_cast<uint4*>(slot + r * rstride + p * 16) = v[j];
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) st_release_cta(&filled[s], uint32_t(k + 1));
+            my_node = next_node;
+        }
+    } else {  // ---- hash warps: groups (k, k + 1) for k = 2 hw, 2 hw + 2 Wh, ...
+        const uint32_t hw = warp - kWsCopyWarps;
+        uint64_t sum = 0;
+        const uint64_t seed = 0x27d4eb2f165667c5ull ^ (uint64_t(rb) * 0x9e3779b97f4a7c15ull);
+        for (uint64_t k = 2 * uint64_t(hw); k < nk; k += 2 * kWsHashWarps) {
+            const bool two = k + 1 < nk;
+            const uint32_t sa = uint32_t(k % D), sb = uint32_t((k + 1) % D);
+            const uint64_t ga = blockIdx.x + k * gridDim.x, gb = ga + gridDim.x;
+            const uint32_t ra = uint32_t(n - ga * 32 < 32 ? n - ga * 32 : 32);
+            const uint32_t rb2 = two ? uint32_t(n - gb * 32 < 32 ? n - gb * 32 : 32) : 0;
+            wait_seq(&filled[sa], uint32_t(k + 1));
+            if (two) wait_seq(&filled[sb], uint32_t(k + 2));
+            const uint4* pa = reinterpret_cast<const uint4*>(ws_smem + size_t(sa) * slot_bytes + lane * rstride);
+            const uint4* pb = reinterpret_cast<const uint4*>(ws_smem + size_t(sb) * slot_bytes + lane * rstride);
+            uint64_t ha = seed, hb = seed;
+            const bool la = lane < int(ra), lb = lane < int(rb2);
+            for (uint32_t q = 0; q < cpr; ++q) {
+                const uint4 wa = la ? pa[q] : make_uint4(0, 0, 0, 0);
+                const uint4 wb = lb ? pb[q] : make_uint4(0, 0, 0, 0);
+                ha = splitmix64(ha ^ (uint64_t(wa.y) << 32 | wa.x));
+                hb = splitmix64(hb ^ (uint64_t(wb.y) << 32 | wb.x));
+                ha = splitmix64(ha ^ (uint64_t(wa.w) << 32 | wa.z));
+                hb = splitmix64(hb ^ (uint64_t(wb.w) << 32 | wb.z));
+            }
+            if (la) sum += splitmix64(ha);
+            if (lb) sum += splitmix64(hb);
+            __syncwarp();  // every lane's shared reads of both slots are done
+            if (lane == 0) {
+                st_release_cta(&freed[sa], uint32_t(k + 1));
+                if (two) st_release_cta(&freed[sb], uint32_t(k + 2));
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
+    }
+}
+
+template <bool ALIAS>
+int launch_hash_ws(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                   const uint32_t* status, const TableRef& t, char* out, uint64_t* checksum, bool sharded) {
+    constexpr size_t kBudget = 200 * 1024;
+    const size_t slot = 32 * size_t(c.row_bytes + 16) + 8;  // + filled/freed words
+    const uint32_t D = uint32_t(std::min<size_t>(24, kBudget / slot));
+    if (D < 4) return fail(FDG_INVALID_ARG, "gather: row too large for the warp-specialised checksum");
+    const size_t smem = D * slot;
+    static bool attr[3] = {false, false, false};
+    auto kfn = ALIAS ? k_gather_hash_ws<false, true> : (sharded ? k_gather_hash_ws<true, false>
+                                                                 : k_gather_hash_ws<false, false>);
+    const int which = ALIAS ? 2 : int(sharded);
+    if (!attr[which]) {
+        FDG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBudget)));
+        attr[which] = true;
+    }
+    kfn<<<c.sm_count, (kWsCopyWarps + kWsHashWarps) * 32, smem, st>>>(nodes, n_dev, n_host, status, t, out, checksum, D);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
 }
 
 constexpr int kHashWarps = 4;
@@ -280,7 +517,10 @@ TableRef table_ref(const Ctx& c) {
 // isolation and never slower inside the pipeline (profiles/README.md).
 int g_gather_impl = FDG_GATHER_LDG;
 int g_gather_evict_first = 1;
-int g_gather_ctas_per_sm = 2;
+int g_gather_ctas_per_sm = 1;
+int64_t g_gather_dynamic = 1;
+int64_t g_hash_kernel = 1;  // 1: striped LDG k_gather_hash16, 2: warp-specialised k_gather_hash_ws
+int64_t g_checksum_impl = FDG_GATHER_TMA;  // measured best inside the pipeline
 
 int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
                         uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status) {
@@ -288,18 +528,26 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
     TableRef t = table_ref(c);
     const bool sharded = c.n_shards > 1;
     if (n_bound == 0) return FDG_OK;
-    if (g_gather_impl == FDG_GATHER_TMA && out &&
+    const int impl = (checksum && g_checksum_impl >= 0) ? int(g_checksum_impl) : g_gather_impl;
+    if (impl == FDG_GATHER_TMA_WS && launch_gather_ws(c, st, nodes, n_dev, n_host, out, checksum, status,
+                                                      dyn_counter()) == FDG_OK)
+        return FDG_OK;
+    if (impl == FDG_GATHER_TMA && out &&
         launch_gather_tma(c, st, nodes, n_dev, n_host, out, checksum, status) == FDG_OK)
-        return FDG_OK;  // rows that do not suit the TMA path fall through to the LDG kernels
+        return FDG_OK;  // rows that do not suit the TMA paths fall through to the LDG kernels
     if (checksum && c.row_bytes % 16 == 0) {
         uint64_t groups = (n_bound + 31) / 32;
         int blocks = int(std::min<uint64_t>((groups + kH16Warps - 1) / kH16Warps, uint64_t(c.sm_count) * 2));
-        if (sharded)
+        if (g_hash_kernel == 2 && c.row_bytes <= 2048) {
+            FDG_TRY(launch_hash_ws<false>(c, st, nodes, n_dev, n_host, status, t, static_cast<char*>(out), checksum,
+                                          sharded));
+        } else if (sharded) {
             k_gather_hash16<true, false><<<blocks, kH16Warps * 32, 0, st>>>(nodes, n_dev, n_host, status, t,
                                                                           static_cast<char*>(out), checksum);
-        else
+        } else {
             k_gather_hash16<false, false><<<blocks, kH16Warps * 32, 0, st>>>(nodes, n_dev, n_host, status, t,
                                                                            static_cast<char*>(out), checksum);
+        }
         FDG_CUDA(cudaGetLastError());
         return FDG_OK;
     }
@@ -325,7 +573,16 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
         d.init(cpr);
         uint64_t total = n_bound * cpr;
         int blocks = int(std::min<uint64_t>((total + 511) / 512, uint64_t(c.sm_count) * g_gather_ctas_per_sm));
-        if (sharded)
+        if (g_gather_dynamic) {
+            uint32_t* ctr = dyn_counter();
+            if (!ctr) return cuda_fail(cudaGetLastError(), "cudaGetSymbolAddress(g_dyn_ctr)", __FILE__, __LINE__);
+            if (sharded)
+                k_gather16_dyn<true><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr,
+                                                             static_cast<uint4*>(out), ctr);
+            else
+                k_gather16_dyn<false><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr,
+                                                              static_cast<uint4*>(out), ctr);
+        } else if (sharded)
             k_gather16<true><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr, static_cast<uint4*>(out));
         else
             k_gather16<false><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr, static_cast<uint4*>(out));
@@ -359,8 +616,12 @@ int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, con
     if (c.row_bytes % 16 == 0) {
         uint64_t groups = (std::max<uint64_t>(n_host, 1) + 31) / 32;
         int blocks = int(std::min<uint64_t>((groups + kH16Warps - 1) / kH16Warps, uint64_t(c.sm_count) * 2));
-        k_gather_hash16<false, true><<<blocks, kH16Warps * 32, 0, st>>>(reinterpret_cast<const uint64_t*>(alias),
-                                                                       n_dev, n_host, status, t, nullptr, checksum);
+        if (g_hash_kernel == 2 && c.row_bytes <= 2048)
+            FDG_TRY(launch_hash_ws<true>(c, st, reinterpret_cast<const uint64_t*>(alias), n_dev, n_host, status, t,
+                                         nullptr, checksum, false));
+        else
+            k_gather_hash16<false, true><<<blocks, kH16Warps * 32, 0, st>>>(
+                reinterpret_cast<const uint64_t*>(alias), n_dev, n_host, status, t, nullptr, checksum);
         FDG_CUDA(cudaGetLastError());
         return FDG_OK;
     }

@@ -104,10 +104,19 @@ int launch_gather(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const ui
 extern int g_gather_impl;  // FDG_GATHER_TMA (default) or FDG_GATHER_LDG
 extern int g_gather_evict_first;
 extern int g_gather_ctas_per_sm;
+extern int64_t g_gather_dynamic;
+extern int64_t g_hash_kernel;
+extern int64_t g_checksum_impl;  // gather impl for the fused-checksum path (-1: same as g_gather_impl)
+extern int g_ws_hashers;
+extern int g_ws_stg;
+int launch_gather_ws(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                     void* out, uint64_t* checksum, const uint32_t* status, uint32_t* ctr);  // fused gather+checksum kernel variant (A/B)  // k_gather16_dyn (atomic work claiming) instead of a fixed grid-stride split
 extern int64_t g_l2_persist_mb;
 extern int64_t g_hash_load_pct;
 extern int64_t g_sampler_ctas_per_sm;
-extern int64_t g_hash_clear;  // 1: clear batch hash tables with a fill kernel, 0: cudaMemsetAsync
+extern int64_t g_extract_streams;  // 1 or 2 extraction streams in the pipeline runner
+extern int64_t g_hash_clear;
+extern int64_t g_hash_keep;  // evict_last L2 policy on the batch hash  // 1: clear batch hash tables with a fill kernel, 0: cudaMemsetAsync
 int launch_gather_tma(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                       void* out, uint64_t* checksum, const uint32_t* status);
 int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, const int64_t* alias,

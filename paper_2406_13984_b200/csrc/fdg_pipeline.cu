@@ -44,6 +44,7 @@ struct fdg_pipeline {
     std::vector<cudaStream_t> sstream;
     std::vector<cudaStream_t> mstream;   // per-sampler MT prefetch streams
     cudaStream_t xstream = nullptr;
+    cudaStream_t xstream2 = nullptr;     // second extraction stream (plain gathers alternate)
     uint64_t cap = 0, max_nodes = 0;
     uint32_t nslots = 0;             // per-batch output slots (2 * S * G)
     std::vector<uint64_t*> nodes;
@@ -57,6 +58,8 @@ struct fdg_pipeline {
     uint64_t counts_cap = 0;
     std::vector<cudaEvent_t> tev;        // per-batch extract timing events (2 per batch)
     fdg_bm* bm = nullptr;
+    cudaEvent_t t0 = nullptr;            // start of the last run (timing base)
+    uint64_t timed_batches = 0;          // batches of the last run with extraction events
 };
 
 using namespace fdg;
@@ -69,6 +72,7 @@ void destroy(fdg_pipeline* p) {
     for (auto s : p->samplers) sampler_destroy(s);
     for (auto s : p->sstream) cudaStreamDestroy(s);
     if (p->xstream) cudaStreamDestroy(p->xstream);
+    if (p->xstream2) cudaStreamDestroy(p->xstream2);
     for (auto s : p->mstream) cudaStreamDestroy(s);
     for (auto v : p->nodes) cudaFree(v);
     for (auto v : p->edges) cudaFree(v);
@@ -79,6 +83,7 @@ void destroy(fdg_pipeline* p) {
     for (auto e : p->extracted) cudaEventDestroy(e);
     for (auto e : p->tev) cudaEventDestroy(e);
     if (p->counts) cudaFree(p->counts);
+    if (p->t0) cudaEventDestroy(p->t0);
     if (p->bm) fdg_bm_destroy(p->bm);
     delete p;
 }
@@ -95,7 +100,7 @@ int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers
     auto p = new fdg_pipeline();
     p->ctx = ctx;
     p->cfg = *cfg;
-    if (p->cfg.n_samplers == 0) p->cfg.n_samplers = 2;
+    if (p->cfg.n_samplers == 0) p->cfg.n_samplers = 6;  // measured best on B200 (5-8 plateau)
     if (p->cfg.prefetch_group == 0) p->cfg.prefetch_group = 16;
     if (p->cfg.group_batches == 0) p->cfg.group_batches = 1;
     p->cfg.group_batches = std::min<uint32_t>(p->cfg.group_batches, 8);
@@ -155,6 +160,11 @@ int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers
     p->max_nodes = mn;
     p->cap = std::max<uint64_t>(std::max(mn, me), 1);
     FDG_CUDA(cudaStreamCreateWithPriority(&p->xstream, cudaStreamNonBlocking, prio_lo));
+    // Plain gathers of consecutive batches alternate between two streams so the tail
+    // of one overlaps the head of the next (the buffer-manager path is stateful and
+    // stays on one stream).
+    if (!cfg->use_buffer_manager && g_extract_streams > 1)
+        FDG_CUDA(cudaStreamCreateWithPriority(&p->xstream2, cudaStreamNonBlocking, prio_lo));
     // one MT stream per sampler: prefetch launches of different samplers overlap
     for (uint32_t i = 0; i < S; ++i) {
         cudaStream_t st;
@@ -254,11 +264,14 @@ int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, 
         FDG_CUDA(cudaDeviceSynchronize());
         cudaProfilerStart();
     }
-    cudaEvent_t t0, t1;
-    FDG_CUDA(cudaEventCreate(&t0));
+    cudaEvent_t t1;
+    if (!p->t0) FDG_CUDA(cudaEventCreate(&p->t0));
+    cudaEvent_t t0 = p->t0;
+    p->timed_batches = 0;
     FDG_CUDA(cudaEventCreate(&t1));
     FDG_CUDA(cudaEventRecord(t0, p->xstream));
     for (uint32_t s = 0; s < S; ++s) FDG_CUDA(cudaStreamWaitEvent(p->sstream[s], t0, 0));
+    if (p->xstream2) FDG_CUDA(cudaStreamWaitEvent(p->xstream2, t0, 0));
     auto h0 = std::chrono::steady_clock::now();
     for (uint64_t g = 0; g < n_groups; ++g) {
         const uint64_t j0 = g * G, j1 = std::min<uint64_t>(j0 + G, n_batches);
@@ -295,24 +308,26 @@ int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, 
             consumed[s] += n;
             FDG_CUDA(cudaEventRecord(p->sampled[gslot], ss));
             FDG_CUDA(cudaStreamWaitEvent(p->xstream, p->sampled[gslot], 0));
+            if (p->xstream2) FDG_CUDA(cudaStreamWaitEvent(p->xstream2, p->sampled[gslot], 0));
         }
         for (uint64_t j = j0; j < j1; ++j) {
             const uint32_t slot = uint32_t(j % p->nslots);
             // extract-only diagnostics re-extract the batches sampled in the first groups
             const uint64_t src_j = do_sample ? j : (j % (sampled_groups * G));
             fdg_batch_counts* cnt = p->counts + src_j;
+            cudaStream_t xs = (p->xstream2 && (j & 1)) ? p->xstream2 : p->xstream;
             if (sample_only) {
-                FDG_CUDA(cudaEventRecord(p->extracted[slot], p->xstream));
+                FDG_CUDA(cudaEventRecord(p->extracted[slot], xs));
                 continue;
             }
-            FDG_TRACE("extract", p->xstream);
-            if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j], p->xstream));
+            FDG_TRACE("extract", xs);
+            if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j], xs));
             const uint32_t* n_dev = &cnt->n_nodes;
             uint64_t* cs = p->cfg.checksum ? &cnt->checksum : nullptr;
             void* X = p->X[j & 1];
             const uint32_t nslot = uint32_t(src_j % p->nslots);
             if (!p->bm) {
-                FDG_TRY(launch_gather_bound(*p->ctx, p->xstream, p->nodes[nslot], n_dev, p->cap, p->cap, X, cs,
+                FDG_TRY(launch_gather_bound(*p->ctx, xs, p->nodes[nslot], n_dev, p->cap, p->cap, X, cs,
                                             &cnt->status));
             } else {
                 FDG_TRY(fdg_bm_extract(p->bm, p->xstream, p->nodes[nslot], n_dev, p->cap, p->alias[j & 1], X, cs));
@@ -325,11 +340,10 @@ int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, 
                     FDG_CUDA(cudaEventRecord(p->extracted[(j - 1) % p->nslots], p->xstream));
                 }
             }
-            if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j + 1], p->xstream));
+            if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j + 1], xs));
             if (records_host)  // device -> host read of the batch record (counts + checksum)
-                FDG_CUDA(cudaMemcpyAsync(records_host + j, cnt, sizeof(fdg_batch_counts), cudaMemcpyDeviceToHost,
-                                         p->xstream));
-            if (!p->bm) FDG_CUDA(cudaEventRecord(p->extracted[slot], p->xstream));
+                FDG_CUDA(cudaMemcpyAsync(records_host + j, cnt, sizeof(fdg_batch_counts), cudaMemcpyDeviceToHost, xs));
+            if (!p->bm) FDG_CUDA(cudaEventRecord(p->extracted[slot], xs));
         }
     }
     if (p->bm && !sample_only) {  // drain: release the last batch
@@ -337,10 +351,11 @@ int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, 
         FDG_TRY(fdg_bm_release(p->bm, p->xstream, p->nodes[lj % p->nslots], &p->counts[lj].n_nodes, p->cap));
         FDG_CUDA(cudaEventRecord(p->extracted[(n_batches - 1) % p->nslots], p->xstream));
     }
-    for (uint32_t s = 0; s < S; ++s) {  // join the sampler streams
+    for (uint32_t s = 0; s <= S; ++s) {  // join the sampler streams and the second extract stream
+        if (s == S && !p->xstream2) break;
         cudaEvent_t e;
         FDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        FDG_CUDA(cudaEventRecord(e, p->sstream[s]));
+        FDG_CUDA(cudaEventRecord(e, s < S ? p->sstream[s] : p->xstream2));
         FDG_CUDA(cudaStreamWaitEvent(p->xstream, e, 0));
         cudaEventDestroy(e);
     }
@@ -356,8 +371,18 @@ int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, 
     if (extract_ms && !sample_only)
         for (uint64_t j = 0; j < n_batches; ++j)
             FDG_CUDA(cudaEventElapsedTime(extract_ms + j, p->tev[2 * j], p->tev[2 * j + 1]));
-    cudaEventDestroy(t0);
     cudaEventDestroy(t1);
+    if (extract_ms && !sample_only) p->timed_batches = n_batches;
+    return FDG_OK;
+}
+
+int fdg_pipeline_extract_times(fdg_pipeline* p, uint64_t first, uint64_t n, float* start_ms, float* end_ms) {
+    if (first + n > p->timed_batches)
+        return fail(FDG_INVALID_ARG, "pipeline_extract_times: range beyond the last run's timed batches");
+    for (uint64_t j = first; j < first + n; ++j) {
+        FDG_CUDA(cudaEventElapsedTime(start_ms + (j - first), p->t0, p->tev[2 * j]));
+        FDG_CUDA(cudaEventElapsedTime(end_ms + (j - first), p->t0, p->tev[2 * j + 1]));
+    }
     return FDG_OK;
 }
 

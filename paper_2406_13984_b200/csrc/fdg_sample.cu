@@ -57,8 +57,29 @@ struct FrontierBuf {
     uint32_t* draw_off;  // exclusive scan of (deg > f ? f : 0) within the layer
 };
 
-__device__ __forceinline__ uint32_t hslot(uint64_t key, uint32_t mask) {
-    return uint32_t((key * 0x9E3779B97F4A7C15ull) >> 32) & mask;
+// Home slot of `key` in a table of `size` entries (any size: Fibonacci hash, then
+// a multiply-shift range reduction instead of a power-of-two mask, so the table
+// can be sized to the batch's node bound and stay small enough for L2).
+__device__ __forceinline__ uint32_t hslot(uint64_t key, uint32_t size) {
+    return __umulhi(uint32_t((key * 0x9E3779B97F4A7C15ull) >> 32), size);
+}
+__device__ __forceinline__ uint32_t hnext(uint32_t h, uint32_t size) { return h + 1 == size ? 0 : h + 1; }
+
+// L2 residency of the batch hash: the clear and the intern pass's loads/stores carry
+// an evict_last policy so the table (one per sampler lane, reused every batch) stays
+// in L2 while the extraction streams ~1 GB per batch past it (atomics take no hint).
+__device__ __forceinline__ uint64_t keep_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ unsigned long long ld_keep(const unsigned long long* p, uint64_t pol) {
+    unsigned long long v;
+    asm volatile("ld.global.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_keep(unsigned long long* p, unsigned long long v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
 }
 
 // ---- batch hash: node id -> {pending min position | final local id} ----------------
@@ -68,11 +89,12 @@ template <typename IdT> struct HashTab;
 
 template <> struct HashTab<uint32_t> {
     unsigned long long* e;
-    uint32_t mask;
+    uint32_t size;
+    uint32_t keep;  // evict_last policy on loads / stores
     static constexpr unsigned long long kEmpty = ~0ull;
     __device__ __forceinline__ uint32_t insert(uint32_t key, uint32_t pos) const {
         const unsigned long long want = (uint64_t(key) << 32) | (kPend | pos);
-        uint32_t h = hslot(key, mask);
+        uint32_t h = hslot(key, size);
         for (;;) {
             // CAS straight away: one scattered L2 operation per new key
             unsigned long long cur = atomicCAS(e + h, kEmpty, want);
@@ -86,33 +108,35 @@ template <> struct HashTab<uint32_t> {
                 }
                 return h;
             }
-            h = (h + 1) & mask;
+            h = hnext(h, size);
         }
     }
     __device__ __forceinline__ void load(uint32_t h, uint32_t& key, uint32_t& val) const {
-        unsigned long long v = e[h];
+        unsigned long long v = keep ? ld_keep(e + h, keep_policy()) : e[h];
         key = uint32_t(v >> 32);
         val = uint32_t(v);
     }
     __device__ __forceinline__ void finalize(uint32_t h, uint32_t key, uint32_t local) const {
-        e[h] = (uint64_t(key) << 32) | local;
+        const unsigned long long v = (uint64_t(key) << 32) | local;
+        if (keep) st_keep(e + h, v, keep_policy());
+        else e[h] = v;
     }
 };
 
 template <> struct HashTab<uint64_t> {
     unsigned long long* keys;
     uint32_t* vals;
-    uint32_t mask;
+    uint32_t size;
     static constexpr unsigned long long kEmpty = ~0ull;
     __device__ __forceinline__ uint32_t insert(uint64_t key, uint32_t pos) const {
-        uint32_t h = hslot(key, mask);
+        uint32_t h = hslot(key, size);
         for (;;) {
             unsigned long long cur = atomicCAS(keys + h, kEmpty, (unsigned long long)key);
             if (cur == kEmpty || cur == key) {
                 atomicMin(vals + h, kPend | pos);
                 return h;
             }
-            h = (h + 1) & mask;
+            h = hnext(h, size);
         }
     }
     __device__ __forceinline__ void load(uint32_t h, uint64_t& key, uint32_t& val) const {
@@ -710,13 +734,20 @@ int64_t g_l2_persist_mb = 0;
 int64_t g_hash_load_pct = 50;
 int64_t g_sampler_ctas_per_sm = 16;
 int64_t g_hash_clear = 1;
+int64_t g_extract_streams = 2;
+int64_t g_hash_keep = 1;
 
 namespace {
 // Fill `n16` 16-byte words with all-ones (the empty hash entry), grid-stride.
-__global__ void __launch_bounds__(512) k_fill_ones(uint4* p, uint64_t n16) {
-    const uint4 v = make_uint4(~0u, ~0u, ~0u, ~0u);
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16; i += uint64_t(gridDim.x) * blockDim.x)
-        p[i] = v;
+__global__ void __launch_bounds__(512) k_fill_ones(uint4* p, uint64_t n16, int keep) {
+    const uint64_t pol = keep_policy();
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16; i += uint64_t(gridDim.x) * blockDim.x) {
+        if (keep)
+            asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %1, %1, %1}, %2;" ::"l"(p + i), "r"(~0u), "l"(pol)
+                         : "memory");
+        else
+            p[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    }
 }
 }  // namespace
 
@@ -725,7 +756,7 @@ cudaError_t clear_hash(void* base, uint64_t bytes, int sm_count, cudaStream_t st
     const uint64_t n16 = bytes / 16;
     const uint64_t want = (n16 + 511) / 512;
     const int grid = int(std::min<uint64_t>(want, uint64_t(sm_count) * 4));
-    k_fill_ones<<<std::max(grid, 1), 512, 0, st>>>((uint4*)base, n16);
+    k_fill_ones<<<std::max(grid, 1), 512, 0, st>>>((uint4*)base, n16, int(g_hash_keep));
     return cudaGetLastError();
 }
 
@@ -794,12 +825,6 @@ struct BatchArgs {  // one batch of a group launch
 
 namespace {
 
-uint64_t next_pow2(uint64_t v) {
-    uint64_t p = 1;
-    while (p < v) p <<= 1;
-    return p;
-}
-
 template <typename IdT>
 Work<IdT> make_work(Sampler& s, const Lane& ln, const BatchArgs& a) {
     Work<IdT> w;
@@ -812,7 +837,8 @@ Work<IdT> make_work(Sampler& s, const Lane& ln, const BatchArgs& a) {
         w.tab.keys = static_cast<unsigned long long*>(ln.hash);
         w.tab.vals = reinterpret_cast<uint32_t*>(static_cast<char*>(ln.hash) + uint64_t(s.hsize) * 8);
     }
-    w.tab.mask = s.hsize - 1;
+    w.tab.size = s.hsize;
+    if constexpr (sizeof(IdT) == 4) w.tab.keep = uint32_t(g_hash_keep);
     w.seeds = a.seeds;
     w.n_seeds = a.n_seeds;
     w.n_layers = s.n_layers;
@@ -1008,7 +1034,8 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
         return fail(FDG_INVALID_ARG, "sampler: batch bound exceeds 2^31 picks");
     }
     s->small_f = fmax <= uint32_t(kMaxF);
-    s->hsize = uint32_t(next_pow2(std::max<uint64_t>(s->max_nodes * 100 / uint64_t(g_hash_load_pct), 1024)));
+    // exact sizing (load factor g_hash_load_pct at the batch's node bound); any size works (hslot)
+    s->hsize = uint32_t((std::max<uint64_t>(s->max_nodes * 100 / uint64_t(g_hash_load_pct), 1024) + 31) & ~uint64_t(31));
     const uint32_t ib = ctx->idx_bytes;
     auto al = [](uint64_t b) { return (b + 255) & ~uint64_t(255); };
     s->hash_bytes = al(uint64_t(s->hsize) * (ib == 4 ? 8 : 12));

@@ -160,6 +160,12 @@ def set_option(key: str, value: int) -> None:
     check(lib().fdg_set_option(key.encode(), int(value)))
 
 
+def get_option(key: str) -> int:
+    v = C.c_int64()
+    check(lib().fdg_get_option(key.encode(), C.byref(v)))
+    return v.value
+
+
 def device_count() -> int:
     n = C.c_int()
     check(lib().fdg_device_count(C.byref(n)))
@@ -486,7 +492,7 @@ class Pipeline:
     (pipeline.hpp:325-543), batches pipelined across CUDA streams."""
 
     def __init__(self, topo: Topology, fanouts, batch_size: int = 1000, buffer_slots: int | None = None,
-                 checksum: bool = False, samplers: int = 2, group_batches: int = 1, prefetch_group: int = 16,
+                 checksum: bool = False, samplers: int = 6, group_batches: int = 1, prefetch_group: int = 16,
                  flags: int = 0):
         self.topo = topo
         cfg = _lib.PipelineConfig(batch_size=batch_size, n_samplers=samplers, prefetch_group=prefetch_group,
@@ -518,6 +524,12 @@ class Pipeline:
         out = np.zeros(n, COUNTS_DTYPE)
         check(lib().fdg_pipeline_records(self.ptr, 0, n, _p(out)))
         return out
+
+    def extract_times(self, n: int) -> tuple[np.ndarray, np.ndarray]:
+        """(start_ms, end_ms) of each batch's extraction in the last run (run with extract_ms)."""
+        a, b = np.zeros(n, np.float32), np.zeros(n, np.float32)
+        check(lib().fdg_pipeline_extract_times(self.ptr, 0, n, _p(a), _p(b)))
+        return a, b
 
     def host_enqueue_ms(self) -> float:
         cfg = _lib.PipelineConfig()

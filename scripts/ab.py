@@ -21,18 +21,22 @@ rng = np.array([L.fdg_batch_seed(0, 0, int(g)) for g in range(K)], np.uint64)
 seeds = DeviceBuffer.from_array(np.ascontiguousarray(order[:K * B]))
 f = np.ascontiguousarray(fan, np.uint32)
 defaults = {"gather_impl": 1, "gather_evict_first": 1, "l2_persist_mb": 0, "hash_load_pct": 50,
-            "hash_clear": 1, "sampler_ctas_per_sm": 16, "gather_ctas_per_sm": 2}
+            "hash_clear": 1, "sampler_ctas_per_sm": 16, "gather_ctas_per_sm": 1,
+            "extract_streams": 2, "hash_keep": 1, "gather_dynamic": 1, "hash_kernel": 1,
+            "ws_hashers": 8, "ws_stg": 1, "checksum_impl": 0}
 for spec in sys.argv[1:]:
     kv = dict(x.split("=") for x in spec.split(",") if x)
     S = int(kv.pop("S", 2))
     Gb = int(kv.pop("G", 1))
     mode = kv.pop("mode", "full")
+    cs = int(kv.pop("cs", 0))
     flags = int(kv.pop("flags", 0)) | {"full": 0, "sample": 1, "extract": 2}[mode]
     opts = dict(defaults)
     opts.update({k: int(v) for k, v in kv.items()})
     for k, v in opts.items():
         fd.featdrive.check(L.fdg_set_option(k.encode(), v))
-    cfg = _lib.PipelineConfig(batch_size=B, n_samplers=S, prefetch_group=16, write_x=1, flags=flags, group_batches=Gb)
+    cfg = _lib.PipelineConfig(batch_size=B, n_samplers=S, prefetch_group=16, write_x=1, flags=flags, group_batches=Gb,
+                              checksum=cs)
     p = C.c_void_p()
     fd.featdrive.check(L.fdg_pipeline_create(topo.ctx, f.ctypes.data_as(C.c_void_p), len(f), C.byref(cfg), C.byref(p)))
     ms = C.c_float()

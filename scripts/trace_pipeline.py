@@ -14,7 +14,7 @@ from paper_2406_13984_b200 import _lib  # noqa: E402
 from paper_2406_13984_b200.featdrive import DeviceBuffer  # noqa: E402
 
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-impl = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+impl = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 n, dim, avg, fan, B, t_ids, dtype, frac = bench.CONFIGS["papers"]
 L = fd.featdrive.lib()
 L.fdg_trace_enable.argtypes = [C.c_int]
@@ -57,7 +57,7 @@ for st, rs in chains.items():
     for r in rs:
         if r["name"] == "memset":
             cur = float(r["start_ms"])
-        elif r["name"] == "fix_src" and cur is not None:
+        elif r["name"] == f"intern{len(fan)}" and cur is not None:
             lat.append(float(r["end_ms"]) - cur)
             cur = None
 print(f"  sampler chain latency mean {np.mean(lat) * 1e3:.1f} us (n={len(lat)})")

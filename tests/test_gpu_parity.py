@@ -358,18 +358,46 @@ def test_pipeline_host_seeds_e2e(fd):
     L.fdg_host_free(rec.value)
 
 
-@pytest.mark.parametrize("impl", [0, 1])
-def test_gather_impls_agree(fd, port, impl):
-    """TMA bulk-copy gather and LDG gather: identical rows and checksums."""
+@pytest.mark.parametrize("impl", [0, 1, 2])
+@pytest.mark.parametrize("dim,rows", [(128, 50_000), (100, 33), (256, 1), (128, 0), (64, 70_001)])
+def test_gather_impls_agree(fd, port, impl, dim, rows):
+    """TMA bulk-copy, LDG and warp-specialised TMA gathers (dynamic work claiming on):
+    identical rows and checksums, including ragged chunk tails and empty batches."""
     n = 40_000
-    t = fd.Topology.generate(n, 128, 8, 9)
+    t = fd.Topology.generate(n, dim, 8, 9)
     table = t.download_rows(0, n)
-    nodes = np.random.RandomState(impl).randint(0, n, size=50_000).astype(np.uint64)
+    nodes = np.random.RandomState(impl + rows).randint(0, n, size=rows).astype(np.uint64)
     fd.set_option("gather_impl", impl)
+    fd.set_option("checksum_impl", -1)  # the fused checksum path follows gather_impl
     try:
-        x, cs = fd.gather(t, nodes, checksum=True)
-        np.testing.assert_array_equal(x, table[nodes.astype(np.int64)])
-        assert cs == port.checksum_rows(x)
-        np.testing.assert_array_equal(fd.gather(t, nodes), x)
+        for _ in range(3):  # repeated launches reuse the per-launch claim counters
+            x, cs = fd.gather(t, nodes, checksum=True)
+            np.testing.assert_array_equal(x, table[nodes.astype(np.int64)])
+            assert cs == port.checksum_rows(x)
+            np.testing.assert_array_equal(fd.gather(t, nodes), x)
     finally:
         fd.set_option("gather_impl", 1)
+        fd.set_option("checksum_impl", 0)
+
+
+@pytest.mark.parametrize("hk", [1, 2])
+@pytest.mark.parametrize("dim,rows", [(128, 50_000), (100, 33), (256, 1), (64, 70_001), (384, 4_097)])
+def test_checksum_kernels_agree(fd, port, hk, dim, rows):
+    """The LDG fused gather+checksum kernels (striped, warp-specialised):
+    identical rows and trainer checksums, ragged group tails included."""
+    n = 40_000
+    t = fd.Topology.generate(n, dim, 8, 9)
+    table = t.download_rows(0, n)
+    nodes = np.random.RandomState(hk + rows).randint(0, n, size=rows).astype(np.uint64)
+    old = fd.featdrive.get_option("hash_kernel")
+    fd.set_option("gather_impl", 1)
+    fd.set_option("checksum_impl", -1)
+    fd.set_option("hash_kernel", hk)
+    try:
+        for _ in range(2):
+            x, cs = fd.gather(t, nodes, checksum=True)
+            np.testing.assert_array_equal(x, table[nodes.astype(np.int64)])
+            assert cs == port.checksum_rows(x)
+    finally:
+        fd.set_option("hash_kernel", old)
+        fd.set_option("checksum_impl", 0)
