@@ -267,42 +267,44 @@ __device__ __forceinline__ uint4 ld_volatile4(const uint4* p) {
     return v;
 }
 
-// Warp 0: exclusive prefix of this tile's aggregate via decoupled look-back.
-__device__ Tri tri_lookback(uint32_t* flags, uint4* aggs, uint4* incls, uint32_t tile, Tri agg, uint32_t epoch,
-                            int lane) {
+// CTA-wide look-back (all kScanThreads threads): thread t inspects tile (j - t), so a
+// window of 256 predecessors is examined per step. Waits are for predecessors'
+// AGGREGATES only (published as soon as each tile's local scan is done), so the
+// wait is one tile's local work, not a serial chain of inclusive prefixes; the
+// nearest inclusive predecessor in the window cuts the sum short. The caller has
+// already published this tile's aggregate (flag E|1); this publishes the inclusive
+// (E|2) unless publish_incl is false (the caller must then do it).
+__device__ Tri tri_lookback_cta(uint32_t* flags, uint4* aggs, uint4* incls, uint32_t tile, uint32_t epoch) {
+    __shared__ int s_stop[kScanThreads / 32];
+    __shared__ Tri s_part[kScanThreads / 32];
     const uint32_t E = (epoch & 0x3FFFFFFFu) << 2;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     Tri excl{0, 0, 0};
-    if (tile == 0) {
-        if (lane == 0) {
-            incls[0] = make_uint4(agg.c, agg.p, agg.d, 0);
-            __threadfence();
-            atomicExch(flags, E | 2u);
-        }
-        return excl;
-    }
-    if (lane == 0) {
-        aggs[tile] = make_uint4(agg.c, agg.p, agg.d, 0);
-        __threadfence();
-        atomicExch(flags + tile, E | 1u);
-    }
-    int j = int(tile) - 1;
-    for (;;) {
-        int jj = j - lane;
-        uint32_t st = 2;
+    for (int64_t j = int64_t(tile) - 1; j >= 0; j -= kScanThreads) {
+        const int64_t jj = j - tid;
+        uint32_t st = 2;  // before tile 0: an inclusive boundary of value 0
         if (jj >= 0) {
-            uint32_t fl = ld_volatile(flags + jj);
-            st = (fl & ~3u) == E ? (fl & 3u) : 0u;
+            for (;;) {
+                const uint32_t fl = ld_volatile(flags + jj);
+                st = (fl & ~3u) == E ? (fl & 3u) : 0u;
+                if (st) break;
+                __nanosleep(32);
+            }
         }
-        if (__any_sync(0xffffffffu, st == 0)) continue;
-        uint32_t im = __ballot_sync(0xffffffffu, st == 2);
-        int stop = im ? __ffs(im) - 1 : 32;  // nearest inclusive predecessor in this window
+        // nearest inclusive predecessor: the smallest tid with st == 2
+        const uint32_t m = __ballot_sync(0xffffffffu, st == 2);
+        if (lane == 0) s_stop[warp] = m ? warp * 32 + __ffs(m) - 1 : kScanThreads;
+        __syncthreads();
+        int stop = kScanThreads;
+#pragma unroll
+        for (int w = 0; w < kScanThreads / 32; ++w) stop = min(stop, s_stop[w]);
         __threadfence();
         Tri v{0, 0, 0};
-        if (lane < stop) {
-            uint4 a = ld_volatile4(aggs + jj);
+        if (tid < stop) {
+            const uint4 a = ld_volatile4(aggs + jj);
             v = Tri{a.x, a.y, a.z};
-        } else if (lane == stop && jj >= 0) {
-            uint4 a = ld_volatile4(incls + jj);
+        } else if (tid == stop && jj >= 0) {
+            const uint4 a = ld_volatile4(incls + jj);
             v = Tri{a.x, a.y, a.z};
         }
 #pragma unroll
@@ -311,15 +313,12 @@ __device__ Tri tri_lookback(uint32_t* flags, uint4* aggs, uint4* incls, uint32_t
             v.p += __shfl_xor_sync(0xffffffffu, v.p, o);
             v.d += __shfl_xor_sync(0xffffffffu, v.d, o);
         }
-        excl = excl + v;
-        if (stop < 32) break;
-        j -= 32;
-    }
-    if (lane == 0) {
-        Tri tot = excl + agg;
-        incls[tile] = make_uint4(tot.c, tot.p, tot.d, 0);
-        __threadfence();
-        atomicExch(flags + tile, E | 2u);
+        if (lane == 0) s_part[warp] = v;
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < kScanThreads / 32; ++w) excl = excl + s_part[w];
+        __syncthreads();  // s_stop / s_part reused by the next step
+        if (stop < kScanThreads) break;
     }
     return excl;
 }
@@ -424,6 +423,7 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
         if (lane == 31) s_rowx[r] = wi;  // row total for now
     }
     __syncthreads();
+    const uint32_t E = (epoch & 0x3FFFFFFFu) << 2;
     if (tid == 0) {
         Tri run{0, 0, 0};
         for (int r = 0; r < kScanItems; ++r) {
@@ -432,6 +432,10 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
             run = run + t;
         }
         s_agg = run;
+        // publish the aggregate at once: successors' look-backs wait only for this
+        W.tile_agg[tile] = make_uint4(run.c, run.p, run.d, 0);
+        __threadfence();
+        atomicExch(W.tile_flag + tile, E | 1u);
     }
     __syncthreads();
     Tri ex[kScanItems];  // tile-relative exclusive prefix of item k
@@ -447,10 +451,15 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
         __threadfence();
         __syncthreads();
     }
-    if (warp == 0) {
+    {
         const Tri agg = s_agg;
-        Tri excl = tri_lookback(W.tile_flag, W.tile_agg, W.tile_incl, tile, agg, epoch, lane);
-        if (lane == 0) {
+        const Tri excl = tri_lookback_cta(W.tile_flag, W.tile_agg, W.tile_incl, tile, epoch);
+        if (tid == 0) {
+            // ranks (above) and the aggregate are visible before the inclusive flag
+            const Tri tot = excl + agg;
+            W.tile_incl[tile] = make_uint4(tot.c, tot.p, tot.d, 0);
+            __threadfence();
+            atomicExch(W.tile_flag + tile, E | 2u);
             s_excl = excl;
             if (tile == ntiles - 1) {  // totals of this pass -> the batch record
                 Tri tot = excl + agg;
@@ -468,7 +477,6 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
     }
     __syncthreads();
     const Tri base = s_excl;
-    const uint32_t E = (epoch & 0x3FFFFFFFu) << 2;
     const FrontierBuf fr = W.fr[q & 1];
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
