@@ -255,6 +255,18 @@ int fdg_pipeline_destroy(fdg_pipeline* p);
  * elapsed_ms = device time of the whole run. Synchronises before returning. */
 int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, const uint64_t* rng_seeds,
                      uint64_t n_batches, fdg_batch_counts* records_host, float* extract_ms, float* elapsed_ms);
+/* As fdg_pipeline_run, but the seed list holds n_seeds_total seeds: batch j takes
+ * [j*batch_size, min((j+1)*batch_size, n_seeds_total)) -- the last chunk of
+ * partition_epoch (sampling.hpp:57-70) may be short. */
+int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, uint64_t n_seeds_total,
+                            const uint64_t* rng_seeds, uint64_t n_batches, fdg_batch_counts* records_host,
+                            float* extract_ms, float* elapsed_ms);
+/* Sampling stage time of the last run (which must have passed extract_ms): the sum over
+ * launch groups of the sampler stream's busy interval (sample_busy of EpochStats). */
+int fdg_pipeline_sample_times(fdg_pipeline* p, uint64_t* n_groups, float* busy_ms);
+/* Buffer-manager counters of a pipeline created with use_buffer_manager (cumulative
+ * over its runs; FDG_NOT_LOADED without a buffer manager). */
+int fdg_pipeline_bm_stats(fdg_pipeline* p, fdg_bm_stats* out);
 /* Device batch records of the last run, [first, first+n). */
 int fdg_pipeline_records(fdg_pipeline* p, uint64_t first, uint64_t n, fdg_batch_counts* out);
 /* Extraction intervals of the last run (which must have passed extract_ms): start/end of

@@ -10,6 +10,9 @@
 //   featdrive::extract::Extractor        -> featdrive_gpu::extract::Extractor
 //   featdrive::pipeline::trainer_step    -> featdrive_gpu::pipeline::trainer_step (GPU checksum)
 //   PipelineSession::batch_seed          -> featdrive_gpu::pipeline::batch_seed
+//   pipeline::PipelineSession / EpochStats -> featdrive_gpu::pipeline::PipelineSession / EpochStats
+//                                            (run_epoch, run_epoch_multi, run_sync_reference,
+//                                             the same per-epoch JSON document, stats.hpp:96-146)
 //
 // Exceptions: FDG_OUT_OF_RANGE -> std::out_of_range, FDG_INVALID_ARG ->
 // std::invalid_argument, FDG_INVARIANT -> InvariantViolation (std::logic_error),
@@ -18,11 +21,16 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <exception>
 #include <memory>
+#include <mutex>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "fdg.h"
@@ -269,6 +277,386 @@ inline std::uint64_t trainer_step(const graph::SampledBatch& batch, const extrac
     fdg_free(cs);
     return sum;
 }
+// ------------------------------------------------------------------ session ----
+// PipelineSession (pipeline.hpp:127-299) on the GPU runner (fdg_pipeline_*): one
+// persistent pipeline (sampler streams + extraction + optional buffer manager) per
+// worker segment, reused across epochs like the reference's per-worker buffer.
 
-}  // namespace pipeline
+inline std::uint64_t splitmix64(std::uint64_t x) {  // common.hpp:77-82
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+inline std::uint64_t hash_combine(std::uint64_t a, std::uint64_t b) {  // common.hpp:84-86
+    return splitmix64(a ^ (b + 0x9e3779b97f4a7c15ull + (a << 6) + (a >> 2)));
+}
+
+enum class RunMode { Async, SyncReference };
+
+/// pipeline.hpp:30-76. GPU meaning: num_samplers = concurrent sampler streams;
+/// num_extractors (N_e) only sizes the default slot count N_e * M_b, as in the
+/// reference; slots = kNoBuffer extracts by direct gather (no buffer manager).
+struct PipelineConfig {
+    static constexpr std::uint64_t kNoBuffer = ~0ull;
+    std::uint32_t num_samplers = 6;
+    std::uint32_t num_extractors = 4;
+    std::uint64_t batch_size = 1000;
+    graph::Fanouts fanouts{{10, 10, 10}};
+    std::uint64_t slots = 0;  // per-worker feature-buffer slots; 0 = N_e * M_b
+    RunMode mode = RunMode::Async;
+    std::uint32_t workers = 1;  // segments (concurrent pipelines on the topology's GPU)
+    std::uint32_t group_batches = 1;
+    bool verify = false;  // re-derive every batch on the non-pipelined path and compare
+
+    void validate() const {
+        if (num_samplers < 1 || num_extractors < 1)
+            throw std::invalid_argument("config: need at least one sampler and one extractor");
+        if (batch_size < 1) throw std::invalid_argument("config: batch_size must be >= 1");
+        if (workers < 1) throw std::invalid_argument("config: workers must be >= 1");
+        fanouts.validate();
+    }
+    std::uint64_t max_batch_nodes(std::uint64_t num_nodes) const {
+        return std::min(fanouts.max_batch_nodes(batch_size), num_nodes);
+    }
+};
+
+struct BatchRecord {  // stats.hpp:21-27
+    std::uint64_t batch_id = 0, seed_count = 0, node_count = 0, checksum = 0;
+    bool failed = false;
+};
+
+class PipelineError : public std::runtime_error {  // pipeline.hpp:84-93
+public:
+    PipelineError(std::string stage, const std::string& what)
+        : std::runtime_error("[" + stage + "] " + what), stage_(std::move(stage)) {}
+    const std::string& stage() const { return stage_; }
+
+private:
+    std::string stage_;
+};
+
+/// stats.hpp:47-146, same JSON document. Stage times: sample_busy = sampler-stream
+/// busy time, extract_busy = extraction (gather / buffer manager + fused trainer
+/// checksum) time, both from CUDA events; the GPU runner has no blocking queues, so
+/// the *_block and train/release fields are 0 (training is fused into extraction).
+struct EpochStats {
+    std::uint64_t epoch = 0;
+    std::uint32_t worker = 0;
+    std::string mode;
+    double wall_time_s = 0;
+    std::uint64_t batches_sampled = 0, batches_trained = 0, batches_failed = 0, batches_released = 0;
+    double sample_busy_s = 0, sample_block_s = 0;
+    double extract_busy_s = 0, extract_block_s = 0, extract_io_wait_s = 0;
+    double train_busy_s = 0, train_block_s = 0;
+    double release_busy_s = 0, release_block_s = 0;
+    std::uint64_t bytes_useful = 0, bytes_redundant = 0, bytes_requested = 0;
+    std::uint64_t read_requests = 0, nodes_loaded = 0, staging_hits = 0;
+    featbuf::BufferStats buffer;
+    std::uint64_t feature_buffer_bytes = 0, staging_bytes = 0, slot_count = 0;
+    std::uint64_t staging_borrows = 0, staging_cross_hits = 0;
+    std::vector<BatchRecord> batch_records;
+
+    std::string to_json() const {
+        std::string o;
+        auto num = [&](const char* k, double v, bool comma = true) {
+            char b[64];
+            std::snprintf(b, sizeof b, "\"%s\":%.17g%s", k, v, comma ? "," : "");
+            o += b;
+        };
+        auto u = [&](const char* k, std::uint64_t v, bool comma = true) {
+            o += "\"" + std::string(k) + "\":" + std::to_string(v) + (comma ? "," : "");
+        };
+        o += "{";
+        u("epoch", epoch);
+        u("worker", worker);
+        o += "\"mode\":\"" + mode + "\",";
+        num("wall_time_s", wall_time_s);
+        o += "\"batches\":{";
+        u("sampled", batches_sampled);
+        u("trained", batches_trained);
+        u("failed", batches_failed);
+        u("released", batches_released, false);
+        o += "},\"stage_time_s\":{";
+        num("sample_busy", sample_busy_s);
+        num("sample_block", sample_block_s);
+        num("extract_busy", extract_busy_s);
+        num("extract_block", extract_block_s);
+        num("extract_io_wait", extract_io_wait_s);
+        num("train_busy", train_busy_s);
+        num("train_block", train_block_s);
+        num("release_busy", release_busy_s);
+        num("release_block", release_block_s, false);
+        o += "},\"bytes\":{";
+        u("useful", bytes_useful);
+        u("redundant", bytes_redundant);
+        u("requested", bytes_requested, false);
+        o += "},\"reads\":{";
+        u("requests", read_requests);
+        u("nodes_loaded", nodes_loaded);
+        u("staging_hits", staging_hits, false);
+        o += "},\"buffer\":{";
+        u("hits", buffer.hits);
+        u("loads", buffer.loads);
+        u("waits", buffer.waits);
+        u("evictions", buffer.evictions);
+        u("takeovers", buffer.takeovers);
+        u("standby_len", buffer.standby_len, false);
+        o += "},\"memory\":{";
+        u("feature_buffer_bytes", feature_buffer_bytes);
+        u("staging_bytes", staging_bytes);
+        u("slot_count", slot_count);
+        u("staging_borrows", staging_borrows);
+        u("staging_cross_hits", staging_cross_hits, false);
+        o += "},\"batch_checksums\":[";
+        for (std::size_t i = 0; i < batch_records.size(); ++i) {
+            const auto& b = batch_records[i];
+            o += i ? ",{" : "{";
+            u("batch", b.batch_id);
+            u("seeds", b.seed_count);
+            u("nodes", b.node_count);
+            u("checksum", b.checksum);
+            o += std::string("\"failed\":") + (b.failed ? "true" : "false") + "}";
+        }
+        o += "]}";
+        return o;
+    }
+};
+
+class PipelineSession {
+public:
+    PipelineSession(const graph::Topology& topo, PipelineConfig cfg) : topo_(topo), cfg_(std::move(cfg)) {
+        cfg_.validate();
+        mb_ = cfg_.max_batch_nodes(topo_.num_nodes());
+        slots_ = cfg_.slots == PipelineConfig::kNoBuffer ? 0
+                 : cfg_.slots                            ? cfg_.slots
+                                                         : std::uint64_t(cfg_.num_extractors) * mb_;
+        // pipeline.hpp:137-141 refuses slots below its N_e * M_b reservation; the GPU
+        // runner holds at most two batches (the one extracted + the lag-1 release), so
+        // its reservation is 2 * M_b.
+        if (slots_ && slots_ < 2 * mb_)
+            throw std::invalid_argument("config: slots " + std::to_string(slots_) +
+                                        " below the deadlock reservation 2*M_b = " + std::to_string(2 * mb_));
+        for (std::uint32_t w = 0; w < cfg_.workers; ++w) {
+            fdg_pipeline_config pc{};
+            pc.batch_size = std::uint32_t(cfg_.batch_size);
+            pc.n_samplers = cfg_.num_samplers;
+            pc.use_buffer_manager = slots_ ? 1 : 0;
+            pc.buffer_slots = slots_;
+            pc.write_x = 1;
+            pc.checksum = 1;
+            pc.group_batches = cfg_.group_batches;
+            fdg_pipeline* p = nullptr;
+            check(fdg_pipeline_create(topo_.handle(), cfg_.fanouts.per_layer.data(),
+                                      std::uint32_t(cfg_.fanouts.per_layer.size()), &pc, &p));
+            pipes_.push_back(p);
+        }
+    }
+    ~PipelineSession() {
+        for (auto p : pipes_) fdg_pipeline_destroy(p);
+        if (sampler_) fdg_sampler_destroy(sampler_);
+    }
+    PipelineSession(const PipelineSession&) = delete;
+    PipelineSession& operator=(const PipelineSession&) = delete;
+
+    std::uint64_t max_batch_nodes() const { return mb_; }
+    std::uint64_t slots_per_worker() const { return slots_; }
+    const PipelineConfig& config() const { return cfg_; }
+
+    static std::uint64_t batch_seed(std::uint64_t seed, std::uint64_t epoch, std::uint64_t global_batch) {
+        return hash_combine(hash_combine(seed, epoch), global_batch);  // pipeline.hpp:295-298
+    }
+
+    EpochStats run_epoch(std::span<const NodeId> train_ids, std::uint64_t epoch, std::uint64_t seed) {
+        auto all = run_epoch_multi(train_ids, epoch, seed);
+        return std::move(all.front());
+    }
+
+    /// pipeline.hpp:185-259: contiguous chunk ranges per worker (sizes differ by at
+    /// most one), all workers concurrently; the root-cause error is rethrown.
+    std::vector<EpochStats> run_epoch_multi(std::span<const NodeId> train_ids, std::uint64_t epoch,
+                                            std::uint64_t seed) {
+        auto chunks = graph::partition_epoch({train_ids.begin(), train_ids.end()}, cfg_.batch_size,
+                                             hash_combine(seed, epoch));
+        const std::uint64_t total = chunks.size(), W = cfg_.workers;
+        std::vector<EpochStats> out(W);
+        std::vector<std::exception_ptr> err(W);
+        auto work = [&](std::uint32_t w) {
+            try {
+                const std::uint64_t base = total / W, rem = total % W;
+                const std::uint64_t lo = w * base + std::min<std::uint64_t>(w, rem);
+                const std::uint64_t hi = lo + base + (w < rem ? 1 : 0);
+                out[w] = run_segment(w, chunks, lo, hi, epoch, seed);
+            } catch (...) {
+                err[w] = std::current_exception();
+            }
+        };
+        if (W == 1) {
+            work(0);
+        } else {
+            std::vector<std::thread> th;
+            for (std::uint32_t w = 0; w < W; ++w) th.emplace_back(work, w);
+            for (auto& t : th) t.join();
+        }
+        for (auto& e : err)
+            if (e) std::rethrow_exception(e);
+        return out;
+    }
+
+    /// pipeline.hpp:263-293: sample -> extract (gather + checksum) one batch at a time,
+    /// synchronously, with no feature buffer.
+    EpochStats run_sync_reference(std::span<const NodeId> train_ids, std::uint64_t epoch, std::uint64_t seed) {
+        auto chunks = graph::partition_epoch({train_ids.begin(), train_ids.end()}, cfg_.batch_size,
+                                             hash_combine(seed, epoch));
+        EpochStats st;
+        st.epoch = epoch;
+        st.mode = "sync-reference";
+        const auto t0 = std::chrono::steady_clock::now();
+        const std::uint32_t rb = topo_.row_bytes();
+        for (std::uint64_t b = 0; b < chunks.size(); ++b) {
+            auto r = sync_batch(chunks[b], batch_seed(seed, epoch, b));
+            ++st.batches_sampled;
+            st.batch_records.push_back({b, chunks[b].size(), r.first, r.second, false});
+            st.bytes_useful += r.first * rb;
+            st.bytes_requested += r.first * rb;
+            st.read_requests += r.first;
+            st.nodes_loaded += r.first;
+            ++st.batches_trained;
+            ++st.batches_released;
+        }
+        st.wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return st;
+    }
+
+private:
+    // one batch on the non-pipelined path: (node count, trainer checksum)
+    std::pair<std::uint64_t, std::uint64_t> sync_batch(std::span<const NodeId> seeds, std::uint64_t rng_seed) {
+        std::lock_guard<std::mutex> lk(sync_mu_);  // one sync workspace, shared by verifying workers
+        if (!sampler_) {
+            check(fdg_sampler_create(topo_.handle(), std::uint32_t(cfg_.batch_size), cfg_.fanouts.per_layer.data(),
+                                     std::uint32_t(cfg_.fanouts.per_layer.size()), &sampler_));
+            std::uint64_t mn = 0, me = 0;
+            check(fdg_sampler_capacity(sampler_, &mn, &me));
+            cap_ = std::max<std::uint64_t>({mn, me, 1});
+            sbuf_ = std::make_unique<Dev>((8 + 8 + 8 + std::uint64_t(topo_.row_bytes())) * cap_ + 8 * cfg_.batch_size +
+                                          sizeof(fdg_batch_counts) + 512);
+        }
+        char* base = static_cast<char*>(sbuf_->p);
+        auto* seeds_d = reinterpret_cast<std::uint64_t*>(base);
+        auto* nodes_d = seeds_d + cfg_.batch_size;
+        auto* edges_d = reinterpret_cast<std::uint32_t*>(nodes_d + cap_);
+        auto* cs_d = reinterpret_cast<std::uint64_t*>(edges_d + 2 * cap_);
+        auto* cnt_d = reinterpret_cast<fdg_batch_counts*>(cs_d + 1);
+        void* x_d = reinterpret_cast<void*>((reinterpret_cast<std::uintptr_t>(cnt_d + 1) + 255) & ~std::uintptr_t(255));
+        check(fdg_memcpy_h2d(seeds_d, seeds.data(), seeds.size() * 8, nullptr));
+        check(fdg_sample_khop(sampler_, nullptr, seeds_d, std::uint32_t(seeds.size()), rng_seed, nodes_d, edges_d, cap_,
+                              cnt_d));
+        check(fdg_memset(cs_d, 0, 8, nullptr));
+        check(fdg_gather(topo_.handle(), nullptr, nodes_d, &cnt_d->n_nodes, cap_, x_d, cs_d));
+        fdg_batch_counts c{};
+        std::uint64_t cs = 0;
+        check(fdg_memcpy_d2h(&c, cnt_d, sizeof c, nullptr));
+        check(fdg_memcpy_d2h(&cs, cs_d, 8, nullptr));
+        check(fdg_stream_sync(nullptr));
+        if (c.status == FDG_OUT_OF_RANGE) throw std::out_of_range("sample_khop: seed out of range");
+        if (c.status) check(int(c.status));
+        return {c.n_nodes, cs};
+    }
+
+    EpochStats run_segment(std::uint32_t w, const std::vector<std::vector<NodeId>>& chunks, std::uint64_t lo,
+                           std::uint64_t hi, std::uint64_t epoch, std::uint64_t seed) {
+        EpochStats st;
+        st.epoch = epoch;
+        st.worker = w;
+        st.mode = "async";
+        const std::uint32_t rb = topo_.row_bytes();
+        st.slot_count = slots_;
+        st.feature_buffer_bytes = slots_ * rb;
+        const std::uint64_t n = hi - lo;
+        if (n == 0) return st;
+        fdg_pipeline* p = pipes_[w];
+        std::vector<NodeId> seeds;
+        std::vector<std::uint64_t> rng(n);
+        for (std::uint64_t b = lo; b < hi; ++b) {
+            if (b + 1 < hi && chunks[b].size() != cfg_.batch_size)
+                throw PipelineError("sample", "only the last chunk of an epoch may be short");
+            seeds.insert(seeds.end(), chunks[b].begin(), chunks[b].end());
+            rng[b - lo] = batch_seed(seed, epoch, b);
+        }
+        featbuf::BufferStats before = buffer_stats(w);
+        Dev sd(seeds.size() * 8);
+        check(fdg_memcpy_h2d(sd.p, seeds.data(), seeds.size() * 8, nullptr));
+        check(fdg_stream_sync(nullptr));
+        std::vector<float> xms(n);
+        float ms = 0;
+        const auto t0 = std::chrono::steady_clock::now();
+        check(fdg_pipeline_run_ragged(p, static_cast<const std::uint64_t*>(sd.p), 0, seeds.size(), rng.data(), n,
+                                      nullptr, xms.data(), &ms));
+        st.wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        std::vector<fdg_batch_counts> recs(n);
+        check(fdg_pipeline_records(p, 0, n, recs.data()));
+        float sample_ms = 0;
+        check(fdg_pipeline_sample_times(p, nullptr, &sample_ms));
+        st.sample_busy_s = sample_ms / 1e3;
+        for (float x : xms) st.extract_busy_s += x / 1e3;
+        std::uint64_t nodes_total = 0;
+        for (std::uint64_t j = 0; j < n; ++j) {
+            const auto& c = recs[j];
+            const bool failed = c.status != 0;
+            st.batch_records.push_back({lo + j, chunks[lo + j].size(), c.n_nodes, failed ? 0 : c.checksum, failed});
+            ++st.batches_sampled;
+            if (failed) {
+                ++st.batches_failed;
+            } else {
+                ++st.batches_trained;
+                nodes_total += c.n_nodes;
+            }
+            ++st.batches_released;
+            if (cfg_.verify && !failed) {
+                auto ref = sync_batch(chunks[lo + j], rng[j]);
+                if (ref.first != c.n_nodes || ref.second != c.checksum)
+                    throw PipelineError("train", "batch " + std::to_string(lo + j) +
+                                                     " differs from the synchronous path (nodes " +
+                                                     std::to_string(c.n_nodes) + " vs " + std::to_string(ref.first) +
+                                                     ")");
+            }
+        }
+        featbuf::BufferStats after = buffer_stats(w);
+        if (slots_) {
+            st.buffer = {after.hits - before.hits,     after.loads - before.loads,
+                         after.waits - before.waits,   after.evictions - before.evictions,
+                         after.takeovers - before.takeovers, after.releases - before.releases,
+                         after.standby_len};
+            st.nodes_loaded = st.buffer.loads;
+        } else {
+            st.nodes_loaded = nodes_total;  // direct gather: every row is read
+        }
+        st.read_requests = st.nodes_loaded;
+        st.bytes_useful = st.bytes_requested = st.nodes_loaded * rb;
+        return st;
+    }
+
+    featbuf::BufferStats buffer_stats(std::uint32_t w) const {
+        if (!slots_) return {};
+        fdg_bm_stats s{};
+        check(fdg_pipeline_bm_stats(pipes_[w], &s));
+        return {s.hits, s.loads, s.waits, s.evictions, s.takeovers, s.releases, s.standby_len};
+    }
+
+    struct Dev {
+        explicit Dev(std::uint64_t bytes) { check(fdg_malloc(&p, std::max<std::uint64_t>(bytes, 8))); }
+        ~Dev() { fdg_free(p); }
+        void* p = nullptr;
+    };
+
+    const graph::Topology& topo_;
+    PipelineConfig cfg_;
+    std::uint64_t mb_ = 0, slots_ = 0, cap_ = 0;
+    std::vector<fdg_pipeline*> pipes_;
+    fdg_sampler* sampler_ = nullptr;
+    std::unique_ptr<Dev> sbuf_;
+    std::mutex sync_mu_;
+};
+
+  }  // namespace pipeline
 }  // namespace featdrive_gpu

@@ -112,6 +112,9 @@ SIGNATURES = {
     "fdg_pipeline_run": (ci, [vp, vp, ci, vp, u64, vp, vp, C.POINTER(C.c_float)]),
     "fdg_pipeline_records": (ci, [vp, u64, u64, vp]),
     "fdg_pipeline_extract_times": (ci, [vp, u64, u64, vp, vp]),
+    "fdg_pipeline_run_ragged": (ci, [vp, vp, ci, u64, vp, u64, vp, vp, vp]),
+    "fdg_pipeline_sample_times": (ci, [vp, vp, vp]),
+    "fdg_pipeline_bm_stats": (ci, [vp, C.POINTER(BmStats)]),
     "fdg_pipeline_get_config": (ci, [vp, C.POINTER(PipelineConfig)]),
     "fdg_partition_epoch": (ci, [vp, u64, u64, u64, vp]),
     "fdg_batch_seed": (u64, [u64, u64, u64]),

@@ -57,6 +57,8 @@ struct fdg_pipeline {
     fdg_batch_counts* counts = nullptr;  // device, one per batch of the current run
     uint64_t counts_cap = 0;
     std::vector<cudaEvent_t> tev;        // per-batch extract timing events (2 per batch)
+    std::vector<cudaEvent_t> sev;        // per-group sampling timing events (2 per group)
+    uint64_t timed_groups = 0;
     fdg_bm* bm = nullptr;
     cudaEvent_t t0 = nullptr;            // start of the last run (timing base)
     uint64_t timed_batches = 0;          // batches of the last run with extraction events
@@ -82,6 +84,7 @@ void destroy(fdg_pipeline* p) {
     for (auto e : p->sampled) cudaEventDestroy(e);
     for (auto e : p->extracted) cudaEventDestroy(e);
     for (auto e : p->tev) cudaEventDestroy(e);
+    for (auto e : p->sev) cudaEventDestroy(e);
     if (p->counts) cudaFree(p->counts);
     if (p->t0) cudaEventDestroy(p->t0);
     if (p->bm) fdg_bm_destroy(p->bm);
@@ -219,10 +222,21 @@ int fdg_pipeline_destroy(fdg_pipeline* p) {
 
 int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, const uint64_t* rng_seeds,
                      uint64_t n_batches, fdg_batch_counts* records_host, float* extract_ms, float* elapsed_ms) {
+    return fdg_pipeline_run_ragged(p, seeds, seeds_on_host, n_batches * p->cfg.batch_size, rng_seeds, n_batches,
+                                   records_host, extract_ms, elapsed_ms);
+}
+
+int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, uint64_t n_seeds_total,
+                            const uint64_t* rng_seeds, uint64_t n_batches, fdg_batch_counts* records_host,
+                            float* extract_ms, float* elapsed_ms) {
     cudaSetDevice(p->ctx->device);
     const uint32_t S = p->cfg.n_samplers, PG = p->cfg.prefetch_group, B = p->cfg.batch_size;
     const uint32_t G = p->cfg.group_batches;
     if (n_batches == 0) return FDG_OK;
+    if (n_seeds_total > n_batches * uint64_t(B) || n_seeds_total <= (n_batches - 1) * uint64_t(B))
+        return fail(FDG_INVALID_ARG, "pipeline_run: every batch but the last must hold batch_size seeds");
+    // seeds of batch j: [j*B, min((j+1)*B, n_seeds_total)) (the last chunk of partition_epoch may be short)
+    auto seeds_of = [&](uint64_t j) { return uint32_t(std::min<uint64_t>(B, n_seeds_total - j * B)); };
     if (p->counts_cap < n_batches) {
         if (p->counts) cudaFree(p->counts);
         FDG_CUDA(cudaMalloc(&p->counts, n_batches * sizeof(fdg_batch_counts)));
@@ -233,6 +247,14 @@ int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, 
             cudaEvent_t e;
             FDG_CUDA(cudaEventCreate(&e));
             p->tev.push_back(e);
+        }
+    }
+    const uint64_t n_groups_all = (n_batches + G - 1) / G;
+    if (extract_ms && p->sev.size() < 2 * n_groups_all) {
+        for (size_t i = p->sev.size(); i < 2 * n_groups_all; ++i) {
+            cudaEvent_t e;
+            FDG_CUDA(cudaEventCreate(&e));
+            p->sev.push_back(e);
         }
     }
     const bool sample_only = p->cfg.flags & FDG_PIPE_SAMPLE_ONLY;
@@ -268,6 +290,7 @@ int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, 
     if (!p->t0) FDG_CUDA(cudaEventCreate(&p->t0));
     cudaEvent_t t0 = p->t0;
     p->timed_batches = 0;
+    p->timed_groups = 0;
     FDG_CUDA(cudaEventCreate(&t1));
     FDG_CUDA(cudaEventRecord(t0, p->xstream));
     for (uint32_t s = 0; s < S; ++s) FDG_CUDA(cudaStreamWaitEvent(p->sstream[s], t0, 0));
@@ -294,17 +317,19 @@ int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, 
                 const uint32_t slot = uint32_t(j % p->nslots);
                 FDG_CUDA(cudaStreamWaitEvent(ss, p->extracted[slot], 0));
                 sd[i] = seeds + j * B;
+                ns[i] = seeds_of(j);
                 if (seeds_on_host) {  // host -> device copy of this batch's seeds (pinned for async)
-                    FDG_CUDA(cudaMemcpyAsync(p->seeds[slot], sd[i], uint64_t(B) * 8, cudaMemcpyHostToDevice, ss));
+                    FDG_CUDA(cudaMemcpyAsync(p->seeds[slot], sd[i], uint64_t(ns[i]) * 8, cudaMemcpyHostToDevice, ss));
                     sd[i] = p->seeds[slot];
                 }
-                ns[i] = B;
                 rs[i] = rng_seeds[j];
                 nd[i] = p->nodes[slot];
                 ed[i] = p->edges[slot];
                 cn[i] = p->counts + j;
             }
+            if (extract_ms) FDG_CUDA(cudaEventRecord(p->sev[2 * g], ss));
             FDG_TRY(sampler_sample_group(p->samplers[s], ss, n, sd, ns, rs, nd, ed, p->cap, cn));
+            if (extract_ms) FDG_CUDA(cudaEventRecord(p->sev[2 * g + 1], ss));
             consumed[s] += n;
             FDG_CUDA(cudaEventRecord(p->sampled[gslot], ss));
             FDG_CUDA(cudaStreamWaitEvent(p->xstream, p->sampled[gslot], 0));
@@ -373,6 +398,7 @@ int fdg_pipeline_run(fdg_pipeline* p, const uint64_t* seeds, int seeds_on_host, 
             FDG_CUDA(cudaEventElapsedTime(extract_ms + j, p->tev[2 * j], p->tev[2 * j + 1]));
     cudaEventDestroy(t1);
     if (extract_ms && !sample_only) p->timed_batches = n_batches;
+    if (extract_ms) p->timed_groups = sampled_groups;
     return FDG_OK;
 }
 
@@ -383,6 +409,23 @@ int fdg_pipeline_extract_times(fdg_pipeline* p, uint64_t first, uint64_t n, floa
         FDG_CUDA(cudaEventElapsedTime(start_ms + (j - first), p->t0, p->tev[2 * j]));
         FDG_CUDA(cudaEventElapsedTime(end_ms + (j - first), p->t0, p->tev[2 * j + 1]));
     }
+    return FDG_OK;
+}
+
+int fdg_pipeline_bm_stats(fdg_pipeline* p, fdg_bm_stats* out) {
+    if (!p->bm) return fail(FDG_NOT_LOADED, "pipeline_bm_stats: pipeline has no buffer manager");
+    return fdg_bm_stats_get(p->bm, out);
+}
+
+int fdg_pipeline_sample_times(fdg_pipeline* p, uint64_t* n_groups, float* busy_ms) {
+    float tot = 0;
+    for (uint64_t g = 0; g < p->timed_groups; ++g) {
+        float ms = 0;
+        FDG_CUDA(cudaEventElapsedTime(&ms, p->sev[2 * g], p->sev[2 * g + 1]));
+        tot += ms;
+    }
+    if (n_groups) *n_groups = p->timed_groups;
+    if (busy_ms) *busy_ms = tot;
     return FDG_OK;
 }
 

@@ -505,19 +505,28 @@ class Pipeline:
         self.batch_size = batch_size
 
     def run(self, seeds_ptr: int, on_host: bool, rng_seeds, records_ptr: int | None = None,
-            extract_ms: np.ndarray | None = None) -> float:
-        """Run len(rng_seeds) batches; returns the device time of the run in ms."""
+            extract_ms: np.ndarray | None = None, n_seeds: int | None = None) -> float:
+        """Run len(rng_seeds) batches; returns the device time of the run in ms. n_seeds
+        (default len(rng_seeds) * batch_size) lets the last batch be short."""
         rng = np.ascontiguousarray(rng_seeds, np.uint64)
         ms = C.c_float()
-        check(lib().fdg_pipeline_run(self.ptr, seeds_ptr, 1 if on_host else 0, _p(rng), len(rng), records_ptr,
-                                     _p(extract_ms), C.byref(ms)))
+        total = len(rng) * self.batch_size if n_seeds is None else int(n_seeds)
+        check(lib().fdg_pipeline_run_ragged(self.ptr, seeds_ptr, 1 if on_host else 0, total, _p(rng), len(rng),
+                                            records_ptr, _p(extract_ms), C.byref(ms)))
+        return ms.value
+
+    def sample_busy_ms(self) -> float:
+        """Sampling-stage busy time of the last run (run with extract_ms)."""
+        ms = C.c_float()
+        check(lib().fdg_pipeline_sample_times(self.ptr, None, C.byref(ms)))
         return ms.value
 
     def run_batches(self, seeds: np.ndarray, rng_seeds, checksum_records: bool = True) -> np.ndarray:
-        """Convenience: host seeds [n_batches * batch_size] -> per-batch records (COUNTS_DTYPE)."""
+        """Convenience: host seeds (batch j = seeds[j*B:(j+1)*B], the last may be short)
+        -> per-batch records (COUNTS_DTYPE)."""
         seeds = np.ascontiguousarray(seeds, np.uint64)
         dev = DeviceBuffer.from_array(seeds)
-        self.run(dev.ptr, False, rng_seeds)
+        self.run(dev.ptr, False, rng_seeds, n_seeds=len(seeds))
         return self.records(len(rng_seeds))
 
     def records(self, n: int) -> np.ndarray:

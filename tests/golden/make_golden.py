@@ -168,6 +168,11 @@ def main():
     g["sync_records"] = recs
     recs2, _ = R.run_epoch(ds, np.arange(200, dtype=np.uint64), 0, 0, 50, [4, 4], sync=False)
     g["async_records"] = recs2
+    # PipelineSession epochs with a short last chunk (1050 ids, batch 100) and a
+    # nonzero seed, for the featdrive-gpu CLI / C++ session parity test
+    for e in (0, 1):
+        r, _ = R.run_epoch(ds, np.arange(1050, dtype=np.uint64), e, 3, 100, [5, 5], sync=True)
+        g[f"session_e{e}"] = r
 
     np.savez_compressed(OUT, **g)
     print("wrote", OUT, os.path.getsize(OUT), "bytes")
