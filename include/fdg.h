@@ -180,8 +180,10 @@ int fdg_mt_stream(void* stream, uint64_t rng_seed, uint64_t n, uint64_t* out_dev
  * common.hpp:88-105) into *checksum_dev (caller zeroes it). */
 int fdg_gather(fdg_ctx* ctx, void* stream, const uint64_t* nodes_dev, const uint32_t* n_dev, uint64_t n_host,
                void* out_dev, uint64_t* checksum_dev);
-/* Gather engine: TMA bulk copies (default; one 4-warp CTA per SM) or the 16-byte
- * LDG/STG kernel (also used for sharded tables and rows not a multiple of 16 B). */
+/* Gather engine: the 16-byte LDG/STG kernels (default, also for sharded tables and
+ * rows not a multiple of 16 B) or TMA bulk copies (one 4-warp CTA per SM). The
+ * fused-checksum gather uses option "checksum_impl" (default LDG) and "hash_kernel"
+ * (default 4: software-pipelined, row size fixed at compile time). */
 #define FDG_GATHER_TMA 0
 #define FDG_GATHER_LDG 1
 #define FDG_GATHER_TMA_WS 2 /* warp-specialised TMA: producer warp + consumer (hashing) warps */

@@ -421,7 +421,16 @@ int fdg_set_option(const char* key, int64_t v) {
     if (k == "hash_clear") { g_hash_clear = v != 0; return FDG_OK; }
     if (k == "hash_keep") { g_hash_keep = v != 0; return FDG_OK; }
     if (k == "gather_dynamic") { g_gather_dynamic = v != 0; return FDG_OK; }
-    if (k == "hash_kernel") { g_hash_kernel = v; return FDG_OK; }
+    if (k == "hash_kernel") {
+        if (v < 1 || v > 4) return fail(FDG_INVALID_ARG, "hash_kernel must be in [1, 4]");
+        g_hash_kernel = v;
+        return FDG_OK;
+    }
+    if (k == "hash_chunk") {
+        if (v != 0 && v != 128 && v != 256) return fail(FDG_INVALID_ARG, "hash_chunk must be 0, 128 or 256");
+        g_hash_chunk = v;
+        return FDG_OK;
+    }
     if (k == "checksum_impl") {
         if (v < -1 || v > FDG_GATHER_TMA_WS) return fail(FDG_INVALID_ARG, "checksum_impl must be -1 or a gather impl");
         g_checksum_impl = v;
@@ -458,6 +467,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "hash_keep") *v = g_hash_keep;
     else if (k == "gather_dynamic") *v = g_gather_dynamic;
     else if (k == "hash_kernel") *v = g_hash_kernel;
+    else if (k == "hash_chunk") *v = g_hash_chunk;
     else if (k == "checksum_impl") *v = g_checksum_impl;
     else if (k == "ws_hashers") *v = g_ws_hashers;
     else if (k == "ws_stg") *v = g_ws_stg;

@@ -268,6 +268,288 @@ __global__ void __launch_bounds__(kH16Warps * 32, 2)
     if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
 }
 
+// Software-pipelined gather + checksum. Same 32-row x 128-byte work items as
+// k_gather_hash16, but each warp issues the loads of its NEXT item (the next
+// chunk of the group, or chunk 0 of its next group) before it hashes the current
+// one from shared memory, so loads stay in flight during the serial splitmix
+// chains instead of alternating with them (hash16's load and hash phases add up:
+// 217 vs 160 us per Papers batch). Up to kHpMinBlocks x 8 warps per SM keep
+// ~128 KB of rows in flight.
+constexpr int kHpWarps = 8;
+constexpr int kHpMinBlocks = 3;
+
+template <bool SHARDED, bool ALIAS>
+__global__ void __launch_bounds__(kHpWarps * 32, kHpMinBlocks)
+    k_gather_hash_pipe(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
+                       const uint32_t* status, TableRef t, char* __restrict__ out, uint64_t* checksum) {
+    __shared__ __align__(16) char smem[kHpWarps][32 * kH16Stride];
+    if (status && *status) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    char* wbuf = smem[warp];
+    const uint32_t rb = t.row_bytes;
+    const uint32_t nch = (rb + 127) >> 7;  // 128-byte chunks per row
+    const uint64_t n = n_dev ? *n_dev : n_host;
+    const uint64_t groups = (n + 31) / 32;
+    const uint64_t gstride = uint64_t(gridDim.x) * kHpWarps;
+    const uint64_t g0 = blockIdx.x * uint64_t(kHpWarps) + warp;
+    if (g0 >= groups) return;
+    const uint64_t my_groups = (groups - g0 + gstride - 1) / gstride;
+    const uint64_t items = my_groups * nch;
+    const uint64_t pol = gather_policy(t.evict_first);
+    const uint32_t part = lane & 7;
+    auto node_of = [&](uint64_t g) -> uint64_t {
+        const uint64_t r = g * 32 + lane;
+        return (g < groups && r < n) ? __ldg(nodes + r) : 0;
+    };
+    auto rows_of = [&](uint64_t g) -> uint32_t { return uint32_t(n - g * 32 < 32 ? n - g * 32 : 32); };
+    uint4 v[8];
+    auto issue = [&](uint64_t g, uint32_t c, uint64_t node_reg) {
+        const uint32_t rows = rows_of(g);
+        const uint32_t c0 = c << 7;
+        const uint32_t parts = (rb - c0 < 128 ? rb - c0 : 128) >> 4;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t r = k * 4 + (lane >> 3);
+            const uint64_t node = __shfl_sync(0xffffffffu, node_reg, int(r));
+            if (r < rows && part < parts) {
+                const char* src = ALIAS ? t.base + node * rb : row_ptr<SHARDED>(t, node);
+                v[k] = ldg_stream(reinterpret_cast<const uint4*>(src + c0) + part, pol);
+            }
+        }
+    };
+    uint64_t cur_node = node_of(g0);
+    uint64_t nxt_node = node_of(g0 + gstride);
+    const uint64_t seed = 0x27d4eb2f165667c5ull ^ (uint64_t(rb) * 0x9e3779b97f4a7c15ull);
+    uint64_t h = seed, sum = 0;
+    issue(g0, 0, cur_node);
+    uint64_t g = g0;
+    uint32_t c = 0;
+    for (uint64_t it = 0; it < items; ++it) {
+        const uint32_t rows = rows_of(g);
+        const uint32_t c0 = c << 7;
+        const uint32_t parts = (rb - c0 < 128 ? rb - c0 : 128) >> 4;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t r = k * 4 + (lane >> 3);
+            if (r < rows && part < parts) {
+                if (!ALIAS && out) stg_stream(reinterpret_cast<uint4*>(out + (g * 32 + r) * rb + c0) + part, v[k], pol);
+                *reinterpret_cast<uint4*>(wbuf + r * kH16Stride + part * 16) = v[k];
+            }
+        }
+        __syncwarp();
+        const bool last = c + 1 == nch;
+        if (it + 1 < items) issue(last ? g + gstride : g, last ? 0 : c + 1, last ? nxt_node : cur_node);
+        if (lane < int(rows)) {
+            const uint4* p = reinterpret_cast<const uint4*>(wbuf + lane * kH16Stride);
+            for (uint32_t s = 0; s < parts; ++s) {
+                const uint4 w = p[s];
+                h = splitmix64(h ^ (uint64_t(w.y) << 32 | w.x));
+                h = splitmix64(h ^ (uint64_t(w.w) << 32 | w.z));
+            }
+        }
+        __syncwarp();
+        if (last) {
+            if (lane < int(rows)) sum += splitmix64(h);
+            h = seed;
+            g += gstride;
+            c = 0;
+            cur_node = nxt_node;
+            nxt_node = node_of(g + gstride);
+        } else {
+            ++c;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
+}
+
+// Lean variant of k_gather_hash_pipe for a compile-time row size RB, staging
+// CH-byte chunks of 32 rows. ncu of the runtime-rb kernel (Friendster, 1 KB rows)
+// showed 744 warp-instructions per 32-row x 128-byte item against 320 for the
+// splitmix chains themselves: per-chunk shuffles of node ids, 64-bit address
+// arithmetic and predicated loads. Here a full 32-row group resolves its per-lane
+// source pointers once (reused by every chunk), destination offsets are
+// immediates, and only the one ragged last group takes the predicated path.
+// CH = 256 (rows >= 256 B): a row's bytes are requested in 256-byte runs instead
+// of 128-byte ones spaced a whole hash phase apart. Measured per batch with the
+// checksum, extraction alone: Papers 155 us (128-byte chunks: 176 us; plain
+// gather without checksum: 159 us), Friendster 312 us (361 us).
+template <int CH>
+struct HashRbShape {
+    static constexpr int LPR = CH / 16;    // lanes per row in one load instruction
+    static constexpr int RPI = 32 / LPR;   // rows per load instruction
+    static constexpr int NI = 32 / RPI;    // load instructions per chunk (= 16-byte parts per row chunk)
+    static constexpr int STRIDE = CH + 16; // staged row stride: conflict-free 16-byte lane reads
+    static constexpr int MINB = CH == 128 ? 3 : 2;
+};
+
+template <int RB, int CH, bool SHARDED, bool ALIAS>
+__global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
+    k_gather_hash_rb(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
+                     const uint32_t* status, TableRef t, char* __restrict__ out, uint64_t* checksum) {
+    using S = HashRbShape<CH>;
+    static_assert(RB % 16 == 0, "16-byte rows");
+    constexpr int NCH = (RB + CH - 1) / CH;
+    constexpr int LASTP = (RB - (NCH - 1) * CH) / 16;  // 16-byte parts in the last chunk
+    constexpr bool EVEN = RB % CH == 0;
+    extern __shared__ __align__(16) char rb_smem[];  // kHpWarps x 32 rows x STRIDE
+    if (status && *status) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    char* wbuf = rb_smem + warp * 32 * S::STRIDE;
+    const uint64_t n = n_dev ? *n_dev : n_host;
+    const uint64_t full = n / 32;
+    const uint64_t gstride = uint64_t(gridDim.x) * kHpWarps;
+    const uint64_t g0 = blockIdx.x * uint64_t(kHpWarps) + warp;
+    const uint64_t pol = gather_policy(t.evict_first);
+    const uint32_t part = lane % S::LPR, rsub = lane / S::LPR;
+    const uint64_t seed = 0x27d4eb2f165667c5ull ^ (uint64_t(RB) * 0x9e3779b97f4a7c15ull);
+    uint64_t sum = 0;
+    const uint64_t my_full = g0 < full ? (full - g0 + gstride - 1) / gstride : 0;
+    if (my_full) {
+        const char* src[S::NI];
+        uint4 v[S::NI];
+        auto setup = [&](uint64_t node_reg) {
+#pragma unroll
+            for (int k = 0; k < S::NI; ++k) {
+                const uint64_t node = __shfl_sync(0xffffffffu, node_reg, k * S::RPI + int(rsub));
+                src[k] = (ALIAS ? t.base + node * RB : row_ptr<SHARDED>(t, node)) + part * 16;
+            }
+        };
+        auto issue = [&](int c) {
+#pragma unroll
+            for (int k = 0; k < S::NI; ++k)
+                if (EVEN || c + 1 < NCH || int(part) < LASTP)
+                    v[k] = ldg_stream(reinterpret_cast<const uint4*>(src[k] + c * CH), pol);
+        };
+        uint64_t g = g0;
+        uint64_t nxt_node = (g0 + gstride < full) ? __ldg(nodes + (g0 + gstride) * 32 + lane) : 0;
+        setup(__ldg(nodes + g0 * 32 + lane));
+        issue(0);
+        for (uint64_t i = 0; i < my_full; ++i) {
+            char* dst = ALIAS ? nullptr : out + (g * 32 + rsub) * RB + part * 16;
+            uint64_t h = seed;
+#pragma unroll 1
+            for (int c = 0; c < NCH; ++c) {
+                const bool lastc = c + 1 == NCH;
+#pragma unroll
+                for (int k = 0; k < S::NI; ++k) {
+                    if (EVEN || !lastc || int(part) < LASTP) {
+                        if (!ALIAS && out)
+                            stg_stream(reinterpret_cast<uint4*>(dst + k * S::RPI * RB + c * CH), v[k], pol);
+                        *reinterpret_cast<uint4*>(wbuf + (k * S::RPI + rsub) * S::STRIDE + part * 16) = v[k];
+                    }
+                }
+                __syncwarp();
+                if (!lastc) {
+                    issue(c + 1);
+                } else if (i + 1 < my_full) {  // chunk 0 of this warp's next group
+                    setup(nxt_node);
+                    issue(0);
+                    const uint64_t g2 = g + 2 * gstride;
+                    nxt_node = g2 < full ? __ldg(nodes + g2 * 32 + lane) : 0;
+                }
+                const uint4* p = reinterpret_cast<const uint4*>(wbuf + lane * S::STRIDE);
+                const int parts = (EVEN || !lastc) ? S::NI : LASTP;
+#pragma unroll
+                for (int s = 0; s < S::NI; ++s) {
+                    if (s < parts) {
+                        const uint4 w = p[s];
+                        h = splitmix64(h ^ (uint64_t(w.y) << 32 | w.x));
+                        h = splitmix64(h ^ (uint64_t(w.w) << 32 | w.z));
+                    }
+                }
+                __syncwarp();
+            }
+            sum += splitmix64(h);
+            g += gstride;
+        }
+    }
+    // the ragged last group (n % 32 rows), if this warp owns it
+    const uint64_t tail = full;
+    if (n % 32 && tail >= g0 && (tail - g0) % gstride == 0) {
+        const uint32_t rows = uint32_t(n - tail * 32);
+        const uint64_t my_node = lane < int(rows) ? __ldg(nodes + tail * 32 + lane) : 0;
+        uint64_t h = seed;
+        for (int c = 0; c < NCH; ++c) {
+            const int parts = c + 1 < NCH ? S::NI : LASTP;
+#pragma unroll
+            for (int k = 0; k < S::NI; ++k) {
+                const uint32_t r = k * S::RPI + rsub;
+                const uint64_t node = __shfl_sync(0xffffffffu, my_node, int(r));
+                if (r < rows && int(part) < parts) {
+                    const char* src = ALIAS ? t.base + node * RB : row_ptr<SHARDED>(t, node);
+                    const uint4 w = ldg_stream(reinterpret_cast<const uint4*>(src + c * CH) + part, pol);
+                    if (!ALIAS && out)
+                        stg_stream(reinterpret_cast<uint4*>(out + (tail * 32 + r) * RB + c * CH) + part, w, pol);
+                    *reinterpret_cast<uint4*>(wbuf + r * S::STRIDE + part * 16) = w;
+                }
+            }
+            __syncwarp();
+            if (lane < int(rows)) {
+                const uint4* p = reinterpret_cast<const uint4*>(wbuf + lane * S::STRIDE);
+                for (int s = 0; s < parts; ++s) {
+                    const uint4 w = p[s];
+                    h = splitmix64(h ^ (uint64_t(w.y) << 32 | w.x));
+                    h = splitmix64(h ^ (uint64_t(w.w) << 32 | w.z));
+                }
+            }
+            __syncwarp();
+        }
+        if (lane < int(rows)) sum += splitmix64(h);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
+}
+
+
+template <int RB, int CH, bool SHARDED, bool ALIAS>
+int launch_hash_rb_one(int blocks, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                       const uint32_t* status, const TableRef& t, char* out, uint64_t* checksum) {
+    constexpr int smem = kHpWarps * 32 * HashRbShape<CH>::STRIDE;
+    static bool attr = false;
+    if (!attr) {
+        FDG_CUDA(cudaFuncSetAttribute(k_gather_hash_rb<RB, CH, SHARDED, ALIAS>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    k_gather_hash_rb<RB, CH, SHARDED, ALIAS><<<blocks, kHpWarps * 32, smem, st>>>(nodes, n_dev, n_host, status, t,
+                                                                                   out, checksum);
+    return FDG_OK;
+}
+
+// Row sizes with a compile-time instantiation of k_gather_hash_rb (the bench and
+// BASELINE shapes: 100/128/256 x f32, 768 x f16, 768 x f32, plus 64 x f32).
+// Returns -1 when the row size has no instantiation (the caller falls back).
+template <bool SHARDED, bool ALIAS>
+int launch_hash_rb(const Ctx& c, cudaStream_t st, uint64_t groups, const uint64_t* nodes, const uint32_t* n_dev,
+                    uint64_t n_host, const uint32_t* status, const TableRef& t, char* out, uint64_t* checksum) {
+    const int ch = g_hash_chunk ? int(g_hash_chunk) : (c.row_bytes >= 256 ? 256 : 128);
+    const int minb = ch == 128 ? HashRbShape<128>::MINB : HashRbShape<256>::MINB;
+    const int blocks = int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps, uint64_t(c.sm_count) * minb));
+#define FDG_HRB(R)                                                                                      \
+    case R:                                                                                             \
+        if (ch == 256)                                                                                  \
+            FDG_TRY((launch_hash_rb_one<R, 256, SHARDED, ALIAS>(blocks, st, nodes, n_dev, n_host, status, t, out, \
+                                                               checksum)));                             \
+        else                                                                                            \
+            FDG_TRY((launch_hash_rb_one<R, 128, SHARDED, ALIAS>(blocks, st, nodes, n_dev, n_host, status, t, out, \
+                                                               checksum)));                             \
+        return FDG_OK;
+    switch (c.row_bytes) {
+        FDG_HRB(256)
+        FDG_HRB(400)
+        FDG_HRB(512)
+        FDG_HRB(1024)
+        FDG_HRB(1536)
+        FDG_HRB(3072)
+        default:
+            return -1;
+    }
+#undef FDG_HRB
+}
+
 // Warp-specialised gather + checksum (LDG): Wc copy warps move 32-row groups
 // table -> X with coalesced 16-byte loads/stores (the flattened (row, part) items
 // of a group are contiguous in X) and stage each group in a shared-memory slot; Wh
@@ -519,8 +801,15 @@ int g_gather_impl = FDG_GATHER_LDG;
 int g_gather_evict_first = 1;
 int g_gather_ctas_per_sm = 1;
 int64_t g_gather_dynamic = 1;
-int64_t g_hash_kernel = 1;  // 1: striped LDG k_gather_hash16, 2: warp-specialised k_gather_hash_ws
-int64_t g_checksum_impl = FDG_GATHER_TMA;  // measured best inside the pipeline
+// Fused gather + trainer checksum: 1 striped k_gather_hash16, 2 warp-specialised
+// k_gather_hash_ws, 3 software-pipelined k_gather_hash_pipe, 4 the same with a
+// compile-time row size (k_gather_hash_rb; other sizes fall back to 3). 4 on the
+// LDG engine is the default: Papers batch extraction with checksum 175 us vs 242 us
+// (TMA + per-warp hashing, the previous default), Friendster 360 vs 636 us
+// (scripts/ab_checksum.sh).
+int64_t g_hash_kernel = 4;
+int64_t g_hash_chunk = 0;  // 0: 256-byte chunks for rows >= 256 B, else 128; or force 128 / 256
+int64_t g_checksum_impl = FDG_GATHER_LDG;
 
 int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
                         uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status) {
@@ -541,6 +830,21 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
         if (g_hash_kernel == 2 && c.row_bytes <= 2048) {
             FDG_TRY(launch_hash_ws<false>(c, st, nodes, n_dev, n_host, status, t, static_cast<char*>(out), checksum,
                                           sharded));
+        } else if (g_hash_kernel >= 3) {
+            const int pb = int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps, uint64_t(c.sm_count) * kHpMinBlocks));
+            const int rc = g_hash_kernel != 4 ? -1
+                           : sharded ? launch_hash_rb<true, false>(c, st, groups, nodes, n_dev, n_host, status, t,
+                                                                   static_cast<char*>(out), checksum)
+                                     : launch_hash_rb<false, false>(c, st, groups, nodes, n_dev, n_host, status, t,
+                                                                    static_cast<char*>(out), checksum);
+            if (rc > 0) return rc;
+            if (rc == FDG_OK) {
+            } else if (sharded)
+                k_gather_hash_pipe<true, false><<<pb, kHpWarps * 32, 0, st>>>(nodes, n_dev, n_host, status, t,
+                                                                             static_cast<char*>(out), checksum);
+            else
+                k_gather_hash_pipe<false, false><<<pb, kHpWarps * 32, 0, st>>>(nodes, n_dev, n_host, status, t,
+                                                                              static_cast<char*>(out), checksum);
         } else if (sharded) {
             k_gather_hash16<true, false><<<blocks, kH16Warps * 32, 0, st>>>(nodes, n_dev, n_host, status, t,
                                                                           static_cast<char*>(out), checksum);
@@ -619,6 +923,14 @@ int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, con
         if (g_hash_kernel == 2 && c.row_bytes <= 2048)
             FDG_TRY(launch_hash_ws<true>(c, st, reinterpret_cast<const uint64_t*>(alias), n_dev, n_host, status, t,
                                          nullptr, checksum, false));
+        else if (g_hash_kernel == 4 &&
+                 launch_hash_rb<false, true>(c, st, groups, reinterpret_cast<const uint64_t*>(alias), n_dev, n_host,
+                                             status, t, nullptr, checksum) == FDG_OK) {
+        } else if (g_hash_kernel >= 3)
+            k_gather_hash_pipe<false, true>
+                <<<int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps, uint64_t(c.sm_count) * kHpMinBlocks)),
+                   kHpWarps * 32, 0, st>>>(reinterpret_cast<const uint64_t*>(alias), n_dev, n_host, status, t, nullptr,
+                                           checksum);
         else
             k_gather_hash16<false, true><<<blocks, kH16Warps * 32, 0, st>>>(
                 reinterpret_cast<const uint64_t*>(alias), n_dev, n_host, status, t, nullptr, checksum);

@@ -106,6 +106,7 @@ extern int g_gather_evict_first;
 extern int g_gather_ctas_per_sm;
 extern int64_t g_gather_dynamic;
 extern int64_t g_hash_kernel;
+extern int64_t g_hash_chunk;  // k_gather_hash_rb staging chunk (0 = by row size)
 extern int64_t g_checksum_impl;  // gather impl for the fused-checksum path (-1: same as g_gather_impl)
 extern int g_ws_hashers;
 extern int g_ws_stg;

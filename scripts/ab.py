@@ -11,19 +11,20 @@ import paper_2406_13984_b200 as fd  # noqa: E402
 from paper_2406_13984_b200 import _lib  # noqa: E402
 from paper_2406_13984_b200.featdrive import DeviceBuffer  # noqa: E402
 
-cfgname = "papers"
+import os
+cfgname = os.environ.get("CFG", "papers")
 n, dim, avg, fan, B, t_ids, dtype, frac = bench.CONFIGS[cfgname]
 L = fd.featdrive.lib()
 topo = fd.Topology.generate(n, dim, avg, 7, dtype=dtype)
 order = np.concatenate(fd.partition_epoch(np.arange(t_ids, dtype=np.uint64), B, bench.hash_combine(0, 0)))
-K = 300
+K = int(os.environ.get("K", "300"))
 rng = np.array([L.fdg_batch_seed(0, 0, int(g)) for g in range(K)], np.uint64)
 seeds = DeviceBuffer.from_array(np.ascontiguousarray(order[:K * B]))
 f = np.ascontiguousarray(fan, np.uint32)
 defaults = {"gather_impl": 1, "gather_evict_first": 1, "l2_persist_mb": 0, "hash_load_pct": 50,
             "hash_clear": 1, "sampler_ctas_per_sm": 16, "gather_ctas_per_sm": 1,
-            "extract_streams": 2, "hash_keep": 1, "gather_dynamic": 1, "hash_kernel": 1,
-            "ws_hashers": 8, "ws_stg": 1, "checksum_impl": 0}
+            "extract_streams": 2, "hash_keep": 1, "gather_dynamic": 1, "hash_kernel": 4,
+            "ws_hashers": 8, "ws_stg": 1, "checksum_impl": 1, "hash_chunk": 0}
 for spec in sys.argv[1:]:
     kv = dict(x.split("=") for x in spec.split(",") if x)
     S = int(kv.pop("S", 2))

@@ -367,6 +367,7 @@ def test_gather_impls_agree(fd, port, impl, dim, rows):
     t = fd.Topology.generate(n, dim, 8, 9)
     table = t.download_rows(0, n)
     nodes = np.random.RandomState(impl + rows).randint(0, n, size=rows).astype(np.uint64)
+    old = fd.featdrive.get_option("checksum_impl")
     fd.set_option("gather_impl", impl)
     fd.set_option("checksum_impl", -1)  # the fused checksum path follows gather_impl
     try:
@@ -377,19 +378,20 @@ def test_gather_impls_agree(fd, port, impl, dim, rows):
             np.testing.assert_array_equal(fd.gather(t, nodes), x)
     finally:
         fd.set_option("gather_impl", 1)
-        fd.set_option("checksum_impl", 0)
+        fd.set_option("checksum_impl", old)
 
 
-@pytest.mark.parametrize("hk", [1, 2])
-@pytest.mark.parametrize("dim,rows", [(128, 50_000), (100, 33), (256, 1), (64, 70_001), (384, 4_097)])
+@pytest.mark.parametrize("hk", [1, 2, 3, 4])
+@pytest.mark.parametrize("dim,rows", [(128, 50_000), (100, 33), (256, 1), (64, 70_001), (384, 4_097), (256, 4_128), (100, 65), (768, 999)])
 def test_checksum_kernels_agree(fd, port, hk, dim, rows):
-    """The LDG fused gather+checksum kernels (striped, warp-specialised):
+    """The LDG fused gather+checksum kernels (striped, warp-specialised, pipelined):
     identical rows and trainer checksums, ragged group tails included."""
     n = 40_000
     t = fd.Topology.generate(n, dim, 8, 9)
     table = t.download_rows(0, n)
     nodes = np.random.RandomState(hk + rows).randint(0, n, size=rows).astype(np.uint64)
     old = fd.featdrive.get_option("hash_kernel")
+    old_cs = fd.featdrive.get_option("checksum_impl")
     fd.set_option("gather_impl", 1)
     fd.set_option("checksum_impl", -1)
     fd.set_option("hash_kernel", hk)
@@ -400,4 +402,4 @@ def test_checksum_kernels_agree(fd, port, hk, dim, rows):
             assert cs == port.checksum_rows(x)
     finally:
         fd.set_option("hash_kernel", old)
-        fd.set_option("checksum_impl", 0)
+        fd.set_option("checksum_impl", old_cs)
