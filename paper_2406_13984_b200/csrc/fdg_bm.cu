@@ -6,13 +6,22 @@
 // reference's state transitions and LRU order, computed batch-parallel:
 //
 //   mapping table  node -> packed {i32 slot, u32 valid<<31 | ref}  (8 B/node)
-//   reverse map    slot -> node (~0 = free)
+//   slot table     slot -> {u64 owner node (~0 = free), u64 ring position of its
+//                  live standby entry (~0 = not in the standby list)}: one 16-byte
+//                  record, so the reverse map and list membership share a sector
 //   standby list   the reference's intrusive LRU list becomes a FIFO ring of
 //                  slot ids with tombstones: push_mru = append at `tail`
 //                  (recording the slot's ring position), remove(slot) on a hit
-//                  = clear in_list[slot] (the stale ring entry is skipped
+//                  = clear the slot's position (the stale ring entry is skipped
 //                  later), pop_lru = the next live entry from `head`. An entry
-//                  at position p is live iff in_list[slot] && pos[slot] == p.
+//                  at position p is live iff slot[s].pos == p.
+//
+// The metadata kernels are bound by random DRAM sector accesses (~23 G sectors/s
+// on B200, measured: long-scoreboard stalls at <1 TB/s): every kernel issues all
+// of a thread's independent random loads before its first store (items of one
+// batch are distinct nodes / slots, so there are no hazards between them), and the
+// row traffic of k_move is marked L2 evict-first so the batch's metadata sectors
+// stay L2-resident between acquire, bind and the lag-1 release.
 //
 // extract(nodes):                                   reference
 //   k_acquire  classify + ref++ + standby remove;   acquire_for_batch 241-269
@@ -46,6 +55,12 @@ struct Entry {
     uint32_t refv;
 };
 
+constexpr uint64_t kUnlisted = ~0ull;
+struct __align__(16) SlotMeta {
+    uint64_t node;  // owner (kNoNode = free)
+    uint64_t pos;   // ring position of the live standby entry (kUnlisted = none)
+};
+
 struct BmState {
     uint64_t head, tail;   // ring positions (monotonic)
     uint64_t live;         // standby size
@@ -60,9 +75,7 @@ struct BmState {
 
 struct BmDev {
     Entry* map;
-    uint64_t* reverse;
-    uint64_t* pos;        // slot -> ring position of its live entry
-    uint8_t* in_list;
+    SlotMeta* slot;       // slot -> {owner node, live ring position}
     int32_t* ring[2];
     uint64_t R;           // ring capacity
     uint64_t S;           // slots
@@ -71,7 +84,7 @@ struct BmDev {
     unsigned long long* tiles;  // packed look-back words
     uint32_t* load_pos;   // [max_batch] to-load rank -> batch position
     uint32_t* sel;        // [max_batch] to-load rank -> slot
-    uint8_t* is_load;     // [max_batch]
+    uint8_t* is_load[2];  // [max_batch] per batch parity: acquire of batch j+1 may run under the move of j
     uint64_t max_batch;
 };
 
@@ -153,7 +166,7 @@ __device__ __forceinline__ uint64_t load_n(const uint32_t* n_dev, uint64_t n_hos
 
 // ------------------------------------------------------------- k_acquire ----
 __global__ void __launch_bounds__(kT) k_acquire(BmDev B, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
-                                                int64_t* alias, uint32_t epoch) {
+                                                int64_t* alias, uint8_t* is_load, uint32_t epoch) {
     __shared__ uint32_t s_warp[kT / 32], s_misc[2], s_tile;
     __shared__ unsigned long long s_hits, s_removed;
     BmState* S = B.st;
@@ -171,30 +184,36 @@ __global__ void __launch_bounds__(kT) k_acquire(BmDev B, const uint64_t* nodes, 
     const uint64_t i0 = uint64_t(tile) * kTileN + threadIdx.x * kI;
     uint32_t load_mask = 0, mine = 0, hits = 0, removed = 0;
     bool bad = false;
+    uint64_t nd[kI];
+    Entry en[kI];
+#pragma unroll
+    for (int k = 0; k < kI; ++k) nd[k] = i0 + k < n ? nodes[i0 + k] : kNoNode;
+#pragma unroll
+    for (int k = 0; k < kI; ++k) en[k] = nd[k] < B.N ? B.map[nd[k]] : Entry{-1, 0u};  // all loads in flight
 #pragma unroll
     for (int k = 0; k < kI; ++k) {
-        uint64_t i = i0 + k;
+        const uint64_t i = i0 + k;
         if (i >= n) break;
-        uint64_t node = nodes[i];
+        const uint64_t node = nd[k];
         if (node >= B.N) {
             bad = true;
             continue;
         }
-        Entry e = B.map[node];
-        uint32_t ref = e.refv & kRefMask;
+        const Entry e = en[k];
+        const uint32_t ref = e.refv & kRefMask;
         if (e.refv & kValid) {
             if (ref == 0) {  // StandbyList::remove (buffer_manager.hpp:250)
-                B.in_list[e.slot] = 0;
+                B.slot[e.slot].pos = kUnlisted;
                 ++removed;
             }
             alias[i] = e.slot;
-            B.is_load[i] = 0;
+            is_load[i] = 0;
             ++hits;
         } else if (ref > 0) {
             bad = true;  // in flight elsewhere: impossible for stream-ordered batches
         } else {
             alias[i] = -1;
-            B.is_load[i] = 1;
+            is_load[i] = 1;
             load_mask |= 1u << k;
             ++mine;
         }
@@ -248,12 +267,17 @@ __global__ void __launch_bounds__(kT) k_select(BmDev B, uint32_t epoch) {
             uint64_t p = p0 + threadIdx.x * kI + k;
             slots[k] = -1;
             if (p < tail) {
-                int32_t s = ring[p % B.R];
-                if (B.in_list[s] && B.pos[s] == p) {
-                    slots[k] = s;
-                    live_mask |= 1u << k;
-                    ++mine;
-                }
+                slots[k] = ring[p % B.R];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kI; ++k) {  // list membership: one random 8-byte load per entry, all in flight
+            const uint64_t p = p0 + threadIdx.x * kI + k;
+            if (slots[k] >= 0 && B.slot[slots[k]].pos == p) {
+                live_mask |= 1u << k;
+                ++mine;
+            } else {
+                slots[k] = -1;
             }
         }
         uint32_t r = block_rank(B.tiles, tile, mine, epoch, s_warp, s_misc);
@@ -273,26 +297,29 @@ __global__ void __launch_bounds__(kT) k_select(BmDev B, uint32_t epoch) {
 }
 
 // --------------------------------------------------------------- k_bind ----
+// One miss per thread (grid covers the batch bound): the chain sel -> slot record ->
+// previous owner's entry is three dependent random loads, so parallelism comes
+// from threads, not from a per-thread loop (whose stores would serialise it).
 __global__ void k_bind(BmDev B, const uint64_t* nodes, int64_t* alias) {
     BmState* S = B.st;
     if (S->status) return;
     const uint32_t L = S->n_load;
     uint32_t ev = 0;
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < L) {
         const int32_t slot = B.sel[k];
         const uint32_t i = B.load_pos[k];
         const uint64_t node = nodes[i];
-        const uint64_t prev = B.reverse[slot];
+        const uint64_t prev = B.slot[slot].node;
+        Entry e = B.map[node];
         if (prev != kNoNode) {  // invalidate the previous owner (buffer_manager.hpp:281-291)
-            Entry pe = B.map[prev];
+            const Entry pe = B.map[prev];
             if ((pe.refv & kRefMask) != 0 || pe.slot != slot) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
             B.map[prev] = Entry{-1, 0u};
             ++ev;
         }
-        Entry e = B.map[node];
         B.map[node] = Entry{slot, e.refv | kValid};  // bind + publish
-        B.reverse[slot] = node;
-        B.in_list[slot] = 0;
+        B.slot[slot] = SlotMeta{node, kUnlisted};
         alias[i] = slot;
     }
 #pragma unroll
@@ -306,26 +333,40 @@ __global__ void k_bind(BmDev B, const uint64_t* nodes, int64_t* alias) {
 
 // --------------------------------------------------------------- k_move ----
 // 16-byte chunks over the batch: misses read the table and fill their slot
-// (and X); hits read their slot (into X). Without X only misses move.
+// (and X); hits read their slot (into X). Without X only misses move. Reads only
+// per-batch state (alias, is_load[parity]), so it may run on its own stream while
+// the next batch's acquire / select / bind proceed.
 __global__ void __launch_bounds__(512) k_move(BmDev B, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
-                                              const int64_t* alias, const char* table, char* region, uint32_t rb,
-                                              char* X) {
+                                              const int64_t* alias, const uint8_t* is_load, const char* table,
+                                              char* region, uint32_t rb, char* X) {
     BmState* S = B.st;
     if (S->status) return;
     const uint32_t cpr = rb / 16;
-    const uint64_t n = X ? load_n(n_dev, n_host) : S->n_load;
+    const uint64_t n = load_n(n_dev, n_host);
     const uint64_t total = n * cpr;
+    uint64_t pol;  // row traffic must not flush the batch's metadata sectors out of L2
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     for (uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; c < total; c += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t r = c / cpr, col = c - r * cpr;
-        const uint64_t i = X ? r : B.load_pos[r];
+        const uint64_t i = c / cpr, col = c - i * cpr;
+        const bool miss = is_load[i];
+        if (!miss && !X) continue;
         const int64_t slot = alias[i];
         uint4* dst_slot = reinterpret_cast<uint4*>(region + uint64_t(slot) * rb) + col;
-        if (B.is_load[i]) {
-            uint4 v = reinterpret_cast<const uint4*>(table + nodes[i] * rb)[col];
-            *dst_slot = v;
-            if (X) reinterpret_cast<uint4*>(X + i * rb)[col] = v;
-        } else if (X) {
-            reinterpret_cast<uint4*>(X + i * rb)[col] = *dst_slot;
+        const uint4* src = miss ? reinterpret_cast<const uint4*>(table + nodes[i] * rb) + col : dst_slot;
+        if (miss || X) {
+            uint4 v;
+            asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "l"(src), "l"(pol));
+            if (miss)
+                asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dst_slot), "r"(v.x),
+                             "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+                             : "memory");
+            if (X)
+                asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(
+                                 reinterpret_cast<uint4*>(X + i * rb) + col),
+                             "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+                             : "memory");
         }
     }
 }
@@ -346,16 +387,22 @@ __global__ void __launch_bounds__(kT) k_release(BmDev B, const uint64_t* nodes, 
     uint32_t mask = 0, mine = 0;
     int32_t slots[kI];
     bool bad = false;
+    uint64_t nd[kI];
+    Entry en[kI];
+#pragma unroll
+    for (int k = 0; k < kI; ++k) nd[k] = i0 + k < n ? nodes[i0 + k] : kNoNode;
+#pragma unroll
+    for (int k = 0; k < kI; ++k) en[k] = nd[k] < B.N ? B.map[nd[k]] : Entry{-1, 0u};  // all loads in flight
 #pragma unroll
     for (int k = 0; k < kI; ++k) {
         uint64_t i = i0 + k;
         if (i >= n) break;
-        uint64_t node = nodes[i];
+        uint64_t node = nd[k];
         if (node >= B.N) {
             bad = true;
             continue;
         }
-        Entry e = B.map[node];
+        Entry e = en[k];
         uint32_t ref = e.refv & kRefMask;
         if (!(e.refv & kValid) || ref == 0) {  // buffer_manager.hpp:357, 462
             bad = true;
@@ -377,8 +424,7 @@ __global__ void __launch_bounds__(kT) k_release(BmDev B, const uint64_t* nodes, 
         if (mask & (1u << k)) {  // push_mru in batch order (buffer_manager.hpp:467)
             uint64_t p = tail + r++;
             ring[p % B.R] = slots[k];
-            B.pos[slots[k]] = p;
-            B.in_list[slots[k]] = 1;
+            B.slot[slots[k]].pos = p;
         }
     if (threadIdx.x == 0 && tile == ntiles - 1) {
         uint32_t tot = s_misc[1];
@@ -416,7 +462,7 @@ __global__ void __launch_bounds__(kT) k_compact(BmDev B, uint64_t slack, uint32_
             uint64_t p = p0 + k;
             if (p < tail) {
                 int32_t s = src[p % B.R];
-                if (B.in_list[s] && B.pos[s] == p) {
+                if (B.slot[s].pos == p) {
                     slots[k] = s;
                     mask |= 1u << k;
                     ++mine;
@@ -428,7 +474,7 @@ __global__ void __launch_bounds__(kT) k_compact(BmDev B, uint64_t slack, uint32_
         for (int k = 0; k < kI; ++k)
             if (mask & (1u << k)) {
                 dst[r] = slots[k];
-                B.pos[slots[k]] = r;
+                B.slot[slots[k]].pos = r;
                 ++r;
             }
         if (threadIdx.x == 0 && tile == ntiles - 1) S->new_head = s_misc[1];  // live count
@@ -457,9 +503,7 @@ __global__ void k_init(BmDev B) {
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < B.N; v += stride) B.map[v] = Entry{-1, 0u};
     for (uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; s < B.S; s += stride) {
-        B.reverse[s] = kNoNode;
-        B.pos[s] = s;
-        B.in_list[s] = 1;
+        B.slot[s] = SlotMeta{kNoNode, s};
         B.ring[0][s] = int32_t(s);
     }
 }
@@ -510,9 +554,7 @@ int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint
     auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
     uint64_t sz = 0;
     const uint64_t o_map = sz; sz += al(N * 8);
-    const uint64_t o_rev = sz; sz += al(slot_count * 8);
-    const uint64_t o_pos = sz; sz += al(slot_count * 8);
-    const uint64_t o_inl = sz; sz += al(slot_count);
+    const uint64_t o_slot = sz; sz += al(slot_count * sizeof(SlotMeta));
     const uint64_t o_r0 = sz; sz += al(R * 4);
     const uint64_t o_r1 = sz; sz += al(R * 4);
     const uint64_t o_st = sz; sz += al(sizeof(BmState));
@@ -521,6 +563,7 @@ int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint
     const uint64_t o_lp = sz; sz += al(uint64_t(b->max_batch) * 4);
     const uint64_t o_sel = sz; sz += al(uint64_t(b->max_batch) * 4);
     const uint64_t o_isl = sz; sz += al(uint64_t(b->max_batch));
+    const uint64_t o_isl1 = sz; sz += al(uint64_t(b->max_batch));
     cudaError_t e = cudaMalloc(&b->arena, sz);
     if (e == cudaSuccess) e = cudaMalloc((void**)&b->region, slot_count * ctx->row_bytes);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking);
@@ -532,9 +575,7 @@ int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint
     char* a = static_cast<char*>(b->arena);
     BmDev& d = b->d;
     d.map = reinterpret_cast<Entry*>(a + o_map);
-    d.reverse = reinterpret_cast<uint64_t*>(a + o_rev);
-    d.pos = reinterpret_cast<uint64_t*>(a + o_pos);
-    d.in_list = reinterpret_cast<uint8_t*>(a + o_inl);
+    d.slot = reinterpret_cast<SlotMeta*>(a + o_slot);
     d.ring[0] = reinterpret_cast<int32_t*>(a + o_r0);
     d.ring[1] = reinterpret_cast<int32_t*>(a + o_r1);
     d.R = R;
@@ -544,7 +585,8 @@ int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint
     d.tiles = reinterpret_cast<unsigned long long*>(a + o_tl);
     d.load_pos = reinterpret_cast<uint32_t*>(a + o_lp);
     d.sel = reinterpret_cast<uint32_t*>(a + o_sel);
-    d.is_load = reinterpret_cast<uint8_t*>(a + o_isl);
+    d.is_load[0] = reinterpret_cast<uint8_t*>(a + o_isl);
+    d.is_load[1] = reinterpret_cast<uint8_t*>(a + o_isl1);
     d.max_batch = b->max_batch;
     FDG_CUDA(cudaMemset(d.st, 0, sizeof(BmState)));
     FDG_CUDA(cudaMemset(d.tiles, 0, tiles * 8));
@@ -570,27 +612,66 @@ int fdg_bm_destroy(fdg_bm* b) {
     return FDG_OK;
 }
 
-int fdg_bm_extract(fdg_bm* b, void* stv, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host, int64_t* alias,
-                   void* out, uint64_t* checksum) {
-    cudaStream_t st = (cudaStream_t)stv;
+}  // extern "C"
+
+namespace fdg {
+// Algorithm 1's metadata half for one batch (acquire, LRU pops, bind + publish):
+// strictly stream-ordered with the releases, it fixes the alias list.
+int bm_extract_meta(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                    int64_t* alias, uint32_t parity) {
     const uint64_t bound = n_host;
     if (bound > b->max_batch) return fail(FDG_INVALID_ARG, "bm_extract: batch larger than max_batch_nodes");
     const BmDev& d = b->d;
     k_reset_ctrs<<<1, 32, 0, st>>>(d.st);
-    k_acquire<<<n_tiles_for(bound), kT, 0, st>>>(d, nodes, n_dev, n_host, alias, b->epoch++);
-    k_select<<<bm_persistent_grid(b), kT, 0, st>>>(d, b->epoch++);
-    k_bind<<<std::max<uint32_t>(1, std::min<uint32_t>((bound + 255) / 256, b->ctx->sm_count * 8)), 256, 0, st>>>(
-        d, nodes, alias);
+    {
+        FDG_TRACE("bm_acquire", st);
+        k_acquire<<<n_tiles_for(bound), kT, 0, st>>>(d, nodes, n_dev, n_host, alias, d.is_load[parity & 1],
+                                                    b->epoch++);
+    }
+    {
+        FDG_TRACE("bm_select", st);
+        k_select<<<bm_persistent_grid(b), kT, 0, st>>>(d, b->epoch++);
+    }
+    {
+        FDG_TRACE("bm_bind", st);
+        k_bind<<<std::max<uint32_t>(1, uint32_t((bound + 255) / 256)), 256, 0, st>>>(d, nodes, alias);
+    }
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
+// The row half: misses table -> slot (-> X), hits slot -> X, optional trainer
+// checksum over the batch's slots. Reads only the batch's alias list and
+// is_load[parity], so it can overlap the next batch's metadata half.
+int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                    const int64_t* alias, void* out, uint64_t* checksum, uint32_t parity) {
+    const BmDev& d = b->d;
     const uint32_t rb = b->ctx->row_bytes;
     const char* table = static_cast<const char*>(b->ctx->shard_bases[0]);
-    uint64_t chunks = bound * (rb / 16);
-    int blocks = int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 511) / 512, uint64_t(b->ctx->sm_count) * 4)));
-    k_move<<<blocks, 512, 0, st>>>(d, nodes, n_dev, n_host, alias, table, b->region, rb, static_cast<char*>(out));
+    const uint64_t chunks = n_host * (rb / 16);
+    const int blocks =
+        int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 511) / 512, uint64_t(b->ctx->sm_count) * 4)));
+    {
+        FDG_TRACE("bm_move", st);
+        k_move<<<blocks, 512, 0, st>>>(d, nodes, n_dev, n_host, alias, d.is_load[parity & 1], table, b->region, rb,
+                                       static_cast<char*>(out));
+    }
     FDG_CUDA(cudaGetLastError());
     if (checksum) {
+        FDG_TRACE("bm_checksum", st);
         FDG_TRY(launch_checksum_alias(*b->ctx, st, b->region, alias, n_dev, n_host, checksum, &d.st->status));
     }
     return FDG_OK;
+}
+}  // namespace fdg
+
+extern "C" {
+
+int fdg_bm_extract(fdg_bm* b, void* stv, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host, int64_t* alias,
+                   void* out, uint64_t* checksum) {
+    cudaStream_t st = (cudaStream_t)stv;
+    FDG_TRY(bm_extract_meta(b, st, nodes, n_dev, n_host, alias, 0));
+    return bm_extract_move(b, st, nodes, n_dev, n_host, alias, out, checksum, 0);
 }
 
 int fdg_bm_release(fdg_bm* b, void* stv, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host) {
@@ -598,8 +679,14 @@ int fdg_bm_release(fdg_bm* b, void* stv, const uint64_t* nodes, const uint32_t* 
     const BmDev& d = b->d;
     const uint64_t slack = 2 * uint64_t(b->max_batch) + kTileN;
     k_reset_ctrs<<<1, 32, 0, st>>>(d.st);
-    k_release<<<n_tiles_for(n_host), kT, 0, st>>>(d, nodes, n_dev, n_host, b->epoch++);
-    k_compact<<<bm_persistent_grid(b), kT, 0, st>>>(d, slack, b->epoch++);
+    {
+        FDG_TRACE("bm_release", st);
+        k_release<<<n_tiles_for(n_host), kT, 0, st>>>(d, nodes, n_dev, n_host, b->epoch++);
+    }
+    {
+        FDG_TRACE("bm_compact", st);
+        k_compact<<<bm_persistent_grid(b), kT, 0, st>>>(d, slack, b->epoch++);
+    }
     k_compact_finish<<<1, 1, 0, st>>>(d, slack);
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;
@@ -656,7 +743,7 @@ int fdg_bm_reverse(fdg_bm* b, uint64_t slot, int64_t* node) {
     if (slot >= b->slots) return fail(FDG_OUT_OF_RANGE, "bm_reverse: slot out of range");
     FDG_CUDA(cudaDeviceSynchronize());
     uint64_t v;
-    FDG_CUDA(cudaMemcpy(&v, b->d.reverse + slot, 8, cudaMemcpyDeviceToHost));
+    FDG_CUDA(cudaMemcpy(&v, &b->d.slot[slot].node, 8, cudaMemcpyDeviceToHost));
     *node = v == kNoNode ? -1 : int64_t(v);
     return FDG_OK;
 }
@@ -668,15 +755,17 @@ int fdg_bm_validate(fdg_bm* b) {
     FDG_CUDA(cudaDeviceSynchronize());
     const BmDev& d = b->d;
     std::vector<Entry> map(d.N);
+    std::vector<SlotMeta> meta(d.S);
     std::vector<uint64_t> rev(d.S), pos(d.S);
-    std::vector<uint8_t> inl(d.S);
     BmState h;
     FDG_CUDA(cudaMemcpy(&h, d.st, sizeof(h), cudaMemcpyDeviceToHost));
     if (h.status) return fail(int(h.status), "buffer manager in error state " + std::to_string(h.status));
     FDG_CUDA(cudaMemcpy(map.data(), d.map, d.N * 8, cudaMemcpyDeviceToHost));
-    FDG_CUDA(cudaMemcpy(rev.data(), d.reverse, d.S * 8, cudaMemcpyDeviceToHost));
-    FDG_CUDA(cudaMemcpy(pos.data(), d.pos, d.S * 8, cudaMemcpyDeviceToHost));
-    FDG_CUDA(cudaMemcpy(inl.data(), d.in_list, d.S, cudaMemcpyDeviceToHost));
+    FDG_CUDA(cudaMemcpy(meta.data(), d.slot, d.S * sizeof(SlotMeta), cudaMemcpyDeviceToHost));
+    for (uint64_t s = 0; s < d.S; ++s) {
+        rev[s] = meta[s].node;
+        pos[s] = meta[s].pos;
+    }
     std::vector<int32_t> ring(d.R);
     FDG_CUDA(cudaMemcpy(ring.data(), d.ring[h.ring_sel], d.R * 4, cudaMemcpyDeviceToHost));
     std::vector<uint8_t> seen(d.S, 0);
@@ -693,7 +782,7 @@ int fdg_bm_validate(fdg_bm* b) {
     uint64_t live = 0;
     for (uint64_t p = h.head; p < h.tail; ++p) {
         int32_t s = ring[p % d.R];
-        if (!(inl[s] && pos[s] == p)) continue;
+        if (pos[s] != p) continue;
         ++live;
         if (rev[s] != kNoNode && (map[rev[s]].refv & kRefMask) != 0)
             return fail(FDG_INVARIANT, "standby slot whose node still holds references");

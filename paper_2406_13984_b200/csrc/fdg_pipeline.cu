@@ -35,6 +35,10 @@ int sampler_sample_group(Sampler* s, cudaStream_t st, uint32_t n, const uint64_t
 void sampler_capacity(const Sampler* s, uint64_t* max_nodes, uint64_t* max_edges);
 void sampler_hash_region(const Sampler* s, void** base, uint64_t* bytes);
 int bm_status_to(fdg_bm* b, cudaStream_t st, uint32_t* dst);
+int bm_extract_meta(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                    int64_t* alias, uint32_t parity);
+int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                    const int64_t* alias, void* out, uint64_t* checksum, uint32_t parity);
 }  // namespace fdg
 
 struct fdg_pipeline {
@@ -44,7 +48,10 @@ struct fdg_pipeline {
     std::vector<cudaStream_t> sstream;
     std::vector<cudaStream_t> mstream;   // per-sampler MT prefetch streams
     cudaStream_t xstream = nullptr;
-    cudaStream_t xstream2 = nullptr;     // second extraction stream (plain gathers alternate)
+    cudaStream_t xstream2 = nullptr;     // second extraction stream (plain gathers alternate; with the
+                                         // buffer manager: the row-move stream)
+    cudaEvent_t bound[2] = {nullptr, nullptr};  // buffer manager: batch parity's metadata half done
+    cudaEvent_t moved[2] = {nullptr, nullptr};  // buffer manager: batch parity's row move done
     uint64_t cap = 0, max_nodes = 0;
     uint32_t nslots = 0;             // per-batch output slots (2 * S * G)
     std::vector<uint64_t*> nodes;
@@ -85,6 +92,8 @@ void destroy(fdg_pipeline* p) {
     for (auto e : p->extracted) cudaEventDestroy(e);
     for (auto e : p->tev) cudaEventDestroy(e);
     for (auto e : p->sev) cudaEventDestroy(e);
+    for (auto e : p->bound) if (e) cudaEventDestroy(e);
+    for (auto e : p->moved) if (e) cudaEventDestroy(e);
     if (p->counts) cudaFree(p->counts);
     if (p->t0) cudaEventDestroy(p->t0);
     if (p->bm) fdg_bm_destroy(p->bm);
@@ -166,8 +175,15 @@ int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers
     // Plain gathers of consecutive batches alternate between two streams so the tail
     // of one overlaps the head of the next (the buffer-manager path is stateful and
     // stays on one stream).
-    if (!cfg->use_buffer_manager && g_extract_streams > 1)
+    // With the buffer manager the row moves get their own stream: batch j's move
+    // overlaps batch j+1's acquire / select / bind (the metadata chain stays in order).
+    if (cfg->use_buffer_manager || g_extract_streams > 1)
         FDG_CUDA(cudaStreamCreateWithPriority(&p->xstream2, cudaStreamNonBlocking, prio_lo));
+    if (cfg->use_buffer_manager)
+        for (int i = 0; i < 2; ++i) {
+            FDG_CUDA(cudaEventCreateWithFlags(&p->bound[i], cudaEventDisableTiming));
+            FDG_CUDA(cudaEventCreateWithFlags(&p->moved[i], cudaEventDisableTiming));
+        }
     // one MT stream per sampler: prefetch launches of different samplers overlap
     for (uint32_t i = 0; i < S; ++i) {
         cudaStream_t st;
@@ -340,7 +356,8 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
             // extract-only diagnostics re-extract the batches sampled in the first groups
             const uint64_t src_j = do_sample ? j : (j % (sampled_groups * G));
             fdg_batch_counts* cnt = p->counts + src_j;
-            cudaStream_t xs = (p->xstream2 && (j & 1)) ? p->xstream2 : p->xstream;
+            cudaStream_t xs = (!p->bm && p->xstream2 && (j & 1)) ? p->xstream2 : p->xstream;
+            cudaStream_t xe = p->bm ? p->xstream2 : xs;  // stream on which the batch's extraction ends
             if (sample_only) {
                 FDG_CUDA(cudaEventRecord(p->extracted[slot], xs));
                 continue;
@@ -355,24 +372,33 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 FDG_TRY(launch_gather_bound(*p->ctx, xs, p->nodes[nslot], n_dev, p->cap, p->cap, X, cs,
                                             &cnt->status));
             } else {
-                FDG_TRY(fdg_bm_extract(p->bm, p->xstream, p->nodes[nslot], n_dev, p->cap, p->alias[j & 1], X, cs));
-                FDG_TRY(bm_status_to(p->bm, p->xstream, &cnt->status));  // e.g. CAPACITY = StandbyTimeout
+                const uint32_t par = uint32_t(j & 1);
+                // alias[par], is_load[par] and X[par] were last used by batch j-2's move
+                if (j >= 2) FDG_CUDA(cudaStreamWaitEvent(p->xstream, p->moved[par], 0));
+                FDG_TRY(bm_extract_meta(p->bm, p->xstream, p->nodes[nslot], n_dev, p->cap, p->alias[par], par));
+                FDG_CUDA(cudaEventRecord(p->bound[par], p->xstream));
+                FDG_CUDA(cudaStreamWaitEvent(xe, p->bound[par], 0));
+                FDG_TRY(bm_extract_move(p->bm, xe, p->nodes[nslot], n_dev, p->cap, p->alias[par], X, cs, par));
+                FDG_TRY(bm_status_to(p->bm, xe, &cnt->status));  // e.g. CAPACITY = StandbyTimeout
+                FDG_CUDA(cudaEventRecord(p->moved[par], xe));
                 if (j > 0) {  // lag-1 release (the releaser stage, pipeline.hpp:525-543)
                     const uint64_t pj = do_sample ? j - 1 : ((j - 1) % (sampled_groups * G));
+                    // batch j-1's move reads its node list: the list is free once both are done
+                    FDG_CUDA(cudaStreamWaitEvent(p->xstream, p->moved[par ^ 1], 0));
                     FDG_TRY(fdg_bm_release(p->bm, p->xstream, p->nodes[pj % p->nslots], &p->counts[pj].n_nodes,
                                            p->cap));
-                    // batch j-1's node list is free only once it has been released
                     FDG_CUDA(cudaEventRecord(p->extracted[(j - 1) % p->nslots], p->xstream));
                 }
             }
-            if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j + 1], xs));
+            if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j + 1], xe));
             if (records_host)  // device -> host read of the batch record (counts + checksum)
-                FDG_CUDA(cudaMemcpyAsync(records_host + j, cnt, sizeof(fdg_batch_counts), cudaMemcpyDeviceToHost, xs));
+                FDG_CUDA(cudaMemcpyAsync(records_host + j, cnt, sizeof(fdg_batch_counts), cudaMemcpyDeviceToHost, xe));
             if (!p->bm) FDG_CUDA(cudaEventRecord(p->extracted[slot], xs));
         }
     }
     if (p->bm && !sample_only) {  // drain: release the last batch
         const uint64_t lj = extract_only ? (n_batches - 1) % (sampled_groups * G) : n_batches - 1;
+        FDG_CUDA(cudaStreamWaitEvent(p->xstream, p->moved[(n_batches - 1) & 1], 0));
         FDG_TRY(fdg_bm_release(p->bm, p->xstream, p->nodes[lj % p->nslots], &p->counts[lj].n_nodes, p->cap));
         FDG_CUDA(cudaEventRecord(p->extracted[(n_batches - 1) % p->nslots], p->xstream));
     }

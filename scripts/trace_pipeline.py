@@ -25,7 +25,10 @@ order = np.concatenate(fd.partition_epoch(np.arange(t_ids, dtype=np.uint64), B, 
 K = 200
 rng = np.array([L.fdg_batch_seed(0, 0, int(g)) for g in range(K)], np.uint64)
 seeds = DeviceBuffer.from_array(np.ascontiguousarray(order[:K * B]))
-cfg = _lib.PipelineConfig(batch_size=B, n_samplers=S, prefetch_group=16, write_x=1)
+import os
+bm_slots = int(os.environ.get("BM", "0"))
+cfg = _lib.PipelineConfig(batch_size=B, n_samplers=S, prefetch_group=16, write_x=1,
+                          use_buffer_manager=1 if bm_slots else 0, buffer_slots=bm_slots)
 f = np.ascontiguousarray(fan, np.uint32)
 p = C.c_void_p()
 fd.featdrive.check(L.fdg_pipeline_create(topo.ctx, f.ctypes.data_as(C.c_void_p), len(f), C.byref(cfg), C.byref(p)))
