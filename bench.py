@@ -372,6 +372,8 @@ def run_ours(args):
                 "includes": "seed H2D, sample, extract, fused trainer checksum, batch-record D2H"},
         "clocks": clk.summary(),
     }
+    if args.train:
+        line["train_stage"] = _train_stage(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist)
     if dist.world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"], line["checksum_match_vs_reference"] = _cpu_baseline(cfg, topo, order, args, gpu_cs,
@@ -385,6 +387,31 @@ def run_ours(args):
     if sharded:
         sharded.close()
     dist.close()
+
+
+def _train_stage(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist):
+    """sample -> extract -> GraphSAGE forward + loss (the paper's 3-layer model, hidden 256,
+    PAPER.md:405, 1122-1125) per batch through the same runner, device-resident seeds."""
+    from paper_2406_13984_b200.featdrive import DeviceBuffer
+    dim = topo.row_bytes // 4
+    classes = 172  # ogbn-papers100M label count
+    dims = [dim] + [256] * (len(fan) - 1) + [classes]
+    model = fd.GraphSAGE(topo, dims, fan, max_seeds=B, seed=0)
+    pipe = Pipeline(fd, topo, fan, B, bm_slots=bm_slots, checksum=False, samplers=args.samplers, group=args.group)
+    pipe.set_model(model, label_seed=0)
+    warm = DeviceBuffer.from_array(seeds_for(ids_warm))
+    timed = DeviceBuffer.from_array(seeds_for(ids))
+    pipe.run(warm.ptr, False, rng_of(ids_warm))
+    dist.barrier()
+    ms = dist.reduce(pipe.run(timed.ptr, False, rng_of(ids)), "max")
+    losses = pipe.losses(len(ids))
+    pipe.close()
+    model.close()
+    K = len(ids)
+    return {"value": dist.reduce(K, "sum") / (ms / 1e3), "unit": "batches/s", "ms_per_step": ms / K,
+            "model": "GraphSAGE mean-aggregator " + "-".join(map(str, dims)) + ", fp32 CUDA-core GEMMs",
+            "mean_loss": float(np.mean(losses)), "finite": bool(np.all(np.isfinite(losses))),
+            "includes": "sample + extract + per-layer scatter-mean + GEMM + bias/ReLU + softmax cross-entropy"}
 
 
 def _union_ms(starts, ends):
@@ -471,6 +498,8 @@ def main():
     ap.add_argument("--shard", action="store_true",
                     help="N>1: row-shard the feature table across GPUs (remote rows over NVLink P2P)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--train", action="store_true",
+                    help="also time sample -> extract -> GraphSAGE forward + loss (key train_stage)")
     ap.add_argument("--cpu-batches", type=int, default=0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

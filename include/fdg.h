@@ -276,6 +276,34 @@ int fdg_pipeline_records(fdg_pipeline* p, uint64_t first, uint64_t n, fdg_batch_
  * launches alternating over the two extraction streams can be unioned). */
 int fdg_pipeline_extract_times(fdg_pipeline* p, uint64_t first, uint64_t n, float* start_ms, float* end_ms);
 
+/* ---- train stage: GraphSAGE forward + loss on a sampled batch --------------------------
+ * The consumer of the mini-batch tensor. The reference's trainer is a checksum
+ * (trainer_step, pipeline.hpp:103-124); the paper trains a 3-layer GraphSAGE on these
+ * blocks. Model (PyG SAGEConv, mean aggregator): layer
+ * k = 1..L computes local nodes [0, D_{L-k}), D_j = layer_nodes[j+1] (nodes within j
+ * hops), as h_v = W_neigh . mean_{(u->v) in edges} h_u + W_self . h_v + b, ReLU between
+ * layers, h^0 = X; loss = mean softmax cross-entropy over the unique seeds with
+ * label(v) = splitmix64(node_id ^ label_seed) % dims[L]. fp32 (CUDA-core FMA).
+ * dims: L+1 widths, dims[0] = feature width of the context's table (f32 or f16), every
+ * dim a multiple of 4; fanouts / max_seeds bound the block sizes (sampling.hpp:32-40). */
+typedef struct fdg_sage fdg_sage;
+int fdg_sage_create(fdg_ctx* ctx, const uint32_t* dims, uint32_t n_layers, const uint32_t* fanouts,
+                    uint32_t max_seeds, fdg_sage** out);
+int fdg_sage_destroy(fdg_sage* m);
+/* Host fp32 weights of layer `layer`: w_neigh, w_self [dims[layer]][dims[layer+1]] row-major
+ * (input-major: out = in . W), bias [dims[layer+1]] (NULL = 0). */
+int fdg_sage_set_layer(fdg_sage* m, uint32_t layer, const float* w_neigh, const float* w_self, const float* bias);
+/* Stream-ordered forward on one batch: x_dev = X [n_nodes][dims[0]] (table dtype), nodes /
+ * edges / counts as written by fdg_sample_khop. *loss_dev (device float) = the loss;
+ * logits_dev (nullable) = [D_0][dims[L]]. */
+int fdg_sage_forward(fdg_sage* m, void* stream, const void* x_dev, const uint64_t* nodes_dev,
+                     const uint32_t* edges_dev, const fdg_batch_counts* counts_dev, uint64_t label_seed,
+                     float* loss_dev, float* logits_dev);
+/* Run the model after each batch's extraction inside fdg_pipeline_run (NULL = off; the
+ * pipeline must materialise X). Per-batch losses of the last run: fdg_pipeline_losses. */
+int fdg_pipeline_set_model(fdg_pipeline* p, fdg_sage* m, uint64_t label_seed);
+int fdg_pipeline_losses(fdg_pipeline* p, uint64_t first, uint64_t n, float* out);
+
 /* ---- tracing: per-launch CUDA-event timeline (DurationCounter analogue, common.hpp:240-260) */
 int fdg_trace_enable(int on);          /* clears previous records when turning on */
 int fdg_trace_dump(const char* path);  /* CSV: name,stream,start_ms,end_ms       */

@@ -116,6 +116,12 @@ SIGNATURES = {
     "fdg_pipeline_sample_times": (ci, [vp, vp, vp]),
     "fdg_pipeline_bm_stats": (ci, [vp, C.POINTER(BmStats)]),
     "fdg_pipeline_get_config": (ci, [vp, C.POINTER(PipelineConfig)]),
+    "fdg_sage_create": (ci, [vp, vp, u32, vp, u32, C.POINTER(vp)]),
+    "fdg_sage_destroy": (ci, [vp]),
+    "fdg_sage_set_layer": (ci, [vp, u32, vp, vp, vp]),
+    "fdg_sage_forward": (ci, [vp, vp, vp, vp, vp, vp, u64, vp, vp]),
+    "fdg_pipeline_set_model": (ci, [vp, vp, u64]),
+    "fdg_pipeline_losses": (ci, [vp, u64, u64, vp]),
     "fdg_partition_epoch": (ci, [vp, u64, u64, u64, vp]),
     "fdg_batch_seed": (u64, [u64, u64, u64]),
 }

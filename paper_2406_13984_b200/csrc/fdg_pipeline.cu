@@ -67,6 +67,11 @@ struct fdg_pipeline {
     std::vector<cudaEvent_t> sev;        // per-group sampling timing events (2 per group)
     uint64_t timed_groups = 0;
     fdg_bm* bm = nullptr;
+    fdg_sage* model = nullptr;           // optional train stage after each extraction
+    uint64_t label_seed = 0;
+    float* losses = nullptr;             // device, one per batch of the current run
+    uint64_t losses_cap = 0;
+    uint64_t loss_batches = 0;           // batches of the last run with a loss
     cudaEvent_t t0 = nullptr;            // start of the last run (timing base)
     uint64_t timed_batches = 0;          // batches of the last run with extraction events
 };
@@ -95,6 +100,7 @@ void destroy(fdg_pipeline* p) {
     for (auto e : p->bound) if (e) cudaEventDestroy(e);
     for (auto e : p->moved) if (e) cudaEventDestroy(e);
     if (p->counts) cudaFree(p->counts);
+    if (p->losses) cudaFree(p->losses);
     if (p->t0) cudaEventDestroy(p->t0);
     if (p->bm) fdg_bm_destroy(p->bm);
     delete p;
@@ -274,6 +280,13 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
         }
     }
     const bool sample_only = p->cfg.flags & FDG_PIPE_SAMPLE_ONLY;
+    const bool train = p->model != nullptr && !sample_only;
+    if (train && p->losses_cap < n_batches) {
+        if (p->losses) cudaFree(p->losses);
+        FDG_CUDA(cudaMalloc(&p->losses, n_batches * sizeof(float)));
+        p->losses_cap = n_batches;
+    }
+    p->loss_batches = 0;
     const bool extract_only = p->cfg.flags & FDG_PIPE_EXTRACT_ONLY;
     const uint64_t n_groups = (n_batches + G - 1) / G;
     const uint64_t sampled_groups = extract_only ? std::min<uint64_t>(n_groups, 2 * S) : n_groups;
@@ -356,7 +369,8 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
             // extract-only diagnostics re-extract the batches sampled in the first groups
             const uint64_t src_j = do_sample ? j : (j % (sampled_groups * G));
             fdg_batch_counts* cnt = p->counts + src_j;
-            cudaStream_t xs = (!p->bm && p->xstream2 && (j & 1)) ? p->xstream2 : p->xstream;
+            // the train stage shares one model workspace: with a model the plain gathers stay on one stream
+            cudaStream_t xs = (!p->bm && !train && p->xstream2 && (j & 1)) ? p->xstream2 : p->xstream;
             cudaStream_t xe = p->bm ? p->xstream2 : xs;  // stream on which the batch's extraction ends
             if (sample_only) {
                 FDG_CUDA(cudaEventRecord(p->extracted[slot], xs));
@@ -371,6 +385,9 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
             if (!p->bm) {
                 FDG_TRY(launch_gather_bound(*p->ctx, xs, p->nodes[nslot], n_dev, p->cap, p->cap, X, cs,
                                             &cnt->status));
+                if (train)
+                    FDG_TRY(fdg_sage_forward(p->model, xs, X, p->nodes[nslot], p->edges[nslot], cnt, p->label_seed,
+                                             p->losses + j, nullptr));
             } else {
                 const uint32_t par = uint32_t(j & 1);
                 // alias[par], is_load[par] and X[par] were last used by batch j-2's move
@@ -380,6 +397,9 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 FDG_CUDA(cudaStreamWaitEvent(xe, p->bound[par], 0));
                 FDG_TRY(bm_extract_move(p->bm, xe, p->nodes[nslot], n_dev, p->cap, p->alias[par], X, cs, par));
                 FDG_TRY(bm_status_to(p->bm, xe, &cnt->status));  // e.g. CAPACITY = StandbyTimeout
+                if (train)  // the trainer consumes X (and the batch's blocks) before they are reused
+                    FDG_TRY(fdg_sage_forward(p->model, xe, X, p->nodes[nslot], p->edges[nslot], cnt, p->label_seed,
+                                             p->losses + j, nullptr));
                 FDG_CUDA(cudaEventRecord(p->moved[par], xe));
                 if (j > 0) {  // lag-1 release (the releaser stage, pipeline.hpp:525-543)
                     const uint64_t pj = do_sample ? j - 1 : ((j - 1) % (sampled_groups * G));
@@ -424,6 +444,7 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
             FDG_CUDA(cudaEventElapsedTime(extract_ms + j, p->tev[2 * j], p->tev[2 * j + 1]));
     cudaEventDestroy(t1);
     if (extract_ms && !sample_only) p->timed_batches = n_batches;
+    if (train) p->loss_batches = n_batches;
     if (extract_ms) p->timed_groups = sampled_groups;
     return FDG_OK;
 }
@@ -452,6 +473,19 @@ int fdg_pipeline_sample_times(fdg_pipeline* p, uint64_t* n_groups, float* busy_m
     }
     if (n_groups) *n_groups = p->timed_groups;
     if (busy_ms) *busy_ms = tot;
+    return FDG_OK;
+}
+
+int fdg_pipeline_set_model(fdg_pipeline* p, fdg_sage* m, uint64_t label_seed) {
+    if (m && !p->cfg.write_x) return fail(FDG_INVALID_ARG, "pipeline_set_model: the train stage needs X (write_x)");
+    p->model = m;
+    p->label_seed = label_seed;
+    return FDG_OK;
+}
+
+int fdg_pipeline_losses(fdg_pipeline* p, uint64_t first, uint64_t n, float* out) {
+    if (first + n > p->loss_batches) return fail(FDG_INVALID_ARG, "pipeline_losses: range beyond the last run's batches");
+    FDG_CUDA(cudaMemcpy(out, p->losses + first, n * sizeof(float), cudaMemcpyDeviceToHost));
     return FDG_OK;
 }
 

@@ -515,6 +515,16 @@ class Pipeline:
                                             records_ptr, _p(extract_ms), C.byref(ms)))
         return ms.value
 
+    def set_model(self, model: "GraphSAGE | None", label_seed: int = 0):
+        """Run the train stage (GraphSAGE forward + loss) after every extraction."""
+        self.model = model
+        check(lib().fdg_pipeline_set_model(self.ptr, model.ptr if model else None, label_seed))
+
+    def losses(self, n: int, first: int = 0) -> np.ndarray:
+        out = np.empty(n, np.float32)
+        check(lib().fdg_pipeline_losses(self.ptr, first, n, _p(out)))
+        return out
+
     def sample_busy_ms(self) -> float:
         """Sampling-stage busy time of the last run (run with extract_ms)."""
         ms = C.c_float()
@@ -577,3 +587,79 @@ def trainer_step(batch: SampledBatch, alias: np.ndarray, buffer: BufferManager) 
     check(lib().fdg_checksum_alias(buffer.topo.ctx, None, buffer.region_ptr, ad.ptr, None, len(alias), cs.ptr))
     check(lib().fdg_device_sync())
     return int(cs.download(np.uint64)[0])
+
+
+# -------------------------------------------------------------- train stage --
+class GraphSAGE:
+    """The train stage behind fdg_sage_* (include/fdg.h): GraphSAGE forward + loss over a
+    sampled batch's blocks, fed from the mini-batch tensor X. The reference's trainer is
+    the checksum above (pipeline.hpp:103-124); the paper's model is a 3-layer GraphSAGE,
+    hidden 256. Layer k computes local nodes [0, D_{L-k}),
+    D_j = layer_nodes[j+1]: h_v = W_neigh . mean_{u->v} h_u + W_self . h_v + b (ReLU
+    between layers); loss = mean softmax cross-entropy over the unique seeds with
+    label(v) = splitmix64(v ^ label_seed) % dims[-1]. fp32 on the GPU."""
+
+    def __init__(self, topo: Topology, dims, fanouts, max_seeds: int = 1000, seed: int = 0, weights=None):
+        self.topo = topo
+        self.dims = [int(d) for d in dims]
+        fan = list(fanouts.per_layer if isinstance(fanouts, Fanouts) else fanouts)
+        if len(fan) != len(self.dims) - 1:
+            raise InvalidArgument("GraphSAGE: one layer per sampling hop (len(dims) == len(fanouts) + 1)")
+        d = np.ascontiguousarray(self.dims, np.uint32)
+        f = np.ascontiguousarray(fan, np.uint32)
+        p = C.c_void_p()
+        check(lib().fdg_sage_create(topo.ctx, _p(d), len(f), _p(f), max_seeds, C.byref(p)))
+        self.ptr = p.value
+        self.weights = weights if weights is not None else GraphSAGE.init_weights(self.dims, seed)
+        for layer, (wn, ws, b) in enumerate(self.weights):
+            wn, ws, b = (np.ascontiguousarray(a, np.float32) for a in (wn, ws, b))
+            check(lib().fdg_sage_set_layer(self.ptr, layer, _p(wn), _p(ws), _p(b)))
+
+    @staticmethod
+    def init_weights(dims, seed: int = 0):
+        """Glorot-uniform W_neigh / W_self ([d_in, d_out], input-major) and small biases."""
+        rng = np.random.default_rng(seed)
+        out = []
+        for din, dout in zip(dims[:-1], dims[1:]):
+            a = np.sqrt(6.0 / (din + dout))
+            out.append((rng.uniform(-a, a, (din, dout)).astype(np.float32),
+                        rng.uniform(-a, a, (din, dout)).astype(np.float32),
+                        rng.uniform(-0.1, 0.1, dout).astype(np.float32)))
+        return out
+
+    def forward_async(self, stream, x_ptr: int, nodes_ptr: int, edges_ptr: int, counts_ptr: int, label_seed: int,
+                      loss_ptr: int, logits_ptr: int | None = None):
+        check(lib().fdg_sage_forward(self.ptr, stream.ptr if stream else None, x_ptr, nodes_ptr, edges_ptr,
+                                     counts_ptr, label_seed, loss_ptr, logits_ptr))
+
+    def forward(self, batch: SampledBatch, label_seed: int = 0):
+        """Host convenience: X gathered on the device from the batch's nodes, then the
+        forward; returns (loss, logits of the unique seeds)."""
+        n, e = len(batch.nodes), len(batch.edges)
+        cnt = _lib.BatchCounts()
+        cnt.n_nodes, cnt.n_edges, cnt.n_layers = n, e, len(batch.layer_nodes) - 2
+        for i, v in enumerate(batch.layer_nodes):
+            cnt.layer_nodes[i] = int(v)
+        for i, v in enumerate(batch.layer_edges):
+            cnt.layer_edges[i] = int(v)
+        cd = DeviceBuffer(C.sizeof(cnt))
+        check(lib().fdg_memcpy_h2d(cd.ptr, C.addressof(cnt), C.sizeof(cnt), None))
+        nd = DeviceBuffer.from_array(batch.nodes) if n else DeviceBuffer(8)
+        ed = DeviceBuffer.from_array(np.ascontiguousarray(batch.edges, np.uint32)) if e else DeviceBuffer(8)
+        x = DeviceBuffer(max(n, 1) * self.topo.row_bytes)
+        if n:
+            check(lib().fdg_gather(self.topo.ctx, None, nd.ptr, None, n, x.ptr, None))
+        loss = DeviceBuffer(4)
+        seeds = int(max(batch.layer_nodes[:2])) if len(batch.layer_nodes) > 1 else 0
+        logits = DeviceBuffer(max(seeds, 1) * self.dims[-1] * 4)
+        self.forward_async(None, x.ptr, nd.ptr, ed.ptr, cd.ptr, label_seed, loss.ptr, logits.ptr)
+        check(lib().fdg_device_sync())
+        return (float(loss.download(np.float32)[0]),
+                logits.download(np.float32, seeds * self.dims[-1]).reshape(seeds, self.dims[-1]))
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            lib().fdg_sage_destroy(self.ptr)
+            self.ptr = None
+
+    __del__ = close

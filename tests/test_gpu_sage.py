@@ -1,0 +1,108 @@
+"""GPU parity of the train stage (fdg_sage_*): GraphSAGE forward + loss on sampled
+blocks, fp32 on the GPU against the fp64 restatement oracle/sage.py. Tolerance:
+loss within 1e-5 relative (BASELINE.json north_star), logits within 1e-4 relative /
+1e-5 absolute."""
+import numpy as np
+import pytest
+
+from oracle import sage
+
+pytestmark = pytest.mark.gpu
+
+LOSS_RTOL = 1e-5
+
+
+def _rows(t, nodes, dtype):
+    table = t.download_rows(0, t.num_nodes)
+    return table.view(dtype)[nodes.astype(np.int64)]
+
+
+def _check(model, t, batch, dtype, label_seed):
+    loss, logits = model.forward(batch, label_seed)
+    want, want_logits = sage.sage_forward(_rows(t, batch.nodes, dtype), batch.nodes, batch.edges,
+                                          batch.layer_nodes, model.weights, label_seed)
+    assert abs(loss - want) <= LOSS_RTOL * abs(want), (loss, want)
+    np.testing.assert_allclose(logits, want_logits, rtol=1e-4, atol=1e-5)
+    return loss
+
+
+@pytest.mark.parametrize("dim,dims,fan,seeds", [
+    (32, [32, 64, 64, 12], [10, 10, 10], 300),
+    (128, [128, 256, 256, 172], [10, 10, 10], 200),   # the paper's Papers100M model shape
+    (64, [64, 132, 40], [15, 10], 257),               # ragged GEMM tiles (N = 132, 40)
+    (16, [16, 8], [25], 1000),
+])
+def test_sage_forward_vs_oracle(fd, dim, dims, fan, seeds):
+    t = fd.Topology.generate(60_000, dim, 12, 5)
+    s = np.random.RandomState(dim).randint(0, 60_000, seeds).astype(np.uint64)
+    batch = fd.sample_khop(t, s, fan, fd.batch_seed(0, 0, dim))
+    model = fd.GraphSAGE(t, dims, fan, max_seeds=seeds, seed=dim)
+    _check(model, t, batch, np.float32, 0x1234)
+    _check(model, t, batch, np.float32, 99)  # a second forward reuses the workspace
+
+
+def test_sage_forward_fp16_table(fd):
+    """MAG240M-style f16 feature rows: aggregation upconverts to fp32."""
+    t = fd.Topology.generate(40_000, 96, 8, 11, dtype="f16")
+    s = np.arange(0, 40_000, 97, dtype=np.uint64)
+    batch = fd.sample_khop(t, s, [10, 5], 31)
+    model = fd.GraphSAGE(t, [96, 64, 20], [10, 5], max_seeds=len(s), seed=3)
+    _check(model, t, batch, np.float16, 7)
+
+
+def test_sage_zero_degree_and_early_stop(fd):
+    """Seeds without in-edges (mean aggregates 0), duplicate seeds and a frontier that
+    empties before the last hop (D_j of unreached hops = all nodes)."""
+    n = 2000
+    rs = np.random.RandomState(4)
+    indptr = [0]
+    indices = []
+    for v in range(n):
+        nb = [] if v < 1000 else sorted(set(rs.randint(1000, n, rs.randint(1, 6)).tolist()) - {v})
+        indices += nb
+        indptr.append(len(indices))
+    feats = rs.standard_normal((n, 8)).astype(np.float32)
+    t = fd.Topology.from_arrays(np.array(indptr, np.uint64), np.array(indices, np.uint64), feats)
+    seeds = np.array([5, 5, 17, 1500, 1999, 3, 1200], np.uint64)
+    batch = fd.sample_khop(t, seeds, [4, 4, 4], 9)
+    model = fd.GraphSAGE(t, [8, 12, 4, 8], [4, 4, 4], max_seeds=len(seeds), seed=1)
+    _check(model, t, batch, np.float32, 3)
+    only_isolated = fd.sample_khop(t, np.array([1, 2, 3], np.uint64), [4, 4, 4], 9)
+    assert len(only_isolated.edges) == 0
+    _check(model, t, only_isolated, np.float32, 3)
+
+
+def test_sage_bad_config(fd):
+    t = fd.Topology.generate(1000, 16, 4, 1)
+    with pytest.raises(fd.InvalidArgument):
+        fd.GraphSAGE(t, [32, 8], [5])       # dims[0] != feature width
+    with pytest.raises(fd.InvalidArgument):
+        fd.GraphSAGE(t, [16, 6], [5])       # not a multiple of 4
+    with pytest.raises(fd.InvalidArgument):
+        fd.GraphSAGE(t, [16, 8, 4], [5])    # one layer per hop
+
+
+@pytest.mark.parametrize("bm", [False, True])
+def test_pipeline_train_stage(fd, bm):
+    """The runner's train stage: per-batch losses equal the standalone forward on the
+    same batch (same kernels, same bytes -> bitwise) and the fp64 oracle (1e-5)."""
+    n, B, fan = 200_000, 256, [10, 5, 5]
+    t = fd.Topology.generate(n, 32, 12, 3)
+    order = np.concatenate(fd.partition_epoch(np.arange(12 * B, dtype=np.uint64), B, 77))
+    nb = 12
+    rng = np.array([fd.batch_seed(0, 0, b) for b in range(nb)], np.uint64)
+    model = fd.GraphSAGE(t, [32, 64, 64, 16], fan, max_seeds=B, seed=2)
+    pipe = fd.Pipeline(t, fan, B, buffer_slots=(150_000 if bm else None), checksum=True, samplers=2)
+    pipe.set_model(model, label_seed=5)
+    recs = pipe.run_batches(order, rng)
+    losses = pipe.losses(nb)
+    pipe.close()
+    assert np.all(recs["status"] == 0)
+    for b in range(nb):
+        batch = fd.sample_khop(t, order[b * B:(b + 1) * B], fan, int(rng[b]))
+        loss, _ = model.forward(batch, 5)
+        assert losses[b] == np.float32(loss), b
+        if b < 3:
+            want, _ = sage.sage_forward(_rows(t, batch.nodes, np.float32), batch.nodes, batch.edges,
+                                        batch.layer_nodes, model.weights, 5)
+            assert abs(loss - want) <= LOSS_RTOL * abs(want)

@@ -156,3 +156,46 @@ def test_port_vs_ref_live_buffer(port, ref):
             b.release(old)
         np.testing.assert_array_equal(a.stats(), b.stats())
     a.validate()
+
+
+def _torch_sage(x, nodes, edges, layer_nodes, weights, label_seed):
+    """Independent formulation of the train stage (torch fp64, index_add_ scatter-mean
+    per layer over the dst-sorted block edges) used to pin oracle/sage.py."""
+    import torch
+    L = len(weights)
+    ln = [int(v) for v in layer_nodes]
+    D = [min(max(ln[: j + 2]), len(nodes)) for j in range(L + 1)]
+    h = torch.tensor(np.asarray(x, np.float64))
+    e = torch.tensor(np.asarray(edges, np.int64)).reshape(-1, 2)
+    for k in range(1, L + 1):
+        rows = D[L - k]
+        wn, ws, b = (torch.tensor(np.asarray(a, np.float64)) for a in weights[k - 1])
+        m = e[:, 1] < rows
+        s = torch.zeros(rows, h.shape[1], dtype=torch.float64).index_add_(0, e[m, 1], h[e[m, 0]])
+        c = torch.zeros(rows, dtype=torch.float64).index_add_(0, e[m, 1], torch.ones(int(m.sum()), dtype=torch.float64))
+        out = (s / c.clamp(min=1).unsqueeze(1)) @ wn + h[:rows] @ ws + b
+        h = torch.relu(out) if k < L else out
+    from oracle import sage
+    y = torch.tensor(sage.labels(nodes[: len(h)], label_seed, h.shape[1]))
+    return float(torch.nn.functional.cross_entropy(h, y)), h.numpy()
+
+
+@pytest.mark.parametrize("fan,dims", [([10, 10, 10], [16, 32, 32, 12]), ([5, 3], [8, 8, 4]), ([25], [12, 20])])
+def test_sage_oracle_matches_torch(port, fan, dims):
+    """oracle/sage.py (numpy fp64) against an independent torch fp64 formulation on blocks
+    sampled by the C restatement of sample_khop (parity for the train stage is pinned here:
+    the reference has no model)."""
+    from oracle import sage
+    n = 5000
+    indptr, indices = port.generate_topology(3, n, 6)
+    x = np.random.RandomState(1).standard_normal((n, dims[0])).astype(np.float32)
+    seeds = np.random.RandomState(2).randint(0, n, 300).astype(np.uint64)
+    b = port.sample_khop(indptr, indices, seeds, fan, 77)
+    w = [(np.random.RandomState(10 + i).standard_normal((a, c)) * 0.2, np.random.RandomState(20 + i).standard_normal((a, c)) * 0.2,
+          np.random.RandomState(30 + i).standard_normal(c) * 0.1) for i, (a, c) in enumerate(zip(dims[:-1], dims[1:]))]
+    xb = x[b["nodes"].astype(np.int64)]
+    l1, g1 = sage.sage_forward(xb, b["nodes"], b["edges"], b["layer_nodes"], w, 5)
+    l2, g2 = _torch_sage(xb, b["nodes"], b["edges"], b["layer_nodes"], w, 5)
+    assert abs(l1 - l2) <= 1e-12 * abs(l2)
+    np.testing.assert_allclose(g1, g2, rtol=1e-12, atol=1e-12)
+    assert g1.shape == (len(np.unique(seeds)), dims[-1])
