@@ -126,6 +126,13 @@ int fdg_ctx_generate_features(fdg_ctx* ctx, uint64_t seed, uint64_t num_nodes, u
 int fdg_ctx_set_feature_shards(fdg_ctx* ctx, const void* const* bases_dev, uint32_t n_shards,
                                uint64_t rows_per_shard, uint64_t num_nodes, uint32_t row_bytes, uint32_t dtype);
 int fdg_ctx_download_topology(const fdg_ctx* ctx, uint64_t* indptr, void* indices /* idx_bytes each */);
+/* Out-of-core tier (the paper's host-resident feature store): move the
+ * context's single-shard table to pinned host memory mapped into the device address space.
+ * fdg_gather and the buffer manager's misses then read rows over PCIe / C2C with the same
+ * kernels; put a buffer manager (fdg_bm_* / use_buffer_manager) in front of it so hits are
+ * served from HBM slots. fdg_ctx_features_on_host returns 1 when the table lives on the host. */
+int fdg_ctx_features_to_host(fdg_ctx* ctx);
+int fdg_ctx_features_on_host(const fdg_ctx* ctx);
 
 /* ---- multi-GPU: one process per GPU, row-sharded feature table read over NVLink ----
  * Rank r generates only its block of rows (owner = node / ceil(N / n_shards)) into a

@@ -84,6 +84,8 @@ SIGNATURES = {
     "fdg_ipc_open_handle": (ci, [vp, C.POINTER(vp)]),
     "fdg_ipc_close_handle": (ci, [vp]),
     "fdg_ctx_download_rows": (ci, [vp, u64, u64, vp]),
+    "fdg_ctx_features_to_host": (ci, [vp]),
+    "fdg_ctx_features_on_host": (ci, [vp]),
     "fdg_sampler_create": (ci, [vp, u32, vp, u32, C.POINTER(vp)]),
     "fdg_sampler_destroy": (ci, [vp]),
     "fdg_sampler_capacity": (ci, [vp, C.POINTER(u64), C.POINTER(u64)]),

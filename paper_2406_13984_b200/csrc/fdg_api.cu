@@ -151,6 +151,7 @@ int fdg_ctx_destroy(fdg_ctx* c) {
     if (c->indptr) cudaFree(c->indptr);
     if (c->indices) cudaFree(c->indices);
     for (void* p : c->owned_shards) cudaFree(p);
+    if (c->host_table) cudaFreeHost(c->host_table);
     if (c->shard_table) cudaFree((void*)c->shard_table);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -227,6 +228,8 @@ int fdg_ctx_generate_topology(fdg_ctx* c, uint64_t seed, uint64_t n, uint32_t av
 
 static int install_table(fdg_ctx* c, void* dev, uint64_t n, uint32_t row_bytes, uint32_t dtype) {
     for (void* p : c->owned_shards) cudaFree(p);
+    if (c->host_table) cudaFreeHost(c->host_table);
+    c->host_table = nullptr;
     c->owned_shards.assign(1, dev);
     c->shard_bases.assign(1, dev);
     c->row_bytes = row_bytes;
@@ -273,6 +276,36 @@ int fdg_ctx_load_features_file(fdg_ctx* c, const char* path) {
     FDG_TRY(read_file(path, data_offset, n * row_bytes, buf.data()));
     return fdg_ctx_load_features(c, buf.data(), n, row_bytes, 0);
 }
+
+// Out-of-core tier: move the (single-shard) table to pinned host memory mapped into the
+// device address space. The gather and the buffer manager's miss path then read rows
+// over PCIe / C2C with the same kernels -- the paper's host-resident feature store
+// with the GPU feature buffer in front of it (PAPER.md:1033-1047 future work).
+int fdg_ctx_features_to_host(fdg_ctx* c) {
+    if (c->row_bytes == 0 || c->shard_bases.empty()) return fail(FDG_NOT_LOADED, "features_to_host: no feature table");
+    if (c->n_shards != 1 || c->owned_shards.size() != 1)
+        return fail(FDG_INVALID_ARG, "features_to_host: only an owned single-shard table can move to the host tier");
+    if (c->host_table) return FDG_OK;
+    cudaSetDevice(c->device);
+    const uint64_t bytes = c->feat_nodes * c->row_bytes;
+    void* h = nullptr;
+    FDG_CUDA(cudaHostAlloc(&h, std::max<uint64_t>(bytes, 1), cudaHostAllocMapped | cudaHostAllocPortable));
+    cudaError_t e = cudaMemcpy(h, c->owned_shards[0], bytes, cudaMemcpyDeviceToHost);
+    void* dptr = nullptr;
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(&dptr, h, 0);
+    if (e != cudaSuccess) {
+        cudaFreeHost(h);
+        return cuda_fail(e, "fdg_ctx_features_to_host", __FILE__, __LINE__);
+    }
+    cudaFree(c->owned_shards[0]);
+    c->owned_shards.clear();
+    c->host_table = h;
+    c->shard_bases.assign(1, dptr);
+    FDG_CUDA(cudaMemcpy((void*)c->shard_table, &dptr, sizeof(void*), cudaMemcpyHostToDevice));
+    return FDG_OK;
+}
+
+int fdg_ctx_features_on_host(const fdg_ctx* c) { return c->host_table != nullptr; }
 
 int fdg_ctx_generate_features(fdg_ctx* c, uint64_t seed, uint64_t n, uint32_t dim, uint32_t dtype, uint32_t n_shards) {
     cudaSetDevice(c->device);

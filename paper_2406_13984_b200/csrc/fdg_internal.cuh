@@ -76,6 +76,7 @@ struct Ctx {
     uint64_t feat_nodes = 0;
     std::vector<void*> shard_bases;   // device pointers (may be peers)
     std::vector<void*> owned_shards;  // allocations owned by this ctx
+    void* host_table = nullptr;       // out-of-core tier: pinned, mapped host copy (owned)
     const void** shard_table = nullptr;  // device copy of shard_bases
     cudaStream_t stream = nullptr;    // setup stream
     int sm_count = 148;

@@ -255,6 +255,16 @@ class Topology:
         check(lib().fdg_ctx_download_topology(self.ctx, _p(indptr), _p(indices)))
         return indptr, indices
 
+    def features_to_host(self) -> "Topology":
+        """Out-of-core tier: keep the feature table in pinned host memory (mapped); the
+        gather and buffer-manager misses read it over PCIe / C2C."""
+        check(lib().fdg_ctx_features_to_host(self.ctx))
+        return self
+
+    @property
+    def features_on_host(self) -> bool:
+        return bool(lib().fdg_ctx_features_on_host(self.ctx))
+
     def download_rows(self, first: int, count: int) -> np.ndarray:
         rb = self.row_bytes
         out = np.empty((count, rb), np.uint8)

@@ -403,3 +403,53 @@ def test_checksum_kernels_agree(fd, port, hk, dim, rows):
     finally:
         fd.set_option("hash_kernel", old)
         fd.set_option("checksum_impl", old_cs)
+
+
+# ------------------------------------------------------------ out-of-core tier --
+def test_host_tier_gather_and_buffer_manager(fd, port):
+    """Table in pinned host memory (mapped): gather rows/checksums and buffer-manager
+    alias lists / stats / rows are identical to the HBM-resident table."""
+    n = 120_000
+    dev = fd.Topology.generate(n, 32, 10, 21)
+    host = fd.Topology.generate(n, 32, 10, 21).features_to_host()
+    assert host.features_on_host and not dev.features_on_host
+    table = dev.download_rows(0, n)
+    np.testing.assert_array_equal(host.download_rows(0, n), table)
+    nodes = np.random.RandomState(5).randint(0, n, 30_001).astype(np.uint64)
+    x, cs = fd.gather(host, nodes, checksum=True)
+    np.testing.assert_array_equal(x, table[nodes.astype(np.int64)])
+    assert cs == port.checksum_rows(x)
+    a, b = fd.BufferManager(dev, 20_000), fd.BufferManager(host, 20_000)
+    rs = np.random.RandomState(8)
+    prev = None
+    for _ in range(6):
+        batch = np.unique(rs.randint(0, 40_000, 9_000)).astype(np.uint64)
+        rs.shuffle(batch)
+        ra = a.extract(batch, want_rows=True, checksum=True)
+        rb = b.extract(batch, want_rows=True, checksum=True)
+        for u, v in zip(ra, rb):
+            np.testing.assert_array_equal(np.asarray(u), np.asarray(v))
+        if prev is not None:
+            a.release_batch(prev)
+            b.release_batch(prev)
+        prev = batch
+        assert a.stats() == b.stats()
+
+
+def test_host_tier_pipeline(fd):
+    """The runner with the buffer manager in front of a host-resident table reproduces the
+    HBM-tier per-batch records."""
+    n, B, fan = 200_000, 256, [10, 5, 5]
+    order = np.concatenate(fd.partition_epoch(np.arange(10 * B, dtype=np.uint64), B, 9))
+    rng = np.array([fd.batch_seed(0, 0, b) for b in range(10)], np.uint64)
+    recs = []
+    for to_host in (False, True):
+        t = fd.Topology.generate(n, 32, 12, 3)
+        if to_host:
+            t.features_to_host()
+        pipe = fd.Pipeline(t, fan, B, buffer_slots=150_000, checksum=True, samplers=2)
+        recs.append(pipe.run_batches(order, rng))
+        pipe.close()
+    assert np.all(recs[1]["status"] == 0)
+    np.testing.assert_array_equal(recs[0]["checksum"], recs[1]["checksum"])
+    np.testing.assert_array_equal(recs[0]["n_nodes"], recs[1]["n_nodes"])
