@@ -53,8 +53,8 @@ __device__ __forceinline__ const char* row_ptr(const TableRef& t, uint64_t node)
     }
 }
 
-// Gather traffic is marked L2 evict-first so the ~1 GB/batch stream does not
-// flush the samplers' hash tables and CSR lines out of the 126 MB L2.
+// Optional L2 evict-first marking of the gather stream (option "gather_evict_first",
+// off by default: the samplers' hash tables carry evict-last hints instead).
 __device__ __forceinline__ uint64_t gather_policy(bool evict_first) {
     uint64_t pol;
     if (evict_first)
@@ -798,7 +798,11 @@ TableRef table_ref(const Ctx& c) {
 // LDG/STG is the default: measured 177 us vs 203 us (TMA bulk) per Papers batch in
 // isolation and never slower inside the pipeline (profiles/README.md).
 int g_gather_impl = FDG_GATHER_LDG;
-int g_gather_evict_first = 1;
+// L2 evict-first on the gather stream: helped the gather in isolation in an earlier version
+// (177 vs 186 us), but with the current samplers (evict-last hash tables) the pipeline is
+// faster without it: Papers 199 vs 206 us per batch, Friendster 330 vs 338, extraction
+// alone 154 vs 159 (scripts/sweep_overlap.sh). Off by default.
+int g_gather_evict_first = 0;
 int g_gather_ctas_per_sm = 1;
 int64_t g_gather_dynamic = 1;
 // Fused gather + trainer checksum: 1 striped k_gather_hash16, 2 warp-specialised

@@ -21,7 +21,7 @@ K = int(os.environ.get("K", "300"))
 rng = np.array([L.fdg_batch_seed(0, 0, int(g)) for g in range(K)], np.uint64)
 seeds = DeviceBuffer.from_array(np.ascontiguousarray(order[:K * B]))
 f = np.ascontiguousarray(fan, np.uint32)
-defaults = {"gather_impl": 1, "gather_evict_first": 1, "l2_persist_mb": 0, "hash_load_pct": 50,
+defaults = {"gather_impl": 1, "gather_evict_first": 0, "l2_persist_mb": 0, "hash_load_pct": 50,
             "hash_clear": 1, "sampler_ctas_per_sm": 16, "gather_ctas_per_sm": 1,
             "extract_streams": 2, "hash_keep": 1, "gather_dynamic": 1, "hash_kernel": 4,
             "ws_hashers": 8, "ws_stg": 1, "checksum_impl": 1, "hash_chunk": 0}
