@@ -422,7 +422,9 @@ def _train_stage(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, a
     model.close()
     K = len(ids)
     return {"value": dist.reduce(K, "sum") / (ms / 1e3), "unit": "batches/s", "ms_per_step": ms / K,
-            "model": "GraphSAGE mean-aggregator " + "-".join(map(str, dims)) + ", fp32 CUDA-core GEMMs",
+            "model": "GraphSAGE mean-aggregator " + "-".join(map(str, dims)) + (
+                ", layer GEMMs on tcgen05 (kind::tf32, 3xTF32 fp32-accurate)" if fd.featdrive.get_option("sage_gemm")
+                else ", fp32 CUDA-core GEMMs"),
             "mean_loss": float(np.mean(losses)), "finite": bool(np.all(np.isfinite(losses))),
             "includes": "sample + extract + per-layer scatter-mean + GEMM + bias/ReLU + softmax cross-entropy"}
 

@@ -27,6 +27,7 @@
 //   k_loss_rows/_mean     warp per seed row: log-softmax CE; one CTA: fixed-order mean
 // Row counts live on the device (the batch record), so a forward is enqueued
 // without a host round trip; grids are sized from the fanout bounds.
+#include <cuda.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -36,6 +37,16 @@
 #include "fdg_internal.cuh"
 
 namespace fdg {
+// tensor-core GEMM (fdg_sage_tc.cu)
+int tc_make_map(CUtensorMap* map, const float* base, uint64_t rows, uint32_t K);
+void tc_split_weights(const float* Wcat, uint32_t K, uint32_t dout, uint32_t npad, std::vector<float>& hi,
+                      std::vector<float>& lo);
+int tc_gemm(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tBhi, const CUtensorMap& tBlo,
+            const float* bias, float* C, const fdg_batch_counts* cnt, int j, uint64_t rows_bound, int N, int npad,
+            int K, bool relu);
+// 1: layer GEMMs on the tensor cores (tcgen05 kind::tf32, 3xTF32 fp32-accurate); 0: CUDA-core fp32
+int64_t g_sage_gemm = 1;
+
 namespace {
 
 constexpr int kBM = 128, kBN = 128, kBK = 8;
@@ -297,6 +308,10 @@ struct Sage {
     uint64_t partial_floats = 0;
     float* row_loss = nullptr;
     std::vector<uint8_t> set;
+    // tensor-core path: transposed K-major W_hi / W_lo and TMA maps per layer
+    std::vector<float*> Whi, Wlo;
+    std::vector<CUtensorMap> mapA, mapBhi, mapBlo;
+    std::vector<uint8_t> tc_ok;     // layer K is a multiple of 32 and the maps were built
 };
 
 }  // namespace fdg
@@ -363,6 +378,24 @@ int fdg_sage_create(fdg_ctx* ctx, const uint32_t* dims, uint32_t n_layers, const
         m->b.push_back(bb);
     }
     m->set.assign(n_layers, 0);
+    m->Whi.assign(n_layers, nullptr);
+    m->Wlo.assign(n_layers, nullptr);
+    m->mapA.resize(n_layers);
+    m->mapBhi.resize(n_layers);
+    m->mapBlo.resize(n_layers);
+    m->tc_ok.assign(n_layers, 0);
+    for (uint32_t l = 0; l < n_layers && e == cudaSuccess; ++l) {
+        const uint32_t K = 2 * dims[l];
+        if (K % 32) continue;
+        e = al((void**)&m->Whi[l], uint64_t(m->npad[l]) * K * 4);
+        if (e == cudaSuccess) e = al((void**)&m->Wlo[l], uint64_t(m->npad[l]) * K * 4);
+        if (e != cudaSuccess) break;
+        const uint64_t rows_l = m->bound[n_layers - 1 - l];  // layer l+1 writes D_{L-1-l}
+        if (tc_make_map(&m->mapA[l], m->A, rows_l, K) == FDG_OK &&
+            tc_make_map(&m->mapBhi[l], m->Whi[l], m->npad[l], K) == FDG_OK &&
+            tc_make_map(&m->mapBlo[l], m->Wlo[l], m->npad[l], K) == FDG_OK)
+            m->tc_ok[l] = 1;
+    }
     if (e != cudaSuccess) {
         fdg_sage_destroy(m);
         return cuda_fail(e, "fdg_sage_create", __FILE__, __LINE__);
@@ -383,6 +416,8 @@ int fdg_sage_destroy(fdg_sage* m) {
     cudaFree(m->row_loss);
     for (auto p : m->W) cudaFree(p);
     for (auto p : m->b) cudaFree(p);
+    for (auto p : m->Whi) cudaFree(p);
+    for (auto p : m->Wlo) cudaFree(p);
     delete m;
     return FDG_OK;
 }
@@ -399,6 +434,17 @@ int fdg_sage_set_layer(fdg_sage* m, uint32_t layer, const float* w_neigh, const 
         }
     for (uint32_t c = 0; c < dout; ++c) bb[c] = bias ? bias[c] : 0.f;
     FDG_CUDA(cudaMemcpy(m->W[layer], w.data(), w.size() * 4, cudaMemcpyHostToDevice));
+    if (m->Whi[layer]) {
+        std::vector<float> cat(uint64_t(2) * din * dout), hi, lo;
+        for (uint32_t k = 0; k < din; ++k)
+            for (uint32_t c = 0; c < dout; ++c) {
+                cat[uint64_t(k) * dout + c] = w_neigh[uint64_t(k) * dout + c];
+                cat[uint64_t(din + k) * dout + c] = w_self[uint64_t(k) * dout + c];
+            }
+        tc_split_weights(cat.data(), 2 * din, dout, np, hi, lo);
+        FDG_CUDA(cudaMemcpy(m->Whi[layer], hi.data(), hi.size() * 4, cudaMemcpyHostToDevice));
+        FDG_CUDA(cudaMemcpy(m->Wlo[layer], lo.data(), lo.size() * 4, cudaMemcpyHostToDevice));
+    }
     FDG_CUDA(cudaMemcpy(m->b[layer], bb.data(), bb.size() * 4, cudaMemcpyHostToDevice));
     m->set[layer] = 1;
     return FDG_OK;
@@ -433,6 +479,12 @@ int fdg_sage_forward(fdg_sage* m, void* stv, const void* x_dev, const uint64_t* 
             k_aggregate<float><<<agg_blocks, 256, 0, st>>>(k == 1 ? static_cast<const float*>(x_dev) : hin, din,
                                                            m->seg, edges, counts_dev, j, m->A);
         float* hout = k == L ? m->logits : m->H[k & 1];
+        if (g_sage_gemm == 1 && m->tc_ok[k - 1]) {
+            FDG_TRY(tc_gemm(st, m->mapA[k - 1], m->mapBhi[k - 1], m->mapBlo[k - 1], m->b[k - 1], hout, counts_dev,
+                            j, rows, int(dout), int(m->npad[k - 1]), int(2 * din), k != L));
+            hin = hout;
+            continue;
+        }
         const int z = splitk_for(rows, 2 * din, m->npad[k - 1] / kBN, c.sm_count);
         dim3 grid(m->npad[k - 1] / kBN, uint32_t((rows + kBM - 1) / kBM), uint32_t(z));
         float* gout = z > 1 ? m->partial : hout;

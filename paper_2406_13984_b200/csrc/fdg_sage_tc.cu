@@ -1,0 +1,303 @@
+// fdg_sage_tc.cu -- the train stage's GEMM on the 5th-generation tensor cores.
+//
+// C[M x N] = act(A[M x K] . W + b) for the GraphSAGE layers (fdg_sage.cu), fp32
+// accurate via 3xTF32: every fp32 operand x splits into hi = x with the low 13
+// mantissa bits cleared (exact in TF32) and lo = x - hi (exact in fp32), and
+//   A . W ~= A_hi . W_hi + A_hi . W_lo + A_lo . W_hi
+// accumulates in fp32 in TMEM (the dropped A_lo . W_lo term and lo's own TF32
+// rounding are ~2^-20 relative), so the loss stays within 1e-5 of the fp64 oracle.
+//
+// One 128 x 128 output tile per CTA, K in 32-element (128-byte) blocks:
+//   warp 0 lane 0 : TMA producer -- A block (128 rows x 32) and W_hi / W_lo blocks
+//                   (W stored transposed, K-major) into a 3-stage ring, 128-byte
+//                   swizzled (the canonical K-major SW128 UMMA layout)
+//   warps 4-7     : split the A block in place into A_hi and a separate A_lo tile
+//                   (elementwise, so the swizzle is preserved), fence to the async
+//                   proxy, arrive; after the K loop they are the epilogue:
+//                   tcgen05.ld 32 columns at a time, + bias, ReLU, store
+//   warp 1 lane 0 : MMA issuer -- per K block 4 x 3 tcgen05.mma.kind::tf32
+//                   (M=128, N=128, K=8) into one TMEM accumulator; tcgen05.commit
+//                   frees the stage, the last commit signals the epilogue
+//   warp 2        : TMEM allocation (128 columns) and release
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "fdg_internal.cuh"
+
+namespace fdg {
+namespace {
+
+constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32, kTcStages = 3;
+constexpr int kTcTile = kTcBM * kTcBK * 4;  // 16 KB (A and B tiles alike: 128 rows x 128 bytes)
+constexpr int kTcStageBytes = 4 * kTcTile;  // A_hi (TMA lands here), A_lo, W_hi, W_lo
+constexpr int kTcThreads = 256;
+constexpr int kTcSmem = kTcStages * kTcStageBytes + 1024 /* alignment */ + 256 /* barriers */;
+
+__device__ __forceinline__ uint32_t d_rows_tc(const fdg_batch_counts* c, int j) {
+    uint32_t d = 0;
+    for (int i = 0; i <= j + 1 && i < FDG_MAX_LAYERS + 2; ++i) d = max(d, c->layer_nodes[i]);
+    return min(d, c->n_nodes);
+}
+
+__device__ __forceinline__ uint32_t sa(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(sa(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            sa(dst)),
+        "l"(map), "r"(sa(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+// K-major, 128-byte swizzle UMMA shared-memory descriptor: start >> 4, LBO unused (SW128
+// K-major), SBO = 1024 B between 8-row groups, version 1 (sm_100), layout SWIZZLE_128B.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+    return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ void umma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(bar))
+                 : "memory");
+}
+
+template <bool RELU>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_sgemm_tc(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tBhi,
+               const __grid_constant__ CUtensorMap tBlo, const float* __restrict__ bias, float* __restrict__ C,
+               const fdg_batch_counts* cnt, int j, int N, int K) {
+    extern __shared__ uint8_t tc_raw[];
+    const int M = int(d_rows_tc(cnt, j));
+    const int m0 = blockIdx.y * kTcBM, n0 = blockIdx.x * kTcBN;
+    if (m0 >= M) return;  // uniform, before any barrier or TMEM allocation
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + kTcStages * kTcStageBytes);
+    uint64_t* conv = full + kTcStages;
+    uint64_t* empty = conv + kTcStages;
+    uint64_t* tmem_full = empty + kTcStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto a_hi = [&](int s) { return sm + s * kTcStageBytes; };
+    auto a_lo = [&](int s) { return sm + s * kTcStageBytes + kTcTile; };
+    auto b_hi = [&](int s) { return sm + s * kTcStageBytes + 2 * kTcTile; };
+    auto b_lo = [&](int s) { return sm + s * kTcStageBytes + 3 * kTcTile; };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(conv + s, 128);
+            mbar_init(empty + s, 1);
+        }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tmem_slot)), "n"(128)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const int nk = K / kTcBK;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % kTcStages;
+                if (kb >= kTcStages) mbar_wait(empty + s, uint32_t((kb / kTcStages - 1) & 1));
+                mbar_expect_tx(full + s, 3 * kTcTile);
+                tma_load_2d(a_hi(s), &tA, full + s, kb * kTcBK, m0);
+                tma_load_2d(b_hi(s), &tBhi, full + s, kb * kTcBK, n0);
+                tma_load_2d(b_lo(s), &tBlo, full + s, kb * kTcBK, n0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            // kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(kTcBN >> 3) << 17) |
+                                   (uint32_t(kTcBM >> 4) << 24);
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % kTcStages;
+                mbar_wait(conv + s, uint32_t((kb / kTcStages) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int k = 0; k < kTcBK / 8; ++k) {  // UMMA_K = 8 tf32 = 32 bytes along the swizzled row
+                    const uint64_t dah = umma_desc(sa(a_hi(s)) + k * 32), dal = umma_desc(sa(a_lo(s)) + k * 32);
+                    const uint64_t dbh = umma_desc(sa(b_hi(s)) + k * 32), dbl = umma_desc(sa(b_lo(s)) + k * 32);
+                    umma_tf32(tmem, dah, dbh, idesc, (kb | k) ? 1u : 0u);
+                    umma_tf32(tmem, dah, dbl, idesc, 1u);
+                    umma_tf32(tmem, dal, dbh, idesc, 1u);
+                }
+                umma_commit(empty + s);  // the stage is free once these MMAs have read it
+            }
+            umma_commit(tmem_full);
+        }
+    } else if (warp >= 4) {
+        const int t = threadIdx.x - 128;
+        // ---- split A blocks: hi in place, lo into its own tile (same swizzled offsets)
+        for (int kb = 0; kb < nk; ++kb) {
+            const int s = kb % kTcStages;
+            mbar_wait(full + s, uint32_t((kb / kTcStages) & 1));
+            float4* hi = reinterpret_cast<float4*>(a_hi(s));
+            float4* lo = reinterpret_cast<float4*>(a_lo(s));
+#pragma unroll
+            for (int i = t; i < kTcTile / 16; i += 128) {
+                const float4 v = hi[i];
+                float4 h;
+                h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                hi[i] = h;
+                lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+            mbar_arrive(conv + s);
+        }
+        // ---- epilogue: TMEM lane = tile row; warp w reads lanes 32 (w % 4) ..
+        mbar_wait(tmem_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int wq = warp & 3;
+        const int row = m0 + wq * 32 + lane;
+        for (int c0 = 0; c0 < kTcBN; c0 += 32) {
+            uint32_t r[32];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(tmem + (uint32_t(wq * 32) << 16) + uint32_t(c0)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (row < M) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int col = n0 + c0 + q * 4;
+                    if (col >= N) break;
+                    float4 v = make_float4(__uint_as_float(r[q * 4 + 0]) + bias[col + 0],
+                                           __uint_as_float(r[q * 4 + 1]) + bias[col + 1],
+                                           __uint_as_float(r[q * 4 + 2]) + bias[col + 2],
+                                           __uint_as_float(r[q * 4 + 3]) + bias[col + 3]);
+                    if (RELU) {
+                        v.x = fmaxf(v.x, 0.f);
+                        v.y = fmaxf(v.y, 0.f);
+                        v.z = fmaxf(v.z, 0.f);
+                        v.w = fmaxf(v.w, 0.f);
+                    }
+                    *reinterpret_cast<float4*>(C + size_t(row) * N + col) = v;
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 2) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(128) : "memory");
+    }
+}
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+    static EncodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiled>(p);
+    }
+    return fn;
+}
+
+}  // namespace
+
+// fp32 row-major [rows x K] (K contiguous) as a TMA map with 32 x 128 boxes, 128-byte swizzle.
+int tc_make_map(CUtensorMap* map, const float* base, uint64_t rows, uint32_t K) {
+    EncodeTiled enc = encode_fn();
+    if (!enc) return fail(FDG_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {K, std::max<uint64_t>(rows, 1)};
+    const cuuint64_t strides[1] = {uint64_t(K) * 4};
+    const cuuint32_t box[2] = {uint32_t(kTcBK), uint32_t(kTcBM)};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FDG_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return FDG_OK;
+}
+
+// Host split of W (input-major [K x dout]) into transposed K-major hi / lo [npad x K].
+void tc_split_weights(const float* Wcat, uint32_t K, uint32_t dout, uint32_t npad, std::vector<float>& hi,
+                      std::vector<float>& lo) {
+    hi.assign(uint64_t(npad) * K, 0.f);
+    lo.assign(uint64_t(npad) * K, 0.f);
+    for (uint32_t k = 0; k < K; ++k)
+        for (uint32_t n = 0; n < dout; ++n) {
+            const float v = Wcat[uint64_t(k) * dout + n];
+            uint32_t u;
+            std::memcpy(&u, &v, 4);
+            u &= 0xFFFFE000u;
+            float h;
+            std::memcpy(&h, &u, 4);
+            hi[uint64_t(n) * K + k] = h;
+            lo[uint64_t(n) * K + k] = v - h;
+        }
+}
+
+int tc_gemm(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tBhi, const CUtensorMap& tBlo,
+            const float* bias, float* C, const fdg_batch_counts* cnt, int j, uint64_t rows_bound, int N, int npad,
+            int K, bool relu) {
+    static bool attr = false;
+    if (!attr) {
+        FDG_CUDA(cudaFuncSetAttribute(k_sgemm_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+        FDG_CUDA(cudaFuncSetAttribute(k_sgemm_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+        attr = true;
+    }
+    if (K % kTcBK) return fail(FDG_INVALID_ARG, "tc_gemm: K must be a multiple of 32");
+    dim3 grid(uint32_t(npad / kTcBN), uint32_t((rows_bound + kTcBM - 1) / kTcBM));
+    if (relu)
+        k_sgemm_tc<true><<<grid, kTcThreads, kTcSmem, st>>>(tA, tBhi, tBlo, bias, C, cnt, j, N, K);
+    else
+        k_sgemm_tc<false><<<grid, kTcThreads, kTcSmem, st>>>(tA, tBhi, tBlo, bias, C, cnt, j, N, K);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
+}  // namespace fdg

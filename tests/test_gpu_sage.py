@@ -26,13 +26,23 @@ def _check(model, t, batch, dtype, label_seed):
     return loss
 
 
+@pytest.fixture(params=[1, 0], ids=["tcgen05", "cudacore"])
+def gemm(request, fd):
+    """Both GEMM engines: tcgen05 kind::tf32 with 3xTF32 splitting, and CUDA-core fp32."""
+    old = fd.featdrive.get_option("sage_gemm")
+    fd.set_option("sage_gemm", request.param)
+    yield request.param
+    fd.set_option("sage_gemm", old)
+
+
 @pytest.mark.parametrize("dim,dims,fan,seeds", [
     (32, [32, 64, 64, 12], [10, 10, 10], 300),
     (128, [128, 256, 256, 172], [10, 10, 10], 200),   # the paper's Papers100M model shape
     (64, [64, 132, 40], [15, 10], 257),               # ragged GEMM tiles (N = 132, 40)
     (16, [16, 8], [25], 1000),
+    (4, [4, 12, 8], [3, 3], 50),                      # K = 8 / 24: no tensor-core tiling -> CUDA cores
 ])
-def test_sage_forward_vs_oracle(fd, dim, dims, fan, seeds):
+def test_sage_forward_vs_oracle(fd, gemm, dim, dims, fan, seeds):
     t = fd.Topology.generate(60_000, dim, 12, 5)
     s = np.random.RandomState(dim).randint(0, 60_000, seeds).astype(np.uint64)
     batch = fd.sample_khop(t, s, fan, fd.batch_seed(0, 0, dim))
@@ -41,7 +51,7 @@ def test_sage_forward_vs_oracle(fd, dim, dims, fan, seeds):
     _check(model, t, batch, np.float32, 99)  # a second forward reuses the workspace
 
 
-def test_sage_forward_fp16_table(fd):
+def test_sage_forward_fp16_table(fd, gemm):
     """MAG240M-style f16 feature rows: aggregation upconverts to fp32."""
     t = fd.Topology.generate(40_000, 96, 8, 11, dtype="f16")
     s = np.arange(0, 40_000, 97, dtype=np.uint64)
@@ -50,7 +60,7 @@ def test_sage_forward_fp16_table(fd):
     _check(model, t, batch, np.float16, 7)
 
 
-def test_sage_zero_degree_and_early_stop(fd):
+def test_sage_zero_degree_and_early_stop(fd, gemm):
     """Seeds without in-edges (mean aggregates 0), duplicate seeds and a frontier that
     empties before the last hop (D_j of unreached hops = all nodes)."""
     n = 2000
