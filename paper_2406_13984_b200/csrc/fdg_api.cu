@@ -439,7 +439,11 @@ int fdg_set_gather_impl(int impl) {
 int fdg_set_option(const char* key, int64_t v) {
     std::string k(key);
     if (k == "gather_impl") return fdg_set_gather_impl(int(v));
-    if (k == "gather_evict_first") { g_gather_evict_first = v != 0; return FDG_OK; }
+    if (k == "gather_evict_first") {  // 0 off, 1 loads + stores, 2 table loads only, 3 X stores only
+        if (v < 0 || v > 3) return fail(FDG_INVALID_ARG, "gather_evict_first must be in [0, 3]");
+        g_gather_evict_first = int(v);
+        return FDG_OK;
+    }
     if (k == "l2_persist_mb") { g_l2_persist_mb = v < 0 ? 0 : v; return FDG_OK; }
     if (k == "sampler_ctas_per_sm") {
         if (v < 1 || v > 64) return fail(FDG_INVALID_ARG, "sampler_ctas_per_sm must be in [1, 64]");

@@ -63,6 +63,9 @@ __device__ __forceinline__ uint64_t gather_policy(bool evict_first) {
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+// "gather_evict_first": 0 off, 1 loads and stores, 2 table loads only, 3 X stores only.
+__device__ __forceinline__ uint64_t gather_policy_ld(uint32_t ef) { return gather_policy(ef == 1 || ef == 2); }
+__device__ __forceinline__ uint64_t gather_policy_st(uint32_t ef) { return gather_policy(ef == 1 || ef == 3); }
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p, uint64_t pol) {
     uint4 v;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
@@ -142,7 +145,7 @@ __global__ void __launch_bounds__(512) k_gather16_dyn(const uint64_t* __restrict
     const uint32_t total = uint32_t(n * cpr);
     constexpr uint32_t kStep = kUnroll * 512;
     constexpr uint32_t kUnit = kStep * kDynIters;
-    const uint64_t pol = gather_policy(t.evict_first);
+    const uint64_t pol = gather_policy_ld(t.evict_first), pol_st = gather_policy_st(t.evict_first);
     for (;;) {
         if (threadIdx.x == 0) s_unit = atomicAdd(ctr, 1u);
         __syncthreads();
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(512) k_gather16_dyn(const uint64_t* __restrict
                                       pol);
                 }
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) stg_stream(out + cc[u], v[u], pol);
+                for (int u = 0; u < kUnroll; ++u) stg_stream(out + cc[u], v[u], pol_st);
             } else {
                 for (uint32_t c = b + threadIdx.x; c < u1; c += 512) {
                     uint32_t row = cdiv.div(c);
@@ -172,7 +175,7 @@ __global__ void __launch_bounds__(512) k_gather16_dyn(const uint64_t* __restrict
                     stg_stream(out + c,
                                ldg_stream(reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, __ldg(nodes + row))) + col,
                                           pol),
-                               pol);
+                               pol_st);
                 }
             }
         }
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
     const uint64_t full = n / 32;
     const uint64_t gstride = uint64_t(gridDim.x) * kHpWarps;
     const uint64_t g0 = blockIdx.x * uint64_t(kHpWarps) + warp;
-    const uint64_t pol = gather_policy(t.evict_first);
+    const uint64_t pol = gather_policy_ld(t.evict_first), pol_st = gather_policy_st(t.evict_first);
     const uint32_t part = lane % S::LPR, rsub = lane / S::LPR;
     const uint64_t seed = 0x27d4eb2f165667c5ull ^ (uint64_t(RB) * 0x9e3779b97f4a7c15ull);
     uint64_t sum = 0;
@@ -436,7 +439,7 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
                 for (int k = 0; k < S::NI; ++k) {
                     if (EVEN || !lastc || int(part) < LASTP) {
                         if (!ALIAS && out)
-                            stg_stream(reinterpret_cast<uint4*>(dst + k * S::RPI * RB + c * CH), v[k], pol);
+                            stg_stream(reinterpret_cast<uint4*>(dst + k * S::RPI * RB + c * CH), v[k], pol_st);
                         *reinterpret_cast<uint4*>(wbuf + (k * S::RPI + rsub) * S::STRIDE + part * 16) = v[k];
                     }
                 }
@@ -481,7 +484,7 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
                     const char* src = ALIAS ? t.base + node * RB : row_ptr<SHARDED>(t, node);
                     const uint4 w = ldg_stream(reinterpret_cast<const uint4*>(src + c * CH) + part, pol);
                     if (!ALIAS && out)
-                        stg_stream(reinterpret_cast<uint4*>(out + (tail * 32 + r) * RB + c * CH) + part, w, pol);
+                        stg_stream(reinterpret_cast<uint4*>(out + (tail * 32 + r) * RB + c * CH) + part, w, pol_st);
                     *reinterpret_cast<uint4*>(wbuf + r * S::STRIDE + part * 16) = w;
                 }
             }

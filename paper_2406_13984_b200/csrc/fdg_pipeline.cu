@@ -67,6 +67,7 @@ struct fdg_pipeline {
     std::vector<cudaEvent_t> sev;        // per-group sampling timing events (2 per group)
     uint64_t timed_groups = 0;
     fdg_bm* bm = nullptr;
+    bool l2_persist = false;             // this pipeline set aside persisting L2 (undone on destroy)
     fdg_sage* model = nullptr;           // optional train stage after each extraction
     uint64_t label_seed = 0;
     float* losses = nullptr;             // device, one per batch of the current run
@@ -83,6 +84,11 @@ namespace {
 void destroy(fdg_pipeline* p) {
     if (!p) return;
     cudaDeviceSynchronize();
+    if (p->l2_persist) {  // the set-aside is device-wide: give it back
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+        cudaGetLastError();
+    }
     for (auto s : p->samplers) sampler_destroy(s);
     for (auto s : p->sstream) cudaStreamDestroy(s);
     if (p->xstream) cudaStreamDestroy(p->xstream);
@@ -158,6 +164,7 @@ int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers
             const uint64_t persist =
                 std::min<uint64_t>(std::min<uint64_t>(want, uint64_t(max_persist)), uint64_t(g_l2_persist_mb) << 20);
             cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist);
+            p->l2_persist = true;
             for (uint32_t i = 0; i < S; ++i) {
                 void* b;
                 uint64_t n;
