@@ -16,9 +16,10 @@ rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 dist.init_process_group("gloo", rank=rank, world_size=world)
 dev = fdist.local_device(int(os.environ.get("LOCAL_RANK", "0")))
 n, dim = 50_003, 64
+dtype = os.environ.get("MP_SHARD_DTYPE", "f32")  # f16: the MAG240M-style table
 topo = fd.Topology.generate(n, dim, 8, 7, device=dev, features=False)
-sh = fdist.ShardedFeatures(topo, rank, world, 7, n, dim)
-ref = fd.Topology.generate(n, dim, 8, 7, device=dev)  # the full table, single process
+sh = fdist.ShardedFeatures(topo, rank, world, 7, n, dim, dtype=dtype)
+ref = fd.Topology.generate(n, dim, 8, 7, dtype=dtype, device=dev)  # the full table, single process
 nodes = np.random.RandomState(rank).randint(0, n, size=20_000).astype(np.uint64)
 x, cs = fd.gather(topo, nodes, checksum=True)
 want, want_cs = fd.gather(ref, nodes, checksum=True)

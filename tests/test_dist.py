@@ -78,7 +78,8 @@ def test_shard_geometry_and_segments():
 
 
 @pytest.mark.gpu
-def test_two_process_ipc_sharded_gather():
+@pytest.mark.parametrize("dtype", ["f32", "f16"])
+def test_two_process_ipc_sharded_gather(dtype):
     """Two ranks (torchrun, one GPU): each generates its half of the table, the halves
     are exchanged over CUDA IPC, and every rank's sharded gather equals the rows of
     the full single-process table."""
@@ -86,6 +87,7 @@ def test_two_process_ipc_sharded_gather():
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                           "--master-addr", "127.0.0.1", "--master-port", str(port),
                           os.path.join(ROOT, "tests", "mp_shard_check.py")],
-                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+                         capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env=dict(os.environ, MP_SHARD_DTYPE=dtype))
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert out.stdout.count("shard-ok") == 2
