@@ -391,6 +391,7 @@ def run_ours(args):
                              "run; consecutive gathers alternate between two streams and can overlap, so the "
                              "average launch duration is the union of the launch intervals / launches; "
                              "pipeline_gbs = all gather bytes / whole timed region"},
+        "step_roofline": _step_roofline(cfg, max_ms / K, hbm),
         "gpu_launches": _launch_count(K, len(fan), frac is not None, args.samplers),
         "e2e": {"value": e2e_value, "unit": "batches/s", "h2d_bytes_per_step": B * 8, "d2h_bytes_per_step": csz,
                 "includes": "seed H2D, sample, extract, fused trainer checksum, batch-record D2H"},
@@ -463,6 +464,17 @@ def _launch_count(K, layers, bm, samplers, prefetch=16):
     per_batch = 2 + (layers + 1) + layers + (1 if not bm else 10)
     per_sampler = -(-K // samplers)
     return K * per_batch + samplers * (-(-per_sampler // prefetch))
+
+
+def _step_roofline(cfg, ms_per_step, peak_gbs):
+    """Whole pipelined step against the DRAM roofline: profiled DRAM bytes per batch
+    (ncu range replay, profiles/ncu_traffic.json '<cfg>_step') / peak vs the live step time."""
+    t = _traffic(cfg + "_step")
+    if not t:
+        return None
+    floor_ms = t["bytes"] / (peak_gbs * 1e9) * 1e3
+    return {"bytes_per_step": t["bytes"], "floor_ms": floor_ms, "ms_per_step": ms_per_step,
+            "frac": floor_ms / ms_per_step, "source": t["source"]}
 
 
 def _traffic(cfg):
