@@ -7,18 +7,19 @@
 // accumulates in fp32 in TMEM (the dropped A_lo . W_lo term and lo's own TF32
 // rounding are ~2^-20 relative), so the loss stays within 1e-5 of the fp64 oracle.
 //
-// One 128 x 128 output tile per CTA, K in 32-element (128-byte) blocks:
+// Persistent CTAs (one per SM) walk the 128 x 128 output tiles, K in 32-element (128-byte) blocks:
 //   warp 0 lane 0 : TMA producer -- A block (128 rows x 32) and W_hi / W_lo blocks
 //                   (W stored transposed, K-major) into a 3-stage ring, 128-byte
 //                   swizzled (the canonical K-major SW128 UMMA layout)
 //   warps 4-7     : split the A block in place into A_hi and a separate A_lo tile
 //                   (elementwise, so the swizzle is preserved), fence to the async
-//                   proxy, arrive; after the K loop they are the epilogue:
-//                   tcgen05.ld 32 columns at a time, + bias, ReLU, store
+//                   proxy, arrive
+//   warps 8-11    : epilogue: tcgen05.ld 32 columns at a time, + bias, ReLU, store;
+//                   two TMEM accumulators let tile i's epilogue overlap tile i+1's MMAs
 //   warp 1 lane 0 : MMA issuer -- per K block 4 x 3 tcgen05.mma.kind::tf32
 //                   (M=128, N=128, K=8) into one TMEM accumulator; tcgen05.commit
 //                   frees the stage, the last commit signals the epilogue
-//   warp 2        : TMEM allocation (128 columns) and release
+//   warp 2        : TMEM allocation (2 x 128 columns) and release
 #include <cuda.h>
 
 #include <algorithm>
@@ -33,7 +34,7 @@ namespace {
 constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32, kTcStages = 3;
 constexpr int kTcTile = kTcBM * kTcBK * 4;  // 16 KB (A and B tiles alike: 128 rows x 128 bytes)
 constexpr int kTcStageBytes = 4 * kTcTile;  // A_hi (TMA lands here), A_lo, W_hi, W_lo
-constexpr int kTcThreads = 256;
+constexpr int kTcThreads = 384;  // warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4-7 split, 8-11 epilogue
 constexpr int kTcSmem = kTcStages * kTcStageBytes + 1024 /* alignment */ + 256 /* barriers */;
 
 __device__ __forceinline__ uint32_t d_rows_tc(const fdg_batch_counts* c, int j) {
@@ -91,21 +92,25 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+// Persistent: CTA c takes tiles c, c + grid, ... (row-tile major: the column tiles of a row
+// tile go to neighbouring CTAs at the same time, so the A block is reused from L2). Two TMEM accumulators (2 x 128
+// columns): the epilogue of tile i overlaps the MMAs of tile i + 1.
 template <bool RELU>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_sgemm_tc(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tBhi,
                const __grid_constant__ CUtensorMap tBlo, const float* __restrict__ bias, float* __restrict__ C,
-               const fdg_batch_counts* cnt, int j, int N, int K) {
+               const fdg_batch_counts* cnt, int j, int N, int K, int n_tiles) {
     extern __shared__ uint8_t tc_raw[];
     const int M = int(d_rows_tc(cnt, j));
-    const int m0 = blockIdx.y * kTcBM, n0 = blockIdx.x * kTcBN;
-    if (m0 >= M) return;  // uniform, before any barrier or TMEM allocation
+    const int tiles = (M + kTcBM - 1) / kTcBM * n_tiles;
+    if (int(blockIdx.x) >= tiles) return;  // uniform, before any barrier or TMEM allocation
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + kTcStages * kTcStageBytes);
     uint64_t* conv = full + kTcStages;
     uint64_t* empty = conv + kTcStages;
-    uint64_t* tmem_full = empty + kTcStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* tmem_full = empty + kTcStages;  // [2]
+    uint64_t* tmem_empty = tmem_full + 2;     // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto a_hi = [&](int s) { return sm + s * kTcStageBytes; };
     auto a_lo = [&](int s) { return sm + s * kTcStageBytes + kTcTile; };
@@ -117,11 +122,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_init(conv + s, 128);
             mbar_init(empty + s, 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tmem_full + a, 1);
+            mbar_init(tmem_empty + a, 128);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tmem_slot)), "n"(128)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tmem_slot)), "n"(256)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -133,13 +141,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % kTcStages;
-                if (kb >= kTcStages) mbar_wait(empty + s, uint32_t((kb / kTcStages - 1) & 1));
-                mbar_expect_tx(full + s, 3 * kTcTile);
-                tma_load_2d(a_hi(s), &tA, full + s, kb * kTcBK, m0);
-                tma_load_2d(b_hi(s), &tBhi, full + s, kb * kTcBK, n0);
-                tma_load_2d(b_lo(s), &tBlo, full + s, kb * kTcBK, n0);
+            int it = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int m0 = (t / n_tiles) * kTcBM, n0 = (t % n_tiles) * kTcBN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % kTcStages;
+                    if (it >= kTcStages) mbar_wait(empty + s, uint32_t((it / kTcStages - 1) & 1));
+                    mbar_expect_tx(full + s, 3 * kTcTile);
+                    tma_load_2d(a_hi(s), &tA, full + s, kb * kTcBK, m0);
+                    tma_load_2d(b_hi(s), &tBhi, full + s, kb * kTcBK, n0);
+                    tma_load_2d(b_lo(s), &tBlo, full + s, kb * kTcBK, n0);
+                }
             }
         }
     } else if (warp == 1) {
@@ -147,77 +159,97 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             // kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
             const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(kTcBN >> 3) << 17) |
                                    (uint32_t(kTcBM >> 4) << 24);
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % kTcStages;
-                mbar_wait(conv + s, uint32_t((kb / kTcStages) & 1));
+            int it = 0, ti = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ti) {
+                const int acc = ti & 1;
+                if (ti >= 2) mbar_wait(tmem_empty + acc, uint32_t((ti / 2 - 1) & 1));  // epilogue drained it
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t d = tmem + uint32_t(acc * kTcBN);
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % kTcStages;
+                    mbar_wait(conv + s, uint32_t((it / kTcStages) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-                for (int k = 0; k < kTcBK / 8; ++k) {  // UMMA_K = 8 tf32 = 32 bytes along the swizzled row
-                    const uint64_t dah = umma_desc(sa(a_hi(s)) + k * 32), dal = umma_desc(sa(a_lo(s)) + k * 32);
-                    const uint64_t dbh = umma_desc(sa(b_hi(s)) + k * 32), dbl = umma_desc(sa(b_lo(s)) + k * 32);
-                    umma_tf32(tmem, dah, dbh, idesc, (kb | k) ? 1u : 0u);
-                    umma_tf32(tmem, dah, dbl, idesc, 1u);
-                    umma_tf32(tmem, dal, dbh, idesc, 1u);
-                }
-                umma_commit(empty + s);  // the stage is free once these MMAs have read it
-            }
-            umma_commit(tmem_full);
-        }
-    } else if (warp >= 4) {
-        const int t = threadIdx.x - 128;
-        // ---- split A blocks: hi in place, lo into its own tile (same swizzled offsets)
-        for (int kb = 0; kb < nk; ++kb) {
-            const int s = kb % kTcStages;
-            mbar_wait(full + s, uint32_t((kb / kTcStages) & 1));
-            float4* hi = reinterpret_cast<float4*>(a_hi(s));
-            float4* lo = reinterpret_cast<float4*>(a_lo(s));
-#pragma unroll
-            for (int i = t; i < kTcTile / 16; i += 128) {
-                const float4 v = hi[i];
-                float4 h;
-                h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                hi[i] = h;
-                lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
-            mbar_arrive(conv + s);
-        }
-        // ---- epilogue: TMEM lane = tile row; warp w reads lanes 32 (w % 4) ..
-        mbar_wait(tmem_full, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int wq = warp & 3;
-        const int row = m0 + wq * 32 + lane;
-        for (int c0 = 0; c0 < kTcBN; c0 += 32) {
-            uint32_t r[32];
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                : "r"(tmem + (uint32_t(wq * 32) << 16) + uint32_t(c0)));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (row < M) {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int col = n0 + c0 + q * 4;
-                    if (col >= N) break;
-                    float4 v = make_float4(__uint_as_float(r[q * 4 + 0]) + bias[col + 0],
-                                           __uint_as_float(r[q * 4 + 1]) + bias[col + 1],
-                                           __uint_as_float(r[q * 4 + 2]) + bias[col + 2],
-                                           __uint_as_float(r[q * 4 + 3]) + bias[col + 3]);
-                    if (RELU) {
-                        v.x = fmaxf(v.x, 0.f);
-                        v.y = fmaxf(v.y, 0.f);
-                        v.z = fmaxf(v.z, 0.f);
-                        v.w = fmaxf(v.w, 0.f);
+                    for (int k = 0; k < kTcBK / 8; ++k) {  // UMMA_K = 8 tf32 = 32 bytes along the swizzled row
+                        const uint64_t dah = umma_desc(sa(a_hi(s)) + k * 32), dal = umma_desc(sa(a_lo(s)) + k * 32);
+                        const uint64_t dbh = umma_desc(sa(b_hi(s)) + k * 32), dbl = umma_desc(sa(b_lo(s)) + k * 32);
+                        umma_tf32(d, dah, dbh, idesc, (kb | k) ? 1u : 0u);
+                        umma_tf32(d, dah, dbl, idesc, 1u);
+                        umma_tf32(d, dal, dbh, idesc, 1u);
                     }
-                    *reinterpret_cast<float4*>(C + size_t(row) * N + col) = v;
+                    umma_commit(empty + s);  // the stage is free once these MMAs have read it
+                }
+                umma_commit(tmem_full + acc);
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ---- split A blocks: hi in place, lo into its own tile (same swizzled offsets)
+        const int t4 = threadIdx.x - 128;
+        int it = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            for (int kb = 0; kb < nk; ++kb, ++it) {
+                const int s = it % kTcStages;
+                mbar_wait(full + s, uint32_t((it / kTcStages) & 1));
+                float4* hi = reinterpret_cast<float4*>(a_hi(s));
+                float4* lo = reinterpret_cast<float4*>(a_lo(s));
+#pragma unroll
+                for (int i = t4; i < kTcTile / 16; i += 128) {
+                    const float4 v = hi[i];
+                    float4 h;
+                    h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                    h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                    h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                    h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                    hi[i] = h;
+                    lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+                mbar_arrive(conv + s);
+            }
+        }
+    } else if (warp >= 8) {
+        // ---- epilogue: TMEM lane = tile row; warp w reads lanes 32 (w % 4) ..
+        const int wq = warp & 3;
+        int ti = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ti) {
+            const int acc = ti & 1;
+            const int m0 = (t / n_tiles) * kTcBM, n0 = (t % n_tiles) * kTcBN;
+            mbar_wait(tmem_full + acc, uint32_t((ti / 2) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int row = m0 + wq * 32 + lane;
+            for (int c0 = 0; c0 < kTcBN; c0 += 32) {
+                uint32_t r[32];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(tmem + (uint32_t(wq * 32) << 16) + uint32_t(acc * kTcBN + c0)));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c0 + 32 == kTcBN) {  // every column of this accumulator is in registers: hand it back
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    mbar_arrive(tmem_empty + acc);
+                }
+                if (row < M) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int col = n0 + c0 + q * 4;
+                        if (col >= N) break;
+                        float4 v = make_float4(__uint_as_float(r[q * 4 + 0]) + bias[col + 0],
+                                               __uint_as_float(r[q * 4 + 1]) + bias[col + 1],
+                                               __uint_as_float(r[q * 4 + 2]) + bias[col + 2],
+                                               __uint_as_float(r[q * 4 + 3]) + bias[col + 3]);
+                        if (RELU) {
+                            v.x = fmaxf(v.x, 0.f);
+                            v.y = fmaxf(v.y, 0.f);
+                            v.z = fmaxf(v.z, 0.f);
+                            v.w = fmaxf(v.w, 0.f);
+                        }
+                        *reinterpret_cast<float4*>(C + size_t(row) * N + col) = v;
+                    }
                 }
             }
         }
@@ -226,7 +258,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __syncthreads();
     if (warp == 2) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(128) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256) : "memory");
     }
 }
 
@@ -291,11 +323,19 @@ int tc_gemm(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tBhi, con
         attr = true;
     }
     if (K % kTcBK) return fail(FDG_INVALID_ARG, "tc_gemm: K must be a multiple of 32");
-    dim3 grid(uint32_t(npad / kTcBN), uint32_t((rows_bound + kTcBM - 1) / kTcBM));
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int n_tiles = npad / kTcBN;
+    const uint64_t tiles = (rows_bound + kTcBM - 1) / kTcBM * uint64_t(n_tiles);
+    const uint32_t grid = uint32_t(std::min<uint64_t>(tiles, uint64_t(sms)));  // persistent: one CTA per SM
     if (relu)
-        k_sgemm_tc<true><<<grid, kTcThreads, kTcSmem, st>>>(tA, tBhi, tBlo, bias, C, cnt, j, N, K);
+        k_sgemm_tc<true><<<grid, kTcThreads, kTcSmem, st>>>(tA, tBhi, tBlo, bias, C, cnt, j, N, K, n_tiles);
     else
-        k_sgemm_tc<false><<<grid, kTcThreads, kTcSmem, st>>>(tA, tBhi, tBlo, bias, C, cnt, j, N, K);
+        k_sgemm_tc<false><<<grid, kTcThreads, kTcSmem, st>>>(tA, tBhi, tBlo, bias, C, cnt, j, N, K, n_tiles);
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;
 }
