@@ -84,6 +84,12 @@ public:
     Topology(const Topology&) = delete;
     Topology& operator=(const Topology&) = delete;
 
+    /// Out-of-core tier: the feature table moves to pinned host memory mapped into the
+    /// device; gathers and buffer-manager misses read it over PCIe (put a BufferManager
+    /// in front of it).
+    void features_to_host() { check(fdg_ctx_features_to_host(ctx_)); }
+    bool features_on_host() const { return fdg_ctx_features_on_host(ctx_) != 0; }
+
     std::uint64_t num_nodes() const { return info().num_nodes; }
     std::uint64_t num_edges() const { return info().num_edges; }
     std::uint32_t row_bytes() const { return info().row_bytes; }
@@ -128,6 +134,9 @@ struct SampledBatch {  // sampling.hpp:48-54
     std::vector<NodeId> seeds;
     std::vector<NodeId> nodes;
     std::vector<LocalEdge> edges;
+    // extension (not in the reference): nodes before each hop's new nodes, [1] = unique
+    // seeds -- the block structure the train stage consumes
+    std::vector<std::uint64_t> layer_nodes;
 };
 
 /// graph::sample_khop (sampling.hpp:72-134), executed on the GPU, bit-exact.
@@ -147,8 +156,9 @@ inline SampledBatch sample_khop(const Topology& topo, std::span<const NodeId> se
     b.nodes.resize(cap);
     std::vector<std::uint32_t> e(2 * cap);
     std::uint64_t nn = 0, ne = 0;
+    b.layer_nodes.assign(fanouts.per_layer.size() + 2, 0);
     check(fdg_sample_khop_host(s, seeds.data(), std::uint32_t(seeds.size()), rng_seed, b.nodes.data(), e.data(), cap,
-                               &nn, &ne, nullptr, nullptr));
+                               &nn, &ne, b.layer_nodes.data(), nullptr));
     b.nodes.resize(nn);
     b.edges.resize(ne);
     for (std::uint64_t i = 0; i < ne; ++i) b.edges[i] = LocalEdge{e[2 * i], e[2 * i + 1]};
@@ -167,6 +177,74 @@ inline std::vector<std::vector<NodeId>> partition_epoch(std::vector<NodeId> trai
 }
 
 }  // namespace graph
+
+namespace train {
+
+/// The train stage (fdg_sage_*): GraphSAGE forward + softmax cross-entropy over a
+/// sampled batch's blocks. The reference's trainer is the checksum trainer_step
+/// (pipeline.hpp:103-124); the paper's model is a 3-layer GraphSAGE.
+class GraphSAGE {
+public:
+    /// dims: L + 1 widths (dims[0] = feature width), one layer per sampling hop.
+    GraphSAGE(const graph::Topology& topo, std::vector<std::uint32_t> dims, const graph::Fanouts& fanouts,
+              std::uint32_t max_seeds)
+        : topo_(topo), dims_(std::move(dims)) {
+        if (dims_.size() != fanouts.per_layer.size() + 1)
+            throw std::invalid_argument("GraphSAGE: one layer per sampling hop");
+        check(fdg_sage_create(topo.handle(), dims_.data(), std::uint32_t(fanouts.per_layer.size()),
+                              fanouts.per_layer.data(), max_seeds, &m_));
+    }
+    ~GraphSAGE() { fdg_sage_destroy(m_); }
+    GraphSAGE(const GraphSAGE&) = delete;
+    GraphSAGE& operator=(const GraphSAGE&) = delete;
+
+    /// w_neigh, w_self: [dims[l]][dims[l+1]] row-major (out = in . W); bias: [dims[l+1]].
+    void set_layer(std::uint32_t layer, const std::vector<float>& w_neigh, const std::vector<float>& w_self,
+                   const std::vector<float>& bias) {
+        check(fdg_sage_set_layer(m_, layer, w_neigh.data(), w_self.data(), bias.data()));
+    }
+
+    /// Mean loss over the batch's unique seeds, label(v) = splitmix64(v ^ label_seed) % C.
+    float forward(const graph::SampledBatch& b, std::uint64_t label_seed) const {
+        const std::uint64_t n = b.nodes.size(), e = b.edges.size();
+        fdg_batch_counts c{};
+        c.n_nodes = std::uint32_t(n);
+        c.n_edges = std::uint32_t(e);
+        c.n_layers = std::uint32_t(dims_.size() - 1);
+        for (std::size_t i = 0; i < b.layer_nodes.size() && i < FDG_MAX_LAYERS + 2; ++i)
+            c.layer_nodes[i] = std::uint32_t(b.layer_nodes[i]);
+        void *nd = nullptr, *ed = nullptr, *x = nullptr, *cd = nullptr, *ld = nullptr;
+        auto guard = [](void* p) { fdg_free(p); };
+        check(fdg_malloc(&nd, std::max<std::uint64_t>(n, 1) * 8));
+        std::unique_ptr<void, decltype(guard)> g1(nd, guard);
+        check(fdg_malloc(&ed, std::max<std::uint64_t>(e, 1) * 8));
+        std::unique_ptr<void, decltype(guard)> g2(ed, guard);
+        check(fdg_malloc(&x, std::max<std::uint64_t>(n, 1) * topo_.row_bytes()));
+        std::unique_ptr<void, decltype(guard)> g3(x, guard);
+        check(fdg_malloc(&cd, sizeof(c)));
+        std::unique_ptr<void, decltype(guard)> g4(cd, guard);
+        check(fdg_malloc(&ld, sizeof(float)));
+        std::unique_ptr<void, decltype(guard)> g5(ld, guard);
+        check(fdg_memcpy_h2d(nd, b.nodes.data(), n * 8, nullptr));
+        check(fdg_memcpy_h2d(ed, b.edges.data(), e * 8, nullptr));
+        check(fdg_memcpy_h2d(cd, &c, sizeof(c), nullptr));
+        if (n) check(fdg_gather(topo_.handle(), nullptr, static_cast<const std::uint64_t*>(nd), nullptr, n, x, nullptr));
+        check(fdg_sage_forward(m_, nullptr, x, static_cast<const std::uint64_t*>(nd), static_cast<const std::uint32_t*>(ed),
+                               static_cast<const fdg_batch_counts*>(cd), label_seed, static_cast<float*>(ld), nullptr));
+        float loss = 0.f;
+        check(fdg_memcpy_d2h(&loss, ld, sizeof(float), nullptr));
+        check(fdg_device_sync());
+        return loss;
+    }
+    fdg_sage* handle() const { return m_; }
+
+private:
+    const graph::Topology& topo_;
+    std::vector<std::uint32_t> dims_;
+    fdg_sage* m_ = nullptr;
+};
+
+}  // namespace train
 
 namespace featbuf {
 

@@ -37,6 +37,25 @@ int main(int argc, char** argv) {
                         (unsigned long long)st.loads, (unsigned long long)st.evictions);
         }
         buffer.validate();
+        // the train stage on the same blocks (extension: GraphSAGE forward + loss)
+        {
+            train::GraphSAGE model(*topo, {dim, 8, 4}, fan, std::uint32_t(batch));
+            const std::uint32_t d[3] = {dim, 8, 4};
+            for (std::uint32_t l = 0; l < 2; ++l) {
+                std::vector<float> wn(d[l] * d[l + 1]), ws(d[l] * d[l + 1]), bias(d[l + 1]);
+                for (std::uint32_t k = 0; k < d[l]; ++k)
+                    for (std::uint32_t c = 0; c < d[l + 1]; ++c) {
+                        wn[k * d[l + 1] + c] = float(int((k * 7 + c * 3) % 11) - 5) * 0.05f;
+                        ws[k * d[l + 1] + c] = float(int((k * 5 + c * 2) % 13) - 6) * 0.04f;
+                    }
+                for (std::uint32_t c = 0; c < d[l + 1]; ++c) bias[c] = float(int(c % 3) - 1) * 0.1f;
+                model.set_layer(l, wn, ws, bias);
+            }
+            for (std::uint64_t b = 0; b < 2; ++b) {
+                auto sb = graph::sample_khop(*topo, chunks[b], fan, pipeline::batch_seed(0, 0, b));
+                std::printf("loss %llu %.9g\n", (unsigned long long)b, double(model.forward(sb, 77)));
+            }
+        }
         // reference error behaviour: an out-of-range seed throws std::out_of_range
         std::vector<NodeId> bad{1, n + 5};
         try {
