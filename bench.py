@@ -430,10 +430,21 @@ def _train_stage(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, a
     dist.barrier()
     ms = dist.reduce(pipe.run(timed.ptr, False, rng_of(ids)), "max")
     losses = pipe.losses(len(ids))
+    # training mode: + backward (ReLU masks, transposed scatter-mean, weight gradients) + SGD
+    pipe.set_training(0.01)
+    pipe.run(warm.ptr, False, rng_of(ids_warm))
+    dist.barrier()
+    ms_train = dist.reduce(pipe.run(timed.ptr, False, rng_of(ids)), "max")
+    train_losses = pipe.losses(len(ids))
     pipe.close()
     model.close()
     K = len(ids)
     return {"value": dist.reduce(K, "sum") / (ms / 1e3), "unit": "batches/s", "ms_per_step": ms / K,
+            "train_step": {"value": dist.reduce(K, "sum") / (ms_train / 1e3), "unit": "batches/s",
+                           "ms_per_step": ms_train / K, "lr": 0.01,
+                           "loss_first_last": [float(train_losses[0]), float(train_losses[-1])],
+                           "includes": "forward + loss + backward + SGD per batch (data-parallel gradient "
+                                       "all-reduce not included: one GPU)"},
             "model": "GraphSAGE mean-aggregator " + "-".join(map(str, dims)) + (
                 ", layer GEMMs on tcgen05 (kind::tf32, 3xTF32 fp32-accurate)" if fd.featdrive.get_option("sage_gemm")
                 else ", fp32 CUDA-core GEMMs"),

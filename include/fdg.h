@@ -306,10 +306,26 @@ int fdg_sage_set_layer(fdg_sage* m, uint32_t layer, const float* w_neigh, const 
 int fdg_sage_forward(fdg_sage* m, void* stream, const void* x_dev, const uint64_t* nodes_dev,
                      const uint32_t* edges_dev, const fdg_batch_counts* counts_dev, uint64_t label_seed,
                      float* loss_dev, float* logits_dev);
+/* Host copies of layer `layer`'s current weights (grads = 0) or of its gradients from the
+ * last fdg_sage_backward (grads = 1), in fdg_sage_set_layer's layout; NULL outputs skipped. */
+int fdg_sage_get_layer(fdg_sage* m, uint32_t layer, int grads, float* w_neigh, float* w_self, float* bias);
+/* The contiguous device parameter and gradient blocks (same layout: per layer W_neigh, W_self,
+ * b): the gradient block is what a data-parallel all-reduce sums between backward and sgd. */
+int fdg_sage_buffers(fdg_sage* m, float** params_dev, float** grads_dev, uint64_t* n_floats);
+/* Backward of the last forward (same batch, same stream): d(loss)/d(W_neigh, W_self, b) of
+ * every layer into the gradient block. ReLU masks, scatter-mean transposed with vector
+ * atomics over the dst-sorted blocks, weight gradients as row-sliced A^T . dOut. */
+int fdg_sage_backward(fdg_sage* m, void* stream, const uint64_t* nodes_dev, const uint32_t* edges_dev,
+                      const fdg_batch_counts* counts_dev, uint64_t label_seed);
+/* SGD step params -= lr * grads (stream-ordered), refreshing the kernels' weight layouts. */
+int fdg_sage_sgd(fdg_sage* m, void* stream, float lr);
 /* Run the model after each batch's extraction inside fdg_pipeline_run (NULL = off; the
  * pipeline must materialise X). Per-batch losses of the last run: fdg_pipeline_losses. */
 int fdg_pipeline_set_model(fdg_pipeline* p, fdg_sage* m, uint64_t label_seed);
 int fdg_pipeline_losses(fdg_pipeline* p, uint64_t first, uint64_t n, float* out);
+/* Training mode of the train stage: lr != 0 adds backward + SGD after each batch's forward
+ * (stream-ordered on the extraction stream; the loss recorded is the pre-update one). */
+int fdg_pipeline_set_training(fdg_pipeline* p, float lr);
 
 /* ---- tracing: per-launch CUDA-event timeline (DurationCounter analogue, common.hpp:240-260) */
 int fdg_trace_enable(int on);          /* clears previous records when turning on */

@@ -68,3 +68,26 @@ def sage_forward(x: np.ndarray, nodes: np.ndarray, edges: np.ndarray, layer_node
     mx = logits.max(axis=1)
     lse = np.log(np.exp(logits - mx[:, None]).sum(axis=1)) + mx
     return float(np.mean(lse - logits[np.arange(len(logits)), y])), logits
+
+
+def sage_grads(x: np.ndarray, nodes: np.ndarray, edges: np.ndarray, layer_nodes, weights, label_seed: int):
+    """(loss, [(dW_neigh, dW_self, db) per layer]) of the same model by torch fp64 autograd:
+    the reference for the GPU backward (fdg_sage_backward)."""
+    import torch
+    L = len(weights)
+    D = hop_rows(layer_nodes, len(nodes), L)
+    h = torch.tensor(np.asarray(x, np.float64))
+    e = torch.tensor(np.asarray(edges, np.int64)).reshape(-1, 2)
+    params = [tuple(torch.tensor(np.asarray(a, np.float64), requires_grad=True) for a in w) for w in weights]
+    for k in range(1, L + 1):
+        rows = D[L - k]
+        wn, ws, b = params[k - 1]
+        m = e[:, 1] < rows
+        s = torch.zeros(rows, h.shape[1], dtype=torch.float64).index_add(0, e[m, 1], h[e[m, 0]])
+        c = torch.zeros(rows, dtype=torch.float64).index_add(0, e[m, 1], torch.ones(int(m.sum()), dtype=torch.float64))
+        out = (s / c.clamp(min=1).unsqueeze(1)) @ wn + h[:rows] @ ws + b
+        h = torch.relu(out) if k < L else out
+    y = torch.tensor(labels(nodes[: len(h)], label_seed, h.shape[1]))
+    loss = torch.nn.functional.cross_entropy(h, y)
+    loss.backward()
+    return float(loss.detach()), [tuple(p.grad.numpy() for p in ps) for ps in params]

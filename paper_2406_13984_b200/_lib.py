@@ -122,7 +122,12 @@ SIGNATURES = {
     "fdg_sage_destroy": (ci, [vp]),
     "fdg_sage_set_layer": (ci, [vp, u32, vp, vp, vp]),
     "fdg_sage_forward": (ci, [vp, vp, vp, vp, vp, vp, u64, vp, vp]),
+    "fdg_sage_get_layer": (ci, [vp, u32, ci, vp, vp, vp]),
+    "fdg_sage_buffers": (ci, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(u64)]),
+    "fdg_sage_backward": (ci, [vp, vp, vp, vp, vp, u64]),
+    "fdg_sage_sgd": (ci, [vp, vp, C.c_float]),
     "fdg_pipeline_set_model": (ci, [vp, vp, u64]),
+    "fdg_pipeline_set_training": (ci, [vp, C.c_float]),
     "fdg_pipeline_losses": (ci, [vp, u64, u64, vp]),
     "fdg_partition_epoch": (ci, [vp, u64, u64, u64, vp]),
     "fdg_batch_seed": (u64, [u64, u64, u64]),

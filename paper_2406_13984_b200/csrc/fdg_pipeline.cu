@@ -70,6 +70,7 @@ struct fdg_pipeline {
     bool l2_persist = false;             // this pipeline set aside persisting L2 (undone on destroy)
     fdg_sage* model = nullptr;           // optional train stage after each extraction
     uint64_t label_seed = 0;
+    float lr = 0.f;                      // != 0: backward + SGD after every forward
     float* losses = nullptr;             // device, one per batch of the current run
     uint64_t losses_cap = 0;
     uint64_t loss_batches = 0;           // batches of the last run with a loss
@@ -392,9 +393,14 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
             if (!p->bm) {
                 FDG_TRY(launch_gather_bound(*p->ctx, xs, p->nodes[nslot], n_dev, p->cap, p->cap, X, cs,
                                             &cnt->status));
-                if (train)
+                if (train) {
                     FDG_TRY(fdg_sage_forward(p->model, xs, X, p->nodes[nslot], p->edges[nslot], cnt, p->label_seed,
                                              p->losses + j, nullptr));
+                    if (p->lr != 0.f) {
+                        FDG_TRY(fdg_sage_backward(p->model, xs, p->nodes[nslot], p->edges[nslot], cnt, p->label_seed));
+                        FDG_TRY(fdg_sage_sgd(p->model, xs, p->lr));
+                    }
+                }
             } else {
                 const uint32_t par = uint32_t(j & 1);
                 // alias[par], is_load[par] and X[par] were last used by batch j-2's move
@@ -404,9 +410,14 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 FDG_CUDA(cudaStreamWaitEvent(xe, p->bound[par], 0));
                 FDG_TRY(bm_extract_move(p->bm, xe, p->nodes[nslot], n_dev, p->cap, p->alias[par], X, cs, par));
                 FDG_TRY(bm_status_to(p->bm, xe, &cnt->status));  // e.g. CAPACITY = StandbyTimeout
-                if (train)  // the trainer consumes X (and the batch's blocks) before they are reused
+                if (train) {  // the trainer consumes X (and the batch's blocks) before they are reused
                     FDG_TRY(fdg_sage_forward(p->model, xe, X, p->nodes[nslot], p->edges[nslot], cnt, p->label_seed,
                                              p->losses + j, nullptr));
+                    if (p->lr != 0.f) {
+                        FDG_TRY(fdg_sage_backward(p->model, xe, p->nodes[nslot], p->edges[nslot], cnt, p->label_seed));
+                        FDG_TRY(fdg_sage_sgd(p->model, xe, p->lr));
+                    }
+                }
                 FDG_CUDA(cudaEventRecord(p->moved[par], xe));
                 if (j > 0) {  // lag-1 release (the releaser stage, pipeline.hpp:525-543)
                     const uint64_t pj = do_sample ? j - 1 : ((j - 1) % (sampled_groups * G));
@@ -487,6 +498,11 @@ int fdg_pipeline_set_model(fdg_pipeline* p, fdg_sage* m, uint64_t label_seed) {
     if (m && !p->cfg.write_x) return fail(FDG_INVALID_ARG, "pipeline_set_model: the train stage needs X (write_x)");
     p->model = m;
     p->label_seed = label_seed;
+    return FDG_OK;
+}
+
+int fdg_pipeline_set_training(fdg_pipeline* p, float lr) {
+    p->lr = lr;
     return FDG_OK;
 }
 

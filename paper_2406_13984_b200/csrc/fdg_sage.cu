@@ -31,6 +31,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -39,8 +40,6 @@
 namespace fdg {
 // tensor-core GEMM (fdg_sage_tc.cu)
 int tc_make_map(CUtensorMap* map, const float* base, uint64_t rows, uint32_t K);
-void tc_split_weights(const float* Wcat, uint32_t K, uint32_t dout, uint32_t npad, std::vector<float>& hi,
-                      std::vector<float>& lo);
 int tc_gemm(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tBhi, const CUtensorMap& tBlo,
             const float* bias, float* C, const fdg_batch_counts* cnt, int j, uint64_t rows_bound, int N, int npad,
             int K, bool relu);
@@ -154,8 +153,9 @@ __global__ void __launch_bounds__(256) k_sgemm(const float* __restrict__ A, cons
     for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[i][q] = 0.f;
-    float4 ra = *reinterpret_cast<const float4*>(Ap);
-    float4 rb = *reinterpret_cast<const float4*>(Wp);
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 ra = ak < K ? *reinterpret_cast<const float4*>(Ap) : z4;
+    float4 rb = bk < K ? *reinterpret_cast<const float4*>(Wp) : z4;
     As[0][ak + 0][ar] = ra.x;
     As[0][ak + 1][ar] = ra.y;
     As[0][ak + 2][ar] = ra.z;
@@ -165,9 +165,9 @@ __global__ void __launch_bounds__(256) k_sgemm(const float* __restrict__ A, cons
     int buf = 0;
     for (int k0 = 0; k0 < K; k0 += kBK) {
         const bool more = k0 + kBK < K;
-        if (more) {
-            ra = *reinterpret_cast<const float4*>(Ap + k0 + kBK);
-            rb = *reinterpret_cast<const float4*>(Wp + size_t(k0 + kBK) * Npad);
+        if (more) {  // K is a multiple of 4: a float4 is either fully inside or fully past K
+            ra = k0 + kBK + ak < K ? *reinterpret_cast<const float4*>(Ap + k0 + kBK) : z4;
+            rb = k0 + kBK + bk < K ? *reinterpret_cast<const float4*>(Wp + size_t(k0 + kBK) * Npad) : z4;
         }
 #pragma unroll
         for (int kk = 0; kk < kBK; ++kk) {
@@ -291,6 +291,170 @@ __global__ void __launch_bounds__(kLossThreads) k_loss_mean(const float* __restr
     if (threadIdx.x == 0) *loss = rows ? float(s_part[0] / double(rows)) : 0.f;
 }
 
+// ------------------------------------------------------------------ backward --
+// dZ = (softmax(logits) - onehot(label)) / D_0: gradient of the mean loss.
+__global__ void __launch_bounds__(256) k_loss_grad(const float* __restrict__ logits, int C,
+                                                   const uint64_t* __restrict__ nodes, const fdg_batch_counts* cnt,
+                                                   uint64_t label_seed, float* __restrict__ dZ) {
+    const uint32_t rows = d_rows(cnt, 0);
+    const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const float* x = logits + size_t(r) * C;
+    float mx = -INFINITY;
+    for (int c = lane; c < C; c += 32) mx = fmaxf(mx, x[c]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float se = 0.f;
+    for (int c = lane; c < C; c += 32) se += expf(x[c] - mx);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const uint32_t label = uint32_t(splitmix64(nodes[r] ^ label_seed) % uint64_t(C));
+    const float inv = 1.f / float(rows);
+    for (int c = lane; c < C; c += 32)
+        dZ[size_t(r) * C + c] = (expf(x[c] - mx) / se - (uint32_t(c) == label ? 1.f : 0.f)) * inv;
+}
+
+// g *= (h > 0) over the first D_j rows of width d (ReLU backward).
+__global__ void k_relu_mask(float* __restrict__ g, const float* __restrict__ h, const fdg_batch_counts* cnt, int j,
+                            int d) {
+    const uint64_t total = uint64_t(d_rows(cnt, j)) * d;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x)
+        if (h[i] <= 0.f) g[i] = 0.f;
+}
+
+// Weight gradient A^T . B over the rows R = D_j (A [R x K], B [R x N], row-major), split over
+// row slices (blockIdx.z) into partials P[z] [K x N]; the k-tile-0 CTAs also produce the
+// column sums of B (bias gradient) into Pb[z] [N]. 64 x 64 outputs per CTA, 4 x 4 per thread.
+constexpr int kTn = 64, kTnR = 16;
+__global__ void __launch_bounds__(256) k_gemm_tn(const float* __restrict__ A, const float* __restrict__ B,
+                                                 const fdg_batch_counts* cnt, int j, int K, int N, float* __restrict__ P,
+                                                 float* __restrict__ Pb) {
+    __shared__ __align__(16) float As[kTnR][kTn];
+    __shared__ __align__(16) float Bs[kTnR][kTn];
+    const int R = int(d_rows(cnt, j));
+    const int Z = int(gridDim.z), z = int(blockIdx.z);
+    const int per = (R + Z - 1) / Z;
+    const int r0 = min(R, z * per), r1 = min(R, r0 + per);
+    const int k0 = blockIdx.y * kTn, n0 = blockIdx.x * kTn;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int lr = (tid * 4) / kTn, lc = (tid * 4) % kTn;
+    const bool bias_cta = blockIdx.y == 0;
+    float acc[4][4] = {};
+    float bs[4] = {};
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = r0; r < r1; r += kTnR) {
+        const int rr = r + lr;
+        *reinterpret_cast<float4*>(&As[lr][lc]) =
+            (rr < r1 && k0 + lc < K) ? *reinterpret_cast<const float4*>(A + size_t(rr) * K + k0 + lc) : z4;
+        *reinterpret_cast<float4*>(&Bs[lr][lc]) =
+            (rr < r1 && n0 + lc < N) ? *reinterpret_cast<const float4*>(B + size_t(rr) * N + n0 + lc) : z4;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kTnR; ++q) {
+            const float4 a = *reinterpret_cast<const float4*>(&As[q][ty * 4]);
+            const float4 b = *reinterpret_cast<const float4*>(&Bs[q][tx * 4]);
+            const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[i][c] = fmaf(av[i], bv[c], acc[i][c]);
+            if (bias_cta && ty == 0)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) bs[c] += bv[c];
+        }
+        __syncthreads();
+    }
+    float* Pz = P + size_t(z) * K * N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int k = k0 + ty * 4 + i;
+        if (k >= K) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (n0 + tx * 4 + c < N) Pz[size_t(k) * N + n0 + tx * 4 + c] = acc[i][c];
+    }
+    if (bias_cta && ty == 0)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (n0 + tx * 4 + c < N) Pb[size_t(z) * N + n0 + tx * 4 + c] = bs[c];
+}
+
+// G[0 : K N] = sum_z P[z], G[K N : K N + N] = sum_z Pb[z] (slices added in order).
+__global__ void k_tn_sum(const float* __restrict__ P, const float* __restrict__ Pb, int Z, int KN, int N,
+                         float* __restrict__ G) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < KN + N; i += gridDim.x * blockDim.x) {
+        float s = 0.f;
+        if (i < KN)
+            for (int z = 0; z < Z; ++z) s += P[size_t(z) * KN + i];
+        else
+            for (int z = 0; z < Z; ++z) s += Pb[size_t(z) * N + (i - KN)];
+        G[i] = s;
+    }
+}
+
+// Input gradient of a layer, self half: dH[v] = v < D_j ? dA[v][d:2d] : 0 for v < D_{j+1}.
+__global__ void k_dh_self(const float* __restrict__ dA, int d, const fdg_batch_counts* cnt, int j, float* dH) {
+    const uint32_t dst_rows = d_rows(cnt, j), rows = d_rows(cnt, j + 1);
+    const uint64_t total = uint64_t(rows) * d / 4;
+    for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < total; q += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t v = q * 4 / d, c = q * 4 - v * d;
+        reinterpret_cast<float4*>(dH)[q] = v < dst_rows ? *reinterpret_cast<const float4*>(dA + v * 2 * d + d + c)
+                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// Neighbour half: dH[src] += dA[v][0:d] / deg(v) for every edge src -> v, v < D_j
+// (warp per destination, vector atomics: sources repeat across destinations).
+__global__ void __launch_bounds__(256) k_dh_neigh(const float* __restrict__ dA, int d, const uint2* __restrict__ seg,
+                                                  const uint2* __restrict__ edges, const fdg_batch_counts* cnt, int j,
+                                                  float* dH) {
+    const uint32_t rows = d_rows(cnt, j);
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t v = warp; v < rows; v += nwarps) {
+        const uint2 sg = seg[v];
+        if (sg.y == sg.x) continue;
+        const float inv = 1.0f / float(sg.y - sg.x);
+        for (uint32_t c = lane * 4; c < uint32_t(d); c += 128) {
+            float4 g = *reinterpret_cast<const float4*>(dA + size_t(v) * 2 * d + c);
+            g.x *= inv;
+            g.y *= inv;
+            g.z *= inv;
+            g.w *= inv;
+            for (uint32_t e = sg.x; e < sg.y; ++e) atomicAdd(reinterpret_cast<float4*>(dH + size_t(edges[e].x) * d + c), g);
+        }
+    }
+}
+
+// P -= lr * G (SGD over the contiguous parameter block).
+__global__ void k_sgd(float* __restrict__ P, const float* __restrict__ G, uint64_t n, float lr) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        P[i] -= lr * G[i];
+}
+
+// The forward / backward copies of one layer's master weights Wm [K = 2 d_in x dout] + bias:
+// Wpad [K x npad] (CUDA-core GEMM), bpad [npad], Wt [dout x npadT] (backward dA GEMM),
+// and the tensor cores' transposed K-major hi / lo split [npad x K].
+__global__ void k_derive(const float* __restrict__ Wm, const float* __restrict__ bm, int K, int dout, int npad,
+                         int npadT, float* Wpad, float* bpad, float* Wt, float* Whi, float* Wlo) {
+    const int stride = gridDim.x * blockDim.x, t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int i = t0; i < K * npad; i += stride) {
+        const int k = i / npad, n = i - k * npad;
+        const float v = n < dout ? Wm[size_t(k) * dout + n] : 0.f;
+        Wpad[i] = v;
+        if (Whi) {
+            const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+            Whi[size_t(n) * K + k] = h;
+            Wlo[size_t(n) * K + k] = v - h;
+        }
+    }
+    for (int i = t0; i < dout * npadT; i += stride) {
+        const int n = i / npadT, k = i - n * npadT;
+        Wt[i] = k < K ? Wm[size_t(k) * dout + n] : 0.f;
+    }
+    for (int i = t0; i < npad; i += stride) bpad[i] = i < dout ? bm[i] : 0.f;
+}
+
 }  // namespace
 
 struct Sage {
@@ -298,20 +462,33 @@ struct Sage {
     uint32_t L = 0;
     std::vector<uint32_t> dims;     // L + 1
     std::vector<uint32_t> npad;     // per layer: d_out rounded up to kBN
+    std::vector<uint32_t> npadT;    // per layer: 2 d_in rounded up to kBN (backward dA GEMM)
     std::vector<uint64_t> bound;    // bound[j] >= D_j, j = 0..L
-    std::vector<float*> W, b;       // per layer: [2 d_in x npad], [npad]
-    uint2* seg = nullptr;
-    float* A = nullptr;
-    float* H[2] = {nullptr, nullptr};
-    float* logits = nullptr;
-    float* partial = nullptr;       // split-K slices
-    uint64_t partial_floats = 0;
-    float* row_loss = nullptr;
-    std::vector<uint8_t> set;
-    // tensor-core path: transposed K-major W_hi / W_lo and TMA maps per layer
-    std::vector<float*> Whi, Wlo;
+    // parameters: one contiguous block, per layer [W_neigh; W_self] (2 d_in x d_out, input-major)
+    // then b (d_out); gradients G share the layout (a single buffer to all-reduce)
+    float* P = nullptr;
+    float* G = nullptr;
+    std::vector<uint64_t> off;      // per layer offset into P / G
+    uint64_t n_params = 0;
+    std::vector<float*> W, b;       // derived: [2 d_in x npad], [npad] (CUDA-core forward)
+    std::vector<float*> Wt;         // derived: [d_out x npadT] (backward dA = dOut . W^T)
+    std::vector<float*> Whi, Wlo;   // derived: transposed K-major hi / lo split (tensor cores)
     std::vector<CUtensorMap> mapA, mapBhi, mapBlo;
     std::vector<uint8_t> tc_ok;     // layer K is a multiple of 32 and the maps were built
+    uint2* seg = nullptr;
+    std::vector<float*> Al;         // saved layer inputs [mean | self], [D_{L-1-l} x 2 d_in]
+    std::vector<float*> Hl;         // saved hidden outputs (post-ReLU), [D_{L-1-l} x d_out]
+    float* logits = nullptr;
+    float* partial = nullptr;       // forward split-K slices
+    uint64_t partial_floats = 0;
+    float* row_loss = nullptr;
+    float* dbuf[2] = {nullptr, nullptr};  // backward: output gradients of the current / next layer
+    float* dA = nullptr;
+    float* zeros = nullptr;
+    float* tn_part = nullptr;       // backward weight-gradient slices
+    uint64_t tn_floats = 0;
+    std::vector<uint8_t> set;
+    bool forwarded = false;
 };
 
 }  // namespace fdg
@@ -319,6 +496,22 @@ struct Sage {
 struct fdg_sage : fdg::Sage {};
 
 using namespace fdg;
+
+namespace {
+
+int tn_slices(uint64_t rows) { return int(std::min<uint64_t>(128, std::max<uint64_t>(1, rows / 512))); }
+
+int derive_layer(fdg_sage* m, uint32_t l, cudaStream_t st) {
+    const uint32_t K = 2 * m->dims[l], dout = m->dims[l + 1];
+    const int n = int(std::max<uint64_t>(uint64_t(K) * m->npad[l], uint64_t(dout) * m->npadT[l]));
+    k_derive<<<std::min(1024, (n + 255) / 256), 256, 0, st>>>(m->P + m->off[l], m->P + m->off[l] + uint64_t(K) * dout,
+                                                             int(K), int(dout), int(m->npad[l]), int(m->npadT[l]),
+                                                             m->W[l], m->b[l], m->Wt[l], m->Whi[l], m->Wlo[l]);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -346,19 +539,34 @@ int fdg_sage_create(fdg_ctx* ctx, const uint32_t* dims, uint32_t n_layers, const
             tot += layer;
         }
     }
-    uint32_t max_in = 0, max_out = 0;
-    for (uint32_t l = 0; l < n_layers; ++l) {
-        max_in = std::max(max_in, dims[l]);
-        max_out = std::max(max_out, dims[l + 1]);
-    }
-    const uint64_t rows = m->bound[n_layers - 1];  // destinations of layer 1
     auto al = [&](void** p, uint64_t bytes) { return cudaMalloc(p, std::max<uint64_t>(bytes, 16)); };
-    cudaError_t e = al((void**)&m->seg, rows * sizeof(uint2));
-    if (e == cudaSuccess) e = al((void**)&m->A, rows * 2 * max_in * 4);
-    if (e == cudaSuccess) e = al((void**)&m->H[0], rows * max_out * 4);
-    if (e == cudaSuccess) e = al((void**)&m->H[1], rows * max_out * 4);
+    uint64_t dmax = 0, amax = 0;  // largest gradient / dA buffers (floats)
+    for (uint32_t l = 0; l < n_layers; ++l) {
+        m->off.push_back(m->n_params);
+        m->n_params += uint64_t(2) * dims[l] * dims[l + 1] + dims[l + 1];
+        m->npad.push_back((dims[l + 1] + kBN - 1) / kBN * kBN);
+        m->npadT.push_back((2 * dims[l] + kBN - 1) / kBN * kBN);
+        const uint64_t rows = m->bound[n_layers - 1 - l];  // layer l+1 writes D_{L-1-l}
+        dmax = std::max<uint64_t>(dmax, rows * dims[l + 1]);
+        dmax = std::max<uint64_t>(dmax, m->bound[n_layers - l] * dims[l]);  // its input gradient
+        amax = std::max<uint64_t>(amax, rows * 2 * dims[l]);
+        m->tn_floats = std::max<uint64_t>(m->tn_floats, uint64_t(tn_slices(rows)) * (2 * dims[l] + 1) * dims[l + 1]);
+    }
+    cudaError_t e = al((void**)&m->seg, m->bound[n_layers - 1] * sizeof(uint2));
+    if (e == cudaSuccess) e = al((void**)&m->P, m->n_params * 4);
+    if (e == cudaSuccess) e = al((void**)&m->G, m->n_params * 4);
+    if (e == cudaSuccess) e = cudaMemset(m->P, 0, m->n_params * 4);
+    if (e == cudaSuccess) e = cudaMemset(m->G, 0, m->n_params * 4);
     if (e == cudaSuccess) e = al((void**)&m->logits, m->bound[0] * dims[n_layers] * 4);
     if (e == cudaSuccess) e = al((void**)&m->row_loss, m->bound[0] * 4);
+    if (e == cudaSuccess) e = al((void**)&m->dbuf[0], dmax * 4);
+    if (e == cudaSuccess) e = al((void**)&m->dbuf[1], dmax * 4);
+    if (e == cudaSuccess) e = al((void**)&m->dA, amax * 4);
+    if (e == cudaSuccess) e = al((void**)&m->tn_part, m->tn_floats * 4);
+    uint32_t zmax = 0;
+    for (uint32_t l = 0; l < n_layers; ++l) zmax = std::max(zmax, m->npadT[l]);
+    if (e == cudaSuccess) e = al((void**)&m->zeros, uint64_t(zmax) * 4);
+    if (e == cudaSuccess) e = cudaMemset(m->zeros, 0, uint64_t(zmax) * 4);
     // split-K slices: at most kMaxSplit x (rows of the largest split layer) x N
     for (uint32_t k = 1; k <= n_layers; ++k) {
         const uint64_t r = m->bound[n_layers - k];
@@ -366,34 +574,33 @@ int fdg_sage_create(fdg_ctx* ctx, const uint32_t* dims, uint32_t n_layers, const
         if (z > 1) m->partial_floats = std::max<uint64_t>(m->partial_floats, uint64_t(z) * r * dims[k]);
     }
     if (e == cudaSuccess && m->partial_floats) e = al((void**)&m->partial, m->partial_floats * 4);
-    for (uint32_t l = 0; l < n_layers && e == cudaSuccess; ++l) {
-        const uint32_t np = (dims[l + 1] + kBN - 1) / kBN * kBN;
-        m->npad.push_back(np);
-        float *w = nullptr, *bb = nullptr;
-        e = al((void**)&w, uint64_t(2) * dims[l] * np * 4);
-        if (e == cudaSuccess) e = al((void**)&bb, uint64_t(np) * 4);
-        if (e == cudaSuccess) e = cudaMemset(w, 0, uint64_t(2) * dims[l] * np * 4);
-        if (e == cudaSuccess) e = cudaMemset(bb, 0, uint64_t(np) * 4);
-        m->W.push_back(w);
-        m->b.push_back(bb);
-    }
-    m->set.assign(n_layers, 0);
+    m->W.assign(n_layers, nullptr);
+    m->b.assign(n_layers, nullptr);
+    m->Wt.assign(n_layers, nullptr);
     m->Whi.assign(n_layers, nullptr);
     m->Wlo.assign(n_layers, nullptr);
+    m->Al.assign(n_layers, nullptr);
+    m->Hl.assign(n_layers, nullptr);
     m->mapA.resize(n_layers);
     m->mapBhi.resize(n_layers);
     m->mapBlo.resize(n_layers);
     m->tc_ok.assign(n_layers, 0);
+    m->set.assign(n_layers, 0);
     for (uint32_t l = 0; l < n_layers && e == cudaSuccess; ++l) {
-        const uint32_t K = 2 * dims[l];
-        if (K % 32) continue;
-        e = al((void**)&m->Whi[l], uint64_t(m->npad[l]) * K * 4);
-        if (e == cudaSuccess) e = al((void**)&m->Wlo[l], uint64_t(m->npad[l]) * K * 4);
+        const uint32_t K = 2 * dims[l], np = m->npad[l];
+        const uint64_t rows = m->bound[n_layers - 1 - l];
+        e = al((void**)&m->W[l], uint64_t(K) * np * 4);
+        if (e == cudaSuccess) e = al((void**)&m->b[l], uint64_t(np) * 4);
+        if (e == cudaSuccess) e = al((void**)&m->Wt[l], uint64_t(dims[l + 1]) * m->npadT[l] * 4);
+        if (e == cudaSuccess) e = al((void**)&m->Al[l], rows * K * 4);
+        if (e == cudaSuccess && l + 1 < n_layers) e = al((void**)&m->Hl[l], rows * dims[l + 1] * 4);
+        if (e != cudaSuccess || K % 32) continue;
+        e = al((void**)&m->Whi[l], uint64_t(np) * K * 4);
+        if (e == cudaSuccess) e = al((void**)&m->Wlo[l], uint64_t(np) * K * 4);
         if (e != cudaSuccess) break;
-        const uint64_t rows_l = m->bound[n_layers - 1 - l];  // layer l+1 writes D_{L-1-l}
-        if (tc_make_map(&m->mapA[l], m->A, rows_l, K) == FDG_OK &&
-            tc_make_map(&m->mapBhi[l], m->Whi[l], m->npad[l], K) == FDG_OK &&
-            tc_make_map(&m->mapBlo[l], m->Wlo[l], m->npad[l], K) == FDG_OK)
+        if (tc_make_map(&m->mapA[l], m->Al[l], rows, K) == FDG_OK &&
+            tc_make_map(&m->mapBhi[l], m->Whi[l], np, K) == FDG_OK &&
+            tc_make_map(&m->mapBlo[l], m->Wlo[l], np, K) == FDG_OK)
             m->tc_ok[l] = 1;
     }
     if (e != cudaSuccess) {
@@ -407,17 +614,12 @@ int fdg_sage_create(fdg_ctx* ctx, const uint32_t* dims, uint32_t n_layers, const
 int fdg_sage_destroy(fdg_sage* m) {
     if (!m) return FDG_OK;
     cudaSetDevice(m->ctx->device);
-    cudaFree(m->seg);
-    cudaFree(m->A);
-    cudaFree(m->H[0]);
-    cudaFree(m->H[1]);
-    cudaFree(m->logits);
-    cudaFree(m->partial);
-    cudaFree(m->row_loss);
-    for (auto p : m->W) cudaFree(p);
-    for (auto p : m->b) cudaFree(p);
-    for (auto p : m->Whi) cudaFree(p);
-    for (auto p : m->Wlo) cudaFree(p);
+    for (void* p : {(void*)m->seg, (void*)m->P, (void*)m->G, (void*)m->logits, (void*)m->partial,
+                    (void*)m->row_loss, (void*)m->dbuf[0], (void*)m->dbuf[1], (void*)m->dA, (void*)m->zeros,
+                    (void*)m->tn_part})
+        cudaFree(p);
+    for (auto* v : {&m->W, &m->b, &m->Wt, &m->Whi, &m->Wlo, &m->Al, &m->Hl})
+        for (float* p : *v) cudaFree(p);
     delete m;
     return FDG_OK;
 }
@@ -425,28 +627,35 @@ int fdg_sage_destroy(fdg_sage* m) {
 int fdg_sage_set_layer(fdg_sage* m, uint32_t layer, const float* w_neigh, const float* w_self, const float* bias) {
     if (layer >= m->L) return fail(FDG_OUT_OF_RANGE, "sage_set_layer: layer out of range");
     cudaSetDevice(m->ctx->device);
-    const uint32_t din = m->dims[layer], dout = m->dims[layer + 1], np = m->npad[layer];
-    std::vector<float> w(uint64_t(2) * din * np, 0.f), bb(np, 0.f);
-    for (uint32_t k = 0; k < din; ++k)
-        for (uint32_t c = 0; c < dout; ++c) {
-            w[uint64_t(k) * np + c] = w_neigh[uint64_t(k) * dout + c];
-            w[uint64_t(din + k) * np + c] = w_self[uint64_t(k) * dout + c];
-        }
-    for (uint32_t c = 0; c < dout; ++c) bb[c] = bias ? bias[c] : 0.f;
-    FDG_CUDA(cudaMemcpy(m->W[layer], w.data(), w.size() * 4, cudaMemcpyHostToDevice));
-    if (m->Whi[layer]) {
-        std::vector<float> cat(uint64_t(2) * din * dout), hi, lo;
-        for (uint32_t k = 0; k < din; ++k)
-            for (uint32_t c = 0; c < dout; ++c) {
-                cat[uint64_t(k) * dout + c] = w_neigh[uint64_t(k) * dout + c];
-                cat[uint64_t(din + k) * dout + c] = w_self[uint64_t(k) * dout + c];
-            }
-        tc_split_weights(cat.data(), 2 * din, dout, np, hi, lo);
-        FDG_CUDA(cudaMemcpy(m->Whi[layer], hi.data(), hi.size() * 4, cudaMemcpyHostToDevice));
-        FDG_CUDA(cudaMemcpy(m->Wlo[layer], lo.data(), lo.size() * 4, cudaMemcpyHostToDevice));
-    }
-    FDG_CUDA(cudaMemcpy(m->b[layer], bb.data(), bb.size() * 4, cudaMemcpyHostToDevice));
+    const uint32_t din = m->dims[layer], dout = m->dims[layer + 1];
+    std::vector<float> blk(uint64_t(2) * din * dout + dout);
+    std::memcpy(blk.data(), w_neigh, uint64_t(din) * dout * 4);
+    std::memcpy(blk.data() + uint64_t(din) * dout, w_self, uint64_t(din) * dout * 4);
+    for (uint32_t c = 0; c < dout; ++c) blk[uint64_t(2) * din * dout + c] = bias ? bias[c] : 0.f;
+    FDG_CUDA(cudaMemcpy(m->P + m->off[layer], blk.data(), blk.size() * 4, cudaMemcpyHostToDevice));
+    FDG_TRY(derive_layer(m, layer, nullptr));
+    FDG_CUDA(cudaDeviceSynchronize());
     m->set[layer] = 1;
+    return FDG_OK;
+}
+
+int fdg_sage_get_layer(fdg_sage* m, uint32_t layer, int grads, float* w_neigh, float* w_self, float* bias) {
+    if (layer >= m->L) return fail(FDG_OUT_OF_RANGE, "sage_get_layer: layer out of range");
+    cudaSetDevice(m->ctx->device);
+    FDG_CUDA(cudaDeviceSynchronize());
+    const uint32_t din = m->dims[layer], dout = m->dims[layer + 1];
+    const float* src = (grads ? m->G : m->P) + m->off[layer];
+    const uint64_t wn = uint64_t(din) * dout;
+    if (w_neigh) FDG_CUDA(cudaMemcpy(w_neigh, src, wn * 4, cudaMemcpyDeviceToHost));
+    if (w_self) FDG_CUDA(cudaMemcpy(w_self, src + wn, wn * 4, cudaMemcpyDeviceToHost));
+    if (bias) FDG_CUDA(cudaMemcpy(bias, src + 2 * wn, dout * 4, cudaMemcpyDeviceToHost));
+    return FDG_OK;
+}
+
+int fdg_sage_buffers(fdg_sage* m, float** params_dev, float** grads_dev, uint64_t* n_floats) {
+    if (params_dev) *params_dev = m->P;
+    if (grads_dev) *grads_dev = m->G;
+    if (n_floats) *n_floats = m->n_params;
     return FDG_OK;
 }
 
@@ -471,14 +680,15 @@ int fdg_sage_forward(fdg_sage* m, void* stv, const void* x_dev, const uint64_t* 
         const int j = int(L - k);  // destinations: D_j
         const uint32_t din = m->dims[k - 1], dout = m->dims[k];
         const uint64_t rows = m->bound[j];
+        float* A = m->Al[k - 1];
         const uint32_t agg_blocks = uint32_t(std::min<uint64_t>((rows + 7) / 8, uint64_t(c.sm_count) * 16));
         if (k == 1 && c.dtype == 1)
             k_aggregate<__half><<<agg_blocks, 256, 0, st>>>(static_cast<const __half*>(x_dev), din, m->seg, edges,
-                                                            counts_dev, j, m->A);
+                                                            counts_dev, j, A);
         else
             k_aggregate<float><<<agg_blocks, 256, 0, st>>>(k == 1 ? static_cast<const float*>(x_dev) : hin, din,
-                                                           m->seg, edges, counts_dev, j, m->A);
-        float* hout = k == L ? m->logits : m->H[k & 1];
+                                                           m->seg, edges, counts_dev, j, A);
+        float* hout = k == L ? m->logits : m->Hl[k - 1];
         if (g_sage_gemm == 1 && m->tc_ok[k - 1]) {
             FDG_TRY(tc_gemm(st, m->mapA[k - 1], m->mapBhi[k - 1], m->mapBlo[k - 1], m->b[k - 1], hout, counts_dev,
                             j, rows, int(dout), int(m->npad[k - 1]), int(2 * din), k != L));
@@ -490,10 +700,10 @@ int fdg_sage_forward(fdg_sage* m, void* stv, const void* x_dev, const uint64_t* 
         float* gout = z > 1 ? m->partial : hout;
         const uint64_t slice = rows * dout;
         if (k == L)
-            k_sgemm<false><<<grid, 256, 0, st>>>(m->A, m->W[k - 1], m->b[k - 1], gout, counts_dev, j, int(dout),
+            k_sgemm<false><<<grid, 256, 0, st>>>(A, m->W[k - 1], m->b[k - 1], gout, counts_dev, j, int(dout),
                                                  int(2 * din), int(m->npad[k - 1]), slice);
         else
-            k_sgemm<true><<<grid, 256, 0, st>>>(m->A, m->W[k - 1], m->b[k - 1], gout, counts_dev, j, int(dout),
+            k_sgemm<true><<<grid, 256, 0, st>>>(A, m->W[k - 1], m->b[k - 1], gout, counts_dev, j, int(dout),
                                                 int(2 * din), int(m->npad[k - 1]), slice);
         if (z > 1) {
             const int sb = int(std::min<uint64_t>((slice / 4 + 255) / 256, uint64_t(c.sm_count) * 8));
@@ -509,6 +719,63 @@ int fdg_sage_forward(fdg_sage* m, void* stv, const void* x_dev, const uint64_t* 
     k_loss_rows<<<uint32_t((m->bound[0] + 7) / 8), 256, 0, st>>>(m->logits, int(m->dims[L]), nodes_dev, counts_dev,
                                                                   label_seed, m->row_loss, logits_dev);
     k_loss_mean<<<1, kLossThreads, 0, st>>>(m->row_loss, counts_dev, loss_dev);
+    FDG_CUDA(cudaGetLastError());
+    m->forwarded = true;
+    return FDG_OK;
+}
+
+// Backward of the last forward (same batch, same stream): gradients of the mean loss w.r.t.
+// every layer's W_neigh, W_self and b into the gradient buffer.
+int fdg_sage_backward(fdg_sage* m, void* stv, const uint64_t* nodes_dev, const uint32_t* edges_dev,
+                      const fdg_batch_counts* counts_dev, uint64_t label_seed) {
+    if (!m->forwarded) return fail(FDG_NOT_LOADED, "sage_backward: no forward to differentiate");
+    cudaStream_t st = (cudaStream_t)stv;
+    const Ctx& c = *m->ctx;
+    const uint32_t L = m->L;
+    const uint2* edges = reinterpret_cast<const uint2*>(edges_dev);
+    FDG_TRACE("sage_bwd", st);
+    float* cur = m->dbuf[0];
+    k_loss_grad<<<uint32_t((m->bound[0] + 7) / 8), 256, 0, st>>>(m->logits, int(m->dims[L]), nodes_dev, counts_dev,
+                                                                  label_seed, cur);
+    for (uint32_t k = L; k >= 1; --k) {
+        const int j = int(L - k);
+        const uint32_t din = m->dims[k - 1], dout = m->dims[k], K = 2 * din;
+        const uint64_t rows = m->bound[j];
+        if (k < L)
+            k_relu_mask<<<uint32_t(std::min<uint64_t>((rows * dout + 255) / 256, uint64_t(c.sm_count) * 8)), 256, 0,
+                          st>>>(cur, m->Hl[k - 1], counts_dev, j, int(dout));
+        // weight + bias gradients: A^T . dOut over the D_j rows, in row slices
+        const int Z = tn_slices(rows);
+        dim3 grid((dout + kTn - 1) / kTn, (K + kTn - 1) / kTn, uint32_t(Z));
+        float* Pb = m->tn_part + uint64_t(Z) * K * dout;
+        k_gemm_tn<<<grid, 256, 0, st>>>(m->Al[k - 1], cur, counts_dev, j, int(K), int(dout), m->tn_part, Pb);
+        const int kn = int(K * dout);
+        k_tn_sum<<<std::min(1024, (kn + int(dout) + 255) / 256), 256, 0, st>>>(m->tn_part, Pb, Z, kn, int(dout),
+                                                                              m->G + m->off[k - 1]);
+        if (k == 1) break;
+        // input gradient: dA = dOut . [W_neigh; W_self]^T, then scatter to h^{k-1}
+        dim3 ag(m->npadT[k - 1] / kBN, uint32_t((rows + kBM - 1) / kBM), 1);
+        k_sgemm<false><<<ag, 256, 0, st>>>(cur, m->Wt[k - 1], m->zeros, m->dA, counts_dev, j, int(K), int(dout),
+                                           int(m->npadT[k - 1]), 0);
+        float* nxt = cur == m->dbuf[0] ? m->dbuf[1] : m->dbuf[0];
+        const uint64_t in_rows = m->bound[j + 1];
+        k_dh_self<<<uint32_t(std::min<uint64_t>((in_rows * din / 4 + 255) / 256, uint64_t(c.sm_count) * 8)), 256, 0,
+                    st>>>(m->dA, int(din), counts_dev, j, nxt);
+        k_dh_neigh<<<uint32_t(std::min<uint64_t>((rows + 7) / 8, uint64_t(c.sm_count) * 16)), 256, 0, st>>>(
+            m->dA, int(din), m->seg, edges, counts_dev, j, nxt);
+        cur = nxt;
+    }
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
+// SGD step from the gradient buffer (after an optional all-reduce), then refresh every
+// derived weight copy (CUDA-core, tensor-core and transposed layouts).
+int fdg_sage_sgd(fdg_sage* m, void* stv, float lr) {
+    cudaStream_t st = (cudaStream_t)stv;
+    k_sgd<<<uint32_t(std::min<uint64_t>((m->n_params + 255) / 256, uint64_t(m->ctx->sm_count) * 4)), 256, 0, st>>>(
+        m->P, m->G, m->n_params, lr);
+    for (uint32_t l = 0; l < m->L; ++l) FDG_TRY(derive_layer(m, l, st));
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;
 }

@@ -295,24 +295,6 @@ int tc_make_map(CUtensorMap* map, const float* base, uint64_t rows, uint32_t K) 
     return FDG_OK;
 }
 
-// Host split of W (input-major [K x dout]) into transposed K-major hi / lo [npad x K].
-void tc_split_weights(const float* Wcat, uint32_t K, uint32_t dout, uint32_t npad, std::vector<float>& hi,
-                      std::vector<float>& lo) {
-    hi.assign(uint64_t(npad) * K, 0.f);
-    lo.assign(uint64_t(npad) * K, 0.f);
-    for (uint32_t k = 0; k < K; ++k)
-        for (uint32_t n = 0; n < dout; ++n) {
-            const float v = Wcat[uint64_t(k) * dout + n];
-            uint32_t u;
-            std::memcpy(&u, &v, 4);
-            u &= 0xFFFFE000u;
-            float h;
-            std::memcpy(&h, &u, 4);
-            hi[uint64_t(n) * K + k] = h;
-            lo[uint64_t(n) * K + k] = v - h;
-        }
-}
-
 int tc_gemm(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tBhi, const CUtensorMap& tBlo,
             const float* bias, float* C, const fdg_batch_counts* cnt, int j, uint64_t rows_bound, int N, int npad,
             int K, bool relu) {

@@ -530,6 +530,10 @@ class Pipeline:
         self.model = model
         check(lib().fdg_pipeline_set_model(self.ptr, model.ptr if model else None, label_seed))
 
+    def set_training(self, lr: float):
+        """lr != 0: the train stage also runs backward + SGD after every forward."""
+        check(lib().fdg_pipeline_set_training(self.ptr, lr))
+
     def losses(self, n: int, first: int = 0) -> np.ndarray:
         out = np.empty(n, np.float32)
         check(lib().fdg_pipeline_losses(self.ptr, first, n, _p(out)))
@@ -642,9 +646,8 @@ class GraphSAGE:
         check(lib().fdg_sage_forward(self.ptr, stream.ptr if stream else None, x_ptr, nodes_ptr, edges_ptr,
                                      counts_ptr, label_seed, loss_ptr, logits_ptr))
 
-    def forward(self, batch: SampledBatch, label_seed: int = 0):
-        """Host convenience: X gathered on the device from the batch's nodes, then the
-        forward; returns (loss, logits of the unique seeds)."""
+    def _upload(self, batch: SampledBatch):
+        """Device copies of a host batch: nodes, edges, the batch record and X (gathered)."""
         n, e = len(batch.nodes), len(batch.edges)
         cnt = _lib.BatchCounts()
         cnt.n_nodes, cnt.n_edges, cnt.n_layers = n, e, len(batch.layer_nodes) - 2
@@ -659,6 +662,12 @@ class GraphSAGE:
         x = DeviceBuffer(max(n, 1) * self.topo.row_bytes)
         if n:
             check(lib().fdg_gather(self.topo.ctx, None, nd.ptr, None, n, x.ptr, None))
+        return nd, ed, cd, x
+
+    def forward(self, batch: SampledBatch, label_seed: int = 0):
+        """Host convenience: X gathered on the device from the batch's nodes, then the
+        forward; returns (loss, logits of the unique seeds)."""
+        nd, ed, cd, x = self._upload(batch)
         loss = DeviceBuffer(4)
         seeds = int(max(batch.layer_nodes[:2])) if len(batch.layer_nodes) > 1 else 0
         logits = DeviceBuffer(max(seeds, 1) * self.dims[-1] * 4)
@@ -666,6 +675,38 @@ class GraphSAGE:
         check(lib().fdg_device_sync())
         return (float(loss.download(np.float32)[0]),
                 logits.download(np.float32, seeds * self.dims[-1]).reshape(seeds, self.dims[-1]))
+
+    def train_step(self, batch: SampledBatch, label_seed: int = 0, lr: float = 0.0, allreduce=None) -> float:
+        """forward + backward (+ allreduce(grads) for data parallelism) + SGD; returns the
+        pre-update loss. lr = 0 leaves the weights unchanged (gradients only)."""
+        nd, ed, cd, x = self._upload(batch)
+        loss = DeviceBuffer(4)
+        self.forward_async(None, x.ptr, nd.ptr, ed.ptr, cd.ptr, label_seed, loss.ptr, None)
+        check(lib().fdg_sage_backward(self.ptr, None, nd.ptr, ed.ptr, cd.ptr, label_seed))
+        if allreduce is not None:
+            check(lib().fdg_device_sync())
+            allreduce(self)
+        if lr:
+            check(lib().fdg_sage_sgd(self.ptr, None, lr))
+        check(lib().fdg_device_sync())
+        return float(loss.download(np.float32)[0])
+
+    def sgd(self, lr: float):
+        check(lib().fdg_sage_sgd(self.ptr, None, lr))
+        check(lib().fdg_device_sync())
+
+    def layer(self, layer: int, grads: bool = False):
+        """(W_neigh, W_self, b) of a layer -- or their gradients from the last backward."""
+        din, dout = self.dims[layer], self.dims[layer + 1]
+        wn, ws, b = np.empty((din, dout), np.float32), np.empty((din, dout), np.float32), np.empty(dout, np.float32)
+        check(lib().fdg_sage_get_layer(self.ptr, layer, 1 if grads else 0, _p(wn), _p(ws), _p(b)))
+        return wn, ws, b
+
+    def buffers(self):
+        """(params_dev_ptr, grads_dev_ptr, n_floats): the contiguous parameter / gradient blocks."""
+        pp, gp, n = C.c_void_p(), C.c_void_p(), C.c_uint64()
+        check(lib().fdg_sage_buffers(self.ptr, C.byref(pp), C.byref(gp), C.byref(n)))
+        return pp.value, gp.value, n.value
 
     def close(self):
         if getattr(self, "ptr", None):

@@ -116,3 +116,94 @@ def test_pipeline_train_stage(fd, bm):
             want, _ = sage.sage_forward(_rows(t, batch.nodes, np.float32), batch.nodes, batch.edges,
                                         batch.layer_nodes, model.weights, 5)
             assert abs(loss - want) <= LOSS_RTOL * abs(want)
+
+
+# ------------------------------------------------------------------ backward --
+def _grads_close(model, want, rtol=2e-4):
+    for layer, w in enumerate(want):
+        got = model.layer(layer, grads=True)
+        for g, t in zip(got, w):
+            scale = max(np.abs(t).max(), 1e-12)
+            np.testing.assert_allclose(g, t, rtol=rtol, atol=rtol * scale)
+
+
+@pytest.mark.parametrize("dim,dims,fan,seeds", [
+    (32, [32, 64, 64, 12], [10, 10, 10], 300),
+    (128, [128, 256, 256, 172], [10, 10, 10], 200),   # the paper's model shape (d_out 172: K % 8 = 4)
+    (16, [16, 8], [25], 500),
+])
+def test_sage_backward_vs_autograd(fd, gemm, dim, dims, fan, seeds):
+    """fdg_sage_backward: every layer's W_neigh / W_self / b gradient against torch fp64
+    autograd of the same model (fp32 + atomics: 2e-4 relative to each tensor's scale)."""
+    t = fd.Topology.generate(60_000, dim, 12, 5)
+    s = np.random.RandomState(dim + 1).randint(0, 60_000, seeds).astype(np.uint64)
+    batch = fd.sample_khop(t, s, fan, fd.batch_seed(0, 1, dim))
+    model = fd.GraphSAGE(t, dims, fan, max_seeds=seeds, seed=dim + 1)
+    loss = model.train_step(batch, label_seed=11, lr=0.0)
+    want_loss, want = sage.sage_grads(_rows(t, batch.nodes, np.float32), batch.nodes, batch.edges,
+                                      batch.layer_nodes, model.weights, 11)
+    assert abs(loss - want_loss) <= LOSS_RTOL * abs(want_loss)
+    _grads_close(model, want)
+
+
+def test_sage_sgd_step_and_descent(fd, gemm):
+    """SGD: W' = W - lr * grad exactly as the host computes it, the derived (tensor-core /
+    CUDA-core) copies follow, and repeated steps on one batch reduce its loss."""
+    t = fd.Topology.generate(40_000, 32, 10, 2)
+    s = np.arange(0, 40_000, 157, dtype=np.uint64)
+    batch = fd.sample_khop(t, s, [10, 5], 3)
+    model = fd.GraphSAGE(t, [32, 64, 16], [10, 5], max_seeds=len(s), seed=4)
+    before = [model.layer(i) for i in range(2)]
+    l0 = model.train_step(batch, label_seed=1, lr=0.0)
+    grads = [model.layer(i, grads=True) for i in range(2)]
+    model.sgd(0.5)
+    for i in range(2):
+        for w, g, now in zip(before[i], grads[i], model.layer(i)):
+            np.testing.assert_allclose(now, w.astype(np.float64) - 0.5 * g.astype(np.float64), rtol=1e-6, atol=1e-7)
+    loss1, _ = model.forward(batch, 1)
+    assert loss1 < l0
+    losses = [model.train_step(batch, label_seed=1, lr=0.5) for _ in range(5)]
+    assert losses[-1] < losses[0] < l0
+
+
+def test_sage_backward_zero_degree(fd):
+    """Isolated seeds / an early-stopped frontier: zero-degree destinations scatter nothing."""
+    n = 2000
+    rs = np.random.RandomState(4)
+    indptr, indices = [0], []
+    for v in range(n):
+        nb = [] if v < 1000 else sorted(set(rs.randint(1000, n, rs.randint(1, 6)).tolist()) - {v})
+        indices += nb
+        indptr.append(len(indices))
+    feats = rs.standard_normal((n, 8)).astype(np.float32)
+    t = fd.Topology.from_arrays(np.array(indptr, np.uint64), np.array(indices, np.uint64), feats)
+    batch = fd.sample_khop(t, np.array([5, 5, 17, 1500, 1999, 3, 1200], np.uint64), [4, 4, 4], 9)
+    model = fd.GraphSAGE(t, [8, 12, 4, 8], [4, 4, 4], max_seeds=7, seed=1)
+    model.train_step(batch, label_seed=3)
+    _, want = sage.sage_grads(_rows(t, batch.nodes, np.float32), batch.nodes, batch.edges, batch.layer_nodes,
+                              model.weights, 3)
+    _grads_close(model, want)
+
+
+def test_pipeline_training_matches_host_loop(fd):
+    """The runner in training mode (forward + backward + SGD per batch) reproduces a host
+    loop of train_step over the same batches: losses and final weights."""
+    n, B, fan = 100_000, 128, [5, 5]
+    t = fd.Topology.generate(n, 32, 10, 6)
+    order = np.concatenate(fd.partition_epoch(np.arange(6 * B, dtype=np.uint64), B, 5))
+    rng = np.array([fd.batch_seed(0, 0, b) for b in range(6)], np.uint64)
+    a = fd.GraphSAGE(t, [32, 32, 8], fan, max_seeds=B, seed=9)
+    b = fd.GraphSAGE(t, [32, 32, 8], fan, max_seeds=B, seed=9)
+    pipe = fd.Pipeline(t, fan, B, samplers=2)
+    pipe.set_model(a, label_seed=2)
+    pipe.set_training(0.3)
+    pipe.run_batches(order, rng)
+    losses = pipe.losses(6)
+    pipe.close()
+    for j in range(6):
+        batch = fd.sample_khop(t, order[j * B:(j + 1) * B], fan, int(rng[j]))
+        lj = b.train_step(batch, label_seed=2, lr=0.3)
+        assert abs(losses[j] - lj) <= 1e-5 * abs(lj), j
+    for i in range(2):
+        for u, v in zip(a.layer(i), b.layer(i)):
+            np.testing.assert_allclose(u, v, rtol=1e-4, atol=1e-6)
