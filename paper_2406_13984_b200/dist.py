@@ -94,3 +94,36 @@ def local_device(local_rank: int) -> int:
 def rank_batches(n_batches: int, world: int, rank: int) -> np.ndarray:
     lo, hi = segment(n_batches, world, rank)
     return np.arange(lo, hi, dtype=np.int64)
+
+
+class _DeviceArray:
+    """A libfdg device buffer viewed through __cuda_array_interface__ (no copy)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
+
+
+def allreduce_grads(model: "fdm.GraphSAGE", group=None) -> None:
+    """Data-parallel train stage: average the model's contiguous gradient block over the
+    ranks (call between fdg_sage_backward and fdg_sage_sgd, e.g. as
+    GraphSAGE.train_step(..., allreduce=allreduce_grads)). With NCCL the block is reduced
+    in place on the device (torch wraps the pointer); other backends stage through host
+    memory."""
+    import torch
+    import torch.distributed as dist
+    _, gp, n = model.buffers()
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        t = torch.as_tensor(_DeviceArray(gp, n), device="cuda")
+        dist.all_reduce(t, group=group)
+        t.div_(world)
+        torch.cuda.synchronize()
+        return
+    host = np.empty(n, np.float32)
+    fdm.check(fdm.lib().fdg_memcpy_d2h(host.ctypes.data, gp, n * 4, None))
+    fdm.check(fdm.lib().fdg_device_sync())
+    t = torch.from_numpy(host)
+    dist.all_reduce(t, group=group)
+    t.div_(world)
+    fdm.check(fdm.lib().fdg_memcpy_h2d(gp, host.ctypes.data, n * 4, None))
+    fdm.check(fdm.lib().fdg_device_sync())

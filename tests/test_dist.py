@@ -91,3 +91,16 @@ def test_two_process_ipc_sharded_gather(dtype):
                          env=dict(os.environ, MP_SHARD_DTYPE=dtype))
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert out.stdout.count("shard-ok") == 2
+
+
+@pytest.mark.gpu
+def test_two_process_data_parallel_train_stage():
+    """Two ranks (torchrun, one GPU): per-rank backward, gradient all-reduce
+    (paper_2406_13984_b200.dist.allreduce_grads), identical SGD steps."""
+    port = _free_port()
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port),
+                          os.path.join(ROOT, "tests", "mp_train_check.py")],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert out.stdout.count("train-ok") == 2
