@@ -5,7 +5,11 @@
 // (extractor.hpp:142-151, 391-394) for stream-ordered batches. Exactly the
 // reference's state transitions and LRU order, computed batch-parallel:
 //
-//   mapping table  node -> packed {i32 slot, u32 valid<<31 | ref}  (8 B/node)
+//   mapping table  node -> packed {i32 slot, u32 valid<<31}  (8 B/node)
+//   slot refs      slot -> u32 reference count (the reference keeps ref in the mapping
+//                  entry; a bound node's count lives with its slot here, so the release
+//                  walks the batch's alias list into a compact 4 B/slot array that stays
+//                  L2-resident instead of re-reading 8 B/node entries from DRAM)
 //   slot table     slot -> {u64 owner node (~0 = free), u64 ring position of its
 //                  live standby entry (~0 = not in the standby list)}: one 16-byte
 //                  record, so the reverse map and list membership share a sector
@@ -44,7 +48,6 @@ namespace fdg {
 namespace {
 
 constexpr uint32_t kValid = 0x80000000u;
-constexpr uint32_t kRefMask = 0x7FFFFFFFu;
 constexpr uint64_t kNoNode = ~0ull;
 constexpr int kT = 256;        // threads per tile
 constexpr int kI = 8;          // items per thread
@@ -75,6 +78,7 @@ struct BmState {
 
 struct BmDev {
     Entry* map;
+    uint32_t* ref;        // slot -> reference count of its bound node
     SlotMeta* slot;       // slot -> {owner node, live ring position}
     int32_t* ring[2];
     uint64_t R;           // ring capacity
@@ -200,24 +204,22 @@ __global__ void __launch_bounds__(kT) k_acquire(BmDev B, const uint64_t* nodes, 
             continue;
         }
         const Entry e = en[k];
-        const uint32_t ref = e.refv & kRefMask;
-        if (e.refv & kValid) {
+        if (e.refv & kValid) {  // hit: ref++ (a batch's nodes, hence slots, are distinct)
+            const uint32_t ref = B.ref[e.slot];
             if (ref == 0) {  // StandbyList::remove (buffer_manager.hpp:250)
                 B.slot[e.slot].pos = kUnlisted;
                 ++removed;
             }
+            B.ref[e.slot] = ref + 1;
             alias[i] = e.slot;
             is_load[i] = 0;
             ++hits;
-        } else if (ref > 0) {
-            bad = true;  // in flight elsewhere: impossible for stream-ordered batches
-        } else {
+        } else {  // miss: its ref starts at 1 when k_bind gives it a slot
             alias[i] = -1;
             is_load[i] = 1;
             load_mask |= 1u << k;
             ++mine;
         }
-        B.map[node].refv = e.refv + 1;
     }
     if (bad) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
     if (hits) atomicAdd(&s_hits, (unsigned long long)hits);
@@ -311,15 +313,15 @@ __global__ void k_bind(BmDev B, const uint64_t* nodes, int64_t* alias) {
         const uint32_t i = B.load_pos[k];
         const uint64_t node = nodes[i];
         const uint64_t prev = B.slot[slot].node;
-        Entry e = B.map[node];
         if (prev != kNoNode) {  // invalidate the previous owner (buffer_manager.hpp:281-291)
             const Entry pe = B.map[prev];
-            if ((pe.refv & kRefMask) != 0 || pe.slot != slot) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
+            if (B.ref[slot] != 0 || pe.slot != slot) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
             B.map[prev] = Entry{-1, 0u};
             ++ev;
         }
-        B.map[node] = Entry{slot, e.refv | kValid};  // bind + publish
+        B.map[node] = Entry{slot, kValid};  // bind + publish
         B.slot[slot] = SlotMeta{node, kUnlisted};
+        B.ref[slot] = 1;
         alias[i] = slot;
     }
 #pragma unroll
@@ -332,10 +334,15 @@ __global__ void k_bind(BmDev B, const uint64_t* nodes, int64_t* alias) {
 }
 
 // --------------------------------------------------------------- k_move ----
-// 16-byte chunks over the batch: misses read the table and fill their slot
-// (and X); hits read their slot (into X). Without X only misses move. Reads only
-// per-batch state (alias, is_load[parity]), so it may run on its own stream while
-// the next batch's acquire / select / bind proceed.
+// Misses read the table row and fill their slot (and X); hits read their slot (into
+// X). Without X only misses move. Reads only per-batch state (alias, is_load[parity]),
+// so it runs on its own stream while the next batch's acquire / select / bind proceed
+// -- which is why it is launched on half the SM's thread slots (2 x 512 per SM): a
+// full-occupancy grid keeps the latency-bound metadata kernels off the SMs (release
+// 332 us in the pipeline at 4 x 512 per SM vs 32 us alone). A warp moves kMoveRows rows
+// at a time: their metadata (one lane per row, shuffled) resolves first, then every
+// lane has kMoveRows 16-byte loads in flight.
+constexpr int kMoveRows = 4;
 __global__ void __launch_bounds__(512) k_move(BmDev B, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                                               const int64_t* alias, const uint8_t* is_load, const char* table,
                                               char* region, uint32_t rb, char* X) {
@@ -343,37 +350,63 @@ __global__ void __launch_bounds__(512) k_move(BmDev B, const uint64_t* nodes, co
     if (S->status) return;
     const uint32_t cpr = rb / 16;
     const uint64_t n = load_n(n_dev, n_host);
-    const uint64_t total = n * cpr;
     uint64_t pol;  // row traffic must not flush the batch's metadata sectors out of L2
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    for (uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; c < total; c += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t i = c / cpr, col = c - i * cpr;
-        const bool miss = is_load[i];
-        if (!miss && !X) continue;
-        const int64_t slot = alias[i];
-        uint4* dst_slot = reinterpret_cast<uint4*>(region + uint64_t(slot) * rb) + col;
-        const uint4* src = miss ? reinterpret_cast<const uint4*>(table + nodes[i] * rb) + col : dst_slot;
-        if (miss || X) {
-            uint4 v;
-            asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                         : "l"(src), "l"(pol));
-            if (miss)
-                asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dst_slot), "r"(v.x),
-                             "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
-                             : "memory");
-            if (X)
-                asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(
-                                 reinterpret_cast<uint4*>(X + i * rb) + col),
-                             "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
-                             : "memory");
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t r0 = warp * kMoveRows; r0 < n; r0 += nwarps * kMoveRows) {
+        // lane q < kMoveRows resolves row r0 + q: source row, slot row, miss flag
+        const char* my_src = nullptr;
+        char* my_slot = nullptr;
+        uint32_t my_miss = 0;
+        if (lane < kMoveRows && r0 + lane < n) {
+            const uint64_t i = r0 + lane;
+            my_miss = is_load[i];
+            my_slot = region + uint64_t(alias[i]) * rb;
+            my_src = my_miss ? table + nodes[i] * rb : my_slot;
+        }
+        const char* src[kMoveRows];
+        char* slot[kMoveRows];
+        uint32_t miss[kMoveRows];
+#pragma unroll
+        for (int q = 0; q < kMoveRows; ++q) {
+            src[q] = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_src), q));
+            slot[q] = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_slot), q));
+            miss[q] = __shfl_sync(0xffffffffu, my_miss, q);
+        }
+        for (uint32_t c = lane; c < cpr; c += 32) {
+            uint4 v[kMoveRows];
+#pragma unroll
+            for (int q = 0; q < kMoveRows; ++q)
+                if (src[q] && (miss[q] || X))
+                    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                                 : "=r"(v[q].x), "=r"(v[q].y), "=r"(v[q].z), "=r"(v[q].w)
+                                 : "l"(reinterpret_cast<const uint4*>(src[q]) + c), "l"(pol));
+#pragma unroll
+            for (int q = 0; q < kMoveRows; ++q) {
+                if (!src[q] || !(miss[q] || X)) continue;
+                if (miss[q])
+                    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(
+                                     reinterpret_cast<uint4*>(slot[q]) + c),
+                                 "r"(v[q].x), "r"(v[q].y), "r"(v[q].z), "r"(v[q].w), "l"(pol)
+                                 : "memory");
+                if (X)
+                    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(
+                                     reinterpret_cast<uint4*>(X + (r0 + q) * rb) + c),
+                                 "r"(v[q].x), "r"(v[q].y), "r"(v[q].z), "r"(v[q].w), "l"(pol)
+                                 : "memory");
+            }
         }
     }
 }
 
 // ------------------------------------------------------------ k_release ----
-__global__ void __launch_bounds__(kT) k_release(BmDev B, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
-                                                uint32_t epoch) {
+// Slots come from the batch's alias list (ALIAS) or from the mapping entries of its
+// node ids (the public release_batch(nodes) form).
+template <bool ALIAS>
+__global__ void __launch_bounds__(kT) k_release(BmDev B, const uint64_t* nodes, const int64_t* alias,
+                                                const uint32_t* n_dev, uint64_t n_host, uint32_t epoch) {
     __shared__ uint32_t s_warp[kT / 32], s_misc[2], s_tile;
     BmState* S = B.st;
     if (S->status) return;
@@ -387,30 +420,36 @@ __global__ void __launch_bounds__(kT) k_release(BmDev B, const uint64_t* nodes, 
     uint32_t mask = 0, mine = 0;
     int32_t slots[kI];
     bool bad = false;
-    uint64_t nd[kI];
-    Entry en[kI];
+    int32_t sl[kI];
+    if constexpr (ALIAS) {
 #pragma unroll
-    for (int k = 0; k < kI; ++k) nd[k] = i0 + k < n ? nodes[i0 + k] : kNoNode;
+        for (int k = 0; k < kI; ++k) {
+            const int64_t a = i0 + k < n ? alias[i0 + k] : -1;
+            sl[k] = (a >= 0 && uint64_t(a) < B.S) ? int32_t(a) : -1;
+        }
+    } else {
+        uint64_t nd[kI];
 #pragma unroll
-    for (int k = 0; k < kI; ++k) en[k] = nd[k] < B.N ? B.map[nd[k]] : Entry{-1, 0u};  // all loads in flight
+        for (int k = 0; k < kI; ++k) nd[k] = i0 + k < n ? nodes[i0 + k] : kNoNode;
+#pragma unroll
+        for (int k = 0; k < kI; ++k) {  // all loads in flight
+            const Entry e = nd[k] < B.N ? B.map[nd[k]] : Entry{-1, 0u};
+            sl[k] = (e.refv & kValid) ? e.slot : -1;
+        }
+    }
+    uint32_t rf[kI];
+#pragma unroll
+    for (int k = 0; k < kI; ++k) rf[k] = sl[k] >= 0 ? B.ref[sl[k]] : 0u;
 #pragma unroll
     for (int k = 0; k < kI; ++k) {
-        uint64_t i = i0 + k;
-        if (i >= n) break;
-        uint64_t node = nd[k];
-        if (node >= B.N) {
+        if (i0 + k >= n) break;
+        if (sl[k] < 0 || rf[k] == 0) {  // not resident / no reference (buffer_manager.hpp:357, 462)
             bad = true;
             continue;
         }
-        Entry e = en[k];
-        uint32_t ref = e.refv & kRefMask;
-        if (!(e.refv & kValid) || ref == 0) {  // buffer_manager.hpp:357, 462
-            bad = true;
-            continue;
-        }
-        B.map[node].refv = e.refv - 1;
-        if (ref == 1) {
-            slots[k] = e.slot;
+        B.ref[sl[k]] = rf[k] - 1;
+        if (rf[k] == 1) {
+            slots[k] = sl[k];
             mask |= 1u << k;
             ++mine;
         }
@@ -504,6 +543,7 @@ __global__ void k_init(BmDev B) {
     for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < B.N; v += stride) B.map[v] = Entry{-1, 0u};
     for (uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; s < B.S; s += stride) {
         B.slot[s] = SlotMeta{kNoNode, s};
+        B.ref[s] = 0;
         B.ring[0][s] = int32_t(s);
     }
 }
@@ -524,6 +564,11 @@ struct Bm {
 }  // namespace fdg
 
 struct fdg_bm : fdg::Bm {};
+
+namespace fdg {
+int bm_release(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const int64_t* alias, const uint32_t* n_dev,
+               uint64_t n_host);
+}  // namespace fdg
 
 using namespace fdg;
 
@@ -555,6 +600,7 @@ int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint
     uint64_t sz = 0;
     const uint64_t o_map = sz; sz += al(N * 8);
     const uint64_t o_slot = sz; sz += al(slot_count * sizeof(SlotMeta));
+    const uint64_t o_ref = sz; sz += al(slot_count * 4);
     const uint64_t o_r0 = sz; sz += al(R * 4);
     const uint64_t o_r1 = sz; sz += al(R * 4);
     const uint64_t o_st = sz; sz += al(sizeof(BmState));
@@ -576,6 +622,7 @@ int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint
     BmDev& d = b->d;
     d.map = reinterpret_cast<Entry*>(a + o_map);
     d.slot = reinterpret_cast<SlotMeta*>(a + o_slot);
+    d.ref = reinterpret_cast<uint32_t*>(a + o_ref);
     d.ring[0] = reinterpret_cast<int32_t*>(a + o_r0);
     d.ring[1] = reinterpret_cast<int32_t*>(a + o_r1);
     d.R = R;
@@ -650,7 +697,7 @@ int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
     const char* table = static_cast<const char*>(b->ctx->shard_bases[0]);
     const uint64_t chunks = n_host * (rb / 16);
     const int blocks =
-        int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 511) / 512, uint64_t(b->ctx->sm_count) * 4)));
+        int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 511) / 512, uint64_t(b->ctx->sm_count) * 2)));
     {
         FDG_TRACE("bm_move", st);
         k_move<<<blocks, 512, 0, st>>>(d, nodes, n_dev, n_host, alias, d.is_load[parity & 1], table, b->region, rb,
@@ -675,13 +722,25 @@ int fdg_bm_extract(fdg_bm* b, void* stv, const uint64_t* nodes, const uint32_t* 
 }
 
 int fdg_bm_release(fdg_bm* b, void* stv, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host) {
-    cudaStream_t st = (cudaStream_t)stv;
+    return bm_release(b, (cudaStream_t)stv, nodes, nullptr, n_dev, n_host);
+}
+
+}  // extern "C"
+
+namespace fdg {
+// release_batch (buffer_manager.hpp:352-364) from the batch's node ids or -- when the
+// caller still holds it -- from its alias list (no mapping-table reads).
+int bm_release(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const int64_t* alias, const uint32_t* n_dev,
+               uint64_t n_host) {
     const BmDev& d = b->d;
     const uint64_t slack = 2 * uint64_t(b->max_batch) + kTileN;
     k_reset_ctrs<<<1, 32, 0, st>>>(d.st);
     {
         FDG_TRACE("bm_release", st);
-        k_release<<<n_tiles_for(n_host), kT, 0, st>>>(d, nodes, n_dev, n_host, b->epoch++);
+        if (alias)
+            k_release<true><<<n_tiles_for(n_host), kT, 0, st>>>(d, nodes, alias, n_dev, n_host, b->epoch++);
+        else
+            k_release<false><<<n_tiles_for(n_host), kT, 0, st>>>(d, nodes, alias, n_dev, n_host, b->epoch++);
     }
     {
         FDG_TRACE("bm_compact", st);
@@ -692,9 +751,6 @@ int fdg_bm_release(fdg_bm* b, void* stv, const uint64_t* nodes, const uint32_t* 
     return FDG_OK;
 }
 
-}  // extern "C"
-
-namespace fdg {
 // Copies a device-detected buffer-manager error into a batch record's status (stream-ordered).
 int bm_status_to(fdg_bm* b, cudaStream_t st, uint32_t* dst) {
     k_status_to<<<1, 1, 0, st>>>(b->d.st, dst);
@@ -734,7 +790,8 @@ int fdg_bm_entry(fdg_bm* b, uint64_t node, int64_t* slot, uint32_t* ref, uint32_
     Entry e;
     FDG_CUDA(cudaMemcpy(&e, b->d.map + node, sizeof(e), cudaMemcpyDeviceToHost));
     *slot = e.slot;
-    *ref = e.refv & kRefMask;
+    *ref = 0;
+    if (e.slot >= 0) FDG_CUDA(cudaMemcpy(ref, b->d.ref + e.slot, 4, cudaMemcpyDeviceToHost));
     *valid = e.refv >> 31;
     return FDG_OK;
 }
@@ -762,6 +819,8 @@ int fdg_bm_validate(fdg_bm* b) {
     if (h.status) return fail(int(h.status), "buffer manager in error state " + std::to_string(h.status));
     FDG_CUDA(cudaMemcpy(map.data(), d.map, d.N * 8, cudaMemcpyDeviceToHost));
     FDG_CUDA(cudaMemcpy(meta.data(), d.slot, d.S * sizeof(SlotMeta), cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> ref(d.S);
+    FDG_CUDA(cudaMemcpy(ref.data(), d.ref, d.S * 4, cudaMemcpyDeviceToHost));
     for (uint64_t s = 0; s < d.S; ++s) {
         rev[s] = meta[s].node;
         pos[s] = meta[s].pos;
@@ -784,12 +843,14 @@ int fdg_bm_validate(fdg_bm* b) {
         int32_t s = ring[p % d.R];
         if (pos[s] != p) continue;
         ++live;
-        if (rev[s] != kNoNode && (map[rev[s]].refv & kRefMask) != 0)
-            return fail(FDG_INVARIANT, "standby slot whose node still holds references");
+        if (ref[s] != 0) return fail(FDG_INVARIANT, "standby slot whose node still holds references");
     }
     if (live != h.live) return fail(FDG_INVARIANT, "standby size mismatch");
     for (uint64_t s = 0; s < d.S; ++s) {
-        if (rev[s] == kNoNode) continue;
+        if (rev[s] == kNoNode) {
+            if (ref[s] != 0) return fail(FDG_INVARIANT, "free slot with references");
+            continue;
+        }
         if (map[rev[s]].slot != int32_t(s)) return fail(FDG_INVARIANT, "reverse mapping points at node without matching slot");
     }
     return FDG_OK;

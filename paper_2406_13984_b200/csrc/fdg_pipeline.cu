@@ -39,6 +39,8 @@ int bm_extract_meta(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
                     int64_t* alias, uint32_t parity);
 int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                     const int64_t* alias, void* out, uint64_t* checksum, uint32_t parity);
+int bm_release(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const int64_t* alias, const uint32_t* n_dev,
+               uint64_t n_host);
 }  // namespace fdg
 
 struct fdg_pipeline {
@@ -423,8 +425,9 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                     const uint64_t pj = do_sample ? j - 1 : ((j - 1) % (sampled_groups * G));
                     // batch j-1's move reads its node list: the list is free once both are done
                     FDG_CUDA(cudaStreamWaitEvent(p->xstream, p->moved[par ^ 1], 0));
-                    FDG_TRY(fdg_bm_release(p->bm, p->xstream, p->nodes[pj % p->nslots], &p->counts[pj].n_nodes,
-                                           p->cap));
+                    // (batch j-1's alias list is alias[par ^ 1]: the release needs no mapping-table reads)
+                    FDG_TRY(bm_release(p->bm, p->xstream, p->nodes[pj % p->nslots], p->alias[par ^ 1],
+                                       &p->counts[pj].n_nodes, p->cap));
                     FDG_CUDA(cudaEventRecord(p->extracted[(j - 1) % p->nslots], p->xstream));
                 }
             }
@@ -437,7 +440,8 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
     if (p->bm && !sample_only) {  // drain: release the last batch
         const uint64_t lj = extract_only ? (n_batches - 1) % (sampled_groups * G) : n_batches - 1;
         FDG_CUDA(cudaStreamWaitEvent(p->xstream, p->moved[(n_batches - 1) & 1], 0));
-        FDG_TRY(fdg_bm_release(p->bm, p->xstream, p->nodes[lj % p->nslots], &p->counts[lj].n_nodes, p->cap));
+        FDG_TRY(bm_release(p->bm, p->xstream, p->nodes[lj % p->nslots], p->alias[(n_batches - 1) & 1],
+                           &p->counts[lj].n_nodes, p->cap));
         FDG_CUDA(cudaEventRecord(p->extracted[(n_batches - 1) % p->nslots], p->xstream));
     }
     for (uint32_t s = 0; s <= S; ++s) {  // join the sampler streams and the second extract stream
