@@ -463,6 +463,10 @@ int fdg_set_option(const char* key, int64_t v) {
         g_hash_kernel = v;
         return FDG_OK;
     }
+    if (k == "bm_overlap") {
+        g_bm_overlap = v != 0;
+        return FDG_OK;
+    }
     if (k == "sage_gemm") {
         if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, "sage_gemm must be 0 (CUDA cores) or 1 (tensor cores)");
         g_sage_gemm = v;
@@ -511,6 +515,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "hash_kernel") *v = g_hash_kernel;
     else if (k == "hash_chunk") *v = g_hash_chunk;
     else if (k == "sage_gemm") *v = g_sage_gemm;
+    else if (k == "bm_overlap") *v = g_bm_overlap;
     else if (k == "checksum_impl") *v = g_checksum_impl;
     else if (k == "ws_hashers") *v = g_ws_hashers;
     else if (k == "ws_stg") *v = g_ws_stg;

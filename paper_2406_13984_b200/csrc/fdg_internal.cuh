@@ -107,7 +107,8 @@ extern int g_gather_evict_first;
 extern int g_gather_ctas_per_sm;
 extern int64_t g_gather_dynamic;
 extern int64_t g_hash_kernel;
-extern int64_t g_sage_gemm;  // train-stage GEMMs: 1 tensor cores (3xTF32), 0 CUDA cores
+extern int64_t g_sage_gemm;
+extern int64_t g_bm_overlap;  // buffer-manager row move on its own stream (1) or after the metadata (0)  // train-stage GEMMs: 1 tensor cores (3xTF32), 0 CUDA cores
 extern int64_t g_hash_chunk;  // k_gather_hash_rb staging chunk (0 = by row size)
 extern int64_t g_checksum_impl;  // gather impl for the fused-checksum path (-1: same as g_gather_impl)
 extern int g_ws_hashers;

@@ -82,6 +82,8 @@ struct fdg_pipeline {
 
 using namespace fdg;
 
+int64_t fdg::g_bm_overlap = 1;
+
 namespace {
 
 void destroy(fdg_pipeline* p) {
@@ -381,7 +383,7 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
             fdg_batch_counts* cnt = p->counts + src_j;
             // the train stage shares one model workspace: with a model the plain gathers stay on one stream
             cudaStream_t xs = (!p->bm && !train && p->xstream2 && (j & 1)) ? p->xstream2 : p->xstream;
-            cudaStream_t xe = p->bm ? p->xstream2 : xs;  // stream on which the batch's extraction ends
+            cudaStream_t xe = (p->bm && g_bm_overlap) ? p->xstream2 : xs;  // stream on which the batch's extraction ends
             if (sample_only) {
                 FDG_CUDA(cudaEventRecord(p->extracted[slot], xs));
                 continue;

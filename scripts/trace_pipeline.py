@@ -1,6 +1,7 @@
 """Timeline of the pipelined run (fdg_trace): per-kernel mean duration in situ, extract-stream
 idle gaps and per-batch sampler chain latency."""
 import csv
+import os
 import ctypes as C
 import sys
 from collections import defaultdict
@@ -20,6 +21,8 @@ L = fd.featdrive.lib()
 L.fdg_trace_enable.argtypes = [C.c_int]
 L.fdg_trace_dump.argtypes = [C.c_char_p]
 L.fdg_set_gather_impl(impl)
+if os.environ.get("BM_OVERLAP"):
+    fd.featdrive.check(L.fdg_set_option(b"bm_overlap", int(os.environ["BM_OVERLAP"])))
 topo = fd.Topology.generate(n, dim, avg, 7, dtype=dtype)
 order = np.concatenate(fd.partition_epoch(np.arange(t_ids, dtype=np.uint64), B, bench.hash_combine(0, 0)))
 K = 200
