@@ -129,7 +129,7 @@ int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers
     auto p = new fdg_pipeline();
     p->ctx = ctx;
     p->cfg = *cfg;
-    if (p->cfg.n_samplers == 0) p->cfg.n_samplers = 6;  // measured best on B200 (5-8 plateau)
+    if (p->cfg.n_samplers == 0) p->cfg.n_samplers = 8;  // measured on B200: Papers flat at 6-10, products best from 8
     if (p->cfg.prefetch_group == 0) p->cfg.prefetch_group = 16;
     if (p->cfg.group_batches == 0) p->cfg.group_batches = 1;
     p->cfg.group_batches = std::min<uint32_t>(p->cfg.group_batches, 8);
