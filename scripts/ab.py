@@ -19,7 +19,8 @@ topo = fd.Topology.generate(n, dim, avg, 7, dtype=dtype)
 order = np.concatenate(fd.partition_epoch(np.arange(t_ids, dtype=np.uint64), B, bench.hash_combine(0, 0)))
 K = int(os.environ.get("K", "300"))
 rng = np.array([L.fdg_batch_seed(0, 0, int(g)) for g in range(K)], np.uint64)
-seeds = DeviceBuffer.from_array(np.ascontiguousarray(order[:K * B]))
+nb_epoch = len(order) // B  # wrap at the epoch end (products has 196 batches)
+seeds = DeviceBuffer.from_array(np.ascontiguousarray(np.concatenate([order[(b % nb_epoch) * B:(b % nb_epoch + 1) * B] for b in range(K)])))
 f = np.ascontiguousarray(fan, np.uint32)
 defaults = {"gather_impl": 1, "gather_evict_first": 0, "l2_persist_mb": 0, "hash_load_pct": 50,
             "hash_clear": 1, "sampler_ctas_per_sm": 16, "gather_ctas_per_sm": 1,

@@ -27,7 +27,8 @@ topo = fd.Topology.generate(n, dim, avg, 7, dtype=dtype)
 order = np.concatenate(fd.partition_epoch(np.arange(t_ids, dtype=np.uint64), B, bench.hash_combine(0, 0)))
 K = 200
 rng = np.array([L.fdg_batch_seed(0, 0, int(g)) for g in range(K)], np.uint64)
-seeds = DeviceBuffer.from_array(np.ascontiguousarray(order[:K * B]))
+nb_epoch = len(order) // B  # wrap at the epoch end (products has 196 batches)
+seeds = DeviceBuffer.from_array(np.ascontiguousarray(np.concatenate([order[(b % nb_epoch) * B:(b % nb_epoch + 1) * B] for b in range(K)])))
 import os
 bm_slots = int(os.environ.get("BM", "0"))
 cfg = _lib.PipelineConfig(batch_size=B, n_samplers=S, prefetch_group=16, write_x=1,
