@@ -317,6 +317,10 @@ int fdg_sage_buffers(fdg_sage* m, float** params_dev, float** grads_dev, uint64_
  * atomics over the dst-sorted blocks, weight gradients as row-sliced A^T . dOut. */
 int fdg_sage_backward(fdg_sage* m, void* stream, const uint64_t* nodes_dev, const uint32_t* edges_dev,
                       const fdg_batch_counts* counts_dev, uint64_t label_seed);
+/* Test hook: out_dev [Kin x N] = A^T . B (+ the column sums of B appended, [N]) for device
+ * A [R x Kin], B [R x N], through the backward's weight-gradient engine in Z row slices. */
+int fdg_sage_wgrad_test(const float* A_dev, const float* B_dev, uint32_t R, uint32_t Kin, uint32_t N, uint32_t Z,
+                        float* out_dev);
 /* SGD step params -= lr * grads (stream-ordered), refreshing the kernels' weight layouts. */
 int fdg_sage_sgd(fdg_sage* m, void* stream, float lr);
 /* Run the model after each batch's extraction inside fdg_pipeline_run (NULL = off; the

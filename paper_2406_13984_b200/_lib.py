@@ -126,6 +126,7 @@ SIGNATURES = {
     "fdg_sage_buffers": (ci, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(u64)]),
     "fdg_sage_backward": (ci, [vp, vp, vp, vp, vp, u64]),
     "fdg_sage_sgd": (ci, [vp, vp, C.c_float]),
+    "fdg_sage_wgrad_test": (ci, [vp, vp, u32, u32, u32, u32, vp]),
     "fdg_pipeline_set_model": (ci, [vp, vp, u64]),
     "fdg_pipeline_set_training": (ci, [vp, C.c_float]),
     "fdg_pipeline_losses": (ci, [vp, u64, u64, vp]),

@@ -43,6 +43,9 @@ int tc_make_map(CUtensorMap* map, const float* base, uint64_t rows, uint32_t K);
 int tc_gemm(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tBhi, const CUtensorMap& tBlo,
             const float* bias, float* C, const fdg_batch_counts* cnt, int j, uint64_t rows_bound, int N, int npad,
             int K, bool relu);
+int tc_make_map_mn(CUtensorMap* map, const float* base, uint64_t rows, uint32_t cols);
+int tc_wgrad(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tB, float* P, const fdg_batch_counts* cnt,
+             int j, int Kin, int N, int Z);
 // 1: layer GEMMs on the tensor cores (tcgen05 kind::tf32, 3xTF32 fp32-accurate); 0: CUDA-core fp32
 int64_t g_sage_gemm = 1;
 
@@ -379,6 +382,40 @@ __global__ void __launch_bounds__(256) k_gemm_tn(const float* __restrict__ A, co
             if (n0 + tx * 4 + c < N) Pb[size_t(z) * N + n0 + tx * 4 + c] = bs[c];
 }
 
+// Bias gradient slices for the tensor-core weight gradient: Pb[z][c] = sum of column c of
+// B over row slice z (the k_wgrad_tc slicing: ceil(ceil(R / 32) / Z) 32-row blocks). A CTA
+// is 32 columns x 8 row lanes; the 8 partial sums meet in a fixed order.
+__global__ void __launch_bounds__(256) k_colsum(const float* __restrict__ B, const fdg_batch_counts* cnt, int j, int N,
+                                                float* Pb) {
+    __shared__ float part[8][33];
+    const int R = int(d_rows(cnt, j));
+    const int Z = int(gridDim.y), z = int(blockIdx.y);
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int c = blockIdx.x * 32 + tx;
+    const int nkb = (R + 31) / 32, per = ((nkb + Z - 1) / Z) * 32;
+    const int r0 = min(R, z * per), r1 = min(R, r0 + per);
+    float sum = 0.f;
+    if (c < N) {
+        int r = r0 + ty;
+        for (; r + 24 < r1; r += 32) {  // 4 rows in flight per thread
+            const float a = B[size_t(r) * N + c], b = B[size_t(r + 8) * N + c];
+            const float d = B[size_t(r + 16) * N + c], e = B[size_t(r + 24) * N + c];
+            sum += a;
+            sum += b;
+            sum += d;
+            sum += e;
+        }
+        for (; r < r1; r += 8) sum += B[size_t(r) * N + c];
+    }
+    part[ty][tx] = sum;
+    __syncthreads();
+    if (ty == 0 && c < N) {
+        float t = 0.f;
+        for (int q = 0; q < 8; ++q) t += part[q][tx];
+        Pb[size_t(z) * N + c] = t;
+    }
+}
+
 // G[0 : K N] = sum_z P[z], G[K N : K N + N] = sum_z Pb[z] (slices added in order).
 __global__ void k_tn_sum(const float* __restrict__ P, const float* __restrict__ Pb, int Z, int KN, int N,
                          float* __restrict__ G) {
@@ -436,7 +473,8 @@ __global__ void k_sgd(float* __restrict__ P, const float* __restrict__ G, uint64
 // Wpad [K x npad] (CUDA-core GEMM), bpad [npad], Wt [dout x npadT] (backward dA GEMM),
 // and the tensor cores' transposed K-major hi / lo split [npad x K].
 __global__ void k_derive(const float* __restrict__ Wm, const float* __restrict__ bm, int K, int dout, int npad,
-                         int npadT, float* Wpad, float* bpad, float* Wt, float* Whi, float* Wlo) {
+                         int npadT, float* Wpad, float* bpad, float* Wt, float* Whi, float* Wlo, float* Wdhi,
+                         float* Wdlo) {
     const int stride = gridDim.x * blockDim.x, t0 = blockIdx.x * blockDim.x + threadIdx.x;
     for (int i = t0; i < K * npad; i += stride) {
         const int k = i / npad, n = i - k * npad;
@@ -453,6 +491,12 @@ __global__ void k_derive(const float* __restrict__ Wm, const float* __restrict__
         Wt[i] = k < K ? Wm[size_t(k) * dout + n] : 0.f;
     }
     for (int i = t0; i < npad; i += stride) bpad[i] = i < dout ? bm[i] : 0.f;
+    if (Wdhi)  // backward dA = dOut . W^T on the tensor cores: B operand [K x dout], K-major (Wm's own layout)
+        for (int i = t0; i < K * dout; i += stride) {
+            const float v = Wm[i], h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+            Wdhi[i] = h;
+            Wdlo[i] = v - h;
+        }
 }
 
 }  // namespace
@@ -489,6 +533,13 @@ struct Sage {
     uint64_t tn_floats = 0;
     std::vector<uint8_t> set;
     bool forwarded = false;
+    // tensor-core weight gradients: MN-major maps of each layer's saved input and output gradient
+    std::vector<CUtensorMap> mapAmn, mapDmn;
+    // tensor-core input gradients dA = dOut . W^T: K-major maps of dOut and of W's hi / lo split
+    std::vector<float*> Wdhi, Wdlo;
+    std::vector<CUtensorMap> mapDk, mapWdhi, mapWdlo;
+    std::vector<uint8_t> tc_da;
+    std::vector<int> wz;            // split-K slices per layer (0: CUDA-core k_gemm_tn)
 };
 
 }  // namespace fdg
@@ -506,7 +557,8 @@ int derive_layer(fdg_sage* m, uint32_t l, cudaStream_t st) {
     const int n = int(std::max<uint64_t>(uint64_t(K) * m->npad[l], uint64_t(dout) * m->npadT[l]));
     k_derive<<<std::min(1024, (n + 255) / 256), 256, 0, st>>>(m->P + m->off[l], m->P + m->off[l] + uint64_t(K) * dout,
                                                              int(K), int(dout), int(m->npad[l]), int(m->npadT[l]),
-                                                             m->W[l], m->b[l], m->Wt[l], m->Whi[l], m->Wlo[l]);
+                                                             m->W[l], m->b[l], m->Wt[l], m->Whi[l], m->Wlo[l],
+                                                             m->Wdhi[l], m->Wdlo[l]);
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;
 }
@@ -551,6 +603,10 @@ int fdg_sage_create(fdg_ctx* ctx, const uint32_t* dims, uint32_t n_layers, const
         dmax = std::max<uint64_t>(dmax, m->bound[n_layers - l] * dims[l]);  // its input gradient
         amax = std::max<uint64_t>(amax, rows * 2 * dims[l]);
         m->tn_floats = std::max<uint64_t>(m->tn_floats, uint64_t(tn_slices(rows)) * (2 * dims[l] + 1) * dims[l + 1]);
+        const uint64_t tiles = uint64_t((2 * dims[l] + 127) / 128) * ((dims[l + 1] + 127) / 128);
+        const uint64_t z = std::min<uint64_t>((2 * uint64_t(ctx->sm_count) + tiles - 1) / tiles, (rows + 31) / 32);
+        m->wz.push_back(int(std::max<uint64_t>(z, 1)));
+        m->tn_floats = std::max<uint64_t>(m->tn_floats, uint64_t(m->wz.back()) * (2 * dims[l] + 1) * dims[l + 1]);
     }
     cudaError_t e = al((void**)&m->seg, m->bound[n_layers - 1] * sizeof(uint2));
     if (e == cudaSuccess) e = al((void**)&m->P, m->n_params * 4);
@@ -603,6 +659,34 @@ int fdg_sage_create(fdg_ctx* ctx, const uint32_t* dims, uint32_t n_layers, const
             tc_make_map(&m->mapBlo[l], m->Wlo[l], np, K) == FDG_OK)
             m->tc_ok[l] = 1;
     }
+    m->Wdhi.assign(n_layers, nullptr);
+    m->Wdlo.assign(n_layers, nullptr);
+    m->mapDk.resize(n_layers);
+    m->mapWdhi.resize(n_layers);
+    m->mapWdlo.resize(n_layers);
+    m->tc_da.assign(n_layers, 0);
+    for (uint32_t l = 1; l < n_layers && e == cudaSuccess; ++l) {  // layer 0 needs no input gradient
+        const uint64_t rows = m->bound[n_layers - 1 - l];
+        const uint32_t K2 = 2 * dims[l];
+        e = al((void**)&m->Wdhi[l], uint64_t(K2) * dims[l + 1] * 4);
+        if (e == cudaSuccess) e = al((void**)&m->Wdlo[l], uint64_t(K2) * dims[l + 1] * 4);
+        if (e != cudaSuccess) break;
+        if (tc_make_map(&m->mapDk[l], m->dbuf[(n_layers - 1 - l) % 2], rows, dims[l + 1]) == FDG_OK &&
+            tc_make_map(&m->mapWdhi[l], m->Wdhi[l], K2, dims[l + 1]) == FDG_OK &&
+            tc_make_map(&m->mapWdlo[l], m->Wdlo[l], K2, dims[l + 1]) == FDG_OK)
+            m->tc_da[l] = 1;
+    }
+    m->mapAmn.resize(n_layers);
+    m->mapDmn.resize(n_layers);
+    for (uint32_t l = 0; l < n_layers && e == cudaSuccess; ++l) {
+        const uint64_t rows = m->bound[n_layers - 1 - l];
+        // the backward's output gradient of layer l+1 sits in dbuf[(L-1-l) % 2] (k_loss_grad
+        // writes dbuf[0] for the top layer, each layer's input gradient the other buffer)
+        float* dout_buf = m->dbuf[(n_layers - 1 - l) % 2];
+        if (tc_make_map_mn(&m->mapAmn[l], m->Al[l], rows, 2 * dims[l]) != FDG_OK ||
+            tc_make_map_mn(&m->mapDmn[l], dout_buf, rows, dims[l + 1]) != FDG_OK)
+            m->wz[l] = 0;
+    }
     if (e != cudaSuccess) {
         fdg_sage_destroy(m);
         return cuda_fail(e, "fdg_sage_create", __FILE__, __LINE__);
@@ -618,7 +702,7 @@ int fdg_sage_destroy(fdg_sage* m) {
                     (void*)m->row_loss, (void*)m->dbuf[0], (void*)m->dbuf[1], (void*)m->dA, (void*)m->zeros,
                     (void*)m->tn_part})
         cudaFree(p);
-    for (auto* v : {&m->W, &m->b, &m->Wt, &m->Whi, &m->Wlo, &m->Al, &m->Hl})
+    for (auto* v : {&m->W, &m->b, &m->Wt, &m->Whi, &m->Wlo, &m->Al, &m->Hl, &m->Wdhi, &m->Wdlo})
         for (float* p : *v) cudaFree(p);
     delete m;
     return FDG_OK;
@@ -745,18 +829,29 @@ int fdg_sage_backward(fdg_sage* m, void* stv, const uint64_t* nodes_dev, const u
             k_relu_mask<<<uint32_t(std::min<uint64_t>((rows * dout + 255) / 256, uint64_t(c.sm_count) * 8)), 256, 0,
                           st>>>(cur, m->Hl[k - 1], counts_dev, j, int(dout));
         // weight + bias gradients: A^T . dOut over the D_j rows, in row slices
-        const int Z = tn_slices(rows);
-        dim3 grid((dout + kTn - 1) / kTn, (K + kTn - 1) / kTn, uint32_t(Z));
+        const bool tc = g_sage_gemm == 1 && m->wz[k - 1] > 0;
+        const int Z = tc ? m->wz[k - 1] : tn_slices(rows);
         float* Pb = m->tn_part + uint64_t(Z) * K * dout;
-        k_gemm_tn<<<grid, 256, 0, st>>>(m->Al[k - 1], cur, counts_dev, j, int(K), int(dout), m->tn_part, Pb);
+        if (tc) {
+            FDG_TRY(tc_wgrad(st, m->mapAmn[k - 1], m->mapDmn[k - 1], m->tn_part, counts_dev, j, int(K), int(dout), Z));
+            k_colsum<<<dim3((dout + 31) / 32, uint32_t(Z)), 256, 0, st>>>(cur, counts_dev, j, int(dout), Pb);
+        } else {
+            dim3 grid((dout + kTn - 1) / kTn, (K + kTn - 1) / kTn, uint32_t(Z));
+            k_gemm_tn<<<grid, 256, 0, st>>>(m->Al[k - 1], cur, counts_dev, j, int(K), int(dout), m->tn_part, Pb);
+        }
         const int kn = int(K * dout);
         k_tn_sum<<<std::min(1024, (kn + int(dout) + 255) / 256), 256, 0, st>>>(m->tn_part, Pb, Z, kn, int(dout),
                                                                               m->G + m->off[k - 1]);
         if (k == 1) break;
         // input gradient: dA = dOut . [W_neigh; W_self]^T, then scatter to h^{k-1}
-        dim3 ag(m->npadT[k - 1] / kBN, uint32_t((rows + kBM - 1) / kBM), 1);
-        k_sgemm<false><<<ag, 256, 0, st>>>(cur, m->Wt[k - 1], m->zeros, m->dA, counts_dev, j, int(K), int(dout),
-                                           int(m->npadT[k - 1]), 0);
+        if (g_sage_gemm == 1 && m->tc_da[k - 1]) {
+            FDG_TRY(tc_gemm(st, m->mapDk[k - 1], m->mapWdhi[k - 1], m->mapWdlo[k - 1], m->zeros, m->dA, counts_dev,
+                            j, rows, int(K), int(m->npadT[k - 1]), int(dout), false));
+        } else {
+            dim3 ag(m->npadT[k - 1] / kBN, uint32_t((rows + kBM - 1) / kBM), 1);
+            k_sgemm<false><<<ag, 256, 0, st>>>(cur, m->Wt[k - 1], m->zeros, m->dA, counts_dev, j, int(K), int(dout),
+                                               int(m->npadT[k - 1]), 0);
+        }
         float* nxt = cur == m->dbuf[0] ? m->dbuf[1] : m->dbuf[0];
         const uint64_t in_rows = m->bound[j + 1];
         k_dh_self<<<uint32_t(std::min<uint64_t>((in_rows * din / 4 + 255) / 256, uint64_t(c.sm_count) * 8)), 256, 0,
@@ -780,4 +875,37 @@ int fdg_sage_sgd(fdg_sage* m, void* stv, float lr) {
     return FDG_OK;
 }
 
+}  // extern "C"
+
+extern "C" {
+// Test hook: out[Kin x N] = A^T . B for device A [R x Kin], B [R x N] through the backward's
+// weight-gradient engine (option "sage_gemm": tensor cores or CUDA cores), split into Z slices.
+int fdg_sage_wgrad_test(const float* A, const float* B, uint32_t R, uint32_t Kin, uint32_t N, uint32_t Z, float* out) {
+    fdg_batch_counts h{};
+    h.n_nodes = R;
+    h.layer_nodes[1] = R;
+    fdg_batch_counts* cnt = nullptr;
+    float* part = nullptr;
+    FDG_CUDA(cudaMalloc(&cnt, sizeof(h)));
+    FDG_CUDA(cudaMemcpy(cnt, &h, sizeof(h), cudaMemcpyHostToDevice));
+    FDG_CUDA(cudaMalloc(&part, (uint64_t(Z) * (Kin + 1) * N) * 4));
+    int rc = FDG_OK;
+    if (g_sage_gemm == 1) {
+        CUtensorMap ma, mb;
+        rc = tc_make_map_mn(&ma, A, R, Kin);
+        if (rc == FDG_OK) rc = tc_make_map_mn(&mb, B, R, N);
+        if (rc == FDG_OK) rc = tc_wgrad(nullptr, ma, mb, part, cnt, 0, int(Kin), int(N), int(Z));
+    } else {
+        dim3 grid((N + kTn - 1) / kTn, (Kin + kTn - 1) / kTn, Z);
+        k_gemm_tn<<<grid, 256>>>(A, B, cnt, 0, int(Kin), int(N), part, part + uint64_t(Z) * Kin * N);
+    }
+    if (rc == FDG_OK) {
+        k_colsum<<<dim3((N + 31) / 32, Z), 256>>>(B, cnt, 0, int(N), part + uint64_t(Z) * Kin * N);
+        k_tn_sum<<<256, 256>>>(part, part + uint64_t(Z) * Kin * N, int(Z), int(Kin * N), int(N), out);
+        if (cudaDeviceSynchronize() != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "wgrad_test", __FILE__, __LINE__);
+    }
+    cudaFree(cnt);
+    cudaFree(part);
+    return rc;
+}
 }  // extern "C"

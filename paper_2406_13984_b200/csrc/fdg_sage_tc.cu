@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    const int nk = K / kTcBK;
+    const int nk = (K + kTcBK - 1) / kTcBK;  // a ragged last block is zero-filled by TMA (out of bounds)
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
@@ -262,6 +262,207 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------------------------
+// Weight gradient of the backward pass, dW[Kin x N] = A^T . dOut over the R = D_j rows
+// (A = the layer's saved input [R x Kin], dOut [R x N], both row-major), on the tensor
+// cores with both operands MN-major: a 32-row block of A is 4 TMA boxes of 32 rows x
+// 32 features (128-byte rows, 32-byte swizzle atoms), the MN-major SW128_BASE32B layout
+// with LBO = 4 KB between 32-feature blocks and SBO = 512 B between 4-row groups; each
+// UMMA (K = 8 rows) starts 1 KB further. Both operands are activations, so the split warps
+// split both (hi in place, lo beside) and zero rows past R (stale rows of the buffers).
+// Split-K over R: work item = (row slice z, output tile); slices write partial tiles
+// P[z] that a fixed-order sum adds (k_tn_sum), so the result is deterministic.
+// MN-major tf32 operands only support the "128B swizzle, 32B atom" layout (layout type 1,
+// SWIZZLE_128B_BASE32B): 128-byte rows whose four 32-byte chunks are XOR-permuted by
+// (row % 4) -- TMA's CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B. K groups are 4 rows (SBO = 512 B),
+// 32-feature blocks are the 4 KB TMA boxes (LBO).
+__device__ __forceinline__ uint64_t umma_desc_mn(uint32_t saddr) {
+    return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(4096 >> 4) << 16) | (uint64_t(512 >> 4) << 32) |
+           (1ull << 46) | (1ull << 61);
+}
+
+__device__ __forceinline__ void split_tile(uint8_t* hi_t, uint8_t* lo_t, int t4, int row0, int R) {
+    float4* hi = reinterpret_cast<float4*>(hi_t);
+    float4* lo = reinterpret_cast<float4*>(lo_t);
+#pragma unroll 4
+    for (int i = t4; i < kTcTile / 16; i += 128) {
+        const int row = row0 + ((i * 16) & 4095) / 128;  // 4 KB boxes of 32 rows x 128 B
+        float4 v = hi[i];
+        if (row >= R) v = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 h;
+        h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+        h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+        h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+        h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+        hi[i] = h;
+        lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+    }
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_wgrad_tc(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, float* __restrict__ P,
+               const fdg_batch_counts* cnt, int j, int Kin, int N, int m_tiles, int n_tiles, int Z) {
+    extern __shared__ uint8_t tc_raw[];
+    const int R = int(d_rows_tc(cnt, j));
+    const int tiles = m_tiles * n_tiles, items = tiles * Z;
+    const int nkb = (R + kTcBK - 1) / kTcBK, per = (nkb + Z - 1) / Z;
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + kTcStages * kTcStageBytes);
+    uint64_t* conv = full + kTcStages;
+    uint64_t* empty = conv + kTcStages;
+    uint64_t* tmem_full = empty + kTcStages;  // [2]
+    uint64_t* tmem_empty = tmem_full + 2;     // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto a_hi = [&](int s) { return sm + s * kTcStageBytes; };
+    auto a_lo = [&](int s) { return sm + s * kTcStageBytes + kTcTile; };
+    auto b_hi = [&](int s) { return sm + s * kTcStageBytes + 2 * kTcTile; };
+    auto b_lo = [&](int s) { return sm + s * kTcStageBytes + 3 * kTcTile; };
+    auto kb_range = [&](int z, int& k0, int& k1) {
+        k0 = min(nkb, z * per);
+        k1 = min(nkb, k0 + per);
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(conv + s, 128);
+            mbar_init(empty + s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tmem_full + a, 1);
+            mbar_init(tmem_empty + a, 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tmem_slot)), "n"(256)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer: 4 boxes of A and 4 of B per 32-row block
+            int it = 0;
+            for (int t = blockIdx.x; t < items; t += gridDim.x) {
+                const int tile = t % tiles, z = t / tiles;
+                const int m0 = (tile / n_tiles) * kTcBM, n0 = (tile % n_tiles) * kTcBN;
+                int k0, k1;
+                kb_range(z, k0, k1);
+                for (int kb = k0; kb < k1; ++kb, ++it) {
+                    const int s = it % kTcStages;
+                    if (it >= kTcStages) mbar_wait(empty + s, uint32_t((it / kTcStages - 1) & 1));
+                    mbar_expect_tx(full + s, 2 * kTcTile);
+                    for (int q = 0; q < 4; ++q) {
+                        tma_load_2d(a_hi(s) + q * 4096, &tA, full + s, m0 + 32 * q, kb * kTcBK);
+                        tma_load_2d(b_hi(s) + q * 4096, &tB, full + s, n0 + 32 * q, kb * kTcBK);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer (A and B MN-major)
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
+                                   (uint32_t(kTcBN >> 3) << 17) | (uint32_t(kTcBM >> 4) << 24);
+            int it = 0, ti = 0;
+            for (int t = blockIdx.x; t < items; t += gridDim.x, ++ti) {
+                const int acc = ti & 1;
+                int k0, k1;
+                kb_range(t / tiles, k0, k1);
+                if (ti >= 2) mbar_wait(tmem_empty + acc, uint32_t((ti / 2 - 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t d = tmem + uint32_t(acc * kTcBN);
+                for (int kb = k0; kb < k1; ++kb, ++it) {
+                    const int s = it % kTcStages;
+                    mbar_wait(conv + s, uint32_t((it / kTcStages) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                    for (int k = 0; k < kTcBK / 8; ++k) {  // 8 rows per UMMA: the next 1 KB row group
+                        const uint64_t dah = umma_desc_mn(sa(a_hi(s)) + k * 1024),
+                                       dal = umma_desc_mn(sa(a_lo(s)) + k * 1024);
+                        const uint64_t dbh = umma_desc_mn(sa(b_hi(s)) + k * 1024),
+                                       dbl = umma_desc_mn(sa(b_lo(s)) + k * 1024);
+                        umma_tf32(d, dah, dbh, idesc, (kb > k0 || k) ? 1u : 0u);
+                        umma_tf32(d, dah, dbl, idesc, 1u);
+                        umma_tf32(d, dal, dbh, idesc, 1u);
+                    }
+                    umma_commit(empty + s);
+                }
+                umma_commit(tmem_full + acc);  // (an empty slice commits at once: its epilogue writes zeros)
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        const int t4 = threadIdx.x - 128;
+        int it = 0;
+        for (int t = blockIdx.x; t < items; t += gridDim.x) {
+            int k0, k1;
+            kb_range(t / tiles, k0, k1);
+            for (int kb = k0; kb < k1; ++kb, ++it) {
+                const int s = it % kTcStages;
+                mbar_wait(full + s, uint32_t((it / kTcStages) & 1));
+                split_tile(a_hi(s), a_lo(s), t4, kb * kTcBK, R);
+                split_tile(b_hi(s), b_lo(s), t4, kb * kTcBK, R);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(conv + s);
+            }
+        }
+    } else if (warp >= 8) {
+        const int wq = warp & 3;
+        int ti = 0;
+        for (int t = blockIdx.x; t < items; t += gridDim.x, ++ti) {
+            const int acc = ti & 1;
+            const int tile = t % tiles, z = t / tiles;
+            const int m0 = (tile / n_tiles) * kTcBM, n0 = (tile % n_tiles) * kTcBN;
+            int k0, k1;
+            kb_range(z, k0, k1);
+            mbar_wait(tmem_full + acc, uint32_t((ti / 2) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int row = m0 + wq * 32 + lane;  // input feature
+            float* Pz = P + size_t(z) * Kin * N;
+            for (int c0 = 0; c0 < kTcBN; c0 += 32) {
+                uint32_t r[32];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(tmem + (uint32_t(wq * 32) << 16) + uint32_t(acc * kTcBN + c0)));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c0 + 32 == kTcBN) {
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    mbar_arrive(tmem_empty + acc);
+                }
+                if (row < Kin) {
+                    const bool empty_slice = k1 <= k0;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int col = n0 + c0 + q * 4;
+                        if (col >= N) break;
+                        const float4 v = empty_slice ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                                     : make_float4(__uint_as_float(r[q * 4 + 0]),
+                                                                   __uint_as_float(r[q * 4 + 1]),
+                                                                   __uint_as_float(r[q * 4 + 2]),
+                                                                   __uint_as_float(r[q * 4 + 3]));
+                        *reinterpret_cast<float4*>(Pz + size_t(row) * N + col) = v;
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 2) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256) : "memory");
+    }
+}
+
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -295,6 +496,42 @@ int tc_make_map(CUtensorMap* map, const float* base, uint64_t rows, uint32_t K) 
     return FDG_OK;
 }
 
+// fp32 row-major [rows x cols] as a TMA map with 32 (cols) x 32 (rows) boxes, 128-byte rows
+// swizzled in 32-byte atoms: the MN-major operand blocks of k_wgrad_tc.
+int tc_make_map_mn(CUtensorMap* map, const float* base, uint64_t rows, uint32_t cols) {
+    EncodeTiled enc = encode_fn();
+    if (!enc) return fail(FDG_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {cols, std::max<uint64_t>(rows, 1)};
+    const cuuint64_t strides[1] = {uint64_t(cols) * 4};
+    const cuuint32_t box[2] = {32, uint32_t(kTcBK)};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FDG_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return FDG_OK;
+}
+
+int tc_wgrad(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tB, float* P, const fdg_batch_counts* cnt,
+             int j, int Kin, int N, int Z) {
+    static bool attr = false;
+    if (!attr) {
+        FDG_CUDA(cudaFuncSetAttribute(k_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+        attr = true;
+    }
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int m_tiles = (Kin + kTcBM - 1) / kTcBM, n_tiles = (N + kTcBN - 1) / kTcBN;
+    const int items = m_tiles * n_tiles * Z;
+    k_wgrad_tc<<<std::min(items, sms), kTcThreads, kTcSmem, st>>>(tA, tB, P, cnt, j, Kin, N, m_tiles, n_tiles, Z);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
 int tc_gemm(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tBhi, const CUtensorMap& tBlo,
             const float* bias, float* C, const fdg_batch_counts* cnt, int j, uint64_t rows_bound, int N, int npad,
             int K, bool relu) {
@@ -304,7 +541,7 @@ int tc_gemm(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tBhi, con
         FDG_CUDA(cudaFuncSetAttribute(k_sgemm_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
         attr = true;
     }
-    if (K % kTcBK) return fail(FDG_INVALID_ARG, "tc_gemm: K must be a multiple of 32");
+    if (K % 4) return fail(FDG_INVALID_ARG, "tc_gemm: K must be a multiple of 4 (16-byte row stride)");
     static int sms = 0;
     if (!sms) {
         int dev = 0;

@@ -207,3 +207,22 @@ def test_pipeline_training_matches_host_loop(fd):
     for i in range(2):
         for u, v in zip(a.layer(i), b.layer(i)):
             np.testing.assert_allclose(u, v, rtol=1e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("R,Kin,N,Z", [(64, 128, 128, 1), (1000, 256, 256, 4), (777, 512, 172, 5), (33, 64, 12, 3),
+                                       (5000, 24, 8, 7)])
+def test_weight_gradient_engines(fd, gemm, R, Kin, N, Z):
+    """A^T . B (+ column sums of B) through the backward's weight-gradient engines: the
+    tcgen05 MN-major split-K kernel (128B / 32B-atom swizzle) and the CUDA-core one, with
+    ragged rows / columns and empty row slices, against fp64."""
+    from paper_2406_13984_b200.featdrive import DeviceBuffer, check, lib
+    rs = np.random.RandomState(R + Kin)
+    A = rs.standard_normal((R, Kin)).astype(np.float32)
+    B = rs.standard_normal((R, N)).astype(np.float32)
+    da, db, out = DeviceBuffer.from_array(A), DeviceBuffer.from_array(B), DeviceBuffer((Kin + 1) * N * 4)
+    check(lib().fdg_sage_wgrad_test(da.ptr, db.ptr, R, Kin, N, Z, out.ptr))
+    got = out.download(np.float32, (Kin + 1) * N)
+    want = A.astype(np.float64).T @ B.astype(np.float64)
+    scale = np.abs(want).max()
+    np.testing.assert_allclose(got[:Kin * N].reshape(Kin, N), want, rtol=1e-5, atol=1e-5 * scale)
+    np.testing.assert_allclose(got[Kin * N:], B.astype(np.float64).sum(0), rtol=1e-5, atol=1e-4)
