@@ -194,6 +194,7 @@ int fdg_gather(fdg_ctx* ctx, void* stream, const uint64_t* nodes_dev, const uint
 #define FDG_GATHER_TMA 0
 #define FDG_GATHER_LDG 1
 #define FDG_GATHER_TMA_WS 2 /* warp-specialised TMA: producer warp + consumer (hashing) warps */
+#define FDG_GATHER_RB 3     /* 32-row groups, 256-byte chunks (the fused-checksum kernel's structure) */
 int fdg_set_gather_impl(int impl);
 /* Tuning knobs (process-wide): "gather_impl" (FDG_GATHER_*), "gather_evict_first"
  * (0/1: L2 evict-first hints on the gather stream), "l2_persist_mb" (L2 set-aside

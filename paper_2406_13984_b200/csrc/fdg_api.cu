@@ -430,7 +430,7 @@ int fdg_gather(fdg_ctx* c, void* st, const uint64_t* nodes, const uint32_t* n_de
 }
 
 int fdg_set_gather_impl(int impl) {
-    if (impl != FDG_GATHER_TMA && impl != FDG_GATHER_LDG && impl != FDG_GATHER_TMA_WS)
+    if (impl != FDG_GATHER_TMA && impl != FDG_GATHER_LDG && impl != FDG_GATHER_TMA_WS && impl != FDG_GATHER_RB)
         return fail(FDG_INVALID_ARG, "unknown gather impl");
     g_gather_impl = impl;
     return FDG_OK;

@@ -387,7 +387,8 @@ struct HashRbShape {
     static constexpr int MINB = CH == 128 ? 3 : 2;
 };
 
-template <int RB, int CH, bool SHARDED, bool ALIAS>
+// HASH = false: the same row-group gather without the checksum (FDG_GATHER_RB).
+template <int RB, int CH, bool SHARDED, bool ALIAS, bool HASH = true>
 __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
     k_gather_hash_rb(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
                      const uint32_t* status, TableRef t, char* __restrict__ out, uint64_t* checksum) {
@@ -440,10 +441,10 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
                     if (EVEN || !lastc || int(part) < LASTP) {
                         if (!ALIAS && out)
                             stg_stream(reinterpret_cast<uint4*>(dst + k * S::RPI * RB + c * CH), v[k], pol_st);
-                        *reinterpret_cast<uint4*>(wbuf + (k * S::RPI + rsub) * S::STRIDE + part * 16) = v[k];
+                        if (HASH) *reinterpret_cast<uint4*>(wbuf + (k * S::RPI + rsub) * S::STRIDE + part * 16) = v[k];
                     }
                 }
-                __syncwarp();
+                if (HASH) __syncwarp();
                 if (!lastc) {
                     issue(c + 1);
                 } else if (i + 1 < my_full) {  // chunk 0 of this warp's next group
@@ -452,19 +453,21 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
                     const uint64_t g2 = g + 2 * gstride;
                     nxt_node = g2 < full ? __ldg(nodes + g2 * 32 + lane) : 0;
                 }
-                const uint4* p = reinterpret_cast<const uint4*>(wbuf + lane * S::STRIDE);
-                const int parts = (EVEN || !lastc) ? S::NI : LASTP;
+                if (HASH) {
+                    const uint4* p = reinterpret_cast<const uint4*>(wbuf + lane * S::STRIDE);
+                    const int parts = (EVEN || !lastc) ? S::NI : LASTP;
 #pragma unroll
-                for (int s = 0; s < S::NI; ++s) {
-                    if (s < parts) {
-                        const uint4 w = p[s];
-                        h = splitmix64(h ^ (uint64_t(w.y) << 32 | w.x));
-                        h = splitmix64(h ^ (uint64_t(w.w) << 32 | w.z));
+                    for (int s = 0; s < S::NI; ++s) {
+                        if (s < parts) {
+                            const uint4 w = p[s];
+                            h = splitmix64(h ^ (uint64_t(w.y) << 32 | w.x));
+                            h = splitmix64(h ^ (uint64_t(w.w) << 32 | w.z));
+                        }
                     }
+                    __syncwarp();
                 }
-                __syncwarp();
             }
-            sum += splitmix64(h);
+            if (HASH) sum += splitmix64(h);
             g += gstride;
         }
     }
@@ -485,9 +488,10 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
                     const uint4 w = ldg_stream(reinterpret_cast<const uint4*>(src + c * CH) + part, pol);
                     if (!ALIAS && out)
                         stg_stream(reinterpret_cast<uint4*>(out + (tail * 32 + r) * RB + c * CH) + part, w, pol_st);
-                    *reinterpret_cast<uint4*>(wbuf + r * S::STRIDE + part * 16) = w;
+                    if (HASH) *reinterpret_cast<uint4*>(wbuf + r * S::STRIDE + part * 16) = w;
                 }
             }
+            if (!HASH) continue;
             __syncwarp();
             if (lane < int(rows)) {
                 const uint4* p = reinterpret_cast<const uint4*>(wbuf + lane * S::STRIDE);
@@ -499,8 +503,9 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
             }
             __syncwarp();
         }
-        if (lane < int(rows)) sum += splitmix64(h);
+        if (HASH && lane < int(rows)) sum += splitmix64(h);
     }
+    if (!HASH) return;
 #pragma unroll
     for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
@@ -551,6 +556,30 @@ int launch_hash_rb(const Ctx& c, cudaStream_t st, uint64_t groups, const uint64_
             return -1;
     }
 #undef FDG_HRB
+}
+
+// The plain gather on the row-group structure (FDG_GATHER_RB): 256-byte row chunks, the
+// next chunk's loads issued right after the current chunk's stores.
+template <bool SHARDED>
+int launch_gather_rb(const Ctx& c, cudaStream_t st, uint64_t groups, const uint64_t* nodes, const uint32_t* n_dev,
+                     uint64_t n_host, const uint32_t* status, const TableRef& t, char* out) {
+    const int blocks = int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps,
+                                              uint64_t(c.sm_count) * HashRbShape<256>::MINB));
+#define FDG_GRB(R)                                                                                          \
+    case R:                                                                                                 \
+        k_gather_hash_rb<R, 256, SHARDED, false, false><<<blocks, kHpWarps * 32, 0, st>>>(nodes, n_dev, n_host, \
+                                                                                       status, t, out, nullptr); \
+        return FDG_OK;
+    switch (c.row_bytes) {
+        FDG_GRB(400)
+        FDG_GRB(512)
+        FDG_GRB(1024)
+        FDG_GRB(1536)
+        FDG_GRB(3072)
+        default:
+            return -1;
+    }
+#undef FDG_GRB
 }
 
 // Warp-specialised gather + checksum (LDG): Wc copy warps move 32-row groups
@@ -831,6 +860,17 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
     if (impl == FDG_GATHER_TMA && out &&
         launch_gather_tma(c, st, nodes, n_dev, n_host, out, checksum, status) == FDG_OK)
         return FDG_OK;  // rows that do not suit the TMA paths fall through to the LDG kernels
+    if (impl == FDG_GATHER_RB && !checksum && out) {
+        const uint64_t groups = (n_bound + 31) / 32;
+        const int rc = sharded ? launch_gather_rb<true>(c, st, groups, nodes, n_dev, n_host, status, t,
+                                                        static_cast<char*>(out))
+                               : launch_gather_rb<false>(c, st, groups, nodes, n_dev, n_host, status, t,
+                                                         static_cast<char*>(out));
+        if (rc == FDG_OK) {
+            FDG_CUDA(cudaGetLastError());
+            return FDG_OK;
+        }
+    }
     if (checksum && c.row_bytes % 16 == 0) {
         uint64_t groups = (n_bound + 31) / 32;
         int blocks = int(std::min<uint64_t>((groups + kH16Warps - 1) / kH16Warps, uint64_t(c.sm_count) * 2));

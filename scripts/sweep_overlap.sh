@@ -1,2 +1,4 @@
-# sample || extract overlap knobs on the Papers pipeline (device-resident, no checksum)
-CFG=papers timeout 600 python scripts/ab.py "S=6" "S=6,cs=1" "S=8" "S=6,mode=sample" "S=6"
+# gather engine choices inside the Papers / Friendster pipeline (device-resident, no checksum)
+for c in papers friendster; do
+CFG=$c timeout 600 python scripts/ab.py "S=8" "S=8,gather_impl=3" "S=8,mode=extract" "S=8,mode=extract,gather_impl=3"
+done

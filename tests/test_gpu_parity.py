@@ -358,7 +358,7 @@ def test_pipeline_host_seeds_e2e(fd):
     L.fdg_host_free(rec.value)
 
 
-@pytest.mark.parametrize("impl", [0, 1, 2])
+@pytest.mark.parametrize("impl", [0, 1, 2, 3])
 @pytest.mark.parametrize("dim,rows", [(128, 50_000), (100, 33), (256, 1), (128, 0), (64, 70_001)])
 def test_gather_impls_agree(fd, port, impl, dim, rows):
     """TMA bulk-copy, LDG and warp-specialised TMA gathers (dynamic work claiming on):
