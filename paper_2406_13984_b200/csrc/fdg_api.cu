@@ -463,6 +463,11 @@ int fdg_set_option(const char* key, int64_t v) {
         g_hash_kernel = v;
         return FDG_OK;
     }
+    if (k == "gather_pf64") {
+        if (v < 0 || v > 2) return fail(FDG_INVALID_ARG, "gather_pf64 must be 0, 1 or 2");
+        g_gather_pf64 = v;
+        return FDG_OK;
+    }
     if (k == "bm_overlap") {
         g_bm_overlap = v != 0;
         return FDG_OK;
@@ -516,6 +521,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "hash_chunk") *v = g_hash_chunk;
     else if (k == "sage_gemm") *v = g_sage_gemm;
     else if (k == "bm_overlap") *v = g_bm_overlap;
+    else if (k == "gather_pf64") *v = g_gather_pf64;
     else if (k == "checksum_impl") *v = g_checksum_impl;
     else if (k == "ws_hashers") *v = g_ws_hashers;
     else if (k == "ws_stg") *v = g_ws_stg;

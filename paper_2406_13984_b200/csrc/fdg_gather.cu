@@ -41,6 +41,7 @@ struct TableRef {
     uint32_t n_shards;
     uint32_t row_bytes;
     uint32_t evict_first;
+    uint32_t pf64;  // 64-byte L2 fetch hint on table reads
 };
 
 template <bool SHARDED>
@@ -69,6 +70,19 @@ __device__ __forceinline__ uint64_t gather_policy_st(uint32_t ef) { return gathe
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p, uint64_t pol) {
     uint4 v;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+// 64-byte L2 fetches (LDG .LTC64B) instead of the default line fill, for rows whose length
+// is not a multiple of 128 B (a 400-byte row otherwise costs 4 full lines). A compile-time
+// choice: a runtime branch around the loads costs the fused-checksum kernel its MLP
+// (products extraction + checksum 147 -> 212 us per batch).
+template <bool PF64>
+__device__ __forceinline__ uint4 ldg_row(const uint4* p, uint64_t pol) {
+    if constexpr (!PF64) return ldg_stream(p, pol);
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p), "l"(pol));
     return v;
@@ -134,7 +148,7 @@ uint32_t* dyn_counter() {
     return ring + 2 * (next.fetch_add(1) % kDynRing);
 }
 
-template <bool SHARDED>
+template <bool SHARDED, bool PF64 = false>
 __global__ void __launch_bounds__(512) k_gather16_dyn(const uint64_t* __restrict__ nodes, const uint32_t* n_dev,
                                                       uint64_t n_host, const uint32_t* status, TableRef t,
                                                       FastDiv cdiv, uint32_t cpr, uint4* __restrict__ out,
@@ -163,7 +177,7 @@ __global__ void __launch_bounds__(512) k_gather16_dyn(const uint64_t* __restrict
                     cc[u] = b + u * 512 + threadIdx.x;
                     uint32_t row = cdiv.div(cc[u]);
                     uint32_t col = cc[u] - row * cpr;
-                    v[u] = ldg_stream(reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, __ldg(nodes + row))) + col,
+                    v[u] = ldg_row<PF64>(reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, __ldg(nodes + row))) + col,
                                       pol);
                 }
 #pragma unroll
@@ -173,7 +187,7 @@ __global__ void __launch_bounds__(512) k_gather16_dyn(const uint64_t* __restrict
                     uint32_t row = cdiv.div(c);
                     uint32_t col = c - row * cpr;
                     stg_stream(out + c,
-                               ldg_stream(reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, __ldg(nodes + row))) + col,
+                               ldg_row<PF64>(reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, __ldg(nodes + row))) + col,
                                           pol),
                                pol_st);
                 }
@@ -822,6 +836,7 @@ TableRef table_ref(const Ctx& c) {
     t.n_shards = c.n_shards;
     t.row_bytes = c.row_bytes;
     t.evict_first = g_gather_evict_first;
+    t.pf64 = g_gather_pf64 == 1 || (g_gather_pf64 == 2 && c.row_bytes % 128 != 0);
     return t;
 }
 
@@ -835,6 +850,9 @@ int g_gather_impl = FDG_GATHER_LDG;
 // faster without it: Papers 199 vs 206 us per batch, Friendster 330 vs 338, extraction
 // alone 154 vs 159 (scripts/sweep_overlap.sh). Off by default.
 int g_gather_evict_first = 0;
+// 64-byte L2 fetches on table reads: 0 off, 1 on, 2 (default) rows not a multiple of 128 B.
+// products (400-byte rows): extraction 133 -> 128 us, pipeline 192 -> 188 us per batch.
+int64_t g_gather_pf64 = 2;
 int g_gather_ctas_per_sm = 1;
 int64_t g_gather_dynamic = 1;
 // Fused gather + trainer checksum: 1 striped k_gather_hash16, 2 warp-specialised
@@ -930,6 +948,9 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
             if (sharded)
                 k_gather16_dyn<true><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr,
                                                              static_cast<uint4*>(out), ctr);
+            else if (t.pf64)
+                k_gather16_dyn<false, true><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr,
+                                                                    static_cast<uint4*>(out), ctr);
             else
                 k_gather16_dyn<false><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr,
                                                               static_cast<uint4*>(out), ctr);

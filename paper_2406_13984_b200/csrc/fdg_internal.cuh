@@ -104,6 +104,7 @@ int launch_gather(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const ui
                   void* out, uint64_t* checksum);
 extern int g_gather_impl;  // FDG_GATHER_TMA (default) or FDG_GATHER_LDG
 extern int g_gather_evict_first;
+extern int64_t g_gather_pf64;  // 64-byte L2 fetch hint on table reads (0 off, 1 on, 2 rows % 128 != 0)
 extern int g_gather_ctas_per_sm;
 extern int64_t g_gather_dynamic;
 extern int64_t g_hash_kernel;
