@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
 #pragma unroll
             for (int k = 0; k < S::NI; ++k)
                 if (EVEN || c + 1 < NCH || int(part) < LASTP)
-                    v[k] = ldg_stream(reinterpret_cast<const uint4*>(src[k] + c * CH), pol);
+                    v[k] = ldg_row<RB % 128 != 0>(reinterpret_cast<const uint4*>(src[k] + c * CH), pol);
         };
         uint64_t g = g0;
         uint64_t nxt_node = (g0 + gstride < full) ? __ldg(nodes + (g0 + gstride) * 32 + lane) : 0;
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
                 const uint64_t node = __shfl_sync(0xffffffffu, my_node, int(r));
                 if (r < rows && int(part) < parts) {
                     const char* src = ALIAS ? t.base + node * RB : row_ptr<SHARDED>(t, node);
-                    const uint4 w = ldg_stream(reinterpret_cast<const uint4*>(src + c * CH) + part, pol);
+                    const uint4 w = ldg_row<RB % 128 != 0>(reinterpret_cast<const uint4*>(src + c * CH) + part, pol);
                     if (!ALIAS && out)
                         stg_stream(reinterpret_cast<uint4*>(out + (tail * 32 + r) * RB + c * CH) + part, w, pol_st);
                     if (HASH) *reinterpret_cast<uint4*>(wbuf + r * S::STRIDE + part * 16) = w;
