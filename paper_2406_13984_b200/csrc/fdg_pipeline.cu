@@ -410,6 +410,18 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 // alias[par], is_load[par] and X[par] were last used by batch j-2's move
                 if (j >= 2) FDG_CUDA(cudaStreamWaitEvent(p->xstream, p->moved[par], 0));
                 FDG_TRY(bm_extract_meta(p->bm, p->xstream, p->nodes[nslot], n_dev, p->cap, p->alias[par], par));
+                if (j > 0) {  // lag-1 release (the releaser stage, pipeline.hpp:525-543)
+                    const uint64_t pj = do_sample ? j - 1 : ((j - 1) % (sampled_groups * G));
+                    // batch j-1's move reads its node list: the list is free once both are done
+                    FDG_CUDA(cudaStreamWaitEvent(p->xstream, p->moved[par ^ 1], 0));
+                    // (batch j-1's alias list is alias[par ^ 1]: the release needs no mapping-table reads)
+                    FDG_TRY(bm_release(p->bm, p->xstream, p->nodes[pj % p->nslots], p->alias[par ^ 1],
+                                       &p->counts[pj].n_nodes, p->cap));
+                    FDG_CUDA(cudaEventRecord(p->extracted[(j - 1) % p->nslots], p->xstream));
+                }
+                // Batch j's row move starts after release j-1, not right after bind j: the
+                // release (alias-list walk, latency-bound) then runs without the move saturating
+                // DRAM next to it, and the move overlaps batch j+1's acquire / select / bind.
                 FDG_CUDA(cudaEventRecord(p->bound[par], p->xstream));
                 FDG_CUDA(cudaStreamWaitEvent(xe, p->bound[par], 0));
                 FDG_TRY(bm_extract_move(p->bm, xe, p->nodes[nslot], n_dev, p->cap, p->alias[par], X, cs, par));
@@ -423,15 +435,6 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                     }
                 }
                 FDG_CUDA(cudaEventRecord(p->moved[par], xe));
-                if (j > 0) {  // lag-1 release (the releaser stage, pipeline.hpp:525-543)
-                    const uint64_t pj = do_sample ? j - 1 : ((j - 1) % (sampled_groups * G));
-                    // batch j-1's move reads its node list: the list is free once both are done
-                    FDG_CUDA(cudaStreamWaitEvent(p->xstream, p->moved[par ^ 1], 0));
-                    // (batch j-1's alias list is alias[par ^ 1]: the release needs no mapping-table reads)
-                    FDG_TRY(bm_release(p->bm, p->xstream, p->nodes[pj % p->nslots], p->alias[par ^ 1],
-                                       &p->counts[pj].n_nodes, p->cap));
-                    FDG_CUDA(cudaEventRecord(p->extracted[(j - 1) % p->nslots], p->xstream));
-                }
             }
             if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j + 1], xe));
             if (records_host)  // device -> host read of the batch record (counts + checksum)
