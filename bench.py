@@ -397,6 +397,8 @@ def run_ours(args):
                 "includes": "seed H2D, sample, extract, fused trainer checksum, batch-record D2H"},
         "clocks": clk.summary(),
     }
+    if bm_slots:
+        line["alias_only"] = _alias_only(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist)
     if args.train:
         line["train_stage"] = _train_stage(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist)
     if dist.world == 1 and not args.no_cpu_baseline:
@@ -412,6 +414,28 @@ def run_ours(args):
     if sharded:
         sharded.close()
     dist.close()
+
+
+def _alias_only(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist):
+    """Config 3 in the reference's own form: extraction produces the NodeAliasList and fills
+    the FeatureRegion slots of the misses (extractor.hpp:88-113); the trainer reads rows
+    through the aliases (pipeline.hpp:103-124), so no separate mini-batch tensor is written."""
+    from paper_2406_13984_b200.featdrive import DeviceBuffer
+    pipe = fd.Pipeline(topo, fan, B, buffer_slots=bm_slots, checksum=False, samplers=args.samplers,
+                       group_batches=args.group, write_x=False)
+    warm = DeviceBuffer.from_array(seeds_for(ids_warm))
+    timed = DeviceBuffer.from_array(seeds_for(ids))
+    pipe.run(warm.ptr, False, rng_of(ids_warm))
+    dist.barrier()
+    ms = dist.reduce(pipe.run(timed.ptr, False, rng_of(ids)), "max")
+    recs = pipe.records(len(ids))
+    pipe.close()
+    if np.any(recs["status"] != 0):
+        raise RuntimeError("alias-only run: batch status errors")
+    K = len(ids)
+    return {"value": dist.reduce(K, "sum") / (ms / 1e3), "unit": "batches/s", "ms_per_step": ms / K,
+            "note": "extraction = NodeAliasList + region slot fill of the misses (the reference's Extractor "
+                    "output); the headline value above also materialises X[i] = slot(alias[i])"}
 
 
 def _train_stage(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist):

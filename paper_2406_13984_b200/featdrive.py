@@ -503,11 +503,12 @@ class Pipeline:
 
     def __init__(self, topo: Topology, fanouts, batch_size: int = 1000, buffer_slots: int | None = None,
                  checksum: bool = False, samplers: int = 6, group_batches: int = 1, prefetch_group: int = 16,
-                 flags: int = 0):
+                 flags: int = 0, write_x: bool = True):
         self.topo = topo
         cfg = _lib.PipelineConfig(batch_size=batch_size, n_samplers=samplers, prefetch_group=prefetch_group,
                                   use_buffer_manager=1 if buffer_slots else 0, buffer_slots=buffer_slots or 0,
-                                  write_x=1, checksum=1 if checksum else 0, flags=flags, group_batches=group_batches)
+                                  write_x=1 if write_x else 0, checksum=1 if checksum else 0, flags=flags,
+                                  group_batches=group_batches)
         f = np.ascontiguousarray(list(fanouts.per_layer if isinstance(fanouts, Fanouts) else fanouts), np.uint32)
         p = C.c_void_p()
         check(lib().fdg_pipeline_create(topo.ctx, _p(f), len(f), C.byref(cfg), C.byref(p)))

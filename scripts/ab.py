@@ -33,12 +33,14 @@ for spec in sys.argv[1:]:
     mode = kv.pop("mode", "full")
     cs = int(kv.pop("cs", 0))
     flags = int(kv.pop("flags", 0)) | {"full": 0, "sample": 1, "extract": 2}[mode]
+    bm_slots = int(kv.pop("bm", 0))
     opts = dict(defaults)
     opts.update({k: int(v) for k, v in kv.items()})
     for k, v in opts.items():
         fd.featdrive.check(L.fdg_set_option(k.encode(), v))
+    bm = bm_slots
     cfg = _lib.PipelineConfig(batch_size=B, n_samplers=S, prefetch_group=16, write_x=1, flags=flags, group_batches=Gb,
-                              checksum=cs)
+                              checksum=cs, use_buffer_manager=1 if bm else 0, buffer_slots=bm)
     p = C.c_void_p()
     fd.featdrive.check(L.fdg_pipeline_create(topo.ctx, f.ctypes.data_as(C.c_void_p), len(f), C.byref(cfg), C.byref(p)))
     ms = C.c_float()

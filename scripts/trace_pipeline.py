@@ -32,7 +32,8 @@ seeds = DeviceBuffer.from_array(np.ascontiguousarray(np.concatenate([order[(b % 
 import os
 bm_slots = int(os.environ.get("BM", "0"))
 cfg = _lib.PipelineConfig(batch_size=B, n_samplers=S, prefetch_group=16, write_x=1,
-                          use_buffer_manager=1 if bm_slots else 0, buffer_slots=bm_slots)
+                          use_buffer_manager=1 if bm_slots else 0, buffer_slots=bm_slots,
+                          flags=int(os.environ.get("FLAGS", "0")))
 f = np.ascontiguousarray(fan, np.uint32)
 p = C.c_void_p()
 fd.featdrive.check(L.fdg_pipeline_create(topo.ctx, f.ctypes.data_as(C.c_void_p), len(f), C.byref(cfg), C.byref(p)))
