@@ -187,14 +187,17 @@ int fdg_mt_stream(void* stream, uint64_t rng_seed, uint64_t n, uint64_t* out_dev
  * common.hpp:88-105) into *checksum_dev (caller zeroes it). */
 int fdg_gather(fdg_ctx* ctx, void* stream, const uint64_t* nodes_dev, const uint32_t* n_dev, uint64_t n_host,
                void* out_dev, uint64_t* checksum_dev);
-/* Gather engine: the 16-byte LDG/STG kernels (default, also for sharded tables and
- * rows not a multiple of 16 B) or TMA bulk copies (one 4-warp CTA per SM). The
- * fused-checksum gather uses option "checksum_impl" (default LDG) and "hash_kernel"
+/* Gather engines. fdg_gather (standalone) defaults to FDG_GATHER_RB_DYN (32-row groups
+ * claimed dynamically, 256-byte row chunks; other row sizes fall back to the 16-byte LDG/STG
+ * kernels); the pipeline runner uses option "pipeline_gather_impl" (default FDG_GATHER_LDG,
+ * chunk-striped with dynamic claiming). Sharded tables always take the row-group kernel.
+ * The fused-checksum gather uses option "checksum_impl" (default LDG) and "hash_kernel"
  * (default 4: software-pipelined, row size fixed at compile time). */
 #define FDG_GATHER_TMA 0
 #define FDG_GATHER_LDG 1
 #define FDG_GATHER_TMA_WS 2 /* warp-specialised TMA: producer warp + consumer (hashing) warps */
 #define FDG_GATHER_RB 3     /* 32-row groups, 256-byte chunks (the fused-checksum kernel's structure) */
+#define FDG_GATHER_RB_DYN 4 /* the same, 32-row groups claimed dynamically from a per-launch counter */
 int fdg_set_gather_impl(int impl);
 /* Tuning knobs (process-wide): "gather_impl" (FDG_GATHER_*), "gather_evict_first"
  * (0/1: L2 evict-first hints on the gather stream), "l2_persist_mb" (L2 set-aside

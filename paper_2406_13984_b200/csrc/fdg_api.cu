@@ -430,7 +430,8 @@ int fdg_gather(fdg_ctx* c, void* st, const uint64_t* nodes, const uint32_t* n_de
 }
 
 int fdg_set_gather_impl(int impl) {
-    if (impl != FDG_GATHER_TMA && impl != FDG_GATHER_LDG && impl != FDG_GATHER_TMA_WS && impl != FDG_GATHER_RB)
+    if (impl != FDG_GATHER_TMA && impl != FDG_GATHER_LDG && impl != FDG_GATHER_TMA_WS && impl != FDG_GATHER_RB &&
+        impl != FDG_GATHER_RB_DYN)
         return fail(FDG_INVALID_ARG, "unknown gather impl");
     g_gather_impl = impl;
     return FDG_OK;
@@ -461,6 +462,16 @@ int fdg_set_option(const char* key, int64_t v) {
     if (k == "hash_kernel") {
         if (v < 1 || v > 4) return fail(FDG_INVALID_ARG, "hash_kernel must be in [1, 4]");
         g_hash_kernel = v;
+        return FDG_OK;
+    }
+    if (k == "pipeline_gather_impl") {
+        if (v < 0 || v > FDG_GATHER_RB_DYN) return fail(FDG_INVALID_ARG, "pipeline_gather_impl: unknown gather impl");
+        g_pipeline_gather_impl = v;
+        return FDG_OK;
+    }
+    if (k == "rb_ctas_per_sm") {
+        if (v < 1 || v > 4) return fail(FDG_INVALID_ARG, "rb_ctas_per_sm must be in [1, 4]");
+        g_rb_ctas_per_sm = v;
         return FDG_OK;
     }
     if (k == "gather_pf64") {
@@ -522,6 +533,8 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "sage_gemm") *v = g_sage_gemm;
     else if (k == "bm_overlap") *v = g_bm_overlap;
     else if (k == "gather_pf64") *v = g_gather_pf64;
+    else if (k == "rb_ctas_per_sm") *v = g_rb_ctas_per_sm;
+    else if (k == "pipeline_gather_impl") *v = g_pipeline_gather_impl;
     else if (k == "checksum_impl") *v = g_checksum_impl;
     else if (k == "ws_hashers") *v = g_ws_hashers;
     else if (k == "ws_stg") *v = g_ws_stg;

@@ -574,13 +574,139 @@ int launch_hash_rb(const Ctx& c, cudaStream_t st, uint64_t groups, const uint64_
 #undef FDG_HRB
 }
 
+// Dynamically scheduled row-group gather (FDG_GATHER_RB_DYN): warps claim 32-row groups
+// from a per-launch counter (claimed one group ahead, so the next group's node ids and first
+// loads are in flight while the current group drains), 256-byte row chunks, 16 loads in
+// flight per lane. The row-group layout reads each row's chunks back to back (166 vs 203 us
+// for the chunk-striped gather in isolation); dynamic claiming lets CTAs that become resident
+// late take less work next to the samplers' kernels.
+template <int RB, bool SHARDED, bool PF64>
+__global__ void __launch_bounds__(256) k_gather_rb_dyn(const uint64_t* __restrict__ nodes, const uint32_t* n_dev,
+                                                       uint64_t n_host, const uint32_t* status, TableRef t,
+                                                       char* __restrict__ out, uint32_t* ctr) {
+    using S = HashRbShape<256>;
+    constexpr int CH = 256;
+    constexpr int NCH = (RB + CH - 1) / CH;
+    constexpr int LASTP = (RB - (NCH - 1) * CH) / 16;
+    constexpr bool EVEN = RB % CH == 0;
+    const bool skip = status && *status;
+    const uint64_t n = skip ? 0 : (n_dev ? *n_dev : n_host);
+    const uint32_t full = uint32_t(n / 32), total = full + (n % 32 ? 1u : 0u);
+    const int lane = threadIdx.x & 31;
+    const uint32_t part = lane % S::LPR, rsub = lane / S::LPR;
+    const uint64_t pol = gather_policy_ld(t.evict_first), pol_st = gather_policy_st(t.evict_first);
+    auto claim = [&]() -> uint32_t {
+        uint32_t g = 0;
+        if (lane == 0) g = atomicAdd(ctr, 1u);
+        return __shfl_sync(0xffffffffu, g, 0);
+    };
+    auto node_of = [&](uint32_t g) -> uint64_t {
+        const uint64_t r = uint64_t(g) * 32 + lane;
+        return (g < total && r < n) ? __ldg(nodes + r) : 0;
+    };
+    const char* src[S::NI];
+    uint4 v[S::NI];
+    auto setup = [&](uint64_t node_reg) {
+#pragma unroll
+        for (int k = 0; k < S::NI; ++k) {
+            const uint64_t node = __shfl_sync(0xffffffffu, node_reg, k * S::RPI + int(rsub));
+            src[k] = row_ptr<SHARDED>(t, node) + part * 16;
+        }
+    };
+    auto issue = [&](int c) {
+#pragma unroll
+        for (int k = 0; k < S::NI; ++k)
+            if (EVEN || c + 1 < NCH || int(part) < LASTP)
+                v[k] = ldg_row<PF64>(reinterpret_cast<const uint4*>(src[k] + c * CH), pol);
+    };
+    uint32_t g = claim();
+    uint64_t cur_node = node_of(g);
+    uint32_t gn = g < total ? claim() : total;
+    uint64_t nxt_node = node_of(gn);
+    if (g < full) {
+        setup(cur_node);
+        issue(0);
+    }
+    while (g < total) {
+        if (g < full) {
+            char* dst = out + (uint64_t(g) * 32 + rsub) * RB + part * 16;
+#pragma unroll 1
+            for (int c = 0; c < NCH; ++c) {
+                const bool lastc = c + 1 == NCH;
+#pragma unroll
+                for (int k = 0; k < S::NI; ++k)
+                    if (EVEN || !lastc || int(part) < LASTP)
+                        stg_stream(reinterpret_cast<uint4*>(dst + k * S::RPI * RB + c * CH), v[k], pol_st);
+                if (!lastc) {
+                    issue(c + 1);
+                } else if (gn < full) {  // the next (already claimed) group's first chunk
+                    setup(nxt_node);
+                    issue(0);
+                }
+            }
+        } else {  // the ragged last group (n % 32 rows)
+            const uint32_t rows = uint32_t(n - uint64_t(g) * 32);
+            for (int c = 0; c < NCH; ++c) {
+                const int parts = c + 1 < NCH ? S::NI : LASTP;
+#pragma unroll
+                for (int k = 0; k < S::NI; ++k) {
+                    const uint32_t r = k * S::RPI + rsub;
+                    const uint64_t node = __shfl_sync(0xffffffffu, cur_node, int(r));
+                    if (r < rows && int(part) < parts) {
+                        const uint4 w = ldg_row<PF64>(
+                            reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, node) + c * CH) + part, pol);
+                        stg_stream(reinterpret_cast<uint4*>(out + (uint64_t(g) * 32 + r) * RB + c * CH) + part, w,
+                                   pol_st);
+                    }
+                }
+            }
+            if (gn < full) {
+                setup(nxt_node);
+                issue(0);
+            }
+        }
+        g = gn;
+        cur_node = nxt_node;
+        gn = g < total ? claim() : total;
+        nxt_node = node_of(gn);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // every CTA has claimed past the end
+            ctr[0] = 0;
+            ctr[1] = 0;
+            __threadfence();
+        }
+    }
+}
+
+template <bool SHARDED, bool PF64>
+int launch_gather_rb_dyn(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                         const uint32_t* status, const TableRef& t, char* out, uint32_t* ctr, int blocks) {
+#define FDG_GRD(R)                                                                                           \
+    case R:                                                                                                  \
+        k_gather_rb_dyn<R, SHARDED, PF64><<<blocks, 256, 0, st>>>(nodes, n_dev, n_host, status, t, out, ctr); \
+        return FDG_OK;
+    switch (c.row_bytes) {
+        FDG_GRD(400)
+        FDG_GRD(512)
+        FDG_GRD(1024)
+        FDG_GRD(1536)
+        FDG_GRD(3072)
+        default:
+            return -1;
+    }
+#undef FDG_GRD
+}
+
 // The plain gather on the row-group structure (FDG_GATHER_RB): 256-byte row chunks, the
 // next chunk's loads issued right after the current chunk's stores.
 template <bool SHARDED>
 int launch_gather_rb(const Ctx& c, cudaStream_t st, uint64_t groups, const uint64_t* nodes, const uint32_t* n_dev,
                      uint64_t n_host, const uint32_t* status, const TableRef& t, char* out) {
     const int blocks = int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps,
-                                              uint64_t(c.sm_count) * HashRbShape<256>::MINB));
+                                              uint64_t(c.sm_count) * g_rb_ctas_per_sm));
 #define FDG_GRB(R)                                                                                          \
     case R:                                                                                                 \
         k_gather_hash_rb<R, 256, SHARDED, false, false><<<blocks, kHpWarps * 32, 0, st>>>(nodes, n_dev, n_host, \
@@ -846,9 +972,13 @@ TableRef table_ref(const Ctx& c) {
 
 }  // namespace
 
-// LDG/STG is the default: measured 177 us vs 203 us (TMA bulk) per Papers batch in
-// isolation and never slower inside the pipeline (profiles/README.md).
-int g_gather_impl = FDG_GATHER_LDG;
+// Standalone gathers (fdg_gather) default to the dynamically scheduled row-group kernel:
+// 155 us per Papers batch vs 166 (static row groups), 206 (chunk-striped LDG) and 203 (TMA
+// bulk); it also resolves shards once per row group (2 local shards: 157 vs 329 us).
+// Inside the pipeline the chunk-striped dynamic LDG kernel is faster next to the samplers
+// (199 vs 222 us per batch), so the runner has its own choice.
+int g_gather_impl = FDG_GATHER_RB_DYN;
+int64_t g_pipeline_gather_impl = FDG_GATHER_LDG;
 // L2 evict-first on the gather stream: helped the gather in isolation in an earlier version
 // (177 vs 186 us), but with the current samplers (evict-last hash tables) the pipeline is
 // faster without it: Papers 199 vs 206 us per batch, Friendster 330 vs 338, extraction
@@ -858,6 +988,7 @@ int g_gather_evict_first = 0;
 // products (400-byte rows): extraction 133 -> 128 us, pipeline 192 -> 188 us per batch.
 int64_t g_gather_pf64 = 2;
 int g_gather_ctas_per_sm = 1;
+int64_t g_rb_ctas_per_sm = 2;  // row-group plain gather: CTAs (8 warps) per SM per launch
 int64_t g_gather_dynamic = 1;
 // Fused gather + trainer checksum: 1 striped k_gather_hash16, 2 warp-specialised
 // k_gather_hash_ws, 3 software-pipelined k_gather_hash_pipe, 4 the same with a
@@ -870,21 +1001,44 @@ int64_t g_hash_chunk = 0;  // 0: 256-byte chunks for rows >= 256 B, else 128; or
 int64_t g_checksum_impl = FDG_GATHER_LDG;
 
 int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
-                        uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status) {
+                        uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status,
+                        bool pipeline) {
     if (c.row_bytes == 0 || c.shard_bases.empty()) return fail(FDG_NOT_LOADED, "gather: no feature table loaded");
     TableRef t = table_ref(c);
     const bool sharded = c.n_shards > 1;
     if (n_bound == 0) return FDG_OK;
-    const int impl = (checksum && g_checksum_impl >= 0) ? int(g_checksum_impl) : g_gather_impl;
+    int impl = (checksum && g_checksum_impl >= 0) ? int(g_checksum_impl)
+               : pipeline                             ? int(g_pipeline_gather_impl)
+                                                      : g_gather_impl;
+    if (sharded && impl == FDG_GATHER_LDG && !checksum) impl = FDG_GATHER_RB_DYN;  // shard once per row group
     if (impl == FDG_GATHER_TMA_WS && launch_gather_ws(c, st, nodes, n_dev, n_host, out, checksum, status,
                                                       dyn_counter()) == FDG_OK)
         return FDG_OK;
     if (impl == FDG_GATHER_TMA && out &&
         launch_gather_tma(c, st, nodes, n_dev, n_host, out, checksum, status) == FDG_OK)
         return FDG_OK;  // rows that do not suit the TMA paths fall through to the LDG kernels
-    // Sharded tables take the row-group kernel: it resolves each row's shard once per 32-row
-    // group instead of once per 16-byte chunk (Papers, 2 local shards: 173 vs 329 us).
-    if ((impl == FDG_GATHER_RB || (sharded && impl == FDG_GATHER_LDG)) && !checksum && out) {
+    if (impl == FDG_GATHER_RB_DYN && !checksum && out) {
+        uint32_t* ctr = dyn_counter();
+        if (!ctr) return cuda_fail(cudaGetLastError(), "cudaGetSymbolAddress(g_dyn_ctr)", __FILE__, __LINE__);
+        const uint64_t groups = (n_bound + 31) / 32;
+        const int blocks = int(std::max<uint64_t>(1, std::min<uint64_t>((groups + 7) / 8,
+                                                                      uint64_t(c.sm_count) * g_rb_ctas_per_sm)));
+        int rc;
+        if (sharded)
+            rc = launch_gather_rb_dyn<true, false>(c, st, nodes, n_dev, n_host, status, t, static_cast<char*>(out),
+                                                   ctr, blocks);
+        else if (t.pf64)
+            rc = launch_gather_rb_dyn<false, true>(c, st, nodes, n_dev, n_host, status, t, static_cast<char*>(out),
+                                                   ctr, blocks);
+        else
+            rc = launch_gather_rb_dyn<false, false>(c, st, nodes, n_dev, n_host, status, t, static_cast<char*>(out),
+                                                    ctr, blocks);
+        if (rc == FDG_OK) {
+            FDG_CUDA(cudaGetLastError());
+            return FDG_OK;
+        }
+    }
+    if (impl == FDG_GATHER_RB && !checksum && out) {
         const uint64_t groups = (n_bound + 31) / 32;
         const int rc = sharded ? launch_gather_rb<true>(c, st, groups, nodes, n_dev, n_host, status, t,
                                                         static_cast<char*>(out))
@@ -982,7 +1136,7 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
 int launch_gather(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                   void* out, uint64_t* checksum) {
     uint64_t bound = n_dev ? std::max<uint64_t>(n_host, 1) : n_host;
-    return launch_gather_bound(c, st, nodes, n_dev, n_host, bound, out, checksum, nullptr);
+    return launch_gather_bound(c, st, nodes, n_dev, n_host, bound, out, checksum, nullptr, false);
 }
 
 int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, const int64_t* alias,

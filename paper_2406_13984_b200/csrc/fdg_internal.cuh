@@ -106,6 +106,7 @@ extern int g_gather_impl;  // FDG_GATHER_TMA (default) or FDG_GATHER_LDG
 extern int g_gather_evict_first;
 extern int64_t g_gather_pf64;  // 64-byte L2 fetch hint on table reads (0 off, 1 on, 2 rows % 128 != 0)
 extern int g_gather_ctas_per_sm;
+extern int64_t g_rb_ctas_per_sm;
 extern int64_t g_gather_dynamic;
 extern int64_t g_hash_kernel;
 extern int64_t g_sage_gemm;
@@ -128,5 +129,7 @@ int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, con
                           const uint32_t* n_dev, uint64_t n_host, uint64_t* checksum,
                           const uint32_t* status = nullptr);
 int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
-                        uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status);
+                        uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status,
+                        bool pipeline = false);
+extern int64_t g_pipeline_gather_impl;  // gather engine of the pipeline runner (default LDG)
 }  // namespace fdg

@@ -396,7 +396,7 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
             const uint32_t nslot = uint32_t(src_j % p->nslots);
             if (!p->bm) {
                 FDG_TRY(launch_gather_bound(*p->ctx, xs, p->nodes[nslot], n_dev, p->cap, p->cap, X, cs,
-                                            &cnt->status));
+                                            &cnt->status, true));
                 if (train) {
                     FDG_TRY(fdg_sage_forward(p->model, xs, X, p->nodes[nslot], p->edges[nslot], cnt, p->label_seed,
                                              p->losses + j, nullptr));

@@ -9,7 +9,7 @@ from paper_2406_13984_b200.featdrive import DeviceBuffer, check, lib  # noqa: E4
 n, dim = 111_059_956, 128
 nodes = np.random.RandomState(0).randint(0, n, 933_000).astype(np.uint64)
 nd = DeviceBuffer.from_array(nodes)
-for shards, impl in ((1, 1), (2, 1), (2, 3), (1, 3)):
+for shards, impl in ((1, 1), (1, 3), (1, 4), (2, 3), (2, 4)):
     fd.set_option("gather_impl", impl)
     t = fd.Topology.generate(n, dim, 16, 7, shards=shards)
     out = DeviceBuffer(len(nodes) * 512)

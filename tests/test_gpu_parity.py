@@ -358,7 +358,7 @@ def test_pipeline_host_seeds_e2e(fd):
     L.fdg_host_free(rec.value)
 
 
-@pytest.mark.parametrize("impl", [0, 1, 2, 3])
+@pytest.mark.parametrize("impl", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("dim,rows", [(128, 50_000), (100, 33), (256, 1), (128, 0), (64, 70_001)])
 def test_gather_impls_agree(fd, port, impl, dim, rows):
     """TMA bulk-copy, LDG and warp-specialised TMA gathers (dynamic work claiming on):
@@ -368,6 +368,7 @@ def test_gather_impls_agree(fd, port, impl, dim, rows):
     table = t.download_rows(0, n)
     nodes = np.random.RandomState(impl + rows).randint(0, n, size=rows).astype(np.uint64)
     old = fd.featdrive.get_option("checksum_impl")
+    old_impl = fd.featdrive.get_option("gather_impl")
     fd.set_option("gather_impl", impl)
     fd.set_option("checksum_impl", -1)  # the fused checksum path follows gather_impl
     try:
@@ -377,7 +378,7 @@ def test_gather_impls_agree(fd, port, impl, dim, rows):
             assert cs == port.checksum_rows(x)
             np.testing.assert_array_equal(fd.gather(t, nodes), x)
     finally:
-        fd.set_option("gather_impl", 1)
+        fd.set_option("gather_impl", old_impl)
         fd.set_option("checksum_impl", old)
 
 
@@ -392,7 +393,6 @@ def test_checksum_kernels_agree(fd, port, hk, dim, rows):
     nodes = np.random.RandomState(hk + rows).randint(0, n, size=rows).astype(np.uint64)
     old = fd.featdrive.get_option("hash_kernel")
     old_cs = fd.featdrive.get_option("checksum_impl")
-    fd.set_option("gather_impl", 1)
     fd.set_option("checksum_impl", -1)
     fd.set_option("hash_kernel", hk)
     try:
