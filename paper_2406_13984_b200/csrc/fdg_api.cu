@@ -469,6 +469,11 @@ int fdg_set_option(const char* key, int64_t v) {
         g_pipeline_gather_impl = v;
         return FDG_OK;
     }
+    if (k == "rb_chunk") {
+        if (v != 128 && v != 256) return fail(FDG_INVALID_ARG, "rb_chunk must be 128 or 256");
+        g_rb_chunk = v;
+        return FDG_OK;
+    }
     if (k == "rb_ctas_per_sm") {
         if (v < 1 || v > 4) return fail(FDG_INVALID_ARG, "rb_ctas_per_sm must be in [1, 4]");
         g_rb_ctas_per_sm = v;
@@ -534,6 +539,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "bm_overlap") *v = g_bm_overlap;
     else if (k == "gather_pf64") *v = g_gather_pf64;
     else if (k == "rb_ctas_per_sm") *v = g_rb_ctas_per_sm;
+    else if (k == "rb_chunk") *v = g_rb_chunk;
     else if (k == "pipeline_gather_impl") *v = g_pipeline_gather_impl;
     else if (k == "checksum_impl") *v = g_checksum_impl;
     else if (k == "ws_hashers") *v = g_ws_hashers;

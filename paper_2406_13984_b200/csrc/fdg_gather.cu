@@ -580,12 +580,11 @@ int launch_hash_rb(const Ctx& c, cudaStream_t st, uint64_t groups, const uint64_
 // flight per lane. The row-group layout reads each row's chunks back to back (166 vs 203 us
 // for the chunk-striped gather in isolation); dynamic claiming lets CTAs that become resident
 // late take less work next to the samplers' kernels.
-template <int RB, bool SHARDED, bool PF64>
+template <int RB, bool SHARDED, bool PF64, int CH = 256>
 __global__ void __launch_bounds__(256) k_gather_rb_dyn(const uint64_t* __restrict__ nodes, const uint32_t* n_dev,
                                                        uint64_t n_host, const uint32_t* status, TableRef t,
                                                        char* __restrict__ out, uint32_t* ctr) {
-    using S = HashRbShape<256>;
-    constexpr int CH = 256;
+    using S = HashRbShape<CH>;
     constexpr int NCH = (RB + CH - 1) / CH;
     constexpr int LASTP = (RB - (NCH - 1) * CH) / 16;
     constexpr bool EVEN = RB % CH == 0;
@@ -684,9 +683,13 @@ __global__ void __launch_bounds__(256) k_gather_rb_dyn(const uint64_t* __restric
 template <bool SHARDED, bool PF64>
 int launch_gather_rb_dyn(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                          const uint32_t* status, const TableRef& t, char* out, uint32_t* ctr, int blocks) {
-#define FDG_GRD(R)                                                                                           \
-    case R:                                                                                                  \
-        k_gather_rb_dyn<R, SHARDED, PF64><<<blocks, 256, 0, st>>>(nodes, n_dev, n_host, status, t, out, ctr); \
+#define FDG_GRD(R)                                                                                            \
+    case R:                                                                                                   \
+        if (g_rb_chunk == 128)                                                                                \
+            k_gather_rb_dyn<R, SHARDED, PF64, 128><<<blocks, 256, 0, st>>>(nodes, n_dev, n_host, status, t, out, \
+                                                                           ctr);                              \
+        else                                                                                                  \
+            k_gather_rb_dyn<R, SHARDED, PF64><<<blocks, 256, 0, st>>>(nodes, n_dev, n_host, status, t, out, ctr); \
         return FDG_OK;
     switch (c.row_bytes) {
         FDG_GRD(400)
@@ -989,6 +992,7 @@ int g_gather_evict_first = 0;
 int64_t g_gather_pf64 = 2;
 int g_gather_ctas_per_sm = 1;
 int64_t g_rb_ctas_per_sm = 2;  // row-group plain gather: CTAs (8 warps) per SM per launch
+int64_t g_rb_chunk = 256;      // row-group plain gather: 128- or 256-byte row chunks
 int64_t g_gather_dynamic = 1;
 // Fused gather + trainer checksum: 1 striped k_gather_hash16, 2 warp-specialised
 // k_gather_hash_ws, 3 software-pipelined k_gather_hash_pipe, 4 the same with a

@@ -107,6 +107,7 @@ extern int g_gather_evict_first;
 extern int64_t g_gather_pf64;  // 64-byte L2 fetch hint on table reads (0 off, 1 on, 2 rows % 128 != 0)
 extern int g_gather_ctas_per_sm;
 extern int64_t g_rb_ctas_per_sm;
+extern int64_t g_rb_chunk;
 extern int64_t g_gather_dynamic;
 extern int64_t g_hash_kernel;
 extern int64_t g_sage_gemm;
