@@ -5,7 +5,11 @@
 // (extractor.hpp:142-151, 391-394) for stream-ordered batches. Exactly the
 // reference's state transitions and LRU order, computed batch-parallel:
 //
-//   mapping table  node -> packed {i32 slot, u32 valid<<31}  (8 B/node)
+//   mapping table  node -> packed {i32 slot, u32 valid<<31}  (8 B/node), invalidated
+//                  lazily: an entry is live only while slot[entry.slot].node still
+//                  names the node, so an eviction rebinds the slot without touching the
+//                  previous owner's entry (two random DRAM accesses per miss saved; the
+//                  acquire's owner check reads the slot record, which mostly hits L2)
 //   slot refs      slot -> u32 reference count (the reference keeps ref in the mapping
 //                  entry; a bound node's count lives with its slot here, so the release
 //                  walks the batch's alias list into a compact 4 B/slot array that stays
@@ -195,6 +199,9 @@ __global__ void __launch_bounds__(kT) k_acquire(BmDev B, const uint64_t* nodes, 
 #pragma unroll
     for (int k = 0; k < kI; ++k) en[k] = nd[k] < B.N ? B.map[nd[k]] : Entry{-1, 0u};  // all loads in flight
 #pragma unroll
+    for (int k = 0; k < kI; ++k)  // lazy invalidation: an entry is live only while its slot still names the node
+        if ((en[k].refv & kValid) && B.slot[en[k].slot].node != nd[k]) en[k] = Entry{-1, 0u};
+#pragma unroll
     for (int k = 0; k < kI; ++k) {
         const uint64_t i = i0 + k;
         if (i >= n) break;
@@ -313,10 +320,9 @@ __global__ void k_bind(BmDev B, const uint64_t* nodes, int64_t* alias) {
         const uint32_t i = B.load_pos[k];
         const uint64_t node = nodes[i];
         const uint64_t prev = B.slot[slot].node;
-        if (prev != kNoNode) {  // invalidate the previous owner (buffer_manager.hpp:281-291)
-            const Entry pe = B.map[prev];
-            if (B.ref[slot] != 0 || pe.slot != slot) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
-            B.map[prev] = Entry{-1, 0u};
+        if (prev != kNoNode) {  // evict the previous owner (buffer_manager.hpp:281-291): rebinding the
+            // slot below is the invalidation -- its mapping entry goes stale
+            if (B.ref[slot] != 0) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
             ++ev;
         }
         B.map[node] = Entry{slot, kValid};  // bind + publish
@@ -436,6 +442,9 @@ __global__ void __launch_bounds__(kT) k_release(BmDev B, const uint64_t* nodes, 
             const Entry e = nd[k] < B.N ? B.map[nd[k]] : Entry{-1, 0u};
             sl[k] = (e.refv & kValid) ? e.slot : -1;
         }
+#pragma unroll
+        for (int k = 0; k < kI; ++k)
+            if (sl[k] >= 0 && B.slot[sl[k]].node != nd[k]) sl[k] = -1;  // stale entry: not resident
     }
     uint32_t rf[kI];
 #pragma unroll
@@ -789,6 +798,11 @@ int fdg_bm_entry(fdg_bm* b, uint64_t node, int64_t* slot, uint32_t* ref, uint32_
     FDG_CUDA(cudaDeviceSynchronize());
     Entry e;
     FDG_CUDA(cudaMemcpy(&e, b->d.map + node, sizeof(e), cudaMemcpyDeviceToHost));
+    if (e.slot >= 0) {  // a stale entry (slot rebound since) reads as the reference's evicted state
+        uint64_t owner;
+        FDG_CUDA(cudaMemcpy(&owner, &b->d.slot[e.slot].node, 8, cudaMemcpyDeviceToHost));
+        if (owner != node) e = Entry{-1, 0u};
+    }
     *slot = e.slot;
     *ref = 0;
     if (e.slot >= 0) FDG_CUDA(cudaMemcpy(ref, b->d.ref + e.slot, 4, cudaMemcpyDeviceToHost));
@@ -825,6 +839,8 @@ int fdg_bm_validate(fdg_bm* b) {
         rev[s] = meta[s].node;
         pos[s] = meta[s].pos;
     }
+    for (uint64_t v = 0; v < d.N; ++v)  // stale entries (slot rebound since) are the reference's evicted entries
+        if (map[v].slot >= 0 && uint64_t(map[v].slot) < d.S && rev[map[v].slot] != v) map[v] = Entry{-1, 0u};
     std::vector<int32_t> ring(d.R);
     FDG_CUDA(cudaMemcpy(ring.data(), d.ring[h.ring_sel], d.R * 4, cudaMemcpyDeviceToHost));
     std::vector<uint8_t> seen(d.S, 0);
