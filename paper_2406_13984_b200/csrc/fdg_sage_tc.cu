@@ -14,7 +14,8 @@
 //   warps 4-7     : split the A block in place into A_hi and a separate A_lo tile
 //                   (elementwise, so the swizzle is preserved), fence to the async
 //                   proxy, arrive
-//   warps 8-11    : epilogue: tcgen05.ld 32 columns at a time, + bias, ReLU, store;
+//   warps 8-11    : epilogue: tcgen05.ld 32 columns at a time, + bias, ReLU, then through a
+//                   swizzled 4 KB smem block per warp into coalesced 128-byte row stores;
 //                   two TMEM accumulators let tile i's epilogue overlap tile i+1's MMAs
 //   warp 1 lane 0 : MMA issuer -- per K block 4 x 3 tcgen05.mma.kind::tf32
 //                   (M=128, N=128, K=8) into one TMEM accumulator; tcgen05.commit
@@ -35,7 +36,8 @@ constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32, kTcStages = 3;
 constexpr int kTcTile = kTcBM * kTcBK * 4;  // 16 KB (A and B tiles alike: 128 rows x 128 bytes)
 constexpr int kTcStageBytes = 4 * kTcTile;  // A_hi (TMA lands here), A_lo, W_hi, W_lo
 constexpr int kTcThreads = 384;  // warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4-7 split, 8-11 epilogue
-constexpr int kTcSmem = kTcStages * kTcStageBytes + 1024 /* alignment */ + 256 /* barriers */;
+constexpr int kTcEpiBytes = 4 * 32 * 32 * 4;  // epilogue staging: a 32 x 32 fp32 block per epilogue warp
+constexpr int kTcSmem = kTcStages * kTcStageBytes + 1024 /* alignment */ + 256 /* barriers */ + kTcEpiBytes;
 
 __device__ __forceinline__ uint32_t d_rows_tc(const fdg_batch_counts* c, int j) {
     uint32_t d = 0;
@@ -90,6 +92,73 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem, uint64_t a, uint64_t b,
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(bar))
                  : "memory");
+}
+
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+// hi = x with the low 13 mantissa bits cleared (exact in TF32), lo = x - hi
+__device__ __forceinline__ void split4(float4 v, float4& h, float4& l) {
+    h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+    h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+    h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+    h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+}
+
+// TMEM -> registers: 32 columns of the accumulator, lane = row (32x32b shape).
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Epilogue store of one warp's 32 x 32 block (rows row0.., columns col0..) of out[.. x ld]: the
+// row-per-lane registers go through a 4 KB staging block whose 16-byte chunks are XOR-swizzled
+// by row (conflict-free both ways), then every store instruction writes four full 128-byte row
+// segments (a row per lane wrote 32 half-used sectors). `bcol` = this lane's column's bias.
+template <bool RELU, bool BIAS>
+__device__ __forceinline__ void store_block(uint32_t stage, const uint32_t (&r)[32], float bcol, int lane,
+                                            float* __restrict__ out, size_t ld, int row0, int rows, int col0,
+                                            int cols) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        float4 v = make_float4(__uint_as_float(r[q * 4 + 0]), __uint_as_float(r[q * 4 + 1]),
+                               __uint_as_float(r[q * 4 + 2]), __uint_as_float(r[q * 4 + 3]));
+        if (BIAS) {
+            v.x += __shfl_sync(0xffffffffu, bcol, q * 4 + 0);
+            v.y += __shfl_sync(0xffffffffu, bcol, q * 4 + 1);
+            v.z += __shfl_sync(0xffffffffu, bcol, q * 4 + 2);
+            v.w += __shfl_sync(0xffffffffu, bcol, q * 4 + 3);
+        }
+        if (RELU) {
+            v.x = fmaxf(v.x, 0.f);
+            v.y = fmaxf(v.y, 0.f);
+            v.z = fmaxf(v.z, 0.f);
+            v.w = fmaxf(v.w, 0.f);
+        }
+        sts128(stage + lane * 128 + ((q ^ (lane & 7)) << 4), v);
+    }
+    __syncwarp();
+    const int ch = lane & 7, col = col0 + ch * 4;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int rr = i * 4 + (lane >> 3);
+        const float4 v = lds128(stage + rr * 128 + ((ch ^ (rr & 7)) << 4));
+        if (row0 + rr < rows && col < cols) *reinterpret_cast<float4*>(out + size_t(row0 + rr) * ld + col) = v;
+    }
+    __syncwarp();  // the staging block is rewritten by the next call
 }
 
 // Persistent: CTA c takes tiles c, c + grid, ... (row-tile major: the column tiles of a row
@@ -190,18 +259,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (int kb = 0; kb < nk; ++kb, ++it) {
                 const int s = it % kTcStages;
                 mbar_wait(full + s, uint32_t((it / kTcStages) & 1));
-                float4* hi = reinterpret_cast<float4*>(a_hi(s));
-                float4* lo = reinterpret_cast<float4*>(a_lo(s));
+                const uint32_t hi = sa(a_hi(s)), lo = sa(a_lo(s));
+                float4 v[kTcTile / 16 / 128];
 #pragma unroll
-                for (int i = t4; i < kTcTile / 16; i += 128) {
-                    const float4 v = hi[i];
-                    float4 h;
-                    h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                    h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                    h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                    h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                    hi[i] = h;
-                    lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+                for (int u = 0; u < kTcTile / 16 / 128; ++u) v[u] = lds128(hi + (t4 + u * 128) * 16);  // all loads first
+#pragma unroll
+                for (int u = 0; u < kTcTile / 16 / 128; ++u) {
+                    float4 h, l;
+                    split4(v[u], h, l);
+                    sts128(hi + (t4 + u * 128) * 16, h);
+                    sts128(lo + (t4 + u * 128) * 16, l);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
                 mbar_arrive(conv + s);
@@ -210,47 +277,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     } else if (warp >= 8) {
         // ---- epilogue: TMEM lane = tile row; warp w reads lanes 32 (w % 4) ..
         const int wq = warp & 3;
+        const uint32_t stage = sa(sm + kTcStages * kTcStageBytes + 256) + wq * 4096;
         int ti = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ti) {
             const int acc = ti & 1;
             const int m0 = (t / n_tiles) * kTcBM, n0 = (t % n_tiles) * kTcBN;
+            float bl[kTcBN / 32];  // lane's bias per 32-column chunk, loaded before the accumulator wait
+#pragma unroll
+            for (int c = 0; c < kTcBN / 32; ++c) bl[c] = n0 + c * 32 + lane < N ? bias[n0 + c * 32 + lane] : 0.f;
             mbar_wait(tmem_full + acc, uint32_t((ti / 2) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int row = m0 + wq * 32 + lane;
-            for (int c0 = 0; c0 < kTcBN; c0 += 32) {
+#pragma unroll
+            for (int c = 0; c < kTcBN / 32; ++c) {
                 uint32_t r[32];
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                    : "r"(tmem + (uint32_t(wq * 32) << 16) + uint32_t(acc * kTcBN + c0)));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (c0 + 32 == kTcBN) {  // every column of this accumulator is in registers: hand it back
+                tmem_ld32(tmem + (uint32_t(wq * 32) << 16) + uint32_t(acc * kTcBN + c * 32), r);
+                if (c + 1 == kTcBN / 32) {  // every column of this accumulator is in registers: hand it back
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     mbar_arrive(tmem_empty + acc);
                 }
-                if (row < M) {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const int col = n0 + c0 + q * 4;
-                        if (col >= N) break;
-                        float4 v = make_float4(__uint_as_float(r[q * 4 + 0]) + bias[col + 0],
-                                               __uint_as_float(r[q * 4 + 1]) + bias[col + 1],
-                                               __uint_as_float(r[q * 4 + 2]) + bias[col + 2],
-                                               __uint_as_float(r[q * 4 + 3]) + bias[col + 3]);
-                        if (RELU) {
-                            v.x = fmaxf(v.x, 0.f);
-                            v.y = fmaxf(v.y, 0.f);
-                            v.z = fmaxf(v.z, 0.f);
-                            v.w = fmaxf(v.w, 0.f);
-                        }
-                        *reinterpret_cast<float4*>(C + size_t(row) * N + col) = v;
-                    }
-                }
+                if (n0 + c * 32 < N) store_block<RELU, true>(stage, r, bl[c], lane, C, N, m0 + wq * 32, M, n0 + c * 32, N);
             }
         }
     }
@@ -282,20 +327,19 @@ __device__ __forceinline__ uint64_t umma_desc_mn(uint32_t saddr) {
 }
 
 __device__ __forceinline__ void split_tile(uint8_t* hi_t, uint8_t* lo_t, int t4, int row0, int R) {
-    float4* hi = reinterpret_cast<float4*>(hi_t);
-    float4* lo = reinterpret_cast<float4*>(lo_t);
-#pragma unroll 4
-    for (int i = t4; i < kTcTile / 16; i += 128) {
+    const uint32_t hi = sa(hi_t), lo = sa(lo_t);
+    float4 v[kTcTile / 16 / 128];
+#pragma unroll
+    for (int u = 0; u < kTcTile / 16 / 128; ++u) v[u] = lds128(hi + (t4 + u * 128) * 16);
+#pragma unroll
+    for (int u = 0; u < kTcTile / 16 / 128; ++u) {
+        const int i = t4 + u * 128;
         const int row = row0 + ((i * 16) & 4095) / 128;  // 4 KB boxes of 32 rows x 128 B
-        float4 v = hi[i];
-        if (row >= R) v = make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 h;
-        h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-        h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-        h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-        h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-        hi[i] = h;
-        lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        if (row >= R) v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 h, l;
+        split4(v[u], h, l);
+        sts128(hi + i * 16, h);
+        sts128(lo + i * 16, l);
     }
 }
 
@@ -411,6 +455,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
     } else if (warp >= 8) {
         const int wq = warp & 3;
+        const uint32_t stage = sa(sm + kTcStages * kTcStageBytes + 256) + wq * 4096;
         int ti = 0;
         for (int t = blockIdx.x; t < items; t += gridDim.x, ++ti) {
             const int acc = ti & 1;
@@ -420,38 +465,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             kb_range(z, k0, k1);
             mbar_wait(tmem_full + acc, uint32_t((ti / 2) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int row = m0 + wq * 32 + lane;  // input feature
-            float* Pz = P + size_t(z) * Kin * N;
-            for (int c0 = 0; c0 < kTcBN; c0 += 32) {
+            float* Pz = P + size_t(z) * Kin * N;  // rows = input features
+#pragma unroll
+            for (int c = 0; c < kTcBN / 32; ++c) {
                 uint32_t r[32];
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                    : "r"(tmem + (uint32_t(wq * 32) << 16) + uint32_t(acc * kTcBN + c0)));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (c0 + 32 == kTcBN) {
+                tmem_ld32(tmem + (uint32_t(wq * 32) << 16) + uint32_t(acc * kTcBN + c * 32), r);
+                if (c + 1 == kTcBN / 32) {
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     mbar_arrive(tmem_empty + acc);
                 }
-                if (row < Kin) {
-                    const bool empty_slice = k1 <= k0;
+                if (k1 <= k0) {  // an empty slice writes zeros
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const int col = n0 + c0 + q * 4;
-                        if (col >= N) break;
-                        const float4 v = empty_slice ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                                     : make_float4(__uint_as_float(r[q * 4 + 0]),
-                                                                   __uint_as_float(r[q * 4 + 1]),
-                                                                   __uint_as_float(r[q * 4 + 2]),
-                                                                   __uint_as_float(r[q * 4 + 3]));
-                        *reinterpret_cast<float4*>(Pz + size_t(row) * N + col) = v;
-                    }
+                    for (int q = 0; q < 32; ++q) r[q] = 0u;
                 }
+                if (n0 + c * 32 < N) store_block<false, false>(stage, r, 0.f, lane, Pz, N, m0 + wq * 32, Kin, n0 + c * 32, N);
             }
         }
     }
