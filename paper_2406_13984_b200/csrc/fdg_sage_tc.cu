@@ -11,9 +11,9 @@
 //   warp 0 lane 0 : TMA producer -- A block (128 rows x 32) and W_hi / W_lo blocks
 //                   (W stored transposed, K-major) into a 3-stage ring, 128-byte
 //                   swizzled (the canonical K-major SW128 UMMA layout)
-//   warps 4-7     : split the A block in place into A_hi and a separate A_lo tile
-//                   (elementwise, so the swizzle is preserved), fence to the async
-//                   proxy, arrive
+//   warps 4-7     : split the A block: A_lo = A - A_hi into its own tile (elementwise, so
+//                   the swizzle is preserved; A_hi is A itself, see kWriteHi), fence to
+//                   the async proxy, arrive
 //   warps 8-11    : epilogue: tcgen05.ld 32 columns at a time, + bias, ReLU, then through a
 //                   swizzled 4 KB smem block per warp into coalesced 128-byte row stores;
 //                   two TMEM accumulators let tile i's epilogue overlap tile i+1's MMAs
@@ -35,6 +35,11 @@ namespace {
 constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32, kTcStages = 3;
 constexpr int kTcTile = kTcBM * kTcBK * 4;  // 16 KB (A and B tiles alike: 128 rows x 128 bytes)
 constexpr int kTcStageBytes = 4 * kTcTile;  // A_hi (TMA lands here), A_lo, W_hi, W_lo
+// kind::tf32 reads only the top 19 bits of an fp32 operand (the low 13 mantissa bits are
+// ignored: truncation), so the TMA-landed block already is A_hi for the tensor core; the split
+// warps only write A_lo = A - trunc(A). Pinned by the 1e-5 parity tests (rounding there would
+// be a ~2^-12 relative error).
+constexpr bool kWriteHi = false;
 constexpr int kTcThreads = 384;  // warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4-7 split, 8-11 epilogue
 constexpr int kTcEpiBytes = 4 * 32 * 32 * 4;  // epilogue staging: a 32 x 32 fp32 block per epilogue warp
 constexpr int kTcSmem = kTcStages * kTcStageBytes + 1024 /* alignment */ + 256 /* barriers */ + kTcEpiBytes;
@@ -267,7 +272,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 for (int u = 0; u < kTcTile / 16 / 128; ++u) {
                     float4 h, l;
                     split4(v[u], h, l);
-                    sts128(hi + (t4 + u * 128) * 16, h);
+                    if (kWriteHi) sts128(hi + (t4 + u * 128) * 16, h);
                     sts128(lo + (t4 + u * 128) * 16, l);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
@@ -335,10 +340,11 @@ __device__ __forceinline__ void split_tile(uint8_t* hi_t, uint8_t* lo_t, int t4,
     for (int u = 0; u < kTcTile / 16 / 128; ++u) {
         const int i = t4 + u * 128;
         const int row = row0 + ((i * 16) & 4095) / 128;  // 4 KB boxes of 32 rows x 128 B
-        if (row >= R) v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const bool past = row >= R;  // stale rows of the buffers: zero both halves
+        if (past) v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
         float4 h, l;
         split4(v[u], h, l);
-        sts128(hi + i * 16, h);
+        if (kWriteHi || past) sts128(hi + i * 16, h);
         sts128(lo + i * 16, l);
     }
 }
