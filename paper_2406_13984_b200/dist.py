@@ -127,3 +127,84 @@ def allreduce_grads(model: "fdm.GraphSAGE", group=None) -> None:
     t.div_(world)
     fdm.check(fdm.lib().fdg_memcpy_h2d(gp, host.ctypes.data, n * 4, None))
     fdm.check(fdm.lib().fdg_device_sync())
+
+
+class AllToAllGather:
+    """The comparison baseline of SURVEY §8e for a row-sharded table: rows move by two
+    all-to-allv collectives instead of the gather kernel's one-sided NVLink loads
+    (ShardedFeatures). Per batch:
+
+      1. bucket the batch's node ids by owner (owner = node // rows_per_shard), stable, so
+         every bucket keeps batch order;
+      2. all_to_all_single of the per-owner counts, then of the ids;
+      3. every owner gathers the requested rows from its local shard (`local_gather`, e.g.
+         LocalShardGather = fdg_gather on the shard alone);
+      4. all_to_all_single of the rows back; X = the received rows in batch order.
+
+    With the NCCL backend steps 2 and 4 are the grouped ncclSend/ncclRecv all-to-allv the
+    one-sided design avoids (pipeline.hpp:193-203 splits batches, not rows, so the
+    reference has no such exchange). Tensors live wherever the backend wants them (CUDA
+    for NCCL, CPU for gloo: tests/test_dist.py runs the protocol with two gloo ranks)."""
+
+    def __init__(self, rows_per_shard: int, rank: int, world: int, local_gather, group=None):
+        self.rps, self.rank, self.world = int(rows_per_shard), rank, world
+        self.local_gather, self.group = local_gather, group
+
+    def plan(self, nodes):
+        """(order, send_counts): the stable owner-major permutation of the batch and the
+        number of ids bound for each rank."""
+        import torch
+        owner = torch.div(nodes, self.rps, rounding_mode="floor")
+        if len(nodes) and int(owner.max()) >= self.world:
+            raise fdm.OutOfRange("AllToAllGather: node id beyond the sharded table")
+        order = torch.argsort(owner, stable=True)
+        return order, torch.bincount(owner, minlength=self.world)
+
+    def __call__(self, nodes):
+        import torch
+        import torch.distributed as dist
+        nodes = nodes.to(torch.int64)
+        order, send_counts = self.plan(nodes)
+        recv_counts = torch.empty_like(send_counts)
+        dist.all_to_all_single(recv_counts, send_counts, group=self.group)
+        sc, rc = send_counts.tolist(), recv_counts.tolist()
+        want = torch.empty(sum(rc), dtype=torch.int64, device=nodes.device)
+        dist.all_to_all_single(want, nodes[order], rc, sc, group=self.group)
+        rows = self.local_gather(want - self.rank * self.rps)  # [sum(rc), row elems], request order
+        back = torch.empty((len(nodes),) + tuple(rows.shape[1:]), dtype=rows.dtype, device=rows.device)
+        dist.all_to_all_single(back, rows, sc, rc, group=self.group)
+        x = torch.empty_like(back)
+        x[order] = back
+        return x
+
+
+class LocalShardGather:
+    """fdg_gather over this rank's shard alone (local row ids): the owner-side step of
+    AllToAllGather on the GPU. `base` is the shard's device pointer (e.g. from
+    fdg_ctx_generate_feature_shard), `rows` its row count."""
+
+    def __init__(self, device: int, base: int, rows: int, row_bytes: int, dtype: str = "f32"):
+        L = fdm.lib()
+        self.ctx = C.c_void_p()
+        fdm.check(L.fdg_ctx_create(device, C.byref(self.ctx)))
+        arr = (C.c_void_p * 1)(base)
+        self.dt = 0 if dtype == "f32" else 1
+        fdm.check(L.fdg_ctx_set_feature_shards(self.ctx, C.cast(arr, C.c_void_p), 1, rows, rows, row_bytes, self.dt))
+        self.row_bytes = row_bytes
+
+    def __call__(self, ids):
+        import torch
+        tdt = torch.float32 if self.dt == 0 else torch.float16
+        elems = self.row_bytes // (4 if self.dt == 0 else 2)
+        ids = ids.to(torch.int64).contiguous()
+        out = torch.empty((len(ids), elems), dtype=tdt, device=ids.device)
+        if len(ids):
+            stream = torch.cuda.current_stream(ids.device).cuda_stream
+            fdm.check(fdm.lib().fdg_gather(self.ctx, C.c_void_p(stream), C.c_void_p(ids.data_ptr()), None, len(ids),
+                                           C.c_void_p(out.data_ptr()), None))
+        return out
+
+    def close(self):
+        if self.ctx:
+            fdm.lib().fdg_ctx_destroy(self.ctx)
+            self.ctx = None

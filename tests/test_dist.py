@@ -104,3 +104,72 @@ def test_two_process_data_parallel_train_stage():
                          capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert out.stdout.count("train-ok") == 2
+
+
+def _a2a_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    from paper_2406_13984_b200 import dist as fdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, d = 1001, 6
+        table = np.random.RandomState(5).randn(n, d).astype(np.float32)
+        rps, blocks = fdist.shard_geometry(n, world)
+        lo, hi = blocks[rank]
+        local = torch.from_numpy(table[lo:hi].copy())
+        g = fdist.AllToAllGather(rps, rank, world, lambda ids: local[ids])
+        rs = np.random.RandomState(100 + rank)
+        cases = [rs.randint(0, n, 700), np.arange(lo, hi)[::-1], np.zeros(0, np.int64),
+                 np.array([n - 1, 0, n - 1, 500])]
+        ok = []
+        for nodes in cases:
+            x = g(torch.from_numpy(np.ascontiguousarray(nodes, np.int64)))
+            ok.append(bool(np.array_equal(x.numpy(), table[np.asarray(nodes, np.int64)])))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_all_to_all_gather_protocol_two_ranks():
+    """SURVEY §8e's all-to-allv baseline (dist.AllToAllGather) with two gloo ranks: each
+    rank's rows, in batch order, equal the full table's -- random, own-shard-only, empty
+    and repeated-id batches (the ranks' batches differ, so the exchange is asymmetric)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_a2a_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    assert res == [(0, [True] * 4), (1, [True] * 4)]
+
+
+@pytest.mark.gpu
+def test_all_to_all_gather_nccl_one_rank():
+    """The device path of the all-to-allv baseline: NCCL collectives (one rank) around
+    fdg_gather on a single-shard context (dist.LocalShardGather) reproduce the gather."""
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    import paper_2406_13984_b200 as fd
+    from paper_2406_13984_b200 import dist as fdist
+    t = fd.Topology.generate(5000, 32, 8, 3)
+    info = t.info()
+    dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1)
+    try:
+        lg = fdist.LocalShardGather(0, info.table_dev, 5000, t.row_bytes)
+        g = fdist.AllToAllGather(5000, 0, 1, lg)
+        nodes = np.random.RandomState(9).randint(0, 5000, 3000).astype(np.int64)
+        x = g(torch.from_numpy(nodes).cuda())
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(x.cpu().numpy(), t.download_rows(0, 5000).view(np.float32)[nodes])
+        lg.close()
+    finally:
+        dist.destroy_process_group()
