@@ -509,6 +509,11 @@ int fdg_set_option(const char* key, int64_t v) {
         g_ws_hashers = int(v);
         return FDG_OK;
     }
+    if (k == "sampler_sms") {
+        if (v < 0 || v > 1024) return fail(FDG_INVALID_ARG, "sampler_sms must be in [0, 1024]");
+        g_sampler_sms = v;
+        return FDG_OK;
+    }
     if (k == "extract_streams") {
         if (v < 1 || v > 2) return fail(FDG_INVALID_ARG, "extract_streams must be 1 or 2");
         g_extract_streams = v;
@@ -545,6 +550,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "ws_hashers") *v = g_ws_hashers;
     else if (k == "ws_stg") *v = g_ws_stg;
     else if (k == "extract_streams") *v = g_extract_streams;
+    else if (k == "sampler_sms") *v = g_sampler_sms;
     else return fail(FDG_INVALID_ARG, "unknown option " + k);
     return FDG_OK;
 }

@@ -14,6 +14,7 @@
 //                     trainer checksum and the optional D2H of the batch record
 // so groups g+1..g+S are sampled while group g is extracted. Batch j is keyed
 // exactly as the reference (rng seed = batch_seed(seed, epoch, global id)).
+#include <cuda.h>
 #include <cuda_profiler_api.h>
 
 #include <algorithm>
@@ -50,6 +51,8 @@ struct fdg_pipeline {
     std::vector<cudaStream_t> sstream;
     std::vector<cudaStream_t> mstream;   // per-sampler MT prefetch streams
     cudaStream_t xstream = nullptr;
+    CUgreenCtx green_s = nullptr;        // SM partitions (option sampler_sms): samplers + MT streams
+    CUgreenCtx green_x = nullptr;        // ... and everything on the extraction streams
     cudaStream_t xstream2 = nullptr;     // second extraction stream (plain gathers alternate; with the
                                          // buffer manager: the row-move stream)
     cudaEvent_t bound[2] = {nullptr, nullptr};  // buffer manager: batch parity's metadata half done
@@ -83,8 +86,77 @@ struct fdg_pipeline {
 using namespace fdg;
 
 int64_t fdg::g_bm_overlap = 1;
+int64_t fdg::g_sampler_sms = 0;
 
 namespace {
+
+// Green contexts (driver API, CUDA 12.4+) through cudaGetDriverEntryPoint: the runtime's own
+// launches and events work on their streams (scripts/probes/green_ctx_probe.cu).
+struct GreenApi {
+    CUresult (*dev_get)(CUdevice*, int) = nullptr;
+    CUresult (*get_res)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
+    CUresult (*split)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*, unsigned int,
+                      unsigned int) = nullptr;
+    CUresult (*gen_desc)(CUdevResourceDesc*, CUdevResource*, unsigned int) = nullptr;
+    CUresult (*create)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int) = nullptr;
+    CUresult (*destroy)(CUgreenCtx) = nullptr;
+    CUresult (*stream)(CUstream*, CUgreenCtx, unsigned int, int) = nullptr;
+    bool ok = false;
+};
+
+const GreenApi& green_api() {
+    static GreenApi g = [] {
+        GreenApi a;
+        auto get = [](const char* name, auto& fn) {
+            void* ptr = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint(name, &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(ptr);
+            return fn != nullptr;
+        };
+        a.ok = get("cuDeviceGet", a.dev_get) && get("cuDeviceGetDevResource", a.get_res) &&
+               get("cuDevSmResourceSplitByCount", a.split) && get("cuDevResourceGenerateDesc", a.gen_desc) &&
+               get("cuGreenCtxCreate", a.create) && get("cuGreenCtxDestroy", a.destroy) &&
+               get("cuGreenCtxStreamCreate", a.stream);
+        cudaGetLastError();
+        return a;
+    }();
+    return g;
+}
+
+// Splits the device's SMs: `want` (rounded by the driver's partition granularity) for the
+// samplers, the rest for extraction.
+int make_partitions(int device, uint32_t want, CUgreenCtx* gs, CUgreenCtx* gx) {
+    const GreenApi& g = green_api();
+    if (!g.ok) return fail(FDG_CUDA_ERROR, "sampler_sms: green contexts unavailable in this driver");
+    CUdevice dev;
+    CUdevResource all, grp, rest;
+    unsigned int ng = 1;
+    if (g.dev_get(&dev, device) != CUDA_SUCCESS || g.get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+        g.split(&grp, &ng, &all, &rest, 0, want) != CUDA_SUCCESS || ng != 1 || rest.sm.smCount == 0)
+        return fail(FDG_INVALID_ARG, "sampler_sms: cannot split the device's SMs into " + std::to_string(want) +
+                                         " + rest");
+    CUdevResourceDesc d1, d2;
+    if (g.gen_desc(&d1, &grp, 1) != CUDA_SUCCESS || g.gen_desc(&d2, &rest, 1) != CUDA_SUCCESS ||
+        g.create(gs, d1, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+        g.create(gx, d2, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
+        return fail(FDG_CUDA_ERROR, "sampler_sms: green context creation failed");
+    return FDG_OK;
+}
+
+// A non-blocking stream with priority `prio`, inside green context `gc` when given.
+int make_stream(cudaStream_t* st, CUgreenCtx gc, int prio) {
+    if (!gc) {
+        FDG_CUDA(cudaStreamCreateWithPriority(st, cudaStreamNonBlocking, prio));
+        return FDG_OK;
+    }
+    CUstream s;
+    if (green_api().stream(&s, gc, CU_STREAM_NON_BLOCKING, prio) != CUDA_SUCCESS)
+        return fail(FDG_CUDA_ERROR, "cuGreenCtxStreamCreate failed");
+    *st = reinterpret_cast<cudaStream_t>(s);
+    return FDG_OK;
+}
 
 void destroy(fdg_pipeline* p) {
     if (!p) return;
@@ -99,6 +171,8 @@ void destroy(fdg_pipeline* p) {
     if (p->xstream) cudaStreamDestroy(p->xstream);
     if (p->xstream2) cudaStreamDestroy(p->xstream2);
     for (auto s : p->mstream) cudaStreamDestroy(s);
+    if (p->green_s) green_api().destroy(p->green_s);
+    if (p->green_x) green_api().destroy(p->green_x);
     for (auto v : p->nodes) cudaFree(v);
     for (auto v : p->edges) cudaFree(v);
     for (auto v : p->seeds) cudaFree(v);
@@ -141,6 +215,16 @@ int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     const bool prio = !(p->cfg.flags & FDG_PIPE_NO_PRIORITY);
+    // Optional SM partitioning: the latency-bound sampler chains on their own SMs, the
+    // bandwidth-bound extraction on the rest (no buffer manager: its k_compact assumes a
+    // device-wide co-resident grid).
+    if (g_sampler_sms > 0 && !cfg->use_buffer_manager) {
+        const int rc = make_partitions(ctx->device, uint32_t(g_sampler_sms), &p->green_s, &p->green_x);
+        if (rc) {
+            destroy(p);
+            return rc;
+        }
+    }
     for (uint32_t i = 0; i < S; ++i) {
         Sampler* s = nullptr;
         int rc = sampler_create(ctx, cfg->batch_size, fanouts, n_layers, &s, G);
@@ -150,7 +234,7 @@ int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers
         }
         p->samplers.push_back(s);
         cudaStream_t st;
-        FDG_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio ? prio_hi : prio_lo));
+        FDG_TRY(make_stream(&st, p->green_s, prio ? prio_hi : prio_lo));
         p->sstream.push_back(st);
     }
     // Optional: keep the samplers' batch hash tables L2-resident (persisting window).
@@ -189,14 +273,14 @@ int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers
     sampler_capacity(p->samplers[0], &mn, &me);
     p->max_nodes = mn;
     p->cap = std::max<uint64_t>(std::max(mn, me), 1);
-    FDG_CUDA(cudaStreamCreateWithPriority(&p->xstream, cudaStreamNonBlocking, prio_lo));
+    FDG_TRY(make_stream(&p->xstream, p->green_x, prio_lo));
     // Plain gathers of consecutive batches alternate between two streams so the tail
     // of one overlaps the head of the next (the buffer-manager path is stateful and
     // stays on one stream).
     // With the buffer manager the row moves get their own stream: batch j's move
     // overlaps batch j+1's acquire / select / bind (the metadata chain stays in order).
     if (cfg->use_buffer_manager || g_extract_streams > 1)
-        FDG_CUDA(cudaStreamCreateWithPriority(&p->xstream2, cudaStreamNonBlocking, prio_lo));
+        FDG_TRY(make_stream(&p->xstream2, p->green_x, prio_lo));
     if (cfg->use_buffer_manager)
         for (int i = 0; i < 2; ++i) {
             FDG_CUDA(cudaEventCreateWithFlags(&p->bound[i], cudaEventDisableTiming));
@@ -205,7 +289,7 @@ int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers
     // one MT stream per sampler: prefetch launches of different samplers overlap
     for (uint32_t i = 0; i < S; ++i) {
         cudaStream_t st;
-        FDG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        FDG_TRY(make_stream(&st, p->green_s, 0));
         p->mstream.push_back(st);
     }
     p->nslots = 2 * S * G;

@@ -324,6 +324,26 @@ def test_pipeline_runner_matches_host_api(fd, samplers, group, bm):
         assert int(recs["checksum"][b]) == cs, f"batch {b}"
 
 
+def test_pipeline_sm_partitions(fd):
+    """Option sampler_sms: samplers and extraction on disjoint green-context SM partitions
+    give the same batches and checksums as the host API."""
+    n, B, fan = 300_000, 256, [10, 5, 5]
+    t = fd.Topology.generate(n, 32, 12, 3)
+    order = np.concatenate(fd.partition_epoch(np.arange(8 * B, dtype=np.uint64), B, 99))
+    rng = np.array([fd.batch_seed(0, 0, b) for b in range(8)], np.uint64)
+    fd.set_option("sampler_sms", 32)
+    try:
+        pipe = fd.Pipeline(t, fan, B, checksum=True, samplers=2)
+        recs = pipe.run_batches(order, rng)
+        pipe.close()
+    finally:
+        fd.set_option("sampler_sms", 0)
+    for b in range(8):
+        batch = fd.sample_khop(t, order[b * B:(b + 1) * B], fan, int(rng[b]))
+        _, cs = fd.gather(t, batch.nodes, checksum=True)
+        assert int(recs["n_nodes"][b]) == len(batch.nodes) and int(recs["checksum"][b]) == cs
+
+
 def test_pipeline_buffer_capacity_reported(fd):
     """An undersized feature buffer (S below one batch's nodes) is the reference's
     StandbyTimeout; the runner reports it in the batch record instead of faulting."""
