@@ -334,6 +334,7 @@ def run_ours(args):
     achieved = float(gather_bytes.sum()) / (busy_ms / 1e3) / 1e9
     hbm, hbm_kind = peaks()
     pipe.close()
+    alone = None if frac else _gather_alone(fd, L, topo, fan, seeds_for, rng_of, ids[:3], hbm)
 
     # ---------------- end to end through the C ABI with host buffers ----------------
     # every step: H2D of the batch's seeds from pinned memory, sample, extract with the
@@ -392,6 +393,7 @@ def run_ours(args):
                              "average launch duration is the union of the launch intervals / launches; "
                              "pipeline_gbs = all gather bytes / whole timed region"},
         "step_roofline": _step_roofline(cfg, max_ms / K, hbm),
+        "gather_alone": alone,
         "gpu_launches": _launch_count(K, len(fan), frac is not None, args.samplers),
         "e2e": {"value": e2e_value, "unit": "batches/s", "h2d_bytes_per_step": B * 8, "d2h_bytes_per_step": csz,
                 "includes": "seed H2D, sample, extract, fused trainer checksum, batch-record D2H"},
@@ -499,6 +501,43 @@ def _launch_count(K, layers, bm, samplers, prefetch=16):
     per_batch = 2 + (layers + 1) + layers + (1 if not bm else 10)
     per_sampler = -(-K // samplers)
     return K * per_batch + samplers * (-(-per_sampler // prefetch))
+
+
+def _gather_alone(fd, L, topo, fan, seeds_for, rng_of, ids, peak_gbs, reps=10):
+    """The standalone fdg_gather (default engine) on three of the timed batches' node lists,
+    nothing else running: CUDA events around each launch on its stream, batches alternating
+    so consecutive launches read different rows. Explains the in-pipeline roofline fraction
+    (the same bytes next to the sampler chains)."""
+    from paper_2406_13984_b200.featdrive import DeviceBuffer
+    rb = topo.row_bytes
+    lists = [fd.sample_khop(topo, seeds_for([g]), fan, int(r)).nodes for g, r in zip(ids, rng_of(ids))]
+    bufs = [DeviceBuffer.from_array(np.ascontiguousarray(x, np.uint64)) for x in lists]
+    out = DeviceBuffer(max(len(x) for x in lists) * rb)
+    evs = []
+    for _ in range(2 * reps + 2):
+        e = C.c_void_p()
+        fd.featdrive.check(L.fdg_event_create(C.byref(e)))
+        evs.append(e)
+    times, nbytes = [], []
+    for i in range(reps + 1):
+        b = i % len(bufs)
+        fd.featdrive.check(L.fdg_event_record(evs[2 * i], None))
+        fd.featdrive.check(L.fdg_gather(topo.ctx, None, bufs[b].ptr, None, len(lists[b]), out.ptr, None))
+        fd.featdrive.check(L.fdg_event_record(evs[2 * i + 1], None))
+        if i:  # the first launch warms the engine up
+            nbytes.append(2 * len(lists[b]) * rb)
+    fd.featdrive.check(L.fdg_device_sync())
+    for i in range(1, reps + 1):
+        ms = C.c_float()
+        fd.featdrive.check(L.fdg_event_elapsed_ms(evs[2 * i], evs[2 * i + 1], C.byref(ms)))
+        times.append(ms.value)
+    for e in evs:
+        L.fdg_event_destroy(e)
+    us = float(np.mean(times)) * 1e3
+    gbs = float(np.sum(nbytes)) / (float(np.sum(times)) / 1e3) / 1e9
+    return {"engine": "fdg_gather default (k_gather_rb_dyn, 32-row groups, 256-byte chunks)", "us_per_launch": us,
+            "achieved": gbs, "peak": peak_gbs, "unit": "GB/s", "frac": gbs / peak_gbs, "launches": reps,
+            "note": "same algorithmic bytes (2 x nodes x row_bytes) as roofline.achieved, gather alone on the GPU"}
 
 
 def _step_roofline(cfg, ms_per_step, peak_gbs):
