@@ -509,6 +509,11 @@ int fdg_set_option(const char* key, int64_t v) {
         g_ws_hashers = int(v);
         return FDG_OK;
     }
+    if (k == "tma_cfg") {
+        if (v < 0 || v > 3) return fail(FDG_INVALID_ARG, "tma_cfg must be in [0, 3]");
+        g_tma_cfg = v;
+        return FDG_OK;
+    }
     if (k == "sampler_sms") {
         if (v < 0 || v > 1024) return fail(FDG_INVALID_ARG, "sampler_sms must be in [0, 1024]");
         g_sampler_sms = v;
@@ -551,6 +556,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "ws_stg") *v = g_ws_stg;
     else if (k == "extract_streams") *v = g_extract_streams;
     else if (k == "sampler_sms") *v = g_sampler_sms;
+    else if (k == "tma_cfg") *v = g_tma_cfg;
     else return fail(FDG_INVALID_ARG, "unknown option " + k);
     return FDG_OK;
 }

@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(1024, 1)
 constexpr int kD = 8, kA = 6;     // plain gather: 8 stages, 6 chunks of loads in flight per warp
 constexpr int kDh = 3, kAh = 2;   // fused checksum: 32-row stages for one-row-per-lane hashing
 constexpr size_t kSmemBudget = 200 * 1024;
+constexpr size_t kSmemMax = 227 * 1024;
 
 }  // namespace
 
@@ -316,17 +317,24 @@ int launch_gather_tma(const Ctx& c, cudaStream_t st, const uint64_t* nodes, cons
                       void* out, uint64_t* checksum, const uint32_t* status) {
     const uint32_t rb = c.row_bytes;
     if (rb % 16 || c.n_shards != 1 || rb > 8192) return FDG_INVALID_ARG;
-    const int D = checksum ? kDh : kD;
-    uint32_t rs_cap = checksum ? 32u : std::max<uint32_t>(1, 4096 / rb);
-    uint32_t RS = uint32_t(std::min<size_t>(rs_cap, kSmemBudget / (size_t(kTmaWarps) * D * (rb + 16))));
+    // plain-gather ring shapes (option tma_cfg): {stages, chunks in flight, row cap per stage, smem}
+    struct Cfg { int D, A; uint32_t rs_cap; size_t budget; };
+    static const Cfg cfgs[4] = {{8, 6, 0, kSmemBudget}, {8, 7, 16, kSmemMax}, {12, 10, 16, kSmemMax},
+                                {16, 14, 16, kSmemMax}};
+    const Cfg cf = checksum ? Cfg{kDh, kAh, 32, kSmemBudget} : cfgs[std::min<int64_t>(std::max<int64_t>(g_tma_cfg, 0), 3)];
+    const int D = cf.D;
+    uint32_t rs_cap = cf.rs_cap ? cf.rs_cap : std::max<uint32_t>(1, 4096 / rb);
+    uint32_t RS = uint32_t(std::min<size_t>(rs_cap, cf.budget / (size_t(kTmaWarps) * D * (rb + 16))));
     if (RS == 0) return FDG_INVALID_ARG;
     const size_t smem = size_t(kTmaWarps) * D * RS * (rb + 16);
-    static bool attr[2] = {false, false};
-    auto kfn = checksum ? k_gather_tma<true, kDh, kAh> : k_gather_tma<false, kD, kA>;
-    if (!attr[checksum != nullptr]) {
-        FDG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBudget)));
-        attr[checksum != nullptr] = true;
-    }
+    using KFn = void (*)(const uint64_t*, const uint32_t*, uint64_t, const uint32_t*, const char*, uint32_t, uint32_t,
+                         char*, uint64_t*, int);
+    KFn kfn = checksum          ? KFn(k_gather_tma<true, kDh, kAh>)
+              : cf.D == 8 && cf.A == 6 ? KFn(k_gather_tma<false, 8, 6>)
+              : cf.D == 8          ? KFn(k_gather_tma<false, 8, 7>)
+              : cf.D == 12         ? KFn(k_gather_tma<false, 12, 10>)
+                                   : KFn(k_gather_tma<false, 16, 14>);
+    FDG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kfn<<<c.sm_count, kTmaWarps * 32, smem, st>>>(nodes, n_dev, n_host, status,
                                                    static_cast<const char*>(c.shard_bases[0]), rb, RS,
                                                    static_cast<char*>(out), checksum, g_gather_evict_first);
@@ -334,6 +342,7 @@ int launch_gather_tma(const Ctx& c, cudaStream_t st, const uint64_t* nodes, cons
     return FDG_OK;
 }
 
+int64_t g_tma_cfg = 0;  // plain TMA gather ring shape (launch_gather_tma)
 int g_ws_hashers = 8;  // consumer warps per CTA of k_gather_ws
 int g_ws_stg = 1;      // k_gather_ws stores X with 16-byte STG (1) or per-row bulk copies (0)
 

@@ -121,6 +121,7 @@ int launch_gather_ws(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const
 extern int64_t g_l2_persist_mb;
 extern int64_t g_hash_load_pct;
 extern int64_t g_sampler_ctas_per_sm;
+extern int64_t g_tma_cfg;          // plain TMA gather ring shape 0-3
 extern int64_t g_sampler_sms;      // >0: pipeline samplers on their own green-context SM partition
 extern int64_t g_extract_streams;  // 1 or 2 extraction streams in the pipeline runner
 extern int64_t g_hash_clear;
