@@ -197,9 +197,11 @@ def stage_reference_dataset(cfg, threads):
     return d, feats
 
 
-def cpu_reference(cfg, staged, order, batch_ids, threads):
+def cpu_reference(cfg, staged, order, batch_ids, threads, bm=None):
     """The reference's sample_khop -> row extraction -> trainer checksum for `batch_ids`
-    (contiguous), one batch per host thread. Returns (secs, checksums, node_counts)."""
+    (contiguous), one batch per host thread. With `bm` (RefBuffer, config 3) the batches
+    go in order through the reference BufferManager into its region (samplers on the other
+    threads). Returns (secs, checksums, node_counts)."""
     import oracle
     n, dim, avg, fan, b, t_ids, dtype, _ = CONFIGS[cfg]
     R = oracle.Ref()
@@ -207,9 +209,31 @@ def cpu_reference(cfg, staged, order, batch_ids, threads):
     topo = oracle.RefTopology(R, d)
     first = int(batch_ids[0])
     seeds = np.ascontiguousarray(order[first * b:(first + len(batch_ids)) * b])
-    secs, cs, nc = R.bench_sample_extract(topo, feats, seeds, len(batch_ids), b, fan, 0, 0, first, threads)
+    if bm is not None:
+        secs, cs, nc = R.bench_sample_extract_bm(topo, feats, seeds, len(batch_ids), b, fan, 0, 0, first, threads,
+                                                 bm.h, bm.region)
+    else:
+        secs, cs, nc = R.bench_sample_extract(topo, feats, seeds, len(batch_ids), b, fan, 0, 0, first, threads)
     topo.close()
     return secs, cs, nc
+
+
+class RefBuffer:
+    """The reference's featbuf::BufferManager (default mapping: dense below 32 M nodes,
+    sparse above) + a host region of `slots` rows, persisting across cpu_reference calls."""
+
+    def __init__(self, num_nodes, slots, row_bytes):
+        import oracle
+        self.R = oracle.Ref()
+        self.h = self.R.lib.fdref_bm_create(num_nodes, slots, 0, 0)
+        if not self.h:
+            raise RuntimeError("fdref_bm_create: " + self.R.err())
+        self.region = np.empty(slots * row_bytes, np.uint8)
+
+    def close(self):
+        if self.h:
+            self.R.lib.fdref_bm_destroy(self.h)
+            self.h = None
 
 
 def run_reference_arm(args):
@@ -230,28 +254,36 @@ def run_reference_arm(args):
     R = oracle.Ref()
     order = R.partition_epoch(np.arange(t_ids, dtype=np.uint64), b, R.hash_combine(0, 0))
     nb = t_ids // b
+    bm = RefBuffer(n, int(n * frac), dim * (4 if dtype == "f32" else 2)) if frac else None
     try:
         W, K = args.warmup, args.steps
-        cpu_reference(cfg, staged, order, np.arange(W) % nb, threads)
+        cpu_reference(cfg, staged, order, np.arange(W) % nb, threads, bm)
         ids = (W + np.arange(K)) % nb
         # contiguous runs of batch ids (wrap at the epoch end)
         secs, nodes = 0.0, 0
         at = 0
         while at < K:
             run = int(min(K - at, nb - ids[at]))
-            s, cs, nc = cpu_reference(cfg, staged, order, ids[at:at + run], threads)
+            s, cs, nc = cpu_reference(cfg, staged, order, ids[at:at + run], threads, bm)
             secs += s
             nodes += int(nc.sum())
             at += run
     finally:
         shutil.rmtree(staged[0], ignore_errors=True)
+        if bm:
+            bm.close()
     value = K / secs
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "batches/s", "n_gpus": args.gpus,
         "steps": K, "warmup": W, "ms_per_step": 1e3 * secs / K, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (reference generator, seed 7)",
         "config": {"workload": DESCR[cfg], "threads": threads,
-                   "path": "graph::sample_khop + per-row extraction copy + trainer_step hash (oracle/_ref)",
+                   "path": ("graph::sample_khop on threads-1 workers; batches in order through "
+                            "featbuf::BufferManager (acquire, get_standby_slot + bind_slot + row copy per miss, "
+                            "publish_valid, lag-1 release_batch) + trainer_step hash over region[alias] (oracle/_ref)"
+                            if frac else
+                            "graph::sample_khop + per-row extraction copy + trainer_step hash (oracle/_ref)"),
+                   "buffer_slots": int(n * frac) if frac else None,
                    "mean_nodes_per_batch": nodes / K},
         "cpu_baseline": {"value": value, "unit": "batches/s", "cores": threads, "kind": "reference",
                          "sample": f"{K} batches of the epoch-0 partition, one batch per thread"},
@@ -585,16 +617,21 @@ def _cpu_baseline(cfg, topo, order, args, gpu_cs, gpu_nn):
     log(f"[cpu] staged the dataset in host memory in {time.time() - t0:.1f}s")
     threads = os.cpu_count()
     first = min(gpu_cs) if gpu_cs else 0
-    nbat = args.cpu_batches or 4 * threads
+    frac = CONFIGS[cfg][7]
+    nbat = args.cpu_batches or (16 if frac else 4 * threads)  # config 3 extracts batch after batch
+    bm = RefBuffer(n, int(n * frac), topo.row_bytes) if frac else None
     try:
-        secs, cs, nc = cpu_reference(cfg, (d, feats), order, np.arange(first, first + nbat), threads)
+        secs, cs, nc = cpu_reference(cfg, (d, feats), order, np.arange(first, first + nbat), threads, bm)
     finally:
         shutil.rmtree(d, ignore_errors=True)
+        if bm:
+            bm.close()
     compared = [b for b in range(nbat) if first + b in gpu_cs]
     equal = all(gpu_cs[first + b] == int(cs[b]) and gpu_nn[first + b] == int(nc[b]) for b in compared)
     return ({"value": nbat / secs, "unit": "batches/s", "cores": threads, "kind": "reference",
-             "sample": f"batches {first}..{first + nbat - 1} of the epoch-0 partition (sample_khop + row "
-                       f"extraction + trainer checksum), {secs:.1f}s on {threads} threads"},
+             "sample": f"batches {first}..{first + nbat - 1} of the epoch-0 partition (sample_khop + "
+                       + ("reference BufferManager extraction into a cold buffer" if frac else "row extraction")
+                       + f" + trainer checksum), {secs:.1f}s on {threads} threads"},
             {"batches_compared": len(compared), "all_equal": bool(equal)})
 
 

@@ -261,6 +261,9 @@ class Ref:
         L.fdref_bench_sample_extract.restype = C.c_double
         L.fdref_bench_sample_extract.argtypes = [vp, vp, u32, vp, u64, u64, vp, u32, u64, u64, u64, u32,
                                                  vp, vp]
+        L.fdref_bench_sample_extract_bm.restype = C.c_double
+        L.fdref_bench_sample_extract_bm.argtypes = [vp, vp, u32, vp, u64, u64, vp, u32, u64, u64, u64, u32,
+                                                    vp, vp, vp, vp]
 
     def err(self):
         return self.lib.fdref_last_error().decode()
@@ -342,6 +345,23 @@ class Ref:
         nc = np.zeros(n_batches, np.uint64)
         secs = self.lib.fdref_bench_sample_extract(topo.h, _p(table), rb, _p(seeds), n_batches, batch_size, _p(f),
                                                    len(f), seed, epoch, first_batch, threads, _p(cs), _p(nc))
+        if secs < 0:
+            raise OracleError(9, self.err())
+        return secs, cs, nc
+
+    def bench_sample_extract_bm(self, topo, table, seeds, n_batches, batch_size, fanouts, seed, epoch, first_batch,
+                                threads, bm, region):
+        """Config 3: sampling on threads - 1 workers, extraction in batch order through the
+        reference BufferManager `bm` (fdref_bm_create) into `region` (slots x row bytes)."""
+        table = np.ascontiguousarray(table)
+        rb = table.shape[1] * table.itemsize
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        f = np.ascontiguousarray(fanouts, np.uint32)
+        cs = np.zeros(n_batches, np.uint64)
+        nc = np.zeros(n_batches, np.uint64)
+        secs = self.lib.fdref_bench_sample_extract_bm(topo.h, _p(table), rb, _p(seeds), n_batches, batch_size,
+                                                      _p(f), len(f), seed, epoch, first_batch, threads, bm,
+                                                      _p(region), _p(cs), _p(nc))
         if secs < 0:
             raise OracleError(9, self.err())
         return secs, cs, nc

@@ -8,6 +8,9 @@
 // No reference source is copied here; this file only calls the reference API.
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
+#include <optional>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -424,6 +427,104 @@ double fdref_bench_sample_extract(void* topo, const void* table, uint32_t row_by
     for (auto& th : pool) th.join();
     double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return failed ? -1.0 : s;
+}
+
+// Config 3 on the CPU: the same sampling fan-out, then the batches in order through ONE
+// reference BufferManager (its single mutex serialises these operations in the reference
+// anyway): acquire_for_batch, get_standby_slot + bind_slot per miss, the miss rows copied
+// table -> region slot, publish_valid, trainer_step's hash over region[alias], and the
+// lag-1 release_batch -- the GPU runner's buffer-manager path with the full table as the
+// miss source. `bm` (fdref_bm_create) persists across calls, so a warm-up call warms it;
+// `region` is slots x row_bytes bytes. Batches are sampled by `threads - 1` workers at
+// most 2 x threads ahead of the extraction; `prev_*` carry the unreleased last batch.
+double fdref_bench_sample_extract_bm(void* topo, const void* table, uint32_t row_bytes, const uint64_t* seeds,
+                                     uint64_t n_batches, uint64_t batch_size, const uint32_t* fanouts,
+                                     uint32_t n_layers, uint64_t seed, uint64_t epoch, uint64_t first_batch,
+                                     uint32_t threads, void* bm, void* region, uint64_t* checksums,
+                                     uint64_t* node_counts) {
+    auto& t = *static_cast<graph::Topology*>(topo);
+    auto& mgr = *static_cast<featbuf::BufferManager*>(bm);
+    static thread_local std::vector<NodeId> held;  // the last extracted batch, released by the next call
+    static thread_local void* held_bm = nullptr;
+    if (held_bm != bm) {  // a different buffer manager: nothing of it is held
+        held.clear();
+        held_bm = bm;
+    }
+    graph::Fanouts f;
+    f.per_layer.assign(fanouts, fanouts + n_layers);
+    const uint64_t window = 2 * uint64_t(std::max<uint32_t>(threads, 2));
+    std::vector<std::optional<graph::SampledBatch>> ready(n_batches);
+    std::mutex mu;
+    std::condition_variable cv;
+    std::atomic<uint64_t> next{0}, consumed{0};
+    std::atomic<bool> failed{false};
+    auto t0 = std::chrono::steady_clock::now();
+    auto sampler = [&] {
+        try {
+            while (!failed) {
+                const uint64_t b = next.fetch_add(1);
+                if (b >= n_batches) return;
+                {
+                    std::unique_lock lk(mu);
+                    cv.wait(lk, [&] { return b < consumed + window || failed; });
+                }
+                auto batch = graph::sample_khop(
+                    t, std::span<const NodeId>(seeds + b * batch_size, batch_size), f,
+                    pipeline::PipelineSession::batch_seed(seed, epoch, first_batch + b));
+                {
+                    std::lock_guard lk(mu);
+                    ready[b] = std::move(batch);
+                }
+                cv.notify_all();
+            }
+        } catch (const std::exception& e) {
+            g_err = e.what();
+            failed = true;
+            cv.notify_all();
+        }
+    };
+    std::vector<std::thread> pool;
+    for (uint32_t i = 0; i + 1 < std::max<uint32_t>(threads, 2); ++i) pool.emplace_back(sampler);
+    const auto* tab = static_cast<const std::byte*>(table);
+    auto* reg = static_cast<std::byte*>(region);
+    try {
+        for (uint64_t b = 0; b < n_batches && !failed; ++b) {
+            graph::SampledBatch batch;
+            {
+                std::unique_lock lk(mu);
+                cv.wait(lk, [&] { return ready[b].has_value() || failed; });
+                if (failed) break;
+                batch = std::move(*ready[b]);
+                ready[b].reset();
+                consumed = b + 1;
+            }
+            cv.notify_all();
+            const auto& nodes = batch.nodes;
+            auto plan = mgr.acquire_for_batch(std::span<const NodeId>(nodes.data(), nodes.size()));
+            for (auto pos : plan.to_load) {
+                const SlotId s = mgr.get_standby_slot();
+                mgr.bind_slot(nodes[pos], s);
+                plan.alias[pos] = s;
+                std::memcpy(reg + uint64_t(s) * row_bytes, tab + nodes[pos] * uint64_t(row_bytes), row_bytes);
+            }
+            for (auto pos : plan.to_load) mgr.publish_valid(nodes[pos]);
+            if (!plan.waits.empty()) throw std::runtime_error("waits under a sequential schedule");
+            uint64_t sum = 0;
+            for (std::size_t i = 0; i < nodes.size(); ++i)
+                sum += hash_bytes64(std::span<const std::byte>(reg + uint64_t(plan.alias[i]) * row_bytes, row_bytes));
+            checksums[b] = sum;
+            node_counts[b] = nodes.size();
+            if (!held.empty()) mgr.release_batch(std::span<const NodeId>(held.data(), held.size()));
+            held = nodes;
+        }
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        failed = true;
+        cv.notify_all();
+    }
+    for (auto& th : pool) th.join();
+    double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return failed ? -1.0 : secs;
 }
 
 }  // extern "C"

@@ -199,3 +199,33 @@ def test_sage_oracle_matches_torch(port, fan, dims):
     assert abs(l1 - l2) <= 1e-12 * abs(l2)
     np.testing.assert_allclose(g1, g2, rtol=1e-12, atol=1e-12)
     assert g1.shape == (len(np.unique(seeds)), dims[-1])
+
+
+def test_ref_config3_baseline_checksums(ref):
+    """bench.py's config-3 CPU baseline (batches in order through the reference
+    BufferManager, rows hashed from the region via the alias list) yields the same
+    per-batch trainer checksums as the plain extraction path, across two calls that share
+    the warm buffer (lag-1 release carried over)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    d = tempfile.mkdtemp(prefix="fd_c3_")
+    n, dim = 300_000, 8
+    feats, _ = ref.stage_dataset(d, n, dim, 10, 7, 4)
+    order = ref.partition_epoch(np.arange(8000, dtype=np.uint64), 500, ref.hash_combine(0, 0))
+    bench.CONFIGS["c3_test"] = (n, dim, 10, [5, 5, 5], 500, 8000, "f32", 0.5)
+    bm = bench.RefBuffer(n, n // 2, dim * 4)
+    try:
+        _, cs0, nc0 = bench.cpu_reference("c3_test", (d, feats), order, np.arange(0, 10), 4)
+        _, cs1, nc1 = bench.cpu_reference("c3_test", (d, feats), order, np.arange(0, 5), 4, bm)
+        _, cs2, nc2 = bench.cpu_reference("c3_test", (d, feats), order, np.arange(5, 10), 4, bm)
+        st = np.zeros(7, np.uint64)
+        ref.lib.fdref_bm_stats(bm.h, st.ctypes.data)
+    finally:
+        bm.close()
+        del bench.CONFIGS["c3_test"]
+        import shutil
+        shutil.rmtree(d, ignore_errors=True)
+    np.testing.assert_array_equal(cs0, np.concatenate([cs1, cs2]))
+    np.testing.assert_array_equal(nc0, np.concatenate([nc1, nc2]))
+    assert int(st[1]) > 0 and int(st[3]) > 0 and int(st[5]) == 9  # loads, evictions, 9 lag-1 releases
