@@ -286,7 +286,10 @@ def run_reference_arm(args):
                    "buffer_slots": int(n * frac) if frac else None,
                    "mean_nodes_per_batch": nodes / K},
         "cpu_baseline": {"value": value, "unit": "batches/s", "cores": threads, "kind": "reference",
-                         "sample": f"{K} batches of the epoch-0 partition, one batch per thread"},
+                         "sample": f"{K} batches of the epoch-0 partition, "
+                                   + ("sampled on threads - 1 workers, extracted in order through one "
+                                      "reference BufferManager (warm after the warm-up batches)" if frac
+                                      else "one batch per thread")},
         "e2e": {"value": value, "unit": "batches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
