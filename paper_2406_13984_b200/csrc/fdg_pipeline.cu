@@ -191,16 +191,9 @@ void destroy(fdg_pipeline* p) {
     delete p;
 }
 
-}  // namespace
-
-extern "C" {
-
-int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers, const fdg_pipeline_config* cfg,
-                        fdg_pipeline** out) {
-    if (cfg->batch_size == 0) return fail(FDG_INVALID_ARG, "config: batch_size must be >= 1");
-    if (ctx->row_bytes == 0) return fail(FDG_NOT_LOADED, "pipeline: no feature table loaded");
-    cudaSetDevice(ctx->device);
-    auto p = new fdg_pipeline();
+// Builds everything of `p`; on failure the caller destroys the partial pipeline.
+int pipeline_build(fdg_pipeline* p, fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers,
+                   const fdg_pipeline_config* cfg) {
     p->ctx = ctx;
     p->cfg = *cfg;
     if (p->cfg.n_samplers == 0) p->cfg.n_samplers = 8;  // measured on B200: Papers flat at 6-10, products best from 8
@@ -220,18 +213,12 @@ int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers
     // device-wide co-resident grid).
     if (g_sampler_sms > 0 && !cfg->use_buffer_manager) {
         const int rc = make_partitions(ctx->device, uint32_t(g_sampler_sms), &p->green_s, &p->green_x);
-        if (rc) {
-            destroy(p);
-            return rc;
-        }
+        if (rc) return rc;
     }
     for (uint32_t i = 0; i < S; ++i) {
         Sampler* s = nullptr;
         int rc = sampler_create(ctx, cfg->batch_size, fanouts, n_layers, &s, G);
-        if (rc) {
-            destroy(p);
-            return rc;
-        }
+        if (rc) return rc;
         p->samplers.push_back(s);
         cudaStream_t st;
         FDG_TRY(make_stream(&st, p->green_s, prio ? prio_hi : prio_lo));
@@ -324,10 +311,25 @@ int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers
     }
     if (cfg->use_buffer_manager) {
         int rc = fdg_bm_create(ctx, cfg->buffer_slots, 0, uint32_t(p->max_nodes), &p->bm);
-        if (rc) {
-            destroy(p);
-            return rc;
-        }
+        if (rc) return rc;
+    }
+    return FDG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fdg_pipeline_create(fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers, const fdg_pipeline_config* cfg,
+                        fdg_pipeline** out) {
+    if (cfg->batch_size == 0) return fail(FDG_INVALID_ARG, "config: batch_size must be >= 1");
+    if (ctx->row_bytes == 0) return fail(FDG_NOT_LOADED, "pipeline: no feature table loaded");
+    cudaSetDevice(ctx->device);
+    auto p = new fdg_pipeline();
+    const int rc = pipeline_build(p, ctx, fanouts, n_layers, cfg);
+    if (rc) {
+        destroy(p);  // everything built so far
+        return rc;
     }
     *out = p;
     return FDG_OK;
