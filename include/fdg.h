@@ -199,9 +199,14 @@ int fdg_gather(fdg_ctx* ctx, void* stream, const uint64_t* nodes_dev, const uint
 #define FDG_GATHER_RB 3     /* 32-row groups, 256-byte chunks (the fused-checksum kernel's structure) */
 #define FDG_GATHER_RB_DYN 4 /* the same, 32-row groups claimed dynamically from a per-launch counter */
 int fdg_set_gather_impl(int impl);
-/* Tuning knobs (process-wide): "gather_impl" (FDG_GATHER_*), "gather_evict_first"
- * (0/1: L2 evict-first hints on the gather stream), "l2_persist_mb" (L2 set-aside
- * for the samplers' hash tables; 0 = off), "hash_load_pct" (hash table sizing). */
+/* Tuning knobs (process-wide; fdg_api.cu lists all, with their ranges). Main ones:
+ * "gather_impl" / "pipeline_gather_impl" / "checksum_impl" (FDG_GATHER_*),
+ * "gather_evict_first" (0-3: L2 evict-first hints on the gather stream), "l2_persist_mb"
+ * (L2 set-aside for the samplers' hash tables; 0 = off), "hash_load_pct" (hash table
+ * sizing), "extract_streams" (1/2), "sage_gemm" (1 tcgen05 3xTF32, 0 CUDA cores),
+ * "bm_overlap" (buffer-manager row move on its own stream), "sampler_sms" (> 0: pipeline
+ * samplers on a green-context SM partition of that size, extraction on the rest; measured
+ * slower than sharing, default 0), "tma_cfg" (TMA gather ring shape 0-3). */
 int fdg_set_option(const char* key, int64_t value);
 int fdg_get_option(const char* key, int64_t* value);
 /* Checksum of rows already resident (region slot payloads addressed by alias). */
