@@ -51,6 +51,8 @@ struct fdg_pipeline {
     std::vector<cudaStream_t> sstream;
     std::vector<cudaStream_t> mstream;   // per-sampler MT prefetch streams
     cudaStream_t xstream = nullptr;
+    cudaStream_t tstream = nullptr;      // train stage (plain extraction): batch j's model step overlaps
+    cudaEvent_t gathered[2] = {}, trained[2] = {};  // the next gathers; per X parity
     CUgreenCtx green_s = nullptr;        // SM partitions (option sampler_sms): samplers + MT streams
     CUgreenCtx green_x = nullptr;        // ... and everything on the extraction streams
     cudaStream_t xstream2 = nullptr;     // second extraction stream (plain gathers alternate; with the
@@ -170,6 +172,11 @@ void destroy(fdg_pipeline* p) {
     for (auto s : p->sstream) cudaStreamDestroy(s);
     if (p->xstream) cudaStreamDestroy(p->xstream);
     if (p->xstream2) cudaStreamDestroy(p->xstream2);
+    if (p->tstream) cudaStreamDestroy(p->tstream);
+    for (int i = 0; i < 2; ++i) {
+        if (p->gathered[i]) cudaEventDestroy(p->gathered[i]);
+        if (p->trained[i]) cudaEventDestroy(p->trained[i]);
+    }
     for (auto s : p->mstream) cudaStreamDestroy(s);
     if (p->green_s) green_api().destroy(p->green_s);
     if (p->green_x) green_api().destroy(p->green_x);
@@ -467,9 +474,12 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
             // extract-only diagnostics re-extract the batches sampled in the first groups
             const uint64_t src_j = do_sample ? j : (j % (sampled_groups * G));
             fdg_batch_counts* cnt = p->counts + src_j;
-            // the train stage shares one model workspace: with a model the plain gathers stay on one stream
-            cudaStream_t xs = (!p->bm && !train && p->xstream2 && (j & 1)) ? p->xstream2 : p->xstream;
-            cudaStream_t xe = (p->bm && g_bm_overlap) ? p->xstream2 : xs;  // stream on which the batch's extraction ends
+            // plain gathers alternate between the two extraction streams; with a model the train
+            // stage (one model workspace) runs in batch order on its own stream behind them
+            cudaStream_t xs = (!p->bm && p->xstream2 && (j & 1)) ? p->xstream2 : p->xstream;
+            const bool tsplit = train && !p->bm;
+            // stream on which the batch's work ends
+            cudaStream_t xe = (p->bm && g_bm_overlap) ? p->xstream2 : tsplit ? p->tstream : xs;
             if (sample_only) {
                 FDG_CUDA(cudaEventRecord(p->extracted[slot], xs));
                 continue;
@@ -481,15 +491,22 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
             void* X = p->X[j & 1];
             const uint32_t nslot = uint32_t(src_j % p->nslots);
             if (!p->bm) {
+                const uint32_t par = uint32_t(j & 1);
+                // X[par] was last read by batch j-2's train stage
+                if (tsplit && j >= 2) FDG_CUDA(cudaStreamWaitEvent(xs, p->trained[par], 0));
                 FDG_TRY(launch_gather_bound(*p->ctx, xs, p->nodes[nslot], n_dev, p->cap, p->cap, X, cs,
                                             &cnt->status, true));
-                if (train) {
-                    FDG_TRY(fdg_sage_forward(p->model, xs, X, p->nodes[nslot], p->edges[nslot], cnt, p->label_seed,
-                                             p->losses + j, nullptr));
+                if (tsplit) {
+                    FDG_CUDA(cudaEventRecord(p->gathered[par], xs));
+                    FDG_CUDA(cudaStreamWaitEvent(p->tstream, p->gathered[par], 0));
+                    FDG_TRY(fdg_sage_forward(p->model, p->tstream, X, p->nodes[nslot], p->edges[nslot], cnt,
+                                             p->label_seed, p->losses + j, nullptr));
                     if (p->lr != 0.f) {
-                        FDG_TRY(fdg_sage_backward(p->model, xs, p->nodes[nslot], p->edges[nslot], cnt, p->label_seed));
-                        FDG_TRY(fdg_sage_sgd(p->model, xs, p->lr));
+                        FDG_TRY(fdg_sage_backward(p->model, p->tstream, p->nodes[nslot], p->edges[nslot], cnt,
+                                                  p->label_seed));
+                        FDG_TRY(fdg_sage_sgd(p->model, p->tstream, p->lr));
                     }
+                    FDG_CUDA(cudaEventRecord(p->trained[par], p->tstream));
                 }
             } else {
                 const uint32_t par = uint32_t(j & 1);
@@ -522,10 +539,10 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 }
                 FDG_CUDA(cudaEventRecord(p->moved[par], xe));
             }
-            if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j + 1], xe));
+            if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j + 1], tsplit ? xs : xe));
             if (records_host)  // device -> host read of the batch record (counts + checksum)
                 FDG_CUDA(cudaMemcpyAsync(records_host + j, cnt, sizeof(fdg_batch_counts), cudaMemcpyDeviceToHost, xe));
-            if (!p->bm) FDG_CUDA(cudaEventRecord(p->extracted[slot], xs));
+            if (!p->bm) FDG_CUDA(cudaEventRecord(p->extracted[slot], xe));  // the node / edge lists are free
         }
     }
     if (p->bm && !sample_only) {  // drain: release the last batch
@@ -535,11 +552,12 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                            &p->counts[lj].n_nodes, p->cap));
         FDG_CUDA(cudaEventRecord(p->extracted[(n_batches - 1) % p->nslots], p->xstream));
     }
-    for (uint32_t s = 0; s <= S; ++s) {  // join the sampler streams and the second extract stream
-        if (s == S && !p->xstream2) break;
+    for (uint32_t s = 0; s <= S + 1; ++s) {  // join the sampler, second extraction and train streams
+        cudaStream_t js = s < S ? p->sstream[s] : s == S ? p->xstream2 : p->tstream;
+        if (!js) continue;
         cudaEvent_t e;
         FDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        FDG_CUDA(cudaEventRecord(e, s < S ? p->sstream[s] : p->xstream2));
+        FDG_CUDA(cudaEventRecord(e, js));
         FDG_CUDA(cudaStreamWaitEvent(p->xstream, e, 0));
         cudaEventDestroy(e);
     }
@@ -593,6 +611,15 @@ int fdg_pipeline_set_model(fdg_pipeline* p, fdg_sage* m, uint64_t label_seed) {
     if (m && !p->cfg.write_x) return fail(FDG_INVALID_ARG, "pipeline_set_model: the train stage needs X (write_x)");
     p->model = m;
     p->label_seed = label_seed;
+    if (m && !p->tstream) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        FDG_TRY(make_stream(&p->tstream, p->green_x, lo));
+        for (int i = 0; i < 2; ++i) {
+            FDG_CUDA(cudaEventCreateWithFlags(&p->gathered[i], cudaEventDisableTiming));
+            FDG_CUDA(cudaEventCreateWithFlags(&p->trained[i], cudaEventDisableTiming));
+        }
+    }
     return FDG_OK;
 }
 
