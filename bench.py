@@ -369,7 +369,10 @@ def run_ours(args):
     achieved = float(gather_bytes.sum()) / (busy_ms / 1e3) / 1e9
     hbm, hbm_kind = peaks()
     pipe.close()
-    alone = None if frac else _gather_alone(fd, L, topo, fan, seeds_for, rng_of, ids[:3], hbm)
+    try:  # explanatory extra: never let it cost the bench line
+        alone = None if frac else _gather_alone(fd, L, topo, fan, seeds_for, rng_of, ids[:3], hbm)
+    except Exception as e:  # noqa: BLE001
+        alone = {"error": repr(e)}
 
     # ---------------- end to end through the C ABI with host buffers ----------------
     # every step: H2D of the batch's seeds from pinned memory, sample, extract with the
