@@ -290,6 +290,34 @@ def test_buffer_manager_vs_port_random(fd, port, S, lag):
     np.testing.assert_array_equal(got, table[nodes.astype(np.int64)])
 
 
+def test_buffer_manager_eviction_reads_as_reference(fd):
+    """Evicted nodes (mapping entries invalidated lazily on the GPU: the slot is rebound, the
+    old entry is left in place) read exactly as the reference's evicted entries: slot -1,
+    ref 0, invalid; acquiring one again is a miss that reloads its row; validate() holds."""
+    t = fd.Topology.generate(2000, 16, 8, 1)
+    table = t.download_rows(0, 2000)
+    bm = fd.BufferManager(t, 8, max_batch_nodes=8)
+    a = np.arange(0, 4, dtype=np.uint64)
+    b = np.arange(100, 104, dtype=np.uint64)
+    c = np.arange(200, 208, dtype=np.uint64)
+    bm.extract(a)
+    bm.release_batch(a)
+    bm.extract(b)
+    bm.release_batch(b)
+    bm.extract(c)  # 8 misses: evicts a (LRU first) and b
+    for v in list(a) + list(b):
+        assert tuple(bm.mapping_entry(int(v))) == (-1, 0, 0)
+    assert all(bm.mapping_entry(int(v))[0] >= 0 for v in c)
+    s = bm.stats()
+    assert s["evictions"] == 8 and s["loads"] == 16 and s["hits"] == 0
+    bm.validate()
+    bm.release_batch(c)
+    alias, x, _ = bm.extract(a, want_rows=True, checksum=True)  # misses again: reloaded rows
+    assert bm.stats()["hits"] == 0 and bm.stats()["loads"] == 20
+    np.testing.assert_array_equal(x, table[a.astype(np.int64)])
+    bm.validate()
+
+
 def test_buffer_manager_capacity_and_invariants(fd):
     t = fd.Topology.generate(1000, 16, 8, 1)
     with pytest.raises(fd.InvariantViolation):
