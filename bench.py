@@ -422,7 +422,9 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "pipeline_gbs": float(gather_bytes.sum()) / (max_ms / 1e3) / 1e9,
                      "traffic": _traffic(cfg), "peak_kind": hbm_kind,
-                     "kernel": "k_move (buffer manager extract)" if frac else "k_gather16_dyn",
+                     "kernel": ("k_move (buffer-manager row move: misses table -> slot and X, hits slot -> X; "
+                                "its launches timed alone, the metadata chain runs before them on the other "
+                                "stream)") if frac else "k_gather16_dyn",
                      "launch_ms_mean": busy_ms / K, "launch_ms_mean_per_stream": float(ext_ms.mean()),
                      "bytes_per_launch": float(gather_bytes.mean()),
                      "note": "algorithmic bytes = 2 x nodes x row_bytes per launch; launch duration = CUDA "

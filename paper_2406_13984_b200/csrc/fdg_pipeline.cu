@@ -485,7 +485,9 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 continue;
             }
             FDG_TRACE("extract", xs);
-            if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j], xs));
+            // extraction window: the gather (plain), or the row move alone (buffer manager: the
+            // metadata chain runs before it on the other stream)
+            if (extract_ms && !p->bm) FDG_CUDA(cudaEventRecord(p->tev[2 * j], xs));
             const uint32_t* n_dev = &cnt->n_nodes;
             uint64_t* cs = p->cfg.checksum ? &cnt->checksum : nullptr;
             void* X = p->X[j & 1];
@@ -527,7 +529,9 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 // DRAM next to it, and the move overlaps batch j+1's acquire / select / bind.
                 FDG_CUDA(cudaEventRecord(p->bound[par], p->xstream));
                 FDG_CUDA(cudaStreamWaitEvent(xe, p->bound[par], 0));
+                if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j], xe));
                 FDG_TRY(bm_extract_move(p->bm, xe, p->nodes[nslot], n_dev, p->cap, p->alias[par], X, cs, par));
+                if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j + 1], xe));
                 FDG_TRY(bm_status_to(p->bm, xe, &cnt->status));  // e.g. CAPACITY = StandbyTimeout
                 if (train) {  // the trainer consumes X (and the batch's blocks) before they are reused
                     FDG_TRY(fdg_sage_forward(p->model, xe, X, p->nodes[nslot], p->edges[nslot], cnt, p->label_seed,
@@ -539,7 +543,7 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 }
                 FDG_CUDA(cudaEventRecord(p->moved[par], xe));
             }
-            if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j + 1], tsplit ? xs : xe));
+            if (extract_ms && !p->bm) FDG_CUDA(cudaEventRecord(p->tev[2 * j + 1], tsplit ? xs : xe));
             if (records_host)  // device -> host read of the batch record (counts + checksum)
                 FDG_CUDA(cudaMemcpyAsync(records_host + j, cnt, sizeof(fdg_batch_counts), cudaMemcpyDeviceToHost, xe));
             if (!p->bm) FDG_CUDA(cudaEventRecord(p->extracted[slot], xe));  // the node / edge lists are free
