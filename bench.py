@@ -164,6 +164,16 @@ class Dist:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
         return float(t.item())
 
+    def gather(self, x: float) -> list:
+        """x of every rank, in rank order."""
+        if self.world == 1:
+            return [x]
+        import torch
+        t = torch.zeros(self.world, dtype=torch.float64)
+        t[self.rank] = x
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return [float(v) for v in t.tolist()]
+
     def close(self):
         if self.world > 1:
             self.dist.destroy_process_group()
@@ -182,6 +192,40 @@ def counts_dtype():
                      ("bad_seed", "<u8"), ("checksum", "<u8"), ("bad_seed_pos", "<u4"), ("n_layers", "<u4"),
                      ("layer_nodes", "<u4", (MAX_LAYERS + 2,)), ("layer_edges", "<u4", (MAX_LAYERS + 1,)),
                      ("layer_draws", "<u4", (MAX_LAYERS + 1,)), ("words_used", "<u4"), ("pad", "<u4")])
+
+
+EDGES = {"products": 63_177_558, "papers": 1_613_492_860, "papers_bm": 1_613_492_860, "friendster": 1_813_633_279,
+         "mag": 1_720_983_565, "products_host_bm": 63_177_558, "papers_host_bm": 1_613_492_860}
+
+
+def bench_config(cfg, world, layout):
+    """The workload description both arms print as `config` (identical for the same
+    --config / --gpus): what is computed, not how (that goes under "execution")."""
+    n, dim, avg, fan, B, t_ids, dtype, frac = CONFIGS[cfg]
+    rb = dim * (4 if dtype == "f32" else 2)
+    return {"workload": DESCR[cfg], "config": cfg, "nodes": n, "edges": EDGES[cfg], "row_bytes": rb,
+            "fanouts": fan, "batch": B, "global_batch": B * world, "train_ids": t_ids,
+            "parallelism": f"dp{world}" + ({"sharded": " (replicated CSR, feature table row-sharded, remote rows "
+                                                       "over NVLink P2P)",
+                                            "replicas": " (replicated CSR + table)",
+                                            "local": ""}[layout]),
+            "l2_policy": "inputs > L2 (the table and ~0.5 GB of X per batch); no flush",
+            "table_tier": "pinned host memory (mapped)" if cfg in HOST_TIER else "HBM",
+            "buffer_slots": int(n * frac) if frac else None}
+
+
+def host_cpu():
+    """nproc and the lscpu model name of this host."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
 
 
 # ------------------------------------------------------------ reference (CPU) ----
@@ -237,6 +281,9 @@ class RefBuffer:
 
 
 def run_reference_arm(args):
+    """The reference's own CPU implementation (oracle/_ref) on all host threads, timed in
+    whole waves: every timed call runs a multiple of `threads` batches (one batch per
+    thread, and >= 4 waves), so no thread idles through a partial last wave."""
     dist = Dist()
     if dist.rank != 0:  # rank 0 alone runs the CPU reference
         dist.close()
@@ -255,45 +302,77 @@ def run_reference_arm(args):
     order = R.partition_epoch(np.arange(t_ids, dtype=np.uint64), b, R.hash_combine(0, 0))
     nb = t_ids // b
     bm = RefBuffer(n, int(n * frac), dim * (4 if dtype == "f32" else 2)) if frac else None
+    W, K = args.warmup, args.steps
+    # buffer configs extract in batch order through one BufferManager (its mutex serialises
+    # the reference anyway): K batches; otherwise whole waves of `threads` batches.
+    total = K if frac else -(-max(K, 4 * threads) // threads) * threads
     try:
-        W, K = args.warmup, args.steps
-        cpu_reference(cfg, staged, order, np.arange(W) % nb, threads, bm)
-        ids = (W + np.arange(K)) % nb
-        # contiguous runs of batch ids (wrap at the epoch end)
+        cpu_reference(cfg, staged, order, np.arange(min(W, nb)) % nb, threads, bm)
+        ids = (W + np.arange(total)) % nb
         secs, nodes = 0.0, 0
         at = 0
-        while at < K:
-            run = int(min(K - at, nb - ids[at]))
-            s, cs, nc = cpu_reference(cfg, staged, order, ids[at:at + run], threads, bm)
-            secs += s
+        while at < total:
+            run = int(min(total - at, nb - ids[at]))
+            sc, cs, nc = cpu_reference(cfg, staged, order, ids[at:at + run], threads, bm)
+            secs += sc
             nodes += int(nc.sum())
             at += run
     finally:
         shutil.rmtree(staged[0], ignore_errors=True)
         if bm:
             bm.close()
-    value = K / secs
+    value = total / secs
+    cpu = host_cpu()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "batches/s", "n_gpus": args.gpus,
-        "steps": K, "warmup": W, "ms_per_step": 1e3 * secs / K, "higher_is_better": True, "scaling": "weak",
+        "steps": K, "warmup": W, "ms_per_step": 1e3 * secs / total, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (reference generator, seed 7)",
-        "config": {"workload": DESCR[cfg], "threads": threads,
-                   "path": ("graph::sample_khop on threads-1 workers; batches in order through "
-                            "featbuf::BufferManager (acquire, get_standby_slot + bind_slot + row copy per miss, "
-                            "publish_valid, lag-1 release_batch) + trainer_step hash over region[alias] (oracle/_ref)"
-                            if frac else
-                            "graph::sample_khop + per-row extraction copy + trainer_step hash (oracle/_ref)"),
-                   "buffer_slots": int(n * frac) if frac else None,
-                   "mean_nodes_per_batch": nodes / K},
+        "config": bench_config(cfg, args.gpus, "local" if args.gpus == 1 else "replicas"),
+        "execution": {"threads": threads, "cpu": cpu, "batches_timed": total, "batches_per_step": total / K,
+                      "path": ("graph::sample_khop on threads-1 workers; batches in order through "
+                               "featbuf::BufferManager (acquire, get_standby_slot + bind_slot + row copy per miss, "
+                               "publish_valid, lag-1 release_batch) + trainer_step hash over region[alias] (oracle/_ref)"
+                               if frac else
+                               "graph::sample_khop + per-row extraction copy + trainer_step hash (oracle/_ref), one "
+                               "batch per host thread, whole waves"),
+                      "mean_nodes_per_batch": nodes / total},
         "cpu_baseline": {"value": value, "unit": "batches/s", "cores": threads, "kind": "reference",
-                         "sample": f"{K} batches of the epoch-0 partition, "
+                         "cpu_model": cpu["model"],
+                         "sample": f"{total} batches of the epoch-0 partition "
                                    + ("sampled on threads - 1 workers, extracted in order through one "
                                       "reference BufferManager (warm after the warm-up batches)" if frac
-                                      else "one batch per thread")},
+                                      else f"in {total // threads} whole waves of one batch per thread")},
         "e2e": {"value": value, "unit": "batches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.sync_reference:
+        line["sync_reference"] = _sync_reference(cfg, args)
     print(json.dumps(line), flush=True)
     dist.close()
+
+
+def _sync_reference(cfg, args):
+    """BASELINE.md section 2 (iii): the reference PipelineSession::run_sync_reference
+    (pipeline.hpp:261-293) on a dataset written by the reference generator (features.bin
+    included), over a bounded prefix of the epoch's train ids."""
+    import shutil
+
+    import oracle
+    n, dim, avg, fan, b, t_ids, dtype, frac = CONFIGS[cfg]
+    R = oracle.Ref()
+    d = f"/dev/shm/fd_sync_ref_{cfg}_{os.getpid()}"
+    try:
+        t0 = time.time()
+        R.generate_dataset(d, n, dim, avg, GEN_SEED)
+        log(f"[ref] wrote the {cfg} dataset (features.bin included) in {time.time() - t0:.1f}s")
+        ids = np.arange(args.sync_batches * b, dtype=np.uint64)
+        t0 = time.perf_counter()
+        recs, _ = R.run_epoch(d, ids, 0, 0, b, fan, sync=True)
+        secs = time.perf_counter() - t0
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+    return {"value": len(recs) / secs, "unit": "batches/s", "batches": int(len(recs)), "threads": 1,
+            "path": "PipelineSession::run_sync_reference (sample, blocking row reads, trainer checksum, verify on)",
+            "sample": f"train ids 0..{len(ids) - 1} of the {cfg} shape, epoch 0"}
 
 
 # ------------------------------------------------------------------ our arm ----
@@ -304,35 +383,42 @@ def Pipeline(fd, topo, fan, B, bm_slots=None, checksum=False, samplers=6, group=
 
 def run_ours(args):
     import paper_2406_13984_b200 as fd
+    from paper_2406_13984_b200 import dist as fdist
     from paper_2406_13984_b200.featdrive import DeviceBuffer
 
     dist = Dist()
-    if args.config == "mag" and not (args.shard and dist.world >= 3):
-        if dist.rank == 0:
-            print(json.dumps({"metric": METRIC, "config": {"workload": DESCR["mag"]},
-                              "unavailable": "the 375 GB fp16 table needs --shard on >= 3 GPUs (46.9 GB/GPU at 8)"}),
-                  flush=True)
-        dist.close()
-        return
-    from paper_2406_13984_b200 import dist as fdist
     dev = fdist.local_device(dist.local)
     L = fd.featdrive.lib()
     fd.featdrive.check(L.fdg_set_device(dev))
     cfg = args.config
     n, dim, avg, fan, B, t_ids, dtype, frac = CONFIGS[cfg]
+    # North-star layout at N > 1: the table row-sharded over the GPUs, remote rows read by
+    # one-sided P2P loads inside the gather. The buffer-manager and host-tier configs keep
+    # one table per GPU (their miss source is a single table).
+    layout = args.layout
+    if layout == "auto":
+        layout = "sharded" if dist.world > 1 and not frac and cfg not in HOST_TIER else (
+            "replicas" if dist.world > 1 else "local")
+    proxy = cfg == "mag" and dist.world < 3  # the 375 GB fp16 table needs >= 3 GPUs
+    if proxy:
+        layout = "proxy"
     t0 = time.time()
-    shard = args.shard and dist.world > 1
-    topo = fd.Topology.generate(n, dim, avg, GEN_SEED, dtype=dtype, device=dev, features=not shard)
-    sharded = None
-    if shard:  # row-sharded table: own rows generated locally, peers' rows read over NVLink (IPC)
+    topo = fd.Topology.generate(n, dim, avg, GEN_SEED, dtype=dtype, device=dev,
+                                features=layout in ("local", "replicas"))
+    sharded, rps, shard_of = None, None, dist.rank
+    if layout == "sharded":  # own rows generated locally, peers' rows read over NVLink (IPC)
         sharded = fdist.ShardedFeatures(topo, dist.rank, dist.world, GEN_SEED, n, dim, dtype)
+        rps = sharded.rows_per_shard
+    elif layout == "proxy":
+        rps, shard_of = _c4_proxy_table(fd, L, topo, n, dim, dtype, shards=8)
     if cfg in HOST_TIER:
         t1 = time.time()
         topo.features_to_host()
         log(f"[rank {dist.rank}] feature table moved to pinned host memory in {time.time() - t1:.1f}s")
     info = topo.info()
     rb = info.row_bytes
-    log(f"[rank {dist.rank}] generated {cfg} in HBM: {info.num_edges} edges, {rb} B rows, {time.time() - t0:.1f}s")
+    log(f"[rank {dist.rank}] generated {cfg} ({layout}) on GPU {dev}: {info.num_edges} edges, {rb} B rows, "
+        f"{time.time() - t0:.1f}s")
     order = np.concatenate(fd.partition_epoch(np.arange(t_ids, dtype=np.uint64), B, hash_combine(0, 0)))
     nb = t_ids // B
     lo, hi = segment(nb, dist.world, dist.rank)  # this rank's contiguous batch segment
@@ -346,37 +432,22 @@ def run_ours(args):
         return np.ascontiguousarray(np.concatenate([order[g * B:(g + 1) * B] for g in ids_]))
 
     bm_slots = int(n * frac) if frac else None
-    pipe = Pipeline(fd, topo, fan, B, bm_slots=bm_slots, checksum=False, samplers=args.samplers, group=args.group)
-    # ---------------- device-resident timed region ----------------
-    warm_dev = DeviceBuffer.from_array(seeds_for(ids_warm))
-    timed_dev = DeviceBuffer.from_array(seeds_for(ids))
-    pipe.run(warm_dev.ptr, False, rng_of(ids_warm))
-    dist.barrier()
-    ext_ms = np.zeros(K, np.float32)
-    with ClockSampler(dev) as clk:
-        ms = pipe.run(timed_dev.ptr, False, rng_of(ids), extract_ms=ext_ms)
-    dist.barrier()
-    recs = pipe.records(K)
-    xs, xe = pipe.extract_times(K)
-    if np.any(recs["status"] != 0):
-        raise RuntimeError(f"batch status errors in the timed region: {np.unique(recs['status'])}")
-    n_nodes = recs["n_nodes"].astype(np.int64)
-    max_ms = dist.reduce(ms, "max")
-    total = dist.reduce(K, "sum")
-    value = total / (max_ms / 1e3)
+    timed = _timed_run(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist, dev, extract=True)
+    n_nodes, value, max_ms, ext_ms, busy_ms, clk = (timed[k] for k in ("n_nodes", "value", "max_ms", "ext_ms",
+                                                                      "busy_ms", "clocks"))
     gather_bytes = 2 * n_nodes * rb
-    busy_ms = _union_ms(xs, xe)  # time at least one extraction launch is running
     achieved = float(gather_bytes.sum()) / (busy_ms / 1e3) / 1e9
     hbm, hbm_kind = peaks()
-    pipe.close()
     try:  # explanatory extra: never let it cost the bench line
-        alone = None if frac else _gather_alone(fd, L, topo, fan, seeds_for, rng_of, ids[:3], hbm)
+        alone = None if (frac or layout != "local") else _gather_alone(fd, L, topo, fan, seeds_for, rng_of, ids[:3],
+                                                                      hbm)
     except Exception as e:  # noqa: BLE001
         alone = {"error": repr(e)}
 
     # ---------------- end to end through the C ABI with host buffers ----------------
     # every step: H2D of the batch's seeds from pinned memory, sample, extract with the
     # fused trainer checksum, D2H of the batch record (counts + checksum) into pinned memory.
+    # Timed on the host wall clock around the call (enqueue + final synchronisation included).
     e2e = Pipeline(fd, topo, fan, B, bm_slots=bm_slots, checksum=True, samplers=args.samplers, group=args.group)
     csz = counts_dtype().itemsize
     pins = []
@@ -392,39 +463,41 @@ def run_ours(args):
     C.memmove(pw, hw.ctypes.data, hw.nbytes)
     C.memmove(pt, ht.ctypes.data, ht.nbytes)
     rec_w, rec_t = pinned(W * csz), pinned(K * csz)
-    e2e.run(pw, True, rng_of(ids_warm), rec_w)
+    rng_w, rng_t = rng_of(ids_warm), rng_of(ids)
+    e2e.run(pw, True, rng_w, rec_w)
     dist.barrier()
-    e2e_ms = dist.reduce(e2e.run(pt, True, rng_of(ids), rec_t), "max")
+    h0 = time.perf_counter()
+    dev_ms = e2e.run(pt, True, rng_t, rec_t)
+    wall_ms = (time.perf_counter() - h0) * 1e3
+    e2e_ms = dist.reduce(wall_ms, "max")
     dist.barrier()
     host_recs = np.frombuffer((C.c_uint8 * (K * csz)).from_address(rec_t), counts_dtype()).copy()
     e2e.close()
     if np.any(host_recs["status"] != 0):
         raise RuntimeError("e2e batch status errors")
+    total = dist.reduce(K, "sum")
     e2e_value = total / (e2e_ms / 1e3)
     gpu_cs = {int(g): int(c) for g, c in zip(ids, host_recs["checksum"])}
     gpu_nn = {int(g): int(c) for g, c in zip(ids, host_recs["n_nodes"])}
     for p in pins:
         L.fdg_host_free(p)
 
+    kernel = ("k_move (buffer-manager row move: misses table -> slot and X, hits slot -> X; its launches timed "
+              "alone, the metadata chain runs before them on the other stream)") if frac else (
+        "k_gather_rb_dyn<SHARDED> (row groups; remote rows loaded through the peers' IPC mappings)"
+        if layout in ("sharded", "proxy") else "k_gather16_dyn")
     line = {
         "metric": METRIC, "value": value, "unit": "batches/s", "n_gpus": dist.world, "steps": K, "warmup": W,
         "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u64", "data": "synthetic (bit-exact GPU port of the reference generator, seed 7)",
-        "config": {"workload": DESCR[cfg], "config": cfg, "nodes": n, "edges": int(info.num_edges),
-                   "row_bytes": rb, "fanouts": fan, "batch": B, "global_batch": B * dist.world,
-                   "parallelism": (f"dp{dist.world} (replicated CSR, table row-sharded over NVLink P2P)" if shard
-                                   else f"dp{dist.world} (replicated CSR + table)"),
-                   "l2_policy": "inputs > L2 (57 GB table, ~0.5 GB X per batch); no flush",
-                   "table_tier": "pinned host memory (mapped)" if cfg in HOST_TIER else "HBM",
-                   "mean_nodes_per_batch": float(n_nodes.mean()), "samplers": args.samplers,
-                   "buffer_slots": bm_slots},
+        "config": bench_config(cfg, dist.world, "sharded" if layout == "proxy" else layout),
+        "execution": {"layout": layout, "samplers": args.samplers, "group_batches": args.group,
+                      "mean_nodes_per_batch": float(n_nodes.mean()), "gpus_visible": fd.device_count(),
+                      "device_of_rank0": dev},
         "gather_gbs": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "pipeline_gbs": float(gather_bytes.sum()) / (max_ms / 1e3) / 1e9,
-                     "traffic": _traffic(cfg), "peak_kind": hbm_kind,
-                     "kernel": ("k_move (buffer-manager row move: misses table -> slot and X, hits slot -> X; "
-                                "its launches timed alone, the metadata chain runs before them on the other "
-                                "stream)") if frac else "k_gather16_dyn",
+                     "traffic": _traffic(cfg), "peak_kind": hbm_kind, "kernel": kernel,
                      "launch_ms_mean": busy_ms / K, "launch_ms_mean_per_stream": float(ext_ms.mean()),
                      "bytes_per_launch": float(gather_bytes.mean()),
                      "note": "algorithmic bytes = 2 x nodes x row_bytes per launch; launch duration = CUDA "
@@ -432,30 +505,124 @@ def run_ours(args):
                              "run; consecutive gathers alternate between two streams and can overlap, so the "
                              "average launch duration is the union of the launch intervals / launches; "
                              "pipeline_gbs = all gather bytes / whole timed region"},
-        "step_roofline": _step_roofline(cfg, max_ms / K, hbm),
+        "step_roofline": _step_roofline(cfg, max_ms / K, hbm) if layout == "local" else None,
         "gather_alone": alone,
         "gpu_launches": _launch_count(K, len(fan), frac is not None, args.samplers),
         "e2e": {"value": e2e_value, "unit": "batches/s", "h2d_bytes_per_step": B * 8, "d2h_bytes_per_step": csz,
+                "timing": "host wall clock around fdg_pipeline_run (enqueue + final synchronisation), max over ranks",
+                "device_ms": dev_ms, "wall_ms": wall_ms,
                 "includes": "seed H2D, sample, extract, fused trainer checksum, batch-record D2H"},
-        "clocks": clk.summary(),
+        "clocks": clk,
     }
+    if dist.world > 1:
+        line["per_rank_gather_gbs"] = dist.gather(achieved)
+    if layout in ("sharded", "proxy"):
+        line["sharding"] = _shard_stats(fd, topo, fan, seeds_for, rng_of, ids[:3], rps, shard_of, rb,
+                                        max_ms / K, proxy=layout == "proxy")
+    if layout == "proxy":
+        line["unavailable_full"] = ("the 375 GB fp16 MAG240M table needs >= 3 GPUs; this line is the 1-GPU C4 proxy: "
+                                    "the MAG-shaped CSR + one 1/8 fp16 shard, all 8 shard pointers aliasing it, so "
+                                    "the per-GPU sampling and gather bytes are real and remote rows read local HBM")
+        line["value_kind"] = "c4_proxy"
+    if sharded is not None:
+        dist.barrier()  # peers read this rank's shard until every rank is done
+        sharded.close()
+        dist.barrier()
+        if cfg != "mag":  # the same batches with a full table copy per GPU (replicas)
+            fd.featdrive.check(L.fdg_ctx_generate_features(topo.ctx, GEN_SEED, n, dim, 0 if dtype == "f32" else 1, 1))
+            rep = _timed_run(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist, dev,
+                             extract=False)
+            line["replicas"] = {"value": rep["value"], "unit": "batches/s", "ms_per_step": rep["max_ms"] / K,
+                                "layout": "replicated CSR + full table per GPU (no data-path exchange)"}
     if bm_slots:
         line["alias_only"] = _alias_only(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist)
-    if args.train:
+    if args.train and layout == "local":
         line["train_stage"] = _train_stage(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist)
-    if dist.world == 1 and not args.no_cpu_baseline:
+    if args.per_call and layout == "local" and not frac:
+        line["per_call"] = _per_call(fd, topo, fan, B, seeds_for, rng_of, ids)
+    if dist.world == 1 and not args.no_cpu_baseline and layout == "local":
         try:
             line["cpu_baseline"], line["checksum_match_vs_reference"] = _cpu_baseline(cfg, topo, order, args, gpu_cs,
                                                                                     gpu_nn)
+            line["cpu_baseline"]["cpu_model"] = host_cpu()["model"]
         except Exception as e:  # pragma: no cover
             log("cpu baseline failed:", repr(e))
             line["cpu_baseline"] = {"value": None, "error": repr(e)}
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
-    dist.barrier()  # peers' shards stay mapped until every rank is done
-    if sharded:
-        sharded.close()
+    dist.barrier()
     dist.close()
+
+
+def _timed_run(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist, dev, extract):
+    """The device-resident timed region: W warm-up batches, then exactly K batches between
+    barriers, CUDA events on the runner's streams, max over ranks."""
+    from paper_2406_13984_b200.featdrive import DeviceBuffer
+    K = len(ids)
+    pipe = Pipeline(fd, topo, fan, B, bm_slots=bm_slots, checksum=False, samplers=args.samplers, group=args.group)
+    warm_dev = DeviceBuffer.from_array(seeds_for(ids_warm))
+    timed_dev = DeviceBuffer.from_array(seeds_for(ids))
+    pipe.run(warm_dev.ptr, False, rng_of(ids_warm))
+    dist.barrier()
+    ext_ms = np.zeros(K, np.float32)
+    with ClockSampler(dev) as clk:
+        ms = pipe.run(timed_dev.ptr, False, rng_of(ids), extract_ms=ext_ms)
+    dist.barrier()
+    recs = pipe.records(K)
+    xs, xe = pipe.extract_times(K)
+    pipe.close()
+    if np.any(recs["status"] != 0):
+        raise RuntimeError(f"batch status errors in the timed region: {np.unique(recs['status'])}")
+    max_ms = dist.reduce(ms, "max")
+    return {"n_nodes": recs["n_nodes"].astype(np.int64), "max_ms": max_ms,
+            "value": dist.reduce(K, "sum") / (max_ms / 1e3), "ext_ms": ext_ms, "busy_ms": _union_ms(xs, xe),
+            "clocks": clk.summary()}
+
+
+def _c4_proxy_table(fd, L, topo, n, dim, dtype, shards):
+    """C4 on one GPU: shard 0 of the 8-way fp16 table (30.5 M rows x 1536 B = 46.9 GB), installed
+    as all 8 shard bases. Returns (rows_per_shard, this GPU's shard index)."""
+    base = C.c_void_p()
+    dt = 0 if dtype == "f32" else 1
+    fd.featdrive.check(L.fdg_ctx_generate_feature_shard(topo.ctx, GEN_SEED, n, dim, dt, 0, shards, C.byref(base)))
+    rps = -(-n // shards)
+    arr = (C.c_void_p * shards)(*([base.value] * shards))
+    fd.featdrive.check(L.fdg_ctx_set_feature_shards(topo.ctx, C.cast(arr, C.c_void_p), shards, rps, n,
+                                                    dim * (4 if dt == 0 else 2), dt))
+    return rps, 0
+
+
+def _shard_stats(fd, topo, fan, seeds_for, rng_of, ids, rps, shard, rb, ms_per_step, proxy):
+    """Remote-row share of this rank's batches (node lists of 3 timed batches through the
+    host API) and the NVLink-bound time per batch it implies."""
+    remote, total = 0, 0
+    for g, r in zip(ids, rng_of(ids)):
+        nodes = fd.sample_khop(topo, seeds_for([g]), fan, int(r)).nodes.astype(np.int64)
+        remote += int(np.count_nonzero(nodes // rps != shard))
+        total += len(nodes)
+    share = remote / max(total, 1)
+    remote_bytes = share * (total / max(len(ids), 1)) * rb
+    nvl = 900e9  # NVLink 5 per direction per GPU (B200_PROFILING.md)
+    return {"rows_per_shard": int(rps), "remote_row_share": share, "remote_bytes_per_batch": remote_bytes,
+            "nvlink_floor_ms_per_batch": remote_bytes / nvl * 1e3, "ms_per_step": ms_per_step,
+            "note": ("proxy: remote rows are read from the aliased local shard (HBM), so ms_per_step is the "
+                     "sampling + gather cost with remote reads at HBM speed; the NVLink floor is what the remote "
+                     "share costs on 8 B200s" if proxy else
+                     "remote rows are loaded one-sided through CUDA IPC peer mappings (NVLink when the ranks own "
+                     "different GPUs)")}
+
+
+def _per_call(fd, topo, fan, B, seeds_for, rng_of, ids):
+    """The reference's per-batch call shape through the C++-shaped Python mirror: one
+    sample_khop + one gather-with-checksum call per batch, host in and out (no pipelining)."""
+    n = min(len(ids), 20)
+    t0 = time.perf_counter()
+    for g, r in zip(ids[:n], rng_of(ids[:n])):
+        b = fd.sample_khop(topo, seeds_for([g]), fan, int(r))
+        fd.gather(topo, b.nodes, checksum=True)
+    secs = time.perf_counter() - t0
+    return {"value": n / secs, "unit": "batches/s", "batches": n,
+            "path": "sample_khop (host seeds -> host nodes/edges) + gather(checksum) per call, synchronous"}
 
 
 def _alias_only(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist):
@@ -643,6 +810,20 @@ def _cpu_baseline(cfg, topo, order, args, gpu_cs, gpu_nn):
             {"batches_compared": len(compared), "all_equal": bool(equal)})
 
 
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-run this command under
+    torch.distributed.run with N local ranks (rank 0 prints the line)."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    log(f"[bench] spawning {n} ranks: {' '.join(cmd[1:])}")
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -653,14 +834,23 @@ def main():
     ap.add_argument("--samplers", type=int, default=8,
                     help="concurrent sampler streams (measured: Papers flat at 6-10, products 155 -> 132 us/batch from 6 to 8)")
     ap.add_argument("--group", type=int, default=1, help="batches sampled per launch chain")
-    ap.add_argument("--shard", action="store_true",
-                    help="N>1: row-shard the feature table across GPUs (remote rows over NVLink P2P)")
+    ap.add_argument("--layout", default="auto", choices=["auto", "local", "sharded", "replicas"],
+                    help="N>1: 'sharded' (default: table row-sharded, remote rows over NVLink P2P) or 'replicas'")
+    ap.add_argument("--shard", action="store_true", help="alias of --layout sharded")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--train", action="store_true",
                     help="also time sample -> extract -> GraphSAGE forward + loss (key train_stage)")
+    ap.add_argument("--per-call", action="store_true", help="also time the reference-shaped per-call SET loop")
+    ap.add_argument("--sync-reference", action="store_true",
+                    help="--impl reference: also time PipelineSession::run_sync_reference (BASELINE.md 2 iii)")
+    ap.add_argument("--sync-batches", type=int, default=4)
     ap.add_argument("--cpu-batches", type=int, default=0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.shard:
+        args.layout = "sharded"
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     if args.impl == "reference":
         run_reference_arm(args)
     else:

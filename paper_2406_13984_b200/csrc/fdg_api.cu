@@ -130,6 +130,15 @@ int fdg_mem_info(uint64_t* f, uint64_t* t) {
     return FDG_OK;
 }
 
+// Counter pair for one dynamically scheduled launch on this context: a per-context ring on
+// its own device, so launches in flight on different streams (up to kDynRing - 1 later
+// launches) never share a pair and contexts on different devices never touch each other's.
+uint32_t* fdg::dyn_counter(const Ctx& c) {
+    if (!c.dyn_ring) return nullptr;
+    const uint32_t k = __atomic_fetch_add(&c.dyn_next, 1u, __ATOMIC_RELAXED);
+    return c.dyn_ring + 2 * (k % kDynRing);
+}
+
 // ---- context -------------------------------------------------------------------
 int fdg_ctx_create(int device, fdg_ctx** out) {
     FDG_CUDA(cudaSetDevice(device));
@@ -137,7 +146,11 @@ int fdg_ctx_create(int device, fdg_ctx** out) {
     c->device = device;
     cudaError_t e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&c->dyn_ring, 2 * kDynRing * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(c->dyn_ring, 0, 2 * kDynRing * sizeof(uint32_t));
     if (e != cudaSuccess) {
+        if (c->dyn_ring) cudaFree(c->dyn_ring);
+        if (c->stream) cudaStreamDestroy(c->stream);
         delete c;
         return cuda_fail(e, "fdg_ctx_create", __FILE__, __LINE__);
     }
@@ -154,6 +167,7 @@ int fdg_ctx_destroy(fdg_ctx* c) {
     if (c->host_table) cudaFreeHost(c->host_table);
     if (c->shard_table) cudaFree((void*)c->shard_table);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->dyn_ring) cudaFree(c->dyn_ring);
     delete c;
     return FDG_OK;
 }

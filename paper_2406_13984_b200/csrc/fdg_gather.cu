@@ -138,17 +138,6 @@ __global__ void __launch_bounds__(512) k_gather16(const uint64_t* __restrict__ n
 // (the SMs are shared with the samplers' kernels) take less of the work instead
 // of stretching the launch. The last CTA to finish resets the counter pair.
 constexpr int kDynIters = 2;
-constexpr uint32_t kDynRing = 64;
-__device__ uint32_t g_dyn_ctr[2 * kDynRing];
-
-// Counter pair for one dynamically scheduled launch (a ring, so launches in flight
-// on different streams never share one). nullptr on failure.
-uint32_t* dyn_counter() {
-    static uint32_t* ring = nullptr;
-    static std::atomic<uint32_t> next{0};
-    if (!ring && cudaGetSymbolAddress((void**)&ring, g_dyn_ctr) != cudaSuccess) return nullptr;
-    return ring + 2 * (next.fetch_add(1) % kDynRing);
-}
 
 template <bool SHARDED, bool PF64 = false>
 __global__ void __launch_bounds__(512) k_gather16_dyn(const uint64_t* __restrict__ nodes, const uint32_t* n_dev,
@@ -532,11 +521,10 @@ template <int RB, int CH, bool SHARDED, bool ALIAS>
 int launch_hash_rb_one(int blocks, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                        const uint32_t* status, const TableRef& t, char* out, uint64_t* checksum) {
     constexpr int smem = kHpWarps * 32 * HashRbShape<CH>::STRIDE;
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    if (attr.first()) {
         FDG_CUDA(cudaFuncSetAttribute(k_gather_hash_rb<RB, CH, SHARDED, ALIAS>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
     }
     k_gather_hash_rb<RB, CH, SHARDED, ALIAS><<<blocks, kHpWarps * 32, smem, st>>>(nodes, n_dev, n_host, status, t,
                                                                                    out, checksum);
@@ -875,13 +863,12 @@ int launch_hash_ws(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const u
     const uint32_t D = uint32_t(std::min<size_t>(24, kBudget / slot));
     if (D < 4) return fail(FDG_INVALID_ARG, "gather: row too large for the warp-specialised checksum");
     const size_t smem = D * slot;
-    static bool attr[3] = {false, false, false};
+    static PerDeviceOnce attr[3];
     auto kfn = ALIAS ? k_gather_hash_ws<false, true> : (sharded ? k_gather_hash_ws<true, false>
                                                                  : k_gather_hash_ws<false, false>);
     const int which = ALIAS ? 2 : int(sharded);
-    if (!attr[which]) {
+    if (attr[which].first()) {
         FDG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBudget)));
-        attr[which] = true;
     }
     kfn<<<c.sm_count, (kWsCopyWarps + kWsHashWarps) * 32, smem, st>>>(nodes, n_dev, n_host, status, t, out, checksum, D);
     FDG_CUDA(cudaGetLastError());
@@ -1016,14 +1003,14 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
                                                       : g_gather_impl;
     if (sharded && impl == FDG_GATHER_LDG && !checksum) impl = FDG_GATHER_RB_DYN;  // shard once per row group
     if (impl == FDG_GATHER_TMA_WS && launch_gather_ws(c, st, nodes, n_dev, n_host, out, checksum, status,
-                                                      dyn_counter()) == FDG_OK)
+                                                      dyn_counter(c)) == FDG_OK)
         return FDG_OK;
     if (impl == FDG_GATHER_TMA && out &&
         launch_gather_tma(c, st, nodes, n_dev, n_host, out, checksum, status) == FDG_OK)
         return FDG_OK;  // rows that do not suit the TMA paths fall through to the LDG kernels
     if (impl == FDG_GATHER_RB_DYN && !checksum && out) {
-        uint32_t* ctr = dyn_counter();
-        if (!ctr) return cuda_fail(cudaGetLastError(), "cudaGetSymbolAddress(g_dyn_ctr)", __FILE__, __LINE__);
+        uint32_t* ctr = dyn_counter(c);
+        if (!ctr) return fail(FDG_NOT_LOADED, "gather: context has no work-claim counters");
         const uint64_t groups = (n_bound + 31) / 32;
         const int blocks = int(std::max<uint64_t>(1, std::min<uint64_t>((groups + 7) / 8,
                                                                       uint64_t(c.sm_count) * g_rb_ctas_per_sm)));
@@ -1086,11 +1073,10 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
     }
     if (checksum) {
         size_t smem = size_t(kHashWarps) * 32 * hash_stride(c.row_bytes);
-        static bool attr_set[2] = {false, false};
+        static PerDeviceOnce attr_set[2];
         auto kfn = sharded ? k_gather_hash<true> : k_gather_hash<false>;
-        if (!attr_set[sharded]) {
+        if (attr_set[sharded].first()) {
             FDG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            attr_set[sharded] = true;
         }
         if (smem > 200 * 1024) return fail(FDG_INVALID_ARG, "gather: row too large for the fused checksum");
         uint64_t groups = (n_bound + 31) / 32;
@@ -1107,8 +1093,8 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
         uint64_t total = n_bound * cpr;
         int blocks = int(std::min<uint64_t>((total + 511) / 512, uint64_t(c.sm_count) * g_gather_ctas_per_sm));
         if (g_gather_dynamic) {
-            uint32_t* ctr = dyn_counter();
-            if (!ctr) return cuda_fail(cudaGetLastError(), "cudaGetSymbolAddress(g_dyn_ctr)", __FILE__, __LINE__);
+            uint32_t* ctr = dyn_counter(c);
+            if (!ctr) return fail(FDG_NOT_LOADED, "gather: context has no work-claim counters");
             if (sharded)
                 k_gather16_dyn<true><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr,
                                                              static_cast<uint4*>(out), ctr);
@@ -1170,11 +1156,10 @@ int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, con
         return FDG_OK;
     }
     size_t smem = size_t(kHashWarps) * 32 * hash_stride(c.row_bytes);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static PerDeviceOnce attr_set;
+    if (attr_set.first()) {
         FDG_CUDA(cudaFuncSetAttribute(k_gather_hash<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       200 * 1024));
-        attr_set = true;
     }
     if (smem > 200 * 1024) return fail(FDG_INVALID_ARG, "checksum: row too large");
     uint64_t groups = (std::max<uint64_t>(n_host, 1) + 31) / 32;

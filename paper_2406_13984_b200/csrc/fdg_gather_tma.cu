@@ -357,11 +357,10 @@ int launch_gather_ws(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const
     const uint32_t D = uint32_t(std::min<size_t>(32, kSmemBudget / (stage + meta)));
     if (D < H + 2) return FDG_INVALID_ARG;
     const size_t smem = D * (stage + meta);
-    static bool attr[2] = {false, false};
+    static PerDeviceOnce attr[2];
     auto kfn = checksum ? k_gather_ws<true> : k_gather_ws<false>;
-    if (!attr[checksum != nullptr]) {
+    if (attr[checksum != nullptr].first()) {
         FDG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBudget)));
-        attr[checksum != nullptr] = true;
     }
     kfn<<<c.sm_count, (H + 1) * 32, smem, st>>>(nodes, n_dev, n_host, status,
                                                 static_cast<const char*>(c.shard_bases[0]), rb, D,

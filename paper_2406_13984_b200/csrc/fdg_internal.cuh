@@ -60,6 +60,18 @@ __host__ __device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t
     return splitmix64(seed + k * 0x9e3779b97f4a7c15ull);
 }
 
+// ---- once-per-device flags (function attributes are per device) --------------------
+// first() is true the first time it is called with each current device.
+struct PerDeviceOnce {
+    unsigned long long mask = 0;
+    bool first() {
+        int d = 0;
+        cudaGetDevice(&d);
+        const unsigned long long bit = 1ull << (d & 63);
+        return !(__atomic_fetch_or(&mask, bit, __ATOMIC_RELAXED) & bit);
+    }
+};
+
 // ---- context ---------------------------------------------------------------------
 struct Ctx {
     int device = 0;
@@ -80,6 +92,10 @@ struct Ctx {
     const void** shard_table = nullptr;  // device copy of shard_bases
     cudaStream_t stream = nullptr;    // setup stream
     int sm_count = 148;
+    // Work-claim counter pairs of the dynamically scheduled gathers: a ring on this
+    // context's device (a launch takes the next pair; the kernel's last CTA resets it).
+    uint32_t* dyn_ring = nullptr;
+    mutable uint32_t dyn_next = 0;
 };
 
 }  // namespace fdg
@@ -131,6 +147,8 @@ int launch_gather_tma(const Ctx& c, cudaStream_t st, const uint64_t* nodes, cons
 int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, const int64_t* alias,
                           const uint32_t* n_dev, uint64_t n_host, uint64_t* checksum,
                           const uint32_t* status = nullptr);
+constexpr uint32_t kDynRing = 256;  // counter pairs per context
+uint32_t* dyn_counter(const Ctx& c);
 int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
                         uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status,
                         bool pipeline = false);

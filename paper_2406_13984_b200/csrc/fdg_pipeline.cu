@@ -400,19 +400,23 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
     for (uint64_t g = 0; g < sampled_groups; ++g)
         for (uint64_t j = g * G; j < std::min<uint64_t>((g + 1) * G, n_batches); ++j) mine[g % S].push_back(j);
     std::vector<uint64_t> fetched(S, 0);  // batches of mine[s] whose streams were requested
+    std::vector<uint64_t> consumed(S, 0);
+    // The sampler's ring holds 2 * PG streams (sized by the first, full chunk). A chunk is
+    // clipped so that at most 2 * PG streams are outstanding (fetched, not yet consumed):
+    // the slot a new stream takes then always belongs to a batch already sampled, for any
+    // group size G <= PG / 2 (a whole-chunk rule let G = 3, 5, 6, 7 overwrite streams of
+    // the group about to be sampled).
     auto prefetch_upto = [&](uint32_t s, uint64_t upto) -> int {
-        upto = std::min<uint64_t>(upto, mine[s].size());
+        upto = std::min<uint64_t>(std::min<uint64_t>(upto, mine[s].size()), consumed[s] + 2 * uint64_t(PG));
         while (fetched[s] < upto) {
             std::vector<uint64_t> r;
-            for (uint64_t k = fetched[s]; k < std::min<uint64_t>(fetched[s] + PG, mine[s].size()); ++k)
-                r.push_back(rng_seeds[mine[s][k]]);
+            const uint64_t end = std::min<uint64_t>(fetched[s] + PG, upto);
+            for (uint64_t k = fetched[s]; k < end; ++k) r.push_back(rng_seeds[mine[s][k]]);
             FDG_TRY(sampler_prefetch(p->samplers[s], p->mstream[s], r.data(), uint32_t(r.size())));
             fetched[s] += r.size();
         }
         return FDG_OK;
     };
-    for (uint32_t s = 0; s < S; ++s) FDG_TRY(prefetch_upto(s, PG));
-    std::vector<uint64_t> consumed(S, 0);
     // FDG_PROFILE_RANGE=1: bracket the run for ncu range replay (concurrent kernels
     // profiled together: --replay-mode app-range --profile-from-start off)
     static const bool prof_range = std::getenv("FDG_PROFILE_RANGE") != nullptr;
@@ -426,10 +430,15 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
     p->timed_batches = 0;
     p->timed_groups = 0;
     FDG_CUDA(cudaEventCreate(&t1));
-    FDG_CUDA(cudaEventRecord(t0, p->xstream));
-    for (uint32_t s = 0; s < S; ++s) FDG_CUDA(cudaStreamWaitEvent(p->sstream[s], t0, 0));
-    if (p->xstream2) FDG_CUDA(cudaStreamWaitEvent(p->xstream2, t0, 0));
+    // Everything of the run -- the first MT prefetch included -- is ordered after t0.
     auto h0 = std::chrono::steady_clock::now();
+    FDG_CUDA(cudaEventRecord(t0, p->xstream));
+    for (uint32_t s = 0; s < S; ++s) {
+        FDG_CUDA(cudaStreamWaitEvent(p->sstream[s], t0, 0));
+        FDG_CUDA(cudaStreamWaitEvent(p->mstream[s], t0, 0));
+    }
+    if (p->xstream2) FDG_CUDA(cudaStreamWaitEvent(p->xstream2, t0, 0));
+    for (uint32_t s = 0; s < S; ++s) FDG_TRY(prefetch_upto(s, PG));
     for (uint64_t g = 0; g < n_groups; ++g) {
         const uint64_t j0 = g * G, j1 = std::min<uint64_t>(j0 + G, n_batches);
         const uint32_t n = uint32_t(j1 - j0);

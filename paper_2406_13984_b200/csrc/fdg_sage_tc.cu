@@ -547,17 +547,13 @@ int tc_make_map_mn(CUtensorMap* map, const float* base, uint64_t rows, uint32_t 
 
 int tc_wgrad(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tB, float* P, const fdg_batch_counts* cnt,
              int j, int Kin, int N, int Z) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    if (attr.first()) {
         FDG_CUDA(cudaFuncSetAttribute(k_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
-        attr = true;
     }
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    int sms = 0, dev = 0;  // per call: the current device may differ between calls
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int m_tiles = (Kin + kTcBM - 1) / kTcBM, n_tiles = (N + kTcBN - 1) / kTcBN;
     const int items = m_tiles * n_tiles * Z;
     k_wgrad_tc<<<std::min(items, sms), kTcThreads, kTcSmem, st>>>(tA, tB, P, cnt, j, Kin, N, m_tiles, n_tiles, Z);
@@ -568,19 +564,15 @@ int tc_wgrad(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tB, floa
 int tc_gemm(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tBhi, const CUtensorMap& tBlo,
             const float* bias, float* C, const fdg_batch_counts* cnt, int j, uint64_t rows_bound, int N, int npad,
             int K, bool relu) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    if (attr.first()) {
         FDG_CUDA(cudaFuncSetAttribute(k_sgemm_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
         FDG_CUDA(cudaFuncSetAttribute(k_sgemm_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
-        attr = true;
     }
     if (K % 4) return fail(FDG_INVALID_ARG, "tc_gemm: K must be a multiple of 4 (16-byte row stride)");
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    int sms = 0, dev = 0;  // per call: the current device may differ between calls
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int n_tiles = npad / kTcBN;
     const uint64_t tiles = (rows_bound + kTcBM - 1) / kTcBM * uint64_t(n_tiles);
     const uint32_t grid = uint32_t(std::min<uint64_t>(tiles, uint64_t(sms)));  // persistent: one CTA per SM

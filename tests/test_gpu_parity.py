@@ -352,6 +352,30 @@ def test_pipeline_runner_matches_host_api(fd, samplers, group, bm):
         assert int(recs["checksum"][b]) == cs, f"batch {b}"
 
 
+@pytest.mark.parametrize("group", [3, 5, 6, 7])
+def test_pipeline_prefetch_ring_odd_groups(fd, port, group):
+    """Group sizes that do not divide the MT prefetch chunk (16): over 320 batches the ring
+    never recycles a stream of the group about to be sampled, and every batch
+    equals the oracle restatement's sample_khop + trainer checksum."""
+    n, B, fan = 50_000, 64, [5, 3]
+    t = fd.Topology.generate(n, 16, 8, 5)
+    indptr, indices = t.download_topology()
+    table = t.download_rows(0, n)
+    nb = 320
+    order = np.concatenate(fd.partition_epoch(np.arange(nb * B, dtype=np.uint64), B, 77))
+    rng = np.array([fd.batch_seed(0, 0, b) for b in range(nb)], np.uint64)
+    pipe = fd.Pipeline(t, fan, B, checksum=True, samplers=2, group_batches=group)
+    recs = pipe.run_batches(order, rng)
+    pipe.close()
+    assert np.all(recs["status"] == 0)
+    for b in range(0, nb, 7):
+        want = port.sample_khop(indptr, indices, order[b * B:(b + 1) * B], fan, int(rng[b]))
+        assert int(recs["n_nodes"][b]) == len(want["nodes"])
+        assert int(recs["n_edges"][b]) == len(want["edges"])
+        _, cs = port.gather(table, want["nodes"])
+        assert int(recs["checksum"][b]) == cs, f"batch {b}"
+
+
 def test_pipeline_sm_partitions(fd):
     """Option sampler_sms: samplers and extraction on disjoint green-context SM partitions
     give the same batches and checksums as the host API."""
