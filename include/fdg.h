@@ -12,7 +12,8 @@
  * thread-local message is available from fdg_last_error(). Reference exception
  * types map as: std::out_of_range -> FDG_OUT_OF_RANGE, std::invalid_argument ->
  * FDG_INVALID_ARG, InvariantViolation -> FDG_INVARIANT, StandbyTimeout ->
- * FDG_CAPACITY. The C++ shim (include/featdrive_gpu.hpp) rethrows those types.
+ * FDG_CAPACITY, dataset-file std::runtime_error / std::system_error -> FDG_IO_ERROR
+ * (+ fdg_last_errno). The C++ shim (include/featdrive_gpu.hpp) rethrows those types.
  * Asynchronous calls report device-detected errors through fdg_batch_counts.status.
  */
 #ifndef FDG_H
@@ -35,7 +36,9 @@ typedef enum {
     FDG_CAPACITY = 4,     /* standby list / arena exhausted (buffer_manager.hpp:274-279)               */
     FDG_CUDA_ERROR = 5,
     FDG_NOT_LOADED = 6,   /* topology / features not resident yet                                        */
-    FDG_REJECTION = 7     /* internal: Lemire rejection seen, batch re-run exactly (never user visible) */
+    FDG_REJECTION = 7,    /* internal: Lemire rejection seen, batch re-run exactly (never user visible) */
+    FDG_IO_ERROR = 8      /* dataset file missing / malformed: std::runtime_error, or std::system_error when
+                             fdg_last_errno() != 0 (topology.hpp:76-113, feature_file.hpp:27-51, format.hpp:54-64) */
 } fdg_status;
 
 typedef struct fdg_ctx fdg_ctx;         /* device + resident CSC topology + feature table (shards)   */
@@ -76,6 +79,9 @@ typedef struct {
 } fdg_ctx_info;
 
 const char* fdg_last_error(void);
+/* errno of the failed system call behind the last FDG_IO_ERROR on this thread (0: a format
+ * error). The reference throws std::system_error(errno, generic_category(), context) there. */
+int fdg_last_errno(void);
 int fdg_version(void);
 
 /* ---- device plumbing (so callers need no CUDA runtime of their own) ---------- */
@@ -238,8 +244,15 @@ void* fdg_bm_region(fdg_bm* bm);                     /* FeatureRegion base: slot
 /* Introspection for tests (mapping_entry / reverse_mapping, buffer_manager.hpp:420-429). */
 int fdg_bm_entry(fdg_bm* bm, uint64_t node, int64_t* slot, uint32_t* ref, uint32_t* valid);
 int fdg_bm_reverse(fdg_bm* bm, uint64_t slot, int64_t* node);
-/* Full invariant sweep (validate_locked, buffer_manager.hpp:488-515) on device. */
+/* Full invariant sweep (validate_locked, buffer_manager.hpp:488-515) on a host copy. Mapping
+ * entries are invalidated lazily (an entry is live while its slot still names the node); a
+ * buffer manager created with option "bm_eager_invalidate" = 1 clears the previous owner's entry
+ * on every eviction as the reference does (buffer_manager.hpp:284-287), and its validate then
+ * treats any stale entry as a corruption. */
 int fdg_bm_validate(fdg_bm* bm);
+/* Standby-ring geometry for tests: positions [head, tail) of capacity `capacity`, and the number
+ * of tombstone compactions so far. */
+int fdg_bm_ring_info(fdg_bm* bm, uint64_t* head, uint64_t* tail, uint64_t* capacity, uint64_t* compactions);
 
 /* ---- native SET-loop runner: PipelineSession's sampler / extractor / trainer /
  *      releaser stages for one worker = one GPU (pipeline.hpp:325-543) ------------ */

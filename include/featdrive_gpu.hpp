@@ -16,8 +16,9 @@
 //
 // Exceptions: FDG_OUT_OF_RANGE -> std::out_of_range, FDG_INVALID_ARG ->
 // std::invalid_argument, FDG_INVARIANT -> InvariantViolation (std::logic_error),
-// FDG_CAPACITY -> StandbyTimeout (std::runtime_error), anything else ->
-// std::runtime_error. Link with -lfdg (paper_2406_13984_b200/libfdg.so).
+// FDG_CAPACITY -> StandbyTimeout (std::runtime_error), FDG_IO_ERROR -> std::system_error
+// (errno set) or std::runtime_error (dataset format), anything else -> std::runtime_error.
+// Link with -lfdg (paper_2406_13984_b200/libfdg.so).
 #pragma once
 
 #include <algorithm>
@@ -30,6 +31,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <system_error>
 #include <thread>
 #include <vector>
 
@@ -57,6 +59,9 @@ inline void check(int rc) {
         case FDG_INVALID_ARG: throw std::invalid_argument(msg);
         case FDG_INVARIANT: throw InvariantViolation(msg);
         case FDG_CAPACITY: throw StandbyTimeout(msg);
+        case FDG_IO_ERROR:  // dataset files: throw_errno (common.hpp:67-69) or a format runtime_error
+            if (const int e = fdg_last_errno()) throw std::system_error(e, std::generic_category(), msg);
+            throw std::runtime_error(msg);
         default: throw std::runtime_error(msg);
     }
 }

@@ -215,6 +215,9 @@ class Ref:
     def __init__(self, path: str = REF_PATH):
         L = self.lib = C.CDLL(path)
         L.fdref_last_error.restype = C.c_char_p
+        L.fdref_last_error_kind.restype = C.c_int
+        L.fdref_last_errno.restype = C.c_int
+        L.fdref_feature_table_check.restype = C.c_int; L.fdref_feature_table_check.argtypes = [C.c_char_p]
         L.fdref_splitmix64.restype = u64; L.fdref_splitmix64.argtypes = [u64]
         L.fdref_hash_combine.restype = u64; L.fdref_hash_combine.argtypes = [u64, u64]
         L.fdref_hash_bytes64.restype = u64; L.fdref_hash_bytes64.argtypes = [vp, u64]
@@ -267,6 +270,25 @@ class Ref:
 
     def err(self):
         return self.lib.fdref_last_error().decode()
+
+    def err_kind(self):
+        """(category, errno) of the last recorded reference exception: 1 std::system_error,
+        2 std::runtime_error, 3 invalid_argument, 4 out_of_range, 5 logic_error, 9 other."""
+        return int(self.lib.fdref_last_error_kind()), int(self.lib.fdref_last_errno())
+
+    def open_topology(self, dataset_dir):
+        """graph::Topology(dataset_dir): None on success, else (message, category, errno)."""
+        h = self.lib.fdref_topology_open(dataset_dir.encode())
+        if h:
+            self.lib.fdref_topology_close(h)
+            return None
+        return (self.err(),) + self.err_kind()
+
+    def open_feature_table(self, path):
+        """storage::FeatureTable(path): None on success, else (message, category, errno)."""
+        if self.lib.fdref_feature_table_check(path.encode()) == 0:
+            return None
+        return (self.err(),) + self.err_kind()
 
     def check(self, rc):
         if rc:

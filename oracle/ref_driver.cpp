@@ -27,6 +27,8 @@
 #include "featdrive/graph/sampling.hpp"
 #include "featdrive/graph/topology.hpp"
 #include "featdrive/pipeline/pipeline.hpp"
+#include <system_error>
+
 #include "featdrive/storage/feature_file.hpp"
 #include "featdrive/storage/generator.hpp"
 
@@ -35,10 +37,33 @@ using namespace featdrive;
 namespace {
 
 thread_local std::string g_err;
+thread_local int g_kind = 0;  // exception category of the last failure (fdref_last_error_kind)
+thread_local int g_sys_errno = 0;
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
+}
+
+// 1 std::system_error (errno in g_sys_errno), 2 other std::runtime_error, 3 std::invalid_argument,
+// 4 std::out_of_range, 5 other std::logic_error, 9 anything else.
+void record(const std::exception& e) {
+    g_err = e.what();
+    g_sys_errno = 0;
+    if (auto* se = dynamic_cast<const std::system_error*>(&e)) {
+        g_kind = 1;
+        g_sys_errno = se->code().value();
+    } else if (dynamic_cast<const std::runtime_error*>(&e)) {
+        g_kind = 2;
+    } else if (dynamic_cast<const std::invalid_argument*>(&e)) {
+        g_kind = 3;
+    } else if (dynamic_cast<const std::out_of_range*>(&e)) {
+        g_kind = 4;
+    } else if (dynamic_cast<const std::logic_error*>(&e)) {
+        g_kind = 5;
+    } else {
+        g_kind = 9;
+    }
 }
 
 // Map the reference's exception types onto the status codes used by the C ABI.
@@ -75,6 +100,20 @@ struct ExtractHandle {
 extern "C" {
 
 const char* fdref_last_error() { return g_err.c_str(); }
+int fdref_last_error_kind() { return g_kind; }
+int fdref_last_errno() { return g_sys_errno; }
+
+// storage::FeatureTable(path) alone (feature_file.hpp:27-51): 0 on success, else the
+// exception is recorded (fdref_last_error / _kind / _errno).
+int fdref_feature_table_check(const char* path) {
+    try {
+        storage::FeatureTable t(path);
+        return 0;
+    } catch (const std::exception& e) {
+        record(e);
+        return 9;
+    }
+}
 
 uint64_t fdref_splitmix64(uint64_t x) { return splitmix64(x); }
 uint64_t fdref_hash_combine(uint64_t a, uint64_t b) { return hash_combine(a, b); }
@@ -171,7 +210,7 @@ void* fdref_topology_open(const char* dir) {
     try {
         return new graph::Topology(dir);
     } catch (const std::exception& e) {
-        g_err = e.what();
+        record(e);
         return nullptr;
     }
 }
@@ -304,7 +343,7 @@ void* fdref_extractor_open(const char* dir, uint64_t slots, uint64_t min_reserve
         h->extractor = std::make_unique<extract::Extractor>(env, ec);
         return h.release();
     } catch (const std::exception& e) {
-        g_err = e.what();
+        record(e);
         return nullptr;
     }
 }

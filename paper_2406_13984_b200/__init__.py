@@ -5,13 +5,13 @@ this package is its Python mirror of the reference's interface
 (see featdrive.py). Import never falls back to a CPU path.
 """
 from .featdrive import (  # noqa: F401
-    BufferManager, CudaError, DeviceBuffer, Event, Extractor, Fanouts, FeatdriveError, GraphSAGE, InvalidArgument,
+    BufferManager, CudaError, DatasetError, DeviceBuffer, Event, Extractor, Fanouts, FeatdriveError, GraphSAGE, InvalidArgument,
     InvariantViolation, OutOfRange, Pipeline, SampledBatch, Sampler, StandbyTimeout, Stream, Topology, batch_seed,
     device_count, gather, mt_stream, partition_epoch, sample_khop, set_option, trainer_step,
 )
 
 __all__ = [
-    "BufferManager", "CudaError", "DeviceBuffer", "Event", "Extractor", "Fanouts", "FeatdriveError", "GraphSAGE",
+    "BufferManager", "CudaError", "DatasetError", "DeviceBuffer", "Event", "Extractor", "Fanouts", "FeatdriveError", "GraphSAGE",
     "InvalidArgument", "InvariantViolation", "OutOfRange", "Pipeline", "SampledBatch", "Sampler", "StandbyTimeout",
     "Stream", "Topology", "batch_seed", "device_count", "gather", "mt_stream", "partition_epoch",
     "sample_khop", "set_option", "trainer_step",

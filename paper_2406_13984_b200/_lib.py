@@ -46,6 +46,7 @@ class BmStats(C.Structure):
 # name -> (restype, argtypes)
 SIGNATURES = {
     "fdg_last_error": (C.c_char_p, []),
+    "fdg_last_errno": (ci, []),
     "fdg_version": (ci, []),
     "fdg_device_count": (ci, [C.POINTER(ci)]),
     "fdg_set_device": (ci, [ci]),
@@ -109,6 +110,7 @@ SIGNATURES = {
     "fdg_bm_entry": (ci, [vp, u64, C.POINTER(i64), C.POINTER(u32), C.POINTER(u32)]),
     "fdg_bm_reverse": (ci, [vp, u64, C.POINTER(i64)]),
     "fdg_bm_validate": (ci, [vp]),
+    "fdg_bm_ring_info": (ci, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
     "fdg_pipeline_create": (ci, [vp, vp, u32, C.POINTER(PipelineConfig), C.POINTER(vp)]),
     "fdg_pipeline_destroy": (ci, [vp]),
     "fdg_pipeline_run": (ci, [vp, vp, ci, vp, u64, vp, vp, C.POINTER(C.c_float)]),

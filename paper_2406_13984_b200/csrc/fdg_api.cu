@@ -14,11 +14,20 @@
 namespace fdg {
 
 static thread_local std::string g_error;
+static thread_local int g_errno = 0;
 
 void set_error(const std::string& msg) { g_error = msg; }
 int fail(int code, const std::string& msg) {
     g_error = msg;
+    g_errno = 0;
     return code;
+}
+// Dataset-file errors: the reference throws std::runtime_error, or std::system_error (errno,
+// generic_category, context) through throw_errno (common.hpp:67-69) when a call failed.
+int io_fail(const std::string& msg, int err) {
+    fail(FDG_IO_ERROR, msg);
+    g_errno = err;
+    return FDG_IO_ERROR;
 }
 int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
     g_error = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ") in " + what +
@@ -40,35 +49,54 @@ void sampler_capacity(const Sampler* s, uint64_t* max_nodes, uint64_t* max_edges
 
 namespace {
 
-int read_file(const std::string& path, uint64_t offset, uint64_t bytes, void* dst) {
-    int fd = ::open(path.c_str(), O_RDONLY);
-    if (fd < 0) return fail(FDG_INVALID_ARG, "open " + path + ": " + std::strerror(errno));
-    uint64_t got = 0;
-    while (got < bytes) {
-        ssize_t n = ::pread(fd, static_cast<char*>(dst) + got, std::min<uint64_t>(bytes - got, 1ull << 30),
-                            offset + got);
-        if (n <= 0) {
-            ::close(fd);
-            return fail(FDG_INVALID_ARG, "read " + path + " failed");
-        }
-        got += uint64_t(n);
+// An open file descriptor closed on scope exit.
+struct Fd {
+    int fd = -1;
+    ~Fd() {
+        if (fd >= 0) ::close(fd);
     }
-    ::close(fd);
+};
+
+// Opens `path` read-only; `what` is the throw_errno context of the reference ("open " + path).
+int open_file(const std::string& path, const std::string& what, Fd& f, int64_t* size) {
+    f.fd = ::open(path.c_str(), O_RDONLY);
+    if (f.fd < 0) return io_fail(what, errno);
+    struct stat st {};
+    if (::fstat(f.fd, &st) != 0) return io_fail("stat " + path, errno);
+    *size = st.st_size;
     return FDG_OK;
 }
 
-int64_t file_size(const std::string& path) {
-    struct stat st {};
-    if (::stat(path.c_str(), &st) != 0) return -1;
-    return st.st_size;
+int read_at(const Fd& f, const std::string& path, uint64_t offset, uint64_t bytes, void* dst) {
+    uint64_t got = 0;
+    while (got < bytes) {
+        ssize_t n = ::pread(f.fd, static_cast<char*>(dst) + got, std::min<uint64_t>(bytes - got, 1ull << 30),
+                            offset + got);
+        if (n < 0 && errno == EINTR) continue;
+        if (n < 0) return io_fail("read " + path, errno);
+        if (n == 0) return io_fail("read " + path + ": unexpected EOF", 0);
+        got += uint64_t(n);
+    }
+    return FDG_OK;
 }
 
 }  // namespace
+// Counter pair for one dynamically scheduled launch on this context: a per-context ring on
+// its own device, so launches in flight on different streams (up to kDynRing - 1 later
+// launches) never share a pair and contexts on different devices never touch each other's.
+uint32_t* dyn_counter(const Ctx& c) {
+    if (!c.dyn_ring) return nullptr;
+    const uint32_t k = __atomic_fetch_add(&c.dyn_next, 1u, __ATOMIC_RELAXED);
+    return c.dyn_ring + 2 * (k % kDynRing);
+}
+
 }  // namespace fdg
 
 using namespace fdg;
 
 extern "C" {
+
+int fdg_last_errno(void) { return g_errno; }
 
 const char* fdg_last_error(void) { return g_error.c_str(); }
 int fdg_version(void) { return 1; }
@@ -130,15 +158,6 @@ int fdg_mem_info(uint64_t* f, uint64_t* t) {
     return FDG_OK;
 }
 
-// Counter pair for one dynamically scheduled launch on this context: a per-context ring on
-// its own device, so launches in flight on different streams (up to kDynRing - 1 later
-// launches) never share a pair and contexts on different devices never touch each other's.
-uint32_t* fdg::dyn_counter(const Ctx& c) {
-    if (!c.dyn_ring) return nullptr;
-    const uint32_t k = __atomic_fetch_add(&c.dyn_next, 1u, __ATOMIC_RELAXED);
-    return c.dyn_ring + 2 * (k % kDynRing);
-}
-
 // ---- context -------------------------------------------------------------------
 int fdg_ctx_create(int device, fdg_ctx** out) {
     FDG_CUDA(cudaSetDevice(device));
@@ -190,8 +209,7 @@ int fdg_ctx_info_get(const fdg_ctx* c, fdg_ctx_info* o) {
 
 int fdg_ctx_load_topology(fdg_ctx* c, const uint64_t* indptr, uint64_t n, const uint64_t* indices, uint64_t e) {
     // Topology::load_indptr / open_indices validation (topology.hpp:84-113)
-    if (n == 0 && (!indptr || indptr[0] != 0)) return fail(FDG_INVALID_ARG, "indptr file has invalid size");
-    if (indptr[0] != 0) return fail(FDG_INVALID_ARG, "indptr must start at 0");
+    if (!indptr) return fail(FDG_INVALID_ARG, "indptr: null array");
     for (uint64_t i = 0; i < n; ++i)
         if (indptr[i] > indptr[i + 1]) return fail(FDG_INVALID_ARG, "indptr is not non-decreasing");
     if (indptr[n] != e) return fail(FDG_INVALID_ARG, "indices size does not match indptr");
@@ -225,13 +243,25 @@ int fdg_ctx_load_topology(fdg_ctx* c, const uint64_t* indptr, uint64_t n, const 
 }
 
 int fdg_ctx_load_topology_files(fdg_ctx* c, const char* dir) {
-    std::string d(dir);
-    int64_t ps = file_size(d + "/indptr.bin"), is = file_size(d + "/indices.bin");
-    if (ps < 8 || ps % 8) return fail(FDG_INVALID_ARG, "indptr file " + d + "/indptr.bin has invalid size");
-    if (is < 0 || is % 8) return fail(FDG_INVALID_ARG, "indices file has invalid size");
-    std::vector<uint64_t> indptr(uint64_t(ps) / 8), indices(uint64_t(is) / 8);
-    FDG_TRY(read_file(d + "/indptr.bin", 0, uint64_t(ps), indptr.data()));
-    FDG_TRY(read_file(d + "/indices.bin", 0, uint64_t(is), indices.data()));
+    // Topology(dataset_dir): load_indptr then open_indices (topology.hpp:34-38, 76-113), with
+    // the reference's checks, messages and exception categories.
+    const std::string d(dir);
+    const std::string ip = d + "/indptr.bin", ix = d + "/indices.bin";
+    Fd fp;
+    int64_t ps = 0;
+    FDG_TRY(open_file(ip, "open " + ip, fp, &ps));
+    if (ps < int64_t(sizeof(uint64_t)) || ps % 8 != 0) return io_fail("indptr file " + ip + " has invalid size", 0);
+    std::vector<uint64_t> indptr(uint64_t(ps) / 8);
+    FDG_TRY(read_at(fp, ip, 0, uint64_t(ps), indptr.data()));
+    for (size_t i = 0; i + 1 < indptr.size(); ++i)
+        if (indptr[i] > indptr[i + 1]) return io_fail("indptr file " + ip + " is not non-decreasing", 0);
+    Fd fx;
+    int64_t is = 0;
+    FDG_TRY(open_file(ix, "open " + ix, fx, &is));
+    if (uint64_t(is) != indptr.back() * sizeof(uint64_t))
+        return io_fail("indices file " + ix + " size does not match indptr", 0);
+    std::vector<uint64_t> indices(uint64_t(is) / 8);
+    FDG_TRY(read_at(fx, ix, 0, uint64_t(is), indices.data()));
     return fdg_ctx_load_topology(c, indptr.data(), indptr.size() - 1, indices.data(), indices.size());
 }
 
@@ -266,11 +296,16 @@ int fdg_ctx_load_features(fdg_ctx* c, const void* rows, uint64_t n, uint32_t row
     return install_table(c, dev, n, row_bytes, dtype);
 }
 
-int fdg_ctx_load_features_file(fdg_ctx* c, const char* path) {
-    // DatasetHeader decode + validate (format.hpp:33-65, 117-136)
+int fdg_ctx_load_features_file(fdg_ctx* c, const char* path_c) {
+    // storage::FeatureTable(path) (feature_file.hpp:27-51): 64-byte header decoded and
+    // validated like DatasetHeader::validate (format.hpp:54-64), file length checked.
+    const std::string path(path_c);
+    Fd f;
+    int64_t size = 0;
+    FDG_TRY(open_file(path, "open feature file " + path, f, &size));
     unsigned char h[64];
-    FDG_TRY(read_file(path, 0, 64, h));
-    if (std::memcmp(h, "FEATDRV1", 8) != 0) return fail(FDG_INVALID_ARG, "feature file: bad magic");
+    const ssize_t got = ::pread(f.fd, h, sizeof h, 0);
+    if (got != ssize_t(sizeof h)) return io_fail("feature file " + path + ": truncated header", 0);
     uint32_t version, dim, dtype, row_bytes;
     uint64_t n, data_offset;
     std::memcpy(&version, h + 8, 4);
@@ -279,16 +314,42 @@ int fdg_ctx_load_features_file(fdg_ctx* c, const char* path) {
     std::memcpy(&dtype, h + 28, 4);
     std::memcpy(&row_bytes, h + 32, 4);
     std::memcpy(&data_offset, h + 40, 8);
-    if (version != 1) return fail(FDG_INVALID_ARG, "feature file: unsupported version");
-    if (dtype != 0) return fail(FDG_INVALID_ARG, "feature file: unsupported dtype code");
-    if (n == 0 || dim == 0) return fail(FDG_INVALID_ARG, "feature file: empty dataset");
-    if (row_bytes != dim * 4) return fail(FDG_INVALID_ARG, "feature file: row_bytes != dim * 4");
-    if (data_offset % 512 || data_offset < 64) return fail(FDG_INVALID_ARG, "feature file: misaligned data_offset");
-    if (file_size(path) != int64_t(data_offset + n * row_bytes))
-        return fail(FDG_INVALID_ARG, "feature file: length != header-implied");
-    std::vector<char> buf(n * row_bytes);
-    FDG_TRY(read_file(path, data_offset, n * row_bytes, buf.data()));
-    return fdg_ctx_load_features(c, buf.data(), n, row_bytes, 0);
+    if (std::memcmp(h, "FEATDRV1", 8) != 0) return io_fail("feature file: bad magic", 0);
+    if (version != 1) return io_fail("feature file: unsupported version " + std::to_string(version), 0);
+    if (dtype != 0) return io_fail("feature file: unsupported dtype code " + std::to_string(dtype), 0);
+    if (n == 0 || dim == 0) return io_fail("feature file: empty dataset", 0);
+    if (row_bytes != dim * 4) return io_fail("feature file: row_bytes != dim * 4", 0);
+    if (data_offset % 512 != 0 || data_offset < 64) return io_fail("feature file: misaligned data_offset", 0);
+    const uint64_t want = data_offset + n * uint64_t(row_bytes);
+    if (uint64_t(size) != want)
+        return io_fail("feature file " + path + ": length " + std::to_string(size) + " != header-implied " +
+                           std::to_string(want),
+                       0);
+    // rows stream to the device in 256 MB pieces through one pinned bounce buffer
+    cudaSetDevice(c->device);
+    void* dev = nullptr;
+    FDG_CUDA(cudaMalloc(&dev, n * row_bytes));
+    const uint64_t total = n * uint64_t(row_bytes), piece = std::min<uint64_t>(total, 256ull << 20);
+    void* bounce = nullptr;
+    cudaError_t e = cudaMallocHost(&bounce, piece);
+    if (e != cudaSuccess) {
+        cudaFree(dev);
+        return cuda_fail(e, "cudaMallocHost(feature bounce buffer)", __FILE__, __LINE__);
+    }
+    int rc = FDG_OK;
+    for (uint64_t at = 0; at < total && rc == FDG_OK; at += piece) {
+        const uint64_t k = std::min<uint64_t>(piece, total - at);
+        rc = read_at(f, path, data_offset + at, k, bounce);
+        if (rc == FDG_OK && (e = cudaMemcpy(static_cast<char*>(dev) + at, bounce, k, cudaMemcpyHostToDevice)) !=
+                                cudaSuccess)
+            rc = cuda_fail(e, "cudaMemcpy(feature rows)", __FILE__, __LINE__);
+    }
+    cudaFreeHost(bounce);
+    if (rc != FDG_OK) {
+        cudaFree(dev);
+        return rc;
+    }
+    return install_table(c, dev, n, row_bytes, 0);
 }
 
 // Out-of-core tier: move the (single-shard) table to pinned host memory mapped into the
@@ -502,6 +563,10 @@ int fdg_set_option(const char* key, int64_t v) {
         g_bm_overlap = v != 0;
         return FDG_OK;
     }
+    if (k == "bm_eager_invalidate") {  // debug: buffer managers created from now on invalidate eagerly
+        g_bm_eager = v != 0;
+        return FDG_OK;
+    }
     if (k == "sage_gemm") {
         if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, "sage_gemm must be 0 (CUDA cores) or 1 (tensor cores)");
         g_sage_gemm = v;
@@ -561,6 +626,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "hash_chunk") *v = g_hash_chunk;
     else if (k == "sage_gemm") *v = g_sage_gemm;
     else if (k == "bm_overlap") *v = g_bm_overlap;
+    else if (k == "bm_eager_invalidate") *v = g_bm_eager;
     else if (k == "gather_pf64") *v = g_gather_pf64;
     else if (k == "rb_ctas_per_sm") *v = g_rb_ctas_per_sm;
     else if (k == "rb_chunk") *v = g_rb_chunk;

@@ -78,6 +78,7 @@ struct BmState {
     uint32_t ring_sel;     // which ring buffer is current
     uint32_t tile_ctr[4];
     uint64_t new_head;
+    uint64_t compactions;  // k_compact_finish swaps (test introspection)
 };
 
 struct BmDev {
@@ -94,6 +95,7 @@ struct BmDev {
     uint32_t* sel;        // [max_batch] to-load rank -> slot
     uint8_t* is_load[2];  // [max_batch] per batch parity: acquire of batch j+1 may run under the move of j
     uint64_t max_batch;
+    uint32_t eager;       // debug: evictions also clear the previous owner's entry (no stale entries)
 };
 
 // 64-bit packed look-back word: [63:62] state (1 aggregate, 2 inclusive),
@@ -323,6 +325,9 @@ __global__ void k_bind(BmDev B, const uint64_t* nodes, int64_t* alias) {
         if (prev != kNoNode) {  // evict the previous owner (buffer_manager.hpp:281-291): rebinding the
             // slot below is the invalidation -- its mapping entry goes stale
             if (B.ref[slot] != 0) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
+            // eager (debug) mode: the reference's invalidation (buffer_manager.hpp:284-287). prev
+            // cannot be a miss of this batch: its entry is live, so it would have been a hit.
+            if (B.eager) B.map[prev] = Entry{-1, 0u};
             ++ev;
         }
         B.map[node] = Entry{slot, kValid};  // bind + publish
@@ -537,6 +542,7 @@ __global__ void k_compact_finish(BmDev B, uint64_t slack) {
     S->ring_sel ^= 1;
     S->head = 0;
     S->tail = S->new_head;
+    S->compactions += 1;
 }
 
 __global__ void k_status_to(const BmState* S, uint32_t* dst) {
@@ -567,6 +573,7 @@ struct Bm {
     uint64_t slots = 0;
     uint32_t max_batch = 0;
     uint32_t epoch = 1;
+    bool eager = false;             // option bm_eager_invalidate at creation
     cudaStream_t stream = nullptr;  // for stats/validate
 };
 
@@ -580,6 +587,8 @@ int bm_release(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const int64_t*
 }  // namespace fdg
 
 using namespace fdg;
+
+int64_t fdg::g_bm_eager = 0;
 
 namespace {
 
@@ -644,6 +653,8 @@ int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint
     d.is_load[0] = reinterpret_cast<uint8_t*>(a + o_isl);
     d.is_load[1] = reinterpret_cast<uint8_t*>(a + o_isl1);
     d.max_batch = b->max_batch;
+    b->eager = g_bm_eager != 0;
+    d.eager = b->eager ? 1u : 0u;
     FDG_CUDA(cudaMemset(d.st, 0, sizeof(BmState)));
     FDG_CUDA(cudaMemset(d.tiles, 0, tiles * 8));
     BmState h{};
@@ -810,6 +821,17 @@ int fdg_bm_entry(fdg_bm* b, uint64_t node, int64_t* slot, uint32_t* ref, uint32_
     return FDG_OK;
 }
 
+int fdg_bm_ring_info(fdg_bm* b, uint64_t* head, uint64_t* tail, uint64_t* capacity, uint64_t* compactions) {
+    FDG_CUDA(cudaDeviceSynchronize());
+    BmState h;
+    FDG_CUDA(cudaMemcpy(&h, b->d.st, sizeof(h), cudaMemcpyDeviceToHost));
+    if (head) *head = h.head;
+    if (tail) *tail = h.tail;
+    if (capacity) *capacity = b->d.R;
+    if (compactions) *compactions = h.compactions;
+    return FDG_OK;
+}
+
 int fdg_bm_reverse(fdg_bm* b, uint64_t slot, int64_t* node) {
     if (slot >= b->slots) return fail(FDG_OUT_OF_RANGE, "bm_reverse: slot out of range");
     FDG_CUDA(cudaDeviceSynchronize());
@@ -839,8 +861,12 @@ int fdg_bm_validate(fdg_bm* b) {
         rev[s] = meta[s].node;
         pos[s] = meta[s].pos;
     }
-    for (uint64_t v = 0; v < d.N; ++v)  // stale entries (slot rebound since) are the reference's evicted entries
-        if (map[v].slot >= 0 && uint64_t(map[v].slot) < d.S && rev[map[v].slot] != v) map[v] = Entry{-1, 0u};
+    // Lazy invalidation: stale entries (slot rebound since) are the reference's evicted
+    // entries. In eager (debug) mode there are none, so any such entry is a corruption and
+    // fails the bijection check below.
+    if (!b->eager)
+        for (uint64_t v = 0; v < d.N; ++v)
+            if (map[v].slot >= 0 && uint64_t(map[v].slot) < d.S && rev[map[v].slot] != v) map[v] = Entry{-1, 0u};
     std::vector<int32_t> ring(d.R);
     FDG_CUDA(cudaMemcpy(ring.data(), d.ring[h.ring_sel], d.R * 4, cudaMemcpyDeviceToHost));
     std::vector<uint8_t> seen(d.S, 0);

@@ -152,5 +152,6 @@ uint32_t* dyn_counter(const Ctx& c);
 int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
                         uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status,
                         bool pipeline = false);
-extern int64_t g_pipeline_gather_impl;  // gather engine of the pipeline runner (default LDG)
+extern int64_t g_pipeline_gather_impl;
+extern int64_t g_bm_eager;  // buffer manager created in eager-invalidation (debug) mode  // gather engine of the pipeline runner (default LDG)
 }  // namespace fdg

@@ -30,6 +30,7 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
                    uint32_t group);
 void sampler_destroy(Sampler* s);
 int sampler_prefetch(Sampler* s, cudaStream_t st, const uint64_t* rng_seeds, uint32_t n);
+int sampler_reserve_ring(Sampler* s, uint32_t n);
 int sampler_sample_group(Sampler* s, cudaStream_t st, uint32_t n, const uint64_t* const* seeds, const uint32_t* n_seeds,
                          const uint64_t* rng_seeds, uint64_t* const* nodes, uint32_t* const* edges, uint64_t cap,
                          fdg_batch_counts* const* cnt);
@@ -198,6 +199,37 @@ void destroy(fdg_pipeline* p) {
     delete p;
 }
 
+// Per-batch records and timing events for runs of up to n batches, grown geometrically
+// (the pipeline reserves kReserveBatches at creation, so ordinary runs allocate nothing:
+// cudaFree would synchronise the device inside the caller's timed region).
+constexpr uint64_t kReserveBatches = 1024;
+int reserve_batches(fdg_pipeline* p, uint64_t n, bool events) {
+    if (p->counts_cap < n) {
+        const uint64_t cap = std::max<uint64_t>(n, 2 * p->counts_cap);
+        if (p->counts) cudaFree(p->counts);
+        p->counts = nullptr;
+        p->counts_cap = 0;
+        FDG_CUDA(cudaMalloc(&p->counts, cap * sizeof(fdg_batch_counts)));
+        p->counts_cap = cap;
+    }
+    if (!events) return FDG_OK;
+    const uint64_t G = std::max<uint32_t>(p->cfg.group_batches, 1);
+    const uint64_t have = p->tev.size() / 2;
+    if (have >= n) return FDG_OK;
+    const uint64_t want = std::max<uint64_t>(n, 2 * have);
+    for (size_t i = p->tev.size(); i < 2 * want; ++i) {
+        cudaEvent_t e;
+        FDG_CUDA(cudaEventCreate(&e));
+        p->tev.push_back(e);
+    }
+    for (size_t i = p->sev.size(); i < 2 * ((want + G - 1) / G); ++i) {
+        cudaEvent_t e;
+        FDG_CUDA(cudaEventCreate(&e));
+        p->sev.push_back(e);
+    }
+    return FDG_OK;
+}
+
 // Builds everything of `p`; on failure the caller destroys the partial pipeline.
 int pipeline_build(fdg_pipeline* p, fdg_ctx* ctx, const uint32_t* fanouts, uint32_t n_layers,
                    const fdg_pipeline_config* cfg) {
@@ -227,6 +259,8 @@ int pipeline_build(fdg_pipeline* p, fdg_ctx* ctx, const uint32_t* fanouts, uint3
         int rc = sampler_create(ctx, cfg->batch_size, fanouts, n_layers, &s, G);
         if (rc) return rc;
         p->samplers.push_back(s);
+        // the MT prefetch ring (2 chunks) is sized here: a run never allocates or synchronises
+        FDG_TRY(sampler_reserve_ring(s, 2 * p->cfg.prefetch_group));
         cudaStream_t st;
         FDG_TRY(make_stream(&st, p->green_s, prio ? prio_hi : prio_lo));
         p->sstream.push_back(st);
@@ -320,6 +354,7 @@ int pipeline_build(fdg_pipeline* p, fdg_ctx* ctx, const uint32_t* fanouts, uint3
         int rc = fdg_bm_create(ctx, cfg->buffer_slots, 0, uint32_t(p->max_nodes), &p->bm);
         if (rc) return rc;
     }
+    FDG_TRY(reserve_batches(p, kReserveBatches, true));
     return FDG_OK;
 }
 
@@ -364,26 +399,7 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
         return fail(FDG_INVALID_ARG, "pipeline_run: every batch but the last must hold batch_size seeds");
     // seeds of batch j: [j*B, min((j+1)*B, n_seeds_total)) (the last chunk of partition_epoch may be short)
     auto seeds_of = [&](uint64_t j) { return uint32_t(std::min<uint64_t>(B, n_seeds_total - j * B)); };
-    if (p->counts_cap < n_batches) {
-        if (p->counts) cudaFree(p->counts);
-        FDG_CUDA(cudaMalloc(&p->counts, n_batches * sizeof(fdg_batch_counts)));
-        p->counts_cap = n_batches;
-    }
-    if (extract_ms && p->tev.size() < 2 * n_batches) {
-        for (size_t i = p->tev.size(); i < 2 * n_batches; ++i) {
-            cudaEvent_t e;
-            FDG_CUDA(cudaEventCreate(&e));
-            p->tev.push_back(e);
-        }
-    }
-    const uint64_t n_groups_all = (n_batches + G - 1) / G;
-    if (extract_ms && p->sev.size() < 2 * n_groups_all) {
-        for (size_t i = p->sev.size(); i < 2 * n_groups_all; ++i) {
-            cudaEvent_t e;
-            FDG_CUDA(cudaEventCreate(&e));
-            p->sev.push_back(e);
-        }
-    }
+    FDG_TRY(reserve_batches(p, n_batches, extract_ms != nullptr));
     const bool sample_only = p->cfg.flags & FDG_PIPE_SAMPLE_ONLY;
     const bool train = p->model != nullptr && !sample_only;
     if (train && p->losses_cap < n_batches) {

@@ -1136,6 +1136,31 @@ void sampler_destroy(Sampler* s) {
     delete s;
 }
 
+// (Re)allocates the prefetch ring for n streams (synchronises the device: callers size it
+// once, e.g. the pipeline runner at creation, so runs never allocate).
+int sampler_reserve_ring(Sampler* s, uint32_t n) {
+    if (s->ring_n >= n) return FDG_OK;
+    FDG_CUDA(cudaDeviceSynchronize());
+    for (auto ev : s->ring_ready) cudaEventDestroy(ev);
+    for (auto ev : s->ring_done) cudaEventDestroy(ev);
+    if (s->ring_words) cudaFree(s->ring_words);
+    s->ring_words = nullptr;
+    s->ring_n = 0;
+    FDG_CUDA(cudaMalloc(&s->ring_words, uint64_t(n) * s->words_cap * 8));
+    s->ring_n = n;
+    s->ring_seed.assign(n, 0);
+    s->ring_valid.assign(n, false);
+    s->ring_ready.resize(n);
+    s->ring_done.resize(n);
+    for (uint32_t i = 0; i < n; ++i) {
+        FDG_CUDA(cudaEventCreateWithFlags(&s->ring_ready[i], cudaEventDisableTiming));
+        FDG_CUDA(cudaEventCreateWithFlags(&s->ring_done[i], cudaEventDisableTiming));
+        FDG_CUDA(cudaEventRecord(s->ring_done[i], s->host_stream));
+    }
+    s->ring_next = 0;
+    return FDG_OK;
+}
+
 // MT streams of upcoming batches, generated concurrently (one CTA each) in a
 // single launch on `st`; the ring holds 2x the largest prefetch group.
 int sampler_prefetch(Sampler* s, cudaStream_t st, const uint64_t* rng_seeds, uint32_t n) {
@@ -1144,24 +1169,7 @@ int sampler_prefetch(Sampler* s, cudaStream_t st, const uint64_t* rng_seeds, uin
         for (uint32_t at = 0; at < n; at += 32) FDG_TRY(sampler_prefetch(s, st, rng_seeds + at, std::min(32u, n - at)));
         return FDG_OK;
     }
-    if (s->ring_n < 2 * n) {
-        FDG_CUDA(cudaDeviceSynchronize());
-        for (auto ev : s->ring_ready) cudaEventDestroy(ev);
-        for (auto ev : s->ring_done) cudaEventDestroy(ev);
-        if (s->ring_words) cudaFree(s->ring_words);
-        s->ring_n = 2 * n;
-        FDG_CUDA(cudaMalloc(&s->ring_words, uint64_t(s->ring_n) * s->words_cap * 8));
-        s->ring_seed.assign(s->ring_n, 0);
-        s->ring_valid.assign(s->ring_n, false);
-        s->ring_ready.resize(s->ring_n);
-        s->ring_done.resize(s->ring_n);
-        for (uint32_t i = 0; i < s->ring_n; ++i) {
-            FDG_CUDA(cudaEventCreateWithFlags(&s->ring_ready[i], cudaEventDisableTiming));
-            FDG_CUDA(cudaEventCreateWithFlags(&s->ring_done[i], cudaEventDisableTiming));
-            FDG_CUDA(cudaEventRecord(s->ring_done[i], st));
-        }
-        s->ring_next = 0;
-    }
+    if (s->ring_n < 2 * n) FDG_TRY(sampler_reserve_ring(s, 2 * n));
     uint32_t slots[32];
     for (uint32_t k = 0; k < n; ++k) {
         uint32_t slot = (s->ring_next + k) % s->ring_n;

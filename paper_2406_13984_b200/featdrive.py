@@ -26,6 +26,7 @@ runs on the GPU through libfdg.so or raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -58,10 +59,22 @@ class CudaError(FeatdriveError):
     pass
 
 
+class DatasetError(FeatdriveError):
+    """A dataset file is missing or malformed (the reference's std::runtime_error from
+    Topology / FeatureTable / DatasetHeader::validate). `errno` is set (non-zero) where the
+    reference throws std::system_error from a failed system call."""
+
+    def __init__(self, msg: str, errno: int = 0):
+        super().__init__(msg if not errno else f"{msg}: {os.strerror(errno)}")
+        self.errno = errno
+
+
 _ERRORS = {1: OutOfRange, 2: InvalidArgument, 3: InvariantViolation, 4: StandbyTimeout, 5: CudaError}
 
 
 def check(rc: int) -> None:
+    if rc == 8:
+        raise DatasetError(_lib.last_error(), lib().fdg_last_errno())
     if rc != 0:
         raise _ERRORS.get(rc, FeatdriveError)(_lib.last_error() or f"fdg status {rc}")
 
@@ -473,6 +486,12 @@ class BufferManager:
 
     def validate(self):
         check(lib().fdg_bm_validate(self.ptr))
+
+    def ring_info(self) -> dict:
+        """Standby ring positions [head, tail), capacity and tombstone compactions so far."""
+        v = [C.c_uint64() for _ in range(4)]
+        check(lib().fdg_bm_ring_info(self.ptr, *[C.byref(x) for x in v]))
+        return dict(zip(("head", "tail", "capacity", "compactions"), (x.value for x in v)))
 
     def region_slots(self, slots) -> np.ndarray:
         """Bytes of FeatureRegion slots (device_region.hpp:36-44), for tests."""

@@ -290,6 +290,35 @@ def test_buffer_manager_vs_port_random(fd, port, S, lag):
     np.testing.assert_array_equal(got, table[nodes.astype(np.int64)])
 
 
+def test_buffer_manager_eager_invalidation_mode(fd, port):
+    """Debug mode bm_eager_invalidate: evictions clear the previous owner's entry as the
+    reference does, so validate() treats any stale entry as a corruption. Same alias lists
+    and counters as the restatement; validate holds after every batch."""
+    n, S = 20000, 2600
+    t = fd.Topology.generate(n, 32, 8, 1)
+    fd.set_option("bm_eager_invalidate", 1)
+    try:
+        bm = fd.BufferManager(t, S, max_batch_nodes=1300)
+    finally:
+        fd.set_option("bm_eager_invalidate", 0)
+    ob = oracle.PortBufferManager(port, n, S)
+    rs = np.random.RandomState(11)
+    prev = None
+    for it in range(40):
+        nodes = np.unique(np.concatenate([rs.randint(0, 3000, 500), rs.randint(0, n, 700)])).astype(np.uint64)[:1300]
+        rs.shuffle(nodes)
+        np.testing.assert_array_equal(bm.extract(nodes), ob.extract(nodes)[0])
+        if prev is not None:
+            bm.release_batch(prev)
+            ob.release(prev)
+        prev = nodes
+        bm.validate()
+        s = bm.stats()
+        assert [s["hits"], s["loads"], s["evictions"], s["standby_len"]] == [int(v) for v in ob.stats()[[0, 1, 3, 6]]]
+    for v in range(0, n, 37):  # evicted entries read slot -1 directly (no owner check needed)
+        assert tuple(bm.mapping_entry(v)) == tuple(ob.entry(v)), v
+
+
 def test_buffer_manager_eviction_reads_as_reference(fd):
     """Evicted nodes (mapping entries invalidated lazily on the GPU: the slot is rebound, the
     old entry is left in place) read exactly as the reference's evicted entries: slot -1,
