@@ -419,11 +419,20 @@ template <bool ALIAS>
 __global__ void __launch_bounds__(kT) k_release(BmDev B, const uint64_t* nodes, const int64_t* alias,
                                                 const uint32_t* n_dev, uint64_t n_host, uint32_t epoch) {
     __shared__ uint32_t s_warp[kT / 32], s_misc[2], s_tile;
+    __shared__ uint64_t s_tail;
     BmState* S = B.st;
     if (S->status) return;
     const uint64_t n = load_n(n_dev, n_host);
     const uint32_t ntiles = n ? uint32_t((n + kTileN - 1) / kTileN) : 1;
-    if (threadIdx.x == 0) s_tile = atomicAdd(&S->tile_ctr[2], 1u);
+    if (threadIdx.x == 0) {
+        // The ring tail this launch appends at is read BEFORE the tile claim: the CTA of the last
+        // tile advances S->tail once its look-back has seen every other tile's aggregate, i.e.
+        // after every other claim -- a read after the look-back could see the advanced tail
+        // (a race that shifted whole tiles of MRU pushes, found by the Papers-scale parity test).
+        s_tail = *reinterpret_cast<volatile uint64_t*>(&S->tail);
+        __threadfence();
+        s_tile = atomicAdd(&S->tile_ctr[2], 1u);
+    }
     __syncthreads();
     const uint32_t tile = s_tile;
     if (tile >= ntiles) return;
@@ -470,7 +479,7 @@ __global__ void __launch_bounds__(kT) k_release(BmDev B, const uint64_t* nodes, 
     }
     if (bad) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
     uint32_t r = block_rank(B.tiles, tile, mine, epoch, s_warp, s_misc);
-    const uint64_t tail = S->tail;
+    const uint64_t tail = s_tail;
     int32_t* ring = B.ring[S->ring_sel];
 #pragma unroll
     for (int k = 0; k < kI; ++k)
