@@ -563,6 +563,14 @@ int fdg_set_option(const char* key, int64_t v) {
         g_bm_overlap = v != 0;
         return FDG_OK;
     }
+    if (k == "debug_zero_word") {  // (batch << 24) | word position, -1 off (pipeline runs)
+        g_debug_zero_word = v;
+        return FDG_OK;
+    }
+    if (k == "debug_reject_batch") {
+        g_debug_reject_batch = v;
+        return FDG_OK;
+    }
     if (k == "bm_eager_invalidate") {  // debug: buffer managers created from now on invalidate eagerly
         g_bm_eager = v != 0;
         return FDG_OK;
@@ -627,6 +635,8 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "sage_gemm") *v = g_sage_gemm;
     else if (k == "bm_overlap") *v = g_bm_overlap;
     else if (k == "bm_eager_invalidate") *v = g_bm_eager;
+    else if (k == "debug_zero_word") *v = g_debug_zero_word;
+    else if (k == "debug_reject_batch") *v = g_debug_reject_batch;
     else if (k == "gather_pf64") *v = g_gather_pf64;
     else if (k == "rb_ctas_per_sm") *v = g_rb_ctas_per_sm;
     else if (k == "rb_chunk") *v = g_rb_chunk;

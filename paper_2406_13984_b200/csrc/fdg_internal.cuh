@@ -153,5 +153,7 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
                         uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status,
                         bool pipeline = false);
 extern int64_t g_pipeline_gather_impl;
-extern int64_t g_bm_eager;  // buffer manager created in eager-invalidation (debug) mode  // gather engine of the pipeline runner (default LDG)
+extern int64_t g_bm_eager;
+extern int64_t g_debug_zero_word;     // pipeline test hook (option debug_zero_word)
+extern int64_t g_debug_reject_batch;  // pipeline test hook (option debug_reject_batch)  // buffer manager created in eager-invalidation (debug) mode  // gather engine of the pipeline runner (default LDG)
 }  // namespace fdg

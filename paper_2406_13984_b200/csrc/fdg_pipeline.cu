@@ -31,6 +31,8 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
 void sampler_destroy(Sampler* s);
 int sampler_prefetch(Sampler* s, cudaStream_t st, const uint64_t* rng_seeds, uint32_t n);
 int sampler_reserve_ring(Sampler* s, uint32_t n);
+int sampler_debug_zero_word(Sampler* s, cudaStream_t st, uint64_t rng_seed, uint64_t pos);
+void sampler_debug_reject(Sampler* s, int lane);
 int sampler_sample_group(Sampler* s, cudaStream_t st, uint32_t n, const uint64_t* const* seeds, const uint32_t* n_seeds,
                          const uint64_t* rng_seeds, uint64_t* const* nodes, uint32_t* const* edges, uint64_t cap,
                          fdg_batch_counts* const* cnt);
@@ -90,6 +92,8 @@ using namespace fdg;
 
 int64_t fdg::g_bm_overlap = 1;
 int64_t fdg::g_sampler_sms = 0;
+int64_t fdg::g_debug_zero_word = -1;     // (batch of the run << 24) | word position; -1 = off
+int64_t fdg::g_debug_reject_batch = -1;  // batch of the run flagged as rejected; -1 = off
 
 namespace {
 
@@ -486,6 +490,15 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 ed[i] = p->edges[slot];
                 cn[i] = p->counts + j;
             }
+            if (g_debug_zero_word >= 0) {  // test hook: a genuine Lemire rejection in batch jz
+                const uint64_t jz = uint64_t(g_debug_zero_word) >> 24;
+                if (jz >= j0 && jz < j1)
+                    FDG_TRY(sampler_debug_zero_word(p->samplers[s], p->mstream[s], rng_seeds[jz],
+                                                    uint64_t(g_debug_zero_word) & 0xFFFFFFu));
+            }
+            if (g_debug_reject_batch >= 0 && uint64_t(g_debug_reject_batch) >= j0 &&
+                uint64_t(g_debug_reject_batch) < j1)
+                sampler_debug_reject(p->samplers[s], int(uint64_t(g_debug_reject_batch) - j0));
             if (extract_ms) FDG_CUDA(cudaEventRecord(p->sev[2 * g], ss));
             FDG_TRY(sampler_sample_group(p->samplers[s], ss, n, sd, ns, rs, nd, ed, p->cap, cn));
             if (extract_ms) FDG_CUDA(cudaEventRecord(p->sev[2 * g + 1], ss));

@@ -92,6 +92,7 @@ template <> struct HashTab<uint32_t> {
     uint32_t size;
     uint32_t keep;  // evict_last policy on loads / stores
     static constexpr unsigned long long kEmpty = ~0ull;
+    __device__ __forceinline__ void* base() const { return e; }
     __device__ __forceinline__ uint32_t insert(uint32_t key, uint32_t pos) const {
         const unsigned long long want = (uint64_t(key) << 32) | (kPend | pos);
         uint32_t h = hslot(key, size);
@@ -128,6 +129,7 @@ template <> struct HashTab<uint64_t> {
     uint32_t* vals;
     uint32_t size;
     static constexpr unsigned long long kEmpty = ~0ull;
+    __device__ __forceinline__ void* base() const { return keys; }  // keys, then vals, contiguous
     __device__ __forceinline__ uint32_t insert(uint64_t key, uint32_t pos) const {
         uint32_t h = hslot(key, size);
         for (;;) {
@@ -204,9 +206,9 @@ __device__ __forceinline__ uint64_t lemire(const uint64_t* words, uint64_t cap, 
 }
 
 // ---------------------------------------------------------------- k_seeds ----
+// Initialises the batch record and inserts the seeds (one CTA per batch).
 template <typename IdT>
-__global__ void __launch_bounds__(256) k_seeds(const __grid_constant__ Group<IdT> G) {
-    const Work<IdT>& W = G.w[blockIdx.y];
+__device__ __forceinline__ void seeds_body(const Work<IdT>& W) {
     fdg_batch_counts* cnt = W.cnt;
     if (threadIdx.x == 0) {
         cnt->status = 0;
@@ -240,6 +242,11 @@ __global__ void __launch_bounds__(256) k_seeds(const __grid_constant__ Group<IdT
     }
     __syncthreads();
     if (threadIdx.x == 0 && cnt->status == FDG_OUT_OF_RANGE) cnt->bad_seed = W.seeds[cnt->bad_seed_pos];
+}
+
+template <typename IdT>
+__global__ void __launch_bounds__(256) k_seeds(const __grid_constant__ Group<IdT> G) {
+    seeds_body(G.w[blockIdx.y]);
 }
 
 // ----------------------------------------------------------- block scan ----
@@ -337,9 +344,7 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
 // Persistent: a capped number of CTAs claim tiles in order (keeps SM slots free
 // for the concurrently running gather; look-back needs only claim order).
 template <typename IdT, bool SEEDS, bool HAS_NEXT>
-__global__ void __launch_bounds__(kScanThreads) k_intern_s(const __grid_constant__ Group<IdT> G, uint32_t q,
-                                                           uint32_t epoch) {
-    const Work<IdT>& W = G.w[blockIdx.y];
+__device__ __forceinline__ void intern_pass(const Work<IdT>& W, uint32_t q, uint32_t epoch) {
     __shared__ uint32_t s_tile;
     fdg_batch_counts* cnt = W.cnt;
     if (cnt->status) return;
@@ -354,6 +359,12 @@ __global__ void __launch_bounds__(kScanThreads) k_intern_s(const __grid_constant
         intern_tile<IdT, SEEDS, HAS_NEXT>(W, q, epoch, tile, P, ntiles);
         __syncthreads();
     }
+}
+
+template <typename IdT, bool SEEDS, bool HAS_NEXT>
+__global__ void __launch_bounds__(kScanThreads) k_intern_s(const __grid_constant__ Group<IdT> G, uint32_t q,
+                                                           uint32_t epoch) {
+    intern_pass<IdT, SEEDS, HAS_NEXT>(G.w[blockIdx.y], q, epoch);
 }
 
 template <typename IdT, bool SEEDS, bool HAS_NEXT>
@@ -524,8 +535,7 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
 // MODE 1: exact-mode probe (count words consumed per node, no outputs). MODE 2:
 // exact-mode final (offsets re-derived). Writes picks + edge dst; k_insert hashes.
 template <typename IdT, bool SMALLF, int MODE>
-__global__ void __launch_bounds__(256) k_sample(const __grid_constant__ Group<IdT> G, uint32_t l) {
-    const Work<IdT>& W = G.w[blockIdx.y];
+__device__ __forceinline__ void sample_nodes(const Work<IdT>& W, uint32_t l, uint32_t first, uint32_t stride) {
     fdg_batch_counts* cnt = W.cnt;
     if (cnt->status) return;
     const uint32_t fs = cnt->layer_nodes[l];
@@ -534,7 +544,7 @@ __global__ void __launch_bounds__(256) k_sample(const __grid_constant__ Group<Id
     const uint64_t db = cnt->layer_draws[l];
     const uint32_t f = W.fan[l];
     const FrontierBuf fr = W.fr[l & 1];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < F; i += gridDim.x * blockDim.x) {
+    for (uint32_t i = first; i < F; i += stride) {
         const uint64_t start = fr.start[i];
         const uint32_t deg = fr.deg[i];
         const uint32_t e0 = eb + fr.pick_off[i];
@@ -614,17 +624,26 @@ __global__ void __launch_bounds__(256) k_sample(const __grid_constant__ Group<Id
     }
 }
 
+template <typename IdT, bool SMALLF, int MODE>
+__global__ void __launch_bounds__(256) k_sample(const __grid_constant__ Group<IdT> G, uint32_t l) {
+    sample_nodes<IdT, SMALLF, MODE>(G.w[blockIdx.y], l, blockIdx.x * blockDim.x + threadIdx.x,
+                                    gridDim.x * blockDim.x);
+}
+
 // ---------------------------------------------------------------- k_insert ----
 // Thread per pick of layer l (position = pick index within the layer).
 template <typename IdT>
-__global__ void __launch_bounds__(256) k_insert(const __grid_constant__ Group<IdT> G, uint32_t l) {
-    const Work<IdT>& W = G.w[blockIdx.y];
+__device__ __forceinline__ void insert_picks(const Work<IdT>& W, uint32_t l, uint32_t first, uint32_t stride) {
     fdg_batch_counts* cnt = W.cnt;
     if (cnt->status) return;
     const uint32_t eb = cnt->layer_edges[l];
     const uint32_t P = cnt->layer_edges[l + 1] - eb;
-    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x)
-        W.pick_slot[eb + p] = W.tab.insert(W.picks[eb + p], p);
+    for (uint32_t p = first; p < P; p += stride) W.pick_slot[eb + p] = W.tab.insert(W.picks[eb + p], p);
+}
+
+template <typename IdT>
+__global__ void __launch_bounds__(256) k_insert(const __grid_constant__ Group<IdT> G, uint32_t l) {
+    insert_picks(G.w[blockIdx.y], l, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 // ---------------------------------------------------------------- k_expand ----
@@ -695,45 +714,113 @@ __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ Group<Id
     }
 }
 
-// exact mode helper: draw_off = exclusive scan(consumed) over the frontier (single block)
-__global__ void k_rescan_draws(uint32_t* consumed, uint32_t* draw_off, const fdg_batch_counts* cnt, uint32_t l,
-                               uint32_t* changed, uint32_t* total) {
-    __shared__ uint32_t s_carry;
-    __shared__ uint32_t s_warp[32];
+// ---------------------------------------------------------------- k_replay ----
+// In-stream exact re-run of a batch whose fast path saw a Lemire rejection (an extra
+// word consumed by some draw, p ~ 2^-57 per draw, shifting every later word offset;
+// uniform_int_dist.h:257-281, sampling.hpp:113). Launched after every group chain
+// with one 256-thread CTA per batch; it returns at once unless the batch's status is
+// FDG_REJECTION, so nothing downstream (gather, buffer manager, train stage) ever
+// sees a rejected batch and no host synchronisation is needed. When it fires it
+// re-samples the batch from scratch on its CTA: hash cleared, seeds, then per layer
+// the exact word offsets (iterated to a fixed point: probe each node's consumption at
+// its current offset, rescan, repeat until no offset moves -- one extra round per
+// rejection), the thread-per-node sampling at those offsets, hash inserts and the
+// intern pass. Slow (~ms) but exact; the fast path never pays for it.
+
+// Exact draw offsets of layer l on one CTA; sets layer_draws[l+1].
+template <typename IdT, bool SMALLF>
+__device__ void exact_offsets(const Work<IdT>& W, uint32_t l) {
+    __shared__ uint32_t s_warp[8], s_carry, s_changed;
+    fdg_batch_counts* cnt = W.cnt;
     const uint32_t F = cnt->layer_nodes[l + 1] - cnt->layer_nodes[l];
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
+    const FrontierBuf fr = W.fr[l & 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t base = 0; base < F; base += blockDim.x) {
-        uint32_t i = base + threadIdx.x;
-        uint32_t v = i < F ? consumed[i] : 0;
-        uint32_t x = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) s_warp[warp] = x;
+    for (int round = 0;; ++round) {
+        sample_nodes<IdT, SMALLF, 1>(W, l, threadIdx.x, blockDim.x);  // consumed[i] at draw_off[i]
         __syncthreads();
-        if (warp == 0) {
-            uint32_t w = lane < int(blockDim.x / 32) ? s_warp[lane] : 0;
-            uint32_t wx = w;
+        if (threadIdx.x == 0) {
+            s_carry = 0;
+            s_changed = 0;
+        }
+        __syncthreads();
+        for (uint32_t base = 0; base < F; base += blockDim.x) {
+            const uint32_t i = base + threadIdx.x;
+            const uint32_t v = i < F ? W.consumed[i] : 0;
+            uint32_t x = v;
+#pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, wx, o);
-                if (lane >= o) wx += y;
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
             }
-            if (lane < int(blockDim.x / 32)) s_warp[lane] = wx - w;
+            if (lane == 31) s_warp[warp] = x;
+            __syncthreads();
+            if (warp == 0) {
+                const uint32_t w = lane < int(blockDim.x / 32) ? s_warp[lane] : 0;
+                uint32_t wx = w;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, wx, o);
+                    if (lane >= o) wx += y;
+                }
+                if (lane < int(blockDim.x / 32)) s_warp[lane] = wx - w;
+            }
+            __syncthreads();
+            const uint32_t excl = s_carry + s_warp[warp] + x - v;
+            if (i < F && fr.draw_off[i] != excl) {
+                fr.draw_off[i] = excl;
+                s_changed = 1;
+            }
+            __syncthreads();
+            if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
+            __syncthreads();
         }
-        __syncthreads();
-        uint32_t excl = s_carry + s_warp[warp] + x - v;
-        if (i < F) {
-            if (draw_off[i] != excl) *changed = 1;
-            draw_off[i] = excl;
-        }
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
+        if (!s_changed || cnt->status) break;
         __syncthreads();
     }
-    if (threadIdx.x == 0) *total = s_carry;
+    if (threadIdx.x == 0) cnt->layer_draws[l + 1] = cnt->layer_draws[l] + s_carry;
+    __syncthreads();
+}
+
+template <typename IdT, bool SMALLF>
+__global__ void __launch_bounds__(kScanThreads) k_replay(const __grid_constant__ Group<IdT> G, uint32_t epoch0,
+                                                         uint64_t hash_bytes) {
+    const Work<IdT>& W = G.w[blockIdx.y];
+    fdg_batch_counts* cnt = W.cnt;
+    if (*reinterpret_cast<volatile uint32_t*>(&cnt->status) != FDG_REJECTION) return;
+    const uint32_t rejections = cnt->rejections;
+    __syncthreads();
+    // the batch hash back to all-empty (0xFF bytes: key ~0, pending values at their maximum)
+    uint4* h = reinterpret_cast<uint4*>(W.tab.base());
+    for (uint64_t k = threadIdx.x; k < hash_bytes / 16; k += blockDim.x) h[k] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    __threadfence_block();
+    __syncthreads();
+    seeds_body(W);
+    if (W.n_layers) intern_pass<IdT, true, true>(W, 0, epoch0);
+    else intern_pass<IdT, true, false>(W, 0, epoch0);
+    __syncthreads();
+    for (uint32_t l = 0; l < W.n_layers; ++l) {
+        exact_offsets<IdT, SMALLF>(W, l);
+        sample_nodes<IdT, SMALLF, 2>(W, l, threadIdx.x, blockDim.x);
+        __syncthreads();
+        insert_picks(W, l, threadIdx.x, blockDim.x);
+        __threadfence_block();
+        __syncthreads();
+        if (l + 1 < W.n_layers) intern_pass<IdT, false, true>(W, l + 1, epoch0 + 1 + l);
+        else intern_pass<IdT, false, false>(W, l + 1, epoch0 + 1 + l);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) cnt->rejections = rejections ? rejections : 1u;
+}
+
+// Debug hook (option "debug_zero_word"): one word of a prefetched MT stream set to 0, which
+// forces a genuine Lemire rejection for any range that is not a power of two.
+__global__ void k_poke_zero(uint64_t* p) { *p = 0; }
+// Test hook: a batch flagged as rejected without one (the replay must reproduce it).
+__global__ void k_force_reject(fdg_batch_counts* cnt) {
+    if (cnt->status == 0) {
+        cnt->status = FDG_REJECTION;
+        cnt->rejections += 1;
+    }
 }
 
 }  // namespace
@@ -813,6 +900,7 @@ struct Sampler {
     fdg_batch_counts* cnt_buf = nullptr;  // host-API counts
     uint64_t* out_nodes = nullptr;        // host-API outputs
     uint32_t* out_edges = nullptr;
+    int debug_reject = -1;                // test hook: lane of the next group flagged as rejected
 };
 
 }  // namespace fdg
@@ -954,47 +1042,18 @@ int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
             launch_intern<IdT>(s, st, G, n, l + 1, max_seeds, next_epoch(s, n));  // also writes edge src ids
         }
     }
-    FDG_CUDA(cudaGetLastError());
-    return FDG_OK;
-}
-
-// Exact mode (after a Lemire rejection), one batch in lane 0: per layer, iterate
-// probe -> rescan of the per-node word consumption until the draw offsets are
-// self-consistent, then run the sampling pass. Host-synchronising; never taken
-// in practice.
-template <typename IdT>
-int run_batch_exact(Sampler& s, cudaStream_t st, const BatchArgs& a) {
-    Group<IdT> G;
-    G.w[0] = make_work<IdT>(s, s.lanes[0], a);
-    fdg_batch_counts* cnt = a.cnt;
-    FDG_CUDA(cudaMemsetAsync(s.lanes[0].hash, 0xFF, s.hash_bytes, st));
-    k_seeds<IdT><<<dim3(1, 1), 256, 0, st>>>(G);
-    launch_intern<IdT>(s, st, G, 1, 0, a.n_seeds, next_epoch(s, 1));
-    for (uint32_t l = 0; l < s.n_layers; ++l) {
-        for (int it = 0;; ++it) {
-            launch_sample<IdT, 1>(s, st, G, 1, l);
-            FDG_CUDA(cudaMemsetAsync(s.exact_flags, 0, 8, st));
-            k_rescan_draws<<<1, 1024, 0, st>>>(s.lanes[0].consumed, s.lanes[0].fr[l & 1].draw_off, cnt, l,
-                                               s.exact_flags, s.exact_flags + 1);
-            uint32_t h[2];
-            FDG_CUDA(cudaMemcpyAsync(h, s.exact_flags, 8, cudaMemcpyDeviceToHost, st));
-            FDG_CUDA(cudaStreamSynchronize(st));
-            if (!h[0]) {
-                // layer_draws[l+1] = layer_draws[l] + words actually consumed by layer l
-                uint32_t base = 0;
-                FDG_CUDA(cudaMemcpy(&base, &cnt->layer_draws[l], 4, cudaMemcpyDeviceToHost));
-                uint32_t nb = base + h[1];
-                FDG_CUDA(cudaMemcpy(&cnt->layer_draws[l + 1], &nb, 4, cudaMemcpyHostToDevice));
-                break;
-            }
-            if (it > (1 << 20)) return fail(FDG_INVARIANT, "exact mode did not converge");
-        }
-        launch_sample<IdT, 2>(s, st, G, 1, l);
-        launch_insert<IdT>(s, st, G, 1, l);
-        launch_intern<IdT>(s, st, G, 1, l + 1, a.n_seeds, next_epoch(s, 1));  // bases layer_draws[l+2] on [l+1]
+    if (s.debug_reject >= 0 && uint32_t(s.debug_reject) < n) {  // test hook: flag one lane as rejected
+        k_force_reject<<<1, 1, 0, st>>>(a[s.debug_reject].cnt);
+        s.debug_reject = -1;
+    }
+    {
+        FDG_TRACE("replay", st);  // exact re-run of rejected batches (no-op otherwise)
+        const uint32_t e0 = next_epoch(s, n);
+        for (uint32_t l = 0; l < s.n_layers; ++l) next_epoch(s, n);
+        if (s.small_f) k_replay<IdT, true><<<dim3(1, n), kScanThreads, 0, st>>>(G, e0, s.hash_bytes);
+        else k_replay<IdT, false><<<dim3(1, n), kScanThreads, 0, st>>>(G, e0, s.hash_bytes);
     }
     FDG_CUDA(cudaGetLastError());
-    FDG_CUDA(cudaStreamSynchronize(st));
     return FDG_OK;
 }
 
@@ -1002,9 +1061,6 @@ int dispatch_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) 
     return s.ctx->idx_bytes == 4 ? run_group<uint32_t>(s, st, n, a) : run_group<uint64_t>(s, st, n, a);
 }
 
-int dispatch_exact(Sampler& s, cudaStream_t st, const BatchArgs& a) {
-    return s.ctx->idx_bytes == 4 ? run_batch_exact<uint32_t>(s, st, a) : run_batch_exact<uint64_t>(s, st, a);
-}
 
 }  // namespace
 
@@ -1056,7 +1112,7 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
     const uint64_t o_seed = lz; lz += al(uint64_t(max_seeds) * 4);
     const uint64_t o_pick = lz; lz += al(std::max<uint64_t>(s->max_edges, 1) * 4);
     const uint64_t o_rank = lz; lz += al(std::max<uint64_t>(s->max_edges, 1) * 4);
-    const uint64_t o_picks = lz; lz += s->small_f ? 0 : al(std::max<uint64_t>(s->max_edges, 1) * ib);
+    const uint64_t o_picks = lz; lz += al(std::max<uint64_t>(s->max_edges, 1) * ib);  // exact replay (any lane)
     uint64_t o_fr[2];
     for (int b = 0; b < 2; ++b) { o_fr[b] = lz; lz += al(fmaxF * 8) + 3 * al(fmaxF * 4); }
     const uint64_t o_cons = lz; lz += al(fmaxF * 4);
@@ -1087,7 +1143,7 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
         ln.seed_slot = reinterpret_cast<uint32_t*>(a + o_seed);
         ln.pick_slot = reinterpret_cast<uint32_t*>(a + o_pick);
         ln.rank = reinterpret_cast<uint32_t*>(a + o_rank);
-        ln.picks = s->small_f ? nullptr : a + o_picks;
+        ln.picks = a + o_picks;
         for (int b = 0; b < 2; ++b) {
             char* p = a + o_fr[b];
             ln.fr[b].start = reinterpret_cast<uint64_t*>(p);
@@ -1111,10 +1167,6 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
     s->cnt_buf = reinterpret_cast<fdg_batch_counts*>(A + o_cnt);
     e = cudaStreamCreateWithFlags(&s->host_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate", __FILE__, __LINE__);
-    if (s->small_f) {  // exact mode (thread-per-node path) needs the picks array of lane 0
-        e = cudaMalloc(&s->lanes[0].picks, std::max<uint64_t>(s->max_edges, 1) * ib);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(picks)", __FILE__, __LINE__);
-    }
     *out = s;
     return FDG_OK;
 }
@@ -1130,7 +1182,6 @@ void sampler_destroy(Sampler* s) {
     if (s->ring_words) cudaFree(s->ring_words);
     if (s->out_nodes) cudaFree(s->out_nodes);
     if (s->out_edges) cudaFree(s->out_edges);
-    if (s->small_f && !s->lanes.empty() && s->lanes[0].picks) cudaFree(s->lanes[0].picks);
     if (s->arena) cudaFree(s->arena);
     if (s->host_stream) cudaStreamDestroy(s->host_stream);
     delete s;
@@ -1186,6 +1237,23 @@ int sampler_prefetch(Sampler* s, cudaStream_t st, const uint64_t* rng_seeds, uin
     s->ring_next = (s->ring_next + n) % s->ring_n;
     return FDG_OK;
 }
+
+// Test hooks (pipeline options "debug_zero_word" / "debug_reject_batch"): zero word `pos` of
+// the prefetched stream of `rng_seed` (a genuine Lemire rejection), or flag lane `lane` of the
+// next group as rejected. Both are exercised through the in-stream exact replay.
+int sampler_debug_zero_word(Sampler* s, cudaStream_t st, uint64_t rng_seed, uint64_t pos) {
+    if (pos >= s->words_cap) return fail(FDG_INVALID_ARG, "debug_zero_word: position beyond the stream");
+    for (uint32_t r = 0; r < s->ring_n; ++r)
+        if (s->ring_valid[r] && s->ring_seed[r] == rng_seed) {
+            k_poke_zero<<<1, 1, 0, st>>>(s->ring_words + uint64_t(r) * s->words_cap + pos);
+            FDG_CUDA(cudaGetLastError());
+            FDG_CUDA(cudaEventRecord(s->ring_ready[r], st));
+            return FDG_OK;
+        }
+    return fail(FDG_INVALID_ARG, "debug_zero_word: stream not prefetched");
+}
+
+void sampler_debug_reject(Sampler* s, int lane) { s->debug_reject = lane; }
 
 // A group of n <= gmax batches in one launch chain on `st`. MT words come from the
 // prefetch ring when present, else they are generated inline (one CTA per batch).
@@ -1260,18 +1328,10 @@ int sampler_sample_host(Sampler* s, const uint64_t* seeds, uint32_t n_seeds, uin
         if (ext) cudaFree(ext);
         return rc;
     }
-    fdg_batch_counts h;
+    fdg_batch_counts h;  // a rejected batch was already re-run exactly in-stream (k_replay)
     FDG_CUDA(cudaMemcpyAsync(&h, s->cnt_buf, sizeof(h), cudaMemcpyDeviceToHost, st));
     FDG_CUDA(cudaStreamSynchronize(st));
-    if (h.status == FDG_REJECTION) {
-        rc = dispatch_exact(*s, st, a);
-        if (rc == FDG_OK) {
-            FDG_CUDA(cudaMemcpyAsync(&h, s->cnt_buf, sizeof(h), cudaMemcpyDeviceToHost, st));
-            FDG_CUDA(cudaStreamSynchronize(st));
-        }
-    }
     if (ext) cudaFree(ext);
-    if (rc) return rc;
     if (h.status == FDG_CAPACITY) return fail(FDG_CAPACITY, "sample_khop: random word stream exhausted");
     if (h.status == FDG_OUT_OF_RANGE)
         return fail(FDG_OUT_OF_RANGE, "sample_khop: seed " + std::to_string(h.bad_seed) + " out of range");

@@ -405,6 +405,65 @@ def test_pipeline_prefetch_ring_odd_groups(fd, port, group):
         assert int(recs["checksum"][b]) == cs, f"batch {b}"
 
 
+@pytest.mark.parametrize("bm", [False, True])
+@pytest.mark.parametrize("hook", ["zero_word", "flag"])
+def test_pipeline_rejection_replayed_exactly(fd, port, bm, hook):
+    """A Lemire rejection inside the pipelined runner (sampling.hpp:113: the reference always
+    produces the batch) is re-run exactly in-stream by k_replay before anything consumes the
+    batch. Hooks: 'zero_word' zeroes word 3 of batch 5's prefetched MT stream (a genuine
+    rejection: the restatement is run on the same modified stream); 'flag' marks batch 5 as
+    rejected without one. Every record, checksum and the buffer manager's counters equal the
+    restatement's."""
+    n, B, fan, nb, target, pos = 300_000, 256, [10, 5, 5], 12, 5, 3
+    t = fd.Topology.generate(n, 32, 12, 3)
+    ip, ix = t.download_topology()
+    table = t.download_rows(0, n)
+    order = np.concatenate(fd.partition_epoch(np.arange(nb * B, dtype=np.uint64), B, 4321))
+    rng = np.array([fd.batch_seed(0, 0, b) for b in range(nb)], np.uint64)
+    key, val = ("debug_zero_word", (target << 24) | pos) if hook == "zero_word" else ("debug_reject_batch", target)
+    fd.set_option(key, val)
+    try:
+        pipe = fd.Pipeline(t, fan, B, buffer_slots=(200_000 if bm else None), checksum=True, samplers=2)
+        recs = pipe.run_batches(order, rng)
+        st = None
+        if bm:
+            import ctypes as C
+
+            from paper_2406_13984_b200._lib import BmStats
+            s = BmStats()
+            fd.featdrive.check(fd.featdrive.lib().fdg_pipeline_bm_stats(pipe.ptr, C.byref(s)))
+            st = [s.hits, s.loads, s.evictions, s.releases, s.standby_len]
+        pipe.close()
+    finally:
+        fd.set_option(key, -1)
+    assert np.all(recs["status"] == 0)
+    ob = oracle.PortBufferManager(port, n, 200_000) if bm else None
+    prev = None
+    for b in range(nb):
+        seeds = order[b * B:(b + 1) * B]
+        words = None
+        if hook == "zero_word" and b == target:
+            words = fd.mt_stream(int(rng[b]), 400_000)
+            words[pos] = 0
+        o = port.sample_khop(ip, ix, seeds, fan, int(rng[b]), words=words)
+        assert int(recs["n_nodes"][b]) == len(o["nodes"]) and int(recs["n_edges"][b]) == len(o["edges"]), b
+        assert int(recs["checksum"][b]) == port.gather(table, o["nodes"])[1], b
+        if b == target:
+            plain = port.sample_khop(ip, ix, seeds, fan, int(rng[b]))
+            rejected = hook == "flag" or o["words_used"] > plain["words_used"]
+            assert (int(recs["rejections"][b]) >= 1) == rejected
+        else:
+            assert int(recs["rejections"][b]) == 0
+        if bm:
+            ob.extract(o["nodes"])
+            if prev is not None:
+                ob.release(prev)
+            prev = o["nodes"]
+    if bm:
+        ob.release(prev)
+        assert st == [int(v) for v in ob.stats()[[0, 1, 3, 5, 6]]]
+
+
 def test_pipeline_sm_partitions(fd):
     """Option sampler_sms: samplers and extraction on disjoint green-context SM partitions
     give the same batches and checksums as the host API."""
