@@ -250,6 +250,36 @@ int fdg_bm_reverse(fdg_bm* bm, uint64_t slot, int64_t* node);
  * on every eviction as the reference does (buffer_manager.hpp:284-287), and its validate then
  * treats any stale entry as a corruption. */
 int fdg_bm_validate(fdg_bm* bm);
+/* ---- the reference's object split and per-node protocol (the C++ drop-in) ----------
+ * featbuf::BufferManager(BufferConfig) holds no table: a standalone buffer manager has its
+ * metadata on `device`, its FeatureRegion at region_dev (slot_count x row_bytes device bytes
+ * owned by the caller; NULL = allocated here) and gets its miss source from the
+ * storage::FeatureTable an Extractor binds (ExtractorEnv, extractor.hpp:58-66). */
+int fdg_bm_create_standalone(int device, uint64_t num_nodes, uint64_t slot_count, uint32_t row_bytes,
+                             uint64_t min_reserved, uint32_t max_batch_nodes, void* region_dev, fdg_bm** out);
+int fdg_bm_bind_table(fdg_bm* bm, const fdg_ctx* table);
+/* acquire_for_batch (buffer_manager.hpp:241-269): alias_dev[i] = slot of a hit, -1 otherwise;
+ * to_load_dev[0..*n_load_dev) = positions to load, in batch order (device outputs). Misses
+ * take their reference when bound. */
+int fdg_bm_acquire(fdg_bm* bm, void* stream, const uint64_t* nodes_dev, uint64_t n, int64_t* alias_dev,
+                   uint32_t* to_load_dev, uint32_t* n_load_dev);
+/* get_standby_slot x count (274-294): the LRU slots, previous owners evicted, in pop order. */
+int fdg_bm_pop_standby(fdg_bm* bm, void* stream, uint32_t count, int64_t* slots_dev);
+/* bind_slot (297-310) and publish_valid (313-324) for n (node, slot) pairs / nodes. */
+int fdg_bm_bind(fdg_bm* bm, void* stream, const uint64_t* nodes_dev, const int64_t* slots_dev, uint32_t n);
+int fdg_bm_publish(fdg_bm* bm, void* stream, const uint64_t* nodes_dev, uint32_t n);
+/* unwind_bound (372-388) and release_ref (392-400) of one node. */
+int fdg_bm_unwind_bound(fdg_bm* bm, void* stream, uint64_t node);
+int fdg_bm_release_ref(fdg_bm* bm, void* stream, uint64_t node);
+/* The load + transfer of planned misses: table rows -> region slots. */
+int fdg_bm_load_rows(fdg_bm* bm, void* stream, const uint64_t* nodes_dev, const int64_t* slots_dev, uint32_t n);
+/* trainer_step over a FeatureRegion (pipeline.hpp:103-124): *checksum_dev += sum_i
+ * hash_bytes64(region[alias[i]]); and its verify: *first_bad_dev = the smallest i whose
+ * region row differs from the table row of nodes[i] (~0 when all equal). */
+int fdg_region_checksum(void* stream, const void* region_dev, uint32_t row_bytes, const int64_t* alias_dev, uint64_t n,
+                        uint64_t* checksum_dev);
+int fdg_region_verify(const fdg_ctx* table, void* stream, const void* region_dev, const int64_t* alias_dev,
+                      const uint64_t* nodes_dev, uint64_t n, uint64_t* first_bad_dev);
 /* Standby-ring geometry for tests: positions [head, tail) of capacity `capacity`, and the number
  * of tombstone compactions so far. */
 int fdg_bm_ring_info(fdg_bm* bm, uint64_t* head, uint64_t* tail, uint64_t* capacity, uint64_t* compactions);

@@ -572,13 +572,153 @@ __global__ void k_init(BmDev B) {
     }
 }
 
+
+// ---------------------------------------------------------- per-node protocol ----
+// The reference's fine-grained BufferManager calls (buffer_manager.hpp:274-324, 370-409)
+// as batch kernels, for callers that drive the protocol themselves (the C++ drop-in's
+// get_standby_slot / bind_slot / publish_valid / unwind_bound / release_ref). The fused
+// extract path (k_acquire .. k_move) is what the extractor and the runner use.
+
+__global__ void k_set_nload(BmState* S, uint32_t count) {
+    S->n_load = count;
+    S->done = 0;
+    S->new_head = S->head;
+    for (int i = 0; i < 4; ++i) S->tile_ctr[i] = 0;
+}
+
+// get_standby_slot x count: the popped slots (k_select ranked them) lose their previous
+// owner (eviction) and become free, off the standby list.
+__global__ void k_pop(BmDev B, int64_t* slots_out) {
+    BmState* S = B.st;
+    if (S->status) return;
+    const uint32_t L = S->n_load;
+    uint32_t ev = 0;
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < L) {
+        const int32_t slot = B.sel[k];
+        const uint64_t prev = B.slot[slot].node;
+        if (prev != kNoNode) {
+            if (B.ref[slot] != 0) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
+            if (B.eager) B.map[prev] = Entry{-1, 0u};
+            ++ev;
+        }
+        B.slot[slot] = SlotMeta{kNoNode, kUnlisted};
+        slots_out[k] = slot;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+    if ((threadIdx.x & 31) == 0 && ev) atomicAdd((unsigned long long*)&S->evictions, (unsigned long long)ev);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        atomicAdd((unsigned long long*)&S->live, (unsigned long long)(-(long long)L));
+        S->head = S->new_head;
+    }
+}
+
+__device__ __forceinline__ bool entry_live(const BmDev& B, uint64_t node, Entry* out) {
+    const Entry e = B.map[node];
+    *out = e;
+    return e.slot >= 0 && uint64_t(e.slot) < B.S && B.slot[e.slot].node == node;
+}
+
+// bind_slot (297-310): the node takes a free slot, not yet valid; its reference from
+// acquire_for_batch starts counting here.
+__global__ void k_bind_explicit(BmDev B, const uint64_t* nodes, const int64_t* slots, uint32_t n) {
+    BmState* S = B.st;
+    if (S->status) return;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t node = nodes[i];
+    const int64_t slot = slots[i];
+    Entry e;
+    if (node >= B.N || slot < 0 || uint64_t(slot) >= B.S || entry_live(B, node, &e) ||
+        B.slot[slot].node != kNoNode || B.slot[slot].pos != kUnlisted) {
+        atomicExch(&S->status, uint32_t(FDG_INVARIANT));  // FD_CHECKs of bind_slot
+        return;
+    }
+    B.map[node] = Entry{int32_t(slot), 0u};
+    B.slot[slot].node = node;
+    B.ref[slot] = 1;
+}
+
+// publish_valid (313-324)
+__global__ void k_publish(BmDev B, const uint64_t* nodes, uint32_t n) {
+    BmState* S = B.st;
+    if (S->status) return;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Entry e;
+    if (nodes[i] >= B.N || !entry_live(B, nodes[i], &e) || (e.refv & kValid)) {
+        atomicExch(&S->status, uint32_t(FDG_INVARIANT));
+        return;
+    }
+    B.map[nodes[i]].refv = e.refv | kValid;
+}
+
+// unwind_bound (372-388): an unpublished bind is reverted, its slot goes back to the MRU end
+// as free space. release_ref (392-400): one reference dropped without the validity
+// requirement (a published node at 0 goes to the MRU end). One node per launch (the
+// reference's per-node calls), single thread.
+__global__ void k_unwind_or_release(BmDev B, uint64_t node, int unwind) {
+    BmState* S = B.st;
+    if (S->status) return;
+    Entry e;
+    const bool live = node < B.N && entry_live(B, node, &e);
+    int32_t push = -1;
+    if (unwind) {
+        if (!live || (e.refv & kValid)) {
+            atomicExch(&S->status, uint32_t(FDG_INVARIANT));
+            return;
+        }
+        B.slot[e.slot].node = kNoNode;
+        B.map[node] = Entry{-1, 0u};
+        push = e.slot;
+    } else {
+        if (!live) return;  // a miss never bound holds no slot-side reference here
+        const uint32_t r = B.ref[e.slot];
+        if (r == 0) {
+            atomicExch(&S->status, uint32_t(FDG_INVARIANT));  // ref_count decrement below zero
+            return;
+        }
+        if (r == 1 && !(e.refv & kValid)) {  // "unreferenced invalid node with a slot" (467-472)
+            atomicExch(&S->status, uint32_t(FDG_INVARIANT));
+            return;
+        }
+        B.ref[e.slot] = r - 1;
+        if (r == 1) push = e.slot;
+    }
+    if (push >= 0) {
+        const uint64_t p = S->tail;
+        B.ring[S->ring_sel][p % B.R] = push;
+        B.slot[push].pos = p;
+        S->tail = p + 1;
+        S->live += 1;
+        if (S->tail - S->head > B.R) atomicExch(&S->status, uint32_t(FDG_CAPACITY));
+    }
+}
+
+// Explicit loads: table rows -> region slots (the extractor's load + transfer for a plan).
+__global__ void __launch_bounds__(256) k_load_rows(const uint64_t* nodes, const int64_t* slots, uint32_t n,
+                                                   const char* table, char* region, uint32_t rb) {
+    const uint32_t cpr = rb / 16;
+    for (uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; c < uint64_t(n) * cpr;
+         c += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = c / cpr, k = c % cpr;
+        reinterpret_cast<uint4*>(region + uint64_t(slots[i]) * rb)[k] =
+            reinterpret_cast<const uint4*>(table + nodes[i] * rb)[k];
+    }
+}
+
+__global__ void k_copy_nload(const BmState* S, uint32_t* dst) { *dst = S->n_load; }
+
 }  // namespace
 
 struct Bm {
     Ctx* ctx = nullptr;
+    fdg_ctx* own_ctx = nullptr;     // standalone buffer manager: a device-only context of its own
     BmDev d{};
     void* arena = nullptr;
     char* region = nullptr;
+    bool own_region = true;         // false: the region is a caller's FeatureRegion allocation
     uint64_t slots = 0;
     uint32_t max_batch = 0;
     uint32_t epoch = 1;
@@ -609,13 +749,19 @@ int bm_persistent_grid(const Bm* b) { return b->ctx->sm_count * 2; }
 
 extern "C" {
 
-int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint32_t max_batch_nodes, fdg_bm** out) {
+}  // extern "C"
+
+namespace {
+// Buffer manager over `ctx` (the miss source when it holds a table); the region is
+// allocated here unless `region` is given (then owned by the caller).
+int bm_build(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint32_t max_batch_nodes, char* region,
+             fdg_bm** out) {
     if (slot_count == 0) return fail(FDG_INVARIANT, "slot_count must be positive");
     if (slot_count < min_reserved) return fail(FDG_INVARIANT, "feature buffer smaller than the N_e * M_b reservation");
     if (slot_count >= uint64_t(INT32_MAX)) return fail(FDG_INVALID_ARG, "slot_count must be < 2^31");
     if (ctx->row_bytes == 0) return fail(FDG_NOT_LOADED, "buffer manager needs a feature table");
     if (ctx->row_bytes % 16) return fail(FDG_INVALID_ARG, "buffer manager: row_bytes must be a multiple of 16");
-    if (ctx->n_shards != 1) return fail(FDG_INVALID_ARG, "buffer manager: sharded tables not supported yet");
+    if (ctx->n_shards > 1) return fail(FDG_INVALID_ARG, "buffer manager: sharded tables not supported yet");
     cudaSetDevice(ctx->device);
     auto b = new fdg_bm();
     b->ctx = ctx;
@@ -638,7 +784,9 @@ int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint
     const uint64_t o_isl = sz; sz += al(uint64_t(b->max_batch));
     const uint64_t o_isl1 = sz; sz += al(uint64_t(b->max_batch));
     cudaError_t e = cudaMalloc(&b->arena, sz);
-    if (e == cudaSuccess) e = cudaMalloc((void**)&b->region, slot_count * ctx->row_bytes);
+    b->own_region = region == nullptr;
+    b->region = region;
+    if (e == cudaSuccess && !region) e = cudaMalloc((void**)&b->region, slot_count * ctx->row_bytes);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         if (b->arena) cudaFree(b->arena);
@@ -677,13 +825,54 @@ int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint
     *out = b;
     return FDG_OK;
 }
+}  // namespace
+
+extern "C" {
+
+int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint32_t max_batch_nodes, fdg_bm** out) {
+    return bm_build(ctx, slot_count, min_reserved, max_batch_nodes, nullptr, out);
+}
+
+int fdg_bm_create_standalone(int device, uint64_t num_nodes, uint64_t slot_count, uint32_t row_bytes,
+                             uint64_t min_reserved, uint32_t max_batch_nodes, void* region_dev, fdg_bm** out) {
+    if (num_nodes == 0) return fail(FDG_INVALID_ARG, "buffer manager: num_nodes must be positive");
+    fdg_ctx* c = nullptr;
+    FDG_TRY(fdg_ctx_create(device, &c));
+    c->num_nodes = num_nodes;
+    c->feat_nodes = num_nodes;
+    c->row_bytes = row_bytes;
+    c->n_shards = 0;  // no miss source until fdg_bm_bind_table
+    const int rc = bm_build(c, slot_count, min_reserved, max_batch_nodes, static_cast<char*>(region_dev), out);
+    if (rc != FDG_OK) {
+        fdg_ctx_destroy(c);
+        return rc;
+    }
+    (*out)->own_ctx = c;
+    return FDG_OK;
+}
+
+int fdg_bm_bind_table(fdg_bm* b, const fdg_ctx* table) {
+    if (!b->own_ctx) return fail(FDG_INVALID_ARG, "bm_bind_table: only a standalone buffer manager takes a table");
+    if (table->shard_bases.empty() || table->n_shards != 1)
+        return fail(FDG_NOT_LOADED, "bm_bind_table: the table context holds no single-shard feature table");
+    if (table->row_bytes != b->own_ctx->row_bytes || table->feat_nodes != b->d.N)
+        return fail(FDG_INVALID_ARG, "bm_bind_table: table shape differs from the buffer config (row_bytes / num_nodes)");
+    if (table->device != b->own_ctx->device) return fail(FDG_INVALID_ARG, "bm_bind_table: table on another device");
+    fdg_ctx* c = b->own_ctx;
+    c->shard_bases = table->shard_bases;
+    c->n_shards = 1;
+    c->rows_per_shard = table->rows_per_shard;
+    c->dtype = table->dtype;
+    return FDG_OK;
+}
 
 int fdg_bm_destroy(fdg_bm* b) {
     if (!b) return FDG_OK;
     cudaSetDevice(b->ctx->device);
     cudaFree(b->arena);
-    cudaFree(b->region);
+    if (b->own_region) cudaFree(b->region);
     cudaStreamDestroy(b->stream);
+    if (b->own_ctx) fdg_ctx_destroy(b->own_ctx);
     delete b;
     return FDG_OK;
 }
@@ -723,6 +912,8 @@ int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
                     const int64_t* alias, void* out, uint64_t* checksum, uint32_t parity) {
     const BmDev& d = b->d;
     const uint32_t rb = b->ctx->row_bytes;
+    if (b->ctx->shard_bases.empty())
+        return fail(FDG_NOT_LOADED, "bm_extract: no feature table bound (fdg_bm_bind_table)");
     const char* table = static_cast<const char*>(b->ctx->shard_bases[0]);
     const uint64_t chunks = n_host * (rb / 16);
     const int blocks =
@@ -904,6 +1095,77 @@ int fdg_bm_validate(fdg_bm* b) {
         }
         if (map[rev[s]].slot != int32_t(s)) return fail(FDG_INVARIANT, "reverse mapping points at node without matching slot");
     }
+    return FDG_OK;
+}
+
+}  // extern "C"
+
+// ---- the reference's per-node protocol (C++ drop-in), stream-ordered ---------------
+extern "C" {
+
+int fdg_bm_acquire(fdg_bm* b, void* stv, const uint64_t* nodes_dev, uint64_t n, int64_t* alias_dev,
+                   uint32_t* to_load_dev, uint32_t* n_load_dev) {
+    cudaStream_t st = (cudaStream_t)stv;
+    if (n > b->max_batch) return fail(FDG_INVALID_ARG, "bm_acquire: batch larger than max_batch_nodes");
+    const BmDev& d = b->d;
+    k_reset_ctrs<<<1, 32, 0, st>>>(d.st);
+    k_acquire<<<n_tiles_for(n), kT, 0, st>>>(d, nodes_dev, nullptr, n, alias_dev, d.is_load[0], b->epoch++);
+    FDG_CUDA(cudaGetLastError());
+    if (to_load_dev && n) FDG_CUDA(cudaMemcpyAsync(to_load_dev, d.load_pos, n * 4, cudaMemcpyDeviceToDevice, st));
+    if (n_load_dev) {
+        k_copy_nload<<<1, 1, 0, st>>>(d.st, n_load_dev);
+        FDG_CUDA(cudaGetLastError());
+    }
+    return FDG_OK;
+}
+
+int fdg_bm_pop_standby(fdg_bm* b, void* stv, uint32_t count, int64_t* slots_dev) {
+    cudaStream_t st = (cudaStream_t)stv;
+    if (count == 0) return FDG_OK;
+    if (count > b->max_batch) return fail(FDG_INVALID_ARG, "bm_pop_standby: more slots than max_batch_nodes");
+    const BmDev& d = b->d;
+    k_set_nload<<<1, 1, 0, st>>>(d.st, count);
+    k_select<<<bm_persistent_grid(b), kT, 0, st>>>(d, b->epoch++);
+    k_pop<<<(count + 255) / 256, 256, 0, st>>>(d, slots_dev);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
+int fdg_bm_bind(fdg_bm* b, void* stv, const uint64_t* nodes_dev, const int64_t* slots_dev, uint32_t n) {
+    if (n == 0) return FDG_OK;
+    k_bind_explicit<<<(n + 255) / 256, 256, 0, (cudaStream_t)stv>>>(b->d, nodes_dev, slots_dev, n);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
+int fdg_bm_publish(fdg_bm* b, void* stv, const uint64_t* nodes_dev, uint32_t n) {
+    if (n == 0) return FDG_OK;
+    k_publish<<<(n + 255) / 256, 256, 0, (cudaStream_t)stv>>>(b->d, nodes_dev, n);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
+int fdg_bm_unwind_bound(fdg_bm* b, void* stv, uint64_t node) {
+    k_unwind_or_release<<<1, 1, 0, (cudaStream_t)stv>>>(b->d, node, 1);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
+int fdg_bm_release_ref(fdg_bm* b, void* stv, uint64_t node) {
+    k_unwind_or_release<<<1, 1, 0, (cudaStream_t)stv>>>(b->d, node, 0);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
+int fdg_bm_load_rows(fdg_bm* b, void* stv, const uint64_t* nodes_dev, const int64_t* slots_dev, uint32_t n) {
+    if (n == 0) return FDG_OK;
+    if (b->ctx->shard_bases.empty()) return fail(FDG_NOT_LOADED, "bm_load_rows: no feature table bound");
+    const uint32_t rb = b->ctx->row_bytes;
+    const uint64_t chunks = uint64_t(n) * (rb / 16);
+    const int blocks = int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 255) / 256, uint64_t(b->ctx->sm_count) * 8)));
+    k_load_rows<<<blocks, 256, 0, (cudaStream_t)stv>>>(nodes_dev, slots_dev, n,
+                                                       static_cast<const char*>(b->ctx->shard_bases[0]), b->region, rb);
+    FDG_CUDA(cudaGetLastError());
     return FDG_OK;
 }
 

@@ -1171,3 +1171,53 @@ int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, con
 }
 
 }  // namespace fdg
+
+namespace {
+// Byte compare of region[alias[i]] with table[nodes[i]] (trainer_step's verify against the
+// synchronous read oracle, pipeline.hpp:110-121): the smallest mismatching i -> *first_bad.
+__global__ void __launch_bounds__(256) k_verify_rows(const char* region, const int64_t* alias, const uint64_t* nodes,
+                                                     uint64_t n, const char* table, uint32_t rb,
+                                                     unsigned long long* first_bad) {
+    const uint32_t cpr = rb / 4;
+    for (uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; c < n * cpr;
+         c += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = c / cpr, k = c % cpr;
+        if (reinterpret_cast<const uint32_t*>(region + uint64_t(alias[i]) * rb)[k] !=
+            reinterpret_cast<const uint32_t*>(table + nodes[i] * rb)[k])
+            atomicMin(first_bad, (unsigned long long)i);
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int fdg_region_checksum(void* stream, const void* region_dev, uint32_t row_bytes, const int64_t* alias_dev, uint64_t n,
+                        uint64_t* checksum_dev) {
+    fdg::Ctx c;
+    int dev = 0;
+    FDG_CUDA(cudaGetDevice(&dev));
+    c.device = dev;
+    FDG_CUDA(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, dev));
+    c.row_bytes = row_bytes;
+    c.n_shards = 1;
+    return fdg::launch_checksum_alias(c, (cudaStream_t)stream, region_dev, alias_dev, nullptr, n, checksum_dev);
+}
+
+int fdg_region_verify(const fdg_ctx* table, void* stream, const void* region_dev, const int64_t* alias_dev,
+                      const uint64_t* nodes_dev, uint64_t n, uint64_t* first_bad_dev) {
+    if (table->shard_bases.empty() || table->n_shards != 1)
+        return fdg::fail(FDG_NOT_LOADED, "region_verify: no single-shard feature table");
+    if (table->row_bytes % 4) return fdg::fail(FDG_INVALID_ARG, "region_verify: row_bytes must be a multiple of 4");
+    FDG_CUDA(cudaMemsetAsync(first_bad_dev, 0xFF, 8, (cudaStream_t)stream));
+    if (n == 0) return FDG_OK;
+    const uint64_t chunks = n * (table->row_bytes / 4);
+    const int blocks = int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 255) / 256, uint64_t(table->sm_count) * 8)));
+    k_verify_rows<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const char*>(region_dev), alias_dev, nodes_dev,
+                                                            n, static_cast<const char*>(table->shard_bases[0]),
+                                                            table->row_bytes,
+                                                            reinterpret_cast<unsigned long long*>(first_bad_dev));
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
+}  // extern "C"

@@ -781,9 +781,13 @@ __device__ void exact_offsets(const Work<IdT>& W, uint32_t l) {
     __syncthreads();
 }
 
+// Launched after every group chain, so its footprint must stay that of an ordinary sampler
+// CTA (<= 64 registers: 4 CTAs per SM) -- a 255-register CTA would wait for an empty SM on
+// every batch. The replay therefore samples through the global-picks path (no 16-wide
+// register arrays), whatever the fanout.
 template <typename IdT, bool SMALLF>
-__global__ void __launch_bounds__(kScanThreads) k_replay(const __grid_constant__ Group<IdT> G, uint32_t epoch0,
-                                                         uint64_t hash_bytes) {
+__global__ void __launch_bounds__(kScanThreads, 4) k_replay(const __grid_constant__ Group<IdT> G, uint32_t epoch0,
+                                                            uint64_t hash_bytes) {
     const Work<IdT>& W = G.w[blockIdx.y];
     fdg_batch_counts* cnt = W.cnt;
     if (*reinterpret_cast<volatile uint32_t*>(&cnt->status) != FDG_REJECTION) return;
@@ -799,8 +803,8 @@ __global__ void __launch_bounds__(kScanThreads) k_replay(const __grid_constant__
     else intern_pass<IdT, true, false>(W, 0, epoch0);
     __syncthreads();
     for (uint32_t l = 0; l < W.n_layers; ++l) {
-        exact_offsets<IdT, SMALLF>(W, l);
-        sample_nodes<IdT, SMALLF, 2>(W, l, threadIdx.x, blockDim.x);
+        exact_offsets<IdT, false>(W, l);
+        sample_nodes<IdT, false, 2>(W, l, threadIdx.x, blockDim.x);
         __syncthreads();
         insert_picks(W, l, threadIdx.x, blockDim.x);
         __threadfence_block();
@@ -1050,8 +1054,7 @@ int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
         FDG_TRACE("replay", st);  // exact re-run of rejected batches (no-op otherwise)
         const uint32_t e0 = next_epoch(s, n);
         for (uint32_t l = 0; l < s.n_layers; ++l) next_epoch(s, n);
-        if (s.small_f) k_replay<IdT, true><<<dim3(1, n), kScanThreads, 0, st>>>(G, e0, s.hash_bytes);
-        else k_replay<IdT, false><<<dim3(1, n), kScanThreads, 0, st>>>(G, e0, s.hash_bytes);
+        k_replay<IdT, false><<<dim3(1, n), kScanThreads, 0, st>>>(G, e0, s.hash_bytes);
     }
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;
