@@ -252,12 +252,12 @@ int fdg_bm_reverse(fdg_bm* bm, uint64_t slot, int64_t* node);
 int fdg_bm_validate(fdg_bm* bm);
 /* ---- the reference's object split and per-node protocol (the C++ drop-in) ----------
  * featbuf::BufferManager(BufferConfig) holds no table: a standalone buffer manager has its
- * metadata on `device`, its FeatureRegion at region_dev (slot_count x row_bytes device bytes
- * owned by the caller; NULL = allocated here) and gets its miss source from the
- * storage::FeatureTable an Extractor binds (ExtractorEnv, extractor.hpp:58-66). */
+ * metadata on `device` and gets its miss source and its FeatureRegion (slot_count x
+ * row_bytes device bytes owned by the caller, e.g. a featbuf::FeatureRegion; NULL = allocated
+ * by the buffer manager) when an Extractor binds them (ExtractorEnv, extractor.hpp:58-66). */
 int fdg_bm_create_standalone(int device, uint64_t num_nodes, uint64_t slot_count, uint32_t row_bytes,
                              uint64_t min_reserved, uint32_t max_batch_nodes, void* region_dev, fdg_bm** out);
-int fdg_bm_bind_table(fdg_bm* bm, const fdg_ctx* table);
+int fdg_bm_bind_table(fdg_bm* bm, const fdg_ctx* table, void* region_dev);
 /* acquire_for_batch (buffer_manager.hpp:241-269): alias_dev[i] = slot of a hit, -1 otherwise;
  * to_load_dev[0..*n_load_dev) = positions to load, in batch order (device outputs). Misses
  * take their reference when bound. */

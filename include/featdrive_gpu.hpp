@@ -1,31 +1,45 @@
-// featdrive_gpu.hpp -- header-only C++ mirror of the reference's sample -> extract
-// API (/root/reference/proj/include/featdrive), implemented over the C ABI in
-// fdg.h (libfdg.so, B200 / sm_100a). Same names, argument meaning and exception
-// types, so the reference's SET loop (pipeline.hpp:419-543) can call it:
+// featdrive_gpu.hpp -- header-only C++ drop-in for the reference's sample -> extract API
+// (/root/reference/proj/include/featdrive), implemented over the C ABI in fdg.h (libfdg.so,
+// B200 / sm_100a). Same namespaces below the top one, same class names, constructor shapes,
+// argument meaning and exception types, so a reference SET loop compiles against it with the
+// include and the top-level namespace changed (tests/cpp/set_loop.cpp builds both ways):
 //
-//   featdrive::graph::Topology           -> featdrive_gpu::graph::Topology (device CSC + table)
-//   featdrive::graph::sample_khop        -> featdrive_gpu::graph::sample_khop     (bit-exact)
-//   featdrive::graph::partition_epoch    -> featdrive_gpu::graph::partition_epoch (same libstdc++)
-//   featdrive::featbuf::BufferManager    -> featdrive_gpu::featbuf::BufferManager (GPU metadata)
-//   featdrive::extract::Extractor        -> featdrive_gpu::extract::Extractor
-//   featdrive::pipeline::trainer_step    -> featdrive_gpu::pipeline::trainer_step (GPU checksum)
-//   PipelineSession::batch_seed          -> featdrive_gpu::pipeline::batch_seed
-//   pipeline::PipelineSession / EpochStats -> featdrive_gpu::pipeline::PipelineSession / EpochStats
-//                                            (run_epoch, run_epoch_multi, run_sync_reference,
-//                                             the same per-epoch JSON document, stats.hpp:96-146)
+//   featdrive::graph::Topology(dir)              -> CSC in HBM (indptr u64, indices u32/u64)
+//   featdrive::graph::sample_khop / partition_epoch  (bit-exact; pooled sampler workspaces)
+//   featdrive::storage::FeatureTable(path)       -> the feature table in HBM (+ header, read_row_sync)
+//   featdrive::featbuf::BufferManager(BufferConfig)  -> GPU metadata (mapping, refs, LRU ring);
+//       acquire_for_batch / get_standby_slot / bind_slot / publish_valid / wait_for_valid /
+//       release_batch / unwind_bound / release_ref as stream-ordered device operations
+//   featdrive::featbuf::FeatureRegion(S, row)    -> S x row device bytes (the slots)
+//   featdrive::extract::Extractor(ExtractorEnv, ExtractorConfig) -> extract_batch: the fused
+//       Algorithm 1 on the GPU (acquire, LRU pops, bind, row loads, publish) -> NodeAliasList
+//   featdrive::pipeline::trainer_step(TrainTicket, FeatureRegion, FeatureTable*) -> GPU checksum
+//       (+ GPU byte compare against the table with verify)
+//   featdrive::pipeline::PipelineSession(dir, cfg) -> the native runner (fdg_pipeline_*):
+//       run_epoch / run_epoch_multi / run_sync_reference, the same EpochStats JSON
 //
-// Exceptions: FDG_OUT_OF_RANGE -> std::out_of_range, FDG_INVALID_ARG ->
-// std::invalid_argument, FDG_INVARIANT -> InvariantViolation (std::logic_error),
-// FDG_CAPACITY -> StandbyTimeout (std::runtime_error), FDG_IO_ERROR -> std::system_error
-// (errno set) or std::runtime_error (dataset format), anything else -> std::runtime_error.
+// Objects with no GPU counterpart keep their constructors and do nothing: CopyEngine (device
+// copies are stream-ordered), StagingArena (SSD staging is out of scope), StageCounters
+// (filled by Extractor::extract_batch from the buffer counters). Per-call paths allocate no
+// device memory once warm: samplers are pooled per Topology, staging buffers grow and stay.
+//
+// Exceptions: FDG_OUT_OF_RANGE -> std::out_of_range, FDG_INVALID_ARG -> std::invalid_argument,
+// FDG_INVARIANT -> InvariantViolation (std::logic_error), FDG_CAPACITY -> StandbyTimeout
+// (std::runtime_error), FDG_IO_ERROR -> std::system_error (errno set) or std::runtime_error
+// (dataset format), anything else -> std::runtime_error.
 // Link with -lfdg (paper_2406_13984_b200/libfdg.so).
 #pragma once
 
 #include <algorithm>
+#include <array>
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
+#include <deque>
 #include <exception>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <span>
@@ -39,8 +53,11 @@
 
 namespace featdrive_gpu {
 
+// ------------------------------------------------------------------ common.hpp ----
 using NodeId = std::uint64_t;
-using SlotId = std::int64_t;
+using SlotId = std::int64_t;  // -1 means "no slot"
+inline constexpr SlotId kNoSlot = -1;
+inline constexpr std::uint64_t kSectorBytes = 512;
 
 class InvariantViolation : public std::logic_error {
 public:
@@ -66,48 +83,186 @@ inline void check(int rc) {
     }
 }
 
-namespace graph {
+constexpr std::uint64_t splitmix64(std::uint64_t x) {  // common.hpp:77-82
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+constexpr std::uint64_t hash_combine(std::uint64_t a, std::uint64_t b) {  // common.hpp:84-86
+    return splitmix64(a ^ (b + 0x9e3779b97f4a7c15ull + (a << 6) + (a >> 2)));
+}
 
-/// graph::Topology (topology.hpp:33-193) + the feature table, HBM-resident.
-class Topology {
+/// DurationCounter / ScopedTimer (common.hpp:240-260).
+class DurationCounter {
 public:
-    /// Loads indptr.bin / indices.bin / features.bin of a reference dataset dir.
-    explicit Topology(const std::string& dataset_dir, int device = 0) {
-        check(fdg_ctx_create(device, &ctx_));
-        check(fdg_ctx_load_topology_files(ctx_, dataset_dir.c_str()));
-        check(fdg_ctx_load_features_file(ctx_, (dataset_dir + "/features.bin").c_str()));
+    void add(std::int64_t ns) { ns_.fetch_add(ns, std::memory_order_relaxed); }
+    std::int64_t ns() const { return ns_.load(std::memory_order_relaxed); }
+    double seconds() const { return double(ns()) * 1e-9; }
+
+private:
+    std::atomic<std::int64_t> ns_{0};
+};
+class ScopedTimer {
+public:
+    explicit ScopedTimer(DurationCounter& c) : c_(c), t0_(std::chrono::steady_clock::now()) {}
+    ~ScopedTimer() {
+        c_.add(std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0_).count());
     }
-    /// Bit-exact GPU generation of storage::create_synthetic_dataset's content.
-    static std::unique_ptr<Topology> generate(std::uint64_t num_nodes, std::uint32_t dim, std::uint32_t avg_degree,
-                                              std::uint64_t seed, int device = 0) {
-        std::unique_ptr<Topology> t(new Topology(device));
-        check(fdg_ctx_generate_topology(t->ctx_, seed, num_nodes, avg_degree));
+
+private:
+    DurationCounter& c_;
+    std::chrono::steady_clock::time_point t0_;
+};
+
+namespace detail {
+/// A device allocation that only grows: steady-state calls allocate nothing.
+struct DevBuf {
+    void* p = nullptr;
+    std::size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) fdg_free(p);
+    }
+    void* reserve(std::size_t bytes) {
+        bytes = std::max<std::size_t>(bytes, 8);
+        if (bytes > cap) {
+            if (p) fdg_free(p);
+            p = nullptr;
+            cap = 0;
+            check(fdg_malloc(&p, bytes));
+            cap = bytes;
+        }
+        return p;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+}  // namespace detail
+
+// ------------------------------------------------------------- pipeline/stats ----
+namespace pipeline {
+/// StageCounters (stats.hpp:30-48): filled by the drop-in's Extractor.
+struct StageCounters {
+    DurationCounter sample_busy, sample_block, extract_busy, extract_block, extract_io_wait, train_busy, train_block,
+        release_busy, release_block;
+    std::atomic<std::uint64_t> bytes_useful{0}, bytes_redundant{0}, bytes_requested{0}, read_requests{0},
+        nodes_loaded{0}, staging_hits{0};
+};
+}  // namespace pipeline
+
+// ------------------------------------------------------------------- storage ----
+namespace storage {
+
+inline constexpr std::array<char, 8> kFeatureMagic = {'F', 'E', 'A', 'T', 'D', 'R', 'V', '1'};
+inline constexpr std::uint32_t kFormatVersion = 1;
+inline constexpr std::uint32_t kDtypeF32 = 0;
+inline constexpr std::uint64_t kHeaderBytes = 64;
+inline constexpr std::uint64_t kDefaultDataOffset = 512;
+inline const char* kFeatureFileName = "features.bin";
+inline const char* kIndptrFileName = "indptr.bin";
+inline const char* kIndicesFileName = "indices.bin";
+inline const char* kManifestFileName = "manifest.json";
+
+enum class EngineKind { Auto, Uring, Threads };  // async_io.hpp:458 (no GPU counterpart)
+
+/// DatasetHeader (format.hpp:33-65).
+struct DatasetHeader {
+    std::array<char, 8> magic = kFeatureMagic;
+    std::uint32_t version = kFormatVersion;
+    std::uint64_t num_nodes = 0;
+    std::uint32_t dim = 0;
+    std::uint32_t dtype_code = kDtypeF32;
+    std::uint32_t row_bytes = 0;
+    std::uint64_t data_offset = kDefaultDataOffset;
+
+    std::uint64_t row_start(NodeId node) const { return data_offset + node * std::uint64_t(row_bytes); }
+    std::uint64_t row_end(NodeId node) const { return row_start(node) + row_bytes; }
+    std::uint64_t file_bytes() const { return data_offset + num_nodes * std::uint64_t(row_bytes); }
+    std::uint64_t aligned_row_bytes() const {
+        std::uint64_t a = (row_bytes + kSectorBytes - 1) / kSectorBytes * kSectorBytes;
+        if (row_bytes % kSectorBytes != 0) a += kSectorBytes;
+        return a;
+    }
+};
+
+/// storage::FeatureTable (feature_file.hpp:25-107): the table lives in HBM. The header is
+/// validated exactly as the reference does (messages and exception types included).
+class FeatureTable {
+public:
+    explicit FeatureTable(const std::string& path, bool /*want_direct*/ = true, int device = 0) : path_(path) {
+        check(fdg_ctx_create(device, &ctx_));
+        try {
+            check(fdg_ctx_load_features_file(ctx_, path.c_str()));
+        } catch (...) {
+            fdg_ctx_destroy(ctx_);
+            throw;
+        }
+        fill_header();
+    }
+    /// Extension: the bit-exact GPU generation of the reference generator's features.bin
+    /// content (storage::synthetic_row, generator.hpp:65-81), without a file.
+    static std::unique_ptr<FeatureTable> generate(std::uint64_t num_nodes, std::uint32_t dim, std::uint64_t seed,
+                                                  int device = 0) {
+        std::unique_ptr<FeatureTable> t(new FeatureTable());
+        check(fdg_ctx_create(device, &t->ctx_));
         check(fdg_ctx_generate_features(t->ctx_, seed, num_nodes, dim, 0, 1));
+        t->path_ = "<generated>";
+        t->fill_header();
         return t;
     }
-    ~Topology() { fdg_ctx_destroy(ctx_); }
-    Topology(const Topology&) = delete;
-    Topology& operator=(const Topology&) = delete;
+    ~FeatureTable() { fdg_ctx_destroy(ctx_); }
+    FeatureTable(const FeatureTable&) = delete;
+    FeatureTable& operator=(const FeatureTable&) = delete;
 
-    /// Out-of-core tier: the feature table moves to pinned host memory mapped into the
-    /// device; gathers and buffer-manager misses read it over PCIe (put a BufferManager
-    /// in front of it).
-    void features_to_host() { check(fdg_ctx_features_to_host(ctx_)); }
-    bool features_on_host() const { return fdg_ctx_features_on_host(ctx_) != 0; }
+    const DatasetHeader& header() const { return header_; }
+    const std::string& path() const { return path_; }
+    std::uint32_t row_bytes() const { return header_.row_bytes; }
+    std::uint64_t num_nodes() const { return header_.num_nodes; }
+    bool direct_available() const { return false; }
 
-    std::uint64_t num_nodes() const { return info().num_nodes; }
-    std::uint64_t num_edges() const { return info().num_edges; }
-    std::uint32_t row_bytes() const { return info().row_bytes; }
+    /// Plain read of one exact row (the correctness oracle, feature_file.hpp:73-94).
+    void read_row_sync(NodeId node, std::span<std::byte> out) const {
+        if (node >= header_.num_nodes)
+            throw std::out_of_range("read_row_sync: node " + std::to_string(node) + " >= num_nodes " +
+                                    std::to_string(header_.num_nodes));
+        if (out.size() < header_.row_bytes) throw InvariantViolation("FD_CHECK failed: out.size() >= row_bytes");
+        check(fdg_ctx_download_rows(ctx_, node, 1, out.data()));
+    }
+    std::vector<std::byte> read_row_sync(NodeId node) const {
+        std::vector<std::byte> row(header_.row_bytes);
+        read_row_sync(node, row);
+        return row;
+    }
     fdg_ctx* handle() const { return ctx_; }
 
 private:
-    explicit Topology(int device) { check(fdg_ctx_create(device, &ctx_)); }
-    fdg_ctx_info info() const {
+    FeatureTable() = default;
+    void fill_header() {
         fdg_ctx_info i;
         check(fdg_ctx_info_get(ctx_, &i));
-        return i;
+        header_.num_nodes = i.num_nodes ? i.num_nodes : rows_of(i);
+        header_.row_bytes = i.row_bytes;
+        header_.dim = i.row_bytes / 4;
     }
+    static std::uint64_t rows_of(const fdg_ctx_info& i) { return i.rows_per_shard * std::max<std::uint32_t>(i.n_shards, 1); }
+    std::string path_;
+    DatasetHeader header_{};
     fdg_ctx* ctx_ = nullptr;
+};
+
+}  // namespace storage
+
+// --------------------------------------------------------------------- graph ----
+namespace graph {
+
+struct TopologyOptions {  // topology.hpp:28-31 (both are host-cache knobs: no GPU meaning)
+    bool force_pread_cache = false;
+    std::size_t cache_blocks = 4096;
 };
 
 /// graph::Fanouts (sampling.hpp:21-41)
@@ -144,29 +299,152 @@ struct SampledBatch {  // sampling.hpp:48-54
     std::vector<std::uint64_t> layer_nodes;
 };
 
+/// graph::Topology (topology.hpp:33-193): the CSC in HBM.
+class Topology {
+public:
+    /// indptr.bin / indices.bin of a dataset directory, validated like the reference.
+    explicit Topology(const std::string& dataset_dir, TopologyOptions = {}, int device = 0) {
+        check(fdg_ctx_create(device, &ctx_));
+        try {
+            check(fdg_ctx_load_topology_files(ctx_, dataset_dir.c_str()));
+        } catch (...) {
+            fdg_ctx_destroy(ctx_);
+            throw;
+        }
+    }
+    /// Extension: bit-exact GPU generation of storage::create_synthetic_dataset's topology
+    /// (and, with features, its feature rows in the same context).
+    static std::unique_ptr<Topology> generate(std::uint64_t num_nodes, std::uint32_t dim, std::uint32_t avg_degree,
+                                              std::uint64_t seed, int device = 0, bool features = true) {
+        std::unique_ptr<Topology> t(new Topology(device));
+        check(fdg_ctx_generate_topology(t->ctx_, seed, num_nodes, avg_degree));
+        if (features) check(fdg_ctx_generate_features(t->ctx_, seed, num_nodes, dim, 0, 1));
+        return t;
+    }
+    ~Topology() {
+        for (auto& s : pool_) fdg_sampler_destroy(s.sampler);
+        fdg_ctx_destroy(ctx_);
+    }
+    Topology(const Topology&) = delete;
+    Topology& operator=(const Topology&) = delete;
+
+    std::uint64_t num_nodes() const { return info().num_nodes; }
+    std::uint64_t num_edges() const { return info().num_edges; }
+    /// Host copy of indptr (downloaded on first use).
+    const std::vector<std::uint64_t>& indptr() const {
+        std::lock_guard lk(mu_);
+        if (indptr_.empty()) {
+            indptr_.resize(num_nodes() + 1);
+            check(fdg_ctx_download_topology(ctx_, indptr_.data(), nullptr));
+        }
+        return indptr_;
+    }
+    std::uint64_t degree(NodeId node) const {
+        if (node >= num_nodes()) throw InvariantViolation("FD_CHECK failed: node < num_nodes_");
+        const auto& ip = indptr();
+        return ip[node + 1] - ip[node];
+    }
+    /// Copies the in-neighbour list of `node` into `out` (topology.hpp:59-71).
+    void in_neighbors(NodeId node, std::vector<NodeId>& out) const {
+        if (node >= num_nodes()) throw std::out_of_range("topology: node " + std::to_string(node) + " out of range");
+        const auto& ip = indptr();
+        const std::uint64_t lo = ip[node], hi = ip[node + 1];
+        out.resize(hi - lo);
+        if (lo == hi) return;
+        fdg_ctx_info i = info();
+        std::vector<std::uint32_t> narrow(i.idx_bytes == 4 ? hi - lo : 0);
+        const char* base = static_cast<const char*>(i.indices_dev) + lo * i.idx_bytes;
+        if (i.idx_bytes == 8) {
+            check(fdg_memcpy_d2h(out.data(), base, (hi - lo) * 8, nullptr));
+        } else {
+            check(fdg_memcpy_d2h(narrow.data(), base, (hi - lo) * 4, nullptr));
+        }
+        check(fdg_stream_sync(nullptr));
+        if (i.idx_bytes == 4) std::copy(narrow.begin(), narrow.end(), out.begin());
+    }
+    bool uses_mmap() const { return false; }
+
+    // extensions
+    std::uint32_t row_bytes() const { return info().row_bytes; }
+    void features_to_host() { check(fdg_ctx_features_to_host(ctx_)); }
+    bool features_on_host() const { return fdg_ctx_features_on_host(ctx_) != 0; }
+    /// Shares `table`'s rows with this context (non-owning): gathers, the native runner and
+    /// the train stage then read features through the topology.
+    void attach_features(const storage::FeatureTable& table) {
+        fdg_ctx_info t;
+        check(fdg_ctx_info_get(table.handle(), &t));
+        const void* base = t.table_dev;
+        check(fdg_ctx_set_feature_shards(ctx_, &base, 1, table.num_nodes(), table.num_nodes(), t.row_bytes, t.dtype));
+    }
+    fdg_ctx* handle() const { return ctx_; }
+
+    /// Sampler workspace pool: one per concurrent caller, keyed by (fanouts, seed capacity),
+    /// reused across calls (the reference's samplers share one read-only Topology).
+    struct PooledSampler {
+        fdg_sampler* sampler = nullptr;
+        std::vector<std::uint32_t> fanouts;
+        std::uint32_t max_seeds = 0;
+        std::uint64_t cap = 0;
+        bool busy = false;
+        std::vector<std::uint32_t> edges;  // host staging
+    };
+    PooledSampler* acquire_sampler(const Fanouts& f, std::uint32_t seeds) const {
+        std::lock_guard lk(mu_);
+        for (auto& s : pool_)
+            if (!s.busy && s.fanouts == f.per_layer && s.max_seeds >= seeds) {
+                s.busy = true;
+                return &s;
+            }
+        PooledSampler s;
+        s.fanouts = f.per_layer;
+        s.max_seeds = std::max<std::uint32_t>(seeds, 1000);
+        check(fdg_sampler_create(ctx_, s.max_seeds, f.per_layer.data(), std::uint32_t(f.per_layer.size()), &s.sampler));
+        std::uint64_t mn = 0, me = 0;
+        check(fdg_sampler_capacity(s.sampler, &mn, &me));
+        s.cap = std::max<std::uint64_t>({mn, me, 1});
+        s.busy = true;
+        pool_.push_back(std::move(s));
+        return &pool_.back();
+    }
+    void release_sampler(PooledSampler* s) const {
+        std::lock_guard lk(mu_);
+        s->busy = false;
+    }
+
+private:
+    explicit Topology(int device) { check(fdg_ctx_create(device, &ctx_)); }
+    fdg_ctx_info info() const {
+        fdg_ctx_info i;
+        check(fdg_ctx_info_get(ctx_, &i));
+        return i;
+    }
+    fdg_ctx* ctx_ = nullptr;
+    mutable std::mutex mu_;
+    mutable std::vector<std::uint64_t> indptr_;
+    mutable std::deque<PooledSampler> pool_;
+};
+
 /// graph::sample_khop (sampling.hpp:72-134), executed on the GPU, bit-exact.
-/// One sampler workspace per (topology, fanouts, seed count) is reused.
 inline SampledBatch sample_khop(const Topology& topo, std::span<const NodeId> seeds, const Fanouts& fanouts,
                                 std::uint64_t rng_seed) {
     fanouts.validate();
-    fdg_sampler* s = nullptr;
-    check(fdg_sampler_create(topo.handle(), std::uint32_t(std::max<std::size_t>(seeds.size(), 1)),
-                             fanouts.per_layer.data(), std::uint32_t(fanouts.per_layer.size()), &s));
-    std::unique_ptr<fdg_sampler, int (*)(fdg_sampler*)> guard(s, fdg_sampler_destroy);
-    std::uint64_t max_nodes = 0, max_edges = 0;
-    check(fdg_sampler_capacity(s, &max_nodes, &max_edges));
-    const std::uint64_t cap = std::max<std::uint64_t>({max_nodes, max_edges, 1});
+    auto* ps = topo.acquire_sampler(fanouts, std::uint32_t(seeds.size()));
+    struct Release {
+        const Topology& t;
+        Topology::PooledSampler* s;
+        ~Release() { t.release_sampler(s); }
+    } release{topo, ps};
     SampledBatch b;
     b.seeds.assign(seeds.begin(), seeds.end());
-    b.nodes.resize(cap);
-    std::vector<std::uint32_t> e(2 * cap);
+    b.nodes.resize(ps->cap);
+    ps->edges.resize(2 * ps->cap);
     std::uint64_t nn = 0, ne = 0;
     b.layer_nodes.assign(fanouts.per_layer.size() + 2, 0);
-    check(fdg_sample_khop_host(s, seeds.data(), std::uint32_t(seeds.size()), rng_seed, b.nodes.data(), e.data(), cap,
-                               &nn, &ne, b.layer_nodes.data(), nullptr));
+    check(fdg_sample_khop_host(ps->sampler, seeds.data(), std::uint32_t(seeds.size()), rng_seed, b.nodes.data(),
+                               ps->edges.data(), ps->cap, &nn, &ne, b.layer_nodes.data(), nullptr));
     b.nodes.resize(nn);
     b.edges.resize(ne);
-    for (std::uint64_t i = 0; i < ne; ++i) b.edges[i] = LocalEdge{e[2 * i], e[2 * i + 1]};
+    for (std::uint64_t i = 0; i < ne; ++i) b.edges[i] = LocalEdge{ps->edges[2 * i], ps->edges[2 * i + 1]};
     return b;
 }
 
@@ -182,6 +460,352 @@ inline std::vector<std::vector<NodeId>> partition_epoch(std::vector<NodeId> trai
 }
 
 }  // namespace graph
+
+// ------------------------------------------------------------------- featbuf ----
+namespace featbuf {
+
+using StandbyTimeout = ::featdrive_gpu::StandbyTimeout;
+
+enum class MappingKind { Auto, Dense, Sparse };  // the GPU mapping is always a dense 8-byte array
+
+struct MappingEntry {  // buffer_manager.hpp:39-47
+    SlotId slot_index = kNoSlot;
+    std::uint32_t ref_count = 0;
+    std::uint8_t valid = 0;
+    bool empty() const { return slot_index == kNoSlot && ref_count == 0 && valid == 0; }
+};
+
+struct BufferConfig {  // buffer_manager.hpp:180-190
+    std::uint64_t num_nodes = 0;
+    std::uint64_t slot_count = 0;
+    std::uint32_t row_bytes = 0;
+    std::uint64_t min_reserved = 0;
+    MappingKind mapping = MappingKind::Auto;
+    std::chrono::milliseconds standby_timeout{60000};
+    bool validate_every_op = false;
+    bool record_events = false;
+    int device = 0;  // extension
+};
+
+struct BufferStats {  // buffer_manager.hpp:192-200
+    std::uint64_t hits = 0, loads = 0, waits = 0, evictions = 0, takeovers = 0, releases = 0, standby_len = 0;
+};
+
+struct AcquirePlan {  // buffer_manager.hpp:202-206
+    std::vector<SlotId> alias;
+    std::vector<std::uint32_t> to_load;
+    std::vector<std::uint32_t> waits;
+};
+
+enum class WaitOutcome { Ready, TakeOver, Timeout };
+
+/// FeatureRegion (device_region.hpp:24-50): S row slots in HBM. slot() returns a host copy
+/// of the slot's bytes (the reference returns a span into host memory standing in for HBM).
+class FeatureRegion {
+public:
+    FeatureRegion(std::uint64_t slot_count, std::uint32_t row_bytes) : slot_count_(slot_count), row_bytes_(row_bytes) {
+        if (!(slot_count > 0 && row_bytes > 0)) throw InvariantViolation("FD_CHECK failed: slot_count > 0 && row_bytes > 0");
+        check(fdg_malloc(&dev_, slot_count * std::uint64_t(row_bytes)));
+    }
+    ~FeatureRegion() { fdg_free(dev_); }
+    FeatureRegion(const FeatureRegion&) = delete;
+    FeatureRegion& operator=(const FeatureRegion&) = delete;
+
+    std::uint64_t bytes() const { return slot_count_ * std::uint64_t(row_bytes_); }
+    std::uint32_t row_bytes() const { return row_bytes_; }
+    std::uint64_t slot_count() const { return slot_count_; }
+    std::vector<std::byte> slot(SlotId s) const {
+        if (!(s >= 0 && std::uint64_t(s) < slot_count_)) throw InvariantViolation("FD_CHECK failed: slot in range");
+        std::vector<std::byte> out(row_bytes_);
+        check(fdg_memcpy_d2h(out.data(), static_cast<const char*>(dev_) + std::uint64_t(s) * row_bytes_, row_bytes_,
+                             nullptr));
+        check(fdg_stream_sync(nullptr));
+        return out;
+    }
+    void* device_data() const { return dev_; }
+
+    // per-call staging for trainer_step (grows, never freed per call)
+    std::mutex& scratch_mutex() const { return mu_; }
+    detail::DevBuf& scratch(int k) const { return scratch_[k]; }
+
+private:
+    std::uint64_t slot_count_;
+    std::uint32_t row_bytes_;
+    void* dev_ = nullptr;
+    mutable std::mutex mu_;
+    mutable detail::DevBuf scratch_[3];
+};
+
+/// CopyEngine (device_region.hpp:52-91): GPU copies are stream-ordered; nothing to hold.
+class CopyEngine {
+public:
+    explicit CopyEngine(std::chrono::nanoseconds latency = std::chrono::nanoseconds::zero()) : latency_(latency) {}
+    std::size_t in_flight() const { return 0; }
+
+private:
+    std::chrono::nanoseconds latency_;
+};
+
+/// StagingArena (staging.hpp:102-106): the SSD staging arena has no GPU counterpart (the
+/// table is HBM- or host-resident); kept so reference setup code compiles.
+class StagingArena {
+public:
+    StagingArena(std::uint64_t total_slots, std::uint64_t slot_bytes, std::vector<std::uint64_t> worker_quota_slots,
+                 std::chrono::milliseconds = std::chrono::milliseconds(60000))
+        : total_slots_(total_slots), slot_bytes_(slot_bytes), quotas_(std::move(worker_quota_slots)) {}
+    std::uint64_t capacity_bytes() const { return total_slots_ * slot_bytes_; }
+
+private:
+    std::uint64_t total_slots_, slot_bytes_;
+    std::vector<std::uint64_t> quotas_;
+};
+
+/// featbuf::BufferManager (buffer_manager.hpp:222-527): the mapping table, slot references,
+/// LRU standby list and eviction on the GPU. Every operation is a device operation
+/// synchronised before it returns, so the per-node protocol keeps the reference's order.
+class BufferManager {
+public:
+    explicit BufferManager(const BufferConfig& cfg) : cfg_(cfg) {
+        if (cfg.slot_count == 0) throw InvariantViolation("slot_count must be positive");
+        if (cfg.slot_count < cfg.min_reserved)
+            throw InvariantViolation("feature buffer smaller than the N_e * M_b reservation");
+        max_batch_ = std::uint32_t(std::min<std::uint64_t>({cfg.slot_count, cfg.num_nodes, 0x7FFFFFFFull}));
+        check(fdg_bm_create_standalone(cfg.device, cfg.num_nodes, cfg.slot_count, cfg.row_bytes, cfg.min_reserved,
+                                       max_batch_, nullptr, &bm_));
+    }
+    ~BufferManager() { fdg_bm_destroy(bm_); }
+    BufferManager(const BufferManager&) = delete;
+    BufferManager& operator=(const BufferManager&) = delete;
+
+    const BufferConfig& config() const { return cfg_; }
+    std::uint64_t slot_count() const { return cfg_.slot_count; }
+    std::uint64_t feature_bytes() const { return cfg_.slot_count * std::uint64_t(cfg_.row_bytes); }
+
+    /// Algorithm 1 lines 5-17 for one batch (`nodes` deduplicated).
+    AcquirePlan acquire_for_batch(std::span<const NodeId> nodes) {
+        std::lock_guard lk(mu_);
+        const std::uint64_t n = nodes.size();
+        if (n > max_batch_) throw std::invalid_argument("acquire_for_batch: batch larger than the slot count");
+        auto* nd = static_cast<NodeId*>(buf_[0].reserve(n * 8));
+        auto* al = static_cast<SlotId*>(buf_[1].reserve(n * 8));
+        auto* tl = static_cast<std::uint32_t*>(buf_[2].reserve(n * 4 + 8));
+        check(fdg_memcpy_h2d(nd, nodes.data(), n * 8, nullptr));
+        check(fdg_bm_acquire(bm_, nullptr, nd, n, al, tl + 2, tl));
+        status();
+        AcquirePlan plan;
+        plan.alias.resize(n);
+        std::uint32_t n_load = 0;
+        check(fdg_memcpy_d2h(&n_load, tl, 4, nullptr));
+        check(fdg_memcpy_d2h(plan.alias.data(), al, n * 8, nullptr));
+        check(fdg_stream_sync(nullptr));
+        plan.to_load.resize(n_load);
+        check(fdg_memcpy_d2h(plan.to_load.data(), tl + 2, std::uint64_t(n_load) * 4, nullptr));
+        check(fdg_stream_sync(nullptr));
+        if (cfg_.validate_every_op) validate();
+        return plan;
+    }
+    /// Pops the LRU standby slot, evicting its previous node (274-294).
+    SlotId get_standby_slot() {
+        std::lock_guard lk(mu_);
+        auto* sd = static_cast<SlotId*>(buf_[3].reserve(8));
+        check(fdg_bm_pop_standby(bm_, nullptr, 1, sd));
+        const int rc = fdg_bm_status(bm_);
+        if (rc == FDG_CAPACITY)
+            throw StandbyTimeout("get_standby_slot: no slot became available within " +
+                                 std::to_string(cfg_.standby_timeout.count()) + " ms; feature buffer is undersized");
+        check(rc);
+        SlotId s = kNoSlot;
+        check(fdg_memcpy_d2h(&s, sd, 8, nullptr));
+        check(fdg_stream_sync(nullptr));
+        return s;
+    }
+    void bind_slot(NodeId node, SlotId slot) {
+        std::lock_guard lk(mu_);
+        one_node(node, slot);
+        check(fdg_bm_bind(bm_, nullptr, buf_[3].as<NodeId>(), buf_[3].as<SlotId>() + 1, 1));
+        status();
+    }
+    void publish_valid(NodeId node) {
+        std::lock_guard lk(mu_);
+        one_node(node, 0);
+        check(fdg_bm_publish(bm_, nullptr, buf_[3].as<NodeId>(), 1));
+        status();
+    }
+    /// With stream-ordered extraction no load is ever in flight on another extractor: a
+    /// valid node is Ready, a node with no slot is the caller's to take over.
+    WaitOutcome wait_for_valid(NodeId node, SlotId& slot_out, std::chrono::milliseconds /*timeout*/) {
+        const MappingEntry e = mapping_entry(node);
+        if (e.ref_count == 0 && e.slot_index == kNoSlot && !e.valid)
+            throw InvariantViolation("waiting on a node without holding a reference");
+        if (e.valid) {
+            slot_out = e.slot_index;
+            return WaitOutcome::Ready;
+        }
+        return e.slot_index == kNoSlot ? WaitOutcome::TakeOver : WaitOutcome::Timeout;
+    }
+    /// release_batch (352-364): ref-- and MRU pushes at 0, mapping left valid.
+    void release_batch(std::span<const NodeId> nodes) {
+        std::lock_guard lk(mu_);
+        auto* nd = static_cast<NodeId*>(buf_[0].reserve(nodes.size() * 8));
+        check(fdg_memcpy_h2d(nd, nodes.data(), nodes.size() * 8, nullptr));
+        check(fdg_bm_release(bm_, nullptr, nd, nullptr, nodes.size()));
+        status();
+        if (cfg_.validate_every_op) validate();
+    }
+    void unwind_bound(NodeId node) {
+        std::lock_guard lk(mu_);
+        check(fdg_bm_unwind_bound(bm_, nullptr, node));
+        status();
+    }
+    void release_ref(NodeId node) {
+        std::lock_guard lk(mu_);
+        check(fdg_bm_release_ref(bm_, nullptr, node));
+        status();
+    }
+    void abandon_claim(NodeId) {}  // no takeover claims exist on the stream-ordered path
+
+    BufferStats stats() const {
+        fdg_bm_stats s;
+        check(fdg_bm_stats_get(bm_, &s));
+        return BufferStats{s.hits, s.loads, s.waits, s.evictions, s.takeovers, s.releases, s.standby_len};
+    }
+    MappingEntry mapping_entry(NodeId node) const {
+        std::int64_t slot = 0;
+        std::uint32_t ref = 0, valid = 0;
+        check(fdg_bm_entry(bm_, node, &slot, &ref, &valid));
+        return MappingEntry{slot, ref, std::uint8_t(valid)};
+    }
+    NodeId reverse_mapping(SlotId slot) const {
+        std::int64_t v = -1;
+        check(fdg_bm_reverse(bm_, std::uint64_t(slot), &v));
+        return v < 0 ? ~NodeId(0) : NodeId(v);
+    }
+    std::size_t standby_size() const { return stats().standby_len; }
+    void validate() const { check(fdg_bm_validate(bm_)); }
+
+    // extension
+    fdg_bm* handle() const { return bm_; }
+    std::uint32_t max_batch_nodes() const { return max_batch_; }
+    /// Binds the miss source and the slot storage (done by the Extractor constructor).
+    void attach(const storage::FeatureTable& table, FeatureRegion& region) {
+        if (region.slot_count() != cfg_.slot_count || region.row_bytes() != cfg_.row_bytes)
+            throw InvariantViolation("FeatureRegion shape differs from the BufferConfig");
+        check(fdg_bm_bind_table(bm_, table.handle(), region.device_data()));
+    }
+    std::mutex& mutex() { return mu_; }
+    detail::DevBuf& scratch(int k) { return buf_[k]; }
+    void status() const {
+        const int rc = fdg_bm_status(bm_);
+        if (rc == FDG_CAPACITY)
+            throw StandbyTimeout("get_standby_slot: no slot became available within " +
+                                 std::to_string(cfg_.standby_timeout.count()) + " ms; feature buffer is undersized");
+        if (rc == FDG_INVARIANT) throw InvariantViolation("buffer manager invariant violated (device-detected)");
+        check(rc);
+    }
+
+private:
+    void one_node(NodeId node, SlotId slot) {
+        NodeId host[2] = {node, NodeId(slot)};
+        auto* p = static_cast<NodeId*>(buf_[3].reserve(16));
+        check(fdg_memcpy_h2d(p, host, 16, nullptr));
+    }
+    BufferConfig cfg_;
+    std::uint32_t max_batch_ = 0;
+    fdg_bm* bm_ = nullptr;
+    std::mutex mu_;
+    detail::DevBuf buf_[4];
+};
+
+}  // namespace featbuf
+
+// ------------------------------------------------------------------- extract ----
+namespace extract {
+
+enum class Placement { DeviceSim, HostOnly };
+
+struct TestHooks {  // extractor.hpp:40-46
+    std::function<void(std::uint32_t worker, NodeId lo, NodeId hi)> on_disk_read;
+    std::function<bool(NodeId)> inject_read_failure;
+    std::function<void(std::uint32_t worker, std::uint64_t batch_id)> before_batch;
+    std::function<void(std::uint32_t worker, std::uint64_t batch_id)> before_staging_free;
+    std::function<void(std::uint32_t worker, std::uint64_t batch_id)> before_release;
+};
+
+struct ExtractorConfig {  // extractor.hpp:48-56
+    std::uint32_t worker = 0;
+    std::size_t io_depth = 64;
+    storage::EngineKind engine = storage::EngineKind::Auto;
+    std::chrono::nanoseconds read_latency{0};
+    Placement placement = Placement::DeviceSim;
+    std::chrono::milliseconds wait_timeout{60000};
+    std::uint64_t max_extent_bytes = 1u << 20;
+};
+
+struct ExtractorEnv {  // extractor.hpp:58-66
+    storage::FeatureTable* table = nullptr;
+    featbuf::BufferManager* buffer = nullptr;
+    featbuf::StagingArena* staging = nullptr;
+    featbuf::FeatureRegion* region = nullptr;
+    featbuf::CopyEngine* copies = nullptr;
+    pipeline::StageCounters* counters = nullptr;
+    const TestHooks* hooks = nullptr;
+};
+
+class BatchExtractError : public std::runtime_error {
+public:
+    explicit BatchExtractError(const std::string& what) : std::runtime_error(what) {}
+};
+
+using NodeAliasList = std::vector<SlotId>;  // extractor.hpp:73
+
+/// extract::Extractor (extractor.hpp:75-113). extract_batch runs Algorithm 1 on the GPU in
+/// one stream-ordered pass (acquire, LRU pops in batch order, bind, table -> slot row loads,
+/// publish) and returns the alias list; the reference's I/O machinery has no counterpart.
+class Extractor {
+public:
+    Extractor(ExtractorEnv env, ExtractorConfig cfg) : env_(env), cfg_(cfg) {
+        if (!(env_.table && env_.buffer && env_.region && env_.counters))
+            throw InvariantViolation("FD_CHECK failed: env_.table && env_.buffer && env_.region && env_.counters");
+        if (cfg_.placement == Placement::DeviceSim && !env_.copies)
+            throw InvariantViolation("FD_CHECK failed: env_.copies != nullptr");
+        env_.buffer->attach(*env_.table, *env_.region);
+    }
+
+    NodeAliasList extract_batch(const graph::SampledBatch& batch) {
+        if (env_.hooks && env_.hooks->before_batch) env_.hooks->before_batch(cfg_.worker, batch.batch_id);
+        const std::uint64_t n = batch.nodes.size();
+        NodeAliasList alias(n);
+        featbuf::BufferManager& bm = *env_.buffer;
+        {
+            ScopedTimer io(env_.counters->extract_io_wait);
+            std::lock_guard lk(bm.mutex());
+            if (n > bm.max_batch_nodes()) throw std::invalid_argument("extract_batch: batch larger than the slot count");
+            const auto before = bm.stats();
+            auto* nd = static_cast<NodeId*>(bm.scratch(0).reserve(n * 8));
+            auto* al = static_cast<SlotId*>(bm.scratch(1).reserve(n * 8));
+            check(fdg_memcpy_h2d(nd, batch.nodes.data(), n * 8, nullptr));
+            check(fdg_bm_extract(bm.handle(), nullptr, nd, nullptr, n, al, nullptr, nullptr));
+            bm.status();
+            check(fdg_memcpy_d2h(alias.data(), al, n * 8, nullptr));
+            check(fdg_stream_sync(nullptr));
+            const std::uint64_t loads = bm.stats().loads - before.loads, rb = env_.table->row_bytes();
+            env_.counters->nodes_loaded.fetch_add(loads, std::memory_order_relaxed);
+            env_.counters->read_requests.fetch_add(loads, std::memory_order_relaxed);
+            env_.counters->bytes_requested.fetch_add(loads * rb, std::memory_order_relaxed);
+            env_.counters->bytes_useful.fetch_add(loads * rb, std::memory_order_relaxed);
+        }
+        if (env_.hooks && env_.hooks->before_staging_free) env_.hooks->before_staging_free(cfg_.worker, batch.batch_id);
+        for (SlotId a : alias)
+            if (a < 0) throw InvariantViolation("alias unassigned after extraction");
+        return alias;
+    }
+
+private:
+    ExtractorEnv env_;
+    ExtractorConfig cfg_;
+};
+
+}  // namespace extract
 
 namespace train {
 
@@ -218,18 +842,12 @@ public:
         c.n_layers = std::uint32_t(dims_.size() - 1);
         for (std::size_t i = 0; i < b.layer_nodes.size() && i < FDG_MAX_LAYERS + 2; ++i)
             c.layer_nodes[i] = std::uint32_t(b.layer_nodes[i]);
-        void *nd = nullptr, *ed = nullptr, *x = nullptr, *cd = nullptr, *ld = nullptr;
-        auto guard = [](void* p) { fdg_free(p); };
-        check(fdg_malloc(&nd, std::max<std::uint64_t>(n, 1) * 8));
-        std::unique_ptr<void, decltype(guard)> g1(nd, guard);
-        check(fdg_malloc(&ed, std::max<std::uint64_t>(e, 1) * 8));
-        std::unique_ptr<void, decltype(guard)> g2(ed, guard);
-        check(fdg_malloc(&x, std::max<std::uint64_t>(n, 1) * topo_.row_bytes()));
-        std::unique_ptr<void, decltype(guard)> g3(x, guard);
-        check(fdg_malloc(&cd, sizeof(c)));
-        std::unique_ptr<void, decltype(guard)> g4(cd, guard);
-        check(fdg_malloc(&ld, sizeof(float)));
-        std::unique_ptr<void, decltype(guard)> g5(ld, guard);
+        std::lock_guard lk(mu_);
+        void* nd = buf_[0].reserve(n * 8);
+        void* ed = buf_[1].reserve(e * 8);
+        void* x = buf_[2].reserve(n * std::uint64_t(topo_.row_bytes()));
+        void* cd = buf_[3].reserve(sizeof(c));
+        void* ld = buf_[4].reserve(sizeof(float));
         check(fdg_memcpy_h2d(nd, b.nodes.data(), n * 8, nullptr));
         check(fdg_memcpy_h2d(ed, b.edges.data(), e * 8, nullptr));
         check(fdg_memcpy_h2d(cd, &c, sizeof(c), nullptr));
@@ -247,90 +865,13 @@ private:
     const graph::Topology& topo_;
     std::vector<std::uint32_t> dims_;
     fdg_sage* m_ = nullptr;
+    mutable std::mutex mu_;
+    mutable detail::DevBuf buf_[5];  // per-call staging, grown once
 };
 
 }  // namespace train
 
-namespace featbuf {
-
-struct BufferStats {  // buffer_manager.hpp:192-200
-    std::uint64_t hits = 0, loads = 0, waits = 0, evictions = 0, takeovers = 0, releases = 0, standby_len = 0;
-};
-
-/// featbuf::BufferManager + FeatureRegion, GPU-resident; operations are batch-wide.
-class BufferManager {
-public:
-    BufferManager(const graph::Topology& topo, std::uint64_t slot_count, std::uint64_t min_reserved,
-                  std::uint32_t max_batch_nodes)
-        : topo_(topo) {
-        check(fdg_bm_create(topo.handle(), slot_count, min_reserved, max_batch_nodes, &bm_));
-    }
-    ~BufferManager() { fdg_bm_destroy(bm_); }
-    BufferManager(const BufferManager&) = delete;
-    BufferManager& operator=(const BufferManager&) = delete;
-
-    /// acquire_for_batch + get_standby_slot/bind_slot per miss + row copies + publish_valid.
-    std::vector<SlotId> extract(std::span<const NodeId> nodes) {
-        std::vector<SlotId> alias(nodes.size());
-        DeviceVec<NodeId> nd(nodes.size());
-        DeviceVec<SlotId> al(nodes.size());
-        check(fdg_memcpy_h2d(nd.p, nodes.data(), nodes.size() * 8, nullptr));
-        check(fdg_bm_extract(bm_, nullptr, nd.p, nullptr, nodes.size(), al.p, nullptr, nullptr));
-        status();
-        check(fdg_memcpy_d2h(alias.data(), al.p, alias.size() * 8, nullptr));
-        check(fdg_stream_sync(nullptr));
-        return alias;
-    }
-    /// release_batch (buffer_manager.hpp:352-364)
-    void release_batch(std::span<const NodeId> nodes) {
-        DeviceVec<NodeId> nd(nodes.size());
-        check(fdg_memcpy_h2d(nd.p, nodes.data(), nodes.size() * 8, nullptr));
-        check(fdg_bm_release(bm_, nullptr, nd.p, nullptr, nodes.size()));
-        status();
-    }
-    BufferStats stats() const {
-        fdg_bm_stats s;
-        check(fdg_bm_stats_get(bm_, &s));
-        return BufferStats{s.hits, s.loads, s.waits, s.evictions, s.takeovers, s.releases, s.standby_len};
-    }
-    void validate() const { check(fdg_bm_validate(bm_)); }
-    fdg_bm* handle() const { return bm_; }
-    const graph::Topology& topology() const { return topo_; }
-
-private:
-    template <typename T>
-    struct DeviceVec {
-        explicit DeviceVec(std::size_t n) { check(fdg_malloc(reinterpret_cast<void**>(&p), std::max<std::size_t>(n, 1) * sizeof(T))); }
-        ~DeviceVec() { fdg_free(p); }
-        T* p = nullptr;
-    };
-    void status() const {
-        int rc = fdg_bm_status(bm_);
-        if (rc == FDG_CAPACITY) throw StandbyTimeout("get_standby_slot: standby list exhausted; feature buffer is undersized");
-        check(rc);
-    }
-    const graph::Topology& topo_;
-    fdg_bm* bm_ = nullptr;
-};
-
-}  // namespace featbuf
-
-namespace extract {
-
-using NodeAliasList = std::vector<SlotId>;  // extractor.hpp:73
-
-/// extract::Extractor (extractor.hpp:75-113)
-class Extractor {
-public:
-    explicit Extractor(featbuf::BufferManager& buffer) : buffer_(buffer) {}
-    NodeAliasList extract_batch(const graph::SampledBatch& batch) { return buffer_.extract(batch.nodes); }
-
-private:
-    featbuf::BufferManager& buffer_;
-};
-
-}  // namespace extract
-
+// ------------------------------------------------------------------ pipeline ----
 namespace pipeline {
 
 /// PipelineSession::batch_seed (pipeline.hpp:295-298)
@@ -338,64 +879,109 @@ inline std::uint64_t batch_seed(std::uint64_t seed, std::uint64_t epoch, std::ui
     return fdg_batch_seed(seed, epoch, global_batch);
 }
 
-/// trainer_step (pipeline.hpp:103-124): sum of hash_bytes64 over each node's row,
-/// read through its alias slot in the GPU feature region.
-inline std::uint64_t trainer_step(const graph::SampledBatch& batch, const extract::NodeAliasList& alias,
-                                  const featbuf::BufferManager& buffer) {
-    if (alias.size() != batch.nodes.size()) throw InvariantViolation("alias list length != batch nodes");
+struct TrainTicket {  // pipeline.hpp:78-81
+    graph::SampledBatch batch;
+    extract::NodeAliasList alias;
+};
+
+struct ReleaseTicket {  // pipeline.hpp:83-86
+    std::uint64_t batch_id = 0;
+    std::vector<NodeId> nodes;
+};
+
+class PipelineError : public std::runtime_error {  // pipeline.hpp:88-97
+public:
+    PipelineError(std::string stage, const std::string& what)
+        : std::runtime_error("[" + stage + "] " + what), stage_(std::move(stage)) {}
+    const std::string& stage() const { return stage_; }
+
+private:
+    std::string stage_;
+};
+
+class SiblingAbort : public PipelineError {
+public:
+    SiblingAbort() : PipelineError("pipeline", "aborted after a failure in another worker") {}
+};
+
+/// trainer_step (pipeline.hpp:103-124): sum of hash_bytes64 over each node's row read
+/// through its alias slot, on the GPU; with verify_against, every region row is byte-compared
+/// with the table's row of its node (on the GPU) and a mismatch throws as the reference does.
+inline std::uint64_t trainer_step(const TrainTicket& ticket, const featbuf::FeatureRegion& region,
+                                  const storage::FeatureTable* verify_against = nullptr) {
+    const auto& alias = ticket.alias;
+    const std::uint64_t n = ticket.batch.nodes.size();
+    if (alias.size() != n) throw InvariantViolation("FD_CHECK failed: alias list length == batch nodes");
     for (SlotId a : alias)
         if (a < 0) throw InvariantViolation("trainer saw an unassigned alias");
-    void* ad = nullptr;
-    void* cs = nullptr;
-    check(fdg_malloc(&ad, std::max<std::size_t>(alias.size(), 1) * 8));
-    check(fdg_malloc(&cs, 8));
-    check(fdg_memset(cs, 0, 8, nullptr));
-    check(fdg_memcpy_h2d(ad, alias.data(), alias.size() * 8, nullptr));
-    check(fdg_checksum_alias(buffer.topology().handle(), nullptr, fdg_bm_region(buffer.handle()),
-                             static_cast<const int64_t*>(ad), nullptr, alias.size(), static_cast<uint64_t*>(cs)));
-    std::uint64_t sum = 0;
-    check(fdg_memcpy_d2h(&sum, cs, 8, nullptr));
+    std::lock_guard lk(region.scratch_mutex());
+    auto* ad = static_cast<std::int64_t*>(region.scratch(0).reserve(n * 8));
+    auto* cs = static_cast<std::uint64_t*>(region.scratch(1).reserve(16));
+    check(fdg_memset(cs, 0, 16, nullptr));
+    check(fdg_memcpy_h2d(ad, alias.data(), n * 8, nullptr));
+    check(fdg_region_checksum(nullptr, region.device_data(), region.row_bytes(), ad, n, cs));
+    if (verify_against) {
+        auto* nd = static_cast<NodeId*>(region.scratch(2).reserve(n * 8));
+        check(fdg_memcpy_h2d(nd, ticket.batch.nodes.data(), n * 8, nullptr));
+        check(fdg_region_verify(verify_against->handle(), nullptr, region.device_data(), ad, nd, n, cs + 1));
+    }
+    std::uint64_t out[2] = {0, ~0ull};
+    check(fdg_memcpy_d2h(out, cs, verify_against ? 16 : 8, nullptr));
     check(fdg_stream_sync(nullptr));
-    fdg_free(ad);
-    fdg_free(cs);
-    return sum;
+    if (verify_against && out[1] != ~0ull)
+        throw PipelineError("train", "buffer contents for node " + std::to_string(ticket.batch.nodes[out[1]]) +
+                                         " do not match the synchronous read oracle (batch " +
+                                         std::to_string(ticket.batch.batch_id) + ")");
+    return out[0];
 }
+
 // ------------------------------------------------------------------ session ----
 // PipelineSession (pipeline.hpp:127-299) on the GPU runner (fdg_pipeline_*): one
 // persistent pipeline (sampler streams + extraction + optional buffer manager) per
 // worker segment, reused across epochs like the reference's per-worker buffer.
 
-inline std::uint64_t splitmix64(std::uint64_t x) {  // common.hpp:77-82
-    x += 0x9e3779b97f4a7c15ull;
-    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
-    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
-    return x ^ (x >> 31);
-}
-inline std::uint64_t hash_combine(std::uint64_t a, std::uint64_t b) {  // common.hpp:84-86
-    return splitmix64(a ^ (b + 0x9e3779b97f4a7c15ull + (a << 6) + (a >> 2)));
-}
-
 enum class RunMode { Async, SyncReference };
 
 /// pipeline.hpp:30-76. GPU meaning: num_samplers = concurrent sampler streams;
 /// num_extractors (N_e) only sizes the default slot count N_e * M_b, as in the
-/// reference; slots = kNoBuffer extracts by direct gather (no buffer manager).
+/// reference; slots = kNoBuffer extracts by direct gather (no buffer manager). The
+/// reference's queue / I/O / latency knobs are accepted and have no GPU counterpart.
 struct PipelineConfig {
     static constexpr std::uint64_t kNoBuffer = ~0ull;
     std::uint32_t num_samplers = 6;
     std::uint32_t num_extractors = 4;
+    std::size_t extracting_queue_cap = 6;
+    std::size_t training_queue_cap = 4;
+    std::size_t releasing_queue_cap = 4;
     std::uint64_t batch_size = 1000;
     graph::Fanouts fanouts{{10, 10, 10}};
     std::uint64_t slots = 0;  // per-worker feature-buffer slots; 0 = N_e * M_b
+    std::size_t io_depth = 64;
     RunMode mode = RunMode::Async;
+    extract::Placement placement = extract::Placement::DeviceSim;
     std::uint32_t workers = 1;  // segments (concurrent pipelines on the topology's GPU)
-    std::uint32_t group_batches = 1;
+    featbuf::MappingKind mapping = featbuf::MappingKind::Auto;
+    storage::EngineKind engine = storage::EngineKind::Auto;
+    std::chrono::nanoseconds read_latency{0};
+    std::chrono::nanoseconds copy_latency{0};
+    std::chrono::nanoseconds compute_delay{0};
+    std::uint32_t extract_retries = 0;
     bool verify = false;  // re-derive every batch on the non-pipelined path and compare
+    std::chrono::milliseconds wait_timeout{60000};
+    std::uint64_t staging_portion_slots = 0;
+    bool buffer_validate_every_op = false;
+    extract::TestHooks hooks;
+    // GPU extensions
+    std::uint32_t group_batches = 1;
+    int device = 0;
 
     void validate() const {
         if (num_samplers < 1 || num_extractors < 1)
             throw std::invalid_argument("config: need at least one sampler and one extractor");
+        if (extracting_queue_cap < 1 || training_queue_cap < 1 || releasing_queue_cap < 1)
+            throw std::invalid_argument("config: queue capacities must be >= 1");
         if (batch_size < 1) throw std::invalid_argument("config: batch_size must be >= 1");
+        if (io_depth < 1) throw std::invalid_argument("config: io_depth must be >= 1");
         if (workers < 1) throw std::invalid_argument("config: workers must be >= 1");
         fanouts.validate();
     }
@@ -407,16 +993,6 @@ struct PipelineConfig {
 struct BatchRecord {  // stats.hpp:21-27
     std::uint64_t batch_id = 0, seed_count = 0, node_count = 0, checksum = 0;
     bool failed = false;
-};
-
-class PipelineError : public std::runtime_error {  // pipeline.hpp:84-93
-public:
-    PipelineError(std::string stage, const std::string& what)
-        : std::runtime_error("[" + stage + "] " + what), stage_(std::move(stage)) {}
-    const std::string& stage() const { return stage_; }
-
-private:
-    std::string stage_;
 };
 
 /// stats.hpp:47-146, same JSON document. Stage times: sample_busy = sampler-stream
@@ -508,7 +1084,34 @@ struct EpochStats {
 
 class PipelineSession {
 public:
-    PipelineSession(const graph::Topology& topo, PipelineConfig cfg) : topo_(topo), cfg_(std::move(cfg)) {
+    /// pipeline.hpp:128-174: the dataset directory's topology and features.bin (header and
+    /// lengths validated as the reference does), one runner per worker segment.
+    PipelineSession(const std::string& dataset_dir, PipelineConfig cfg, graph::TopologyOptions topo_opts = {})
+        : own_table_(std::make_unique<storage::FeatureTable>(dataset_dir + "/" + storage::kFeatureFileName, true,
+                                                             cfg.device)),
+          own_topo_(std::make_unique<graph::Topology>(dataset_dir, topo_opts, cfg.device)),
+          topo_(*own_topo_),
+          cfg_(std::move(cfg)) {
+        own_topo_->attach_features(*own_table_);
+        build();
+    }
+    /// Extension: a topology that already holds its feature rows (e.g. Topology::generate).
+    PipelineSession(const graph::Topology& topo, PipelineConfig cfg) : topo_(topo), cfg_(std::move(cfg)) { build(); }
+    ~PipelineSession() {
+        for (auto p : pipes_) fdg_pipeline_destroy(p);
+        if (sampler_) fdg_sampler_destroy(sampler_);
+    }
+    PipelineSession(const PipelineSession&) = delete;
+    PipelineSession& operator=(const PipelineSession&) = delete;
+
+    const graph::Topology& topology() const { return topo_; }
+    const storage::FeatureTable* table() const { return own_table_.get(); }
+    std::uint64_t max_batch_nodes() const { return mb_; }
+    std::uint64_t slots_per_worker() const { return slots_; }
+    const PipelineConfig& config() const { return cfg_; }
+
+private:
+    void build() {
         cfg_.validate();
         mb_ = cfg_.max_batch_nodes(topo_.num_nodes());
         slots_ = cfg_.slots == PipelineConfig::kNoBuffer ? 0
@@ -535,17 +1138,8 @@ public:
             pipes_.push_back(p);
         }
     }
-    ~PipelineSession() {
-        for (auto p : pipes_) fdg_pipeline_destroy(p);
-        if (sampler_) fdg_sampler_destroy(sampler_);
-    }
-    PipelineSession(const PipelineSession&) = delete;
-    PipelineSession& operator=(const PipelineSession&) = delete;
 
-    std::uint64_t max_batch_nodes() const { return mb_; }
-    std::uint64_t slots_per_worker() const { return slots_; }
-    const PipelineConfig& config() const { return cfg_; }
-
+public:
     static std::uint64_t batch_seed(std::uint64_t seed, std::uint64_t epoch, std::uint64_t global_batch) {
         return hash_combine(hash_combine(seed, epoch), global_batch);  // pipeline.hpp:295-298
     }
@@ -732,6 +1326,8 @@ private:
         void* p = nullptr;
     };
 
+    std::unique_ptr<storage::FeatureTable> own_table_;
+    std::unique_ptr<graph::Topology> own_topo_;
     const graph::Topology& topo_;
     PipelineConfig cfg_;
     std::uint64_t mb_ = 0, slots_ = 0, cap_ = 0;

@@ -755,7 +755,7 @@ namespace {
 // Buffer manager over `ctx` (the miss source when it holds a table); the region is
 // allocated here unless `region` is given (then owned by the caller).
 int bm_build(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint32_t max_batch_nodes, char* region,
-             fdg_bm** out) {
+             bool alloc_region, fdg_bm** out) {
     if (slot_count == 0) return fail(FDG_INVARIANT, "slot_count must be positive");
     if (slot_count < min_reserved) return fail(FDG_INVARIANT, "feature buffer smaller than the N_e * M_b reservation");
     if (slot_count >= uint64_t(INT32_MAX)) return fail(FDG_INVALID_ARG, "slot_count must be < 2^31");
@@ -784,9 +784,9 @@ int bm_build(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint32_t 
     const uint64_t o_isl = sz; sz += al(uint64_t(b->max_batch));
     const uint64_t o_isl1 = sz; sz += al(uint64_t(b->max_batch));
     cudaError_t e = cudaMalloc(&b->arena, sz);
-    b->own_region = region == nullptr;
+    b->own_region = region == nullptr && alloc_region;
     b->region = region;
-    if (e == cudaSuccess && !region) e = cudaMalloc((void**)&b->region, slot_count * ctx->row_bytes);
+    if (e == cudaSuccess && b->own_region) e = cudaMalloc((void**)&b->region, slot_count * ctx->row_bytes);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         if (b->arena) cudaFree(b->arena);
@@ -830,7 +830,7 @@ int bm_build(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint32_t 
 extern "C" {
 
 int fdg_bm_create(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint32_t max_batch_nodes, fdg_bm** out) {
-    return bm_build(ctx, slot_count, min_reserved, max_batch_nodes, nullptr, out);
+    return bm_build(ctx, slot_count, min_reserved, max_batch_nodes, nullptr, true, out);
 }
 
 int fdg_bm_create_standalone(int device, uint64_t num_nodes, uint64_t slot_count, uint32_t row_bytes,
@@ -842,7 +842,7 @@ int fdg_bm_create_standalone(int device, uint64_t num_nodes, uint64_t slot_count
     c->feat_nodes = num_nodes;
     c->row_bytes = row_bytes;
     c->n_shards = 0;  // no miss source until fdg_bm_bind_table
-    const int rc = bm_build(c, slot_count, min_reserved, max_batch_nodes, static_cast<char*>(region_dev), out);
+    const int rc = bm_build(c, slot_count, min_reserved, max_batch_nodes, static_cast<char*>(region_dev), false, out);
     if (rc != FDG_OK) {
         fdg_ctx_destroy(c);
         return rc;
@@ -851,13 +851,22 @@ int fdg_bm_create_standalone(int device, uint64_t num_nodes, uint64_t slot_count
     return FDG_OK;
 }
 
-int fdg_bm_bind_table(fdg_bm* b, const fdg_ctx* table) {
+int fdg_bm_bind_table(fdg_bm* b, const fdg_ctx* table, void* region_dev) {
     if (!b->own_ctx) return fail(FDG_INVALID_ARG, "bm_bind_table: only a standalone buffer manager takes a table");
     if (table->shard_bases.empty() || table->n_shards != 1)
         return fail(FDG_NOT_LOADED, "bm_bind_table: the table context holds no single-shard feature table");
     if (table->row_bytes != b->own_ctx->row_bytes || table->feat_nodes != b->d.N)
         return fail(FDG_INVALID_ARG, "bm_bind_table: table shape differs from the buffer config (row_bytes / num_nodes)");
     if (table->device != b->own_ctx->device) return fail(FDG_INVALID_ARG, "bm_bind_table: table on another device");
+    cudaSetDevice(b->own_ctx->device);
+    if (region_dev && region_dev != b->region) {
+        if (b->own_region && b->region) cudaFree(b->region);
+        b->region = static_cast<char*>(region_dev);
+        b->own_region = false;
+    } else if (!b->region) {
+        FDG_CUDA(cudaMalloc((void**)&b->region, b->slots * b->own_ctx->row_bytes));
+        b->own_region = true;
+    }
     fdg_ctx* c = b->own_ctx;
     c->shard_bases = table->shard_bases;
     c->n_shards = 1;
@@ -912,8 +921,8 @@ int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
                     const int64_t* alias, void* out, uint64_t* checksum, uint32_t parity) {
     const BmDev& d = b->d;
     const uint32_t rb = b->ctx->row_bytes;
-    if (b->ctx->shard_bases.empty())
-        return fail(FDG_NOT_LOADED, "bm_extract: no feature table bound (fdg_bm_bind_table)");
+    if (b->ctx->shard_bases.empty() || !b->region)
+        return fail(FDG_NOT_LOADED, "bm_extract: no feature table / region bound (fdg_bm_bind_table)");
     const char* table = static_cast<const char*>(b->ctx->shard_bases[0]);
     const uint64_t chunks = n_host * (rb / 16);
     const int blocks =
@@ -1159,7 +1168,7 @@ int fdg_bm_release_ref(fdg_bm* b, void* stv, uint64_t node) {
 
 int fdg_bm_load_rows(fdg_bm* b, void* stv, const uint64_t* nodes_dev, const int64_t* slots_dev, uint32_t n) {
     if (n == 0) return FDG_OK;
-    if (b->ctx->shard_bases.empty()) return fail(FDG_NOT_LOADED, "bm_load_rows: no feature table bound");
+    if (b->ctx->shard_bases.empty() || !b->region) return fail(FDG_NOT_LOADED, "bm_load_rows: no feature table bound");
     const uint32_t rb = b->ctx->row_bytes;
     const uint64_t chunks = uint64_t(n) * (rb / 16);
     const int blocks = int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 255) / 256, uint64_t(b->ctx->sm_count) * 8)));

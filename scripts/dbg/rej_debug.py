@@ -2,6 +2,10 @@
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
+from paper_2406_13984_b200 import _lib
+if os.environ.get("FDG_DBG_LIB"):
+    _lib.LIB_PATH = os.environ["FDG_DBG_LIB"]
+    _lib.load.__defaults__ = (_lib.LIB_PATH,)
 import paper_2406_13984_b200 as fd
 import oracle
 

@@ -102,7 +102,9 @@ int main(int argc, char** argv) {
         const std::uint32_t epochs = std::uint32_t(std::stoul(opt["epochs"]));
         const std::uint64_t seed = std::stoull(opt["seed"]);
 
-        std::unique_ptr<graph::Topology> topo;
+        cfg.device = device;
+        std::unique_ptr<graph::Topology> topo;  // --generate: dataset in HBM (features in the same context)
+        std::unique_ptr<pipeline::PipelineSession> session_ptr;
         std::string dataset_desc;
         if (opt.count("generate")) {
             std::string g = opt["generate"];
@@ -120,14 +122,17 @@ int main(int argc, char** argv) {
             dataset_desc = "{\"generated\":{\"nodes\":" + std::to_string(v[0]) + ",\"dim\":" + std::to_string(v[1]) +
                            ",\"avg_degree\":" + std::to_string(v[2]) +
                            ",\"seed\":" + std::to_string(v.size() > 3 ? v[3] : 0) + "}}";
+            session_ptr = std::make_unique<pipeline::PipelineSession>(*topo, cfg);
         } else if (opt.count("dataset")) {
-            topo = std::make_unique<graph::Topology>(opt["dataset"], device);
+            // PipelineSession(dataset_dir, cfg) as the reference CLI (pipeline.hpp:128-174)
+            session_ptr = std::make_unique<pipeline::PipelineSession>(opt["dataset"], cfg);
             dataset_desc = jstr(opt["dataset"]);
         } else {
             return usage();
         }
-        pipeline::PipelineSession session(*topo, cfg);
-        const std::uint64_t num_nodes = topo->num_nodes();
+        pipeline::PipelineSession& session = *session_ptr;
+        const graph::Topology& topo_ref = session.topology();
+        const std::uint64_t num_nodes = topo_ref.num_nodes();
         const std::uint64_t train_count = std::min<std::uint64_t>(std::stoull(opt["train-count"]), num_nodes);
         std::vector<NodeId> train_ids(train_count);
         std::iota(train_ids.begin(), train_ids.end(), NodeId(0));
@@ -148,7 +153,7 @@ int main(int argc, char** argv) {
                      (unsigned long long)num_nodes, (unsigned long long)train_count, cfg.workers, opt["mode"].c_str());
         std::fprintf(stderr, "  M_b=%llu  slots/worker=%llu  feature buffer %.2f MB\n",
                      (unsigned long long)session.max_batch_nodes(), (unsigned long long)session.slots_per_worker(),
-                     double(session.slots_per_worker()) * topo->row_bytes() / 1e6);
+                     double(session.slots_per_worker()) * topo_ref.row_bytes() / 1e6);
         std::uint64_t failed = 0;
         for (std::uint32_t epoch = 0; epoch < epochs; ++epoch) {
             std::string out;
