@@ -2,17 +2,15 @@
 // std::mt19937_64(splitmix64(rng_seed)) as seeded by sample_khop
 // (sampling.hpp:78) and consumed through uniform_int_distribution.
 //
-// The engine is sequential across twists, so one WARP generates one stream with
-// the whole 312-word state in registers: lane l holds x[32k+l] (a[k]) and
-// x[156+32k+l] (b[k]) for k < 5 (k = 4: lanes < 28). In the standard in-place
-// twist, x'[i] (i < 156) = x[i+156] ^ tw(x[i], x[i+1]) and x'[i+156] = x'[i] ^
-// tw(x[i+156], x[i+157]) with x[312] = x'[0]: every neighbour word comes from the
-// next lane (a shuffle) or, at a row end, from lane 0 of the next row -- so a twist
-// is ~20 independent shuffles and 10 twist evaluations, no shared memory and no
-// barrier (the previous one-CTA-per-stream kernel paid a 156-thread barrier per
-// twist: 4x the latency). Four streams per CTA. The latency of a Papers-shaped batch
-// stream is still hidden by generating upcoming batches' streams ahead of time
-// (fdg_sampler_prefetch), but the pipeline's first batch waits for it.
+// The engine is inherently sequential across twists, so one CTA generates one
+// stream: thread i (< 156) keeps x[i] and x[i+156] in registers. In the
+// standard in-place twist, x'[i] (i < 156) needs old x[i], x[i+1], x[i+156];
+// x'[i+156] needs old x[i+156], x[i+157] and NEW x'[i] (own register), except
+// x'[311] which needs x'[0] -- recomputed locally by thread 155 from old
+// x[0], x[1], x[156]. Hence one neighbour exchange and ONE barrier per 312
+// words. Latency (~0.8 ms for a 1.11 M-word stream) is hidden by generating
+// streams for upcoming batches ahead of time (fdg_sampler_prefetch), one CTA
+// per stream.
 #include "fdg_internal.cuh"
 
 namespace fdg {
@@ -38,74 +36,55 @@ __device__ __forceinline__ uint64_t temper(uint64_t z) {
 
 struct MtSeeds {
     uint64_t s[32];
-    uint32_t slot[32];  // output block of stream i = out + slot[i] * stride
-    uint32_t n;         // streams in this launch
+    uint32_t slot[32];  // output block of CTA i = out + slot[i] * stride
 };
 
-constexpr int kMtWarps = 4;  // streams per CTA
-
-__global__ void __launch_bounds__(kMtWarps * 32) k_mt_stream(MtSeeds seeds, uint64_t words, uint64_t* __restrict__ out,
-                                                           uint64_t stride) {
-    __shared__ uint64_t init[kMtWarps][kN];
-    const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const uint32_t sid = blockIdx.x * kMtWarps + warp;
-    if (sid >= seeds.n) return;  // whole warps only: no block-level synchronisation below
-    uint64_t* dst = out + uint64_t(seeds.slot[sid]) * stride;
-    uint64_t* x = init[warp];
-    if (l == 0) {  // [rand.eng.mers] seeding: x_i = f*(x_{i-1} ^ (x_{i-1} >> (w-2))) + i
-        uint64_t v = splitmix64(seeds.s[sid]);
-        x[0] = v;
+__global__ void __launch_bounds__(160) k_mt_stream(MtSeeds seeds, uint64_t words, uint64_t* __restrict__ out,
+                                                   uint64_t stride) {
+    __shared__ uint64_t buf[2][kN];
+    const int i = threadIdx.x;
+    uint64_t* dst = out + uint64_t(seeds.slot[blockIdx.x]) * stride;
+    if (i == 0) {  // [rand.eng.mers] seeding: x_i = f*(x_{i-1} ^ (x_{i-1} >> (w-2))) + i
+        uint64_t x = splitmix64(seeds.s[blockIdx.x]);
+        buf[0][0] = x;
         for (int k = 1; k < kN; ++k) {
-            v = 6364136223846793005ull * (v ^ (v >> 62)) + uint64_t(k);
-            x[k] = v;
+            x = 6364136223846793005ull * (x ^ (x >> 62)) + uint64_t(k);
+            buf[0][k] = x;
         }
     }
-    __syncwarp();
-    uint64_t a[5], b[5];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-        const int i = 32 * k + l;
-        a[k] = i < kM ? x[i] : 0;
-        b[k] = i < kM ? x[i + kM] : 0;
+    __syncthreads();
+    uint64_t a = 0, b = 0;
+    if (i < kM) {
+        a = buf[0][i];
+        b = buf[0][i + kM];
     }
+    __syncthreads();
     const uint64_t twists = (words + kN - 1) / kN;
     for (uint64_t t = 0; t < twists; ++t) {
-        // neighbours x[i+1] and x[i+157] of the OLD state
-        uint64_t an[5], bn[5];
-        const uint64_t b00 = __shfl_sync(0xffffffffu, b[0], 0);  // x[156] (a-row end)
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            const uint64_t ua = __shfl_down_sync(0xffffffffu, a[k], 1);
-            const uint64_t ub = __shfl_down_sync(0xffffffffu, b[k], 1);
-            const uint64_t wa = k < 4 ? __shfl_sync(0xffffffffu, a[k < 4 ? k + 1 : 4], 0) : 0;
-            const uint64_t wb = k < 4 ? __shfl_sync(0xffffffffu, b[k < 4 ? k + 1 : 4], 0) : 0;
-            an[k] = l < 31 ? ua : wa;
-            bn[k] = l < 31 ? ub : wb;
+        uint64_t* s = buf[t & 1];
+        if (i < kM) {
+            s[i] = a;
+            s[i + kM] = b;
         }
-        if (l == kM - 1 - 32 * 4) an[4] = b00;  // i = 155: x[156]
-        uint64_t na[5], nb[5];
-#pragma unroll
-        for (int k = 0; k < 5; ++k) na[k] = b[k] ^ twist(a[k], an[k]);
-        const uint64_t x0 = __shfl_sync(0xffffffffu, na[0], 0);  // x'[0]
-        if (l == kM - 1 - 32 * 4) bn[4] = x0;                   // i = 311: x[312] = x'[0]
-#pragma unroll
-        for (int k = 0; k < 5; ++k) nb[k] = na[k] ^ twist(b[k], bn[k]);
-        const uint64_t base = t * kN;
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            a[k] = na[k];
-            b[k] = nb[k];
-            const int i = 32 * k + l;
-            if (i < kM) {
-                if (base + i < words) dst[base + i] = temper(na[k]);
-                if (base + i + kM < words) dst[base + i + kM] = temper(nb[k]);
+        __syncthreads();
+        if (i < kM) {
+            uint64_t a_next, b_next;
+            if (i < kM - 1) {
+                a_next = s[i + 1];
+                b_next = s[i + kM + 1];
+            } else {
+                a_next = s[kM];                               // old x[156]
+                b_next = s[kM] ^ twist(s[0], s[1]);            // new x'[0]
             }
+            uint64_t na = b ^ twist(a, a_next);                // x'[i]     = x[i+156] ^ tw(x[i], x[i+1])
+            uint64_t nb = na ^ twist(b, b_next);               // x'[i+156] = x'[i]    ^ tw(x[i+156], x[i+157])
+            a = na;
+            b = nb;
+            uint64_t w0 = t * kN + i, w1 = w0 + kM;
+            if (w0 < words) dst[w0] = temper(na);
+            if (w1 < words) dst[w1] = temper(nb);
         }
     }
-}
-
-void launch_chunk(cudaStream_t st, const MtSeeds& p, uint64_t words, uint64_t* out, uint64_t stride) {
-    k_mt_stream<<<(p.n + kMtWarps - 1) / kMtWarps, kMtWarps * 32, 0, st>>>(p, words, out, stride);
 }
 
 }  // namespace
@@ -119,8 +98,7 @@ cudaError_t launch_mt_streams(cudaStream_t st, const uint64_t* rng_seeds, uint32
             p.s[i] = rng_seeds[base + i];
             p.slot[i] = base + i;
         }
-        p.n = k;
-        launch_chunk(st, p, words_per_stream, out_dev, out_stride);
+        k_mt_stream<<<k, 160, 0, st>>>(p, words_per_stream, out_dev, out_stride);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -136,8 +114,7 @@ cudaError_t launch_mt_streams_slots(cudaStream_t st, const uint64_t* rng_seeds, 
             p.s[i] = rng_seeds[base + i];
             p.slot[i] = slots[base + i];
         }
-        p.n = k;
-        launch_chunk(st, p, words_per_stream, ring, stride);
+        k_mt_stream<<<k, 160, 0, st>>>(p, words_per_stream, ring, stride);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

@@ -711,9 +711,6 @@ __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ Group<Id
     if (rejected) {
         atomicAdd(&cnt->rejections, 1u);
         atomicCAS(&cnt->status, 0u, uint32_t(FDG_REJECTION));
-#ifdef FDG_DEBUG_PRINT
-        printf("k_expand rejection l=%u cnt=%p rej=%u status=%u\n", l, cnt, cnt->rejections, cnt->status);
-#endif
     }
 }
 
@@ -817,9 +814,6 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_replay(const __grid_constan
         __syncthreads();
     }
     if (threadIdx.x == 0) cnt->rejections = rejections ? rejections : 1u;
-#ifdef FDG_DEBUG_PRINT
-    if (threadIdx.x == 0) printf("k_replay done cnt=%p rej_in=%u now=%u status=%u words=%u\n", cnt, rejections, cnt->rejections, cnt->status, cnt->words_used);
-#endif
 }
 
 // Debug hook (option "debug_zero_word"): one word of a prefetched MT stream set to 0, which
