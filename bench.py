@@ -191,7 +191,7 @@ def counts_dtype():
     return np.dtype([("status", "<u4"), ("n_nodes", "<u4"), ("n_edges", "<u4"), ("rejections", "<u4"),
                      ("bad_seed", "<u8"), ("checksum", "<u8"), ("bad_seed_pos", "<u4"), ("n_layers", "<u4"),
                      ("layer_nodes", "<u4", (MAX_LAYERS + 2,)), ("layer_edges", "<u4", (MAX_LAYERS + 1,)),
-                     ("layer_draws", "<u4", (MAX_LAYERS + 1,)), ("words_used", "<u4"), ("pad", "<u4")])
+                     ("layer_draws", "<u4", (MAX_LAYERS + 1,)), ("words_used", "<u4"), ("replays", "<u4")])
 
 
 EDGES = {"products": 63_177_558, "papers": 1_613_492_860, "papers_bm": 1_613_492_860, "friendster": 1_813_633_279,

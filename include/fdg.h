@@ -60,7 +60,8 @@ typedef struct {
     uint32_t layer_edges[FDG_MAX_LAYERS + 1]; /* edges before layer l                               */
     uint32_t layer_draws[FDG_MAX_LAYERS + 1]; /* MT19937-64 words before layer l                    */
     uint32_t words_used;
-    uint32_t pad;
+    uint32_t replays;       /* in-stream exact re-runs of the batch (a Lemire rejection, or more MT
+                               words drawn than the prefetched estimate); results are unaffected   */
 } fdg_batch_counts;
 
 typedef struct {

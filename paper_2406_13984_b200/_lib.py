@@ -24,7 +24,7 @@ class BatchCounts(C.Structure):
     _fields_ = [("status", u32), ("n_nodes", u32), ("n_edges", u32), ("rejections", u32),
                 ("bad_seed", u64), ("checksum", u64), ("bad_seed_pos", u32), ("n_layers", u32),
                 ("layer_nodes", u32 * (MAX_LAYERS + 2)), ("layer_edges", u32 * (MAX_LAYERS + 1)),
-                ("layer_draws", u32 * (MAX_LAYERS + 1)), ("words_used", u32), ("pad", u32)]
+                ("layer_draws", u32 * (MAX_LAYERS + 1)), ("words_used", u32), ("replays", u32)]
 
 
 class CtxInfo(C.Structure):

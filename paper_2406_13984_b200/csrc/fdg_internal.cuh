@@ -112,9 +112,12 @@ int generate_feature_shard(Ctx& c, uint64_t seed, uint64_t n, uint32_t dim, uint
 // rng_seeds: HOST array (passed by value to the kernel)
 cudaError_t launch_mt_streams(cudaStream_t st, const uint64_t* rng_seeds, uint32_t n_streams,
                               uint64_t words_per_stream, uint64_t* out_dev, uint64_t out_stride);
-// one CTA per stream, CTA i writing ring + slots[i] * stride
+// one CTA per stream, CTA i writing words [begin, end) (begin a multiple of 312, the last twist
+// completed) of its stream to ring + slots[i] * stride; the 312-word engine state after the
+// last twist is read from / written to state + slots[i] * 312 (state may be null if begin == 0)
 cudaError_t launch_mt_streams_slots(cudaStream_t st, const uint64_t* rng_seeds, const uint32_t* slots,
-                                    uint32_t n_streams, uint64_t words_per_stream, uint64_t* ring, uint64_t stride);
+                                    uint32_t n_streams, uint64_t begin, uint64_t end, uint64_t* ring, uint64_t stride,
+                                    uint64_t* state);
 // gather (fdg_gather.cu)
 int launch_gather(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                   void* out, uint64_t* checksum);
@@ -141,7 +144,8 @@ extern int64_t g_tma_cfg;          // plain TMA gather ring shape 0-3
 extern int64_t g_sampler_sms;      // >0: pipeline samplers on their own green-context SM partition
 extern int64_t g_extract_streams;  // 1 or 2 extraction streams in the pipeline runner
 extern int64_t g_hash_clear;
-extern int64_t g_hash_keep;  // evict_last L2 policy on the batch hash  // 1: clear batch hash tables with a fill kernel, 0: cudaMemsetAsync
+extern int64_t g_hash_keep;
+extern int64_t g_mt_adaptive;  // prefetch the estimated MT draws (1) or the draw bound (0)  // evict_last L2 policy on the batch hash  // 1: clear batch hash tables with a fill kernel, 0: cudaMemsetAsync
 int launch_gather_tma(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                       void* out, uint64_t* checksum, const uint32_t* status);
 int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, const int64_t* alias,

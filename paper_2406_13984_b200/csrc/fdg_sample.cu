@@ -34,6 +34,7 @@
 #include <string>
 
 #include "fdg_internal.cuh"
+#include "fdg_mt.cuh"
 
 namespace fdg {
 namespace {
@@ -169,7 +170,10 @@ struct Work {
     uint4* tile_incl;
     uint32_t* tile_ctr;   // per-pass dynamic tile counters
     const uint64_t* words;
-    uint64_t words_cap;
+    uint64_t words_cap;   // capacity of the word buffer
+    uint64_t words_a;     // words generated before the chain starts (layers < L-1 may use them)
+    uint64_t words_ready; // words generated before the last layer's expansion
+    uint64_t* mt_state;   // engine state after words_ready (null: the stream is complete)
     uint64_t* nodes;      // output
     uint32_t* edges;      // output, {src, dst} pairs
     fdg_batch_counts* cnt;
@@ -220,7 +224,7 @@ __device__ __forceinline__ void seeds_body(const Work<IdT>& W) {
         cnt->bad_seed_pos = 0xFFFFFFFFu;
         cnt->n_layers = W.n_layers;
         cnt->words_used = 0;
-        cnt->pad = 0;
+        cnt->replays = 0;
     }
     for (int i = threadIdx.x; i < FDG_MAX_LAYERS + 2; i += blockDim.x) {
         cnt->layer_nodes[i] = 0;
@@ -538,6 +542,10 @@ template <typename IdT, bool SMALLF, int MODE>
 __device__ __forceinline__ void sample_nodes(const Work<IdT>& W, uint32_t l, uint32_t first, uint32_t stride) {
     fdg_batch_counts* cnt = W.cnt;
     if (cnt->status) return;
+    if (MODE == 0 && cnt->layer_draws[l + 1] > (l + 1 < W.n_layers ? W.words_a : W.words_ready)) {
+        if (first == 0) atomicCAS(&cnt->status, 0u, uint32_t(FDG_REJECTION));  // words beyond the estimate
+        return;
+    }
     const uint32_t fs = cnt->layer_nodes[l];
     const uint32_t F = cnt->layer_nodes[l + 1] - fs;
     const uint32_t eb = cnt->layer_edges[l];
@@ -664,6 +672,13 @@ __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ Group<Id
     const uint64_t db = cnt->layer_draws[l];
     const uint32_t f = W.fan[l];
     const FrontierBuf fr = W.fr[l & 1];
+    // The prefetched stream holds an estimate of the words a batch draws (two pieces: the
+    // early layers', then the rest); a batch drawing more goes to the exact replay, which
+    // extends the stream from the saved engine state.
+    if (cnt->layer_draws[l + 1] > (l + 1 < W.n_layers ? W.words_a : W.words_ready)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(&cnt->status, 0u, uint32_t(FDG_REJECTION));
+        return;
+    }
     const int lane = threadIdx.x & 31, h = lane >> 4, k = lane & 15;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     bool rejected = false;
@@ -788,10 +803,12 @@ __device__ void exact_offsets(const Work<IdT>& W, uint32_t l) {
 template <typename IdT, bool SMALLF>
 __global__ void __launch_bounds__(kScanThreads, 4) k_replay(const __grid_constant__ Group<IdT> G, uint32_t epoch0,
                                                             uint64_t hash_bytes) {
+    __shared__ uint64_t s_mt[2][mt::kN];
     const Work<IdT>& W = G.w[blockIdx.y];
     fdg_batch_counts* cnt = W.cnt;
     if (*reinterpret_cast<volatile uint32_t*>(&cnt->status) != FDG_REJECTION) return;
-    const uint32_t rejections = cnt->rejections;
+    const uint32_t rejections = cnt->rejections, replays = cnt->replays;
+    uint64_t gen = W.words_ready;  // words valid in the stream so far
     __syncthreads();
     // the batch hash back to all-empty (0xFF bytes: key ~0, pending values at their maximum)
     uint4* h = reinterpret_cast<uint4*>(W.tab.base());
@@ -803,6 +820,18 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_replay(const __grid_constan
     else intern_pass<IdT, true, false>(W, 0, epoch0);
     __syncthreads();
     for (uint32_t l = 0; l < W.n_layers; ++l) {
+        // the words layer l can touch: f draws per frontier node plus one per rejection (slack)
+        const uint64_t F = cnt->layer_nodes[l + 1] - cnt->layer_nodes[l];
+        const uint64_t bound = std::min<uint64_t>(W.words_cap, uint64_t(cnt->layer_draws[l]) + F * W.fan[l] + 1024);
+        if (bound > gen) {
+            if (!W.mt_state) {  // a complete stream: nothing to extend (an overflow is FDG_CAPACITY below)
+                gen = W.words_cap;
+            } else {
+                const uint64_t end = std::min<uint64_t>((bound + mt::kN - 1) / mt::kN * mt::kN, W.words_cap);
+                mt::generate(s_mt, 0, gen, end, W.words_cap, const_cast<uint64_t*>(W.words), W.mt_state);
+                gen = end;
+            }
+        }
         exact_offsets<IdT, false>(W, l);
         sample_nodes<IdT, false, 2>(W, l, threadIdx.x, blockDim.x);
         __syncthreads();
@@ -813,7 +842,10 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_replay(const __grid_constan
         else intern_pass<IdT, false, false>(W, l + 1, epoch0 + 1 + l);
         __syncthreads();
     }
-    if (threadIdx.x == 0) cnt->rejections = rejections ? rejections : 1u;
+    if (threadIdx.x == 0) {
+        cnt->rejections = rejections;
+        cnt->replays = replays + 1;
+    }
 }
 
 // Debug hook (option "debug_zero_word"): one word of a prefetched MT stream set to 0, which
@@ -827,6 +859,52 @@ __global__ void k_force_reject(fdg_batch_counts* cnt) {
     }
 }
 
+// Degree statistics behind the prefetch-size estimate: for each layer's fanout f, over
+// `samples` hashed picks of (a) uniform node ids (the seeds' distribution) and (b) uniform
+// edge slots (a frontier node is an in-neighbour: its law is the edge-weighted one),
+// count deg > f and sum min(deg, f). out[(kind * 8 + l) * 2 + {0: gt, 1: sum_min}].
+struct Fans {
+    uint32_t f[FDG_MAX_LAYERS];
+    uint32_t n;
+};
+template <typename IdT>
+__global__ void __launch_bounds__(256) k_degree_stats(const uint64_t* indptr, const IdT* indices, uint64_t N,
+                                                      uint64_t E, Fans fans, uint64_t samples,
+                                                      unsigned long long* out) {
+    uint64_t acc[2][FDG_MAX_LAYERS][2] = {};
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < samples;
+         t += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t v = __umul64hi(splitmix64(t), N);
+        const uint64_t dv = indptr[v + 1] - indptr[v];
+        uint64_t du = dv;
+        if (E) {
+            const uint64_t u = uint64_t(indices[__umul64hi(splitmix64(t ^ 0x5bd1e9955bd1e995ull), E)]);
+            du = indptr[u + 1] - indptr[u];
+        }
+#pragma unroll
+        for (int l = 0; l < FDG_MAX_LAYERS; ++l) {
+            if (l >= int(fans.n)) break;
+            const uint64_t f = fans.f[l];
+            acc[0][l][0] += dv > f;
+            acc[0][l][1] += dv < f ? dv : f;
+            acc[1][l][0] += du > f;
+            acc[1][l][1] += du < f ? du : f;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int l = 0; l < FDG_MAX_LAYERS; ++l)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                if (l >= int(fans.n)) continue;
+                uint64_t x = acc[k][l][j];
+#pragma unroll
+                for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                if ((threadIdx.x & 31) == 0 && x) atomicAdd(out + (k * FDG_MAX_LAYERS + l) * 2 + j, (unsigned long long)x);
+            }
+}
+
 }  // namespace
 
 int64_t g_l2_persist_mb = 0;
@@ -835,6 +913,7 @@ int64_t g_sampler_ctas_per_sm = 16;
 int64_t g_hash_clear = 1;
 int64_t g_extract_streams = 2;
 int64_t g_hash_keep = 1;
+int64_t g_mt_adaptive = 1;  // prefetch the estimated draws (two pieces) instead of the draw bound
 
 namespace {
 // Fill `n16` 16-byte words with all-ones (the empty hash entry), grid-stride.
@@ -891,14 +970,17 @@ struct Sampler {
     uint64_t hash_bytes = 0;   // per lane
     uint32_t* exact_flags = nullptr;  // [changed, total]
     uint64_t* words = nullptr;        // inline MT stream
-    uint64_t words_cap = 0;
+    uint64_t words_cap = 0;           // draw bound + 4096 (the inline stream's length)
+    uint64_t ring_stride = 0;         // ring slot capacity: words_cap rounded up to whole twists
+    uint64_t words_a = 0, words_fast = 0;  // prefetch pieces: [0, words_a), [words_a, words_fast)
+    uint64_t* ring_state = nullptr;   // per ring slot: the 312-word engine state after words_fast
     uint64_t* seeds_buf = nullptr;    // host-API staging
     // prefetch ring
     uint32_t ring_n = 0;
     uint64_t* ring_words = nullptr;
     std::vector<uint64_t> ring_seed;
     std::vector<bool> ring_valid;
-    std::vector<cudaEvent_t> ring_ready, ring_done;
+    std::vector<cudaEvent_t> ring_ready_a, ring_ready, ring_done;  // first piece, whole prefetch, consumed
     uint32_t ring_next = 0;
     cudaStream_t host_stream = nullptr;
     fdg_batch_counts* cnt_buf = nullptr;  // host-API counts
@@ -921,6 +1003,9 @@ struct BatchArgs {  // one batch of a group launch
     uint64_t* nodes;
     uint32_t* edges;
     fdg_batch_counts* cnt;
+    uint64_t words_a = ~0ull, words_ready = ~0ull;  // complete stream unless set
+    uint64_t* mt_state = nullptr;
+    cudaEvent_t ready = nullptr;  // the stream's second piece (waited before the last layer)
 };
 
 namespace {
@@ -955,6 +1040,9 @@ Work<IdT> make_work(Sampler& s, const Lane& ln, const BatchArgs& a) {
     w.tile_ctr = ln.tile_ctr;
     w.words = a.words;
     w.words_cap = a.words_cap;
+    w.words_a = std::min(a.words_a, a.words_cap);
+    w.words_ready = std::min(a.words_ready, a.words_cap);
+    w.mt_state = a.mt_state;
     w.nodes = a.nodes;
     w.edges = a.edges;
     w.cnt = a.cnt;
@@ -1031,6 +1119,9 @@ int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
         {"expand0", "expand1", "expand2", "expand3", "expand4", "expand5", "expand6", "expand7"},
         {"intern1", "intern2", "intern3", "intern4", "intern5", "intern6", "intern7", "intern8"}};
     for (uint32_t l = 0; l < s.n_layers; ++l) {
+        if (l + 1 == s.n_layers)  // the last layer draws from the prefetch's second piece
+            for (uint32_t i = 0; i < n; ++i)
+                if (a[i].ready) FDG_CUDA(cudaStreamWaitEvent(st, a[i].ready, 0));
         {
             FDG_TRACE(names[0][l], st);
             if (s.small_f) {
@@ -1065,6 +1156,65 @@ int dispatch_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) 
 }
 
 
+}  // namespace
+
+void sampler_destroy(Sampler* s);
+
+namespace {
+// How many MT words to prefetch per batch: the expected draws with a 20 % margin (the
+// prefetch is split into the words of the layers before the last one and the rest, so a
+// pipeline's first batch starts sampling after the first piece). Expected draws of layer l
+// = F_l * f_l * P(deg > f_l), F_{l+1} = F_l * E[min(deg, f_l)] (dedup ignored: an upper
+// estimate), with the seeds' degrees uniform over nodes and a frontier node's degree
+// edge-weighted (an in-neighbour), measured on 2^20 hashed samples of the CSR. A batch drawing
+// more than the estimate is re-run exactly in-stream, extending its stream (k_replay).
+int estimate_words(Sampler& s, uint32_t max_seeds) {
+    constexpr uint64_t kN312 = mt::kN;
+    auto round312 = [&](uint64_t w) { return (w + kN312 - 1) / kN312 * kN312; };
+    s.ring_stride = round312(s.words_cap);
+    s.words_a = s.words_fast = s.ring_stride;
+    const Ctx& c = *s.ctx;
+    if (!g_mt_adaptive || (s.words_cap < (1u << 16) && g_mt_adaptive != 2) || c.num_nodes == 0) return FDG_OK;
+    Fans fans{};
+    fans.n = s.n_layers;
+    for (uint32_t l = 0; l < s.n_layers; ++l) fans.f[l] = s.fan[l];
+    unsigned long long* d = nullptr;
+    const size_t bytes = 2 * FDG_MAX_LAYERS * 2 * sizeof(unsigned long long);
+    FDG_CUDA(cudaMalloc(&d, bytes));
+    FDG_CUDA(cudaMemset(d, 0, bytes));
+    const uint64_t samples = 1u << 20;
+    if (c.idx_bytes == 4)
+        k_degree_stats<uint32_t><<<c.sm_count * 4, 256>>>(c.indptr, static_cast<const uint32_t*>(c.indices),
+                                                          c.num_nodes, c.num_edges, fans, samples, d);
+    else
+        k_degree_stats<uint64_t><<<c.sm_count * 4, 256>>>(c.indptr, static_cast<const uint64_t*>(c.indices),
+                                                          c.num_nodes, c.num_edges, fans, samples, d);
+    unsigned long long h[2 * FDG_MAX_LAYERS * 2];
+    cudaError_t e = cudaMemcpy(h, d, bytes, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "degree statistics", __FILE__, __LINE__);
+    double F = double(std::min<uint64_t>(max_seeds, c.num_nodes)), before_last = 0, total = 0;
+    for (uint32_t l = 0; l < s.n_layers; ++l) {
+        const int k = l == 0 ? 0 : 1;
+        const double p_gt = double(h[(k * FDG_MAX_LAYERS + l) * 2]) / double(samples);
+        const double e_min = double(h[(k * FDG_MAX_LAYERS + l) * 2 + 1]) / double(samples);
+        const double w = F * double(s.fan[l]) * p_gt;
+        total += w;
+        if (l + 1 < s.n_layers) before_last += w;
+        F = std::min(F * e_min, double(c.num_nodes));
+    }
+    uint64_t fast = round312(uint64_t(1.2 * total) + 4096);
+    uint64_t a = round312(uint64_t(1.25 * before_last) + 2048);
+    if (g_mt_adaptive == 2) {  // test mode: a deliberately short prefetch, every batch replays
+        fast = round312(fast / 8);
+        a = round312(a / 8);
+    } else if (fast >= s.ring_stride * 9 / 10) {
+        return FDG_OK;  // the bound is nearly reached anyway
+    }
+    s.words_fast = std::min(fast, s.ring_stride);
+    s.words_a = std::min(a, s.words_fast);
+    return FDG_OK;
+}
 }  // namespace
 
 int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32_t n_layers, Sampler** out,
@@ -1170,6 +1320,13 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
     s->cnt_buf = reinterpret_cast<fdg_batch_counts*>(A + o_cnt);
     e = cudaStreamCreateWithFlags(&s->host_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate", __FILE__, __LINE__);
+    {
+        const int rc = estimate_words(*s, max_seeds);
+        if (rc != FDG_OK) {
+            sampler_destroy(s);
+            return rc;
+        }
+    }
     *out = s;
     return FDG_OK;
 }
@@ -1180,9 +1337,11 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
 
 void sampler_destroy(Sampler* s) {
     if (!s) return;
+    for (auto ev : s->ring_ready_a) cudaEventDestroy(ev);
     for (auto ev : s->ring_ready) cudaEventDestroy(ev);
     for (auto ev : s->ring_done) cudaEventDestroy(ev);
     if (s->ring_words) cudaFree(s->ring_words);
+    if (s->ring_state) cudaFree(s->ring_state);
     if (s->out_nodes) cudaFree(s->out_nodes);
     if (s->out_edges) cudaFree(s->out_edges);
     if (s->arena) cudaFree(s->arena);
@@ -1195,18 +1354,25 @@ void sampler_destroy(Sampler* s) {
 int sampler_reserve_ring(Sampler* s, uint32_t n) {
     if (s->ring_n >= n) return FDG_OK;
     FDG_CUDA(cudaDeviceSynchronize());
+    for (auto ev : s->ring_ready_a) cudaEventDestroy(ev);
     for (auto ev : s->ring_ready) cudaEventDestroy(ev);
     for (auto ev : s->ring_done) cudaEventDestroy(ev);
     if (s->ring_words) cudaFree(s->ring_words);
+    if (s->ring_state) cudaFree(s->ring_state);
     s->ring_words = nullptr;
+    s->ring_state = nullptr;
     s->ring_n = 0;
-    FDG_CUDA(cudaMalloc(&s->ring_words, uint64_t(n) * s->words_cap * 8));
+    FDG_CUDA(cudaMalloc(&s->ring_words, uint64_t(n) * s->ring_stride * 8));
+    FDG_CUDA(cudaMalloc(&s->ring_state, uint64_t(n) * mt::kN * 8));
     s->ring_n = n;
     s->ring_seed.assign(n, 0);
     s->ring_valid.assign(n, false);
+    s->ring_ready_a.resize(n);
     s->ring_ready.resize(n);
     s->ring_done.resize(n);
     for (uint32_t i = 0; i < n; ++i) {
+        FDG_CUDA(cudaEventCreateWithFlags(&s->ring_ready_a[i], cudaEventDisableTiming));
+        FDG_CUDA(cudaEventRecord(s->ring_ready_a[i], s->host_stream));
         FDG_CUDA(cudaEventCreateWithFlags(&s->ring_ready[i], cudaEventDisableTiming));
         FDG_CUDA(cudaEventCreateWithFlags(&s->ring_done[i], cudaEventDisableTiming));
         FDG_CUDA(cudaEventRecord(s->ring_done[i], s->host_stream));
@@ -1233,8 +1399,15 @@ int sampler_prefetch(Sampler* s, cudaStream_t st, const uint64_t* rng_seeds, uin
         s->ring_valid[slot] = true;
     }
     {
-        FDG_TRACE("mt", st);
-        FDG_CUDA(launch_mt_streams_slots(st, rng_seeds, slots, n, s->words_cap, s->ring_words, s->words_cap));
+        FDG_TRACE("mt", st);  // piece 1: the words the layers before the last one draw (estimate)
+        FDG_CUDA(launch_mt_streams_slots(st, rng_seeds, slots, n, 0, s->words_a, s->ring_words, s->ring_stride,
+                                         s->ring_state));
+    }
+    for (uint32_t k = 0; k < n; ++k) FDG_CUDA(cudaEventRecord(s->ring_ready_a[slots[k]], st));
+    if (s->words_fast > s->words_a) {
+        FDG_TRACE("mt", st);  // piece 2: up to the estimate of the whole batch, from the saved state
+        FDG_CUDA(launch_mt_streams_slots(st, rng_seeds, slots, n, s->words_a, s->words_fast, s->ring_words,
+                                         s->ring_stride, s->ring_state));
     }
     for (uint32_t k = 0; k < n; ++k) FDG_CUDA(cudaEventRecord(s->ring_ready[slots[k]], st));
     s->ring_next = (s->ring_next + n) % s->ring_n;
@@ -1245,11 +1418,12 @@ int sampler_prefetch(Sampler* s, cudaStream_t st, const uint64_t* rng_seeds, uin
 // the prefetched stream of `rng_seed` (a genuine Lemire rejection), or flag lane `lane` of the
 // next group as rejected. Both are exercised through the in-stream exact replay.
 int sampler_debug_zero_word(Sampler* s, cudaStream_t st, uint64_t rng_seed, uint64_t pos) {
-    if (pos >= s->words_cap) return fail(FDG_INVALID_ARG, "debug_zero_word: position beyond the stream");
+    if (pos >= s->words_a) return fail(FDG_INVALID_ARG, "debug_zero_word: position beyond the stream's first piece");
     for (uint32_t r = 0; r < s->ring_n; ++r)
         if (s->ring_valid[r] && s->ring_seed[r] == rng_seed) {
-            k_poke_zero<<<1, 1, 0, st>>>(s->ring_words + uint64_t(r) * s->words_cap + pos);
+            k_poke_zero<<<1, 1, 0, st>>>(s->ring_words + uint64_t(r) * s->ring_stride + pos);
             FDG_CUDA(cudaGetLastError());
+            FDG_CUDA(cudaEventRecord(s->ring_ready_a[r], st));
             FDG_CUDA(cudaEventRecord(s->ring_ready[r], st));
             return FDG_OK;
         }
@@ -1280,8 +1454,14 @@ int sampler_sample_group(Sampler* s, cudaStream_t st, uint32_t n, const uint64_t
             }
         a[i] = BatchArgs{seeds[i], n_seeds[i], nullptr, s->words_cap, nodes[i], edges[i], cnt[i]};
         if (ring_slot[i] >= 0) {
-            FDG_CUDA(cudaStreamWaitEvent(st, s->ring_ready[ring_slot[i]], 0));
-            a[i].words = s->ring_words + uint64_t(ring_slot[i]) * s->words_cap;
+            const uint32_t r = uint32_t(ring_slot[i]);
+            FDG_CUDA(cudaStreamWaitEvent(st, s->ring_ready_a[r], 0));
+            a[i].words = s->ring_words + uint64_t(r) * s->ring_stride;
+            a[i].words_cap = s->ring_stride;
+            a[i].words_a = s->words_a;
+            a[i].words_ready = s->words_fast;
+            a[i].mt_state = s->ring_state + uint64_t(r) * mt::kN;
+            a[i].ready = s->ring_ready[r];
             s->ring_valid[ring_slot[i]] = false;
         } else {
             if (n_inline > 0) return fail(FDG_INVALID_ARG, "sample_group: at most one batch without a prefetched stream");

@@ -512,7 +512,7 @@ COUNTS_DTYPE = np.dtype([("status", "<u4"), ("n_nodes", "<u4"), ("n_edges", "<u4
                          ("bad_seed", "<u8"), ("checksum", "<u8"), ("bad_seed_pos", "<u4"), ("n_layers", "<u4"),
                          ("layer_nodes", "<u4", (_lib.MAX_LAYERS + 2,)),
                          ("layer_edges", "<u4", (_lib.MAX_LAYERS + 1,)),
-                         ("layer_draws", "<u4", (_lib.MAX_LAYERS + 1,)), ("words_used", "<u4"), ("pad", "<u4")])
+                         ("layer_draws", "<u4", (_lib.MAX_LAYERS + 1,)), ("words_used", "<u4"), ("replays", "<u4")])
 
 
 class Pipeline:

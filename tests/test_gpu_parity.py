@@ -470,6 +470,36 @@ def test_pipeline_rejection_replayed_exactly(fd, port, bm, hook):
         assert st == [int(v) for v in ob.stats()[[0, 1, 3, 5, 6]]]
 
 
+@pytest.mark.parametrize("adaptive", [0, 1, 2])
+def test_pipeline_mt_prefetch_estimate(fd, port, adaptive):
+    """The MT prefetch holds the estimated draws (two pieces) instead of the draw bound:
+    mode 1 (default) must not change any result, mode 2 prefetches an eighth of the estimate
+    so that every batch runs out of words and is re-run exactly in-stream, extending its
+    stream from the saved engine state; mode 0 prefetches the bound. All equal the restatement."""
+    n, B, fan, nb = 400_000, 512, [10, 10, 5], 10
+    t = fd.Topology.generate(n, 16, 16, 11)
+    ip, ix = t.download_topology()
+    table = t.download_rows(0, n)
+    order = np.concatenate(fd.partition_epoch(np.arange(nb * B, dtype=np.uint64), B, 99))
+    rng = np.array([fd.batch_seed(0, 3, b) for b in range(nb)], np.uint64)
+    fd.set_option("mt_adaptive", adaptive)
+    try:
+        pipe = fd.Pipeline(t, fan, B, checksum=True, samplers=3, group_batches=2)
+        recs = pipe.run_batches(order, rng)
+        pipe.close()
+    finally:
+        fd.set_option("mt_adaptive", 1)
+    assert np.all(recs["status"] == 0)
+    for b in range(nb):
+        o = port.sample_khop(ip, ix, order[b * B:(b + 1) * B], fan, int(rng[b]))
+        assert int(recs["n_nodes"][b]) == len(o["nodes"]) and int(recs["words_used"][b]) == o["words_used"], b
+        assert int(recs["checksum"][b]) == port.gather(table, o["nodes"])[1], b
+    if adaptive == 2:
+        assert np.all(recs["replays"] >= 1)
+    else:
+        assert np.all(recs["replays"] == 0)
+
+
 def test_pipeline_sm_partitions(fd):
     """Option sampler_sms: samplers and extraction on disjoint green-context SM partitions
     give the same batches and checksums as the host API."""
