@@ -538,8 +538,11 @@ def run_ours(args):
         line["alias_only"] = _alias_only(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist)
     if args.train and layout == "local":
         line["train_stage"] = _train_stage(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist)
-    if args.per_call and layout == "local" and not frac:
-        line["per_call"] = _per_call(fd, topo, fan, B, seeds_for, rng_of, ids)
+    if not args.no_per_call and layout == "local" and cfg in ("papers", "products"):
+        try:
+            line["per_call"] = _per_call(cfg)
+        except Exception as e:  # noqa: BLE001
+            line["per_call"] = {"error": repr(e)}
     if dist.world == 1 and not args.no_cpu_baseline and layout == "local":
         try:
             line["cpu_baseline"], line["checksum_match_vs_reference"] = _cpu_baseline(cfg, topo, order, args, gpu_cs,
@@ -612,17 +615,27 @@ def _shard_stats(fd, topo, fan, seeds_for, rng_of, ids, rps, shard, rb, ms_per_s
                      "different GPUs)")}
 
 
-def _per_call(fd, topo, fan, B, seeds_for, rng_of, ids):
-    """The reference's per-batch call shape through the C++-shaped Python mirror: one
-    sample_khop + one gather-with-checksum call per batch, host in and out (no pipelining)."""
-    n = min(len(ids), 20)
-    t0 = time.perf_counter()
-    for g, r in zip(ids[:n], rng_of(ids[:n])):
-        b = fd.sample_khop(topo, seeds_for([g]), fan, int(r))
-        fd.gather(topo, b.nodes, checksum=True)
-    secs = time.perf_counter() - t0
-    return {"value": n / secs, "unit": "batches/s", "batches": n,
-            "path": "sample_khop (host seeds -> host nodes/edges) + gather(checksum) per call, synchronous"}
+def _per_call(cfg, batches=50):
+    """The reference's per-call SET loop (tests/cpp/set_loop.cpp: sample_khop -> Extractor::
+    extract_batch -> trainer_step -> release_batch, one batch at a time, host vectors in and
+    out) through the C++ drop-in (include/featdrive_gpu.hpp), at this config's shape, in a
+    separate process (tools/set_loop) on a dataset generated in HBM."""
+    import re
+    import subprocess
+    n, dim, avg, fan, B, t_ids, dtype, frac = CONFIGS[cfg]
+    exe = os.path.join(ROOT, "tools", "set_loop")
+    if not os.path.exists(exe):
+        return {"error": "tools/set_loop not built"}
+    slots = 4 * min(B * (1 + 10 + 100 + 1000), n)  # the reference default N_e * M_b (N_e = 4)
+    p = subprocess.run([exe, "--generate", f"{n}:{dim}:{avg}:{GEN_SEED}", str(slots), str(batches)],
+                       capture_output=True, text=True, timeout=600)
+    m = re.search(r"per_call ([0-9.]+) batches/s", p.stdout)
+    if p.returncode != 0 or not m:
+        return {"error": (p.stderr or p.stdout)[-300:]}
+    return {"value": float(m.group(1)), "unit": "batches/s", "batches": batches, "buffer_slots": slots,
+            "path": "reference-shaped SET loop through the C++ drop-in, one batch per call: graph::sample_khop, "
+                    "extract::Extractor::extract_batch (GPU BufferManager), pipeline::trainer_step, "
+                    "BufferManager::release_batch; host vectors in and out, synchronous"}
 
 
 def _alias_only(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist):
@@ -840,7 +853,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--train", action="store_true",
                     help="also time sample -> extract -> GraphSAGE forward + loss (key train_stage)")
-    ap.add_argument("--per-call", action="store_true", help="also time the reference-shaped per-call SET loop")
+    ap.add_argument("--no-per-call", action="store_true", help="skip the reference-shaped per-call SET loop")
     ap.add_argument("--sync-reference", action="store_true",
                     help="--impl reference: also time PipelineSession::run_sync_reference (BASELINE.md 2 iii)")
     ap.add_argument("--sync-batches", type=int, default=4)

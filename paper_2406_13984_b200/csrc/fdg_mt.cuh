@@ -34,7 +34,7 @@ __device__ __forceinline__ uint64_t temper(uint64_t z) {
     return z;
 }
 
-// Block-level generation (blockDim.x >= 156; every thread of the block must call it):
+// Block-level generation (blockDim.x >= 156, best >= 312; every thread must call it):
 // words [begin, end) of the stream (begin a multiple of 312; the last twist is completed)
 // into dst[w] for w < limit. begin == 0 seeds from splitmix64(rng_seed) ([rand.eng.mers]
 // seeding x_i = f*(x_{i-1} ^ (x_{i-1} >> 62)) + i); otherwise the state after word `begin` is
@@ -63,6 +63,10 @@ __device__ __forceinline__ void generate(uint64_t (*buf)[kN], uint64_t rng_seed,
     }
     __syncthreads();
     const uint64_t t0 = begin / kN, t1 = (end + kN - 1) / kN;
+    // With >= 312 threads, threads 156..311 temper and store twist t-1's words (they sit in
+    // the shared buffer the recurrence threads fill at the start of twist t), so the
+    // recurrence's critical path per twist is one exchange, one barrier and two twist steps.
+    const bool split = blockDim.x >= 2 * kM;
     for (uint64_t t = t0; t < t1; ++t) {
         uint64_t* s = buf[t & 1];
         if (i < kM) {
@@ -83,9 +87,30 @@ __device__ __forceinline__ void generate(uint64_t (*buf)[kN], uint64_t rng_seed,
             const uint64_t nb = na ^ twist(b, b_next);  // x'[i+156] = x'[i]    ^ tw(x[i+156], x[i+157])
             a = na;
             b = nb;
-            const uint64_t w0 = t * kN + i, w1 = w0 + kM;
-            if (w0 < limit) dst[w0] = temper(na);
-            if (w1 < limit) dst[w1] = temper(nb);
+            if (!split) {
+                const uint64_t w0 = t * kN + i, w1 = w0 + kM;
+                if (w0 < limit) dst[w0] = temper(na);
+                if (w1 < limit) dst[w1] = temper(nb);
+            }
+        } else if (split && i < 2 * kM && t > t0) {  // the words of twist t-1
+            const int k = i - kM;
+            const uint64_t w0 = (t - 1) * kN + k, w1 = w0 + kM;
+            if (w0 < limit) dst[w0] = temper(s[k]);
+            if (w1 < limit) dst[w1] = temper(s[k + kM]);
+        }
+    }
+    if (split && t1 > t0) {  // the last twist's words
+        uint64_t* s = buf[t1 & 1];
+        if (i < kM) {
+            s[i] = a;
+            s[i + kM] = b;
+        }
+        __syncthreads();
+        if (i >= kM && i < 2 * kM) {
+            const int k = i - kM;
+            const uint64_t w0 = (t1 - 1) * kN + k, w1 = w0 + kM;
+            if (w0 < limit) dst[w0] = temper(s[k]);
+            if (w1 < limit) dst[w1] = temper(s[k + kM]);
         }
     }
     if (state && i < kM) {
