@@ -145,7 +145,8 @@ extern int64_t g_sampler_sms;      // >0: pipeline samplers on their own green-c
 extern int64_t g_extract_streams;  // 1 or 2 extraction streams in the pipeline runner
 extern int64_t g_hash_clear;
 extern int64_t g_hash_keep;
-extern int64_t g_mt_adaptive;  // prefetch the estimated MT draws (1) or the draw bound (0)  // evict_last L2 policy on the batch hash  // 1: clear batch hash tables with a fill kernel, 0: cudaMemsetAsync
+extern int64_t g_mt_adaptive;
+extern int64_t g_replay;  // prefetch the estimated MT draws (1) or the draw bound (0)  // evict_last L2 policy on the batch hash  // 1: clear batch hash tables with a fill kernel, 0: cudaMemsetAsync
 int launch_gather_tma(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                       void* out, uint64_t* checksum, const uint32_t* status);
 int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, const int64_t* alias,

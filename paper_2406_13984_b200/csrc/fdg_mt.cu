@@ -16,7 +16,7 @@ struct MtSeeds {
     uint32_t slot[32];  // output block of CTA i = out + slot[i] * stride, state at state + slot[i] * 312
 };
 
-__global__ void __launch_bounds__(320) k_mt_stream(MtSeeds seeds, uint64_t begin, uint64_t end, uint64_t limit,
+__global__ void __launch_bounds__(160) k_mt_stream(MtSeeds seeds, uint64_t begin, uint64_t end, uint64_t limit,
                                                    uint64_t* __restrict__ out, uint64_t stride, uint64_t* state) {
     __shared__ uint64_t buf[2][mt::kN];
     const uint64_t slot = seeds.slot[blockIdx.x];
@@ -35,7 +35,7 @@ cudaError_t launch_mt_streams(cudaStream_t st, const uint64_t* rng_seeds, uint32
             p.s[i] = rng_seeds[base + i];
             p.slot[i] = base + i;
         }
-        k_mt_stream<<<k, 320, 0, st>>>(p, 0, words_per_stream, words_per_stream, out_dev, out_stride, nullptr);
+        k_mt_stream<<<k, 160, 0, st>>>(p, 0, words_per_stream, words_per_stream, out_dev, out_stride, nullptr);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -52,7 +52,7 @@ cudaError_t launch_mt_streams_slots(cudaStream_t st, const uint64_t* rng_seeds, 
             p.s[i] = rng_seeds[base + i];
             p.slot[i] = slots[base + i];
         }
-        k_mt_stream<<<k, 320, 0, st>>>(p, begin, end, stride, ring, stride, state);
+        k_mt_stream<<<k, 160, 0, st>>>(p, begin, end, stride, ring, stride, state);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

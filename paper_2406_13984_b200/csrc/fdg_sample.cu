@@ -365,8 +365,11 @@ __device__ __forceinline__ void intern_pass(const Work<IdT>& W, uint32_t q, uint
     }
 }
 
+#ifndef FDG_INTERN_MINB
+#define FDG_INTERN_MINB 1
+#endif
 template <typename IdT, bool SEEDS, bool HAS_NEXT>
-__global__ void __launch_bounds__(kScanThreads) k_intern_s(const __grid_constant__ Group<IdT> G, uint32_t q,
+__global__ void __launch_bounds__(kScanThreads, FDG_INTERN_MINB) k_intern_s(const __grid_constant__ Group<IdT> G, uint32_t q,
                                                            uint32_t epoch) {
     intern_pass<IdT, SEEDS, HAS_NEXT>(G.w[blockIdx.y], q, epoch);
 }
@@ -913,7 +916,8 @@ int64_t g_sampler_ctas_per_sm = 16;
 int64_t g_hash_clear = 1;
 int64_t g_extract_streams = 2;
 int64_t g_hash_keep = 1;
-int64_t g_mt_adaptive = 1;  // prefetch the estimated draws (two pieces) instead of the draw bound
+int64_t g_mt_adaptive = 1;
+int64_t g_replay = 1;  // A/B only: 0 drops the replay launch (rejections then stay visible)  // prefetch the estimated draws (two pieces) instead of the draw bound
 
 namespace {
 // Fill `n16` 16-byte words with all-ones (the empty hash entry), grid-stride.
@@ -1141,7 +1145,7 @@ int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
         k_force_reject<<<1, 1, 0, st>>>(a[s.debug_reject].cnt);
         s.debug_reject = -1;
     }
-    {
+    if (g_replay) {
         FDG_TRACE("replay", st);  // exact re-run of rejected batches (no-op otherwise)
         const uint32_t e0 = next_epoch(s, n);
         for (uint32_t l = 0; l < s.n_layers; ++l) next_epoch(s, n);

@@ -6,6 +6,11 @@ import sys
 import numpy as np
 
 sys.path.insert(0, ".")
+import os  # noqa: E402
+
+from paper_2406_13984_b200 import _lib as _l  # noqa: E402
+if os.environ.get("FDG_DBG_LIB"):  # A/B of a variant build of libfdg.so
+    _l.load.__defaults__ = (os.environ["FDG_DBG_LIB"],)
 import bench  # noqa: E402
 import paper_2406_13984_b200 as fd  # noqa: E402
 from paper_2406_13984_b200 import _lib  # noqa: E402
@@ -25,7 +30,8 @@ f = np.ascontiguousarray(fan, np.uint32)
 defaults = {"gather_impl": 4, "pipeline_gather_impl": 1, "gather_evict_first": 0, "l2_persist_mb": 0, "hash_load_pct": 50,
             "hash_clear": 1, "sampler_ctas_per_sm": 16, "gather_ctas_per_sm": 1,
             "extract_streams": 2, "hash_keep": 1, "gather_dynamic": 1, "hash_kernel": 4,
-            "ws_hashers": 8, "ws_stg": 1, "checksum_impl": 1, "hash_chunk": 0, "gather_pf64": 2, "rb_ctas_per_sm": 2, "rb_chunk": 256, "sampler_sms": 0, "tma_cfg": 0}
+            "ws_hashers": 8, "ws_stg": 1, "checksum_impl": 1, "hash_chunk": 0, "gather_pf64": 2, "rb_ctas_per_sm": 2, "rb_chunk": 256, "sampler_sms": 0, "tma_cfg": 0,
+            "replay": 1, "mt_adaptive": 1}
 for spec in sys.argv[1:]:
     kv = dict(x.split("=") for x in spec.split(",") if x)
     S = int(kv.pop("S", 2))
