@@ -534,6 +534,8 @@ def run_ours(args):
                              extract=False)
             line["replicas"] = {"value": rep["value"], "unit": "batches/s", "ms_per_step": rep["max_ms"] / K,
                                 "layout": "replicated CSR + full table per GPU (no data-path exchange)"}
+    if cfg in HOST_TIER:
+        line["host_tier"] = _host_tier_link(fd, L, timed, rb, max_ms / K)
     if bm_slots:
         line["alias_only"] = _alias_only(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, args, dist)
     if args.train and layout == "local":
@@ -566,6 +568,7 @@ def _timed_run(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, arg
     warm_dev = DeviceBuffer.from_array(seeds_for(ids_warm))
     timed_dev = DeviceBuffer.from_array(seeds_for(ids))
     pipe.run(warm_dev.ptr, False, rng_of(ids_warm))
+    loads_warm = bm_loads(pipe) if bm_slots else None
     dist.barrier()
     ext_ms = np.zeros(K, np.float32)
     with ClockSampler(dev) as clk:
@@ -573,13 +576,24 @@ def _timed_run(fd, topo, fan, B, bm_slots, seeds_for, rng_of, ids, ids_warm, arg
     dist.barrier()
     recs = pipe.records(K)
     xs, xe = pipe.extract_times(K)
+    loads = bm_loads(pipe) if bm_slots else None
     pipe.close()
     if np.any(recs["status"] != 0):
         raise RuntimeError(f"batch status errors in the timed region: {np.unique(recs['status'])}")
     max_ms = dist.reduce(ms, "max")
     return {"n_nodes": recs["n_nodes"].astype(np.int64), "max_ms": max_ms,
+            "loads_per_batch": (loads - loads_warm) / K if loads is not None else None,
             "value": dist.reduce(K, "sum") / (max_ms / 1e3), "ext_ms": ext_ms, "busy_ms": _union_ms(xs, xe),
             "clocks": clk.summary()}
+
+
+def bm_loads(pipe):
+    """Cumulative buffer-manager loads (misses) of a runner."""
+    import paper_2406_13984_b200 as fd
+    from paper_2406_13984_b200._lib import BmStats
+    st = BmStats()
+    fd.featdrive.check(fd.featdrive.lib().fdg_pipeline_bm_stats(pipe.ptr, C.byref(st)))
+    return st.loads
 
 
 def _c4_proxy_table(fd, L, topo, n, dim, dtype, shards):
@@ -613,6 +627,30 @@ def _shard_stats(fd, topo, fan, seeds_for, rng_of, ids, rps, shard, rb, ms_per_s
                      "share costs on 8 B200s" if proxy else
                      "remote rows are loaded one-sided through CUDA IPC peer mappings (NVLink when the ranks own "
                      "different GPUs)")}
+
+
+def _host_tier_link(fd, L, timed, rb, ms_per_step):
+    """The out-of-core tier against its link: the measured pinned host -> device copy peak
+    (1 GiB cudaMemcpy, best of 5) vs the miss rows the buffer manager pulled over it."""
+    nbytes = 1 << 30
+    h, d = C.c_void_p(), C.c_void_p()
+    fd.featdrive.check(L.fdg_host_alloc(C.byref(h), nbytes))
+    fd.featdrive.check(L.fdg_malloc(C.byref(d), nbytes))
+    C.memset(h.value, 1, nbytes)
+    best = 0.0
+    for _ in range(5):
+        t0 = time.perf_counter()
+        fd.featdrive.check(L.fdg_memcpy_h2d(d.value, h.value, nbytes, None))
+        fd.featdrive.check(L.fdg_device_sync())
+        best = max(best, nbytes / (time.perf_counter() - t0) / 1e9)
+    L.fdg_free(d.value)
+    L.fdg_host_free(h.value)
+    loads = timed.get("loads_per_batch")
+    out = {"pcie_h2d_peak_gbs": best, "peak_how": "1 GiB pinned cudaMemcpy H2D, best of 5"}
+    if loads:
+        gbs = loads * rb / (ms_per_step / 1e3) / 1e9
+        out.update({"miss_rows_per_batch": loads, "miss_gbs": gbs, "frac_of_link": gbs / best})
+    return out
 
 
 def _per_call(cfg, batches=50):

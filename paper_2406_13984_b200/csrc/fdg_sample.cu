@@ -984,6 +984,7 @@ struct Sampler {
     uint64_t* ring_words = nullptr;
     std::vector<uint64_t> ring_seed;
     std::vector<bool> ring_valid;
+    std::vector<uint32_t> ring_evt;   // slot -> the slot holding its prefetch chunk's events
     std::vector<cudaEvent_t> ring_ready_a, ring_ready, ring_done;  // first piece, whole prefetch, consumed
     uint32_t ring_next = 0;
     cudaStream_t host_stream = nullptr;
@@ -1371,6 +1372,8 @@ int sampler_reserve_ring(Sampler* s, uint32_t n) {
     s->ring_n = n;
     s->ring_seed.assign(n, 0);
     s->ring_valid.assign(n, false);
+    s->ring_evt.assign(n, 0);
+    for (uint32_t i = 0; i < n; ++i) s->ring_evt[i] = i;
     s->ring_ready_a.resize(n);
     s->ring_ready.resize(n);
     s->ring_done.resize(n);
@@ -1398,22 +1401,27 @@ int sampler_prefetch(Sampler* s, cudaStream_t st, const uint64_t* rng_seeds, uin
     for (uint32_t k = 0; k < n; ++k) {
         uint32_t slot = (s->ring_next + k) % s->ring_n;
         slots[k] = slot;
-        FDG_CUDA(cudaStreamWaitEvent(st, s->ring_done[slot], 0));
         s->ring_seed[slot] = rng_seeds[k];
         s->ring_valid[slot] = true;
+        s->ring_evt[slot] = (s->ring_next) % s->ring_n;  // the chunk's events live at its first slot
     }
+    // Slots are consumed in ring order on the sampler's one stream, so the previous occupant of
+    // the chunk's last slot is the last of them to be released: one wait covers the chunk, and
+    // one pair of events announces it (the host enqueue at a run's start is a few calls per
+    // sampler, not a few per batch).
+    FDG_CUDA(cudaStreamWaitEvent(st, s->ring_done[slots[n - 1]], 0));
     {
         FDG_TRACE("mt", st);  // piece 1: the words the layers before the last one draw (estimate)
         FDG_CUDA(launch_mt_streams_slots(st, rng_seeds, slots, n, 0, s->words_a, s->ring_words, s->ring_stride,
                                          s->ring_state));
     }
-    for (uint32_t k = 0; k < n; ++k) FDG_CUDA(cudaEventRecord(s->ring_ready_a[slots[k]], st));
+    FDG_CUDA(cudaEventRecord(s->ring_ready_a[slots[0]], st));
     if (s->words_fast > s->words_a) {
         FDG_TRACE("mt", st);  // piece 2: up to the estimate of the whole batch, from the saved state
         FDG_CUDA(launch_mt_streams_slots(st, rng_seeds, slots, n, s->words_a, s->words_fast, s->ring_words,
                                          s->ring_stride, s->ring_state));
     }
-    for (uint32_t k = 0; k < n; ++k) FDG_CUDA(cudaEventRecord(s->ring_ready[slots[k]], st));
+    FDG_CUDA(cudaEventRecord(s->ring_ready[slots[0]], st));
     s->ring_next = (s->ring_next + n) % s->ring_n;
     return FDG_OK;
 }
@@ -1427,8 +1435,8 @@ int sampler_debug_zero_word(Sampler* s, cudaStream_t st, uint64_t rng_seed, uint
         if (s->ring_valid[r] && s->ring_seed[r] == rng_seed) {
             k_poke_zero<<<1, 1, 0, st>>>(s->ring_words + uint64_t(r) * s->ring_stride + pos);
             FDG_CUDA(cudaGetLastError());
-            FDG_CUDA(cudaEventRecord(s->ring_ready_a[r], st));
-            FDG_CUDA(cudaEventRecord(s->ring_ready[r], st));
+            FDG_CUDA(cudaEventRecord(s->ring_ready_a[s->ring_evt[r]], st));
+            FDG_CUDA(cudaEventRecord(s->ring_ready[s->ring_evt[r]], st));
             return FDG_OK;
         }
     return fail(FDG_INVALID_ARG, "debug_zero_word: stream not prefetched");
@@ -1459,13 +1467,14 @@ int sampler_sample_group(Sampler* s, cudaStream_t st, uint32_t n, const uint64_t
         a[i] = BatchArgs{seeds[i], n_seeds[i], nullptr, s->words_cap, nodes[i], edges[i], cnt[i]};
         if (ring_slot[i] >= 0) {
             const uint32_t r = uint32_t(ring_slot[i]);
-            FDG_CUDA(cudaStreamWaitEvent(st, s->ring_ready_a[r], 0));
+            if (i == 0 || s->ring_evt[r] != s->ring_evt[uint32_t(ring_slot[i - 1])])
+                FDG_CUDA(cudaStreamWaitEvent(st, s->ring_ready_a[s->ring_evt[r]], 0));
             a[i].words = s->ring_words + uint64_t(r) * s->ring_stride;
             a[i].words_cap = s->ring_stride;
             a[i].words_a = s->words_a;
             a[i].words_ready = s->words_fast;
             a[i].mt_state = s->ring_state + uint64_t(r) * mt::kN;
-            a[i].ready = s->ring_ready[r];
+            a[i].ready = s->ring_ready[s->ring_evt[r]];
             s->ring_valid[ring_slot[i]] = false;
         } else {
             if (n_inline > 0) return fail(FDG_INVALID_ARG, "sample_group: at most one batch without a prefetched stream");
