@@ -198,13 +198,12 @@ int fdg_gather(fdg_ctx* ctx, void* stream, const uint64_t* nodes_dev, const uint
  * claimed dynamically, 256-byte row chunks; other row sizes fall back to the 16-byte LDG/STG
  * kernels); the pipeline runner uses option "pipeline_gather_impl" (default FDG_GATHER_LDG,
  * chunk-striped with dynamic claiming). Sharded tables always take the row-group kernel.
- * The fused-checksum gather uses option "checksum_impl" (default LDG) and "hash_kernel"
- * (default 4: software-pipelined, row size fixed at compile time). */
+ * The fused-checksum gather uses option "checksum_impl" (default LDG: compile-time row-size
+ * kernels for the benchmarked rows, a software-pipelined kernel for other 16-byte multiples,
+ * a generic one otherwise). FDG_GATHER_TMA moves rows with cp.async.bulk (the TMA). */
 #define FDG_GATHER_TMA 0
 #define FDG_GATHER_LDG 1
-#define FDG_GATHER_TMA_WS 2 /* warp-specialised TMA: producer warp + consumer (hashing) warps */
-#define FDG_GATHER_RB 3     /* 32-row groups, 256-byte chunks (the fused-checksum kernel's structure) */
-#define FDG_GATHER_RB_DYN 4 /* the same, 32-row groups claimed dynamically from a per-launch counter */
+#define FDG_GATHER_RB_DYN 4 /* 32-row groups claimed dynamically from a per-launch counter */
 int fdg_set_gather_impl(int impl);
 /* Tuning knobs (process-wide; fdg_api.cu lists all, with their ranges). Main ones:
  * "gather_impl" / "pipeline_gather_impl" / "checksum_impl" (FDG_GATHER_*),

@@ -505,8 +505,7 @@ int fdg_gather(fdg_ctx* c, void* st, const uint64_t* nodes, const uint32_t* n_de
 }
 
 int fdg_set_gather_impl(int impl) {
-    if (impl != FDG_GATHER_TMA && impl != FDG_GATHER_LDG && impl != FDG_GATHER_TMA_WS && impl != FDG_GATHER_RB &&
-        impl != FDG_GATHER_RB_DYN)
+    if (impl != FDG_GATHER_TMA && impl != FDG_GATHER_LDG && impl != FDG_GATHER_RB_DYN)
         return fail(FDG_INVALID_ARG, "unknown gather impl");
     g_gather_impl = impl;
     return FDG_OK;
@@ -533,14 +532,9 @@ int fdg_set_option(const char* key, int64_t v) {
     }
     if (k == "hash_clear") { g_hash_clear = v != 0; return FDG_OK; }
     if (k == "hash_keep") { g_hash_keep = v != 0; return FDG_OK; }
-    if (k == "gather_dynamic") { g_gather_dynamic = v != 0; return FDG_OK; }
-    if (k == "hash_kernel") {
-        if (v < 1 || v > 4) return fail(FDG_INVALID_ARG, "hash_kernel must be in [1, 4]");
-        g_hash_kernel = v;
-        return FDG_OK;
-    }
     if (k == "pipeline_gather_impl") {
-        if (v < 0 || v > FDG_GATHER_RB_DYN) return fail(FDG_INVALID_ARG, "pipeline_gather_impl: unknown gather impl");
+        if (v != FDG_GATHER_TMA && v != FDG_GATHER_LDG && v != FDG_GATHER_RB_DYN)
+            return fail(FDG_INVALID_ARG, "pipeline_gather_impl: unknown gather impl");
         g_pipeline_gather_impl = v;
         return FDG_OK;
     }
@@ -595,14 +589,9 @@ int fdg_set_option(const char* key, int64_t v) {
         return FDG_OK;
     }
     if (k == "checksum_impl") {
-        if (v < -1 || v > FDG_GATHER_TMA_WS) return fail(FDG_INVALID_ARG, "checksum_impl must be -1 or a gather impl");
+        if (v != -1 && v != FDG_GATHER_TMA && v != FDG_GATHER_LDG && v != FDG_GATHER_RB_DYN)
+            return fail(FDG_INVALID_ARG, "checksum_impl must be -1 or a gather impl");
         g_checksum_impl = v;
-        return FDG_OK;
-    }
-    if (k == "ws_stg") { g_ws_stg = v != 0; return FDG_OK; }
-    if (k == "ws_hashers") {
-        if (v < 1 || v > 31) return fail(FDG_INVALID_ARG, "ws_hashers must be in [1, 31]");
-        g_ws_hashers = int(v);
         return FDG_OK;
     }
     if (k == "tma_cfg") {
@@ -638,8 +627,6 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "sampler_ctas_per_sm") *v = g_sampler_ctas_per_sm;
     else if (k == "hash_clear") *v = g_hash_clear;
     else if (k == "hash_keep") *v = g_hash_keep;
-    else if (k == "gather_dynamic") *v = g_gather_dynamic;
-    else if (k == "hash_kernel") *v = g_hash_kernel;
     else if (k == "hash_chunk") *v = g_hash_chunk;
     else if (k == "sage_gemm") *v = g_sage_gemm;
     else if (k == "bm_overlap") *v = g_bm_overlap;
@@ -653,8 +640,6 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "rb_chunk") *v = g_rb_chunk;
     else if (k == "pipeline_gather_impl") *v = g_pipeline_gather_impl;
     else if (k == "checksum_impl") *v = g_checksum_impl;
-    else if (k == "ws_hashers") *v = g_ws_hashers;
-    else if (k == "ws_stg") *v = g_ws_stg;
     else if (k == "extract_streams") *v = g_extract_streams;
     else if (k == "sampler_sms") *v = g_sampler_sms;
     else if (k == "tma_cfg") *v = g_tma_cfg;

@@ -100,39 +100,6 @@ constexpr int kUnroll = 4;
 // saturate HBM while leaving room for the next batch's sampling kernels and the
 // MT prefetch CTAs to co-reside (they run on other streams).
 
-// 16-byte chunk gather over the flattened output.
-template <bool SHARDED>
-__global__ void __launch_bounds__(512) k_gather16(const uint64_t* __restrict__ nodes, const uint32_t* n_dev,
-                                                  uint64_t n_host, const uint32_t* status, TableRef t,
-                                                  FastDiv cdiv, uint32_t cpr, uint4* __restrict__ out) {
-    if (status && *status) return;
-    const uint64_t n = n_dev ? *n_dev : n_host;
-    const uint32_t total = uint32_t(n * cpr);
-    const uint32_t stride = gridDim.x * blockDim.x;
-    const uint64_t pol = gather_policy(t.evict_first);
-    uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    for (; c + (kUnroll - 1) * stride < total; c += kUnroll * stride) {
-        uint4 v[kUnroll];
-        uint32_t cc[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            cc[u] = c + u * stride;
-            uint32_t row = cdiv.div(cc[u]);
-            uint32_t col = cc[u] - row * cpr;
-            const uint4* src = reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, __ldg(nodes + row))) + col;
-            v[u] = ldg_stream(src, pol);
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) stg_stream(out + cc[u], v[u], pol);
-    }
-    for (; c < total; c += stride) {
-        uint32_t row = cdiv.div(c);
-        uint32_t col = c - row * cpr;
-        const uint4* src = reinterpret_cast<const uint4*>(row_ptr<SHARDED>(t, __ldg(nodes + row))) + col;
-        stg_stream(out + c, ldg_stream(src, pol), pol);
-    }
-}
-
 // Dynamically scheduled variant: CTAs claim units of kUnroll * 512 * kDynIters
 // chunks (64 KB) from a per-launch counter, so CTAs that become resident late
 // (the SMs are shared with the samplers' kernels) take less of the work instead
@@ -209,81 +176,15 @@ __global__ void k_gather4(const uint64_t* __restrict__ nodes, const uint32_t* n_
     }
 }
 
-// Gather + trainer checksum for rows that are a multiple of 16 bytes. A warp owns
-// groups of 32 rows (one hashing lane per row) and walks them in 128-byte
-// chunks: lanes load the 32 rows' chunk with coalesced 16-byte loads (8 lanes per
-// 128-byte line), write it to X and stage it in shared memory at a 144-byte row
-// stride, then each lane folds its row's 16 8-byte lanes into its splitmix chain
-// from conflict-free 16-byte shared loads. 16 warps per SM keep ~64 KB of rows in
-// flight while the hash chains of other warps run (hash_bytes64, common.hpp:88-105).
-constexpr int kH16Warps = 8;
-constexpr int kH16Stride = 144;
-
-template <bool SHARDED, bool ALIAS>
-__global__ void __launch_bounds__(kH16Warps * 32, 2)
-    k_gather_hash16(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
-                    const uint32_t* status, TableRef t, char* __restrict__ out, uint64_t* checksum) {
-    __shared__ __align__(16) char smem[kH16Warps][32 * kH16Stride];
-    if (status && *status) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    char* wbuf = smem[warp];
-    const uint32_t rb = t.row_bytes;
-    const uint64_t n = n_dev ? *n_dev : n_host;
-    const uint64_t groups = (n + 31) / 32;
-    const uint64_t pol = gather_policy(t.evict_first);
-    uint64_t sum = 0;
-    for (uint64_t g = blockIdx.x * uint64_t(kH16Warps) + warp; g < groups; g += uint64_t(gridDim.x) * kH16Warps) {
-        const uint64_t r0 = g * 32;
-        const uint32_t rows = uint32_t(n - r0 < 32 ? n - r0 : 32);
-        const uint64_t my_node = lane < int(rows) ? nodes[r0 + lane] : 0;
-        uint64_t h = 0x27d4eb2f165667c5ull ^ (uint64_t(rb) * 0x9e3779b97f4a7c15ull);
-        for (uint32_t c0 = 0; c0 < rb; c0 += 128) {
-            const uint32_t parts = (rb - c0 < 128 ? rb - c0 : 128) >> 4;
-            const uint32_t part = lane & 7;
-            uint4 v[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const uint32_t r = k * 4 + (lane >> 3);
-                const uint64_t node = __shfl_sync(0xffffffffu, my_node, int(r));
-                if (r < rows && part < parts) {
-                    const char* src = ALIAS ? t.base + node * rb : row_ptr<SHARDED>(t, node);
-                    v[k] = ldg_stream(reinterpret_cast<const uint4*>(src + c0) + part, pol);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const uint32_t r = k * 4 + (lane >> 3);
-                if (r < rows && part < parts) {
-                    if (out) stg_stream(reinterpret_cast<uint4*>(out + (r0 + r) * rb + c0) + part, v[k], pol);
-                    *reinterpret_cast<uint4*>(wbuf + r * kH16Stride + part * 16) = v[k];
-                }
-            }
-            __syncwarp();
-            if (lane < int(rows)) {
-                const uint4* p = reinterpret_cast<const uint4*>(wbuf + lane * kH16Stride);
-                for (uint32_t s = 0; s < parts; ++s) {
-                    const uint4 w = p[s];
-                    h = splitmix64(h ^ (uint64_t(w.y) << 32 | w.x));
-                    h = splitmix64(h ^ (uint64_t(w.w) << 32 | w.z));
-                }
-            }
-            __syncwarp();
-        }
-        if (lane < int(rows)) sum += splitmix64(h);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
-}
-
-// Software-pipelined gather + checksum. Same 32-row x 128-byte work items as
-// k_gather_hash16, but each warp issues the loads of its NEXT item (the next
-// chunk of the group, or chunk 0 of its next group) before it hashes the current
-// one from shared memory, so loads stay in flight during the serial splitmix
-// chains instead of alternating with them (hash16's load and hash phases add up:
-// 217 vs 160 us per Papers batch). Up to kHpMinBlocks x 8 warps per SM keep
-// ~128 KB of rows in flight.
+// Software-pipelined gather + checksum for any row size that is a multiple of 16 bytes
+// (k_gather_hash_rb below covers the benchmarked row sizes at compile time): a warp owns
+// 32-row groups walked in 128-byte chunks and issues the loads of its NEXT item (the next
+// chunk of the group, or chunk 0 of its next group) before it hashes the current one from
+// shared memory, so loads stay in flight during the serial splitmix chains (a load-then-
+// hash kernel measured 217 vs 160 us per Papers batch). Up to kHpMinBlocks x 8 warps per SM
+// keep ~128 KB of rows in flight.
 constexpr int kHpWarps = 8;
+constexpr int kH16Stride = 144;  // staged 128-byte chunk row stride (conflict-free 16-byte lane reads)
 constexpr int kHpMinBlocks = 3;
 
 template <bool SHARDED, bool ALIAS>
@@ -392,7 +293,6 @@ struct HashRbShape {
     static constexpr int MINB = CH == 128 ? 3 : 2;
 };
 
-// HASH = false: the same row-group gather without the checksum (FDG_GATHER_RB).
 template <int RB, int CH, bool SHARDED, bool ALIAS, bool HASH = true>
 __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
     k_gather_hash_rb(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
@@ -691,190 +591,6 @@ int launch_gather_rb_dyn(const Ctx& c, cudaStream_t st, const uint64_t* nodes, c
 #undef FDG_GRD
 }
 
-// The plain gather on the row-group structure (FDG_GATHER_RB): 256-byte row chunks, the
-// next chunk's loads issued right after the current chunk's stores.
-template <bool SHARDED>
-int launch_gather_rb(const Ctx& c, cudaStream_t st, uint64_t groups, const uint64_t* nodes, const uint32_t* n_dev,
-                     uint64_t n_host, const uint32_t* status, const TableRef& t, char* out) {
-    const int blocks = int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps,
-                                              uint64_t(c.sm_count) * g_rb_ctas_per_sm));
-#define FDG_GRB(R)                                                                                          \
-    case R:                                                                                                 \
-        k_gather_hash_rb<R, 256, SHARDED, false, false><<<blocks, kHpWarps * 32, 0, st>>>(nodes, n_dev, n_host, \
-                                                                                       status, t, out, nullptr); \
-        return FDG_OK;
-    switch (c.row_bytes) {
-        FDG_GRB(400)
-        FDG_GRB(512)
-        FDG_GRB(1024)
-        FDG_GRB(1536)
-        FDG_GRB(3072)
-        default:
-            return -1;
-    }
-#undef FDG_GRB
-}
-
-// Warp-specialised gather + checksum (LDG): Wc copy warps move 32-row groups
-// table -> X with coalesced 16-byte loads/stores (the flattened (row, part) items
-// of a group are contiguous in X) and stage each group in a shared-memory slot; Wh
-// hash warps fold the staged rows into trainer_step's checksum, two groups per
-// warp so every lane runs two independent splitmix chains (hash_bytes64 is a
-// serial chain per row, common.hpp:88-105: ILP comes from rows, not words).
-// Groups are striped statically over CTAs (group = blockIdx.x + k * gridDim.x).
-// Slot hand-off uses monotonic sequence words in shared memory (filled[s] = k + 1
-// after group k is staged, freed[s] = k + 1 after it is hashed): with many copy
-// warps sharing the ring, a waiter can be several laps ahead, which an mbarrier's
-// phase parity cannot tell apart.
-constexpr int kWsCopyWarps = 20, kWsHashWarps = 4, kWsBatch = 8;
-
-__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
-                 : "=r"(v)
-                 : "r"(uint32_t(__cvta_generic_to_shared(p)))
-                 : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(uint32_t(__cvta_generic_to_shared(p))), "r"(v)
-                 : "memory");
-}
-// lane 0 polls; the warp leaves together (syncwarp orders the other lanes after it)
-__device__ __forceinline__ void wait_seq(const uint32_t* p, uint32_t want) {
-    if ((threadIdx.x & 31) == 0)
-        while (int32_t(ld_acquire_cta(p) - want) < 0) __nanosleep(20);
-    __syncwarp();
-}
-
-template <bool SHARDED, bool ALIAS>
-__global__ void __launch_bounds__((kWsCopyWarps + kWsHashWarps) * 32, 1)
-    k_gather_hash_ws(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
-                     const uint32_t* status, TableRef t, char* __restrict__ out, uint64_t* checksum, uint32_t D) {
-    extern __shared__ __align__(16) char ws_smem[];
-    const uint32_t rb = t.row_bytes, rstride = rb + 16, cpr = rb >> 4;
-    const uint32_t slot_bytes = 32 * rstride;
-    uint32_t* filled = reinterpret_cast<uint32_t*>(ws_smem + size_t(D) * slot_bytes);
-    uint32_t* freed = filled + D;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool skip = status && *status;
-    const uint64_t n = skip ? 0 : (n_dev ? *n_dev : n_host);
-    const uint64_t groups = (n + 31) / 32;
-    const uint64_t nk = blockIdx.x < groups ? (groups - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    for (uint32_t d = threadIdx.x; d < D; d += blockDim.x) {
-        filled[d] = 0;
-        freed[d] = 0;
-    }
-    __syncthreads();
-    const uint64_t pol = gather_policy(t.evict_first);
-    if (warp < kWsCopyWarps) {  // ---- copy warps
-        uint64_t k = warp;
-        uint64_t my_node = 0;
-        if (k < nk) {
-            const uint64_t r = (blockIdx.x + k * gridDim.x) * 32 + lane;
-            my_node = r < n ? nodes[r] : 0;
-        }
-        for (; k < nk; k += kWsCopyWarps) {
-            const uint64_t g = blockIdx.x + k * gridDim.x;
-            const uint32_t rows = uint32_t(n - g * 32 < 32 ? n - g * 32 : 32);
-            const uint64_t nk2 = k + kWsCopyWarps;  // next group's node ids load under this group
-            uint64_t next_node = 0;
-            if (nk2 < nk) {
-                const uint64_t r = (blockIdx.x + nk2 * gridDim.x) * 32 + lane;
-                next_node = r < n ? nodes[r] : 0;
-            }
-            const uint32_t s = uint32_t(k % D);
-            char* slot = ws_smem + size_t(s) * slot_bytes;
-            const uint32_t items = rows * cpr;
-            bool waited = false;
-            for (uint32_t i0 = 0; i0 < items; i0 += 32 * kWsBatch) {
-                uint4 v[kWsBatch];
-#pragma unroll
-                for (int j = 0; j < kWsBatch; ++j) {
-                    const uint32_t i = i0 + j * 32 + lane;
-                    const uint32_t r = i / cpr;
-                    const uint64_t node = __shfl_sync(0xffffffffu, my_node, int(r < 32 ? r : 0));
-                    if (i < items) {
-                        const char* src = ALIAS ? t.base + node * rb : row_ptr<SHARDED>(t, node);
-                        v[j] = ldg_stream(reinterpret_cast<const uint4*>(src) + (i - r * cpr), pol);
-                    }
-                }
-                if (!waited) {  // group k - D (the slot's previous tenant) has been hashed
-                    if (k >= D) wait_seq(&freed[s], uint32_t(k - D + 1));
-                    waited = true;
-                }
-#pragma unroll
-                for (int j = 0; j < kWsBatch; ++j) {
-                    const uint32_t i = i0 + j * 32 + lane;
-                    if (i < items) {
-                        const uint32_t r = i / cpr, p = i - r * cpr;
-                        if (!ALIAS && out) stg_stream(reinterpret_cast<uint4*>(out + g * 32 * rb) + i, v[j], pol);
-                        *reinterpret_cast<uint4*>(slot + r * rstride + p * 16) = v[j];
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) st_release_cta(&filled[s], uint32_t(k + 1));
-            my_node = next_node;
-        }
-    } else {  // ---- hash warps: groups (k, k + 1) for k = 2 hw, 2 hw + 2 Wh, ...
-        const uint32_t hw = warp - kWsCopyWarps;
-        uint64_t sum = 0;
-        const uint64_t seed = 0x27d4eb2f165667c5ull ^ (uint64_t(rb) * 0x9e3779b97f4a7c15ull);
-        for (uint64_t k = 2 * uint64_t(hw); k < nk; k += 2 * kWsHashWarps) {
-            const bool two = k + 1 < nk;
-            const uint32_t sa = uint32_t(k % D), sb = uint32_t((k + 1) % D);
-            const uint64_t ga = blockIdx.x + k * gridDim.x, gb = ga + gridDim.x;
-            const uint32_t ra = uint32_t(n - ga * 32 < 32 ? n - ga * 32 : 32);
-            const uint32_t rb2 = two ? uint32_t(n - gb * 32 < 32 ? n - gb * 32 : 32) : 0;
-            wait_seq(&filled[sa], uint32_t(k + 1));
-            if (two) wait_seq(&filled[sb], uint32_t(k + 2));
-            const uint4* pa = reinterpret_cast<const uint4*>(ws_smem + size_t(sa) * slot_bytes + lane * rstride);
-            const uint4* pb = reinterpret_cast<const uint4*>(ws_smem + size_t(sb) * slot_bytes + lane * rstride);
-            uint64_t ha = seed, hb = seed;
-            const bool la = lane < int(ra), lb = lane < int(rb2);
-            for (uint32_t q = 0; q < cpr; ++q) {
-                const uint4 wa = la ? pa[q] : make_uint4(0, 0, 0, 0);
-                const uint4 wb = lb ? pb[q] : make_uint4(0, 0, 0, 0);
-                ha = splitmix64(ha ^ (uint64_t(wa.y) << 32 | wa.x));
-                hb = splitmix64(hb ^ (uint64_t(wb.y) << 32 | wb.x));
-                ha = splitmix64(ha ^ (uint64_t(wa.w) << 32 | wa.z));
-                hb = splitmix64(hb ^ (uint64_t(wb.w) << 32 | wb.z));
-            }
-            if (la) sum += splitmix64(ha);
-            if (lb) sum += splitmix64(hb);
-            __syncwarp();  // every lane's shared reads of both slots are done
-            if (lane == 0) {
-                st_release_cta(&freed[sa], uint32_t(k + 1));
-                if (two) st_release_cta(&freed[sb], uint32_t(k + 2));
-            }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
-    }
-}
-
-template <bool ALIAS>
-int launch_hash_ws(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
-                   const uint32_t* status, const TableRef& t, char* out, uint64_t* checksum, bool sharded) {
-    constexpr size_t kBudget = 200 * 1024;
-    const size_t slot = 32 * size_t(c.row_bytes + 16) + 8;  // + filled/freed words
-    const uint32_t D = uint32_t(std::min<size_t>(24, kBudget / slot));
-    if (D < 4) return fail(FDG_INVALID_ARG, "gather: row too large for the warp-specialised checksum");
-    const size_t smem = D * slot;
-    static PerDeviceOnce attr[3];
-    auto kfn = ALIAS ? k_gather_hash_ws<false, true> : (sharded ? k_gather_hash_ws<true, false>
-                                                                 : k_gather_hash_ws<false, false>);
-    const int which = ALIAS ? 2 : int(sharded);
-    if (attr[which].first()) {
-        FDG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBudget)));
-    }
-    kfn<<<c.sm_count, (kWsCopyWarps + kWsHashWarps) * 32, smem, st>>>(nodes, n_dev, n_host, status, t, out, checksum, D);
-    FDG_CUDA(cudaGetLastError());
-    return FDG_OK;
-}
-
 constexpr int kHashWarps = 4;
 
 __host__ __device__ __forceinline__ uint32_t hash_stride(uint32_t rb) {
@@ -980,16 +696,57 @@ int64_t g_gather_pf64 = 2;
 int g_gather_ctas_per_sm = 1;
 int64_t g_rb_ctas_per_sm = 2;  // row-group plain gather: CTAs (8 warps) per SM per launch
 int64_t g_rb_chunk = 256;      // row-group plain gather: 128- or 256-byte row chunks
-int64_t g_gather_dynamic = 1;
-// Fused gather + trainer checksum: 1 striped k_gather_hash16, 2 warp-specialised
-// k_gather_hash_ws, 3 software-pipelined k_gather_hash_pipe, 4 the same with a
-// compile-time row size (k_gather_hash_rb; other sizes fall back to 3). 4 on the
-// LDG engine is the default: Papers batch extraction with checksum 175 us vs 242 us
-// (TMA + per-warp hashing, the previous default), Friendster 360 vs 636 us
-// (scripts/ab_checksum.sh).
-int64_t g_hash_kernel = 4;
+// Fused gather + trainer checksum on the LDG engine: k_gather_hash_rb (compile-time row size,
+// 256-byte chunks) for the benchmarked row sizes, k_gather_hash_pipe for other 16-byte
+// multiples, k_gather_hash for the rest. Papers batch extraction with checksum 155 us vs
+// 242 us for TMA + per-warp hashing (the round-1 default), Friendster 312 vs 636 us
+// (scripts/ab_checksum.sh). Round 2 removed the striped and warp-specialised variants that
+// never won an A/B (profiles/README.md, decisions).
 int64_t g_hash_chunk = 0;  // 0: 256-byte chunks for rows >= 256 B, else 128; or force 128 / 256
 int64_t g_checksum_impl = FDG_GATHER_LDG;
+
+namespace {
+// Gather + checksum: the compile-time row-size kernel, else the pipelined one, else generic.
+int launch_checksum(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                    uint64_t n_bound, const uint32_t* status, const TableRef& t, char* out, uint64_t* checksum,
+                    bool sharded, bool alias) {
+    const uint64_t groups = (std::max<uint64_t>(n_bound, 1) + 31) / 32;
+    if (c.row_bytes % 16 == 0) {
+        const int rc = alias ? launch_hash_rb<false, true>(c, st, groups, nodes, n_dev, n_host, status, t, out, checksum)
+                       : sharded ? launch_hash_rb<true, false>(c, st, groups, nodes, n_dev, n_host, status, t, out,
+                                                               checksum)
+                                 : launch_hash_rb<false, false>(c, st, groups, nodes, n_dev, n_host, status, t, out,
+                                                                checksum);
+        if (rc > 0) return rc;
+        if (rc < 0) {  // no compile-time instantiation for this row size
+            const int pb =
+                int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps, uint64_t(c.sm_count) * kHpMinBlocks));
+            if (alias)
+                k_gather_hash_pipe<false, true><<<pb, kHpWarps * 32, 0, st>>>(nodes, n_dev, n_host, status, t, nullptr,
+                                                                             checksum);
+            else if (sharded)
+                k_gather_hash_pipe<true, false><<<pb, kHpWarps * 32, 0, st>>>(nodes, n_dev, n_host, status, t, out,
+                                                                             checksum);
+            else
+                k_gather_hash_pipe<false, false><<<pb, kHpWarps * 32, 0, st>>>(nodes, n_dev, n_host, status, t, out,
+                                                                              checksum);
+        }
+        FDG_CUDA(cudaGetLastError());
+        return FDG_OK;
+    }
+    const size_t smem = size_t(kHashWarps) * 32 * hash_stride(c.row_bytes);
+    if (smem > 200 * 1024) return fail(FDG_INVALID_ARG, "gather: row too large for the fused checksum");
+    static PerDeviceOnce attr_set[3];
+    auto kfn = alias ? k_gather_hash<false, true> : sharded ? k_gather_hash<true> : k_gather_hash<false>;
+    const int which = alias ? 2 : int(sharded);
+    if (attr_set[which].first())
+        FDG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    const int blocks = int(std::min<uint64_t>((groups + kHashWarps - 1) / kHashWarps, uint64_t(c.sm_count) * 8));
+    kfn<<<blocks, kHashWarps * 32, smem, st>>>(nodes, n_dev, n_host, status, t, out, checksum);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+}  // namespace
 
 int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
                         uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status,
@@ -1002,13 +759,13 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
                : pipeline                             ? int(g_pipeline_gather_impl)
                                                       : g_gather_impl;
     if (sharded && impl == FDG_GATHER_LDG && !checksum) impl = FDG_GATHER_RB_DYN;  // shard once per row group
-    if (impl == FDG_GATHER_TMA_WS && launch_gather_ws(c, st, nodes, n_dev, n_host, out, checksum, status,
-                                                      dyn_counter(c)) == FDG_OK)
-        return FDG_OK;
     if (impl == FDG_GATHER_TMA && out &&
         launch_gather_tma(c, st, nodes, n_dev, n_host, out, checksum, status) == FDG_OK)
-        return FDG_OK;  // rows that do not suit the TMA paths fall through to the LDG kernels
-    if (impl == FDG_GATHER_RB_DYN && !checksum && out) {
+        return FDG_OK;  // rows that do not suit the TMA path fall through to the LDG kernels
+    if (checksum)
+        return launch_checksum(c, st, nodes, n_dev, n_host, n_bound, status, t, static_cast<char*>(out), checksum,
+                               sharded, false);
+    if (impl == FDG_GATHER_RB_DYN && out) {
         uint32_t* ctr = dyn_counter(c);
         if (!ctr) return fail(FDG_NOT_LOADED, "gather: context has no work-claim counters");
         const uint64_t groups = (n_bound + 31) / 32;
@@ -1029,85 +786,24 @@ int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, co
             return FDG_OK;
         }
     }
-    if (impl == FDG_GATHER_RB && !checksum && out) {
-        const uint64_t groups = (n_bound + 31) / 32;
-        const int rc = sharded ? launch_gather_rb<true>(c, st, groups, nodes, n_dev, n_host, status, t,
-                                                        static_cast<char*>(out))
-                               : launch_gather_rb<false>(c, st, groups, nodes, n_dev, n_host, status, t,
-                                                         static_cast<char*>(out));
-        if (rc == FDG_OK) {
-            FDG_CUDA(cudaGetLastError());
-            return FDG_OK;
-        }
-    }
-    if (checksum && c.row_bytes % 16 == 0) {
-        uint64_t groups = (n_bound + 31) / 32;
-        int blocks = int(std::min<uint64_t>((groups + kH16Warps - 1) / kH16Warps, uint64_t(c.sm_count) * 2));
-        if (g_hash_kernel == 2 && c.row_bytes <= 2048) {
-            FDG_TRY(launch_hash_ws<false>(c, st, nodes, n_dev, n_host, status, t, static_cast<char*>(out), checksum,
-                                          sharded));
-        } else if (g_hash_kernel >= 3) {
-            const int pb = int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps, uint64_t(c.sm_count) * kHpMinBlocks));
-            const int rc = g_hash_kernel != 4 ? -1
-                           : sharded ? launch_hash_rb<true, false>(c, st, groups, nodes, n_dev, n_host, status, t,
-                                                                   static_cast<char*>(out), checksum)
-                                     : launch_hash_rb<false, false>(c, st, groups, nodes, n_dev, n_host, status, t,
-                                                                    static_cast<char*>(out), checksum);
-            if (rc > 0) return rc;
-            if (rc == FDG_OK) {
-            } else if (sharded)
-                k_gather_hash_pipe<true, false><<<pb, kHpWarps * 32, 0, st>>>(nodes, n_dev, n_host, status, t,
-                                                                             static_cast<char*>(out), checksum);
-            else
-                k_gather_hash_pipe<false, false><<<pb, kHpWarps * 32, 0, st>>>(nodes, n_dev, n_host, status, t,
-                                                                              static_cast<char*>(out), checksum);
-        } else if (sharded) {
-            k_gather_hash16<true, false><<<blocks, kH16Warps * 32, 0, st>>>(nodes, n_dev, n_host, status, t,
-                                                                          static_cast<char*>(out), checksum);
-        } else {
-            k_gather_hash16<false, false><<<blocks, kH16Warps * 32, 0, st>>>(nodes, n_dev, n_host, status, t,
-                                                                           static_cast<char*>(out), checksum);
-        }
-        FDG_CUDA(cudaGetLastError());
-        return FDG_OK;
-    }
-    if (checksum) {
-        size_t smem = size_t(kHashWarps) * 32 * hash_stride(c.row_bytes);
-        static PerDeviceOnce attr_set[2];
-        auto kfn = sharded ? k_gather_hash<true> : k_gather_hash<false>;
-        if (attr_set[sharded].first()) {
-            FDG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        }
-        if (smem > 200 * 1024) return fail(FDG_INVALID_ARG, "gather: row too large for the fused checksum");
-        uint64_t groups = (n_bound + 31) / 32;
-        int blocks = int(std::min<uint64_t>((groups + kHashWarps - 1) / kHashWarps, uint64_t(c.sm_count) * 8));
-        kfn<<<blocks, kHashWarps * 32, smem, st>>>(nodes, n_dev, n_host, status, t, static_cast<char*>(out), checksum);
-        FDG_CUDA(cudaGetLastError());
-        return FDG_OK;
-    }
-    if (c.row_bytes % 16 == 0) {
+    if (c.row_bytes % 16 == 0) {  // chunk-striped 16-byte gather, work claimed dynamically
         uint32_t cpr = c.row_bytes / 16;
         if (n_bound * cpr >= (1ull << 32)) return fail(FDG_INVALID_ARG, "gather: batch too large");
         FastDiv d;
         d.init(cpr);
         uint64_t total = n_bound * cpr;
         int blocks = int(std::min<uint64_t>((total + 511) / 512, uint64_t(c.sm_count) * g_gather_ctas_per_sm));
-        if (g_gather_dynamic) {
-            uint32_t* ctr = dyn_counter(c);
-            if (!ctr) return fail(FDG_NOT_LOADED, "gather: context has no work-claim counters");
-            if (sharded)
-                k_gather16_dyn<true><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr,
-                                                             static_cast<uint4*>(out), ctr);
-            else if (t.pf64)
-                k_gather16_dyn<false, true><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr,
-                                                                    static_cast<uint4*>(out), ctr);
-            else
-                k_gather16_dyn<false><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr,
-                                                              static_cast<uint4*>(out), ctr);
-        } else if (sharded)
-            k_gather16<true><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr, static_cast<uint4*>(out));
+        uint32_t* ctr = dyn_counter(c);
+        if (!ctr) return fail(FDG_NOT_LOADED, "gather: context has no work-claim counters");
+        if (sharded)
+            k_gather16_dyn<true><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr,
+                                                         static_cast<uint4*>(out), ctr);
+        else if (t.pf64)
+            k_gather16_dyn<false, true><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr,
+                                                                static_cast<uint4*>(out), ctr);
         else
-            k_gather16<false><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr, static_cast<uint4*>(out));
+            k_gather16_dyn<false><<<blocks, 512, 0, st>>>(nodes, n_dev, n_host, status, t, d, cpr,
+                                                          static_cast<uint4*>(out), ctr);
     } else {
         uint32_t cpr = c.row_bytes / 4;
         FastDiv d;
@@ -1135,39 +831,8 @@ int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, con
     if (!checksum) return fail(FDG_INVALID_ARG, "checksum: null output");
     TableRef t = table_ref(c);
     t.base = static_cast<const char*>(region);
-    if (c.row_bytes % 16 == 0) {
-        uint64_t groups = (std::max<uint64_t>(n_host, 1) + 31) / 32;
-        int blocks = int(std::min<uint64_t>((groups + kH16Warps - 1) / kH16Warps, uint64_t(c.sm_count) * 2));
-        if (g_hash_kernel == 2 && c.row_bytes <= 2048)
-            FDG_TRY(launch_hash_ws<true>(c, st, reinterpret_cast<const uint64_t*>(alias), n_dev, n_host, status, t,
-                                         nullptr, checksum, false));
-        else if (g_hash_kernel == 4 &&
-                 launch_hash_rb<false, true>(c, st, groups, reinterpret_cast<const uint64_t*>(alias), n_dev, n_host,
-                                             status, t, nullptr, checksum) == FDG_OK) {
-        } else if (g_hash_kernel >= 3)
-            k_gather_hash_pipe<false, true>
-                <<<int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps, uint64_t(c.sm_count) * kHpMinBlocks)),
-                   kHpWarps * 32, 0, st>>>(reinterpret_cast<const uint64_t*>(alias), n_dev, n_host, status, t, nullptr,
-                                           checksum);
-        else
-            k_gather_hash16<false, true><<<blocks, kH16Warps * 32, 0, st>>>(
-                reinterpret_cast<const uint64_t*>(alias), n_dev, n_host, status, t, nullptr, checksum);
-        FDG_CUDA(cudaGetLastError());
-        return FDG_OK;
-    }
-    size_t smem = size_t(kHashWarps) * 32 * hash_stride(c.row_bytes);
-    static PerDeviceOnce attr_set;
-    if (attr_set.first()) {
-        FDG_CUDA(cudaFuncSetAttribute(k_gather_hash<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
-    }
-    if (smem > 200 * 1024) return fail(FDG_INVALID_ARG, "checksum: row too large");
-    uint64_t groups = (std::max<uint64_t>(n_host, 1) + 31) / 32;
-    int blocks = int(std::min<uint64_t>((groups + kHashWarps - 1) / kHashWarps, uint64_t(c.sm_count) * 8));
-    k_gather_hash<false, true><<<blocks, kHashWarps * 32, smem, st>>>(reinterpret_cast<const uint64_t*>(alias), n_dev,
-                                                                     n_host, status, t, nullptr, checksum);
-    FDG_CUDA(cudaGetLastError());
-    return FDG_OK;
+    return launch_checksum(c, st, reinterpret_cast<const uint64_t*>(alias), n_dev, n_host, n_host, status, t, nullptr,
+                           checksum, false, true);
 }
 
 }  // namespace fdg

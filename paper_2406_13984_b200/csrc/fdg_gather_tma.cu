@@ -155,157 +155,6 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1)
     }
 }
 
-// Warp-specialised variant (FDG_GATHER_TMA_WS): one producer warp claims 32-row
-// chunks from a per-launch counter (late-resident CTAs take less work), loads the
-// chunk's node ids one chunk ahead and issues the rows' bulk loads into a ring of
-// D shared-memory stages; H consumer warps each take every H-th chunk, bulk-store
-// its rows to X and, with HASH, fold one row per lane into trainer_step's
-// checksum. Stage hand-off is a full/empty mbarrier pair per stage, so the loads
-// of D - H chunks stay in flight while up to H chunks are being hashed -- the
-// memory stream and the (issue-bound) hash chains overlap inside each SM.
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-
-constexpr uint32_t kWsClaim = 8;  // chunks per claim
-
-struct WsMeta {
-    uint64_t row0;
-    uint32_t rows;
-    uint32_t pad;
-};
-
-template <bool HASH>
-__global__ void __launch_bounds__(1024, 1)
-    k_gather_ws(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host, const uint32_t* status,
-                const char* __restrict__ table, uint32_t rb, uint32_t D, char* __restrict__ out, uint64_t* checksum,
-                uint32_t* ctr, int evict_first, int stg) {
-    extern __shared__ __align__(128) char smem[];
-    const uint32_t rstride = rb + 16;
-    const uint32_t stage_bytes = 32 * rstride;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(D) * stage_bytes);
-    uint64_t* empty = full + D;
-    WsMeta* meta = reinterpret_cast<WsMeta*>(empty + D);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t H = blockDim.x / 32 - 1;
-    const bool skip = status && *status;
-    const uint64_t n = skip ? 0 : (n_dev ? *n_dev : n_host);
-    const uint64_t nchunks = (n + 31) / 32;
-    const uint64_t pol = gather_policy(evict_first);
-    if (threadIdx.x == 0) {
-        for (uint32_t d = 0; d < D; ++d) {
-            mbar_init(smem_u32(&full[d]), 1);
-            mbar_init(smem_u32(&empty[d]), 1);
-        }
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-    if (warp == 0) {  // ---- producer
-        // Claims take kWsClaim chunks at a time and run one claim ahead: the next
-        // claim's atomic and its kWsClaim x 32 node ids are in flight while this
-        // claim's chunks are issued, so neither latency serialises the issue.
-        auto load_ids = [&](uint64_t b, uint64_t (&ids)[kWsClaim]) {
-#pragma unroll
-            for (uint32_t j = 0; j < kWsClaim; ++j) {
-                const uint64_t r = (b + j) * 32 + lane;
-                ids[j] = (b + j < nchunks && r < n) ? __ldg(nodes + r) : 0;
-            }
-        };
-        uint64_t cur[kWsClaim], nxt[kWsClaim];
-        uint32_t pend = lane == 0 ? atomicAdd(ctr, kWsClaim) : 0;
-        uint64_t b0 = __shfl_sync(0xffffffffu, pend, 0);
-        if (b0 < nchunks) load_ids(b0, cur);
-        pend = (b0 < nchunks && lane == 0) ? atomicAdd(ctr, kWsClaim) : 0;
-        uint64_t k = 0;
-        while (b0 < nchunks) {
-            const uint64_t b1 = __shfl_sync(0xffffffffu, pend, 0);
-            if (b1 < nchunks) {
-                load_ids(b1, nxt);
-                pend = lane == 0 ? atomicAdd(ctr, kWsClaim) : 0;
-            }
-#pragma unroll
-            for (uint32_t j = 0; j < kWsClaim; ++j) {
-                const uint64_t g = b0 + j;
-                if (g >= nchunks) break;
-                const uint32_t s = uint32_t(k % D);
-                if (k >= D) mbar_wait(smem_u32(&empty[s]), uint32_t(((k / D) - 1) & 1));
-                const uint64_t row0 = g * 32;
-                const uint32_t rows = uint32_t(n - row0 < 32 ? n - row0 : 32);
-                const uint32_t bar = smem_u32(&full[s]);
-                if (lane == 0) {
-                    meta[s].row0 = row0;
-                    meta[s].rows = rows;
-                    mbar_arrive_expect_tx(bar, rows * rb);
-                }
-                __syncwarp();
-                if (lane < int(rows))
-                    bulk_load(smem_u32(smem + size_t(s) * stage_bytes + lane * rstride), table + cur[j] * rb, rb,
-                              bar, pol);
-                ++k;
-            }
-            b0 = b1;
-#pragma unroll
-            for (uint32_t j = 0; j < kWsClaim; ++j) cur[j] = nxt[j];
-        }
-        // terminators: one per consumer (chunk indices k .. k + H - 1)
-        for (uint32_t t = 0; t < H; ++t, ++k) {
-            const uint32_t s = uint32_t(k % D);
-            if (k >= D) mbar_wait(smem_u32(&empty[s]), uint32_t(((k / D) - 1) & 1));
-            if (lane == 0) {
-                meta[s].rows = 0;
-                mbar_arrive(smem_u32(&full[s]));
-            }
-            __syncwarp();
-        }
-    } else {  // ---- consumers
-        const uint32_t c = warp - 1;
-        uint64_t sum = 0;
-        for (uint64_t k = c;; k += H) {
-            const uint32_t s = uint32_t(k % D);
-            mbar_wait(smem_u32(&full[s]), uint32_t((k / D) & 1));
-            const uint32_t rows = meta[s].rows;
-            if (rows == 0) break;
-            const uint64_t row0 = meta[s].row0;
-            const char* stage = smem + size_t(s) * stage_bytes;
-            const char* srow = stage + lane * rstride;
-            if (out && stg) {  // coalesced 16-byte stores from the staged rows (no TMA op per row)
-                const uint32_t cpr = rb >> 4;
-                for (uint32_t r = 0; r < rows; ++r) {
-                    const uint4* src = reinterpret_cast<const uint4*>(stage + r * rstride);
-                    uint4* dst = reinterpret_cast<uint4*>(out + (row0 + r) * rb);
-                    for (uint32_t c16 = lane; c16 < cpr; c16 += 32) st_stream(dst + c16, src[c16], pol);
-                }
-            }
-            if (lane < int(rows)) {
-                if (out && !stg) {
-                    bulk_store(out + (row0 + lane) * rb, smem_u32(srow), rb, pol);
-                    bulk_commit();
-                }
-                if (HASH) sum += hash_row16(srow, rb);
-                if (out && !stg) bulk_wait_read<0>();
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
-        }
-        if (out && !stg) bulk_wait_all();
-        if (HASH) {
-#pragma unroll
-            for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-            if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {  // the last CTA resets the claim counter pair
-        __threadfence();
-        if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
-            ctr[0] = 0;
-            ctr[1] = 0;
-            __threadfence();
-        }
-    }
-}
-
-constexpr int kD = 8, kA = 6;     // plain gather: 8 stages, 6 chunks of loads in flight per warp
 constexpr int kDh = 3, kAh = 2;   // fused checksum: 32-row stages for one-row-per-lane hashing
 constexpr size_t kSmemBudget = 200 * 1024;
 constexpr size_t kSmemMax = 227 * 1024;
@@ -343,30 +192,4 @@ int launch_gather_tma(const Ctx& c, cudaStream_t st, const uint64_t* nodes, cons
 }
 
 int64_t g_tma_cfg = 0;  // plain TMA gather ring shape (launch_gather_tma)
-int g_ws_hashers = 8;  // consumer warps per CTA of k_gather_ws
-int g_ws_stg = 1;      // k_gather_ws stores X with 16-byte STG (1) or per-row bulk copies (0)
-
-// Warp-specialised TMA gather; FDG_INVALID_ARG if the shape does not suit it.
-int launch_gather_ws(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
-                     void* out, uint64_t* checksum, const uint32_t* status, uint32_t* ctr) {
-    const uint32_t rb = c.row_bytes;
-    if (rb % 16 || c.n_shards != 1 || rb > 2048 || !ctr) return FDG_INVALID_ARG;
-    const uint32_t H = uint32_t(std::max(1, std::min(g_ws_hashers, 31)));
-    const size_t stage = 32 * size_t(rb + 16);
-    const size_t meta = 8 * 2 + 16;  // full + empty barriers + WsMeta per stage
-    const uint32_t D = uint32_t(std::min<size_t>(32, kSmemBudget / (stage + meta)));
-    if (D < H + 2) return FDG_INVALID_ARG;
-    const size_t smem = D * (stage + meta);
-    static PerDeviceOnce attr[2];
-    auto kfn = checksum ? k_gather_ws<true> : k_gather_ws<false>;
-    if (attr[checksum != nullptr].first()) {
-        FDG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBudget)));
-    }
-    kfn<<<c.sm_count, (H + 1) * 32, smem, st>>>(nodes, n_dev, n_host, status,
-                                                static_cast<const char*>(c.shard_bases[0]), rb, D,
-                                                static_cast<char*>(out), checksum, ctr, g_gather_evict_first, g_ws_stg);
-    FDG_CUDA(cudaGetLastError());
-    return FDG_OK;
-}
-
 }  // namespace fdg

@@ -121,32 +121,31 @@ cudaError_t launch_mt_streams_slots(cudaStream_t st, const uint64_t* rng_seeds, 
 // gather (fdg_gather.cu)
 int launch_gather(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                   void* out, uint64_t* checksum);
-extern int g_gather_impl;  // FDG_GATHER_TMA (default) or FDG_GATHER_LDG
-extern int g_gather_evict_first;
-extern int64_t g_gather_pf64;  // 64-byte L2 fetch hint on table reads (0 off, 1 on, 2 rows % 128 != 0)
-extern int g_gather_ctas_per_sm;
-extern int64_t g_rb_ctas_per_sm;
-extern int64_t g_rb_chunk;
-extern int64_t g_gather_dynamic;
-extern int64_t g_hash_kernel;
-extern int64_t g_sage_gemm;
-extern int64_t g_bm_overlap;  // buffer-manager row move on its own stream (1) or after the metadata (0)  // train-stage GEMMs: 1 tensor cores (3xTF32), 0 CUDA cores
-extern int64_t g_hash_chunk;  // k_gather_hash_rb staging chunk (0 = by row size)
-extern int64_t g_checksum_impl;  // gather impl for the fused-checksum path (-1: same as g_gather_impl)
-extern int g_ws_hashers;
-extern int g_ws_stg;
-int launch_gather_ws(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
-                     void* out, uint64_t* checksum, const uint32_t* status, uint32_t* ctr);  // fused gather+checksum kernel variant (A/B)  // k_gather16_dyn (atomic work claiming) instead of a fixed grid-stride split
-extern int64_t g_l2_persist_mb;
-extern int64_t g_hash_load_pct;
-extern int64_t g_sampler_ctas_per_sm;
-extern int64_t g_tma_cfg;          // plain TMA gather ring shape 0-3
-extern int64_t g_sampler_sms;      // >0: pipeline samplers on their own green-context SM partition
-extern int64_t g_extract_streams;  // 1 or 2 extraction streams in the pipeline runner
-extern int64_t g_hash_clear;
-extern int64_t g_hash_keep;
-extern int64_t g_mt_adaptive;
-extern int64_t g_replay;  // prefetch the estimated MT draws (1) or the draw bound (0)  // evict_last L2 policy on the batch hash  // 1: clear batch hash tables with a fill kernel, 0: cudaMemsetAsync
+// Tuning options (fdg_set_option; defaults are the measured best, profiles/README.md)
+extern int g_gather_impl;             // standalone fdg_gather engine (FDG_GATHER_RB_DYN)
+extern int64_t g_pipeline_gather_impl;  // gather engine of the pipeline runner (FDG_GATHER_LDG)
+extern int64_t g_checksum_impl;       // engine of the fused-checksum gather (-1: same as g_gather_impl)
+extern int g_gather_evict_first;      // L2 evict-first hints on the gather (0 off)
+extern int64_t g_gather_pf64;         // 64-byte L2 fetch hint on table reads (0 off, 1 on, 2 rows % 128 != 0)
+extern int g_gather_ctas_per_sm;      // chunk-striped gather: CTAs (512 threads) per SM
+extern int64_t g_rb_ctas_per_sm;      // row-group gather: CTAs (8 warps) per SM
+extern int64_t g_rb_chunk;            // row-group gather: 128- or 256-byte row chunks
+extern int64_t g_hash_chunk;          // k_gather_hash_rb staging chunk (0 = by row size)
+extern int64_t g_tma_cfg;             // TMA gather ring shape 0-3
+extern int64_t g_sage_gemm;           // train-stage GEMMs: 1 tensor cores (3xTF32), 0 CUDA cores
+extern int64_t g_bm_overlap;          // buffer-manager row move on its own stream (1) or after the metadata (0)
+extern int64_t g_bm_eager;            // buffer managers created in eager-invalidation (debug) mode
+extern int64_t g_l2_persist_mb;       // L2 set-aside for the samplers' hash tables (0 off)
+extern int64_t g_hash_load_pct;       // batch hash sizing (load factor, %)
+extern int64_t g_sampler_ctas_per_sm; // sampler kernels: CTA cap per SM per launch
+extern int64_t g_sampler_sms;         // > 0: pipeline samplers on their own green-context SM partition
+extern int64_t g_extract_streams;     // 1 or 2 extraction streams in the pipeline runner
+extern int64_t g_hash_clear;          // 1: clear batch hash tables with a fill kernel, 0: cudaMemsetAsync
+extern int64_t g_hash_keep;           // evict_last L2 policy on the batch hash
+extern int64_t g_mt_adaptive;         // prefetch the estimated MT draws (1), the draw bound (0), test (2)
+extern int64_t g_replay;              // A/B only: 0 drops the in-stream replay launch
+extern int64_t g_debug_zero_word;     // pipeline test hook (option debug_zero_word)
+extern int64_t g_debug_reject_batch;  // pipeline test hook (option debug_reject_batch)
 int launch_gather_tma(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                       void* out, uint64_t* checksum, const uint32_t* status);
 int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, const int64_t* alias,
@@ -157,8 +156,4 @@ uint32_t* dyn_counter(const Ctx& c);
 int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
                         uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status,
                         bool pipeline = false);
-extern int64_t g_pipeline_gather_impl;
-extern int64_t g_bm_eager;
-extern int64_t g_debug_zero_word;     // pipeline test hook (option debug_zero_word)
-extern int64_t g_debug_reject_batch;  // pipeline test hook (option debug_reject_batch)  // buffer manager created in eager-invalidation (debug) mode  // gather engine of the pipeline runner (default LDG)
 }  // namespace fdg
