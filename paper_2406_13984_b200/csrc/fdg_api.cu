@@ -562,6 +562,10 @@ int fdg_set_option(const char* key, int64_t v) {
         g_mt_adaptive = v;
         return FDG_OK;
     }
+    if (k == "prefetch_upfront") {  // A/B only
+        g_prefetch_upfront = v != 0;
+        return FDG_OK;
+    }
     if (k == "replay") {  // A/B only
         g_replay = v != 0;
         return FDG_OK;
@@ -634,6 +638,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "debug_zero_word") *v = g_debug_zero_word;
     else if (k == "mt_adaptive") *v = g_mt_adaptive;
     else if (k == "replay") *v = g_replay;
+    else if (k == "prefetch_upfront") *v = g_prefetch_upfront;
     else if (k == "debug_reject_batch") *v = g_debug_reject_batch;
     else if (k == "gather_pf64") *v = g_gather_pf64;
     else if (k == "rb_ctas_per_sm") *v = g_rb_ctas_per_sm;

@@ -92,6 +92,7 @@ using namespace fdg;
 
 int64_t fdg::g_bm_overlap = 1;
 int64_t fdg::g_sampler_sms = 0;
+int64_t fdg::g_prefetch_upfront = 0;    // A/B: all samplers' first MT chunks before any sampling
 int64_t fdg::g_debug_zero_word = -1;     // (batch of the run << 24) | word position; -1 = off
 int64_t fdg::g_debug_reject_batch = -1;  // batch of the run flagged as rejected; -1 = off
 
@@ -458,7 +459,10 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
         FDG_CUDA(cudaStreamWaitEvent(p->mstream[s], t0, 0));
     }
     if (p->xstream2) FDG_CUDA(cudaStreamWaitEvent(p->xstream2, t0, 0));
-    for (uint32_t s = 0; s < S; ++s) FDG_TRY(prefetch_upto(s, PG));
+    // The first chunk of each sampler's streams is requested right before that sampler's first
+    // group (in the loop below), so batch 0's chain is enqueued behind one prefetch, not S.
+    if (g_prefetch_upfront)
+        for (uint32_t s = 0; s < S; ++s) FDG_TRY(prefetch_upto(s, PG));
     for (uint64_t g = 0; g < n_groups; ++g) {
         const uint64_t j0 = g * G, j1 = std::min<uint64_t>(j0 + G, n_batches);
         const uint32_t n = uint32_t(j1 - j0);

@@ -29,8 +29,8 @@ seeds = DeviceBuffer.from_array(np.ascontiguousarray(np.concatenate([order[(b % 
 f = np.ascontiguousarray(fan, np.uint32)
 defaults = {"gather_impl": 4, "pipeline_gather_impl": 1, "gather_evict_first": 0, "l2_persist_mb": 0, "hash_load_pct": 50,
             "hash_clear": 1, "sampler_ctas_per_sm": 16, "gather_ctas_per_sm": 1,
-            "extract_streams": 2, "hash_keep": 1, "gather_dynamic": 1, "hash_kernel": 4,
-            "ws_hashers": 8, "ws_stg": 1, "checksum_impl": 1, "hash_chunk": 0, "gather_pf64": 2, "rb_ctas_per_sm": 2, "rb_chunk": 256, "sampler_sms": 0, "tma_cfg": 0,
+            "extract_streams": 2, "hash_keep": 1,
+            "checksum_impl": 1, "hash_chunk": 0, "gather_pf64": 2, "rb_ctas_per_sm": 2, "rb_chunk": 256, "sampler_sms": 0, "tma_cfg": 0,
             "replay": 1, "mt_adaptive": 1}
 for spec in sys.argv[1:]:
     kv = dict(x.split("=") for x in spec.split(",") if x)

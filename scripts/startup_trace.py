@@ -30,6 +30,12 @@ rng = np.array([L.fdg_batch_seed(0, 0, int(g)) for g in range(K)], np.uint64)
 seeds = DeviceBuffer.from_array(np.ascontiguousarray(order[:K * B]))
 pipe = fd.Pipeline(topo, fan, B, samplers=S)
 pipe.run(seeds.ptr, False, rng)  # warm-up
+for rep in range(3):  # untraced: time to the first extraction and host enqueue
+    ext = np.zeros(K, np.float32)
+    ms = pipe.run(seeds.ptr, False, rng, extract_ms=ext)
+    xs, xe = pipe.extract_times(K)
+    print(f"untraced run {rep}: {ms:.3f} ms, {ms / K * 1e3:.1f} us/batch, batch 0 extraction {xs[0]:.3f}-{xe[0]:.3f} ms, "
+          f"host enqueue {pipe.host_enqueue_ms():.3f} ms")
 L.fdg_trace_enable(1)
 ext = np.zeros(K, np.float32)
 ms = pipe.run(seeds.ptr, False, rng, extract_ms=ext)
