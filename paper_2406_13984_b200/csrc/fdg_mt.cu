@@ -18,10 +18,12 @@ struct MtSeeds {
 
 __global__ void __launch_bounds__(160) k_mt_stream(MtSeeds seeds, uint64_t begin, uint64_t end, uint64_t limit,
                                                    uint64_t* __restrict__ out, uint64_t stride, uint64_t* state) {
-    __shared__ uint64_t buf[2][mt::kN];
+    __shared__ uint64_t buf[1][mt::kN];
+    __shared__ mt::MtPub pub[8][5];
+    __shared__ int64_t flag[5];
     const uint64_t slot = seeds.slot[blockIdx.x];
-    mt::generate(buf, seeds.s[blockIdx.x], begin, end, limit, out + slot * stride,
-                 state ? state + slot * mt::kN : nullptr);
+    mt::generate_ring(buf, pub, flag, seeds.s[blockIdx.x], begin, end, limit, out + slot * stride,
+                      state ? state + slot * mt::kN : nullptr);
 }
 
 }  // namespace
