@@ -18,12 +18,15 @@ struct MtSeeds {
 
 __global__ void __launch_bounds__(160) k_mt_stream(MtSeeds seeds, uint64_t begin, uint64_t end, uint64_t limit,
                                                    uint64_t* __restrict__ out, uint64_t stride, uint64_t* state) {
-    __shared__ uint64_t buf[1][mt::kN];
-    __shared__ mt::MtPub pub[8][5];
-    __shared__ int64_t flag[5];
+    // One CTA of 160 threads per stream with one barrier per twist (fdg_mt.cuh). Measured
+    // alternatives, per 568 k words under ncu: a warp-per-stream kernel 2.5x slower (one SMSP
+    // does all 312 words of a twist), a 5-warp ring synchronised by shared-memory flags
+    // instead of the barrier 760 vs 549 us, 320 threads with the tempering on the second
+    // half 1.09 vs 0.81 ms per 1.11 M words.
+    __shared__ uint64_t buf[2][mt::kN];
     const uint64_t slot = seeds.slot[blockIdx.x];
-    mt::generate_ring(buf, pub, flag, seeds.s[blockIdx.x], begin, end, limit, out + slot * stride,
-                      state ? state + slot * mt::kN : nullptr);
+    mt::generate(buf, seeds.s[blockIdx.x], begin, end, limit, out + slot * stride,
+                 state ? state + slot * mt::kN : nullptr);
 }
 
 }  // namespace

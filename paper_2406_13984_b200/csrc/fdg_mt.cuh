@@ -121,88 +121,5 @@ __device__ __forceinline__ void generate(uint64_t (*buf)[kN], uint64_t rng_seed,
     __syncthreads();
 }
 
-// Barrier-free variant for a CTA of exactly 5 warps (160 threads). Warp w holds
-// x[32w + l] and x[156 + 32w + l]; within a twist every neighbour word comes from the next
-// lane (a shuffle) except at a warp's last lane, which needs lane 0 of the next warp (and
-// warp 4's last row, x[155], needs x[156] and x'[0] = x[156] ^ tw(x[0], x[1]) from warp 0).
-// So a warp waits only for its successor to publish those words for the twist (a flag in
-// shared memory), never for the whole CTA: the warps form a ring and run at most 4 twists
-// apart (8 publish slots). Same words, same state, same arguments as generate().
-struct alignas(16) MtPub {
-    uint64_t a0, b0, a1, pad;
-};
-__device__ __forceinline__ void generate_ring(uint64_t (*buf)[kN], MtPub (*pub)[5], volatile int64_t* flag,
-                                              uint64_t rng_seed, uint64_t begin, uint64_t end, uint64_t limit,
-                                              uint64_t* __restrict__ dst, uint64_t* state) {
-    const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-    const int i = 32 * w + l;
-    const bool valid = i < kM;
-    if (begin == 0) {
-        if (tid == 0) {
-            uint64_t x = splitmix64(rng_seed);
-            buf[0][0] = x;
-            for (int k = 1; k < kN; ++k) {
-                x = 6364136223846793005ull * (x ^ (x >> 62)) + uint64_t(k);
-                buf[0][k] = x;
-            }
-        }
-    } else {
-        for (int k = tid; k < kN; k += blockDim.x) buf[0][k] = state[k];
-    }
-    if (tid < 5) flag[tid] = -1;
-    __syncthreads();
-    uint64_t a = valid ? buf[0][i] : 0, b = valid ? buf[0][i + kM] : 0;
-    const uint64_t t0 = begin / kN, t1 = (end + kN - 1) / kN;
-    const int succ = w == 4 ? 0 : w + 1;
-    const int last = w == 4 ? kM - 1 - 128 : 31;  // the lane whose neighbours live in the next warp
-    auto publish = [&](uint64_t t) {
-        const uint64_t a1 = __shfl_sync(0xffffffffu, a, 1);
-        if (l == 0) {
-            MtPub& p = pub[t & 7][w];
-            p.a0 = a;
-            p.b0 = b;
-            p.a1 = a1;
-            __threadfence_block();
-            flag[w] = int64_t(t);
-        }
-        __syncwarp();
-    };
-    publish(t0);
-    for (uint64_t t = t0; t < t1; ++t) {
-        // old neighbours: the next lane's words; at the warp's last lane, the successor's
-        const uint64_t ua = __shfl_down_sync(0xffffffffu, a, 1), ub = __shfl_down_sync(0xffffffffu, b, 1);
-        uint64_t an = ua, bn = ub;
-        if (l == last) {
-            while (flag[succ] < int64_t(t)) {
-            }
-            __threadfence_block();
-            const volatile MtPub& p = pub[t & 7][succ];
-            const uint64_t pa0 = p.a0, pb0 = p.b0;
-            if (w < 4) {
-                an = pa0;  // x[32(w+1)]
-                bn = pb0;  // x[156 + 32(w+1)]
-            } else {
-                an = pb0;                      // x[156]
-                bn = pb0 ^ twist(pa0, p.a1);   // x'[0]
-            }
-        }
-        const uint64_t na = b ^ twist(a, an);   // x'[i]     = x[i+156] ^ tw(x[i], x[i+1])
-        const uint64_t nb = na ^ twist(b, bn);  // x'[i+156] = x'[i]    ^ tw(x[i+156], x[i+157])
-        a = na;
-        b = nb;
-        publish(t + 1);
-        if (valid) {
-            const uint64_t w0 = t * kN + i, w1 = w0 + kM;
-            if (w0 < limit) dst[w0] = temper(na);
-            if (w1 < limit) dst[w1] = temper(nb);
-        }
-    }
-    if (state && valid) {
-        state[i] = a;
-        state[i + kM] = b;
-    }
-    __syncthreads();
-}
-
 }  // namespace mt
 }  // namespace fdg
