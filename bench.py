@@ -619,9 +619,9 @@ def _shard_stats(fd, topo, fan, seeds_for, rng_of, ids, rps, shard, rb, ms_per_s
         total += len(nodes)
     share = remote / max(total, 1)
     remote_bytes = share * (total / max(len(ids), 1)) * rb
-    nvl = 900e9  # NVLink 5 per direction per GPU (B200_PROFILING.md)
+    nvl = 770e9  # measured NVLink 5 peer copy per direction per GPU (B200_PROFILING.md; 900 nominal)
     return {"rows_per_shard": int(rps), "remote_row_share": share, "remote_bytes_per_batch": remote_bytes,
-            "nvlink_floor_ms_per_batch": remote_bytes / nvl * 1e3, "ms_per_step": ms_per_step,
+            "nvlink_floor_ms_per_batch": remote_bytes / nvl * 1e3, "nvlink_gbs_basis": "770 GB/s measured peer copy", "ms_per_step": ms_per_step,
             "note": ("proxy: remote rows are read from the aliased local shard (HBM), so ms_per_step is the "
                      "sampling + gather cost with remote reads at HBM speed; the NVLink floor is what the remote "
                      "share costs on 8 B200s" if proxy else

@@ -88,6 +88,9 @@ int fdg_version(void);
 /* ---- device plumbing (so callers need no CUDA runtime of their own) ---------- */
 int fdg_device_count(int* n);
 int fdg_set_device(int device);
+/* Loads and stores of `device` may address `peer`'s memory directly (NVLink); used by a
+ * single process that installs another GPU's shard with fdg_ctx_set_feature_shards. */
+int fdg_enable_peer_access(int device, int peer);
 int fdg_malloc(void** ptr_dev, uint64_t bytes);
 int fdg_free(void* ptr_dev);
 int fdg_host_alloc(void** ptr, uint64_t bytes); /* pinned */

@@ -50,6 +50,7 @@ SIGNATURES = {
     "fdg_version": (ci, []),
     "fdg_device_count": (ci, [C.POINTER(ci)]),
     "fdg_set_device": (ci, [ci]),
+    "fdg_enable_peer_access": (ci, [ci, ci]),
     "fdg_malloc": (ci, [C.POINTER(vp), u64]),
     "fdg_free": (ci, [vp]),
     "fdg_host_alloc": (ci, [C.POINTER(vp), u64]),

@@ -104,6 +104,19 @@ int fdg_version(void) { return 1; }
 // ---- plumbing -----------------------------------------------------------------
 int fdg_device_count(int* n) { FDG_CUDA(cudaGetDeviceCount(n)); return FDG_OK; }
 int fdg_set_device(int d) { FDG_CUDA(cudaSetDevice(d)); return FDG_OK; }
+int fdg_enable_peer_access(int device, int peer) {
+    int can = 0;
+    FDG_CUDA(cudaDeviceCanAccessPeer(&can, device, peer));
+    if (!can) return fail(FDG_INVALID_ARG, "enable_peer_access: device cannot access the peer");
+    FDG_CUDA(cudaSetDevice(device));
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return FDG_OK;
+    }
+    FDG_CUDA(e);
+    return FDG_OK;
+}
 int fdg_malloc(void** p, uint64_t b) { FDG_CUDA(cudaMalloc(p, std::max<uint64_t>(b, 1))); return FDG_OK; }
 int fdg_free(void* p) { FDG_CUDA(cudaFree(p)); return FDG_OK; }
 int fdg_host_alloc(void** p, uint64_t b) { FDG_CUDA(cudaMallocHost(p, std::max<uint64_t>(b, 1))); return FDG_OK; }

@@ -356,7 +356,7 @@ __global__ void k_bind(BmDev B, const uint64_t* nodes, int64_t* alias) {
 constexpr int kMoveRows = 4;
 __global__ void __launch_bounds__(512) k_move(BmDev B, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                                               const int64_t* alias, const uint8_t* is_load, const char* table,
-                                              char* region, uint32_t rb, char* X) {
+                                              char* region, uint32_t rb, char* X, uint32_t host_table) {
     BmState* S = B.st;
     if (S->status) return;
     const uint32_t cpr = rb / 16;
@@ -390,10 +390,16 @@ __global__ void __launch_bounds__(512) k_move(BmDev B, const uint64_t* nodes, co
             uint4 v[kMoveRows];
 #pragma unroll
             for (int q = 0; q < kMoveRows; ++q)
-                if (src[q] && (miss[q] || X))
-                    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                                 : "=r"(v[q].x), "=r"(v[q].y), "=r"(v[q].z), "=r"(v[q].w)
-                                 : "l"(reinterpret_cast<const uint4*>(src[q]) + c), "l"(pol));
+                if (src[q] && (miss[q] || X)) {
+                    if (host_table && miss[q])  // mapped host memory: no L2 policy on PCIe reads
+                        asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                     : "=r"(v[q].x), "=r"(v[q].y), "=r"(v[q].z), "=r"(v[q].w)
+                                     : "l"(reinterpret_cast<const uint4*>(src[q]) + c));
+                    else
+                        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                                     : "=r"(v[q].x), "=r"(v[q].y), "=r"(v[q].z), "=r"(v[q].w)
+                                     : "l"(reinterpret_cast<const uint4*>(src[q]) + c), "l"(pol));
+                }
 #pragma unroll
             for (int q = 0; q < kMoveRows; ++q) {
                 if (!src[q] || !(miss[q] || X)) continue;
@@ -719,6 +725,7 @@ struct Bm {
     void* arena = nullptr;
     char* region = nullptr;
     bool own_region = true;         // false: the region is a caller's FeatureRegion allocation
+    bool host_src = false;          // standalone: the bound table lives in mapped host memory
     uint64_t slots = 0;
     uint32_t max_batch = 0;
     uint32_t epoch = 1;
@@ -872,6 +879,7 @@ int fdg_bm_bind_table(fdg_bm* b, const fdg_ctx* table, void* region_dev) {
     c->n_shards = 1;
     c->rows_per_shard = table->rows_per_shard;
     c->dtype = table->dtype;
+    b->host_src = table->host_table != nullptr;
     return FDG_OK;
 }
 
@@ -930,7 +938,8 @@ int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
     {
         FDG_TRACE("bm_move", st);
         k_move<<<blocks, 512, 0, st>>>(d, nodes, n_dev, n_host, alias, d.is_load[parity & 1], table, b->region, rb,
-                                       static_cast<char*>(out));
+                                       static_cast<char*>(out),
+                                       (b->own_ctx ? b->host_src : b->ctx->host_table != nullptr) ? 1u : 0u);
     }
     FDG_CUDA(cudaGetLastError());
     if (checksum) {
