@@ -1,5 +1,6 @@
 // fdg_api.cu -- the extern "C" boundary (include/fdg.h).
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
@@ -13,6 +14,7 @@
 
 namespace fdg {
 
+int64_t g_host_tier_thp = 0;
 static thread_local std::string g_error;
 static thread_local int g_errno = 0;
 
@@ -190,13 +192,29 @@ int fdg_ctx_create(int device, fdg_ctx** out) {
     return FDG_OK;
 }
 
+// The out-of-core table: either cudaHostAlloc'ed, or (option host_tier_thp) an anonymous
+// mapping with transparent huge pages registered with the driver, so the GPU maps the 57 GB
+// table with 2 MB pages instead of small ones (random row reads then miss the GPU TLB far
+// less).
+static void free_host_table(fdg_ctx* c) {
+    if (!c->host_table) return;
+    if (c->host_table_bytes) {
+        cudaHostUnregister(c->host_table);
+        munmap(c->host_table, c->host_table_bytes);
+    } else {
+        cudaFreeHost(c->host_table);
+    }
+    c->host_table = nullptr;
+    c->host_table_bytes = 0;
+}
+
 int fdg_ctx_destroy(fdg_ctx* c) {
     if (!c) return FDG_OK;
     cudaSetDevice(c->device);
     if (c->indptr) cudaFree(c->indptr);
     if (c->indices) cudaFree(c->indices);
     for (void* p : c->owned_shards) cudaFree(p);
-    if (c->host_table) cudaFreeHost(c->host_table);
+    free_host_table(c);
     if (c->shard_table) cudaFree((void*)c->shard_table);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->dyn_ring) cudaFree(c->dyn_ring);
@@ -285,8 +303,7 @@ int fdg_ctx_generate_topology(fdg_ctx* c, uint64_t seed, uint64_t n, uint32_t av
 
 static int install_table(fdg_ctx* c, void* dev, uint64_t n, uint32_t row_bytes, uint32_t dtype) {
     for (void* p : c->owned_shards) cudaFree(p);
-    if (c->host_table) cudaFreeHost(c->host_table);
-    c->host_table = nullptr;
+    free_host_table(c);
     c->owned_shards.assign(1, dev);
     c->shard_bases.assign(1, dev);
     c->row_bytes = row_bytes;
@@ -377,17 +394,37 @@ int fdg_ctx_features_to_host(fdg_ctx* c) {
     cudaSetDevice(c->device);
     const uint64_t bytes = c->feat_nodes * c->row_bytes;
     void* h = nullptr;
-    FDG_CUDA(cudaHostAlloc(&h, std::max<uint64_t>(bytes, 1), cudaHostAllocMapped | cudaHostAllocPortable));
-    cudaError_t e = cudaMemcpy(h, c->owned_shards[0], bytes, cudaMemcpyDeviceToHost);
+    uint64_t mapped = 0;
+    cudaError_t e = cudaSuccess;
+    if (g_host_tier_thp) {
+        mapped = (std::max<uint64_t>(bytes, 1) + (2ull << 20) - 1) & ~((2ull << 20) - 1);
+        h = mmap(nullptr, mapped, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (h == MAP_FAILED) return io_fail("features_to_host: mmap", errno);
+        madvise(h, mapped, MADV_HUGEPAGE);
+        e = cudaHostRegister(h, mapped, cudaHostRegisterMapped | cudaHostRegisterPortable);
+        if (e != cudaSuccess) {
+            munmap(h, mapped);
+            return cuda_fail(e, "cudaHostRegister(feature table)", __FILE__, __LINE__);
+        }
+    } else {
+        FDG_CUDA(cudaHostAlloc(&h, std::max<uint64_t>(bytes, 1), cudaHostAllocMapped | cudaHostAllocPortable));
+    }
+    e = cudaMemcpy(h, c->owned_shards[0], bytes, cudaMemcpyDeviceToHost);
     void* dptr = nullptr;
     if (e == cudaSuccess) e = cudaHostGetDevicePointer(&dptr, h, 0);
     if (e != cudaSuccess) {
-        cudaFreeHost(h);
+        if (mapped) {
+            cudaHostUnregister(h);
+            munmap(h, mapped);
+        } else {
+            cudaFreeHost(h);
+        }
         return cuda_fail(e, "fdg_ctx_features_to_host", __FILE__, __LINE__);
     }
     cudaFree(c->owned_shards[0]);
     c->owned_shards.clear();
     c->host_table = h;
+    c->host_table_bytes = mapped;
     c->shard_bases.assign(1, dptr);
     FDG_CUDA(cudaMemcpy((void*)c->shard_table, &dptr, sizeof(void*), cudaMemcpyHostToDevice));
     return FDG_OK;
@@ -575,6 +612,15 @@ int fdg_set_option(const char* key, int64_t v) {
         g_mt_adaptive = v;
         return FDG_OK;
     }
+    if (k == "l2_fetch_granularity") {  // cudaLimitMaxL2FetchGranularity of the current device (bytes, 0-128)
+        if (v < 0 || v > 128) return fail(FDG_INVALID_ARG, "l2_fetch_granularity must be in [0, 128]");
+        FDG_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(v)));
+        return FDG_OK;
+    }
+    if (k == "host_tier_thp") {  // features_to_host: THP-backed registered memory instead of cudaHostAlloc
+        g_host_tier_thp = v != 0;
+        return FDG_OK;
+    }
     if (k == "prefetch_upfront") {  // A/B only
         g_prefetch_upfront = v != 0;
         return FDG_OK;
@@ -652,6 +698,12 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "mt_adaptive") *v = g_mt_adaptive;
     else if (k == "replay") *v = g_replay;
     else if (k == "prefetch_upfront") *v = g_prefetch_upfront;
+    else if (k == "host_tier_thp") *v = g_host_tier_thp;
+    else if (k == "l2_fetch_granularity") {
+        size_t g = 0;
+        FDG_CUDA(cudaDeviceGetLimit(&g, cudaLimitMaxL2FetchGranularity));
+        *v = int64_t(g);
+    }
     else if (k == "debug_reject_batch") *v = g_debug_reject_batch;
     else if (k == "gather_pf64") *v = g_gather_pf64;
     else if (k == "rb_ctas_per_sm") *v = g_rb_ctas_per_sm;

@@ -89,6 +89,7 @@ struct Ctx {
     std::vector<void*> shard_bases;   // device pointers (may be peers)
     std::vector<void*> owned_shards;  // allocations owned by this ctx
     void* host_table = nullptr;       // out-of-core tier: pinned, mapped host copy (owned)
+    uint64_t host_table_bytes = 0;    // > 0: an mmap'ed, registered mapping of this size (THP)
     const void** shard_table = nullptr;  // device copy of shard_bases
     cudaStream_t stream = nullptr;    // setup stream
     int sm_count = 148;
@@ -144,7 +145,8 @@ extern int64_t g_hash_clear;          // 1: clear batch hash tables with a fill 
 extern int64_t g_hash_keep;           // evict_last L2 policy on the batch hash
 extern int64_t g_mt_adaptive;         // prefetch the estimated MT draws (1), the draw bound (0), test (2)
 extern int64_t g_replay;              // A/B only: 0 drops the in-stream replay launch
-extern int64_t g_prefetch_upfront;    // A/B only: 1 requests every sampler's first MT chunk before sampling
+extern int64_t g_prefetch_upfront;
+extern int64_t g_host_tier_thp;       // features_to_host on THP-backed registered memory    // A/B only: 1 requests every sampler's first MT chunk before sampling
 extern int64_t g_debug_zero_word;     // pipeline test hook (option debug_zero_word)
 extern int64_t g_debug_reject_batch;  // pipeline test hook (option debug_reject_batch)
 int launch_gather_tma(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,

@@ -24,8 +24,10 @@ L.fdg_set_gather_impl(impl)
 if os.environ.get("BM_OVERLAP"):
     fd.featdrive.check(L.fdg_set_option(b"bm_overlap", int(os.environ["BM_OVERLAP"])))
 topo = fd.Topology.generate(n, dim, avg, 7, dtype=dtype)
+if os.environ.get("HOST"):  # out-of-core tier: table in pinned host memory
+    topo.features_to_host()
 order = np.concatenate(fd.partition_epoch(np.arange(t_ids, dtype=np.uint64), B, bench.hash_combine(0, 0)))
-K = 200
+K = int(os.environ.get("K", "200"))
 rng = np.array([L.fdg_batch_seed(0, 0, int(g)) for g in range(K)], np.uint64)
 nb_epoch = len(order) // B  # wrap at the epoch end (products has 196 batches)
 seeds = DeviceBuffer.from_array(np.ascontiguousarray(np.concatenate([order[(b % nb_epoch) * B:(b % nb_epoch + 1) * B] for b in range(K)])))
@@ -38,7 +40,15 @@ f = np.ascontiguousarray(fan, np.uint32)
 p = C.c_void_p()
 fd.featdrive.check(L.fdg_pipeline_create(topo.ctx, f.ctypes.data_as(C.c_void_p), len(f), C.byref(cfg), C.byref(p)))
 ms = C.c_float()
-fd.featdrive.check(L.fdg_pipeline_run(p, seeds.ptr, 0, rng.ctypes.data_as(C.c_void_p), K, None, None, C.byref(ms)))
+if os.environ.get("COLD"):  # warm up on other batches: the traced batches then miss the feature buffer
+    rng_w = np.array([L.fdg_batch_seed(0, 1, int(g)) for g in range(K)], np.uint64)
+    seeds_w = DeviceBuffer.from_array(np.ascontiguousarray(np.concatenate(
+        [order[((b + K) % nb_epoch) * B:((b + K) % nb_epoch + 1) * B] for b in range(K)])))
+    fd.featdrive.check(L.fdg_pipeline_run(p, seeds_w.ptr, 0, rng_w.ctypes.data_as(C.c_void_p), K, None, None,
+                                          C.byref(ms)))
+else:
+    fd.featdrive.check(L.fdg_pipeline_run(p, seeds.ptr, 0, rng.ctypes.data_as(C.c_void_p), K, None, None,
+                                          C.byref(ms)))
 L.fdg_trace_enable(1)
 fd.featdrive.check(L.fdg_pipeline_run(p, seeds.ptr, 0, rng.ctypes.data_as(C.c_void_p), K, None, None, C.byref(ms)))
 L.fdg_trace_dump(b"gpurun_out/trace.csv")
