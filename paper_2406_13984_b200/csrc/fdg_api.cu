@@ -1,10 +1,13 @@
 // fdg_api.cu -- the extern "C" boundary (include/fdg.h).
 #include <fcntl.h>
 #include <sys/mman.h>
+#include <sys/syscall.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
 #include <algorithm>
+#include <cctype>
+#include <cstdio>
 #include <cstring>
 #include <random>
 #include <string>
@@ -190,6 +193,23 @@ int fdg_ctx_create(int device, fdg_ctx** out) {
     }
     *out = c;
     return FDG_OK;
+}
+
+// NUMA node of the GPU's PCI device (-1 if unknown).
+static int gpu_numa_node(int device) {
+    char bus[32] = {};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    std::string id(bus);
+    for (auto& ch : id) ch = char(std::tolower(static_cast<unsigned char>(ch)));
+    FILE* f = std::fopen(("/sys/bus/pci/devices/" + id + "/numa_node").c_str(), "r");
+    if (!f) return -1;
+    int node = -1;
+    if (std::fscanf(f, "%d", &node) != 1) node = -1;
+    std::fclose(f);
+    return node;
 }
 
 // The out-of-core table: either cudaHostAlloc'ed, or (option host_tier_thp) an anonymous
@@ -401,6 +421,13 @@ int fdg_ctx_features_to_host(fdg_ctx* c) {
         h = mmap(nullptr, mapped, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
         if (h == MAP_FAILED) return io_fail("features_to_host: mmap", errno);
         madvise(h, mapped, MADV_HUGEPAGE);
+        // pages on the GPU's own NUMA node: a table spread over both sockets reads the far half
+        // over the inter-socket link (measured: 26 vs 48 GB/s of random rows for 57 vs 4 GB)
+        const int node = gpu_numa_node(c->device);
+        if (node >= 0 && node < 64) {
+            unsigned long mask = 1ul << node;
+            syscall(SYS_mbind, h, mapped, 2 /* MPOL_BIND */, &mask, 64, 0);
+        }
         e = cudaHostRegister(h, mapped, cudaHostRegisterMapped | cudaHostRegisterPortable);
         if (e != cudaSuccess) {
             munmap(h, mapped);
@@ -617,7 +644,7 @@ int fdg_set_option(const char* key, int64_t v) {
         FDG_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(v)));
         return FDG_OK;
     }
-    if (k == "host_tier_thp") {  // features_to_host: THP-backed registered memory instead of cudaHostAlloc
+    if (k == "host_tier_thp") {  // features_to_host: THP-backed, NUMA-local registered memory (not cudaHostAlloc)
         g_host_tier_thp = v != 0;
         return FDG_OK;
     }

@@ -37,12 +37,14 @@ print(f"pinned H2D copy peak: {best:.1f} GB/s")
 ev = [C.c_void_p(), C.c_void_p()]
 for e in ev:
     fd.featdrive.check(L.fdg_event_create(C.byref(e)))
-for name, impl in (("LDG chunk-striped", 1), ("row-group dyn", 4), ("TMA bulk", 0)):
+nd_sorted = DeviceBuffer.from_array(np.sort(nodes))
+for name, impl in (("LDG chunk-striped", 1), ("row-group dyn", 4), ("TMA bulk", 0), ("LDG, sorted ids", 1)):
+    src = nd_sorted if "sorted" in name else nd
     fd.set_option("gather_impl", impl)
     times = []
     for rep in range(4):
         fd.featdrive.check(L.fdg_event_record(ev[0], None))
-        fd.featdrive.check(L.fdg_gather(t.ctx, None, nd.ptr, None, len(nodes), out.ptr, None))
+        fd.featdrive.check(L.fdg_gather(t.ctx, None, src.ptr, None, len(nodes), out.ptr, None))
         fd.featdrive.check(L.fdg_event_record(ev[1], None))
         fd.featdrive.check(L.fdg_device_sync())
         ms = C.c_float()
