@@ -644,6 +644,10 @@ int fdg_set_option(const char* key, int64_t v) {
         FDG_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(v)));
         return FDG_OK;
     }
+    if (k == "bm_sorted_move") {  // host-resident tables: misses moved in node-id order (1) or batch order (0)
+        g_bm_sorted_move = v != 0;
+        return FDG_OK;
+    }
     if (k == "host_tier_thp") {  // features_to_host: THP-backed, NUMA-local registered memory (not cudaHostAlloc)
         g_host_tier_thp = v != 0;
         return FDG_OK;
@@ -726,6 +730,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "replay") *v = g_replay;
     else if (k == "prefetch_upfront") *v = g_prefetch_upfront;
     else if (k == "host_tier_thp") *v = g_host_tier_thp;
+    else if (k == "bm_sorted_move") *v = g_bm_sorted_move;
     else if (k == "l2_fetch_granularity") {
         size_t g = 0;
         FDG_CUDA(cudaDeviceGetLimit(&g, cudaLimitMaxL2FetchGranularity));

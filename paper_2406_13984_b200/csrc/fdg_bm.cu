@@ -46,6 +46,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "fdg_internal.cuh"
 
 namespace fdg {
@@ -418,6 +420,64 @@ __global__ void __launch_bounds__(512) k_move(BmDev B, const uint64_t* nodes, co
     }
 }
 
+// ----------------------------------------------------------- sorted move ----
+// Host-resident table (out-of-core tier): misses are moved in node-id order. Random 512-B
+// rows over a 57 GB mapped host table reach 26 GB/s over PCIe in batch order but 47 GB/s in
+// address order (0.84 of the measured copy peak; scripts/host_tier_gather.py): the host
+// side's address translation is the limit, not the link. Keys: the node id of a miss, ~0 for
+// a hit (sorted to the end, moved slot -> X); values: batch positions.
+__global__ void __launch_bounds__(256) k_move_keys(const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                                                   const uint8_t* is_load, uint32_t* keys, uint32_t* pos,
+                                                   uint64_t bound) {
+    const uint64_t n = load_n(n_dev, n_host);
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < bound;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const bool live = i < n;
+        keys[i] = live && is_load[i] ? uint32_t(nodes[i]) : (live ? 0xFFFFFFFEu : 0xFFFFFFFFu);
+        pos[i] = uint32_t(i);
+    }
+}
+
+// Chunk-striped over the sorted (position) list: 16-byte chunks, 4 loads in flight per thread.
+__global__ void __launch_bounds__(512) k_move_sorted(BmDev B, const uint32_t* keys, const uint32_t* pos,
+                                                     uint64_t bound, const int64_t* alias, const char* table,
+                                                     char* region, uint32_t rb, char* X) {
+    if (B.st->status) return;
+    const uint32_t cpr = rb / 16;
+    const uint64_t total = bound * cpr;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t c0 = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; c0 < total; c0 += 4 * stride) {
+        uint4 v[4];
+        uint32_t k[4], p[4], col[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t c = c0 + u * stride;
+            k[u] = 0xFFFFFFFFu;
+            if (c < total) {
+                const uint64_t s = c / cpr;
+                col[u] = uint32_t(c - s * cpr);
+                k[u] = keys[s];
+                p[u] = pos[s];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (k[u] == 0xFFFFFFFFu) continue;  // past the batch
+            const char* src = k[u] != 0xFFFFFFFEu ? table + uint64_t(k[u]) * rb : region + uint64_t(alias[p[u]]) * rb;
+            if (k[u] == 0xFFFFFFFEu && !X) continue;  // a hit without X: nothing to move
+            asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                         : "l"(reinterpret_cast<const uint4*>(src) + col[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (k[u] == 0xFFFFFFFFu || (k[u] == 0xFFFFFFFEu && !X)) continue;
+            if (k[u] != 0xFFFFFFFEu) reinterpret_cast<uint4*>(region + uint64_t(alias[p[u]]) * rb)[col[u]] = v[u];
+            if (X) reinterpret_cast<uint4*>(X + uint64_t(p[u]) * rb)[col[u]] = v[u];
+        }
+    }
+}
+
 // ------------------------------------------------------------ k_release ----
 // Slots come from the batch's alias list (ALIAS) or from the mapping entries of its
 // node ids (the public release_batch(nodes) form).
@@ -726,6 +786,10 @@ struct Bm {
     char* region = nullptr;
     bool own_region = true;         // false: the region is a caller's FeatureRegion allocation
     bool host_src = false;          // standalone: the bound table lives in mapped host memory
+    // sorted-move scratch (host-resident tables): keys / positions in and out, CUB temp storage
+    void* sort_arena = nullptr;
+    uint64_t sort_cap = 0;
+    size_t sort_tmp_bytes = 0;
     uint64_t slots = 0;
     uint32_t max_batch = 0;
     uint32_t epoch = 1;
@@ -745,6 +809,7 @@ int bm_release(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const int64_t*
 using namespace fdg;
 
 int64_t fdg::g_bm_eager = 0;
+int64_t fdg::g_bm_sorted_move = 1;
 
 namespace {
 
@@ -888,6 +953,7 @@ int fdg_bm_destroy(fdg_bm* b) {
     cudaSetDevice(b->ctx->device);
     cudaFree(b->arena);
     if (b->own_region) cudaFree(b->region);
+    if (b->sort_arena) cudaFree(b->sort_arena);
     cudaStreamDestroy(b->stream);
     if (b->own_ctx) fdg_ctx_destroy(b->own_ctx);
     delete b;
@@ -935,11 +1001,36 @@ int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
     const uint64_t chunks = n_host * (rb / 16);
     const int blocks =
         int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 511) / 512, uint64_t(b->ctx->sm_count) * 2)));
-    {
+    const bool host = b->own_ctx ? b->host_src : b->ctx->host_table != nullptr;
+    if (host && g_bm_sorted_move && d.N < 0xFFFFFFFEull && n_host > 0) {
+        // misses in node-id order (address locality for the host side's translation)
+        if (b->sort_cap < n_host) {
+            if (b->sort_arena) cudaFree(b->sort_arena);
+            b->sort_arena = nullptr;
+            b->sort_cap = 0;
+            size_t tmp = 0;
+            FDG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                                     (const uint32_t*)nullptr, (uint32_t*)nullptr, int64_t(n_host)));
+            FDG_CUDA(cudaMalloc(&b->sort_arena, 16 * n_host + tmp + 256));
+            b->sort_cap = n_host;
+            b->sort_tmp_bytes = tmp;
+        }
+        uint32_t* kin = static_cast<uint32_t*>(b->sort_arena);
+        uint32_t* kout = kin + b->sort_cap;
+        uint32_t* pin = kout + b->sort_cap;
+        uint32_t* pout = pin + b->sort_cap;
+        void* tmp = pout + b->sort_cap;
+        FDG_TRACE("bm_move", st);
+        k_move_keys<<<std::max<int>(1, int(std::min<uint64_t>((n_host + 255) / 256, uint64_t(b->ctx->sm_count) * 8))),
+                      256, 0, st>>>(nodes, n_dev, n_host, d.is_load[parity & 1], kin, pin, n_host);
+        size_t tb = b->sort_tmp_bytes;
+        FDG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, pin, pout, int64_t(n_host), 0, 32, st));
+        k_move_sorted<<<blocks, 512, 0, st>>>(d, kout, pout, n_host, alias, table, b->region, rb,
+                                              static_cast<char*>(out));
+    } else {
         FDG_TRACE("bm_move", st);
         k_move<<<blocks, 512, 0, st>>>(d, nodes, n_dev, n_host, alias, d.is_load[parity & 1], table, b->region, rb,
-                                       static_cast<char*>(out),
-                                       (b->own_ctx ? b->host_src : b->ctx->host_table != nullptr) ? 1u : 0u);
+                                       static_cast<char*>(out), host ? 1u : 0u);
     }
     FDG_CUDA(cudaGetLastError());
     if (checksum) {

@@ -136,6 +136,7 @@ extern int64_t g_tma_cfg;             // TMA gather ring shape 0-3
 extern int64_t g_sage_gemm;           // train-stage GEMMs: 1 tensor cores (3xTF32), 0 CUDA cores
 extern int64_t g_bm_overlap;          // buffer-manager row move on its own stream (1) or after the metadata (0)
 extern int64_t g_bm_eager;            // buffer managers created in eager-invalidation (debug) mode
+extern int64_t g_bm_sorted_move;      // host-resident table: move the misses in node-id order
 extern int64_t g_l2_persist_mb;       // L2 set-aside for the samplers' hash tables (0 off)
 extern int64_t g_hash_load_pct;       // batch hash sizing (load factor, %)
 extern int64_t g_sampler_ctas_per_sm; // sampler kernels: CTA cap per SM per launch
