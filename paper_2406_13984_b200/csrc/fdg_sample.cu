@@ -341,13 +341,16 @@ __device__ Tri tri_lookback_cta(uint32_t* flags, uint4* aggs, uint4* incls, uint
 // per-item global access of a warp is coalesced (L1TEX wavefronts, not DRAM bytes,
 // bound the sampler); the scan runs as 8 row scans (one per k) -- one warp per
 // row for the cross-warp step -- then one decoupled look-back per tile.
-template <typename IdT, bool SEEDS, bool HAS_NEXT>
+template <typename IdT, bool SEEDS, bool HAS_NEXT, bool PACK>
 __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint32_t epoch, uint32_t tile,
                                             uint32_t P, uint32_t ntiles);
 
 // Persistent: a capped number of CTAs claim tiles in order (keeps SM slots free
 // for the concurrently running gather; look-back needs only claim order).
-template <typename IdT, bool SEEDS, bool HAS_NEXT>
+// PACK (fanout of the next frontier <= 63): the warp scans carry (first, picks, draws)
+// packed in one u32 (6 + 11 + 11 bits); the last pass (no next frontier) counts first
+// occurrences with ballots alone.
+template <typename IdT, bool SEEDS, bool HAS_NEXT, bool PACK = false>
 __device__ __forceinline__ void intern_pass(const Work<IdT>& W, uint32_t q, uint32_t epoch) {
     __shared__ uint32_t s_tile;
     fdg_batch_counts* cnt = W.cnt;
@@ -360,24 +363,66 @@ __device__ __forceinline__ void intern_pass(const Work<IdT>& W, uint32_t q, uint
         const uint32_t tile = s_tile;
         __syncthreads();
         if (tile >= ntiles) return;
-        intern_tile<IdT, SEEDS, HAS_NEXT>(W, q, epoch, tile, P, ntiles);
+        intern_tile<IdT, SEEDS, HAS_NEXT, PACK>(W, q, epoch, tile, P, ntiles);
         __syncthreads();
     }
 }
 
 #ifndef FDG_INTERN_MINB
-#define FDG_INTERN_MINB 1
+#define FDG_INTERN_MINB 2
 #endif
-template <typename IdT, bool SEEDS, bool HAS_NEXT>
-__global__ void __launch_bounds__(kScanThreads, FDG_INTERN_MINB) k_intern_s(const __grid_constant__ Group<IdT> G, uint32_t q,
+#ifndef FDG_INTERN_LAST_MINB
+#define FDG_INTERN_LAST_MINB 4
+#endif
+template <typename IdT, bool SEEDS, bool HAS_NEXT, bool PACK>
+__global__ void __launch_bounds__(kScanThreads, HAS_NEXT ? FDG_INTERN_MINB : FDG_INTERN_LAST_MINB) k_intern_s(const __grid_constant__ Group<IdT> G, uint32_t q,
                                                            uint32_t epoch) {
-    intern_pass<IdT, SEEDS, HAS_NEXT>(G.w[blockIdx.y], q, epoch);
+    intern_pass<IdT, SEEDS, HAS_NEXT, PACK>(G.w[blockIdx.y], q, epoch);
 }
 
-template <typename IdT, bool SEEDS, bool HAS_NEXT>
+// Per-item scan values. Count-only (no next frontier): the first-occurrence bit, counted
+// with ballots. Packed (fanout <= 63): (first, picks, draws) in one u32, 6 + 11 + 11 bits
+// (a warp's sums fit). Otherwise a Tri. Items keep their warp-exclusive value in this
+// compact form until the outputs, so the per-thread item arrays stay small.
+template <bool HAS_NEXT, bool PACK>
+struct ScanVal {
+    using T = Tri;
+    __device__ __forceinline__ static T make(uint32_t c, uint32_t p, uint32_t d) { return Tri{c, p, d}; }
+    __device__ __forceinline__ static T incl(T v, int lane) { return warp_incl_scan(v, lane); }
+    __device__ __forceinline__ static Tri tri(T v) { return v; }
+    __device__ __forceinline__ static T sub(T a, T b) { return Tri{a.c - b.c, a.p - b.p, a.d - b.d}; }
+};
+template <bool PACK>
+struct ScanVal<false, PACK> {
+    using T = uint32_t;
+    __device__ __forceinline__ static T make(uint32_t c, uint32_t, uint32_t) { return c; }
+    __device__ __forceinline__ static T incl(T v, int lane) {
+        return uint32_t(__popc(__ballot_sync(0xffffffffu, v != 0) & (0xffffffffu >> (31 - lane))));
+    }
+    __device__ __forceinline__ static Tri tri(T v) { return Tri{v, 0, 0}; }
+    __device__ __forceinline__ static T sub(T a, T b) { return a - b; }
+};
+template <>
+struct ScanVal<true, true> {
+    using T = uint32_t;
+    __device__ __forceinline__ static T make(uint32_t c, uint32_t p, uint32_t d) { return c | (p << 6) | (d << 17); }
+    __device__ __forceinline__ static T incl(T x, int lane) {
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        return x;
+    }
+    __device__ __forceinline__ static Tri tri(T x) { return Tri{x & 63u, (x >> 6) & 2047u, x >> 17}; }
+    __device__ __forceinline__ static T sub(T a, T b) { return a - b; }
+};
+
+template <typename IdT, bool SEEDS, bool HAS_NEXT, bool PACK>
 __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint32_t epoch, uint32_t tile,
                                             uint32_t P, uint32_t ntiles) {
     static_assert(kScanItems == kScanThreads / 32, "one warp per row scan");
+    using SV = ScanVal<HAS_NEXT, PACK>;
     __shared__ Tri s_row[kScanItems][kScanThreads / 32];  // per row: warp inclusive -> exclusive
     __shared__ Tri s_rowx[kScanItems];                    // per row: exclusive offset within the tile
     __shared__ Tri s_excl, s_agg;
@@ -405,11 +450,10 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
             W.tab.load(slot[k], key[k], val[k]);
             if (val[k] == (kPend | (p0 + k * kScanThreads))) first_mask |= 1u << k;
         }
-    uint64_t lo[kScanItems], hi[kScanItems];
-    Tri v[kScanItems];
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) v[k] = Tri{(first_mask >> k) & 1u, 0, 0};
-    if (HAS_NEXT) {
+    uint64_t lo[HAS_NEXT ? kScanItems : 1];
+    uint32_t dg[HAS_NEXT ? kScanItems : 1];
+    if constexpr (HAS_NEXT) {
+        uint64_t hi[kScanItems];
 #pragma unroll
         for (int k = 0; k < kScanItems; ++k)
             if (first_mask & (1u << k)) {
@@ -417,28 +461,37 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
                 hi[k] = W.indptr[uint64_t(key[k]) + 1];
             }
 #pragma unroll
-        for (int k = 0; k < kScanItems; ++k)
-            if (first_mask & (1u << k)) {
-                uint32_t d = uint32_t(hi[k] - lo[k]);
-                v[k].p = d < f ? d : f;
-                v[k].d = d > f ? f : 0;
-            }
+        for (int k = 0; k < kScanItems; ++k) dg[k] = (first_mask & (1u << k)) ? uint32_t(hi[k] - lo[k]) : 0u;
     }
     // row scans: warp-inclusive per row; warp r turns row r's warp totals into exclusive
-    // warp offsets; thread 0 turns the row totals into row offsets.
-    Tri inc[kScanItems];
+    // warp offsets; thread 0 turns the row totals into row offsets. xe[k] keeps item k's
+    // warp-exclusive value.
+    typename SV::T xe[kScanItems];
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-        inc[k] = warp_incl_scan(v[k], lane);
-        if (lane == 31) s_row[k][warp] = inc[k];
+        const uint32_t c = (first_mask >> k) & 1u;
+        const uint32_t d = HAS_NEXT ? dg[k] : 0u;
+        const typename SV::T v = SV::make(c, HAS_NEXT ? (d < f ? d : f) : 0u, HAS_NEXT ? (d > f ? f : 0u) : 0u);
+        const typename SV::T in = SV::incl(v, lane);
+        xe[k] = SV::sub(in, v);
+        if (lane == 31) s_row[k][warp] = SV::tri(in);
     }
     __syncthreads();
     {
         const int r = warp;
         Tri w = lane < kScanThreads / 32 ? s_row[r][lane] : Tri{0, 0, 0};
-        Tri wi = warp_incl_scan(w, lane);
+        Tri wi = w;
+        if constexpr (HAS_NEXT) {
+            wi = warp_incl_scan(w, lane);
+        } else {
+#pragma unroll
+            for (int o = 1; o < kScanThreads / 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, wi.c, o);
+                if (lane >= o) wi.c += y;
+            }
+        }
         if (lane < kScanThreads / 32) s_row[r][lane] = Tri{wi.c - w.c, wi.p - w.p, wi.d - w.d};
-        if (lane == 31) s_rowx[r] = wi;  // row total for now
+        if (lane == kScanThreads / 32 - 1) s_rowx[r] = wi;  // row total for now
     }
     __syncthreads();
     const uint32_t E = (epoch & 0x3FFFFFFFu) << 2;
@@ -456,16 +509,13 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
         atomicExch(W.tile_flag + tile, E | 1u);
     }
     __syncthreads();
-    Tri ex[kScanItems];  // tile-relative exclusive prefix of item k
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k)
-        ex[k] = s_rowx[k] + s_row[k][warp] + Tri{inc[k].c - v[k].c, inc[k].p - v[k].p, inc[k].d - v[k].d};
     if (!SEEDS) {
         // tile-relative rank of every first occurrence, published (fenced) before this
         // tile's look-back flag so later tiles can resolve their repeated picks
 #pragma unroll
         for (int k = 0; k < kScanItems; ++k)
-            if (first_mask & (1u << k)) W.rank[ebase + p0 + k * kScanThreads] = ex[k].c;
+            if (first_mask & (1u << k))
+                W.rank[ebase + p0 + k * kScanThreads] = s_rowx[k].c + s_row[k][warp].c + SV::tri(xe[k]).c;
         __threadfence();
         __syncthreads();
     }
@@ -501,16 +551,17 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
         if (!(valid_mask & (1u << k))) continue;
         const uint32_t p = p0 + k * kScanThreads;
         if (first_mask & (1u << k)) {
-            const uint32_t r = base.c + ex[k].c;
+            const Tri ex = s_rowx[k] + s_row[k][warp] + SV::tri(xe[k]);  // tile-relative exclusive prefix
+            const uint32_t r = base.c + ex.c;
             const uint32_t local = node_base + r;
             W.nodes[local] = uint64_t(key[k]);
             if (HAS_NEXT) W.tab.finalize(slot[k], key[k], local);  // no later pass reads the last layer's entries
             if (!SEEDS) W.edges[2 * (ebase + p)] = local;
-            if (HAS_NEXT) {
+            if constexpr (HAS_NEXT) {
                 fr.start[r] = lo[k];
-                fr.deg[r] = uint32_t(hi[k] - lo[k]);
-                fr.pick_off[r] = base.p + ex[k].p;
-                fr.draw_off[r] = base.d + ex[k].d;
+                fr.deg[r] = dg[k];
+                fr.pick_off[r] = base.p + ex.p;
+                fr.draw_off[r] = base.d + ex.d;
             }
         } else if (!SEEDS) {
             // src id of a repeated pick (LocalEdge.src, sampling.hpp:124): a final id is used
@@ -658,12 +709,13 @@ __global__ void __launch_bounds__(256) k_insert(const __grid_constant__ Group<Id
 }
 
 // ---------------------------------------------------------------- k_expand ----
-// Fast path for fanouts <= 16: a half-warp per frontier node, one pick per lane.
-// Lane k draws t_k from MT word db + draw_off + k (a Lemire rejection -- p ~ 2^-57
-// per draw -- flags the batch for exact mode), loads cand_k = nb[t_k] and
-// alt_k = nb[j_k]; Floyd's value-compare collision chain is resolved in k order
-// with one shuffle + ballot per step; then every lane inserts its pick into the
-// batch hash and writes its edge's dst (sampling.hpp:104-126).
+// Fast path for fanouts <= 16: floor(32 / f) frontier nodes per warp, f lanes per node,
+// one pick per lane (f = 10: three nodes in 30 lanes). Lane k draws t_k from MT word
+// db + draw_off + k (a Lemire rejection -- p ~ 2^-57 per draw -- flags the batch for the
+// exact replay), loads cand_k = nb[t_k] and alt_k = nb[j_k]; Floyd's value-compare
+// collision chain is resolved in k order with one shuffle + ballot per step; then every
+// lane inserts its pick into the batch hash and writes its edge's dst
+// (sampling.hpp:104-126).
 template <typename IdT>
 __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ Group<IdT> G, uint32_t l) {
     const Work<IdT>& W = G.w[blockIdx.y];
@@ -682,12 +734,16 @@ __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ Group<Id
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(&cnt->status, 0u, uint32_t(FDG_REJECTION));
         return;
     }
-    const int lane = threadIdx.x & 31, h = lane >> 4, k = lane & 15;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t npw = 32 / f;                 // nodes per warp
+    const uint32_t g = lane / f, k = lane - g * f;  // node slot in the warp, pick index
+    const bool in_group = g < npw;
+    const uint32_t gbase = in_group ? g * f : 0;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     bool rejected = false;
-    for (uint32_t pair = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; pair * 2 < F; pair += nwarps) {
-        const uint32_t i = pair * 2 + h;
-        const bool live = i < F;
+    for (uint32_t wt = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wt * npw < F; wt += nwarps) {
+        const uint32_t i = wt * npw + g;
+        const bool live = in_group && i < F;
         uint64_t start = 0;
         uint32_t deg = 0, po = 0, dro = 0;
         if (live) {
@@ -699,7 +755,7 @@ __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ Group<Id
         const bool floyd = deg > f;
         const uint32_t npick = floyd ? f : deg;
         IdT picked = 0, alt = 0;
-        if (live && uint32_t(k) < npick) {
+        if (live && k < npick) {
             if (floyd) {
                 const uint64_t j = uint64_t(deg - f) + k;
                 const uint64_t r = j + 1;
@@ -712,15 +768,15 @@ __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ Group<Id
                 picked = W.indices[start + k];
             }
         }
-        // Floyd collision chain: step s finalises lane s of each half-warp
+        // Floyd collision chain: step s finalises pick s of every node in the warp
         if (__any_sync(0xffffffffu, live && floyd)) {
             for (uint32_t s = 1; s < f; ++s) {
-                const IdT c = __shfl_sync(0xffffffffu, picked, int(s), 16);
-                const uint32_t hits = __ballot_sync(0xffffffffu, uint32_t(k) < s && picked == c);
-                if (uint32_t(k) == s && floyd && ((hits >> (h * 16)) & 0xFFFFu)) picked = alt;
+                const IdT c = __shfl_sync(0xffffffffu, picked, int(gbase + s));
+                const uint32_t hits = __ballot_sync(0xffffffffu, in_group && k < s && picked == c);
+                if (k == s && floyd && ((hits >> gbase) & ((1u << s) - 1u))) picked = alt;
             }
         }
-        if (live && uint32_t(k) < npick) {
+        if (live && k < npick) {
             const uint32_t e = eb + po + k;
             W.pick_slot[e] = W.tab.insert(picked, po + k);
             W.edges[2 * e + 1] = fs + i;
@@ -1070,12 +1126,15 @@ void launch_intern(Sampler& s, cudaStream_t st, const Group<IdT>& G, uint32_t n,
     const uint64_t tiles = std::max<uint64_t>(1, (P + kTile - 1) / kTile);
     const uint64_t cap = std::max<uint64_t>(1, uint64_t(s.ctx->sm_count) * g_sampler_ctas_per_sm / n);
     const dim3 grid(uint32_t(std::min(tiles, cap)), n);
+    const bool pack = has_next && s.fan[q] <= 63;
     if (seeds) {
-        if (has_next) k_intern_s<IdT, true, true><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
-        else k_intern_s<IdT, true, false><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
+        if (pack) k_intern_s<IdT, true, true, true><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
+        else if (has_next) k_intern_s<IdT, true, true, false><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
+        else k_intern_s<IdT, true, false, false><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
     } else {
-        if (has_next) k_intern_s<IdT, false, true><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
-        else k_intern_s<IdT, false, false><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
+        if (pack) k_intern_s<IdT, false, true, true><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
+        else if (has_next) k_intern_s<IdT, false, true, false><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
+        else k_intern_s<IdT, false, false, false><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
     }
 }
 
@@ -1130,7 +1189,9 @@ int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
         {
             FDG_TRACE(names[0][l], st);
             if (s.small_f) {
-                const dim3 grid(grid_for(s.F_bound[l] * 16, 256, int(s.ctx->sm_count * g_sampler_ctas_per_sm / n)), n);
+                const uint64_t npw = 32 / s.fan[l];  // nodes per warp
+                const dim3 grid(grid_for((s.F_bound[l] + npw - 1) / npw * 32, 256,
+                                         int(s.ctx->sm_count * g_sampler_ctas_per_sm / n)), n);
                 k_expand<IdT><<<grid, 256, 0, st>>>(G, l);
             } else {
                 launch_sample<IdT, 0>(s, st, G, n, l);
