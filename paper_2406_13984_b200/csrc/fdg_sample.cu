@@ -160,8 +160,7 @@ struct Work {
     uint32_t n_seeds;
     uint32_t n_layers;
     uint32_t* seed_slot;  // [max_seeds]
-    uint32_t* pick_slot;  // [max_edges], by global edge position
-    uint32_t* rank;       // [max_edges], tile-relative rank of first occurrences
+    uint16_t* rank;       // [max_edges], tile-relative rank of first occurrences (< kTile)
     IdT* picks;           // [max_edges], picked neighbor ids (thread-per-node path)
     FrontierBuf fr[2];
     uint32_t* consumed;   // exact mode: words consumed per frontier node
@@ -265,6 +264,11 @@ __device__ __forceinline__ Tri warp_incl_scan(Tri v, int lane) {
     return v;
 }
 
+__device__ __forceinline__ uint32_t ld_volatile_u16(const uint16_t* p) {
+    uint16_t v;
+    asm volatile("ld.volatile.global.u16 %0, [%1];" : "=h"(v) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -441,7 +445,7 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
         const uint32_t p = p0 + k * kScanThreads;
         if (p < P) {
             valid_mask |= 1u << k;
-            slot[k] = SEEDS ? W.seed_slot[p] : W.pick_slot[ebase + p];
+            slot[k] = SEEDS ? W.seed_slot[p] : W.edges[2 * (ebase + p)];  // the expansion parks the slot in src
         }
     }
 #pragma unroll
@@ -515,7 +519,7 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
 #pragma unroll
         for (int k = 0; k < kScanItems; ++k)
             if (first_mask & (1u << k))
-                W.rank[ebase + p0 + k * kScanThreads] = s_rowx[k].c + s_row[k][warp].c + SV::tri(xe[k]).c;
+                W.rank[ebase + p0 + k * kScanThreads] = uint16_t(s_rowx[k].c + s_row[k][warp].c + SV::tri(xe[k]).c);
         __threadfence();
         __syncthreads();
     }
@@ -581,7 +585,7 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
                     const uint4 in = ld_volatile4(W.tile_incl + tf);
                     bc = tf == 0 ? 0u : in.x - ld_volatile4(W.tile_agg + tf).x;
                 }
-                src = node_base + bc + ld_volatile(W.rank + ebase + pf);
+                src = node_base + bc + ld_volatile_u16(W.rank + ebase + pf);
             }
             W.edges[2 * (ebase + p)] = src;
         }
@@ -700,7 +704,7 @@ __device__ __forceinline__ void insert_picks(const Work<IdT>& W, uint32_t l, uin
     if (cnt->status) return;
     const uint32_t eb = cnt->layer_edges[l];
     const uint32_t P = cnt->layer_edges[l + 1] - eb;
-    for (uint32_t p = first; p < P; p += stride) W.pick_slot[eb + p] = W.tab.insert(W.picks[eb + p], p);
+    for (uint32_t p = first; p < P; p += stride) W.edges[2 * (eb + p)] = W.tab.insert(W.picks[eb + p], p);
 }
 
 template <typename IdT>
@@ -778,8 +782,9 @@ __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ Group<Id
         }
         if (live && k < npick) {
             const uint32_t e = eb + po + k;
-            W.pick_slot[e] = W.tab.insert(picked, po + k);
-            W.edges[2 * e + 1] = fs + i;
+            // {hash slot, dst}: the intern pass reads the slot and overwrites it with the src id
+            const uint32_t slot = W.tab.insert(picked, po + k);
+            *reinterpret_cast<uint2*>(W.edges + 2 * e) = make_uint2(slot, fs + i);
         }
     }
     if (rejected) {
@@ -1002,8 +1007,7 @@ cudaError_t clear_hash(void* base, uint64_t bytes, int sm_count, cudaStream_t st
 struct Lane {  // per-batch workspace of one group slot
     void* hash = nullptr;  // packed entries (u32 ids) or keys then vals (u64 ids)
     uint32_t* seed_slot = nullptr;
-    uint32_t* pick_slot = nullptr;
-    uint32_t* rank = nullptr;
+    uint16_t* rank = nullptr;
     void* picks = nullptr;
     FrontierBuf fr[2];
     uint32_t* consumed = nullptr;
@@ -1089,7 +1093,6 @@ Work<IdT> make_work(Sampler& s, const Lane& ln, const BatchArgs& a) {
     w.n_seeds = a.n_seeds;
     w.n_layers = s.n_layers;
     w.seed_slot = ln.seed_slot;
-    w.pick_slot = ln.pick_slot;
     w.rank = ln.rank;
     w.picks = static_cast<IdT*>(ln.picks);
     w.fr[0] = ln.fr[0];
@@ -1329,8 +1332,7 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
     // per-lane layout
     uint64_t lz = 0;
     const uint64_t o_seed = lz; lz += al(uint64_t(max_seeds) * 4);
-    const uint64_t o_pick = lz; lz += al(std::max<uint64_t>(s->max_edges, 1) * 4);
-    const uint64_t o_rank = lz; lz += al(std::max<uint64_t>(s->max_edges, 1) * 4);
+    const uint64_t o_rank = lz; lz += al(std::max<uint64_t>(s->max_edges, 1) * 2);
     const uint64_t o_picks = lz; lz += al(std::max<uint64_t>(s->max_edges, 1) * ib);  // exact replay (any lane)
     uint64_t o_fr[2];
     for (int b = 0; b < 2; ++b) { o_fr[b] = lz; lz += al(fmaxF * 8) + 3 * al(fmaxF * 4); }
@@ -1360,8 +1362,7 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
         char* a = A + o_lanes + g * lz;
         ln.hash = A + o_hash + g * s->hash_bytes;
         ln.seed_slot = reinterpret_cast<uint32_t*>(a + o_seed);
-        ln.pick_slot = reinterpret_cast<uint32_t*>(a + o_pick);
-        ln.rank = reinterpret_cast<uint32_t*>(a + o_rank);
+        ln.rank = reinterpret_cast<uint16_t*>(a + o_rank);
         ln.picks = a + o_picks;
         for (int b = 0; b < 2; ++b) {
             char* p = a + o_fr[b];
