@@ -40,6 +40,9 @@ namespace fdg {
 namespace {
 
 constexpr uint32_t kPend = 0x80000000u;
+// An edge's src field between the last expansion and the last intern pass holds either the
+// pick's slot in tab_last or, with this bit, the final local id of an earlier layer's node.
+constexpr uint32_t kFinalSrc = 0x80000000u;
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kTile = kScanThreads * kScanItems;
@@ -118,6 +121,16 @@ template <> struct HashTab<uint32_t> {
         key = uint32_t(v >> 32);
         val = uint32_t(v);
     }
+    // Value of `key` (~0u when absent). Used on a table no thread is inserting final ids into.
+    __device__ __forceinline__ uint32_t lookup(uint32_t key) const {
+        uint32_t h = hslot(key, size);
+        for (;;) {
+            const unsigned long long v = keep ? ld_keep(e + h, keep_policy()) : e[h];
+            if (v == kEmpty) return ~0u;
+            if (uint32_t(v >> 32) == key) return uint32_t(v);
+            h = hnext(h, size);
+        }
+    }
     __device__ __forceinline__ void finalize(uint32_t h, uint32_t key, uint32_t local) const {
         const unsigned long long v = (uint64_t(key) << 32) | local;
         if (keep) st_keep(e + h, v, keep_policy());
@@ -146,6 +159,15 @@ template <> struct HashTab<uint64_t> {
         key = keys[h];
         val = vals[h];
     }
+    __device__ __forceinline__ uint32_t lookup(uint64_t key) const {
+        uint32_t h = hslot(key, size);
+        for (;;) {
+            const unsigned long long k = keys[h];
+            if (k == kEmpty) return ~0u;
+            if (k == key) return vals[h];
+            h = hnext(h, size);
+        }
+    }
     __device__ __forceinline__ void finalize(uint32_t h, uint64_t, uint32_t local) const { vals[h] = local; }
 };
 
@@ -155,7 +177,8 @@ struct Work {
     const uint64_t* indptr;
     const IdT* indices;
     uint64_t num_nodes;
-    HashTab<IdT> tab;
+    HashTab<IdT> tab;       // nodes of the passes before the last (seeds, layers < L-1)
+    HashTab<IdT> tab_last;  // the last layer's new nodes (the exact replay: one table for all)
     const uint64_t* seeds;
     uint32_t n_seeds;
     uint32_t n_layers;
@@ -448,10 +471,15 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
             slot[k] = SEEDS ? W.seed_slot[p] : W.edges[2 * (ebase + p)];  // the expansion parks the slot in src
         }
     }
+    const HashTab<IdT>& T = HAS_NEXT ? W.tab : W.tab_last;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k)
         if (valid_mask & (1u << k)) {
-            W.tab.load(slot[k], key[k], val[k]);
+            if (!HAS_NEXT && (slot[k] & kFinalSrc)) {  // an earlier layer's node: its final id
+                val[k] = slot[k] & ~kFinalSrc;
+                continue;
+            }
+            T.load(slot[k], key[k], val[k]);
             if (val[k] == (kPend | (p0 + k * kScanThreads))) first_mask |= 1u << k;
         }
     uint64_t lo[HAS_NEXT ? kScanItems : 1];
@@ -559,7 +587,7 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
             const uint32_t r = base.c + ex.c;
             const uint32_t local = node_base + r;
             W.nodes[local] = uint64_t(key[k]);
-            if (HAS_NEXT) W.tab.finalize(slot[k], key[k], local);  // no later pass reads the last layer's entries
+            if (HAS_NEXT) T.finalize(slot[k], key[k], local);  // no later pass reads the last layer's entries
             if (!SEEDS) W.edges[2 * (ebase + p)] = local;
             if constexpr (HAS_NEXT) {
                 fr.start[r] = lo[k];
@@ -697,6 +725,18 @@ __global__ void __launch_bounds__(256) k_sample(const __grid_constant__ Group<Id
 }
 
 // ---------------------------------------------------------------- k_insert ----
+// A pick's src-field value: its slot in the batch hash, or -- in the last layer, for a node
+// an earlier pass already interned (a final id in W.tab) -- kFinalSrc | that id, with no
+// insert. The last layer's new nodes go to tab_last (cleared right before the last
+// expansion, so its lines are still in L2 for the expansion and the last intern pass).
+template <typename IdT>
+__device__ __forceinline__ uint32_t place_pick(const Work<IdT>& W, bool last, IdT key, uint32_t pos) {
+    if (!last) return W.tab.insert(key, pos);
+    const uint32_t v = W.tab.lookup(key);
+    if (v < kPend) return kFinalSrc | v;
+    return W.tab_last.insert(key, pos);
+}
+
 // Thread per pick of layer l (position = pick index within the layer).
 template <typename IdT>
 __device__ __forceinline__ void insert_picks(const Work<IdT>& W, uint32_t l, uint32_t first, uint32_t stride) {
@@ -704,7 +744,8 @@ __device__ __forceinline__ void insert_picks(const Work<IdT>& W, uint32_t l, uin
     if (cnt->status) return;
     const uint32_t eb = cnt->layer_edges[l];
     const uint32_t P = cnt->layer_edges[l + 1] - eb;
-    for (uint32_t p = first; p < P; p += stride) W.edges[2 * (eb + p)] = W.tab.insert(W.picks[eb + p], p);
+    const bool last = l + 1 == W.n_layers;
+    for (uint32_t p = first; p < P; p += stride) W.edges[2 * (eb + p)] = place_pick(W, last, W.picks[eb + p], p);
 }
 
 template <typename IdT>
@@ -720,8 +761,11 @@ __global__ void __launch_bounds__(256) k_insert(const __grid_constant__ Group<Id
 // collision chain is resolved in k order with one shuffle + ballot per step; then every
 // lane inserts its pick into the batch hash and writes its edge's dst
 // (sampling.hpp:104-126).
+#ifndef FDG_EXPAND_MINB
+#define FDG_EXPAND_MINB 8  // <= 32 registers: the expansion is latency-bound (56 registers: 186 -> 203 us per Papers batch)
+#endif
 template <typename IdT>
-__global__ void __launch_bounds__(256) k_expand(const __grid_constant__ Group<IdT> G, uint32_t l) {
+__global__ void __launch_bounds__(256, FDG_EXPAND_MINB) k_expand(const __grid_constant__ Group<IdT> G, uint32_t l) {
     const Work<IdT>& W = G.w[blockIdx.y];
     fdg_batch_counts* cnt = W.cnt;
     if (cnt->status) return;
@@ -744,6 +788,7 @@ __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ Group<Id
     const bool in_group = g < npw;
     const uint32_t gbase = in_group ? g * f : 0;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const bool last = l + 1 == W.n_layers;
     bool rejected = false;
     for (uint32_t wt = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wt * npw < F; wt += nwarps) {
         const uint32_t i = wt * npw + g;
@@ -783,7 +828,7 @@ __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ Group<Id
         if (live && k < npick) {
             const uint32_t e = eb + po + k;
             // {hash slot, dst}: the intern pass reads the slot and overwrites it with the src id
-            const uint32_t slot = W.tab.insert(picked, po + k);
+            const uint32_t slot = place_pick(W, last, picked, po + k);
             *reinterpret_cast<uint2*>(W.edges + 2 * e) = make_uint2(slot, fs + i);
         }
     }
@@ -1005,7 +1050,8 @@ cudaError_t clear_hash(void* base, uint64_t bytes, int sm_count, cudaStream_t st
 
 // ------------------------------------------------------------------ Sampler ----
 struct Lane {  // per-batch workspace of one group slot
-    void* hash = nullptr;  // packed entries (u32 ids) or keys then vals (u64 ids)
+    void* hash = nullptr;       // last-layer table: packed entries (u32 ids) or keys then vals (u64 ids)
+    void* hash_a = nullptr;     // table of the earlier passes
     uint32_t* seed_slot = nullptr;
     uint16_t* rank = nullptr;
     void* picks = nullptr;
@@ -1026,10 +1072,13 @@ struct Sampler {
     uint32_t fan[FDG_MAX_LAYERS] = {};
     uint64_t max_nodes = 0, max_edges = 0, max_draws = 0;
     uint64_t F_bound[FDG_MAX_LAYERS + 1] = {}, P_bound[FDG_MAX_LAYERS + 1] = {};
-    uint32_t hsize = 0;
+    uint32_t hsize = 0;    // last-layer table (sized for every node of a batch: the replay's one table)
+    uint32_t hsize_a = 0;  // table of the passes before the last
     bool small_f = true;
     void* arena = nullptr;
-    void* hash_all = nullptr;  // the lanes' hash tables, contiguous (one memset per group)
+    void* hash_all = nullptr;  // the lanes' last-layer tables, contiguous (one fill per group)
+    void* hash_all_a = nullptr;  // the lanes' early tables, contiguous, right before hash_all
+    uint64_t hash_bytes_a = 0;
     std::vector<Lane> lanes;
     uint64_t hash_bytes = 0;   // per lane
     uint32_t* exact_flags = nullptr;  // [changed, total]
@@ -1081,14 +1130,18 @@ Work<IdT> make_work(Sampler& s, const Lane& ln, const BatchArgs& a) {
     w.indptr = s.ctx->indptr;
     w.indices = static_cast<const IdT*>(s.ctx->indices);
     w.num_nodes = s.ctx->num_nodes;
-    if constexpr (sizeof(IdT) == 4) {
-        w.tab.e = static_cast<unsigned long long*>(ln.hash);
-    } else {
-        w.tab.keys = static_cast<unsigned long long*>(ln.hash);
-        w.tab.vals = reinterpret_cast<uint32_t*>(static_cast<char*>(ln.hash) + uint64_t(s.hsize) * 8);
-    }
-    w.tab.size = s.hsize;
-    if constexpr (sizeof(IdT) == 4) w.tab.keep = uint32_t(g_hash_keep);
+    auto set_tab = [&](HashTab<IdT>& t, void* base, uint32_t size) {
+        if constexpr (sizeof(IdT) == 4) {
+            t.e = static_cast<unsigned long long*>(base);
+            t.keep = uint32_t(g_hash_keep);
+        } else {
+            t.keys = static_cast<unsigned long long*>(base);
+            t.vals = reinterpret_cast<uint32_t*>(static_cast<char*>(base) + uint64_t(size) * 8);
+        }
+        t.size = size;
+    };
+    set_tab(w.tab, ln.hash_a, s.hsize_a);
+    set_tab(w.tab_last, ln.hash, s.hsize);
     w.seeds = a.seeds;
     w.n_seeds = a.n_seeds;
     w.n_layers = s.n_layers;
@@ -1172,7 +1225,7 @@ int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
     }
     {
         FDG_TRACE("memset", st);
-        FDG_CUDA(clear_hash(s.hash_all, s.hash_bytes * n, s.ctx->sm_count, st));
+        FDG_CUDA(clear_hash(s.hash_all_a, s.hash_bytes_a * n, s.ctx->sm_count, st));
     }
     {
         FDG_TRACE("seeds", st);
@@ -1186,9 +1239,12 @@ int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
         {"expand0", "expand1", "expand2", "expand3", "expand4", "expand5", "expand6", "expand7"},
         {"intern1", "intern2", "intern3", "intern4", "intern5", "intern6", "intern7", "intern8"}};
     for (uint32_t l = 0; l < s.n_layers; ++l) {
-        if (l + 1 == s.n_layers)  // the last layer draws from the prefetch's second piece
+        if (l + 1 == s.n_layers) {  // the last layer draws from the prefetch's second piece
             for (uint32_t i = 0; i < n; ++i)
                 if (a[i].ready) FDG_CUDA(cudaStreamWaitEvent(st, a[i].ready, 0));
+            FDG_TRACE("memset_last", st);  // the last layer's table, filled right before its use
+            FDG_CUDA(clear_hash(s.hash_all, s.hash_bytes * n, s.ctx->sm_count, st));
+        }
         {
             FDG_TRACE(names[0][l], st);
             if (s.small_f) {
@@ -1214,7 +1270,9 @@ int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
         FDG_TRACE("replay", st);  // exact re-run of rejected batches (no-op otherwise)
         const uint32_t e0 = next_epoch(s, n);
         for (uint32_t l = 0; l < s.n_layers; ++l) next_epoch(s, n);
-        k_replay<IdT, false><<<dim3(1, n), kScanThreads, 0, st>>>(G, e0, s.hash_bytes);
+        Group<IdT> R = G;  // the replay samples the whole batch through the last-layer table
+        for (uint32_t i = 0; i < n; ++i) R.w[i].tab = R.w[i].tab_last;
+        k_replay<IdT, false><<<dim3(1, n), kScanThreads, 0, st>>>(R, e0, s.hash_bytes);
     }
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;
@@ -1325,6 +1383,10 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
     const uint32_t ib = ctx->idx_bytes;
     auto al = [](uint64_t b) { return (b + 255) & ~uint64_t(255); };
     s->hash_bytes = al(uint64_t(s->hsize) * (ib == 4 ? 8 : 12));
+    // the early table holds the nodes interned before the last pass (seeds, layers < L-1)
+    const uint64_t early = std::min<uint64_t>(N, nodes - std::min<uint64_t>(s->P_bound[n_layers - 1], N));
+    s->hsize_a = uint32_t((std::max<uint64_t>(early * 100 / uint64_t(g_hash_load_pct), 1024) + 31) & ~uint64_t(31));
+    s->hash_bytes_a = al(uint64_t(s->hsize_a) * (ib == 4 ? 8 : 12));
     uint64_t fmaxF = 1;
     for (uint32_t l = 0; l < n_layers; ++l) fmaxF = std::max(fmaxF, s->F_bound[l]);
     const uint64_t tiles = (std::max<uint64_t>(s->max_edges, max_seeds) + kTile - 1) / kTile + 1;
@@ -1343,6 +1405,7 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
     const uint64_t o_ctr = lz; lz += al((FDG_MAX_LAYERS + 2) * 4);
     // sampler-wide layout: hashes of all lanes first (contiguous), then lanes, then shared
     uint64_t sz = 0;
+    const uint64_t o_hash_a = sz; sz += s->hash_bytes_a * group;
     const uint64_t o_hash = sz; sz += s->hash_bytes * group;
     const uint64_t o_lanes = sz; sz += lz * group;
     const uint64_t o_ex = sz; sz += al(16);
@@ -1356,11 +1419,13 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
     }
     char* A = static_cast<char*>(s->arena);
     s->hash_all = A + o_hash;
+    s->hash_all_a = A + o_hash_a;
     s->lanes.resize(group);
     for (uint32_t g = 0; g < group; ++g) {
         Lane& ln = s->lanes[g];
         char* a = A + o_lanes + g * lz;
         ln.hash = A + o_hash + g * s->hash_bytes;
+        ln.hash_a = A + o_hash_a + g * s->hash_bytes_a;
         ln.seed_slot = reinterpret_cast<uint32_t*>(a + o_seed);
         ln.rank = reinterpret_cast<uint16_t*>(a + o_rank);
         ln.picks = a + o_picks;
@@ -1608,8 +1673,8 @@ int sampler_sample_host(Sampler* s, const uint64_t* seeds, uint32_t n_seeds, uin
 }
 
 void sampler_hash_region(const Sampler* s, void** base, uint64_t* bytes) {
-    *base = s->hash_all;
-    *bytes = s->hash_bytes * s->gmax;
+    *base = s->hash_all_a;  // both tables of every lane (contiguous)
+    *bytes = (s->hash_bytes_a + s->hash_bytes) * s->gmax;
 }
 
 void sampler_capacity(const Sampler* s, uint64_t* max_nodes, uint64_t* max_edges) {
