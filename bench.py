@@ -436,6 +436,8 @@ def run_ours(args):
     n_nodes, value, max_ms, ext_ms, busy_ms, clk = (timed[k] for k in ("n_nodes", "value", "max_ms", "ext_ms",
                                                                       "busy_ms", "clocks"))
     gather_bytes = 2 * n_nodes * rb
+    if frac:  # buffer manager: a miss also fills its slot (the reference Extractor's region write)
+        gather_bytes = gather_bytes + int(round(timed["loads_per_batch"])) * rb
     achieved = float(gather_bytes.sum()) / (busy_ms / 1e3) / 1e9
     hbm, hbm_kind = peaks()
     try:  # explanatory extra: never let it cost the bench line
@@ -500,7 +502,10 @@ def run_ours(args):
                      "traffic": _traffic(cfg), "peak_kind": hbm_kind, "kernel": kernel,
                      "launch_ms_mean": busy_ms / K, "launch_ms_mean_per_stream": float(ext_ms.mean()),
                      "bytes_per_launch": float(gather_bytes.mean()),
-                     "note": "algorithmic bytes = 2 x nodes x row_bytes per launch; launch duration = CUDA "
+                     "note": ("algorithmic bytes = (2 x nodes + misses) x row_bytes per launch (a miss is read "
+                              "from the table and written to its slot and to X; a hit is read from its slot "
+                              "and written to X); " if frac else "algorithmic bytes = 2 x nodes x row_bytes "
+                              "per launch; ") + "launch duration = CUDA "
                              "events around each extraction launch on its stream inside the timed pipelined "
                              "run; consecutive gathers alternate between two streams and can overlap, so the "
                              "average launch duration is the union of the launch intervals / launches; "

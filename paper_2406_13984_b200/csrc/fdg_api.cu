@@ -677,6 +677,11 @@ int fdg_set_option(const char* key, int64_t v) {
         g_sage_gemm = v;
         return FDG_OK;
     }
+    if (k == "hash_dyn") {
+        if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, "hash_dyn must be 0 or 1");
+        g_hash_dyn = v;
+        return FDG_OK;
+    }
     if (k == "hash_chunk") {
         if (v != 0 && v != 128 && v != 256) return fail(FDG_INVALID_ARG, "hash_chunk must be 0, 128 or 256");
         g_hash_chunk = v;
@@ -745,6 +750,8 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "extract_streams") *v = g_extract_streams;
     else if (k == "sampler_sms") *v = g_sampler_sms;
     else if (k == "tma_cfg") *v = g_tma_cfg;
+    else if (k == "hash_dyn") *v = g_hash_dyn;
+    else if (k == "tc_write_hi") *v = tc_write_hi(nullptr);  // runs the once-per-device check
     else return fail(FDG_INVALID_ARG, "unknown option " + k);
     return FDG_OK;
 }

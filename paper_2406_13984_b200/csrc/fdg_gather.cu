@@ -293,29 +293,44 @@ struct HashRbShape {
     static constexpr int MINB = CH == 128 ? 3 : 2;
 };
 
-template <int RB, int CH, bool SHARDED, bool ALIAS, bool HASH = true>
+// DYN: warps claim 32-row groups from a per-launch counter (one group ahead) instead of a
+// static stride, so CTAs that become resident late next to the samplers take less work.
+template <int RB, int CH, bool SHARDED, bool ALIAS, bool HASH = true, bool DYN = false>
 __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
     k_gather_hash_rb(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
-                     const uint32_t* status, TableRef t, char* __restrict__ out, uint64_t* checksum) {
+                     const uint32_t* status, TableRef t, char* __restrict__ out, uint64_t* checksum,
+                     uint32_t* ctr = nullptr) {
     using S = HashRbShape<CH>;
     static_assert(RB % 16 == 0, "16-byte rows");
     constexpr int NCH = (RB + CH - 1) / CH;
     constexpr int LASTP = (RB - (NCH - 1) * CH) / 16;  // 16-byte parts in the last chunk
     constexpr bool EVEN = RB % CH == 0;
     extern __shared__ __align__(16) char rb_smem[];  // kHpWarps x 32 rows x STRIDE
-    if (status && *status) return;
+    const bool skip = status && *status;
+    if (!DYN && skip) return;  // (DYN: every CTA still takes part in the counter reset)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     char* wbuf = rb_smem + warp * 32 * S::STRIDE;
-    const uint64_t n = n_dev ? *n_dev : n_host;
+    const uint64_t n = skip ? 0 : (n_dev ? *n_dev : n_host);
     const uint64_t full = n / 32;
     const uint64_t gstride = uint64_t(gridDim.x) * kHpWarps;
-    const uint64_t g0 = blockIdx.x * uint64_t(kHpWarps) + warp;
     const uint64_t pol = gather_policy_ld(t.evict_first), pol_st = gather_policy_st(t.evict_first);
     const uint32_t part = lane % S::LPR, rsub = lane / S::LPR;
     const uint64_t seed = 0x27d4eb2f165667c5ull ^ (uint64_t(RB) * 0x9e3779b97f4a7c15ull);
+    // this warp's group sequence: g0, g0 + gstride, ... (static) or its claims (DYN); the first
+    // value >= full ends it, and the warp whose sequence ends exactly at `full` owns the ragged
+    // last group
+    auto next = [&](uint64_t g) -> uint64_t {
+        if constexpr (DYN) {
+            uint32_t c = 0;
+            if (lane == 0) c = atomicAdd(ctr, 1u);
+            return __shfl_sync(0xffffffffu, c, 0);
+        } else {
+            return g + gstride;
+        }
+    };
     uint64_t sum = 0;
-    const uint64_t my_full = g0 < full ? (full - g0 + gstride - 1) / gstride : 0;
-    if (my_full) {
+    uint64_t g = DYN ? next(0) : blockIdx.x * uint64_t(kHpWarps) + warp;
+    if (g < full) {
         const char* src[S::NI];
         uint4 v[S::NI];
         auto setup = [&](uint64_t node_reg) {
@@ -331,13 +346,14 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
                 if (EVEN || c + 1 < NCH || int(part) < LASTP)
                     v[k] = ldg_row<RB % 128 != 0>(reinterpret_cast<const uint4*>(src[k] + c * CH), pol);
         };
-        uint64_t g = g0;
-        uint64_t nxt_node = (g0 + gstride < full) ? __ldg(nodes + (g0 + gstride) * 32 + lane) : 0;
-        setup(__ldg(nodes + g0 * 32 + lane));
+        uint64_t gn = next(g);
+        uint64_t nxt_node = gn < full ? __ldg(nodes + gn * 32 + lane) : 0;
+        setup(__ldg(nodes + g * 32 + lane));
         issue(0);
-        for (uint64_t i = 0; i < my_full; ++i) {
+        while (g < full) {
             char* dst = ALIAS ? nullptr : out + (g * 32 + rsub) * RB + part * 16;
             uint64_t h = seed;
+            uint64_t g2 = gn;
 #pragma unroll 1
             for (int c = 0; c < NCH; ++c) {
                 const bool lastc = c + 1 == NCH;
@@ -352,10 +368,10 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
                 if (HASH) __syncwarp();
                 if (!lastc) {
                     issue(c + 1);
-                } else if (i + 1 < my_full) {  // chunk 0 of this warp's next group
+                } else if (gn < full) {  // chunk 0 of this warp's next group
                     setup(nxt_node);
                     issue(0);
-                    const uint64_t g2 = g + 2 * gstride;
+                    g2 = next(gn);
                     nxt_node = g2 < full ? __ldg(nodes + g2 * 32 + lane) : 0;
                 }
                 if (HASH) {
@@ -373,12 +389,13 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
                 }
             }
             if (HASH) sum += splitmix64(h);
-            g += gstride;
+            g = gn;
+            gn = g2;
         }
     }
-    // the ragged last group (n % 32 rows), if this warp owns it
+    // the ragged last group (n % 32 rows), if this warp's sequence ends at it
     const uint64_t tail = full;
-    if (n % 32 && tail >= g0 && (tail - g0) % gstride == 0) {
+    if (n % 32 && g == tail) {
         const uint32_t rows = uint32_t(n - tail * 32);
         const uint64_t my_node = lane < int(rows) ? __ldg(nodes + tail * 32 + lane) : 0;
         uint64_t h = seed;
@@ -410,24 +427,42 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
         }
         if (HASH && lane < int(rows)) sum += splitmix64(h);
     }
-    if (!HASH) return;
+    if (HASH) {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
+    }
+    if constexpr (DYN) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // every CTA has claimed past the end
+                ctr[0] = 0;
+                ctr[1] = 0;
+                __threadfence();
+            }
+        }
+    }
 }
 
 
 template <int RB, int CH, bool SHARDED, bool ALIAS>
 int launch_hash_rb_one(int blocks, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
-                       const uint32_t* status, const TableRef& t, char* out, uint64_t* checksum) {
+                       const uint32_t* status, const TableRef& t, char* out, uint64_t* checksum, uint32_t* ctr) {
     constexpr int smem = kHpWarps * 32 * HashRbShape<CH>::STRIDE;
     static PerDeviceOnce attr;
     if (attr.first()) {
         FDG_CUDA(cudaFuncSetAttribute(k_gather_hash_rb<RB, CH, SHARDED, ALIAS>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        FDG_CUDA(cudaFuncSetAttribute(k_gather_hash_rb<RB, CH, SHARDED, ALIAS, true, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
-    k_gather_hash_rb<RB, CH, SHARDED, ALIAS><<<blocks, kHpWarps * 32, smem, st>>>(nodes, n_dev, n_host, status, t,
-                                                                                   out, checksum);
+    if (ctr)
+        k_gather_hash_rb<RB, CH, SHARDED, ALIAS, true, true><<<blocks, kHpWarps * 32, smem, st>>>(
+            nodes, n_dev, n_host, status, t, out, checksum, ctr);
+    else
+        k_gather_hash_rb<RB, CH, SHARDED, ALIAS><<<blocks, kHpWarps * 32, smem, st>>>(nodes, n_dev, n_host, status, t,
+                                                                                       out, checksum);
     return FDG_OK;
 }
 
@@ -440,14 +475,15 @@ int launch_hash_rb(const Ctx& c, cudaStream_t st, uint64_t groups, const uint64_
     const int ch = g_hash_chunk ? int(g_hash_chunk) : (c.row_bytes >= 256 ? 256 : 128);
     const int minb = ch == 128 ? HashRbShape<128>::MINB : HashRbShape<256>::MINB;
     const int blocks = int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps, uint64_t(c.sm_count) * minb));
+    uint32_t* ctr = g_hash_dyn ? dyn_counter(c) : nullptr;
 #define FDG_HRB(R)                                                                                      \
     case R:                                                                                             \
         if (ch == 256)                                                                                  \
             FDG_TRY((launch_hash_rb_one<R, 256, SHARDED, ALIAS>(blocks, st, nodes, n_dev, n_host, status, t, out, \
-                                                               checksum)));                             \
+                                                               checksum, ctr)));                             \
         else                                                                                            \
             FDG_TRY((launch_hash_rb_one<R, 128, SHARDED, ALIAS>(blocks, st, nodes, n_dev, n_host, status, t, out, \
-                                                               checksum)));                             \
+                                                               checksum, ctr)));                             \
         return FDG_OK;
     switch (c.row_bytes) {
         FDG_HRB(256)
@@ -702,6 +738,8 @@ int64_t g_rb_chunk = 256;      // row-group plain gather: 128- or 256-byte row c
 // 242 us for TMA + per-warp hashing (the round-1 default), Friendster 312 vs 636 us
 // (scripts/ab_checksum.sh). Round 2 removed the striped and warp-specialised variants that
 // never won an A/B (profiles/README.md, decisions).
+// Fused gather + checksum: row groups claimed from a per-launch counter (1) or a static stride (0).
+int64_t g_hash_dyn = 0;
 int64_t g_hash_chunk = 0;  // 0: 256-byte chunks for rows >= 256 B, else 128; or force 128 / 256
 int64_t g_checksum_impl = FDG_GATHER_LDG;
 

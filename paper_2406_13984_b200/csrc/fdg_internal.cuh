@@ -131,8 +131,11 @@ extern int64_t g_gather_pf64;         // 64-byte L2 fetch hint on table reads (0
 extern int g_gather_ctas_per_sm;      // chunk-striped gather: CTAs (512 threads) per SM
 extern int64_t g_rb_ctas_per_sm;      // row-group gather: CTAs (8 warps) per SM
 extern int64_t g_rb_chunk;            // row-group gather: 128- or 256-byte row chunks
+extern int64_t g_hash_dyn;            // fused gather + checksum: dynamic row-group claims
 extern int64_t g_hash_chunk;          // k_gather_hash_rb staging chunk (0 = by row size)
+extern int64_t g_hash_dyn;            // fused gather + checksum: row groups claimed dynamically (1) or static (0)
 extern int64_t g_tma_cfg;             // TMA gather ring shape 0-3
+int tc_write_hi(cudaStream_t st);       // 1: tcgen05 kind::tf32 GEMMs write A_hi (fdg_sage_tc.cu check)
 extern int64_t g_sage_gemm;           // train-stage GEMMs: 1 tensor cores (3xTF32), 0 CUDA cores
 extern int64_t g_bm_overlap;          // buffer-manager row move on its own stream (1) or after the metadata (0)
 extern int64_t g_bm_eager;            // buffer managers created in eager-invalidation (debug) mode

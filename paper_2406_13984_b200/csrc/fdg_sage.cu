@@ -46,6 +46,7 @@ int tc_gemm(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tBhi, con
 int tc_make_map_mn(CUtensorMap* map, const float* base, uint64_t rows, uint32_t cols);
 int tc_wgrad(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tB, float* P, const fdg_batch_counts* cnt,
              int j, int Kin, int N, int Z);
+int tc_write_hi(cudaStream_t st);  // 1: the split warps write A_hi (kind::tf32 does not truncate)
 // 1: layer GEMMs on the tensor cores (tcgen05 kind::tf32, 3xTF32 fp32-accurate); 0: CUDA-core fp32
 int64_t g_sage_gemm = 1;
 
@@ -728,6 +729,7 @@ int fdg_sage_create(fdg_ctx* ctx, const uint32_t* dims, uint32_t n_layers, const
             tc_make_map(&m->mapBlo[l], m->Wlo[l], np, K) == FDG_OK)
             m->tc_ok[l] = 1;
     }
+    if (g_sage_gemm) tc_write_hi(nullptr);  // the kind::tf32 truncation check, once per device, before any run
     m->Wdhi.assign(n_layers, nullptr);
     m->Wdlo.assign(n_layers, nullptr);
     m->mapDk.resize(n_layers);

@@ -24,6 +24,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -37,9 +38,10 @@ constexpr int kTcTile = kTcBM * kTcBK * 4;  // 16 KB (A and B tiles alike: 128 r
 constexpr int kTcStageBytes = 4 * kTcTile;  // A_hi (TMA lands here), A_lo, W_hi, W_lo
 // kind::tf32 reads only the top 19 bits of an fp32 operand (the low 13 mantissa bits are
 // ignored: truncation), so the TMA-landed block already is A_hi for the tensor core; the split
-// warps only write A_lo = A - trunc(A). Pinned by the 1e-5 parity tests (rounding there would
-// be a ~2^-12 relative error).
-constexpr bool kWriteHi = false;
+// warps only write A_lo = A - trunc(A). That is measured hardware behaviour, not a PTX
+// guarantee: tc_write_hi() checks it once per device (the same GEMM with and without the
+// explicit A_hi write must agree bit for bit) and turns the write on if it does not hold.
+// Also pinned by the 1e-5 parity tests (rounding would be a ~2^-12 relative error).
 constexpr int kTcThreads = 384;  // warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4-7 split, 8-11 epilogue
 constexpr int kTcEpiBytes = 4 * 32 * 32 * 4;  // epilogue staging: a 32 x 32 fp32 block per epilogue warp
 constexpr int kTcSmem = kTcStages * kTcStageBytes + 1024 /* alignment */ + 256 /* barriers */ + kTcEpiBytes;
@@ -173,7 +175,7 @@ template <bool RELU>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_sgemm_tc(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tBhi,
                const __grid_constant__ CUtensorMap tBlo, const float* __restrict__ bias, float* __restrict__ C,
-               const fdg_batch_counts* cnt, int j, int N, int K, int n_tiles) {
+               const fdg_batch_counts* cnt, int j, int N, int K, int n_tiles, int write_hi) {
     extern __shared__ uint8_t tc_raw[];
     const int M = int(d_rows_tc(cnt, j));
     const int tiles = (M + kTcBM - 1) / kTcBM * n_tiles;
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 for (int u = 0; u < kTcTile / 16 / 128; ++u) {
                     float4 h, l;
                     split4(v[u], h, l);
-                    if (kWriteHi) sts128(hi + (t4 + u * 128) * 16, h);
+                    if (write_hi) sts128(hi + (t4 + u * 128) * 16, h);
                     sts128(lo + (t4 + u * 128) * 16, l);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
@@ -331,7 +333,7 @@ __device__ __forceinline__ uint64_t umma_desc_mn(uint32_t saddr) {
            (1ull << 46) | (1ull << 61);
 }
 
-__device__ __forceinline__ void split_tile(uint8_t* hi_t, uint8_t* lo_t, int t4, int row0, int R) {
+__device__ __forceinline__ void split_tile(uint8_t* hi_t, uint8_t* lo_t, int t4, int row0, int R, int write_hi) {
     const uint32_t hi = sa(hi_t), lo = sa(lo_t);
     float4 v[kTcTile / 16 / 128];
 #pragma unroll
@@ -344,14 +346,14 @@ __device__ __forceinline__ void split_tile(uint8_t* hi_t, uint8_t* lo_t, int t4,
         if (past) v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
         float4 h, l;
         split4(v[u], h, l);
-        if (kWriteHi || past) sts128(hi + i * 16, h);
+        if (write_hi || past) sts128(hi + i * 16, h);
         sts128(lo + i * 16, l);
     }
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_wgrad_tc(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, float* __restrict__ P,
-               const fdg_batch_counts* cnt, int j, int Kin, int N, int m_tiles, int n_tiles, int Z) {
+               const fdg_batch_counts* cnt, int j, int Kin, int N, int m_tiles, int n_tiles, int Z, int write_hi) {
     extern __shared__ uint8_t tc_raw[];
     const int R = int(d_rows_tc(cnt, j));
     const int tiles = m_tiles * n_tiles, items = tiles * Z;
@@ -453,8 +455,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (int kb = k0; kb < k1; ++kb, ++it) {
                 const int s = it % kTcStages;
                 mbar_wait(full + s, uint32_t((it / kTcStages) & 1));
-                split_tile(a_hi(s), a_lo(s), t4, kb * kTcBK, R);
-                split_tile(b_hi(s), b_lo(s), t4, kb * kTcBK, R);
+                split_tile(a_hi(s), a_lo(s), t4, kb * kTcBK, R, write_hi);
+                split_tile(b_hi(s), b_lo(s), t4, kb * kTcBK, R, write_hi);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive(conv + s);
             }
@@ -545,6 +547,84 @@ int tc_make_map_mn(CUtensorMap* map, const float* base, uint64_t rows, uint32_t 
     return FDG_OK;
 }
 
+// Does kind::tf32 truncate the fp32 operand (ignore its low 13 mantissa bits)? One GEMM
+// (128 x 32 x 128, A with every mantissa bit set, W exact in tf32, W_lo = 0) with and
+// without the explicit A_hi write: equal bits <=> the tensor core saw trunc(A) in both.
+// Once per device, on a private stream; 1 (write A_hi) if the check cannot run.
+namespace {
+int write_hi_check() {
+    constexpr int M = 128, K = 32, N = 128;
+    std::vector<float> a(M * K), w(N * K);
+    uint64_t x = 0x9E3779B97F4A7C15ull;
+    auto next = [&]() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; };
+    for (auto& v : a) {  // [1, 2) with a random full mantissa, low 13 bits never all zero
+        uint32_t b = 0x3F800000u | uint32_t(next() & 0x7FFFFFu) | 1u;
+        std::memcpy(&v, &b, 4);
+    }
+    for (auto& v : w) {  // tf32-exact: low 13 bits clear
+        uint32_t b = 0x3F800000u | (uint32_t(next() & 0x7FFFFFu) & ~0x1FFFu);
+        std::memcpy(&v, &b, 4);
+    }
+    fdg_batch_counts cnt{};
+    cnt.n_nodes = M;
+    cnt.layer_nodes[1] = M;
+    float *dA = nullptr, *dW = nullptr, *dZ = nullptr, *dC = nullptr;
+    fdg_batch_counts* dcnt = nullptr;
+    cudaStream_t st = nullptr;
+    int res = 1;
+    std::vector<float> c0(M * N), c1(M * N);
+    CUtensorMap mA, mW, mZ;
+    bool ok = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaMalloc(&dA, a.size() * 4) == cudaSuccess && cudaMalloc(&dW, w.size() * 4) == cudaSuccess &&
+              cudaMalloc(&dZ, w.size() * 4) == cudaSuccess && cudaMalloc(&dC, 2ull * M * N * 4) == cudaSuccess &&
+              cudaMalloc(&dcnt, sizeof(cnt)) == cudaSuccess;
+    ok = ok && cudaMemcpy(dA, a.data(), a.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(dW, w.data(), w.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemset(dZ, 0, w.size() * 4) == cudaSuccess && cudaMemset(dC, 0, 2ull * M * N * 4) == cudaSuccess &&
+         cudaMemcpy(dcnt, &cnt, sizeof(cnt), cudaMemcpyHostToDevice) == cudaSuccess;
+    ok = ok && tc_make_map(&mA, dA, M, K) == FDG_OK && tc_make_map(&mW, dW, N, K) == FDG_OK &&
+         tc_make_map(&mZ, dZ, N, K) == FDG_OK;
+    ok = ok && cudaFuncSetAttribute(k_sgemm_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem) ==
+                   cudaSuccess;
+    if (ok) {
+        for (int wh = 0; wh < 2; ++wh)  // bias: the zero W_lo block (N floats of zeros)
+            k_sgemm_tc<false><<<1, kTcThreads, kTcSmem, st>>>(mA, mW, mZ, dZ, dC + wh * M * N, dcnt, 0, N, K, 1, wh);
+        ok = cudaStreamSynchronize(st) == cudaSuccess &&
+             cudaMemcpy(c0.data(), dC, c0.size() * 4, cudaMemcpyDeviceToHost) == cudaSuccess &&
+             cudaMemcpy(c1.data(), dC + M * N, c1.size() * 4, cudaMemcpyDeviceToHost) == cudaSuccess;
+    }
+    if (ok) {
+        double err = 0;  // the explicit write must give an fp32-accurate product
+        for (int i = 0; i < M; ++i)
+            for (int n = 0; n < N; ++n) {
+                double ref = 0;
+                for (int k = 0; k < K; ++k) ref += double(a[i * K + k]) * w[n * K + k];
+                err = std::max(err, std::abs(c1[i * N + n] - ref) / std::abs(ref));
+            }
+        if (err < 1e-5) res = std::memcmp(c0.data(), c1.data(), c0.size() * 4) == 0 ? 0 : 1;
+    }
+    cudaGetLastError();
+    cudaFree(dA);
+    cudaFree(dW);
+    cudaFree(dZ);
+    cudaFree(dC);
+    cudaFree(dcnt);
+    if (st) cudaStreamDestroy(st);
+    return res;
+}
+int g_write_hi[64];
+PerDeviceOnce g_write_hi_once;
+}  // namespace
+
+int tc_write_hi(cudaStream_t) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_write_hi_once.first()) __atomic_store_n(&g_write_hi[dev & 63], write_hi_check() + 1, __ATOMIC_RELEASE);
+    while (!__atomic_load_n(&g_write_hi[dev & 63], __ATOMIC_ACQUIRE)) {
+    }
+    return g_write_hi[dev & 63] - 1;
+}
+
 int tc_wgrad(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tB, float* P, const fdg_batch_counts* cnt,
              int j, int Kin, int N, int Z) {
     static PerDeviceOnce attr;
@@ -556,7 +636,8 @@ int tc_wgrad(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tB, floa
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int m_tiles = (Kin + kTcBM - 1) / kTcBM, n_tiles = (N + kTcBN - 1) / kTcBN;
     const int items = m_tiles * n_tiles * Z;
-    k_wgrad_tc<<<std::min(items, sms), kTcThreads, kTcSmem, st>>>(tA, tB, P, cnt, j, Kin, N, m_tiles, n_tiles, Z);
+    k_wgrad_tc<<<std::min(items, sms), kTcThreads, kTcSmem, st>>>(tA, tB, P, cnt, j, Kin, N, m_tiles, n_tiles, Z,
+                                                                 tc_write_hi(st));
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;
 }
@@ -576,10 +657,11 @@ int tc_gemm(cudaStream_t st, const CUtensorMap& tA, const CUtensorMap& tBhi, con
     const int n_tiles = npad / kTcBN;
     const uint64_t tiles = (rows_bound + kTcBM - 1) / kTcBM * uint64_t(n_tiles);
     const uint32_t grid = uint32_t(std::min<uint64_t>(tiles, uint64_t(sms)));  // persistent: one CTA per SM
+    const int wh = tc_write_hi(st);
     if (relu)
-        k_sgemm_tc<true><<<grid, kTcThreads, kTcSmem, st>>>(tA, tBhi, tBlo, bias, C, cnt, j, N, K, n_tiles);
+        k_sgemm_tc<true><<<grid, kTcThreads, kTcSmem, st>>>(tA, tBhi, tBlo, bias, C, cnt, j, N, K, n_tiles, wh);
     else
-        k_sgemm_tc<false><<<grid, kTcThreads, kTcSmem, st>>>(tA, tBhi, tBlo, bias, C, cnt, j, N, K, n_tiles);
+        k_sgemm_tc<false><<<grid, kTcThreads, kTcSmem, st>>>(tA, tBhi, tBlo, bias, C, cnt, j, N, K, n_tiles, wh);
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;
 }

@@ -191,6 +191,14 @@ def test_gather_and_checksum(fd, port, dim, dtype):
     assert cs == port.checksum_rows(table[nodes.astype(np.int64)])
     empty = fd.gather(t, np.zeros(0, np.uint64))
     assert empty.shape == (0, t.row_bytes)
+    fd.set_option("hash_dyn", 1)  # row groups claimed from a per-launch counter (option, A/B)
+    try:
+        for m in (nodes, nodes[:31], nodes[:4097]):  # the ragged last group goes to exactly one warp
+            x3, cs3 = fd.gather(t, m, checksum=True)
+            np.testing.assert_array_equal(x3, table[m.astype(np.int64)])
+            assert cs3 == port.checksum_rows(table[m.astype(np.int64)])
+    finally:
+        fd.set_option("hash_dyn", 0)
 
 
 def test_gather_sharded(fd):

@@ -35,6 +35,16 @@ def gemm(request, fd):
     fd.set_option("sage_gemm", old)
 
 
+def test_tf32_truncation_check(fd):
+    """The 3xTF32 split relies on kind::tf32 ignoring the low 13 mantissa bits of an fp32
+    operand (A_hi is then the TMA-landed block itself). fdg_sage_tc.cu checks this once per
+    device -- the same GEMM with and without the explicit A_hi write must agree bit for bit
+    and be fp32-accurate -- and writes A_hi when it does not hold (option "tc_write_hi").
+    B200 truncates: the check must find that (a 1 here would mean a slower but still exact
+    split, and that the hardware model in DESIGN.md is wrong)."""
+    assert fd.featdrive.get_option("tc_write_hi") == 0
+
+
 @pytest.mark.parametrize("dim,dims,fan,seeds", [
     (32, [32, 64, 64, 12], [10, 10, 10], 300),
     (128, [128, 256, 256, 172], [10, 10, 10], 200),   # the paper's Papers100M model shape
