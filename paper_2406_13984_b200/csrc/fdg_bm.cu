@@ -6,17 +6,16 @@
 // reference's state transitions and LRU order, computed batch-parallel:
 //
 //   mapping table  node -> packed {i32 slot, u32 valid<<31}  (8 B/node), invalidated
-//                  lazily: an entry is live only while slot[entry.slot].node still
+//                  lazily: an entry is live only while slot[entry.slot]'s owner still
 //                  names the node, so an eviction rebinds the slot without touching the
 //                  previous owner's entry (two random DRAM accesses per miss saved; the
 //                  acquire's owner check reads the slot record, which mostly hits L2)
-//   slot refs      slot -> u32 reference count (the reference keeps ref in the mapping
-//                  entry; a bound node's count lives with its slot here, so the release
-//                  walks the batch's alias list into a compact 4 B/slot array that stays
-//                  L2-resident instead of re-reading 8 B/node entries from DRAM)
-//   slot table     slot -> {u64 owner node (~0 = free), u64 ring position of its
-//                  live standby entry (~0 = not in the standby list)}: one 16-byte
-//                  record, so the reverse map and list membership share a sector
+//   slot table     slot -> {u64 owner node (40 bits; all ones = free) | reference count
+//                  << 40, u64 ring position of its live standby entry (~0 = not in the
+//                  standby list)}: one 16-byte record, so the reverse map, the bound node's
+//                  reference count (the reference keeps it in the mapping entry) and list
+//                  membership share a sector -- an acquire hit, a bind and a release each
+//                  touch one random record instead of a record plus a separate count
 //   standby list   the reference's intrusive LRU list becomes a FIFO ring of
 //                  slot ids with tombstones: push_mru = append at `tail`
 //                  (recording the slot's ring position), remove(slot) on a hit
@@ -65,10 +64,34 @@ struct Entry {
 };
 
 constexpr uint64_t kUnlisted = ~0ull;
+constexpr int kRefShift = 40;
+constexpr uint64_t kFree = (1ull << kRefShift) - 1;  // owner field of a free slot (node ids < 2^40 - 1)
+constexpr uint64_t kRef1 = 1ull << kRefShift;
 struct __align__(16) SlotMeta {
-    uint64_t node;  // owner (kNoNode = free)
-    uint64_t pos;   // ring position of the live standby entry (kUnlisted = none)
+    uint64_t nr;   // owner node (low 40 bits, kFree = free) | reference count << 40
+    uint64_t pos;  // ring position of the live standby entry (kUnlisted = none)
 };
+__host__ __device__ __forceinline__ uint64_t m_node(uint64_t nr) { return nr & kFree; }
+__host__ __device__ __forceinline__ uint32_t m_ref(uint64_t nr) { return uint32_t(nr >> kRefShift); }
+// Random metadata reads. FDG_BM_RAND64=1: with a 64-byte L2 fill (ld_rand64, fdg_internal.cuh);
+// measured 540 vs 536 us per Papers batch with plain loads (the metadata chain is bound by the
+// random-access rate, not bytes), so plain loads by default.
+#ifndef FDG_BM_RAND64
+#define FDG_BM_RAND64 0
+#endif
+__device__ __forceinline__ uint64_t ld_meta(const void* p) {
+#if FDG_BM_RAND64
+    return ld_rand64(p);
+#else
+    return *static_cast<const uint64_t*>(p);
+#endif
+}
+__device__ __forceinline__ Entry ld_entry(const Entry* p) {
+    const uint64_t v = ld_meta(p);
+    return Entry{int32_t(uint32_t(v)), uint32_t(v >> 32)};
+}
+__device__ __forceinline__ uint64_t ld_nr(const SlotMeta* p) { return ld_meta(&p->nr); }
+__device__ __forceinline__ uint64_t ld_pos(const SlotMeta* p) { return ld_meta(&p->pos); }
 
 struct BmState {
     uint64_t head, tail;   // ring positions (monotonic)
@@ -85,8 +108,7 @@ struct BmState {
 
 struct BmDev {
     Entry* map;
-    uint32_t* ref;        // slot -> reference count of its bound node
-    SlotMeta* slot;       // slot -> {owner node, live ring position}
+    SlotMeta* slot;       // slot -> {owner node | reference count, live ring position}
     int32_t* ring[2];
     uint64_t R;           // ring capacity
     uint64_t S;           // slots
@@ -196,15 +218,17 @@ __global__ void __launch_bounds__(kT) k_acquire(BmDev B, const uint64_t* nodes, 
     const uint64_t i0 = uint64_t(tile) * kTileN + threadIdx.x * kI;
     uint32_t load_mask = 0, mine = 0, hits = 0, removed = 0;
     bool bad = false;
-    uint64_t nd[kI];
+    uint64_t nd[kI], nr[kI];
     Entry en[kI];
 #pragma unroll
     for (int k = 0; k < kI; ++k) nd[k] = i0 + k < n ? nodes[i0 + k] : kNoNode;
 #pragma unroll
-    for (int k = 0; k < kI; ++k) en[k] = nd[k] < B.N ? B.map[nd[k]] : Entry{-1, 0u};  // all loads in flight
+    for (int k = 0; k < kI; ++k) en[k] = nd[k] < B.N ? ld_entry(B.map + nd[k]) : Entry{-1, 0u};  // all loads in flight
+#pragma unroll
+    for (int k = 0; k < kI; ++k) nr[k] = (en[k].refv & kValid) ? ld_nr(B.slot + en[k].slot) : kFree;
 #pragma unroll
     for (int k = 0; k < kI; ++k)  // lazy invalidation: an entry is live only while its slot still names the node
-        if ((en[k].refv & kValid) && B.slot[en[k].slot].node != nd[k]) en[k] = Entry{-1, 0u};
+        if ((en[k].refv & kValid) && m_node(nr[k]) != nd[k]) en[k] = Entry{-1, 0u};
 #pragma unroll
     for (int k = 0; k < kI; ++k) {
         const uint64_t i = i0 + k;
@@ -216,12 +240,12 @@ __global__ void __launch_bounds__(kT) k_acquire(BmDev B, const uint64_t* nodes, 
         }
         const Entry e = en[k];
         if (e.refv & kValid) {  // hit: ref++ (a batch's nodes, hence slots, are distinct)
-            const uint32_t ref = B.ref[e.slot];
-            if (ref == 0) {  // StandbyList::remove (buffer_manager.hpp:250)
-                B.slot[e.slot].pos = kUnlisted;
+            if (m_ref(nr[k]) == 0) {  // StandbyList::remove (buffer_manager.hpp:250)
+                B.slot[e.slot] = SlotMeta{nr[k] + kRef1, kUnlisted};
                 ++removed;
+            } else {
+                B.slot[e.slot].nr = nr[k] + kRef1;
             }
-            B.ref[e.slot] = ref + 1;
             alias[i] = e.slot;
             is_load[i] = 0;
             ++hits;
@@ -286,7 +310,7 @@ __global__ void __launch_bounds__(kT) k_select(BmDev B, uint32_t epoch) {
 #pragma unroll
         for (int k = 0; k < kI; ++k) {  // list membership: one random 8-byte load per entry, all in flight
             const uint64_t p = p0 + threadIdx.x * kI + k;
-            if (slots[k] >= 0 && B.slot[slots[k]].pos == p) {
+            if (slots[k] >= 0 && ld_pos(B.slot + slots[k]) == p) {
                 live_mask |= 1u << k;
                 ++mine;
             } else {
@@ -323,18 +347,18 @@ __global__ void k_bind(BmDev B, const uint64_t* nodes, int64_t* alias) {
         const int32_t slot = B.sel[k];
         const uint32_t i = B.load_pos[k];
         const uint64_t node = nodes[i];
-        const uint64_t prev = B.slot[slot].node;
-        if (prev != kNoNode) {  // evict the previous owner (buffer_manager.hpp:281-291): rebinding the
+        const uint64_t pnr = ld_nr(B.slot + slot);
+        const uint64_t prev = m_node(pnr);
+        if (prev != kFree) {  // evict the previous owner (buffer_manager.hpp:281-291): rebinding the
             // slot below is the invalidation -- its mapping entry goes stale
-            if (B.ref[slot] != 0) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
+            if (m_ref(pnr) != 0) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
             // eager (debug) mode: the reference's invalidation (buffer_manager.hpp:284-287). prev
             // cannot be a miss of this batch: its entry is live, so it would have been a hit.
             if (B.eager) B.map[prev] = Entry{-1, 0u};
             ++ev;
         }
         B.map[node] = Entry{slot, kValid};  // bind + publish
-        B.slot[slot] = SlotMeta{node, kUnlisted};
-        B.ref[slot] = 1;
+        B.slot[slot] = SlotMeta{node | kRef1, kUnlisted};  // its reference from acquire_for_batch
         alias[i] = slot;
     }
 #pragma unroll
@@ -507,40 +531,45 @@ __global__ void __launch_bounds__(kT) k_release(BmDev B, const uint64_t* nodes, 
     int32_t slots[kI];
     bool bad = false;
     int32_t sl[kI];
+    uint64_t nr[kI];
     if constexpr (ALIAS) {
 #pragma unroll
         for (int k = 0; k < kI; ++k) {
             const int64_t a = i0 + k < n ? alias[i0 + k] : -1;
             sl[k] = (a >= 0 && uint64_t(a) < B.S) ? int32_t(a) : -1;
         }
+#pragma unroll
+        for (int k = 0; k < kI; ++k) nr[k] = sl[k] >= 0 ? ld_nr(B.slot + sl[k]) : kFree;  // all loads in flight
     } else {
         uint64_t nd[kI];
 #pragma unroll
         for (int k = 0; k < kI; ++k) nd[k] = i0 + k < n ? nodes[i0 + k] : kNoNode;
 #pragma unroll
         for (int k = 0; k < kI; ++k) {  // all loads in flight
-            const Entry e = nd[k] < B.N ? B.map[nd[k]] : Entry{-1, 0u};
+            const Entry e = nd[k] < B.N ? ld_entry(B.map + nd[k]) : Entry{-1, 0u};
             sl[k] = (e.refv & kValid) ? e.slot : -1;
         }
 #pragma unroll
-        for (int k = 0; k < kI; ++k)
-            if (sl[k] >= 0 && B.slot[sl[k]].node != nd[k]) sl[k] = -1;  // stale entry: not resident
+        for (int k = 0; k < kI; ++k) {
+            nr[k] = sl[k] >= 0 ? ld_nr(B.slot + sl[k]) : kFree;
+            if (sl[k] >= 0 && m_node(nr[k]) != nd[k]) sl[k] = -1;  // stale entry: not resident
+        }
     }
-    uint32_t rf[kI];
-#pragma unroll
-    for (int k = 0; k < kI; ++k) rf[k] = sl[k] >= 0 ? B.ref[sl[k]] : 0u;
 #pragma unroll
     for (int k = 0; k < kI; ++k) {
         if (i0 + k >= n) break;
-        if (sl[k] < 0 || rf[k] == 0) {  // not resident / no reference (buffer_manager.hpp:357, 462)
+        const uint32_t rf = sl[k] >= 0 ? m_ref(nr[k]) : 0u;
+        if (sl[k] < 0 || rf == 0) {  // not resident / no reference (buffer_manager.hpp:357, 462)
             bad = true;
             continue;
         }
-        B.ref[sl[k]] = rf[k] - 1;
-        if (rf[k] == 1) {
+        nr[k] -= kRef1;
+        if (rf == 1) {  // written with its ring position below
             slots[k] = sl[k];
             mask |= 1u << k;
             ++mine;
+        } else {
+            B.slot[sl[k]].nr = nr[k];
         }
     }
     if (bad) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
@@ -552,7 +581,7 @@ __global__ void __launch_bounds__(kT) k_release(BmDev B, const uint64_t* nodes, 
         if (mask & (1u << k)) {  // push_mru in batch order (buffer_manager.hpp:467)
             uint64_t p = tail + r++;
             ring[p % B.R] = slots[k];
-            B.slot[slots[k]].pos = p;
+            B.slot[slots[k]] = SlotMeta{nr[k], p};
         }
     if (threadIdx.x == 0 && tile == ntiles - 1) {
         uint32_t tot = s_misc[1];
@@ -632,8 +661,7 @@ __global__ void k_init(BmDev B) {
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < B.N; v += stride) B.map[v] = Entry{-1, 0u};
     for (uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; s < B.S; s += stride) {
-        B.slot[s] = SlotMeta{kNoNode, s};
-        B.ref[s] = 0;
+        B.slot[s] = SlotMeta{kFree, s};
         B.ring[0][s] = int32_t(s);
     }
 }
@@ -662,13 +690,14 @@ __global__ void k_pop(BmDev B, int64_t* slots_out) {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < L) {
         const int32_t slot = B.sel[k];
-        const uint64_t prev = B.slot[slot].node;
-        if (prev != kNoNode) {
-            if (B.ref[slot] != 0) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
+        const uint64_t pnr = B.slot[slot].nr;
+        const uint64_t prev = m_node(pnr);
+        if (prev != kFree) {
+            if (m_ref(pnr) != 0) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
             if (B.eager) B.map[prev] = Entry{-1, 0u};
             ++ev;
         }
-        B.slot[slot] = SlotMeta{kNoNode, kUnlisted};
+        B.slot[slot] = SlotMeta{kFree, kUnlisted};
         slots_out[k] = slot;
     }
 #pragma unroll
@@ -683,7 +712,7 @@ __global__ void k_pop(BmDev B, int64_t* slots_out) {
 __device__ __forceinline__ bool entry_live(const BmDev& B, uint64_t node, Entry* out) {
     const Entry e = B.map[node];
     *out = e;
-    return e.slot >= 0 && uint64_t(e.slot) < B.S && B.slot[e.slot].node == node;
+    return e.slot >= 0 && uint64_t(e.slot) < B.S && m_node(B.slot[e.slot].nr) == node;
 }
 
 // bind_slot (297-310): the node takes a free slot, not yet valid; its reference from
@@ -697,13 +726,12 @@ __global__ void k_bind_explicit(BmDev B, const uint64_t* nodes, const int64_t* s
     const int64_t slot = slots[i];
     Entry e;
     if (node >= B.N || slot < 0 || uint64_t(slot) >= B.S || entry_live(B, node, &e) ||
-        B.slot[slot].node != kNoNode || B.slot[slot].pos != kUnlisted) {
+        B.slot[slot].nr != kFree || B.slot[slot].pos != kUnlisted) {
         atomicExch(&S->status, uint32_t(FDG_INVARIANT));  // FD_CHECKs of bind_slot
         return;
     }
     B.map[node] = Entry{int32_t(slot), 0u};
-    B.slot[slot].node = node;
-    B.ref[slot] = 1;
+    B.slot[slot].nr = node | kRef1;
 }
 
 // publish_valid (313-324)
@@ -735,12 +763,13 @@ __global__ void k_unwind_or_release(BmDev B, uint64_t node, int unwind) {
             atomicExch(&S->status, uint32_t(FDG_INVARIANT));
             return;
         }
-        B.slot[e.slot].node = kNoNode;
+        B.slot[e.slot].nr = kFree;  // the node's reference goes with its entry
         B.map[node] = Entry{-1, 0u};
         push = e.slot;
     } else {
         if (!live) return;  // a miss never bound holds no slot-side reference here
-        const uint32_t r = B.ref[e.slot];
+        const uint64_t nr = B.slot[e.slot].nr;
+        const uint32_t r = m_ref(nr);
         if (r == 0) {
             atomicExch(&S->status, uint32_t(FDG_INVARIANT));  // ref_count decrement below zero
             return;
@@ -749,7 +778,7 @@ __global__ void k_unwind_or_release(BmDev B, uint64_t node, int unwind) {
             atomicExch(&S->status, uint32_t(FDG_INVARIANT));
             return;
         }
-        B.ref[e.slot] = r - 1;
+        B.slot[e.slot].nr = nr - kRef1;
         if (r == 1) push = e.slot;
     }
     if (push >= 0) {
@@ -834,6 +863,8 @@ int bm_build(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint32_t 
     if (ctx->row_bytes == 0) return fail(FDG_NOT_LOADED, "buffer manager needs a feature table");
     if (ctx->row_bytes % 16) return fail(FDG_INVALID_ARG, "buffer manager: row_bytes must be a multiple of 16");
     if (ctx->n_shards > 1) return fail(FDG_INVALID_ARG, "buffer manager: sharded tables not supported yet");
+    if ((ctx->num_nodes ? ctx->num_nodes : ctx->feat_nodes) >= kFree)
+        return fail(FDG_INVALID_ARG, "buffer manager: node ids must be < 2^40 - 1");
     cudaSetDevice(ctx->device);
     auto b = new fdg_bm();
     b->ctx = ctx;
@@ -845,7 +876,6 @@ int bm_build(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint32_t 
     uint64_t sz = 0;
     const uint64_t o_map = sz; sz += al(N * 8);
     const uint64_t o_slot = sz; sz += al(slot_count * sizeof(SlotMeta));
-    const uint64_t o_ref = sz; sz += al(slot_count * 4);
     const uint64_t o_r0 = sz; sz += al(R * 4);
     const uint64_t o_r1 = sz; sz += al(R * 4);
     const uint64_t o_st = sz; sz += al(sizeof(BmState));
@@ -869,7 +899,6 @@ int bm_build(fdg_ctx* ctx, uint64_t slot_count, uint64_t min_reserved, uint32_t 
     BmDev& d = b->d;
     d.map = reinterpret_cast<Entry*>(a + o_map);
     d.slot = reinterpret_cast<SlotMeta*>(a + o_slot);
-    d.ref = reinterpret_cast<uint32_t*>(a + o_ref);
     d.ring[0] = reinterpret_cast<int32_t*>(a + o_r0);
     d.ring[1] = reinterpret_cast<int32_t*>(a + o_r1);
     d.R = R;
@@ -1118,14 +1147,13 @@ int fdg_bm_entry(fdg_bm* b, uint64_t node, int64_t* slot, uint32_t* ref, uint32_
     FDG_CUDA(cudaDeviceSynchronize());
     Entry e;
     FDG_CUDA(cudaMemcpy(&e, b->d.map + node, sizeof(e), cudaMemcpyDeviceToHost));
+    uint64_t nr = kFree;
     if (e.slot >= 0) {  // a stale entry (slot rebound since) reads as the reference's evicted state
-        uint64_t owner;
-        FDG_CUDA(cudaMemcpy(&owner, &b->d.slot[e.slot].node, 8, cudaMemcpyDeviceToHost));
-        if (owner != node) e = Entry{-1, 0u};
+        FDG_CUDA(cudaMemcpy(&nr, &b->d.slot[e.slot].nr, 8, cudaMemcpyDeviceToHost));
+        if (m_node(nr) != node) e = Entry{-1, 0u};
     }
     *slot = e.slot;
-    *ref = 0;
-    if (e.slot >= 0) FDG_CUDA(cudaMemcpy(ref, b->d.ref + e.slot, 4, cudaMemcpyDeviceToHost));
+    *ref = e.slot >= 0 ? m_ref(nr) : 0u;
     *valid = e.refv >> 31;
     return FDG_OK;
 }
@@ -1145,8 +1173,8 @@ int fdg_bm_reverse(fdg_bm* b, uint64_t slot, int64_t* node) {
     if (slot >= b->slots) return fail(FDG_OUT_OF_RANGE, "bm_reverse: slot out of range");
     FDG_CUDA(cudaDeviceSynchronize());
     uint64_t v;
-    FDG_CUDA(cudaMemcpy(&v, &b->d.slot[slot].node, 8, cudaMemcpyDeviceToHost));
-    *node = v == kNoNode ? -1 : int64_t(v);
+    FDG_CUDA(cudaMemcpy(&v, &b->d.slot[slot].nr, 8, cudaMemcpyDeviceToHost));
+    *node = m_node(v) == kFree ? -1 : int64_t(m_node(v));
     return FDG_OK;
 }
 
@@ -1165,9 +1193,9 @@ int fdg_bm_validate(fdg_bm* b) {
     FDG_CUDA(cudaMemcpy(map.data(), d.map, d.N * 8, cudaMemcpyDeviceToHost));
     FDG_CUDA(cudaMemcpy(meta.data(), d.slot, d.S * sizeof(SlotMeta), cudaMemcpyDeviceToHost));
     std::vector<uint32_t> ref(d.S);
-    FDG_CUDA(cudaMemcpy(ref.data(), d.ref, d.S * 4, cudaMemcpyDeviceToHost));
     for (uint64_t s = 0; s < d.S; ++s) {
-        rev[s] = meta[s].node;
+        rev[s] = m_node(meta[s].nr);
+        ref[s] = m_ref(meta[s].nr);
         pos[s] = meta[s].pos;
     }
     // Lazy invalidation: stale entries (slot rebound since) are the reference's evicted
@@ -1198,7 +1226,7 @@ int fdg_bm_validate(fdg_bm* b) {
     }
     if (live != h.live) return fail(FDG_INVARIANT, "standby size mismatch");
     for (uint64_t s = 0; s < d.S; ++s) {
-        if (rev[s] == kNoNode) {
+        if (rev[s] == kFree) {
             if (ref[s] != 0) return fail(FDG_INVARIANT, "free slot with references");
             continue;
         }

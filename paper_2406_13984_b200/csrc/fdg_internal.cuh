@@ -44,6 +44,34 @@ private:
 #define FDG_CAT(a, b) FDG_CAT2(a, b)
 #define FDG_TRACE(name, st) ::fdg::TraceScope FDG_CAT(_fdg_trace_, __LINE__)(name, st)
 
+
+// Random loads with a 64-byte L2 fill. B200 fills a random load miss with a whole 128-byte
+// line by default (scripts/probes/rand_gran.cu under ncu: 129.6 DRAM bytes per random 8-byte
+// load under every cudaLimitMaxL2FetchGranularity setting); the .L2::64B prefetch-size hint
+// halves that (66.8 B). Stores are sector-granular already (34 B read + 30 B written per
+// random 8-byte store). FDG_RAND64=0 builds plain loads (A/B).
+#ifndef FDG_RAND64
+#define FDG_RAND64 1
+#endif
+__device__ __forceinline__ uint64_t ld_rand64(const void* p) {
+    uint64_t v;
+#if FDG_RAND64
+    asm volatile("ld.global.L2::64B.b64 %0, [%1];" : "=l"(v) : "l"(p));
+#else
+    v = *static_cast<const uint64_t*>(p);
+#endif
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_rand32(const void* p) {
+    uint32_t v;
+#if FDG_RAND64
+    asm volatile("ld.global.L2::64B.b32 %0, [%1];" : "=r"(v) : "l"(p));
+#else
+    v = *static_cast<const uint32_t*>(p);
+#endif
+    return v;
+}
+
 // ---- reference hashing on device (common.hpp:77-105) ------------------------------
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     x += 0x9e3779b97f4a7c15ull;

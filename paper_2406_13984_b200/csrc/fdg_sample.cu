@@ -207,6 +207,14 @@ struct Group {
     Work<IdT> w[kGMax];
 };
 
+// Random CSR reads (a pick's neighbour entry, a frontier node's indptr pair) with a 64-byte L2
+// fill instead of the default 128-byte line (ld_rand64, fdg_internal.cuh).
+template <typename IdT>
+__device__ __forceinline__ IdT ld_idx(const IdT* p) {
+    if constexpr (sizeof(IdT) == 4) return ld_rand32(p);
+    else return ld_rand64(p);
+}
+
 // libstdc++ uniform_int_distribution<u64>(0, j) on the word stream (uniform_int_dist.h:257-281).
 __device__ __forceinline__ uint64_t lemire(const uint64_t* words, uint64_t cap, uint64_t& pos, uint64_t j,
                                            uint32_t& extra, bool& overflow) {
@@ -489,8 +497,8 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
 #pragma unroll
         for (int k = 0; k < kScanItems; ++k)
             if (first_mask & (1u << k)) {
-                lo[k] = W.indptr[uint64_t(key[k])];
-                hi[k] = W.indptr[uint64_t(key[k]) + 1];
+                lo[k] = ld_rand64(W.indptr + uint64_t(key[k]));
+                hi[k] = ld_rand64(W.indptr + uint64_t(key[k]) + 1);
             }
 #pragma unroll
         for (int k = 0; k < kScanItems; ++k) dg[k] = (first_mask & (1u << k)) ? uint32_t(hi[k] - lo[k]) : 0u;
@@ -672,8 +680,8 @@ __device__ __forceinline__ void sample_nodes(const Work<IdT>& W, uint32_t l, uin
 #pragma unroll
             for (int k = 0; k < kMaxF; ++k)
                 if (k < int(f)) {
-                    cand[k] = W.indices[start + t[k]];
-                    alt[k] = W.indices[start + jlo + k];
+                    cand[k] = ld_idx(W.indices + start + t[k]);
+                    alt[k] = ld_idx(W.indices + start + jlo + k);
                 }
             IdT picked[kMaxF];
 #pragma unroll
@@ -811,8 +819,8 @@ __global__ void __launch_bounds__(256, FDG_EXPAND_MINB) k_expand(const __grid_co
                 const uint64_t w = __ldg(W.words + db + dro + k);
                 const uint64_t lo = w * r;
                 if (lo < r && lo < (0 - r) % r) rejected = true;
-                picked = W.indices[start + __umul64hi(w, r)];
-                alt = W.indices[start + j];
+                picked = ld_idx(W.indices + start + __umul64hi(w, r));
+                alt = ld_idx(W.indices + start + j);
             } else {
                 picked = W.indices[start + k];
             }
