@@ -48,6 +48,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "fdg_internal.cuh"
+#include "fdg_tma.cuh"
 
 namespace fdg {
 namespace {
@@ -379,8 +380,17 @@ __global__ void k_bind(BmDev B, const uint64_t* nodes, int64_t* alias) {
 // 332 us in the pipeline at 4 x 512 per SM vs 32 us alone). A warp moves kMoveRows rows
 // at a time: their metadata (one lane per row, shuffled) resolves first, then every
 // lane has kMoveRows 16-byte loads in flight.
-constexpr int kMoveRows = 4;
-__global__ void __launch_bounds__(512) k_move(BmDev B, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+#ifndef FDG_MOVE_ROWS
+#define FDG_MOVE_ROWS 4
+#endif
+#ifndef FDG_MOVE_MINB
+#define FDG_MOVE_MINB 2
+#endif
+#ifndef FDG_MOVE_CTAS
+#define FDG_MOVE_CTAS 2
+#endif
+constexpr int kMoveRows = FDG_MOVE_ROWS;
+__global__ void __launch_bounds__(512, FDG_MOVE_MINB) k_move(BmDev B, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                                               const int64_t* alias, const uint8_t* is_load, const char* table,
                                               char* region, uint32_t rb, char* X, uint32_t host_table) {
     BmState* S = B.st;
@@ -442,6 +452,81 @@ __global__ void __launch_bounds__(512) k_move(BmDev B, const uint64_t* nodes, co
             }
         }
     }
+}
+
+// ------------------------------------------------------------ TMA move ----
+// The row move on the TMA: each row lands in shared memory by one cp.async.bulk (completing on
+// its stage's mbarrier) and leaves by bulk stores to X and, for a miss, to its slot. The bytes
+// in flight sit in shared memory, not registers: one 4-warp CTA per SM keeps ~96 KB of rows in
+// flight with a few thousand registers, so the rest of the SM stays free for the next batch's
+// metadata kernels, the samplers and the MT prefetch (the LDG k_move's 2 x 512 threads at 60
+// registers hold the whole register file for its ~290 us). Warp w of CTA c takes row chunks
+// w + 4c, w + 4c + 4 * grid, ... (RS rows each, one row per lane); each warp runs a D-stage
+// ring with A chunks of loads in flight.
+constexpr int kMoveTmaWarps = 4;
+template <int D, int A>
+__global__ void __launch_bounds__(kMoveTmaWarps * 32, 1)
+    k_move_tma(BmDev B, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host, const int64_t* alias,
+               const uint8_t* is_load, const char* table, char* region, uint32_t rb, uint32_t RS, char* X) {
+    static_assert(A < D, "lookahead must leave a stage for the stores in flight");
+    using namespace tma;
+    extern __shared__ __align__(128) char mv_smem[];
+    __shared__ __align__(8) uint64_t bars[kMoveTmaWarps][D];
+    if (B.st->status) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t stage_bytes = RS * rb;
+    uint64_t pol;  // row traffic must not flush the batch's metadata sectors out of L2
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    char* wbase = mv_smem + size_t(warp) * D * stage_bytes;
+    const uint64_t n = load_n(n_dev, n_host);
+    const uint64_t nchunks = (n + RS - 1) / RS;
+    const uint64_t gw = uint64_t(blockIdx.x) * kMoveTmaWarps + warp, nw = uint64_t(gridDim.x) * kMoveTmaWarps;
+    const uint64_t my_n = gw < nchunks ? (nchunks - gw + nw - 1) / nw : 0;
+    if (lane == 0)
+        for (int d = 0; d < D; ++d) mbar_init(smem_u32(&bars[warp][d]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    struct Src {
+        const char* p;  // null: nothing to load for this lane
+    };
+    auto src_of = [&](uint64_t i) -> Src {  // this lane's row of chunk i
+        const uint64_t r = (gw + i * nw) * RS + lane;
+        if (i >= my_n || lane >= int(RS) || r >= n) return Src{nullptr};
+        const uint32_t miss = is_load[r];
+        if (!miss && !X) return Src{nullptr};  // a hit without X: nothing moves
+        return Src{miss ? table + nodes[r] * rb : region + uint64_t(alias[r]) * rb};
+    };
+    auto issue = [&](uint64_t i, Src sr) {
+        const int s = int(i % D);
+        const uint32_t bar = smem_u32(&bars[warp][s]);
+        const uint32_t loading = __ballot_sync(0xffffffffu, sr.p != nullptr);
+        if (lane == 0) mbar_arrive_expect_tx(bar, uint32_t(__popc(loading)) * rb);
+        __syncwarp();
+        if (sr.p) bulk_load(smem_u32(wbase + s * stage_bytes + lane * rb), sr.p, rb, bar, pol);
+    };
+    for (int i = 0; i < A; ++i)
+        if (uint64_t(i) < my_n) issue(i, src_of(i));
+    Src pa = src_of(A), pb = src_of(A + 1);  // sources two chunks ahead of issue
+    for (uint64_t i = 0; i < my_n; ++i) {
+        const int s = int(i % D);
+        const uint64_t r = (gw + i * nw) * RS + lane;
+        mbar_wait(smem_u32(&bars[warp][s]), uint32_t((i / D) & 1));
+        if (lane < int(RS) && r < n) {
+            const uint32_t srow = smem_u32(wbase + s * stage_bytes + lane * rb);
+            const uint32_t miss = is_load[r];
+            if (X) bulk_store(X + r * rb, srow, rb, pol);  // with X every row was loaded
+            if (miss) bulk_store(region + uint64_t(alias[r]) * rb, srow, rb, pol);
+        }
+        bulk_commit();
+        const uint64_t j = i + A;
+        if (j < my_n) {
+            bulk_wait_read<D - A>();  // the stores that last read stage j % D have drained
+            issue(j, pa);
+            pa = pb;
+            pb = src_of(j + 2);
+        }
+    }
+    bulk_wait_all();
 }
 
 // ----------------------------------------------------------- sorted move ----
@@ -839,6 +924,7 @@ using namespace fdg;
 
 int64_t fdg::g_bm_eager = 0;
 int64_t fdg::g_bm_sorted_move = 1;
+int64_t fdg::g_bm_move_impl = 0;
 
 namespace {
 
@@ -1028,8 +1114,8 @@ int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
         return fail(FDG_NOT_LOADED, "bm_extract: no feature table / region bound (fdg_bm_bind_table)");
     const char* table = static_cast<const char*>(b->ctx->shard_bases[0]);
     const uint64_t chunks = n_host * (rb / 16);
-    const int blocks =
-        int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 511) / 512, uint64_t(b->ctx->sm_count) * 2)));
+    const int blocks = int(
+        std::max<uint64_t>(1, std::min<uint64_t>((chunks + 511) / 512, uint64_t(b->ctx->sm_count) * FDG_MOVE_CTAS)));
     const bool host = b->own_ctx ? b->host_src : b->ctx->host_table != nullptr;
     if (host && g_bm_sorted_move && d.N < 0xFFFFFFFEull && n_host > 0) {
         // misses in node-id order (address locality for the host side's translation)
@@ -1056,6 +1142,17 @@ int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
         FDG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, pin, pout, int64_t(n_host), 0, 32, st));
         k_move_sorted<<<blocks, 512, 0, st>>>(d, kout, pout, n_host, alias, table, b->region, rb,
                                               static_cast<char*>(out));
+    } else if (!host && g_bm_move_impl == 1 && rb <= 4096) {
+        FDG_TRACE("bm_move", st);
+        constexpr int D = 8, A = 6;
+        const uint32_t RS = std::max<uint32_t>(1, std::min<uint32_t>(
+            32, uint32_t(std::min<uint64_t>(4096 / rb, (160u << 10) / (uint64_t(kMoveTmaWarps) * D * rb)))));
+        const size_t smem = size_t(kMoveTmaWarps) * D * RS * rb;
+        static PerDeviceOnce attr;
+        if (attr.first())
+            FDG_CUDA(cudaFuncSetAttribute(k_move_tma<D, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 << 10));
+        k_move_tma<D, A><<<b->ctx->sm_count, kMoveTmaWarps * 32, smem, st>>>(
+            d, nodes, n_dev, n_host, alias, d.is_load[parity & 1], table, b->region, rb, RS, static_cast<char*>(out));
     } else {
         FDG_TRACE("bm_move", st);
         k_move<<<blocks, 512, 0, st>>>(d, nodes, n_dev, n_host, alias, d.is_load[parity & 1], table, b->region, rb,

@@ -474,7 +474,8 @@ int launch_hash_rb(const Ctx& c, cudaStream_t st, uint64_t groups, const uint64_
                     uint64_t n_host, const uint32_t* status, const TableRef& t, char* out, uint64_t* checksum) {
     const int ch = g_hash_chunk ? int(g_hash_chunk) : (c.row_bytes >= 256 ? 256 : 128);
     const int minb = ch == 128 ? HashRbShape<128>::MINB : HashRbShape<256>::MINB;
-    const int blocks = int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps, uint64_t(c.sm_count) * minb));
+    const int per_sm = g_hash_ctas_per_sm > 0 ? int(g_hash_ctas_per_sm) : minb;
+    const int blocks = int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps, uint64_t(c.sm_count) * per_sm));
     uint32_t* ctr = g_hash_dyn ? dyn_counter(c) : nullptr;
 #define FDG_HRB(R)                                                                                      \
     case R:                                                                                             \
@@ -740,6 +741,11 @@ int64_t g_rb_chunk = 256;      // row-group plain gather: 128- or 256-byte row c
 // never won an A/B (profiles/README.md, decisions).
 // Fused gather + checksum: row groups claimed from a per-launch counter (1) or a static stride (0).
 int64_t g_hash_dyn = 0;
+// Fused gather + checksum CTAs per SM (0: the kernel's min-blocks, 2). At 124 registers x 256
+// threads, two CTAs hold 97 % of an SM's register file, so nothing else (the samplers, the MT
+// prefetch) fits beside them. One per SM: Papers pipeline with checksum 201.3 vs 204.0 us per
+// batch (products and Friendster unchanged; alone 156 vs 152 us).
+int64_t g_hash_ctas_per_sm = 1;
 int64_t g_hash_chunk = 0;  // 0: 256-byte chunks for rows >= 256 B, else 128; or force 128 / 256
 int64_t g_checksum_impl = FDG_GATHER_LDG;
 

@@ -159,6 +159,7 @@ extern int64_t g_gather_pf64;         // 64-byte L2 fetch hint on table reads (0
 extern int g_gather_ctas_per_sm;      // chunk-striped gather: CTAs (512 threads) per SM
 extern int64_t g_rb_ctas_per_sm;      // row-group gather: CTAs (8 warps) per SM
 extern int64_t g_rb_chunk;            // row-group gather: 128- or 256-byte row chunks
+extern int64_t g_hash_ctas_per_sm;    // fused gather + checksum CTAs per SM (0 = min-blocks)
 extern int64_t g_hash_dyn;            // fused gather + checksum: dynamic row-group claims
 extern int64_t g_hash_chunk;          // k_gather_hash_rb staging chunk (0 = by row size)
 extern int64_t g_hash_dyn;            // fused gather + checksum: row groups claimed dynamically (1) or static (0)
@@ -167,6 +168,7 @@ int tc_write_hi(cudaStream_t st);       // 1: tcgen05 kind::tf32 GEMMs write A_h
 extern int64_t g_sage_gemm;           // train-stage GEMMs: 1 tensor cores (3xTF32), 0 CUDA cores
 extern int64_t g_bm_overlap;          // buffer-manager row move on its own stream (1) or after the metadata (0)
 extern int64_t g_bm_eager;            // buffer managers created in eager-invalidation (debug) mode
+extern int64_t g_bm_move_impl;        // buffer-manager row move: 0 LDG (k_move), 1 TMA bulk copies (k_move_tma)
 extern int64_t g_bm_sorted_move;      // host-resident table: move the misses in node-id order
 extern int64_t g_l2_persist_mb;       // L2 set-aside for the samplers' hash tables (0 off)
 extern int64_t g_hash_load_pct;       // batch hash sizing (load factor, %)

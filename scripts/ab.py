@@ -31,7 +31,7 @@ defaults = {"gather_impl": 4, "pipeline_gather_impl": 1, "gather_evict_first": 0
             "hash_clear": 1, "sampler_ctas_per_sm": 16, "gather_ctas_per_sm": 1,
             "extract_streams": 2, "hash_keep": 1,
             "checksum_impl": 1, "hash_chunk": 0, "gather_pf64": 2, "rb_ctas_per_sm": 2, "rb_chunk": 256, "sampler_sms": 0, "tma_cfg": 0,
-            "replay": 1, "mt_adaptive": 1, "hash_dyn": 0}
+            "replay": 1, "mt_adaptive": 1, "hash_dyn": 0, "hash_ctas_per_sm": 1, "bm_move_impl": 0}
 for spec in sys.argv[1:]:
     kv = dict(x.split("=") for x in spec.split(",") if x)
     S = int(kv.pop("S", 2))
@@ -54,6 +54,9 @@ for spec in sys.argv[1:]:
     for rep in range(3):
         fd.featdrive.check(L.fdg_pipeline_run(p, seeds.ptr, 0, rng.ctypes.data_as(C.c_void_p), K, None, None, C.byref(ms)))
         res.append(ms.value / K * 1e3)
+    out = _lib.PipelineConfig()
+    fd.featdrive.check(L.fdg_pipeline_get_config(p, C.byref(out)))
     L.fdg_pipeline_destroy(p)
     best = min(res[1:])
-    print(f"{spec:60s} {best:7.1f} us/batch  {1e6 / best:7.0f} batches/s", flush=True)
+    print(f"{spec:60s} {best:7.1f} us/batch  {1e6 / best:7.0f} batches/s  host enqueue "
+          f"{out.host_enqueue_ms / K * 1e3:6.1f} us/batch", flush=True)

@@ -46,3 +46,18 @@ def test_partition_matches_reference_order(golden, port):
     np.testing.assert_array_equal(order, golden["part_order"])
     with pytest.raises(fd.InvalidArgument):
         fd.partition_epoch(np.arange(3, dtype=np.uint64), 0, 1)
+
+
+def test_library_sets_hardware_queue_default():
+    """Loading libfdg.so sets CUDA_DEVICE_MAX_CONNECTIONS=32 (the runner's 19 streams would share
+    the default 8 hardware queues) unless the process already chose a value."""
+    code = ("import ctypes, sys; ctypes.CDLL(sys.argv[1]); libc = ctypes.CDLL(None); "
+            "libc.getenv.restype = ctypes.c_char_p; print(libc.getenv(b'CUDA_DEVICE_MAX_CONNECTIONS').decode())")
+    import os
+    import sys
+    env = {k: v for k, v in os.environ.items() if k != "CUDA_DEVICE_MAX_CONNECTIONS"}
+    out = subprocess.run([sys.executable, "-c", code, _lib.LIB_PATH], capture_output=True, text=True, env=env)
+    assert out.stdout.strip() == "32", out.stderr
+    env["CUDA_DEVICE_MAX_CONNECTIONS"] = "4"
+    out = subprocess.run([sys.executable, "-c", code, _lib.LIB_PATH], capture_output=True, text=True, env=env)
+    assert out.stdout.strip() == "4", out.stderr

@@ -265,10 +265,19 @@ def test_extractor_checksums_golden(fd, golden):
     assert sums == [int(x) for x in g["ex_checksum"]]
 
 
-@pytest.mark.parametrize("S,lag", [(2600, 1), (5200, 2), (20000, 3)])
-def test_buffer_manager_vs_port_random(fd, port, S, lag):
+@pytest.fixture(params=[0, 1], ids=["ldg_move", "tma_move"])
+def bm_move(request, fd):
+    """Both row-move engines of the buffer manager: LDG (k_move) and TMA bulk copies (k_move_tma)."""
+    old = fd.featdrive.get_option("bm_move_impl")
+    fd.set_option("bm_move_impl", request.param)
+    yield request.param
+    fd.set_option("bm_move_impl", old)
+
+
+@pytest.mark.parametrize("S,lag,dim", [(2600, 1, 32), (5200, 2, 100), (20000, 3, 128)])
+def test_buffer_manager_vs_port_random(fd, port, bm_move, S, lag, dim):
     n = 20000
-    t = fd.Topology.generate(n, 32, 8, 1)
+    t = fd.Topology.generate(n, dim, 8, 1)
     table = t.download_rows(0, n)
     rs = np.random.RandomState(S + lag)
     mb = 1300
@@ -280,11 +289,18 @@ def test_buffer_manager_vs_port_random(fd, port, S, lag):
         cold = rs.randint(0, n, size=rs.randint(1, 700))
         nodes = np.unique(np.concatenate([hot, cold])).astype(np.uint64)[:mb]
         rs.shuffle(nodes)
-        alias, x, cs = bm.extract(nodes, want_rows=True, checksum=True)
-        oa, _ = ob.extract(nodes)
-        np.testing.assert_array_equal(alias, oa)
-        np.testing.assert_array_equal(x, table[nodes.astype(np.int64)])
-        assert cs == port.checksum_rows(x)
+        if it % 4 == 3:  # the reference's form: alias list + slot fills only, no X
+            alias = bm.extract(nodes)
+            oa, _ = ob.extract(nodes)
+            np.testing.assert_array_equal(alias, oa)
+            np.testing.assert_array_equal(bm.region_slots(alias), table[nodes.astype(np.int64)])
+            x = table[nodes.astype(np.int64)]
+        else:
+            alias, x, cs = bm.extract(nodes, want_rows=True, checksum=True)
+            oa, _ = ob.extract(nodes)
+            np.testing.assert_array_equal(alias, oa)
+            np.testing.assert_array_equal(x, table[nodes.astype(np.int64)])
+            assert cs == port.checksum_rows(x)
         hist.append(nodes)
         while len(hist) > lag:
             old = hist.pop(0)
