@@ -688,6 +688,16 @@ int fdg_set_option(const char* key, int64_t v) {
         g_sage_gemm = v;
         return FDG_OK;
     }
+    if (k == "hash_early_pct") {
+        if (v != 0 && (v < 5 || v > 90)) return fail(FDG_INVALID_ARG, "hash_early_pct must be 0 or in [5, 90]");
+        g_hash_early_pct = v;
+        return FDG_OK;
+    }
+    if (k == "bm_move_grid" || k == "bm_meta_prio") {
+        if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, k + " must be 0 or 1");
+        (k == "bm_move_grid" ? g_bm_move_grid : g_bm_meta_prio) = v;
+        return FDG_OK;
+    }
     if (k == "bm_move_impl") {
         if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, "bm_move_impl must be 0 (LDG) or 1 (TMA)");
         g_bm_move_impl = v;
@@ -774,6 +784,9 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "hash_dyn") *v = g_hash_dyn;
     else if (k == "hash_ctas_per_sm") *v = g_hash_ctas_per_sm;
     else if (k == "bm_move_impl") *v = g_bm_move_impl;
+    else if (k == "bm_move_grid") *v = g_bm_move_grid;
+    else if (k == "hash_early_pct") *v = g_hash_early_pct;
+    else if (k == "bm_meta_prio") *v = g_bm_meta_prio;
     else if (k == "tc_write_hi") *v = tc_write_hi(nullptr);  // runs the once-per-device check
     else return fail(FDG_INVALID_ARG, "unknown option " + k);
     return FDG_OK;

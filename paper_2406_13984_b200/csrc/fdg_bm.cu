@@ -925,6 +925,7 @@ using namespace fdg;
 int64_t fdg::g_bm_eager = 0;
 int64_t fdg::g_bm_sorted_move = 1;
 int64_t fdg::g_bm_move_impl = 0;
+int64_t fdg::g_bm_move_grid = 0;
 
 namespace {
 
@@ -1114,8 +1115,12 @@ int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
         return fail(FDG_NOT_LOADED, "bm_extract: no feature table / region bound (fdg_bm_bind_table)");
     const char* table = static_cast<const char*>(b->ctx->shard_bases[0]);
     const uint64_t chunks = n_host * (rb / 16);
-    const int blocks = int(
-        std::max<uint64_t>(1, std::min<uint64_t>((chunks + 511) / 512, uint64_t(b->ctx->sm_count) * FDG_MOVE_CTAS)));
+    // g_bm_move_grid 0: persistent (FDG_MOVE_CTAS per SM, grid-stride); 1: one 4-row group per warp
+    // over the batch bound, so CTAs retire during the move and the block scheduler can put the
+    // next batch's metadata kernels and the samplers (higher-priority streams) in between.
+    const int blocks = g_bm_move_grid
+        ? int(std::max<uint64_t>(1, (n_host + 16 * kMoveRows - 1) / (16 * kMoveRows)))
+        : int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 511) / 512, uint64_t(b->ctx->sm_count) * FDG_MOVE_CTAS)));
     const bool host = b->own_ctx ? b->host_src : b->ctx->host_table != nullptr;
     if (host && g_bm_sorted_move && d.N < 0xFFFFFFFEull && n_host > 0) {
         // misses in node-id order (address locality for the host side's translation)

@@ -168,10 +168,13 @@ int tc_write_hi(cudaStream_t st);       // 1: tcgen05 kind::tf32 GEMMs write A_h
 extern int64_t g_sage_gemm;           // train-stage GEMMs: 1 tensor cores (3xTF32), 0 CUDA cores
 extern int64_t g_bm_overlap;          // buffer-manager row move on its own stream (1) or after the metadata (0)
 extern int64_t g_bm_eager;            // buffer managers created in eager-invalidation (debug) mode
+extern int64_t g_bm_move_grid;        // buffer-manager LDG row move: 0 persistent grid, 1 a CTA per 64 rows
+extern int64_t g_bm_meta_prio;        // pipeline: the buffer manager's metadata stream at high priority
 extern int64_t g_bm_move_impl;        // buffer-manager row move: 0 LDG (k_move), 1 TMA bulk copies (k_move_tma)
 extern int64_t g_bm_sorted_move;      // host-resident table: move the misses in node-id order
 extern int64_t g_l2_persist_mb;       // L2 set-aside for the samplers' hash tables (0 off)
 extern int64_t g_hash_load_pct;       // batch hash sizing (load factor, %)
+extern int64_t g_hash_early_pct;      // early batch-hash table load factor (0: hash_load_pct)
 extern int64_t g_sampler_ctas_per_sm; // sampler kernels: CTA cap per SM per launch
 extern int64_t g_sampler_sms;         // > 0: pipeline samplers on their own green-context SM partition
 extern int64_t g_extract_streams;     // 1 or 2 extraction streams in the pipeline runner

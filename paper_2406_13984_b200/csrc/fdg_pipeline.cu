@@ -91,6 +91,7 @@ struct fdg_pipeline {
 using namespace fdg;
 
 int64_t fdg::g_bm_overlap = 1;
+int64_t fdg::g_bm_meta_prio = 0;
 int64_t fdg::g_sampler_sms = 0;
 int64_t fdg::g_prefetch_upfront = 0;    // A/B: all samplers' first MT chunks before any sampling
 int64_t fdg::g_debug_zero_word = -1;     // (batch of the run << 24) | word position; -1 = off
@@ -306,7 +307,9 @@ int pipeline_build(fdg_pipeline* p, fdg_ctx* ctx, const uint32_t* fanouts, uint3
     sampler_capacity(p->samplers[0], &mn, &me);
     p->max_nodes = mn;
     p->cap = std::max<uint64_t>(std::max(mn, me), 1);
-    FDG_TRY(make_stream(&p->xstream, p->green_x, prio_lo));
+    // With the buffer manager the metadata chain (latency-bound, on the critical path of every
+    // batch) can run at the samplers' priority, ahead of the DRAM-bound row move (option).
+    FDG_TRY(make_stream(&p->xstream, p->green_x, (cfg->use_buffer_manager && g_bm_meta_prio && prio) ? prio_hi : prio_lo));
     // Plain gathers of consecutive batches alternate between two streams so the tail
     // of one overlaps the head of the next (the buffer-manager path is stateful and
     // stays on one stream).

@@ -407,7 +407,7 @@ __device__ __forceinline__ void intern_pass(const Work<IdT>& W, uint32_t q, uint
 #define FDG_INTERN_MINB 2
 #endif
 #ifndef FDG_INTERN_LAST_MINB
-#define FDG_INTERN_LAST_MINB 4
+#define FDG_INTERN_LAST_MINB 6  // 40 registers: sample-only 70.8 -> 66.5 us per Papers batch (4: 64 registers)
 #endif
 template <typename IdT, bool SEEDS, bool HAS_NEXT, bool PACK>
 __global__ void __launch_bounds__(kScanThreads, HAS_NEXT ? FDG_INTERN_MINB : FDG_INTERN_LAST_MINB) k_intern_s(const __grid_constant__ Group<IdT> G, uint32_t q,
@@ -1026,6 +1026,10 @@ __global__ void __launch_bounds__(256) k_degree_stats(const uint64_t* indptr, co
 
 int64_t g_l2_persist_mb = 0;
 int64_t g_hash_load_pct = 50;
+// Load factor (at the bound) of the early table alone (0: hash_load_pct). Every last-layer pick
+// looks its node up there first, and an absent key probes to the next empty entry: the warp
+// waits for the longest of its 30 lanes' chains (8.4 probes per warp at 0.5, ncu).
+int64_t g_hash_early_pct = 0;
 int64_t g_sampler_ctas_per_sm = 16;
 int64_t g_hash_clear = 1;
 int64_t g_extract_streams = 2;
@@ -1393,7 +1397,8 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
     s->hash_bytes = al(uint64_t(s->hsize) * (ib == 4 ? 8 : 12));
     // the early table holds the nodes interned before the last pass (seeds, layers < L-1)
     const uint64_t early = std::min<uint64_t>(N, nodes - std::min<uint64_t>(s->P_bound[n_layers - 1], N));
-    s->hsize_a = uint32_t((std::max<uint64_t>(early * 100 / uint64_t(g_hash_load_pct), 1024) + 31) & ~uint64_t(31));
+    const uint64_t early_pct = g_hash_early_pct > 0 ? uint64_t(g_hash_early_pct) : uint64_t(g_hash_load_pct);
+    s->hsize_a = uint32_t((std::max<uint64_t>(early * 100 / early_pct, 1024) + 31) & ~uint64_t(31));
     s->hash_bytes_a = al(uint64_t(s->hsize_a) * (ib == 4 ? 8 : 12));
     uint64_t fmaxF = 1;
     for (uint32_t l = 0; l < n_layers; ++l) fmaxF = std::max(fmaxF, s->F_bound[l]);
