@@ -688,6 +688,11 @@ int fdg_set_option(const char* key, int64_t v) {
         g_sage_gemm = v;
         return FDG_OK;
     }
+    if (k == "early_fused") {
+        if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, "early_fused must be 0 or 1");
+        g_early_fused = v;
+        return FDG_OK;
+    }
     if (k == "hash_early_pct") {
         if (v != 0 && (v < 5 || v > 90)) return fail(FDG_INVALID_ARG, "hash_early_pct must be 0 or in [5, 90]");
         g_hash_early_pct = v;
@@ -786,6 +791,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "bm_move_impl") *v = g_bm_move_impl;
     else if (k == "bm_move_grid") *v = g_bm_move_grid;
     else if (k == "hash_early_pct") *v = g_hash_early_pct;
+    else if (k == "early_fused") *v = g_early_fused;
     else if (k == "bm_meta_prio") *v = g_bm_meta_prio;
     else if (k == "tc_write_hi") *v = tc_write_hi(nullptr);  // runs the once-per-device check
     else return fail(FDG_INVALID_ARG, "unknown option " + k);

@@ -846,6 +846,264 @@ __global__ void __launch_bounds__(256, FDG_EXPAND_MINB) k_expand(const __grid_co
     }
 }
 
+// ----------------------------------------------------------------- k_early ----
+// The seeds and the first layer of a batch on one 1024-thread CTA, with the dedup hash in
+// shared memory: what k_seeds, k_intern_s (seeds), k_expand (layer 0) and k_intern_s (layer-0
+// picks) do in four launches and global hash round trips, for batches whose seeds and layer-0
+// picks fit the shared table (<= kEarlyMaxKeys keys; Papers / products: 1,000 + 10,000). The
+// interned nodes are then exported, with their final local ids, into the global early table
+// that the next layers probe. Same outputs, bit for bit: nodes[0, layer_nodes[2]), the layer-0
+// edges, the layer-1 frontier (fr[1]) and the batch record's layer counts.
+constexpr int kEarlyThreads = 1024;
+constexpr uint32_t kEarlyH = 16384;         // shared hash entries (128 KB), load factor <= 0.7
+constexpr uint32_t kEarlyMaxKeys = 11468;   // seeds + layer-0 picks
+constexpr uint32_t kEarlyMaxSeeds = kEarlyThreads;
+constexpr size_t kEarlySmem = size_t(kEarlyH) * 8 + size_t(kEarlyMaxKeys) * 4 + size_t(kEarlyMaxSeeds) * 20;
+
+__device__ __forceinline__ uint32_t sh_insert(unsigned long long* h, uint32_t key, uint32_t pos) {
+    const unsigned long long want = (uint64_t(key) << 32) | (kPend | pos);
+    uint32_t i = hslot(key, kEarlyH);
+    for (;;) {
+        unsigned long long cur = atomicCAS(h + i, ~0ull, want);
+        if (cur == ~0ull) return i;
+        if (uint32_t(cur >> 32) == key) {
+            while (uint32_t(cur) > uint32_t(want)) {
+                const unsigned long long prev = atomicCAS(h + i, cur, want);
+                if (prev == cur) break;
+                cur = prev;
+            }
+            return i;
+        }
+        i = (i + 1) & (kEarlyH - 1);
+    }
+}
+
+// CTA-wide exclusive scan of (c, p, d) over kEarlyThreads threads; *tot = the totals.
+__device__ __forceinline__ Tri early_scan(Tri v, Tri* s_warp, Tri* tot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const Tri in = warp_incl_scan(v, lane);
+    if (lane == 31) s_warp[warp] = in;
+    __syncthreads();
+    if (warp == 0) {
+        const Tri w = s_warp[lane];
+        const Tri wi = warp_incl_scan(w, lane);
+        s_warp[lane] = Tri{wi.c - w.c, wi.p - w.p, wi.d - w.d};
+        if (lane == 31) s_warp[32] = wi;
+    }
+    __syncthreads();
+    const Tri ex = s_warp[warp];
+    *tot = s_warp[32];
+    __syncthreads();  // s_warp is reused by the next scan
+    return Tri{ex.c + in.c - v.c, ex.p + in.p - v.p, ex.d + in.d - v.d};
+}
+
+__global__ void __launch_bounds__(kEarlyThreads, 1) k_early(const __grid_constant__ Group<uint32_t> G) {
+    extern __shared__ __align__(16) unsigned char early_smem[];
+    __shared__ Tri s_warp[33];
+    __shared__ uint32_t s_flag;
+    const Work<uint32_t>& W = G.w[blockIdx.y];
+    fdg_batch_counts* cnt = W.cnt;
+    unsigned long long* h = reinterpret_cast<unsigned long long*>(early_smem);
+    uint32_t* pslot = reinterpret_cast<uint32_t*>(h + kEarlyH);           // layer-0 pick -> hash slot
+    uint64_t* f_start = reinterpret_cast<uint64_t*>(pslot + kEarlyMaxKeys);  // layer-0 frontier
+    uint32_t* f_deg = reinterpret_cast<uint32_t*>(f_start + kEarlyMaxSeeds);
+    uint32_t* f_po = f_deg + kEarlyMaxSeeds;
+    uint32_t* f_do = f_po + kEarlyMaxSeeds;
+    const int tid = threadIdx.x;
+    // ---- the batch record (k_seeds) and the shared table
+    if (tid == 0) {
+        cnt->status = 0;
+        cnt->n_nodes = 0;
+        cnt->n_edges = 0;
+        cnt->rejections = 0;
+        cnt->bad_seed = 0;
+        cnt->checksum = 0;
+        cnt->bad_seed_pos = 0xFFFFFFFFu;
+        cnt->n_layers = W.n_layers;
+        cnt->words_used = 0;
+        cnt->replays = 0;
+        s_flag = 0;
+    }
+    for (int i = tid; i < FDG_MAX_LAYERS + 2; i += kEarlyThreads) {
+        cnt->layer_nodes[i] = 0;
+        if (i < FDG_MAX_LAYERS + 1) {
+            cnt->layer_edges[i] = 0;
+            cnt->layer_draws[i] = 0;
+            W.tile_ctr[i] = 0;
+        }
+    }
+    for (uint32_t i = tid; i < kEarlyH; i += kEarlyThreads) h[i] = ~0ull;
+    __syncthreads();
+    // ---- seeds: range check (sampling.hpp:89-93) and insert (key -> min position)
+    const uint32_t S = W.n_seeds;  // <= kEarlyThreads (checked on the host)
+    uint32_t key = 0, slot = 0;
+    if (uint32_t(tid) < S) {
+        const uint64_t sd = W.seeds[tid];
+        if (sd >= W.num_nodes) {
+            atomicMin(&cnt->bad_seed_pos, uint32_t(tid));
+            s_flag = FDG_OUT_OF_RANGE;
+        } else {
+            key = uint32_t(sd);
+            slot = sh_insert(h, key, uint32_t(tid));
+        }
+    }
+    __syncthreads();
+    if (s_flag) {
+        if (tid == 0) {
+            cnt->status = FDG_OUT_OF_RANGE;
+            cnt->bad_seed = W.seeds[cnt->bad_seed_pos];
+        }
+        return;
+    }
+    // ---- intern the seeds (first occurrences in seed order) and set up frontier 0
+    const uint32_t f0 = W.fan[0], f1 = W.fan[1];
+    bool first = uint32_t(tid) < S && uint32_t(h[slot]) == (kPend | uint32_t(tid));
+    uint64_t lo = 0, hi = 0;
+    if (first) {
+        lo = ld_rand64(W.indptr + key);
+        hi = ld_rand64(W.indptr + uint64_t(key) + 1);
+    }
+    uint32_t dg = first ? uint32_t(hi - lo) : 0u;
+    Tri tot0;
+    Tri ex = early_scan(Tri{first ? 1u : 0u, min(dg, f0), dg > f0 ? f0 : 0u}, s_warp, &tot0);
+    const uint32_t U0 = tot0.c, P0 = tot0.p, D0 = tot0.d;
+    if (first) {
+        W.nodes[ex.c] = uint64_t(key);
+        h[slot] = (uint64_t(key) << 32) | ex.c;
+        f_start[ex.c] = lo;
+        f_deg[ex.c] = dg;
+        f_po[ex.c] = ex.p;
+        f_do[ex.c] = ex.d;
+    }
+    if (D0 > W.words_a) {  // words beyond the prefetched estimate: the exact replay re-runs the batch
+        if (tid == 0) {
+            cnt->layer_nodes[1] = U0;
+            cnt->n_nodes = U0;
+            cnt->layer_edges[1] = P0;
+            cnt->layer_draws[1] = D0;
+            atomicCAS(&cnt->status, 0u, uint32_t(FDG_REJECTION));
+        }
+        return;
+    }
+    __syncthreads();
+    // ---- expand layer 0 (k_expand's warp layout: floor(32 / f0) nodes per warp, a lane per pick)
+    {
+        const uint32_t lane = tid & 31;
+        const uint32_t npw = 32 / f0;
+        const uint32_t g = lane / f0, k = lane - g * f0;
+        const bool in_group = g < npw;
+        const uint32_t gbase = in_group ? g * f0 : 0;
+        bool rejected = false;
+        for (uint32_t wt = uint32_t(tid) >> 5; wt * npw < U0; wt += kEarlyThreads / 32) {
+            const uint32_t i = wt * npw + g;
+            const bool live = in_group && i < U0;
+            uint64_t start = 0;
+            uint32_t deg = 0, po = 0, dro = 0;
+            if (live) {
+                start = f_start[i];
+                deg = f_deg[i];
+                po = f_po[i];
+                dro = f_do[i];
+            }
+            const bool floyd = deg > f0;
+            const uint32_t npick = floyd ? f0 : deg;
+            uint32_t picked = 0, alt = 0;
+            if (live && k < npick) {
+                if (floyd) {
+                    const uint64_t j = uint64_t(deg - f0) + k;
+                    const uint64_t r = j + 1;
+                    const uint64_t w = __ldg(W.words + dro + k);
+                    const uint64_t lw = w * r;
+                    if (lw < r && lw < (0 - r) % r) rejected = true;
+                    picked = ld_idx(W.indices + start + __umul64hi(w, r));
+                    alt = ld_idx(W.indices + start + j);
+                } else {
+                    picked = W.indices[start + k];
+                }
+            }
+            if (__any_sync(0xffffffffu, live && floyd)) {
+                for (uint32_t st = 1; st < f0; ++st) {
+                    const uint32_t c = __shfl_sync(0xffffffffu, picked, int(gbase + st));
+                    const uint32_t hits = __ballot_sync(0xffffffffu, in_group && k < st && picked == c);
+                    if (k == st && floyd && ((hits >> gbase) & ((1u << st) - 1u))) picked = alt;
+                }
+            }
+            if (live && k < npick) {
+                pslot[po + k] = sh_insert(h, picked, po + k);
+                W.edges[2 * (po + k) + 1] = i;  // dst: frontier node i is local id i
+            }
+        }
+        if (rejected) {
+            atomicAdd(&cnt->rejections, 1u);
+            atomicCAS(&cnt->status, 0u, uint32_t(FDG_REJECTION));
+            s_flag = 1;
+        }
+    }
+    __syncthreads();
+    if (s_flag) {  // a Lemire rejection: the exact replay re-runs the batch
+        if (tid == 0) {
+            cnt->layer_nodes[1] = U0;
+            cnt->n_nodes = U0;
+            cnt->layer_edges[1] = P0;
+            cnt->layer_draws[1] = D0;
+        }
+        return;
+    }
+    // ---- intern the layer-0 picks in pick order; frontier 1 -> fr[1]
+    Tri run{0, 0, 0};
+    const FrontierBuf fr = W.fr[1];
+    for (uint32_t b = 0; b < P0; b += kEarlyThreads) {
+        const uint32_t pp = b + uint32_t(tid);
+        uint32_t ps = 0;
+        unsigned long long v = 0;
+        bool fst = false;
+        if (pp < P0) {
+            ps = pslot[pp];
+            v = h[ps];
+            fst = uint32_t(v) == (kPend | pp);
+        }
+        uint64_t l1 = 0, h1 = 0;
+        if (fst) {
+            l1 = ld_rand64(W.indptr + (v >> 32));
+            h1 = ld_rand64(W.indptr + (v >> 32) + 1);
+        }
+        const uint32_t d1 = fst ? uint32_t(h1 - l1) : 0u;
+        Tri t;
+        const Tri e = early_scan(Tri{fst ? 1u : 0u, min(d1, f1), d1 > f1 ? f1 : 0u}, s_warp, &t);
+        uint32_t local = 0;
+        if (fst) {
+            const uint32_t r = run.c + e.c;
+            local = U0 + r;
+            W.nodes[local] = v >> 32;
+            h[ps] = (v & 0xFFFFFFFF00000000ull) | local;
+            fr.start[r] = l1;
+            fr.deg[r] = d1;
+            fr.pick_off[r] = run.p + e.p;
+            fr.draw_off[r] = run.d + e.d;
+        }
+        run = run + t;
+        __syncthreads();  // this round's first occurrences are final
+        if (pp < P0) W.edges[2 * pp] = fst ? local : uint32_t(h[ps]);  // LocalEdge.src (sampling.hpp:124)
+    }
+    __syncthreads();
+    // ---- export the interned nodes (final ids) to the global early table
+    for (uint32_t i = tid; i < kEarlyH; i += kEarlyThreads) {
+        const unsigned long long v = h[i];
+        if (v == ~0ull) continue;
+        uint32_t j = hslot(uint32_t(v >> 32), W.tab.size);
+        while (atomicCAS(W.tab.e + j, ~0ull, v) != ~0ull) j = j + 1 == W.tab.size ? 0 : j + 1;
+    }
+    if (tid == 0) {
+        cnt->layer_nodes[1] = U0;
+        cnt->layer_edges[1] = P0;
+        cnt->layer_draws[1] = D0;
+        cnt->layer_nodes[2] = U0 + run.c;
+        cnt->n_nodes = U0 + run.c;
+        cnt->layer_edges[2] = P0 + run.p;
+        cnt->layer_draws[2] = D0 + run.d;
+    }
+}
+
 // ---------------------------------------------------------------- k_replay ----
 // In-stream exact re-run of a batch whose fast path saw a Lemire rejection (an extra
 // word consumed by some draw, p ~ 2^-57 per draw, shifting every later word offset;
@@ -1030,6 +1288,11 @@ int64_t g_hash_load_pct = 50;
 // looks its node up there first, and an absent key probes to the next empty entry: the warp
 // waits for the longest of its 30 lanes' chains (8.4 probes per warp at 0.5, ncu).
 int64_t g_hash_early_pct = 0;
+// Seeds + layer 0 fused into one shared-memory CTA per batch (k_early) when they fit. Measured
+// neutral on the pipelined step (Papers 184.7 / 186.1 vs 186.7 / 184.5 us per batch, sample-only
+// 68.0 / 71.6 vs 69.9 / 72.0; products 181.9 vs 176.8): the early layers are latency, not
+// throughput, and 8 samplers in flight hide it. Off by default; parity-tested both ways.
+int64_t g_early_fused = 0;
 int64_t g_sampler_ctas_per_sm = 16;
 int64_t g_hash_clear = 1;
 int64_t g_extract_streams = 2;
@@ -1087,6 +1350,7 @@ struct Sampler {
     uint32_t hsize = 0;    // last-layer table (sized for every node of a batch: the replay's one table)
     uint32_t hsize_a = 0;  // table of the passes before the last
     bool small_f = true;
+    bool early_fused = false;  // seeds + layer 0 in one shared-memory CTA per batch (k_early)
     void* arena = nullptr;
     void* hash_all = nullptr;  // the lanes' last-layer tables, contiguous (one fill per group)
     void* hash_all_a = nullptr;  // the lanes' early tables, contiguous, right before hash_all
@@ -1239,18 +1503,33 @@ int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
         FDG_TRACE("memset", st);
         FDG_CUDA(clear_hash(s.hash_all_a, s.hash_bytes_a * n, s.ctx->sm_count, st));
     }
-    {
-        FDG_TRACE("seeds", st);
-        k_seeds<IdT><<<dim3(1, n), 256, 0, st>>>(G);
+    uint32_t l0 = 0;  // first layer expanded by the loop below
+    if constexpr (sizeof(IdT) == 4) {
+        if (s.early_fused) {  // seeds + layer 0 on one CTA per batch, shared-memory hash
+            FDG_TRACE("early", st);
+            static PerDeviceOnce attr;
+            if (attr.first())
+                FDG_CUDA(cudaFuncSetAttribute(k_early, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEarlySmem)));
+            k_early<<<dim3(1, n), kEarlyThreads, kEarlySmem, st>>>(G);
+            next_epoch(s, n);
+            next_epoch(s, n);
+            l0 = 1;
+        }
     }
-    {
-        FDG_TRACE("intern0", st);
-        launch_intern<IdT>(s, st, G, n, 0, max_seeds, next_epoch(s, n));
+    if (l0 == 0) {
+        {
+            FDG_TRACE("seeds", st);
+            k_seeds<IdT><<<dim3(1, n), 256, 0, st>>>(G);
+        }
+        {
+            FDG_TRACE("intern0", st);
+            launch_intern<IdT>(s, st, G, n, 0, max_seeds, next_epoch(s, n));
+        }
     }
     static const char* names[2][FDG_MAX_LAYERS] = {
         {"expand0", "expand1", "expand2", "expand3", "expand4", "expand5", "expand6", "expand7"},
         {"intern1", "intern2", "intern3", "intern4", "intern5", "intern6", "intern7", "intern8"}};
-    for (uint32_t l = 0; l < s.n_layers; ++l) {
+    for (uint32_t l = l0; l < s.n_layers; ++l) {
         if (l + 1 == s.n_layers) {  // the last layer draws from the prefetch's second piece
             for (uint32_t i = 0; i < n; ++i)
                 if (a[i].ready) FDG_CUDA(cudaStreamWaitEvent(st, a[i].ready, 0));
@@ -1390,6 +1669,8 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
         return fail(FDG_INVALID_ARG, "sampler: batch bound exceeds 2^31 picks");
     }
     s->small_f = fmax <= uint32_t(kMaxF);
+    s->early_fused = g_early_fused && ctx->idx_bytes == 4 && n_layers >= 2 && fanouts[0] <= uint32_t(kMaxF) &&
+                     max_seeds <= kEarlyMaxSeeds && uint64_t(max_seeds) + s->P_bound[0] <= kEarlyMaxKeys;
     // exact sizing (load factor g_hash_load_pct at the batch's node bound); any size works (hslot)
     s->hsize = uint32_t((std::max<uint64_t>(s->max_nodes * 100 / uint64_t(g_hash_load_pct), 1024) + 31) & ~uint64_t(31));
     const uint32_t ib = ctx->idx_bytes;

@@ -88,7 +88,18 @@ def test_mt_stream_golden(fd, golden, port):
 
 
 # ----------------------------------------------------------------- sampling --
-def test_sample_khop_golden(fd, golden):
+@pytest.fixture(params=[0, 1], ids=["chain", "early_fused"])
+def early(request, fd):
+    """Both sampler front ends: the per-pass kernel chain, and seeds + layer 0 fused into one
+    shared-memory CTA per batch (k_early; fanout <= 16, <= 1024 seeds, >= 2 layers). The option is
+    read when a sampler is created, so each test builds its own topology (fresh sampler pool)."""
+    old = fd.featdrive.get_option("early_fused")
+    fd.set_option("early_fused", request.param)
+    yield request.param
+    fd.set_option("early_fused", old)
+
+
+def test_sample_khop_golden(fd, golden, early):
     t = fd.Topology.generate(5000, 16, 12, 7)
     for seeds, fan, rs, nodes, edges in _sample_cases(golden):
         b = fd.sample_khop(t, seeds, list(fan), rs)
@@ -100,7 +111,7 @@ def test_sample_khop_golden(fd, golden):
     np.testing.assert_array_equal(b.edges, golden["sparse_edges"])
 
 
-def test_sample_khop_errors(fd):
+def test_sample_khop_errors(fd, early):
     t = fd.Topology.generate(5000, 16, 12, 7)
     with pytest.raises(fd.OutOfRange, match="5000"):  # first out-of-range seed in order
         fd.sample_khop(t, np.array([3, 5000, 7, 6000], np.uint64), [2], 1)
@@ -114,7 +125,7 @@ def test_sample_khop_errors(fd):
 
 
 @pytest.mark.parametrize("fan", [[10, 10, 10], [15, 10, 5], [1], [40, 3], [25, 25]])
-def test_sample_khop_vs_port(fd, port, fan):
+def test_sample_khop_vs_port(fd, port, fan, early):
     t = fd.Topology.generate(200_000, 8, 16, 3, features=False)
     ip, ix = t.download_topology()
     rs = np.random.RandomState(len(fan) * 100 + fan[0])
@@ -129,7 +140,7 @@ def test_sample_khop_vs_port(fd, port, fan):
         np.testing.assert_array_equal(b.layer_edges, o["layer_edges"])
 
 
-def test_sample_high_duplicate_rate(fd, port):
+def test_sample_high_duplicate_rate(fd, port, early):
     """A tiny dense graph: almost every pick is a duplicate (dedup stress)."""
     t = fd.Topology.generate(300, 4, 64, 5, features=False)
     ip, ix = t.download_topology()
@@ -431,7 +442,7 @@ def test_pipeline_prefetch_ring_odd_groups(fd, port, group):
 
 @pytest.mark.parametrize("bm", [False, True])
 @pytest.mark.parametrize("hook", ["zero_word", "flag"])
-def test_pipeline_rejection_replayed_exactly(fd, port, bm, hook):
+def test_pipeline_rejection_replayed_exactly(fd, port, bm, hook, early):
     """A Lemire rejection inside the pipelined runner (sampling.hpp:113: the reference always
     produces the batch) is re-run exactly in-stream by k_replay before anything consumes the
     batch. Hooks: 'zero_word' zeroes word 3 of batch 5's prefetched MT stream (a genuine
@@ -495,7 +506,7 @@ def test_pipeline_rejection_replayed_exactly(fd, port, bm, hook):
 
 
 @pytest.mark.parametrize("adaptive", [0, 1, 2])
-def test_pipeline_mt_prefetch_estimate(fd, port, adaptive):
+def test_pipeline_mt_prefetch_estimate(fd, port, adaptive, early):
     """The MT prefetch holds the estimated draws (two pieces) instead of the draw bound:
     mode 1 (default) must not change any result, mode 2 prefetches an eighth of the estimate
     so that every batch runs out of words and is re-run exactly in-stream, extending its
