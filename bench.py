@@ -658,7 +658,7 @@ def _host_tier_link(fd, L, timed, rb, ms_per_step):
     return out
 
 
-def _per_call(cfg, batches=50):
+def _per_call(cfg, batches=200):
     """The reference's per-call SET loop (tests/cpp/set_loop.cpp: sample_khop -> Extractor::
     extract_batch -> trainer_step -> release_batch, one batch at a time, host vectors in and
     out) through the C++ drop-in (include/featdrive_gpu.hpp), at this config's shape, in a
