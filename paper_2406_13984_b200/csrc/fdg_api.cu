@@ -19,6 +19,7 @@
 namespace fdg {
 
 int64_t g_host_tier_thp = 0;
+int64_t g_force_idx64 = 0;
 static thread_local std::string g_error;
 static thread_local int g_errno = 0;
 
@@ -280,7 +281,7 @@ int fdg_ctx_load_topology(fdg_ctx* c, const uint64_t* indptr, uint64_t n, const 
     if (c->indices) cudaFree(c->indices);
     c->indptr = nullptr;
     c->indices = nullptr;
-    c->idx_bytes = n <= 0xFFFFFFFFull ? 4 : 8;
+    c->idx_bytes = (n <= 0xFFFFFFFFull && !g_force_idx64) ? 4 : 8;
     FDG_CUDA(cudaMalloc(&c->indptr, (n + 1) * 8));
     FDG_CUDA(cudaMemcpy(c->indptr, indptr, (n + 1) * 8, cudaMemcpyHostToDevice));
     FDG_CUDA(cudaMalloc(&c->indices, std::max<uint64_t>(e, 1) * c->idx_bytes));
@@ -688,6 +689,11 @@ int fdg_set_option(const char* key, int64_t v) {
         g_sage_gemm = v;
         return FDG_OK;
     }
+    if (k == "force_idx64") {  // test hook: topologies loaded / generated afterwards keep u64 indices
+        if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, "force_idx64 must be 0 or 1");
+        g_force_idx64 = v;
+        return FDG_OK;
+    }
     if (k == "early_fused") {
         if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, "early_fused must be 0 or 1");
         g_early_fused = v;
@@ -792,6 +798,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "bm_move_grid") *v = g_bm_move_grid;
     else if (k == "hash_early_pct") *v = g_hash_early_pct;
     else if (k == "early_fused") *v = g_early_fused;
+    else if (k == "force_idx64") *v = g_force_idx64;
     else if (k == "bm_meta_prio") *v = g_bm_meta_prio;
     else if (k == "tc_write_hi") *v = tc_write_hi(nullptr);  // runs the once-per-device check
     else return fail(FDG_INVALID_ARG, "unknown option " + k);

@@ -167,7 +167,7 @@ int generate_topology(Ctx& c, uint64_t seed, uint64_t n, uint32_t avg) {
     FDG_CUDA(cudaStreamSynchronize(st));
     c.num_nodes = n;
     c.num_edges = e;
-    c.idx_bytes = n <= 0xFFFFFFFFull ? 4 : 8;
+    c.idx_bytes = (n <= 0xFFFFFFFFull && !g_force_idx64) ? 4 : 8;
     FDG_CUDA(cudaMalloc(&c.indices, std::max<uint64_t>(e, 1) * c.idx_bytes));
     int gblocks = int(std::min<uint64_t>((n + kGenWarps - 1) / kGenWarps, uint64_t(c.sm_count) * 64));
     if (c.idx_bytes == 4)

@@ -140,6 +140,54 @@ def test_sample_khop_vs_port(fd, port, fan, early):
         np.testing.assert_array_equal(b.layer_edges, o["layer_edges"])
 
 
+@pytest.fixture
+def idx64(fd):
+    """u64 CSR indices for a small graph: the kernels, hash tables (separate key / value arrays)
+    and loads that N >= 2^32 graphs use, run here against the restatement."""
+    fd.set_option("force_idx64", 1)
+    yield
+    fd.set_option("force_idx64", 0)
+
+
+@pytest.mark.parametrize("fan", [[10, 10, 10], [15, 10, 5], [25, 3]])
+def test_sample_khop_u64_indices_vs_port(fd, port, idx64, fan):
+    t = fd.Topology.generate(100_000, 16, 16, 9)
+    assert t.info().idx_bytes == 8
+    ip, ix = t.download_topology()
+    table = t.download_rows(0, t.num_nodes)
+    rs = np.random.RandomState(sum(fan))
+    for k in range(3):
+        seeds = rs.randint(0, 100_000, size=rs.choice([5, 300, 1000])).astype(np.uint64)
+        r = int(rs.randint(0, 2**63))
+        b = fd.sample_khop(t, seeds, fan, r)
+        o = port.sample_khop(ip, ix, seeds, fan, r)
+        np.testing.assert_array_equal(b.nodes, o["nodes"])
+        np.testing.assert_array_equal(b.edges, o["edges"])
+        x, cs = fd.gather(t, b.nodes, checksum=True)
+        np.testing.assert_array_equal(x, table[b.nodes.astype(np.int64)])
+        assert cs == port.checksum_rows(x)
+
+
+def test_pipeline_u64_indices_vs_port(fd, port, idx64):
+    """The pipelined runner (MT prefetch, in-stream replay hook) on u64 indices."""
+    n, fan, B = 200_000, [10, 10, 10], 500
+    t = fd.Topology.generate(n, 32, 12, 4)
+    assert t.info().idx_bytes == 8
+    ip, ix = t.download_topology()
+    table = t.download_rows(0, n)
+    order = np.concatenate(fd.partition_epoch(np.arange(20 * B, dtype=np.uint64), B, port.hash_combine(0, 0)))
+    rng = np.array([fd.batch_seed(0, 0, b) for b in range(20)], np.uint64)
+    pipe = fd.Pipeline(t, fan, B, checksum=True, samplers=2)
+    recs = pipe.run_batches(order[:20 * B], rng)
+    pipe.close()
+    assert np.all(recs["status"] == 0)
+    for b in range(20):
+        want = port.sample_khop(ip, ix, order[b * B:(b + 1) * B], fan, int(rng[b]))
+        assert int(recs["n_nodes"][b]) == len(want["nodes"])
+        _, cs = port.gather(table, want["nodes"])
+        assert int(recs["checksum"][b]) == cs, f"batch {b}"
+
+
 def test_sample_high_duplicate_rate(fd, port, early):
     """A tiny dense graph: almost every pick is a duplicate (dedup stress)."""
     t = fd.Topology.generate(300, 4, 64, 5, features=False)
