@@ -389,6 +389,9 @@ def run_ours(args):
     dist = Dist()
     dev = fdist.local_device(dist.local)
     L = fd.featdrive.lib()
+    for kv in args.option:
+        k, v = kv.split("=", 1)
+        fd.set_option(k, int(v))
     fd.featdrive.check(L.fdg_set_device(dev))
     cfg = args.config
     n, dim, avg, fan, B, t_ids, dtype, frac = CONFIGS[cfg]
@@ -901,6 +904,8 @@ def main():
                     help="--impl reference: also time PipelineSession::run_sync_reference (BASELINE.md 2 iii)")
     ap.add_argument("--sync-batches", type=int, default=4)
     ap.add_argument("--cpu-batches", type=int, default=0)
+    ap.add_argument("--option", action="append", default=[], metavar="KEY=VALUE",
+                    help="fdg_set_option before the run (repeatable), e.g. host_tier_thp=1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.shard:
