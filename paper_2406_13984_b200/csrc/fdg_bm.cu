@@ -279,27 +279,34 @@ __global__ void __launch_bounds__(kT) k_acquire(BmDev B, const uint64_t* nodes, 
 // ------------------------------------------------------------- k_select ----
 // Persistent CTAs claim ring tiles from `head` in order and rank live entries;
 // the first L live slots are the reference's L successive pop_lru() results.
-__global__ void __launch_bounds__(kT) k_select(BmDev B, uint32_t epoch) {
+// BIND: the thread that ranks a popped slot also binds it (what k_bind does for miss r):
+// the liveness check already brings the slot's record in, so the eviction check and the
+// rebind cost no second random read and no extra launch; k_bind_finish moves head.
+template <bool BIND>
+__global__ void __launch_bounds__(kT) k_select(BmDev B, uint32_t epoch, const uint64_t* nodes, int64_t* alias) {
     __shared__ uint32_t s_warp[kT / 32], s_misc[2], s_tile;
+    __shared__ unsigned long long s_ev;
     BmState* S = B.st;
     if (S->status) return;
     const uint32_t L = S->n_load;
     if (L == 0) return;
     const uint64_t head = S->head, tail = S->tail;
     const int32_t* ring = B.ring[S->ring_sel];
+    if (BIND && threadIdx.x == 0) s_ev = 0;
     for (;;) {
         if (threadIdx.x == 0) s_tile = *(volatile uint32_t*)&S->done ? 0xFFFFFFFFu : atomicAdd(&S->tile_ctr[1], 1u);
         __syncthreads();
         const uint32_t tile = s_tile;
         __syncthreads();
-        if (tile == 0xFFFFFFFFu) return;
+        if (tile == 0xFFFFFFFFu) break;
         const uint64_t p0 = head + uint64_t(tile) * kTileN;
         // Past the ring end: nothing to rank (the tile holding tail-1 -- or tile 0 of
         // an empty ring -- reports a short standby list). No look-back slot is used,
         // so tile ids stay within the tiles array.
-        if (p0 >= tail && tile > 0) return;
+        if (p0 >= tail && tile > 0) break;
         uint32_t live_mask = 0, mine = 0;
         int32_t slots[kI];
+        uint64_t nr[BIND ? kI : 1];
 #pragma unroll
         for (int k = 0; k < kI; ++k) {
             uint64_t p = p0 + threadIdx.x * kI + k;
@@ -309,9 +316,19 @@ __global__ void __launch_bounds__(kT) k_select(BmDev B, uint32_t epoch) {
             }
         }
 #pragma unroll
-        for (int k = 0; k < kI; ++k) {  // list membership: one random 8-byte load per entry, all in flight
+        for (int k = 0; k < kI; ++k) {  // list membership: one random record load per entry, all in flight
             const uint64_t p = p0 + threadIdx.x * kI + k;
-            if (slots[k] >= 0 && ld_pos(B.slot + slots[k]) == p) {
+            bool live = false;
+            if (slots[k] >= 0) {
+                if constexpr (BIND) {
+                    const ulonglong2 m = *reinterpret_cast<const ulonglong2*>(B.slot + slots[k]);
+                    nr[k] = m.x;
+                    live = m.y == p;
+                } else {
+                    live = ld_pos(B.slot + slots[k]) == p;
+                }
+            }
+            if (live) {
                 live_mask |= 1u << k;
                 ++mine;
             } else {
@@ -319,19 +336,50 @@ __global__ void __launch_bounds__(kT) k_select(BmDev B, uint32_t epoch) {
             }
         }
         uint32_t r = block_rank(B.tiles, tile, mine, epoch, s_warp, s_misc);
+        uint32_t ev = 0;
 #pragma unroll
         for (int k = 0; k < kI; ++k)
             if (live_mask & (1u << k)) {
-                if (r < L) B.sel[r] = slots[k];
+                if (r < L) {
+                    if constexpr (BIND) {  // k_bind for miss r (buffer_manager.hpp:281-310)
+                        const int32_t slot = slots[k];
+                        const uint32_t i = B.load_pos[r];
+                        const uint64_t node = nodes[i];
+                        const uint64_t prev = m_node(nr[k]);
+                        if (prev != kFree) {  // evict the previous owner: rebinding the slot invalidates its entry
+                            if (m_ref(nr[k]) != 0) atomicExch(&S->status, uint32_t(FDG_INVARIANT));
+                            if (B.eager) B.map[prev] = Entry{-1, 0u};
+                            ++ev;
+                        }
+                        B.map[node] = Entry{slot, kValid};  // bind + publish
+                        B.slot[slot] = SlotMeta{node | kRef1, kUnlisted};
+                        alias[i] = slot;
+                    } else {
+                        B.sel[r] = slots[k];
+                    }
+                }
                 if (r == L - 1) {
                     S->new_head = p0 + threadIdx.x * kI + k + 1;
                     atomicExch(&S->done, 1u);
                 }
                 ++r;
             }
+        if (BIND && ev) atomicAdd(&s_ev, (unsigned long long)ev);
         if (threadIdx.x == 0 && s_misc[1] < L && p0 + kTileN >= tail) atomicExch(&S->status, uint32_t(FDG_CAPACITY));
         __syncthreads();
     }
+    if (BIND) {
+        __syncthreads();
+        if (threadIdx.x == 0 && s_ev) atomicAdd((unsigned long long*)&S->evictions, s_ev);
+    }
+}
+
+// After the fused select + bind: the L popped slots left the standby list.
+__global__ void k_bind_finish(BmDev B) {
+    BmState* S = B.st;
+    if (S->status) return;
+    S->live -= S->n_load;
+    S->head = S->new_head;
 }
 
 // --------------------------------------------------------------- k_bind ----
@@ -926,6 +974,7 @@ int64_t fdg::g_bm_eager = 0;
 int64_t fdg::g_bm_sorted_move = 1;
 int64_t fdg::g_bm_move_impl = 0;
 int64_t fdg::g_bm_move_grid = 0;
+int64_t fdg::g_bm_fuse_bind = 1;  // select + bind fused: 543 -> 527.5 us per Papers batch (config 3)
 
 namespace {
 
@@ -1092,13 +1141,19 @@ int bm_extract_meta(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
         k_acquire<<<n_tiles_for(bound), kT, 0, st>>>(d, nodes, n_dev, n_host, alias, d.is_load[parity & 1],
                                                     b->epoch++);
     }
-    {
+    if (g_bm_fuse_bind) {  // select + bind in one pass over the popped slots' records
         FDG_TRACE("bm_select", st);
-        k_select<<<bm_persistent_grid(b), kT, 0, st>>>(d, b->epoch++);
-    }
-    {
-        FDG_TRACE("bm_bind", st);
-        k_bind<<<std::max<uint32_t>(1, uint32_t((bound + 255) / 256)), 256, 0, st>>>(d, nodes, alias);
+        k_select<true><<<bm_persistent_grid(b), kT, 0, st>>>(d, b->epoch++, nodes, alias);
+        k_bind_finish<<<1, 1, 0, st>>>(d);
+    } else {
+        {
+            FDG_TRACE("bm_select", st);
+            k_select<false><<<bm_persistent_grid(b), kT, 0, st>>>(d, b->epoch++, nullptr, nullptr);
+        }
+        {
+            FDG_TRACE("bm_bind", st);
+            k_bind<<<std::max<uint32_t>(1, uint32_t((bound + 255) / 256)), 256, 0, st>>>(d, nodes, alias);
+        }
     }
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;
@@ -1364,7 +1419,7 @@ int fdg_bm_pop_standby(fdg_bm* b, void* stv, uint32_t count, int64_t* slots_dev)
     if (count > b->max_batch) return fail(FDG_INVALID_ARG, "bm_pop_standby: more slots than max_batch_nodes");
     const BmDev& d = b->d;
     k_set_nload<<<1, 1, 0, st>>>(d.st, count);
-    k_select<<<bm_persistent_grid(b), kT, 0, st>>>(d, b->epoch++);
+    k_select<false><<<bm_persistent_grid(b), kT, 0, st>>>(d, b->epoch++, nullptr, nullptr);
     k_pop<<<(count + 255) / 256, 256, 0, st>>>(d, slots_dev);
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;

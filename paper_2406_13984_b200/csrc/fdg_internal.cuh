@@ -168,6 +168,7 @@ int tc_write_hi(cudaStream_t st);       // 1: tcgen05 kind::tf32 GEMMs write A_h
 extern int64_t g_sage_gemm;           // train-stage GEMMs: 1 tensor cores (3xTF32), 0 CUDA cores
 extern int64_t g_bm_overlap;          // buffer-manager row move on its own stream (1) or after the metadata (0)
 extern int64_t g_bm_eager;            // buffer managers created in eager-invalidation (debug) mode
+extern int64_t g_bm_fuse_bind;        // buffer manager: select and bind in one kernel
 extern int64_t g_bm_move_grid;        // buffer-manager LDG row move: 0 persistent grid, 1 a CTA per 64 rows
 extern int64_t g_bm_meta_prio;        // pipeline: the buffer manager's metadata stream at high priority
 extern int64_t g_bm_move_impl;        // buffer-manager row move: 0 LDG (k_move), 1 TMA bulk copies (k_move_tma)

@@ -333,8 +333,17 @@ def bm_move(request, fd):
     fd.set_option("bm_move_impl", old)
 
 
+@pytest.fixture(params=[0, 1], ids=["select_then_bind", "fused_bind"])
+def bm_bind(request, fd):
+    """Pops and binds: k_select then k_bind, or bound by the thread that ranks the popped slot."""
+    old = fd.featdrive.get_option("bm_fuse_bind")
+    fd.set_option("bm_fuse_bind", request.param)
+    yield request.param
+    fd.set_option("bm_fuse_bind", old)
+
+
 @pytest.mark.parametrize("S,lag,dim", [(2600, 1, 32), (5200, 2, 100), (20000, 3, 128)])
-def test_buffer_manager_vs_port_random(fd, port, bm_move, S, lag, dim):
+def test_buffer_manager_vs_port_random(fd, port, bm_move, bm_bind, S, lag, dim):
     n = 20000
     t = fd.Topology.generate(n, dim, 8, 1)
     table = t.download_rows(0, n)
