@@ -760,13 +760,15 @@ def _union_ms(starts, ends):
 
 
 def _launch_count(K, layers, bm, samplers, prefetch=16):
-    # per batch: k_fill_ones (hash clear), k_seeds, k_intern_s x (layers + 1), k_expand x layers,
-    # then the gather (k_gather16_dyn) -- or, with the buffer manager, 5 extract kernels
-    # (reset, acquire, select, bind, move) + k_status_to + 4 release kernels (reset, release,
-    # compact, finish). Plus one k_mt_stream launch per prefetch chunk of each sampler.
-    per_batch = 2 + (layers + 1) + layers + (1 if not bm else 10)
+    # per batch: 2 k_fill_ones (early and last-layer hash clears), k_seeds, k_intern_s x (layers + 1),
+    # k_expand x layers, k_replay (a no-op unless the batch saw a Lemire rejection), then the
+    # gather (k_gather16_dyn) -- or, with the buffer manager, 5 extract kernels (reset, acquire,
+    # select + bind, bind_finish, move) + k_status_to + 4 release kernels (reset, release,
+    # compact, finish). Plus two k_mt_stream launches (the stream's two pieces) per prefetch
+    # request of each sampler: one chunk of `prefetch` streams up front, then one stream per batch.
+    per_batch = 2 + 1 + (layers + 1) + layers + 1 + (1 if not bm else 10)
     per_sampler = -(-K // samplers)
-    return K * per_batch + samplers * (-(-per_sampler // prefetch))
+    return K * per_batch + samplers * 2 * (1 + max(per_sampler - prefetch, 0))
 
 
 def _gather_alone(fd, L, topo, fan, seeds_for, rng_of, ids, peak_gbs, reps=10):
