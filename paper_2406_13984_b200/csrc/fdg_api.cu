@@ -704,6 +704,11 @@ int fdg_set_option(const char* key, int64_t v) {
         g_hash_early_pct = v;
         return FDG_OK;
     }
+    if (k == "bm_move_hash") {
+        if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, "bm_move_hash must be 0 or 1");
+        g_bm_move_hash = v;
+        return FDG_OK;
+    }
     if (k == "bm_fuse_bind") {
         if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, "bm_fuse_bind must be 0 or 1");
         g_bm_fuse_bind = v;
@@ -802,6 +807,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "bm_move_impl") *v = g_bm_move_impl;
     else if (k == "bm_move_grid") *v = g_bm_move_grid;
     else if (k == "bm_fuse_bind") *v = g_bm_fuse_bind;
+    else if (k == "bm_move_hash") *v = g_bm_move_hash;
     else if (k == "hash_early_pct") *v = g_hash_early_pct;
     else if (k == "early_fused") *v = g_early_fused;
     else if (k == "force_idx64") *v = g_force_idx64;

@@ -974,6 +974,7 @@ int64_t fdg::g_bm_eager = 0;
 int64_t fdg::g_bm_sorted_move = 1;
 int64_t fdg::g_bm_move_impl = 0;
 int64_t fdg::g_bm_move_grid = 0;
+int64_t fdg::g_bm_move_hash = 1;
 int64_t fdg::g_bm_fuse_bind = 1;  // select + bind fused: 543 -> 527.5 us per Papers batch (config 3)
 
 namespace {
@@ -1177,6 +1178,12 @@ int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
         ? int(std::max<uint64_t>(1, (n_host + 16 * kMoveRows - 1) / (16 * kMoveRows)))
         : int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 511) / 512, uint64_t(b->ctx->sm_count) * FDG_MOVE_CTAS)));
     const bool host = b->own_ctx ? b->host_src : b->ctx->host_table != nullptr;
+    if (checksum && out && !host && g_bm_move_hash) {  // move + trainer checksum in one pass over the rows
+        FDG_TRACE("bm_move", st);
+        const int rc = launch_move_hash(*b->ctx, st, nodes, n_dev, n_host, &d.st->status, alias, d.is_load[parity & 1],
+                                        table, b->region, static_cast<char*>(out), checksum);
+        if (rc != -1) return rc;
+    }
     if (host && g_bm_sorted_move && d.N < 0xFFFFFFFEull && n_host > 0) {
         // misses in node-id order (address locality for the host side's translation)
         if (b->sort_cap < n_host) {

@@ -446,6 +446,137 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
 }
 
 
+// The buffer manager's row move with the trainer checksum folded in (config 3's e2e path):
+// per row, a miss reads the table and writes its slot and X, a hit reads its slot and writes X
+// (k_move's semantics), and every row is staged in shared memory and hashed by one lane, as in
+// k_gather_hash_rb. Replaces k_move + a second pass over the batch's slots for the checksum
+// (another n x row_bytes of reads). Lane l's row of a group: is_load / alias / node resolve
+// once into a source pointer and a slot pointer (null for a hit), shuffled per load.
+template <int RB, int CH>
+__global__ void __launch_bounds__(kHpWarps * 32, 1)  // one CTA per SM (g_hash_ctas_per_sm): no register cap
+    k_move_hash_rb(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
+                   const uint32_t* status, const int64_t* __restrict__ alias, const uint8_t* __restrict__ is_load,
+                   const char* __restrict__ table, char* __restrict__ region, char* __restrict__ out,
+                   uint64_t* checksum) {
+    using S = HashRbShape<CH>;
+    static_assert(RB % 16 == 0, "16-byte rows");
+    constexpr int NCH = (RB + CH - 1) / CH;
+    constexpr int LASTP = (RB - (NCH - 1) * CH) / 16;
+    constexpr bool EVEN = RB % CH == 0;
+    extern __shared__ __align__(16) char rb_smem[];
+    if (status && *status) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    char* wbuf = rb_smem + warp * 32 * S::STRIDE;
+    const uint64_t n = n_dev ? *n_dev : n_host;
+    const uint64_t groups = (n + 31) / 32;
+    const uint64_t gstride = uint64_t(gridDim.x) * kHpWarps;
+    uint64_t pol;  // row traffic must not flush the batch's metadata sectors out of L2
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    const uint32_t part = lane % S::LPR, rsub = lane / S::LPR;
+    const uint64_t seed = 0x27d4eb2f165667c5ull ^ (uint64_t(RB) * 0x9e3779b97f4a7c15ull);
+    uint64_t sum = 0;
+    auto resolve = [&](uint64_t g, uintptr_t& src, uintptr_t& slot) {  // this lane's row of group g
+        const uint64_t r = g * 32 + lane;
+        src = 0;
+        slot = 0;
+        if (g < groups && r < n) {
+            char* sl = region + uint64_t(alias[r]) * RB;
+            if (is_load[r]) {
+                src = reinterpret_cast<uintptr_t>(table + nodes[r] * RB);
+                slot = reinterpret_cast<uintptr_t>(sl);
+            } else {
+                src = reinterpret_cast<uintptr_t>(sl);
+            }
+        }
+    };
+    uint64_t g = blockIdx.x * uint64_t(kHpWarps) + warp;
+    if (g >= groups) return;
+    uintptr_t my_src, my_slot, nx_src, nx_slot;
+    resolve(g, my_src, my_slot);
+    resolve(g + gstride, nx_src, nx_slot);
+    const char* src[S::NI];
+    uint4 v[S::NI];
+    auto setup = [&](uintptr_t s_reg) {
+#pragma unroll
+        for (int k = 0; k < S::NI; ++k)
+            src[k] = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, s_reg, k * S::RPI + int(rsub))) + part * 16;
+    };
+    auto issue = [&](int c, uint32_t rows) {
+#pragma unroll
+        for (int k = 0; k < S::NI; ++k)
+            if ((EVEN || c + 1 < NCH || int(part) < LASTP) && uint32_t(k * S::RPI) + rsub < rows)
+                v[k] = ldg_row<RB % 128 != 0>(reinterpret_cast<const uint4*>(src[k] + c * CH), pol);
+    };
+    auto rows_of = [&](uint64_t gg) -> uint32_t { return uint32_t(n - gg * 32 < 32 ? n - gg * 32 : 32); };
+    setup(my_src);
+    issue(0, rows_of(g));
+    while (g < groups) {
+        const uint32_t rows = rows_of(g);
+        uint64_t h = seed;
+        const uint64_t gn = g + gstride;
+#pragma unroll 1
+        for (int c = 0; c < NCH; ++c) {
+            const bool lastc = c + 1 == NCH;
+#pragma unroll
+            for (int k = 0; k < S::NI; ++k) {
+                const uint32_t r = k * S::RPI + rsub;
+                const uintptr_t sl = __shfl_sync(0xffffffffu, my_slot, int(r));
+                if ((EVEN || !lastc || int(part) < LASTP) && r < rows) {
+                    const uint32_t off = c * CH + part * 16;
+                    if (out) stg_stream(reinterpret_cast<uint4*>(out + (g * 32 + r) * RB + off), v[k], pol);
+                    if (sl) stg_stream(reinterpret_cast<uint4*>(reinterpret_cast<char*>(sl) + off), v[k], pol);
+                    *reinterpret_cast<uint4*>(wbuf + r * S::STRIDE + part * 16) = v[k];
+                }
+            }
+            __syncwarp();
+            if (!lastc) {
+                issue(c + 1, rows);
+            } else if (gn < groups) {  // chunk 0 of this warp's next group
+                setup(nx_src);
+                issue(0, rows_of(gn));
+            }
+            if (lane < int(rows)) {
+                const uint4* p = reinterpret_cast<const uint4*>(wbuf + lane * S::STRIDE);
+                const int parts = (EVEN || !lastc) ? S::NI : LASTP;
+#pragma unroll
+                for (int s2 = 0; s2 < S::NI; ++s2) {
+                    if (s2 < parts) {
+                        const uint4 w = p[s2];
+                        h = splitmix64(h ^ (uint64_t(w.y) << 32 | w.x));
+                        h = splitmix64(h ^ (uint64_t(w.w) << 32 | w.z));
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        if (lane < int(rows)) sum += splitmix64(h);
+        g = gn;
+        my_src = nx_src;
+        my_slot = nx_slot;
+        resolve(g + gstride, nx_src, nx_slot);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
+}
+
+template <int RB, int CH>
+int launch_move_hash_one(const Ctx& c, cudaStream_t st, uint64_t groups, const uint64_t* nodes, const uint32_t* n_dev,
+                         uint64_t n_host, const uint32_t* status, const int64_t* alias, const uint8_t* is_load,
+                         const char* table, char* region, char* out, uint64_t* checksum) {
+    constexpr int smem = kHpWarps * 32 * HashRbShape<CH>::STRIDE;
+    static PerDeviceOnce attr;
+    if (attr.first())
+        FDG_CUDA(cudaFuncSetAttribute(k_move_hash_rb<RB, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int per_sm = g_hash_ctas_per_sm > 0 ? int(g_hash_ctas_per_sm) : HashRbShape<CH>::MINB;
+    const int blocks = int(std::max<uint64_t>(1, std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps,
+                                                                   uint64_t(c.sm_count) * per_sm)));
+    k_move_hash_rb<RB, CH><<<blocks, kHpWarps * 32, smem, st>>>(nodes, n_dev, n_host, status, alias, is_load, table,
+                                                               region, out, checksum);
+    FDG_CUDA(cudaGetLastError());
+    return FDG_OK;
+}
+
 template <int RB, int CH, bool SHARDED, bool ALIAS>
 int launch_hash_rb_one(int blocks, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                        const uint32_t* status, const TableRef& t, char* out, uint64_t* checksum, uint32_t* ctr) {
@@ -791,6 +922,27 @@ int launch_checksum(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const 
     return FDG_OK;
 }
 }  // namespace
+
+// Buffer-manager row move + trainer checksum in one pass (k_move_hash_rb) for the compiled row
+// sizes; returns -1 when the row size has none (the caller moves and hashes separately).
+int launch_move_hash(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                     const uint32_t* status, const int64_t* alias, const uint8_t* is_load, const char* table,
+                     char* region, char* out, uint64_t* checksum) {
+    const uint64_t groups = (std::max<uint64_t>(n_host, 1) + 31) / 32;
+    switch (c.row_bytes) {
+        case 512:
+            return launch_move_hash_one<512, 256>(c, st, groups, nodes, n_dev, n_host, status, alias, is_load, table,
+                                                  region, out, checksum);
+        case 400:
+            return launch_move_hash_one<400, 256>(c, st, groups, nodes, n_dev, n_host, status, alias, is_load, table,
+                                                  region, out, checksum);
+        case 1024:
+            return launch_move_hash_one<1024, 256>(c, st, groups, nodes, n_dev, n_host, status, alias, is_load, table,
+                                                   region, out, checksum);
+        default:
+            return -1;
+    }
+}
 
 int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
                         uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status,

@@ -168,6 +168,7 @@ int tc_write_hi(cudaStream_t st);       // 1: tcgen05 kind::tf32 GEMMs write A_h
 extern int64_t g_sage_gemm;           // train-stage GEMMs: 1 tensor cores (3xTF32), 0 CUDA cores
 extern int64_t g_bm_overlap;          // buffer-manager row move on its own stream (1) or after the metadata (0)
 extern int64_t g_bm_eager;            // buffer managers created in eager-invalidation (debug) mode
+extern int64_t g_bm_move_hash;        // buffer manager: row move + trainer checksum in one pass
 extern int64_t g_bm_fuse_bind;        // buffer manager: select and bind in one kernel
 extern int64_t g_bm_move_grid;        // buffer-manager LDG row move: 0 persistent grid, 1 a CTA per 64 rows
 extern int64_t g_bm_meta_prio;        // pipeline: the buffer manager's metadata stream at high priority
@@ -196,6 +197,9 @@ int launch_checksum_alias(const Ctx& c, cudaStream_t st, const void* region, con
                           const uint32_t* status = nullptr);
 constexpr uint32_t kDynRing = 256;  // counter pairs per context
 uint32_t* dyn_counter(const Ctx& c);
+int launch_move_hash(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
+                     const uint32_t* status, const int64_t* alias, const uint8_t* is_load, const char* table,
+                     char* region, char* out, uint64_t* checksum);
 int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
                         uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status,
                         bool pipeline = false);
