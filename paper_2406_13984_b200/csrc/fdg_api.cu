@@ -720,7 +720,7 @@ int fdg_set_option(const char* key, int64_t v) {
         return FDG_OK;
     }
     if (k == "bm_move_impl") {
-        if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, "bm_move_impl must be 0 (LDG) or 1 (TMA)");
+        if (v < 0 || v > 2) return fail(FDG_INVALID_ARG, "bm_move_impl must be 0 (LDG), 1 (TMA) or 2 (row groups)");
         g_bm_move_impl = v;
         return FDG_OK;
     }

@@ -972,7 +972,7 @@ using namespace fdg;
 
 int64_t fdg::g_bm_eager = 0;
 int64_t fdg::g_bm_sorted_move = 1;
-int64_t fdg::g_bm_move_impl = 0;
+int64_t fdg::g_bm_move_impl = 2;  // row-group move (k_move_hash_rb without the hash): 524.7 -> 514.4 us per batch
 int64_t fdg::g_bm_move_grid = 0;
 int64_t fdg::g_bm_move_hash = 1;
 int64_t fdg::g_bm_fuse_bind = 1;  // select + bind fused: 543 -> 527.5 us per Papers batch (config 3)
@@ -1178,7 +1178,8 @@ int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
         ? int(std::max<uint64_t>(1, (n_host + 16 * kMoveRows - 1) / (16 * kMoveRows)))
         : int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 511) / 512, uint64_t(b->ctx->sm_count) * FDG_MOVE_CTAS)));
     const bool host = b->own_ctx ? b->host_src : b->ctx->host_table != nullptr;
-    if (checksum && out && !host && g_bm_move_hash) {  // move + trainer checksum in one pass over the rows
+    if (!host && out && ((checksum && g_bm_move_hash) || (!checksum && g_bm_move_impl == 2))) {
+        // move + trainer checksum in one pass over the rows (or the same row-group move alone)
         FDG_TRACE("bm_move", st);
         const int rc = launch_move_hash(*b->ctx, st, nodes, n_dev, n_host, &d.st->status, alias, d.is_load[parity & 1],
                                         table, b->region, static_cast<char*>(out), checksum);

@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
 // k_gather_hash_rb. Replaces k_move + a second pass over the batch's slots for the checksum
 // (another n x row_bytes of reads). Lane l's row of a group: is_load / alias / node resolve
 // once into a source pointer and a slot pointer (null for a hit), shuffled per load.
-template <int RB, int CH>
+template <int RB, int CH, bool HASH = true>
 __global__ void __launch_bounds__(kHpWarps * 32, 1)  // one CTA per SM (g_hash_ctas_per_sm): no register cap
     k_move_hash_rb(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
                    const uint32_t* status, const int64_t* __restrict__ alias, const uint8_t* __restrict__ is_load,
@@ -525,17 +525,17 @@ __global__ void __launch_bounds__(kHpWarps * 32, 1)  // one CTA per SM (g_hash_c
                     const uint32_t off = c * CH + part * 16;
                     if (out) stg_stream(reinterpret_cast<uint4*>(out + (g * 32 + r) * RB + off), v[k], pol);
                     if (sl) stg_stream(reinterpret_cast<uint4*>(reinterpret_cast<char*>(sl) + off), v[k], pol);
-                    *reinterpret_cast<uint4*>(wbuf + r * S::STRIDE + part * 16) = v[k];
+                    if (HASH) *reinterpret_cast<uint4*>(wbuf + r * S::STRIDE + part * 16) = v[k];
                 }
             }
-            __syncwarp();
+            if (HASH) __syncwarp();
             if (!lastc) {
                 issue(c + 1, rows);
             } else if (gn < groups) {  // chunk 0 of this warp's next group
                 setup(nx_src);
                 issue(0, rows_of(gn));
             }
-            if (lane < int(rows)) {
+            if (HASH && lane < int(rows)) {
                 const uint4* p = reinterpret_cast<const uint4*>(wbuf + lane * S::STRIDE);
                 const int parts = (EVEN || !lastc) ? S::NI : LASTP;
 #pragma unroll
@@ -547,14 +547,15 @@ __global__ void __launch_bounds__(kHpWarps * 32, 1)  // one CTA per SM (g_hash_c
                     }
                 }
             }
-            __syncwarp();
+            if (HASH) __syncwarp();
         }
-        if (lane < int(rows)) sum += splitmix64(h);
+        if (HASH && lane < int(rows)) sum += splitmix64(h);
         g = gn;
         my_src = nx_src;
         my_slot = nx_slot;
         resolve(g + gstride, nx_src, nx_slot);
     }
+    if (!HASH) return;
 #pragma unroll
     for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(checksum), (unsigned long long)sum);
@@ -566,13 +567,20 @@ int launch_move_hash_one(const Ctx& c, cudaStream_t st, uint64_t groups, const u
                          const char* table, char* region, char* out, uint64_t* checksum) {
     constexpr int smem = kHpWarps * 32 * HashRbShape<CH>::STRIDE;
     static PerDeviceOnce attr;
-    if (attr.first())
+    if (attr.first()) {
         FDG_CUDA(cudaFuncSetAttribute(k_move_hash_rb<RB, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        FDG_CUDA(
+            cudaFuncSetAttribute(k_move_hash_rb<RB, CH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
     const int per_sm = g_hash_ctas_per_sm > 0 ? int(g_hash_ctas_per_sm) : HashRbShape<CH>::MINB;
     const int blocks = int(std::max<uint64_t>(1, std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps,
                                                                    uint64_t(c.sm_count) * per_sm)));
-    k_move_hash_rb<RB, CH><<<blocks, kHpWarps * 32, smem, st>>>(nodes, n_dev, n_host, status, alias, is_load, table,
-                                                               region, out, checksum);
+    if (checksum)
+        k_move_hash_rb<RB, CH><<<blocks, kHpWarps * 32, smem, st>>>(nodes, n_dev, n_host, status, alias, is_load,
+                                                                   table, region, out, checksum);
+    else  // the same row-group move without the hash (option bm_move_impl 2)
+        k_move_hash_rb<RB, CH, false><<<blocks, kHpWarps * 32, 0, st>>>(nodes, n_dev, n_host, status, alias,
+                                                                       is_load, table, region, out, nullptr);
     FDG_CUDA(cudaGetLastError());
     return FDG_OK;
 }

@@ -324,9 +324,10 @@ def test_extractor_checksums_golden(fd, golden):
     assert sums == [int(x) for x in g["ex_checksum"]]
 
 
-@pytest.fixture(params=[0, 1], ids=["ldg_move", "tma_move"])
+@pytest.fixture(params=[0, 1, 2], ids=["ldg_move", "tma_move", "rowgroup_move"])
 def bm_move(request, fd):
-    """Both row-move engines of the buffer manager: LDG (k_move) and TMA bulk copies (k_move_tma)."""
+    """The buffer manager's row-move engines: LDG (k_move), TMA bulk copies (k_move_tma) and the
+    row-group move (k_move_hash_rb without its hash); with the checksum the fused move + hash runs."""
     old = fd.featdrive.get_option("bm_move_impl")
     fd.set_option("bm_move_impl", request.param)
     yield request.param
