@@ -487,7 +487,8 @@ def run_ours(args):
     for p in pins:
         L.fdg_host_free(p)
 
-    kernel = ("k_move (buffer-manager row move: misses table -> slot and X, hits slot -> X; its launches timed "
+    kernel = ("k_move_hash_rb<HASH=false> (buffer-manager row move, 32-row groups: misses table -> slot and X, "
+              "hits slot -> X; its launches timed "
               "alone, the metadata chain runs before them on the other stream)") if frac else (
         "k_gather_rb_dyn<SHARDED> (row groups; remote rows loaded through the peers' IPC mappings)"
         if layout in ("sharded", "proxy") else "k_gather16_dyn")
