@@ -92,6 +92,7 @@ using namespace fdg;
 
 int64_t fdg::g_bm_overlap = 1;
 int64_t fdg::g_bm_meta_prio = 0;
+int64_t fdg::g_bm_move_early = 0;
 int64_t fdg::g_sampler_sms = 0;
 int64_t fdg::g_prefetch_upfront = 0;    // A/B: all samplers' first MT chunks before any sampling
 int64_t fdg::g_debug_zero_word = -1;     // (batch of the run << 24) | word position; -1 = off
@@ -560,6 +561,9 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 // alias[par], is_load[par] and X[par] were last used by batch j-2's move
                 if (j >= 2) FDG_CUDA(cudaStreamWaitEvent(p->xstream, p->moved[par], 0));
                 FDG_TRY(bm_extract_meta(p->bm, p->xstream, p->nodes[nslot], n_dev, p->cap, p->alias[par], par));
+                // option bm_move_early: batch j's move may start right after its bind, next to release j-1
+                // (measured 517 -> 538 us per Papers batch: off)
+                if (g_bm_move_early) FDG_CUDA(cudaEventRecord(p->bound[par], p->xstream));
                 if (j > 0) {  // lag-1 release (the releaser stage, pipeline.hpp:525-543)
                     const uint64_t pj = do_sample ? j - 1 : ((j - 1) % (sampled_groups * G));
                     // batch j-1's move reads its node list: the list is free once both are done
@@ -572,7 +576,7 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 // Batch j's row move starts after release j-1, not right after bind j: the
                 // release (alias-list walk, latency-bound) then runs without the move saturating
                 // DRAM next to it, and the move overlaps batch j+1's acquire / select / bind.
-                FDG_CUDA(cudaEventRecord(p->bound[par], p->xstream));
+                if (!g_bm_move_early) FDG_CUDA(cudaEventRecord(p->bound[par], p->xstream));
                 FDG_CUDA(cudaStreamWaitEvent(xe, p->bound[par], 0));
                 if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j], xe));
                 FDG_TRY(bm_extract_move(p->bm, xe, p->nodes[nslot], n_dev, p->cap, p->alias[par], X, cs, par));
