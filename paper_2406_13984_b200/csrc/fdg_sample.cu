@@ -91,12 +91,43 @@ __device__ __forceinline__ void st_keep(unsigned long long* p, unsigned long lon
 // costs one CAS and a lookup one load. u64 ids: separate key / value arrays.
 template <typename IdT> struct HashTab;
 
+// Early-table Bloom filter (2 bits per key, 32 bits per bounded key, right after the early
+// table so the same all-ones fill clears it; a clear bit = present). Every last-layer pick
+// looks its node up in the early table, and almost all are absent (Papers: ~0.1 % of picks
+// are earlier layers' nodes), so the lookup probed to the next empty entry -- 8.4 probe
+// iterations per warp, the longest of 30 lanes' chains. The filter answers "absent" for all
+// but ~0.4 % of them with two loads from a ~0.4 MB L2-resident bitmap.
+__device__ __forceinline__ void bloom_hash(uint32_t key, uint32_t nbits, uint32_t& b0, uint32_t& b1) {
+    uint32_t h = key * 0x9E3779B1u;
+    h ^= h >> 15;
+    h *= 0x85EBCA77u;
+    h ^= h >> 13;
+    b0 = __umulhi(h, nbits);
+    b1 = __umulhi(h * 0xC2B2AE3Du + 0x27D4EB2Fu, nbits);
+}
+
 template <> struct HashTab<uint32_t> {
     unsigned long long* e;
     uint32_t size;
     uint32_t keep;  // evict_last policy on loads / stores
+    uint32_t* bloom;      // early table only (null: no filter)
+    uint32_t bloom_bits;
     static constexpr unsigned long long kEmpty = ~0ull;
     __device__ __forceinline__ void* base() const { return e; }
+    __device__ __forceinline__ void mark(uint32_t key) const {
+        if (!bloom) return;
+        uint32_t b0, b1;
+        bloom_hash(key, bloom_bits, b0, b1);
+        atomicAnd(bloom + (b0 >> 5), ~(1u << (b0 & 31)));
+        atomicAnd(bloom + (b1 >> 5), ~(1u << (b1 & 31)));
+    }
+    __device__ __forceinline__ bool maybe_present(uint32_t key) const {
+        if (!bloom) return true;
+        uint32_t b0, b1;
+        bloom_hash(key, bloom_bits, b0, b1);
+        const uint32_t w0 = bloom[b0 >> 5], w1 = bloom[b1 >> 5];
+        return !(((w0 >> (b0 & 31)) | (w1 >> (b1 & 31))) & 1u);
+    }
     __device__ __forceinline__ uint32_t insert(uint32_t key, uint32_t pos) const {
         const unsigned long long want = (uint64_t(key) << 32) | (kPend | pos);
         uint32_t h = hslot(key, size);
@@ -169,6 +200,8 @@ template <> struct HashTab<uint64_t> {
         }
     }
     __device__ __forceinline__ void finalize(uint32_t h, uint64_t, uint32_t local) const { vals[h] = local; }
+    __device__ __forceinline__ void mark(uint64_t) const {}
+    __device__ __forceinline__ bool maybe_present(uint64_t) const { return true; }
 };
 
 // Everything one batch needs (passed by value, kGMax per launch, in kernel params).
@@ -595,7 +628,10 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
             const uint32_t r = base.c + ex.c;
             const uint32_t local = node_base + r;
             W.nodes[local] = uint64_t(key[k]);
-            if (HAS_NEXT) T.finalize(slot[k], key[k], local);  // no later pass reads the last layer's entries
+            if (HAS_NEXT) {  // no later pass reads the last layer's entries
+                T.finalize(slot[k], key[k], local);
+                T.mark(key[k]);
+            }
             if (!SEEDS) W.edges[2 * (ebase + p)] = local;
             if constexpr (HAS_NEXT) {
                 fr.start[r] = lo[k];
@@ -740,8 +776,10 @@ __global__ void __launch_bounds__(256) k_sample(const __grid_constant__ Group<Id
 template <typename IdT>
 __device__ __forceinline__ uint32_t place_pick(const Work<IdT>& W, bool last, IdT key, uint32_t pos) {
     if (!last) return W.tab.insert(key, pos);
-    const uint32_t v = W.tab.lookup(key);
-    if (v < kPend) return kFinalSrc | v;
+    if (W.tab.maybe_present(key)) {
+        const uint32_t v = W.tab.lookup(key);
+        if (v < kPend) return kFinalSrc | v;
+    }
     return W.tab_last.insert(key, pos);
 }
 
@@ -1092,6 +1130,7 @@ __global__ void __launch_bounds__(kEarlyThreads, 1) k_early(const __grid_constan
         if (v == ~0ull) continue;
         uint32_t j = hslot(uint32_t(v >> 32), W.tab.size);
         while (atomicCAS(W.tab.e + j, ~0ull, v) != ~0ull) j = j + 1 == W.tab.size ? 0 : j + 1;
+        W.tab.mark(uint32_t(v >> 32));
     }
     if (tid == 0) {
         cnt->layer_nodes[1] = U0;
@@ -1293,6 +1332,8 @@ int64_t g_hash_early_pct = 0;
 // 68.0 / 71.6 vs 69.9 / 72.0; products 181.9 vs 176.8): the early layers are latency, not
 // throughput, and 8 samplers in flight hide it. Off by default; parity-tested both ways.
 int64_t g_early_fused = 0;
+// Bloom filter over the early table's keys for the last layer's lookups (see bloom_hash).
+int64_t g_early_bloom = 1;
 int64_t g_sampler_ctas_per_sm = 16;
 int64_t g_hash_clear = 1;
 int64_t g_extract_streams = 2;
@@ -1349,6 +1390,7 @@ struct Sampler {
     uint64_t F_bound[FDG_MAX_LAYERS + 1] = {}, P_bound[FDG_MAX_LAYERS + 1] = {};
     uint32_t hsize = 0;    // last-layer table (sized for every node of a batch: the replay's one table)
     uint32_t hsize_a = 0;  // table of the passes before the last
+    uint32_t bloom_bits = 0;  // early-table Bloom filter bits (0: none)
     bool small_f = true;
     bool early_fused = false;  // seeds + layer 0 in one shared-memory CTA per batch (k_early)
     void* arena = nullptr;
@@ -1410,6 +1452,8 @@ Work<IdT> make_work(Sampler& s, const Lane& ln, const BatchArgs& a) {
         if constexpr (sizeof(IdT) == 4) {
             t.e = static_cast<unsigned long long*>(base);
             t.keep = uint32_t(g_hash_keep);
+            t.bloom = nullptr;
+            t.bloom_bits = 0;
         } else {
             t.keys = static_cast<unsigned long long*>(base);
             t.vals = reinterpret_cast<uint32_t*>(static_cast<char*>(base) + uint64_t(size) * 8);
@@ -1418,6 +1462,12 @@ Work<IdT> make_work(Sampler& s, const Lane& ln, const BatchArgs& a) {
     };
     set_tab(w.tab, ln.hash_a, s.hsize_a);
     set_tab(w.tab_last, ln.hash, s.hsize);
+    if constexpr (sizeof(IdT) == 4) {
+        if (s.bloom_bits) {  // right after the early table, inside the region the early fill clears
+            w.tab.bloom = reinterpret_cast<uint32_t*>(static_cast<char*>(ln.hash_a) + uint64_t(s.hsize_a) * 8);
+            w.tab.bloom_bits = s.bloom_bits;
+        }
+    }
     w.seeds = a.seeds;
     w.n_seeds = a.n_seeds;
     w.n_layers = s.n_layers;
@@ -1562,7 +1612,7 @@ int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
         const uint32_t e0 = next_epoch(s, n);
         for (uint32_t l = 0; l < s.n_layers; ++l) next_epoch(s, n);
         Group<IdT> R = G;  // the replay samples the whole batch through the last-layer table
-        for (uint32_t i = 0; i < n; ++i) R.w[i].tab = R.w[i].tab_last;
+        for (uint32_t i = 0; i < n; ++i) R.w[i].tab = R.w[i].tab_last;  // (no filter on the last table)
         k_replay<IdT, false><<<dim3(1, n), kScanThreads, 0, st>>>(R, e0, s.hash_bytes);
     }
     FDG_CUDA(cudaGetLastError());
@@ -1680,7 +1730,10 @@ int sampler_create(Ctx* ctx, uint32_t max_seeds, const uint32_t* fanouts, uint32
     const uint64_t early = std::min<uint64_t>(N, nodes - std::min<uint64_t>(s->P_bound[n_layers - 1], N));
     const uint64_t early_pct = g_hash_early_pct > 0 ? uint64_t(g_hash_early_pct) : uint64_t(g_hash_load_pct);
     s->hsize_a = uint32_t((std::max<uint64_t>(early * 100 / early_pct, 1024) + 31) & ~uint64_t(31));
-    s->hash_bytes_a = al(uint64_t(s->hsize_a) * (ib == 4 ? 8 : 12));
+    s->bloom_bits = (ib == 4 && g_early_bloom && n_layers >= 2)
+                        ? uint32_t(std::min<uint64_t>(std::max<uint64_t>(early * 32, 1024), 1ull << 31) & ~uint64_t(31))
+                        : 0u;
+    s->hash_bytes_a = al(uint64_t(s->hsize_a) * (ib == 4 ? 8 : 12) + uint64_t(s->bloom_bits) / 8);
     uint64_t fmaxF = 1;
     for (uint32_t l = 0; l < n_layers; ++l) fmaxF = std::max(fmaxF, s->F_bound[l]);
     const uint64_t tiles = (std::max<uint64_t>(s->max_edges, max_seeds) + kTile - 1) / kTile + 1;

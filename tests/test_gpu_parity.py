@@ -188,6 +188,28 @@ def test_pipeline_u64_indices_vs_port(fd, port, idx64):
         assert int(recs["checksum"][b]) == cs, f"batch {b}"
 
 
+@pytest.mark.parametrize("bloom", [0, 1])
+def test_sample_early_bloom_vs_port(fd, port, bloom):
+    """The last layer's early-table lookups with and without the Bloom filter in front of them;
+    a small graph makes earlier layers' nodes common among the last layer's picks."""
+    old = fd.featdrive.get_option("early_bloom")
+    fd.set_option("early_bloom", bloom)
+    try:
+        for n in (3_000, 200_000):
+            t = fd.Topology.generate(n, 8, 16, 11, features=False)
+            ip, ix = t.download_topology()
+            rs = np.random.RandomState(n + bloom)
+            for k in range(3):
+                seeds = rs.randint(0, n, size=1000).astype(np.uint64)
+                r = int(rs.randint(0, 2**63))
+                b = fd.sample_khop(t, seeds, [10, 10, 10], r)
+                o = port.sample_khop(ip, ix, seeds, [10, 10, 10], r)
+                np.testing.assert_array_equal(b.nodes, o["nodes"])
+                np.testing.assert_array_equal(b.edges, o["edges"])
+    finally:
+        fd.set_option("early_bloom", old)
+
+
 def test_sample_high_duplicate_rate(fd, port, early):
     """A tiny dense graph: almost every pick is a duplicate (dedup stress)."""
     t = fd.Topology.generate(300, 4, 64, 5, features=False)
