@@ -719,9 +719,12 @@ int fdg_set_option(const char* key, int64_t v) {
         g_bm_fuse_bind = v;
         return FDG_OK;
     }
-    if (k == "bm_move_grid" || k == "bm_meta_prio" || k == "bm_move_early") {
+    if (k == "bm_move_grid" || k == "bm_meta_prio" || k == "bm_move_early" || k == "extract_prio") {
         if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, k + " must be 0 or 1");
-        (k == "bm_move_grid" ? g_bm_move_grid : k == "bm_meta_prio" ? g_bm_meta_prio : g_bm_move_early) = v;
+        (k == "bm_move_grid"    ? g_bm_move_grid
+         : k == "bm_meta_prio"  ? g_bm_meta_prio
+         : k == "bm_move_early" ? g_bm_move_early
+                                : g_extract_prio) = v;
         return FDG_OK;
     }
     if (k == "bm_move_impl") {
@@ -819,6 +822,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "force_idx64") *v = g_force_idx64;
     else if (k == "bm_meta_prio") *v = g_bm_meta_prio;
     else if (k == "bm_move_early") *v = g_bm_move_early;
+    else if (k == "extract_prio") *v = g_extract_prio;
     else if (k == "tc_write_hi") *v = tc_write_hi(nullptr);  // runs the once-per-device check
     else return fail(FDG_INVALID_ARG, "unknown option " + k);
     return FDG_OK;

@@ -93,6 +93,7 @@ using namespace fdg;
 int64_t fdg::g_bm_overlap = 1;
 int64_t fdg::g_bm_meta_prio = 0;
 int64_t fdg::g_bm_move_early = 0;
+int64_t fdg::g_extract_prio = 0;
 int64_t fdg::g_sampler_sms = 0;
 int64_t fdg::g_prefetch_upfront = 0;    // A/B: all samplers' first MT chunks before any sampling
 int64_t fdg::g_debug_zero_word = -1;     // (batch of the run << 24) | word position; -1 = off
@@ -310,14 +311,23 @@ int pipeline_build(fdg_pipeline* p, fdg_ctx* ctx, const uint32_t* fanouts, uint3
     p->cap = std::max<uint64_t>(std::max(mn, me), 1);
     // With the buffer manager the metadata chain (latency-bound, on the critical path of every
     // batch) can run at the samplers' priority, ahead of the DRAM-bound row move (option).
-    FDG_TRY(make_stream(&p->xstream, p->green_x, (cfg->use_buffer_manager && g_bm_meta_prio && prio) ? prio_hi : prio_lo));
+    // option extract_prio: the extraction streams at the highest priority and the samplers at the
+    // lowest (pending gather CTAs are placed before pending sampler CTAs)
+    const bool xprio = g_extract_prio && prio;
+    if (xprio)
+        for (auto& st : p->sstream) {
+            cudaStreamDestroy(st);
+            FDG_TRY(make_stream(&st, p->green_s, prio_lo));
+        }
+    FDG_TRY(make_stream(&p->xstream, p->green_x,
+                        xprio || (cfg->use_buffer_manager && g_bm_meta_prio && prio) ? prio_hi : prio_lo));
     // Plain gathers of consecutive batches alternate between two streams so the tail
     // of one overlaps the head of the next (the buffer-manager path is stateful and
     // stays on one stream).
     // With the buffer manager the row moves get their own stream: batch j's move
     // overlaps batch j+1's acquire / select / bind (the metadata chain stays in order).
     if (cfg->use_buffer_manager || g_extract_streams > 1)
-        FDG_TRY(make_stream(&p->xstream2, p->green_x, prio_lo));
+        FDG_TRY(make_stream(&p->xstream2, p->green_x, xprio ? prio_hi : prio_lo));
     if (cfg->use_buffer_manager)
         for (int i = 0; i < 2; ++i) {
             FDG_CUDA(cudaEventCreateWithFlags(&p->bound[i], cudaEventDisableTiming));
