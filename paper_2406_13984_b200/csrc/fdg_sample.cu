@@ -440,7 +440,7 @@ __device__ __forceinline__ void intern_pass(const Work<IdT>& W, uint32_t q, uint
 #define FDG_INTERN_MINB 2
 #endif
 #ifndef FDG_INTERN_LAST_MINB
-#define FDG_INTERN_LAST_MINB 6  // 40 registers: sample-only 70.8 -> 66.5 us per Papers batch (4: 64 registers)
+#define FDG_INTERN_LAST_MINB 4  // 64 registers: at 40 (6) the spills cost the full pipeline 1-1.5 % though sample-only gains
 #endif
 template <typename IdT, bool SEEDS, bool HAS_NEXT, bool PACK>
 __global__ void __launch_bounds__(kScanThreads, HAS_NEXT ? FDG_INTERN_MINB : FDG_INTERN_LAST_MINB) k_intern_s(const __grid_constant__ Group<IdT> G, uint32_t q,
