@@ -412,6 +412,9 @@ __device__ Tri tri_lookback_cta(uint32_t* flags, uint4* aggs, uint4* incls, uint
 template <typename IdT, bool SEEDS, bool HAS_NEXT, bool PACK>
 __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint32_t epoch, uint32_t tile,
                                             uint32_t P, uint32_t ntiles);
+template <typename IdT>
+__device__ __forceinline__ void intern_tile_last(const Work<IdT>& W, uint32_t q, uint32_t epoch, uint32_t tile,
+                                                 uint32_t P, uint32_t ntiles);
 
 // Persistent: a capped number of CTAs claim tiles in order (keeps SM slots free
 // for the concurrently running gather; look-back needs only claim order).
@@ -431,7 +434,8 @@ __device__ __forceinline__ void intern_pass(const Work<IdT>& W, uint32_t q, uint
         const uint32_t tile = s_tile;
         __syncthreads();
         if (tile >= ntiles) return;
-        intern_tile<IdT, SEEDS, HAS_NEXT, PACK>(W, q, epoch, tile, P, ntiles);
+        if constexpr (!HAS_NEXT && !SEEDS) intern_tile_last<IdT>(W, q, epoch, tile, P, ntiles);
+        else intern_tile<IdT, SEEDS, HAS_NEXT, PACK>(W, q, epoch, tile, P, ntiles);
         __syncthreads();
     }
 }
@@ -440,7 +444,7 @@ __device__ __forceinline__ void intern_pass(const Work<IdT>& W, uint32_t q, uint
 #define FDG_INTERN_MINB 2
 #endif
 #ifndef FDG_INTERN_LAST_MINB
-#define FDG_INTERN_LAST_MINB 4  // 64 registers: at 40 (6) the spills cost the full pipeline 1-1.5 % though sample-only gains
+#define FDG_INTERN_LAST_MINB 6  // 40 registers with the one-register-per-item last pass (intern_tile_last)
 #endif
 template <typename IdT, bool SEEDS, bool HAS_NEXT, bool PACK>
 __global__ void __launch_bounds__(kScanThreads, HAS_NEXT ? FDG_INTERN_MINB : FDG_INTERN_LAST_MINB) k_intern_s(const __grid_constant__ Group<IdT> G, uint32_t q,
@@ -650,6 +654,148 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
                 uint32_t bc;
                 if (tf == tile) {
                     bc = base.c;
+                } else {
+                    while (ld_volatile(W.tile_flag + tf) != (E | 2u)) {
+                    }
+                    __threadfence();
+                    const uint4 in = ld_volatile4(W.tile_incl + tf);
+                    bc = tf == 0 ? 0u : in.x - ld_volatile4(W.tile_agg + tf).x;
+                }
+                src = node_base + bc + ld_volatile_u16(W.rank + ebase + pf);
+            }
+            W.edges[2 * (ebase + p)] = src;
+        }
+    }
+}
+
+// The last pass (no next frontier) with one register per item: an item keeps its key if it is
+// a first occurrence and its entry's value otherwise (the hash slot is not needed after the
+// load: the last layer's entries are never finalised), and its warp-relative rank is recounted
+// from a ballot where it is used instead of being kept -- the general tile's four per-item
+// arrays spilled 56-144 bytes at 64-40 registers.
+template <typename IdT>
+__device__ __forceinline__ void intern_tile_last(const Work<IdT>& W, uint32_t q, uint32_t epoch, uint32_t tile,
+                                                 uint32_t P, uint32_t ntiles) {
+    __shared__ uint32_t s_rowc[kScanItems][kScanThreads / 32];  // per row: warp counts -> exclusive offsets
+    __shared__ uint32_t s_rowx[kScanItems];                     // per row: offset within the tile
+    __shared__ uint32_t s_excl;
+    fdg_batch_counts* cnt = W.cnt;
+    const uint32_t ebase = cnt->layer_edges[q - 1];
+    const uint32_t node_base = cnt->layer_nodes[q];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t p0 = tile * kTile + tid;  // item k: p0 + k * kScanThreads
+    IdT kv[kScanItems];
+    uint32_t first_mask = 0, valid_mask = 0;
+    {
+        uint32_t slot[kScanItems];
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            const uint32_t p = p0 + k * kScanThreads;
+            if (p < P) {
+                valid_mask |= 1u << k;
+                slot[k] = W.edges[2 * (ebase + p)];  // the expansion parks the slot in src
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k)
+            if (valid_mask & (1u << k)) {
+                if (slot[k] & kFinalSrc) {  // an earlier layer's node: its final id
+                    kv[k] = IdT(slot[k] & ~kFinalSrc);
+                    continue;
+                }
+                IdT key;
+                uint32_t val;
+                W.tab_last.load(slot[k], key, val);
+                if (val == (kPend | (p0 + k * kScanThreads))) {
+                    first_mask |= 1u << k;
+                    kv[k] = key;
+                } else {
+                    kv[k] = IdT(val);
+                }
+            }
+    }
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const uint32_t m = __ballot_sync(0xffffffffu, (first_mask >> k) & 1u);
+        if (lane == 0) s_rowc[k][warp] = uint32_t(__popc(m));
+    }
+    __syncthreads();
+    {  // warp r: exclusive offsets of row r's warps and the row total
+        const int r = warp;
+        const uint32_t c = lane < kScanThreads / 32 ? s_rowc[r][lane] : 0u;
+        uint32_t in = c;
+#pragma unroll
+        for (int o = 1; o < kScanThreads / 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, in, o);
+            if (lane >= o) in += y;
+        }
+        if (lane < kScanThreads / 32) s_rowc[r][lane] = in - c;
+        if (lane == kScanThreads / 32 - 1) s_rowx[r] = in;
+    }
+    __syncthreads();
+    const uint32_t E = (epoch & 0x3FFFFFFFu) << 2;
+    __shared__ uint32_t s_agg;
+    if (tid == 0) {
+        uint32_t run = 0;
+        for (int r = 0; r < kScanItems; ++r) {
+            const uint32_t t = s_rowx[r];
+            s_rowx[r] = run;
+            run += t;
+        }
+        s_agg = run;
+        W.tile_agg[tile] = make_uint4(run, 0, 0, 0);  // successors' look-backs wait only for this
+        __threadfence();
+        atomicExch(W.tile_flag + tile, E | 1u);
+    }
+    __syncthreads();
+    // tile-relative ranks of the first occurrences, fenced before this tile's inclusive flag
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const uint32_t m = __ballot_sync(0xffffffffu, (first_mask >> k) & 1u);
+        if (first_mask & (1u << k))
+            W.rank[ebase + p0 + k * kScanThreads] = uint16_t(s_rowx[k] + s_rowc[k][warp] + __popc(m & lt));
+    }
+    __threadfence();
+    __syncthreads();
+    {
+        const uint32_t agg = s_agg;
+        const Tri excl = tri_lookback_cta(W.tile_flag, W.tile_agg, W.tile_incl, tile, epoch);
+        if (tid == 0) {
+            const uint32_t tot = excl.c + agg;
+            W.tile_incl[tile] = make_uint4(tot, 0, 0, 0);
+            __threadfence();
+            atomicExch(W.tile_flag + tile, E | 2u);
+            s_excl = excl.c;
+            if (tile == ntiles - 1) {  // totals of this pass -> the batch record
+                cnt->layer_nodes[q + 1] = node_base + tot;
+                cnt->n_nodes = node_base + tot;
+                cnt->n_edges = cnt->layer_edges[q];
+                cnt->words_used = cnt->layer_draws[q];
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t base = s_excl;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const uint32_t m = __ballot_sync(0xffffffffu, (first_mask >> k) & 1u);
+        if (!(valid_mask & (1u << k))) continue;
+        const uint32_t p = p0 + k * kScanThreads;
+        if (first_mask & (1u << k)) {
+            const uint32_t local = node_base + base + s_rowx[k] + s_rowc[k][warp] + uint32_t(__popc(m & lt));
+            W.nodes[local] = uint64_t(kv[k]);
+            W.edges[2 * (ebase + p)] = local;
+        } else {
+            // src id of a repeated pick (LocalEdge.src, sampling.hpp:124): a final id as is; a
+            // pending entry names its first occurrence, whose tile published its rank first
+            uint32_t src = uint32_t(kv[k]);
+            if (src & kPend) {
+                const uint32_t pf = src & ~kPend;
+                const uint32_t tf = pf / kTile;
+                uint32_t bc;
+                if (tf == tile) {
+                    bc = base;
                 } else {
                     while (ld_volatile(W.tile_flag + tf) != (E | 2u)) {
                     }
