@@ -956,7 +956,9 @@ __global__ void __launch_bounds__(256) k_insert(const __grid_constant__ Group<Id
 #ifndef FDG_EXPAND_MINB
 #define FDG_EXPAND_MINB 8  // <= 32 registers: the expansion is latency-bound (56 registers: 186 -> 203 us per Papers batch)
 #endif
-template <typename IdT>
+// FC: the fanout at compile time (0: read from the batch), so the Floyd chain's steps unroll
+// with constant masks and bounds.
+template <typename IdT, int FC = 0>
 __global__ void __launch_bounds__(256, FDG_EXPAND_MINB) k_expand(const __grid_constant__ Group<IdT> G, uint32_t l) {
     const Work<IdT>& W = G.w[blockIdx.y];
     fdg_batch_counts* cnt = W.cnt;
@@ -965,7 +967,7 @@ __global__ void __launch_bounds__(256, FDG_EXPAND_MINB) k_expand(const __grid_co
     const uint32_t F = cnt->layer_nodes[l + 1] - fs;
     const uint32_t eb = cnt->layer_edges[l];
     const uint64_t db = cnt->layer_draws[l];
-    const uint32_t f = W.fan[l];
+    const uint32_t f = FC ? uint32_t(FC) : W.fan[l];
     const FrontierBuf fr = W.fr[l & 1];
     // The prefetched stream holds an estimate of the words a batch draws (two pieces: the
     // early layers', then the rest); a batch drawing more goes to the exact replay, which
@@ -1011,7 +1013,8 @@ __global__ void __launch_bounds__(256, FDG_EXPAND_MINB) k_expand(const __grid_co
         }
         // Floyd collision chain: step s finalises pick s of every node in the warp
         if (__any_sync(0xffffffffu, live && floyd)) {
-            for (uint32_t s = 1; s < f; ++s) {
+#pragma unroll
+            for (uint32_t s = 1; s < (FC ? uint32_t(FC) : f); ++s) {
                 const IdT c = __shfl_sync(0xffffffffu, picked, int(gbase + s));
                 const uint32_t hits = __ballot_sync(0xffffffffu, in_group && k < s && picked == c);
                 if (k == s && floyd && ((hits >> gbase) & ((1u << s) - 1u))) picked = alt;
@@ -1738,7 +1741,12 @@ int run_group(Sampler& s, cudaStream_t st, uint32_t n, const BatchArgs* a) {
                 const uint64_t npw = 32 / s.fan[l];  // nodes per warp
                 const dim3 grid(grid_for((s.F_bound[l] + npw - 1) / npw * 32, 256,
                                          int(s.ctx->sm_count * g_sampler_ctas_per_sm / n)), n);
-                k_expand<IdT><<<grid, 256, 0, st>>>(G, l);
+                switch (s.fan[l]) {  // compile-time fanouts of the benchmarked configurations
+                    case 5: k_expand<IdT, 5><<<grid, 256, 0, st>>>(G, l); break;
+                    case 10: k_expand<IdT, 10><<<grid, 256, 0, st>>>(G, l); break;
+                    case 15: k_expand<IdT, 15><<<grid, 256, 0, st>>>(G, l); break;
+                    default: k_expand<IdT><<<grid, 256, 0, st>>>(G, l); break;
+                }
             } else {
                 launch_sample<IdT, 0>(s, st, G, n, l);
                 launch_insert<IdT>(s, st, G, n, l);
