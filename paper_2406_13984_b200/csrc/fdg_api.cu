@@ -719,12 +719,14 @@ int fdg_set_option(const char* key, int64_t v) {
         g_bm_fuse_bind = v;
         return FDG_OK;
     }
-    if (k == "bm_move_grid" || k == "bm_meta_prio" || k == "bm_move_early" || k == "extract_prio") {
+    if (k == "bm_move_grid" || k == "bm_meta_prio" || k == "bm_move_early" || k == "extract_prio" ||
+        k == "records_stream") {
         if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, k + " must be 0 or 1");
         (k == "bm_move_grid"    ? g_bm_move_grid
          : k == "bm_meta_prio"  ? g_bm_meta_prio
          : k == "bm_move_early" ? g_bm_move_early
-                                : g_extract_prio) = v;
+         : k == "extract_prio"  ? g_extract_prio
+                                : g_records_stream) = v;
         return FDG_OK;
     }
     if (k == "bm_move_impl") {
@@ -823,6 +825,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "bm_meta_prio") *v = g_bm_meta_prio;
     else if (k == "bm_move_early") *v = g_bm_move_early;
     else if (k == "extract_prio") *v = g_extract_prio;
+    else if (k == "records_stream") *v = g_records_stream;
     else if (k == "tc_write_hi") *v = tc_write_hi(nullptr);  // runs the once-per-device check
     else return fail(FDG_INVALID_ARG, "unknown option " + k);
     return FDG_OK;

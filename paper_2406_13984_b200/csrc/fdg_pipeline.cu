@@ -60,6 +60,8 @@ struct fdg_pipeline {
     CUgreenCtx green_x = nullptr;        // ... and everything on the extraction streams
     cudaStream_t xstream2 = nullptr;     // second extraction stream (plain gathers alternate; with the
                                          // buffer manager: the row-move stream)
+    cudaStream_t dstream = nullptr;      // option records_stream: batch records' D2H off the extraction streams
+    std::vector<cudaEvent_t> rec_ev;     // ... one event per in-flight record
     cudaEvent_t bound[2] = {nullptr, nullptr};  // buffer manager: batch parity's metadata half done
     cudaEvent_t moved[2] = {nullptr, nullptr};  // buffer manager: batch parity's row move done
     uint64_t cap = 0, max_nodes = 0;
@@ -94,6 +96,7 @@ int64_t fdg::g_bm_overlap = 1;
 int64_t fdg::g_bm_meta_prio = 0;
 int64_t fdg::g_bm_move_early = 0;
 int64_t fdg::g_extract_prio = 0;
+int64_t fdg::g_records_stream = 0;
 int64_t fdg::g_sampler_sms = 0;
 int64_t fdg::g_prefetch_upfront = 0;    // A/B: all samplers' first MT chunks before any sampling
 int64_t fdg::g_debug_zero_word = -1;     // (batch of the run << 24) | word position; -1 = off
@@ -181,6 +184,8 @@ void destroy(fdg_pipeline* p) {
     for (auto s : p->sstream) cudaStreamDestroy(s);
     if (p->xstream) cudaStreamDestroy(p->xstream);
     if (p->xstream2) cudaStreamDestroy(p->xstream2);
+    if (p->dstream) cudaStreamDestroy(p->dstream);
+    for (auto e : p->rec_ev) cudaEventDestroy(e);
     if (p->tstream) cudaStreamDestroy(p->tstream);
     for (int i = 0; i < 2; ++i) {
         if (p->gathered[i]) cudaEventDestroy(p->gathered[i]);
@@ -603,8 +608,23 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 FDG_CUDA(cudaEventRecord(p->moved[par], xe));
             }
             if (extract_ms && !p->bm) FDG_CUDA(cudaEventRecord(p->tev[2 * j + 1], tsplit ? xs : xe));
-            if (records_host)  // device -> host read of the batch record (counts + checksum)
-                FDG_CUDA(cudaMemcpyAsync(records_host + j, cnt, sizeof(fdg_batch_counts), cudaMemcpyDeviceToHost, xe));
+            if (records_host) {  // device -> host read of the batch record (counts + checksum)
+                if (g_records_stream) {  // on its own stream: the next gather on xe does not queue behind it
+                    if (!p->dstream) {
+                        FDG_CUDA(cudaStreamCreateWithFlags(&p->dstream, cudaStreamNonBlocking));
+                        p->rec_ev.resize(64);
+                        for (auto& e : p->rec_ev) FDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                    }
+                    cudaEvent_t e = p->rec_ev[j % p->rec_ev.size()];
+                    FDG_CUDA(cudaEventRecord(e, xe));
+                    FDG_CUDA(cudaStreamWaitEvent(p->dstream, e, 0));
+                    FDG_CUDA(cudaMemcpyAsync(records_host + j, cnt, sizeof(fdg_batch_counts), cudaMemcpyDeviceToHost,
+                                             p->dstream));
+                } else {
+                    FDG_CUDA(cudaMemcpyAsync(records_host + j, cnt, sizeof(fdg_batch_counts), cudaMemcpyDeviceToHost,
+                                             xe));
+                }
+            }
             if (!p->bm) FDG_CUDA(cudaEventRecord(p->extracted[slot], xe));  // the node / edge lists are free
         }
     }
@@ -615,8 +635,8 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                            &p->counts[lj].n_nodes, p->cap));
         FDG_CUDA(cudaEventRecord(p->extracted[(n_batches - 1) % p->nslots], p->xstream));
     }
-    for (uint32_t s = 0; s <= S + 1; ++s) {  // join the sampler, second extraction and train streams
-        cudaStream_t js = s < S ? p->sstream[s] : s == S ? p->xstream2 : p->tstream;
+    for (uint32_t s = 0; s <= S + 2; ++s) {  // join the sampler, second extraction, train and record streams
+        cudaStream_t js = s < S ? p->sstream[s] : s == S ? p->xstream2 : s == S + 1 ? p->tstream : p->dstream;
         if (!js) continue;
         cudaEvent_t e;
         FDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

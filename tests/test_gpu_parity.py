@@ -646,9 +646,13 @@ def test_pipeline_buffer_capacity_reported(fd):
     assert int(recs["status"][0]) == 4  # FDG_CAPACITY
 
 
-def test_pipeline_host_seeds_e2e(fd):
-    """The e2e path: seeds copied from pinned host memory per batch, records read back per batch."""
+@pytest.mark.parametrize("records_stream", [0, 1])
+def test_pipeline_host_seeds_e2e(fd, records_stream):
+    """The e2e path: seeds copied from pinned host memory per batch, records read back per batch
+    (on the extraction stream, or on a stream of their own)."""
     import ctypes as C
+    old = fd.featdrive.get_option("records_stream")
+    fd.set_option("records_stream", records_stream)
     t = fd.Topology.generate(100_000, 16, 10, 5)
     B, nb, fan = 128, 9, [4, 4]
     seeds = np.random.RandomState(0).randint(0, 100_000, size=nb * B).astype(np.uint64)
@@ -667,6 +671,7 @@ def test_pipeline_host_seeds_e2e(fd):
         assert int(recs["checksum"][b]) == fd.gather(t, batch.nodes, checksum=True)[1]
     L.fdg_host_free(pin.value)
     L.fdg_host_free(rec.value)
+    fd.set_option("records_stream", old)
 
 
 @pytest.mark.parametrize("impl", [0, 1, 4])
