@@ -96,7 +96,7 @@ int64_t fdg::g_bm_overlap = 1;
 int64_t fdg::g_bm_meta_prio = 0;
 int64_t fdg::g_bm_move_early = 0;
 int64_t fdg::g_extract_prio = 0;
-int64_t fdg::g_records_stream = 0;
+int64_t fdg::g_records_stream = 1;  // e2e 5286 / 5256 -> 5300 / 5349 batches/s (Papers bench, 2 runs each)
 int64_t fdg::g_sampler_sms = 0;
 int64_t fdg::g_prefetch_upfront = 0;    // A/B: all samplers' first MT chunks before any sampling
 int64_t fdg::g_debug_zero_word = -1;     // (batch of the run << 24) | word position; -1 = off
