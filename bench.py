@@ -503,7 +503,8 @@ def run_ours(args):
         "gather_gbs": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "pipeline_gbs": float(gather_bytes.sum()) / (max_ms / 1e3) / 1e9,
-                     "traffic": _traffic(cfg), "peak_kind": hbm_kind, "kernel": kernel,
+                     "traffic": (_traffic(cfg) or {}).get("bytes"), "traffic_detail": _traffic(cfg),
+                     "peak_kind": hbm_kind, "kernel": kernel,
                      "launch_ms_mean": busy_ms / K, "launch_ms_mean_per_stream": float(ext_ms.mean()),
                      "bytes_per_launch": float(gather_bytes.mean()),
                      "note": ("algorithmic bytes = (2 x nodes + misses) x row_bytes per launch (a miss is read "
