@@ -719,13 +719,16 @@ int fdg_set_option(const char* key, int64_t v) {
         g_bm_fuse_bind = v;
         return FDG_OK;
     }
-    if (k == "bm_move_grid" || k == "bm_meta_prio" || k == "bm_move_early" || k == "extract_prio" ||
-        k == "records_stream") {
+    if (k == "extract_prio") {
+        if (v < 0 || v > 2) return fail(FDG_INVALID_ARG, "extract_prio must be 0, 1 or 2 (buffer manager only)");
+        g_extract_prio = v;
+        return FDG_OK;
+    }
+    if (k == "bm_move_grid" || k == "bm_meta_prio" || k == "bm_move_early" || k == "records_stream") {
         if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, k + " must be 0 or 1");
         (k == "bm_move_grid"    ? g_bm_move_grid
          : k == "bm_meta_prio"  ? g_bm_meta_prio
          : k == "bm_move_early" ? g_bm_move_early
-         : k == "extract_prio"  ? g_extract_prio
                                 : g_records_stream) = v;
         return FDG_OK;
     }

@@ -95,7 +95,7 @@ using namespace fdg;
 int64_t fdg::g_bm_overlap = 1;
 int64_t fdg::g_bm_meta_prio = 0;
 int64_t fdg::g_bm_move_early = 0;
-int64_t fdg::g_extract_prio = 0;
+int64_t fdg::g_extract_prio = 2;
 int64_t fdg::g_records_stream = 1;  // e2e 5286 / 5256 -> 5300 / 5349 batches/s (Papers bench, 2 runs each)
 int64_t fdg::g_sampler_sms = 0;
 int64_t fdg::g_prefetch_upfront = 0;    // A/B: all samplers' first MT chunks before any sampling
@@ -317,8 +317,10 @@ int pipeline_build(fdg_pipeline* p, fdg_ctx* ctx, const uint32_t* fanouts, uint3
     // With the buffer manager the metadata chain (latency-bound, on the critical path of every
     // batch) can run at the samplers' priority, ahead of the DRAM-bound row move (option).
     // option extract_prio: the extraction streams at the highest priority and the samplers at the
-    // lowest (pending gather CTAs are placed before pending sampler CTAs)
-    const bool xprio = g_extract_prio && prio;
+    // lowest (pending gather CTAs are placed before pending sampler CTAs): 1 always, 2 (default)
+    // with the buffer manager only. Papers 181.7 -> 188.0 us per batch with plain gathers, but
+    // config 3 523.4 -> 514.5 (its metadata chain is the critical path there).
+    const bool xprio = (g_extract_prio == 1 || (g_extract_prio == 2 && cfg->use_buffer_manager)) && prio;
     if (xprio)
         for (auto& st : p->sstream) {
             cudaStreamDestroy(st);
