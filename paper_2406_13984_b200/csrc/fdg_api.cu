@@ -719,6 +719,11 @@ int fdg_set_option(const char* key, int64_t v) {
         g_bm_fuse_bind = v;
         return FDG_OK;
     }
+    if (k == "pipe_slots") {
+        if (v < 0 || v > 256) return fail(FDG_INVALID_ARG, "pipe_slots must be in [0, 256]");
+        g_pipe_slots = v;
+        return FDG_OK;
+    }
     if (k == "extract_prio") {
         if (v < 0 || v > 2) return fail(FDG_INVALID_ARG, "extract_prio must be 0, 1 or 2 (buffer manager only)");
         g_extract_prio = v;
@@ -829,6 +834,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "bm_move_early") *v = g_bm_move_early;
     else if (k == "extract_prio") *v = g_extract_prio;
     else if (k == "records_stream") *v = g_records_stream;
+    else if (k == "pipe_slots") *v = g_pipe_slots;
     else if (k == "tc_write_hi") *v = tc_write_hi(nullptr);  // runs the once-per-device check
     else return fail(FDG_INVALID_ARG, "unknown option " + k);
     return FDG_OK;

@@ -171,6 +171,7 @@ extern int64_t g_bm_eager;            // buffer managers created in eager-invali
 extern int64_t g_bm_move_hash;        // buffer manager: row move + trainer checksum in one pass
 extern int64_t g_bm_fuse_bind;        // buffer manager: select and bind in one kernel
 extern int64_t g_bm_move_grid;        // buffer-manager LDG row move: 0 persistent grid, 1 a CTA per 64 rows
+extern int64_t g_pipe_slots;          // pipeline: per-batch output slots (0: 2 x samplers x group)
 extern int64_t g_records_stream;      // pipeline: batch records' D2H on their own stream
 extern int64_t g_extract_prio;        // pipeline: extraction streams above the samplers' priority
 extern int64_t g_bm_move_early;       // pipeline: batch j's row move starts after its bind, not after release j-1

@@ -96,7 +96,8 @@ int64_t fdg::g_bm_overlap = 1;
 int64_t fdg::g_bm_meta_prio = 0;
 int64_t fdg::g_bm_move_early = 0;
 int64_t fdg::g_extract_prio = 2;
-int64_t fdg::g_records_stream = 1;  // e2e 5286 / 5256 -> 5300 / 5349 batches/s (Papers bench, 2 runs each)
+int64_t fdg::g_records_stream = 1;
+int64_t fdg::g_pipe_slots = 0;  // e2e 5286 / 5256 -> 5300 / 5349 batches/s (Papers bench, 2 runs each)
 int64_t fdg::g_sampler_sms = 0;
 int64_t fdg::g_prefetch_upfront = 0;    // A/B: all samplers' first MT chunks before any sampling
 int64_t fdg::g_debug_zero_word = -1;     // (batch of the run << 24) | word position; -1 = off
@@ -346,7 +347,9 @@ int pipeline_build(fdg_pipeline* p, fdg_ctx* ctx, const uint32_t* fanouts, uint3
         FDG_TRY(make_stream(&st, p->green_s, 0));
         p->mstream.push_back(st);
     }
-    p->nslots = 2 * S * G;
+    // per-batch output slots: how far the samplers may run ahead of the extraction (option
+    // pipe_slots overrides 2 * S * G; at least G + 1)
+    p->nslots = g_pipe_slots > 0 ? std::max<uint32_t>(uint32_t(g_pipe_slots), G + 1) : 2 * S * G;
     for (uint32_t i = 0; i < p->nslots; ++i) {
         uint64_t* n;
         uint32_t* e;
