@@ -729,6 +729,11 @@ int fdg_set_option(const char* key, int64_t v) {
         g_extract_prio = v;
         return FDG_OK;
     }
+    if (k == "bm_split_move") {
+        if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, "bm_split_move must be 0 or 1");
+        g_bm_split_move = v;
+        return FDG_OK;
+    }
     if (k == "bm_move_grid" || k == "bm_meta_prio" || k == "bm_move_early" || k == "records_stream") {
         if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, k + " must be 0 or 1");
         (k == "bm_move_grid"    ? g_bm_move_grid
@@ -835,6 +840,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "extract_prio") *v = g_extract_prio;
     else if (k == "records_stream") *v = g_records_stream;
     else if (k == "pipe_slots") *v = g_pipe_slots;
+    else if (k == "bm_split_move") *v = g_bm_split_move;
     else if (k == "tc_write_hi") *v = tc_write_hi(nullptr);  // runs the once-per-device check
     else return fail(FDG_INVALID_ARG, "unknown option " + k);
     return FDG_OK;

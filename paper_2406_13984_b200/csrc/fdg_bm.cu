@@ -1132,7 +1132,7 @@ namespace fdg {
 // Algorithm 1's metadata half for one batch (acquire, LRU pops, bind + publish):
 // strictly stream-ordered with the releases, it fixes the alias list.
 int bm_extract_meta(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
-                    int64_t* alias, uint32_t parity) {
+                    int64_t* alias, uint32_t parity, cudaEvent_t after_acquire) {
     const uint64_t bound = n_host;
     if (bound > b->max_batch) return fail(FDG_INVALID_ARG, "bm_extract: batch larger than max_batch_nodes");
     const BmDev& d = b->d;
@@ -1142,6 +1142,7 @@ int bm_extract_meta(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
         k_acquire<<<n_tiles_for(bound), kT, 0, st>>>(d, nodes, n_dev, n_host, alias, d.is_load[parity & 1],
                                                     b->epoch++);
     }
+    if (after_acquire) FDG_CUDA(cudaEventRecord(after_acquire, st));
     if (g_bm_fuse_bind) {  // select + bind in one pass over the popped slots' records
         FDG_TRACE("bm_select", st);
         k_select<true><<<bm_persistent_grid(b), kT, 0, st>>>(d, b->epoch++, nodes, alias);
@@ -1164,7 +1165,7 @@ int bm_extract_meta(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
 // checksum over the batch's slots. Reads only the batch's alias list and
 // is_load[parity], so it can overlap the next batch's metadata half.
 int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
-                    const int64_t* alias, void* out, uint64_t* checksum, uint32_t parity) {
+                    const int64_t* alias, void* out, uint64_t* checksum, uint32_t parity, int mode) {
     const BmDev& d = b->d;
     const uint32_t rb = b->ctx->row_bytes;
     if (b->ctx->shard_bases.empty() || !b->region)
@@ -1178,6 +1179,12 @@ int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
         ? int(std::max<uint64_t>(1, (n_host + 16 * kMoveRows - 1) / (16 * kMoveRows)))
         : int(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 511) / 512, uint64_t(b->ctx->sm_count) * FDG_MOVE_CTAS)));
     const bool host = b->own_ctx ? b->host_src : b->ctx->host_table != nullptr;
+    if (mode == 1 || mode == 2) {  // split move (the pipeline checks the row size and the tier)
+        FDG_TRACE(mode == 1 ? "bm_move_x" : "bm_fill", st);
+        const int rc = launch_move_hash(*b->ctx, st, nodes, n_dev, n_host, &d.st->status, alias,
+                                        d.is_load[parity & 1], table, b->region, static_cast<char*>(out), nullptr, mode);
+        return rc == -1 ? fail(FDG_INVALID_ARG, "bm split move: no instantiation for this row size") : rc;
+    }
     if (!host && out && ((checksum && g_bm_move_hash) || (!checksum && g_bm_move_impl == 2))) {
         // move + trainer checksum in one pass over the rows (or the same row-group move alone)
         FDG_TRACE("bm_move", st);
@@ -1240,8 +1247,8 @@ extern "C" {
 int fdg_bm_extract(fdg_bm* b, void* stv, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host, int64_t* alias,
                    void* out, uint64_t* checksum) {
     cudaStream_t st = (cudaStream_t)stv;
-    FDG_TRY(bm_extract_meta(b, st, nodes, n_dev, n_host, alias, 0));
-    return bm_extract_move(b, st, nodes, n_dev, n_host, alias, out, checksum, 0);
+    FDG_TRY(bm_extract_meta(b, st, nodes, n_dev, n_host, alias, 0, nullptr));
+    return bm_extract_move(b, st, nodes, n_dev, n_host, alias, out, checksum, 0, 0);
 }
 
 int fdg_bm_release(fdg_bm* b, void* stv, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host) {

@@ -452,7 +452,9 @@ __global__ void __launch_bounds__(kHpWarps * 32, HashRbShape<CH>::MINB)
 // k_gather_hash_rb. Replaces k_move + a second pass over the batch's slots for the checksum
 // (another n x row_bytes of reads). Lane l's row of a group: is_load / alias / node resolve
 // once into a source pointer and a slot pointer (null for a hit), shuffled per load.
-template <int RB, int CH, bool HASH = true>
+// MODE 0: the whole move; 1: X rows only (before the bind: misses read the table, hits their
+// pinned slots); 2: the misses' slot fills only (after the bind). Split moves are never hashed.
+template <int RB, int CH, bool HASH = true, int MODE = 0>
 __global__ void __launch_bounds__(kHpWarps * 32, 1)  // one CTA per SM (g_hash_ctas_per_sm): no register cap
     k_move_hash_rb(const uint64_t* __restrict__ nodes, const uint32_t* n_dev, uint64_t n_host,
                    const uint32_t* status, const int64_t* __restrict__ alias, const uint8_t* __restrict__ is_load,
@@ -480,12 +482,11 @@ __global__ void __launch_bounds__(kHpWarps * 32, 1)  // one CTA per SM (g_hash_c
         src = 0;
         slot = 0;
         if (g < groups && r < n) {
-            char* sl = region + uint64_t(alias[r]) * RB;
             if (is_load[r]) {
                 src = reinterpret_cast<uintptr_t>(table + nodes[r] * RB);
-                slot = reinterpret_cast<uintptr_t>(sl);
-            } else {
-                src = reinterpret_cast<uintptr_t>(sl);
+                if (MODE != 1) slot = reinterpret_cast<uintptr_t>(region + uint64_t(alias[r]) * RB);  // bound
+            } else if (MODE != 2) {
+                src = reinterpret_cast<uintptr_t>(region + uint64_t(alias[r]) * RB);
             }
         }
     };
@@ -496,15 +497,21 @@ __global__ void __launch_bounds__(kHpWarps * 32, 1)  // one CTA per SM (g_hash_c
     resolve(g + gstride, nx_src, nx_slot);
     const char* src[S::NI];
     uint4 v[S::NI];
+    uint32_t live = 0;  // MODE 2: rows of this lane's loads that move (misses)
     auto setup = [&](uintptr_t s_reg) {
+        live = 0;
 #pragma unroll
-        for (int k = 0; k < S::NI; ++k)
-            src[k] = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, s_reg, k * S::RPI + int(rsub))) + part * 16;
+        for (int k = 0; k < S::NI; ++k) {
+            const uintptr_t sp = __shfl_sync(0xffffffffu, s_reg, k * S::RPI + int(rsub));
+            src[k] = reinterpret_cast<const char*>(sp) + part * 16;
+            if (sp) live |= 1u << k;
+        }
     };
     auto issue = [&](int c, uint32_t rows) {
 #pragma unroll
         for (int k = 0; k < S::NI; ++k)
-            if ((EVEN || c + 1 < NCH || int(part) < LASTP) && uint32_t(k * S::RPI) + rsub < rows)
+            if ((EVEN || c + 1 < NCH || int(part) < LASTP) && uint32_t(k * S::RPI) + rsub < rows &&
+                (MODE != 2 || (live & (1u << k))))
                 v[k] = ldg_row<RB % 128 != 0>(reinterpret_cast<const uint4*>(src[k] + c * CH), pol);
     };
     auto rows_of = [&](uint64_t gg) -> uint32_t { return uint32_t(n - gg * 32 < 32 ? n - gg * 32 : 32); };
@@ -521,9 +528,9 @@ __global__ void __launch_bounds__(kHpWarps * 32, 1)  // one CTA per SM (g_hash_c
             for (int k = 0; k < S::NI; ++k) {
                 const uint32_t r = k * S::RPI + rsub;
                 const uintptr_t sl = __shfl_sync(0xffffffffu, my_slot, int(r));
-                if ((EVEN || !lastc || int(part) < LASTP) && r < rows) {
+                if ((EVEN || !lastc || int(part) < LASTP) && r < rows && (MODE != 2 || (live & (1u << k)))) {
                     const uint32_t off = c * CH + part * 16;
-                    if (out) stg_stream(reinterpret_cast<uint4*>(out + (g * 32 + r) * RB + off), v[k], pol);
+                    if (MODE != 2 && out) stg_stream(reinterpret_cast<uint4*>(out + (g * 32 + r) * RB + off), v[k], pol);
                     if (sl) stg_stream(reinterpret_cast<uint4*>(reinterpret_cast<char*>(sl) + off), v[k], pol);
                     if (HASH) *reinterpret_cast<uint4*>(wbuf + r * S::STRIDE + part * 16) = v[k];
                 }
@@ -564,13 +571,27 @@ __global__ void __launch_bounds__(kHpWarps * 32, 1)  // one CTA per SM (g_hash_c
 template <int RB, int CH>
 int launch_move_hash_one(const Ctx& c, cudaStream_t st, uint64_t groups, const uint64_t* nodes, const uint32_t* n_dev,
                          uint64_t n_host, const uint32_t* status, const int64_t* alias, const uint8_t* is_load,
-                         const char* table, char* region, char* out, uint64_t* checksum) {
+                         const char* table, char* region, char* out, uint64_t* checksum, int mode) {
     constexpr int smem = kHpWarps * 32 * HashRbShape<CH>::STRIDE;
     static PerDeviceOnce attr;
     if (attr.first()) {
         FDG_CUDA(cudaFuncSetAttribute(k_move_hash_rb<RB, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         FDG_CUDA(
             cudaFuncSetAttribute(k_move_hash_rb<RB, CH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+    if (mode == 1 || mode == 2) {  // split move (no hash, no shared memory)
+        if (mode == 1)
+            k_move_hash_rb<RB, CH, false, 1><<<std::max<int>(1, int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps,
+                                                                              uint64_t(c.sm_count)))),
+                                               kHpWarps * 32, 0, st>>>(nodes, n_dev, n_host, status, alias, is_load,
+                                                                       table, region, out, nullptr);
+        else
+            k_move_hash_rb<RB, CH, false, 2><<<std::max<int>(1, int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps,
+                                                                              uint64_t(c.sm_count)))),
+                                               kHpWarps * 32, 0, st>>>(nodes, n_dev, n_host, status, alias, is_load,
+                                                                       table, region, nullptr, nullptr);
+        FDG_CUDA(cudaGetLastError());
+        return FDG_OK;
     }
     const int per_sm = g_hash_ctas_per_sm > 0 ? int(g_hash_ctas_per_sm) : HashRbShape<CH>::MINB;
     const int blocks = int(std::max<uint64_t>(1, std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps,
@@ -935,18 +956,18 @@ int launch_checksum(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const 
 // sizes; returns -1 when the row size has none (the caller moves and hashes separately).
 int launch_move_hash(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                      const uint32_t* status, const int64_t* alias, const uint8_t* is_load, const char* table,
-                     char* region, char* out, uint64_t* checksum) {
+                     char* region, char* out, uint64_t* checksum, int mode) {
     const uint64_t groups = (std::max<uint64_t>(n_host, 1) + 31) / 32;
     switch (c.row_bytes) {
         case 512:
             return launch_move_hash_one<512, 256>(c, st, groups, nodes, n_dev, n_host, status, alias, is_load, table,
-                                                  region, out, checksum);
+                                                  region, out, checksum, mode);
         case 400:
             return launch_move_hash_one<400, 256>(c, st, groups, nodes, n_dev, n_host, status, alias, is_load, table,
-                                                  region, out, checksum);
+                                                  region, out, checksum, mode);
         case 1024:
             return launch_move_hash_one<1024, 256>(c, st, groups, nodes, n_dev, n_host, status, alias, is_load, table,
-                                                   region, out, checksum);
+                                                   region, out, checksum, mode);
         default:
             return -1;
     }

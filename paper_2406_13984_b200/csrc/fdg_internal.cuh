@@ -171,6 +171,7 @@ extern int64_t g_bm_eager;            // buffer managers created in eager-invali
 extern int64_t g_bm_move_hash;        // buffer manager: row move + trainer checksum in one pass
 extern int64_t g_bm_fuse_bind;        // buffer manager: select and bind in one kernel
 extern int64_t g_bm_move_grid;        // buffer-manager LDG row move: 0 persistent grid, 1 a CTA per 64 rows
+extern int64_t g_bm_split_move;       // pipeline: X rows moved after the acquire, slot fills after the bind
 extern int64_t g_pipe_slots;          // pipeline: per-batch output slots (0: 2 x samplers x group)
 extern int64_t g_records_stream;      // pipeline: batch records' D2H on their own stream
 extern int64_t g_extract_prio;        // pipeline: extraction streams above the samplers' priority
@@ -204,7 +205,7 @@ constexpr uint32_t kDynRing = 256;  // counter pairs per context
 uint32_t* dyn_counter(const Ctx& c);
 int launch_move_hash(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                      const uint32_t* status, const int64_t* alias, const uint8_t* is_load, const char* table,
-                     char* region, char* out, uint64_t* checksum);
+                     char* region, char* out, uint64_t* checksum, int mode = 0);
 int launch_gather_bound(const Ctx& c, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev,
                         uint64_t n_host, uint64_t n_bound, void* out, uint64_t* checksum, const uint32_t* status,
                         bool pipeline = false);

@@ -40,9 +40,9 @@ void sampler_capacity(const Sampler* s, uint64_t* max_nodes, uint64_t* max_edges
 void sampler_hash_region(const Sampler* s, void** base, uint64_t* bytes);
 int bm_status_to(fdg_bm* b, cudaStream_t st, uint32_t* dst);
 int bm_extract_meta(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
-                    int64_t* alias, uint32_t parity);
+                    int64_t* alias, uint32_t parity, cudaEvent_t after_acquire = nullptr);
 int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
-                    const int64_t* alias, void* out, uint64_t* checksum, uint32_t parity);
+                    const int64_t* alias, void* out, uint64_t* checksum, uint32_t parity, int mode = 0);
 int bm_release(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const int64_t* alias, const uint32_t* n_dev,
                uint64_t n_host);
 }  // namespace fdg
@@ -64,6 +64,7 @@ struct fdg_pipeline {
     std::vector<cudaEvent_t> rec_ev;     // ... one event per in-flight record
     cudaEvent_t bound[2] = {nullptr, nullptr};  // buffer manager: batch parity's metadata half done
     cudaEvent_t moved[2] = {nullptr, nullptr};  // buffer manager: batch parity's row move done
+    cudaEvent_t acquired[2] = {nullptr, nullptr};  // buffer manager, split move: batch parity's acquire done
     uint64_t cap = 0, max_nodes = 0;
     uint32_t nslots = 0;             // per-batch output slots (2 * S * G)
     std::vector<uint64_t*> nodes;
@@ -97,7 +98,8 @@ int64_t fdg::g_bm_meta_prio = 0;
 int64_t fdg::g_bm_move_early = 0;
 int64_t fdg::g_extract_prio = 2;
 int64_t fdg::g_records_stream = 1;
-int64_t fdg::g_pipe_slots = 0;  // e2e 5286 / 5256 -> 5300 / 5349 batches/s (Papers bench, 2 runs each)
+int64_t fdg::g_pipe_slots = 0;
+int64_t fdg::g_bm_split_move = 0;  // e2e 5286 / 5256 -> 5300 / 5349 batches/s (Papers bench, 2 runs each)
 int64_t fdg::g_sampler_sms = 0;
 int64_t fdg::g_prefetch_upfront = 0;    // A/B: all samplers' first MT chunks before any sampling
 int64_t fdg::g_debug_zero_word = -1;     // (batch of the run << 24) | word position; -1 = off
@@ -186,6 +188,8 @@ void destroy(fdg_pipeline* p) {
     if (p->xstream) cudaStreamDestroy(p->xstream);
     if (p->xstream2) cudaStreamDestroy(p->xstream2);
     if (p->dstream) cudaStreamDestroy(p->dstream);
+    for (auto e : p->acquired)
+        if (e) cudaEventDestroy(e);
     for (auto e : p->rec_ev) cudaEventDestroy(e);
     if (p->tstream) cudaStreamDestroy(p->tstream);
     for (int i = 0; i < 2; ++i) {
@@ -340,6 +344,7 @@ int pipeline_build(fdg_pipeline* p, fdg_ctx* ctx, const uint32_t* fanouts, uint3
         for (int i = 0; i < 2; ++i) {
             FDG_CUDA(cudaEventCreateWithFlags(&p->bound[i], cudaEventDisableTiming));
             FDG_CUDA(cudaEventCreateWithFlags(&p->moved[i], cudaEventDisableTiming));
+            FDG_CUDA(cudaEventCreateWithFlags(&p->acquired[i], cudaEventDisableTiming));
         }
     // one MT stream per sampler: prefetch launches of different samplers overlap
     for (uint32_t i = 0; i < S; ++i) {
@@ -580,7 +585,16 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 const uint32_t par = uint32_t(j & 1);
                 // alias[par], is_load[par] and X[par] were last used by batch j-2's move
                 if (j >= 2) FDG_CUDA(cudaStreamWaitEvent(p->xstream, p->moved[par], 0));
-                FDG_TRY(bm_extract_meta(p->bm, p->xstream, p->nodes[nslot], n_dev, p->cap, p->alias[par], par));
+                // option bm_split_move: X rows move right after the acquire (hits read their pinned
+                // slots, misses the table), the misses' slot fills after the bind
+                const bool split = g_bm_split_move && !cs && !p->ctx->host_table &&
+                                   (p->ctx->row_bytes == 400 || p->ctx->row_bytes == 512 || p->ctx->row_bytes == 1024);
+                FDG_TRY(bm_extract_meta(p->bm, p->xstream, p->nodes[nslot], n_dev, p->cap, p->alias[par], par,
+                                        split ? p->acquired[par] : nullptr));
+                if (split) {
+                    FDG_CUDA(cudaStreamWaitEvent(xe, p->acquired[par], 0));
+                    FDG_TRY(bm_extract_move(p->bm, xe, p->nodes[nslot], n_dev, p->cap, p->alias[par], X, nullptr, par, 1));
+                }
                 // option bm_move_early: batch j's move may start right after its bind, next to release j-1
                 // (measured 517 -> 538 us per Papers batch: off)
                 if (g_bm_move_early) FDG_CUDA(cudaEventRecord(p->bound[par], p->xstream));
@@ -599,7 +613,8 @@ int fdg_pipeline_run_ragged(fdg_pipeline* p, const uint64_t* seeds, int seeds_on
                 if (!g_bm_move_early) FDG_CUDA(cudaEventRecord(p->bound[par], p->xstream));
                 FDG_CUDA(cudaStreamWaitEvent(xe, p->bound[par], 0));
                 if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j], xe));
-                FDG_TRY(bm_extract_move(p->bm, xe, p->nodes[nslot], n_dev, p->cap, p->alias[par], X, cs, par));
+                FDG_TRY(bm_extract_move(p->bm, xe, p->nodes[nslot], n_dev, p->cap, p->alias[par], X, cs, par,
+                                        split ? 2 : 0));
                 if (extract_ms) FDG_CUDA(cudaEventRecord(p->tev[2 * j + 1], xe));
                 FDG_TRY(bm_status_to(p->bm, xe, &cnt->status));  // e.g. CAPACITY = StandbyTimeout
                 if (train) {  // the trainer consumes X (and the batch's blocks) before they are reused

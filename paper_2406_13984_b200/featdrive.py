@@ -554,6 +554,12 @@ class Pipeline:
         """lr != 0: the train stage also runs backward + SGD after every forward."""
         check(lib().fdg_pipeline_set_training(self.ptr, lr))
 
+    def bm_stats(self) -> dict:
+        """Cumulative counters of the runner's buffer manager (BufferManager::stats())."""
+        s = BmStats()
+        check(lib().fdg_pipeline_bm_stats(self.ptr, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in BmStats._fields_}
+
     def losses(self, n: int, first: int = 0) -> np.ndarray:
         out = np.empty(n, np.float32)
         check(lib().fdg_pipeline_losses(self.ptr, first, n, _p(out)))

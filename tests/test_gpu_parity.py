@@ -496,6 +496,34 @@ def test_pipeline_runner_matches_host_api(fd, samplers, group, bm):
         assert int(recs["checksum"][b]) == cs, f"batch {b}"
 
 
+def test_pipeline_bm_split_move(fd):
+    """Config 3's split row move (X rows right after the acquire, the misses' slot fills after the
+    bind; option bm_split_move) against the one-pass move: the train stage's per-batch losses (a
+    function of X, whose hits read the slots earlier batches filled) and the buffer manager's
+    counters are identical."""
+    n, B, fan, dim = 120_000, 256, [10, 5], 128
+    t = fd.Topology.generate(n, dim, 12, 3)
+    order = np.concatenate(fd.partition_epoch(np.arange(24 * B, dtype=np.uint64), B, 77))
+    nb = 24
+    rng = np.array([fd.batch_seed(0, 0, b) for b in range(nb)], np.uint64)
+    out = []
+    old = fd.featdrive.get_option("bm_split_move")
+    try:
+        for split in (0, 1):
+            fd.set_option("bm_split_move", split)
+            model = fd.GraphSAGE(t, [dim, 32, 16], fan, max_seeds=B, seed=5)
+            pipe = fd.Pipeline(t, fan, B, buffer_slots=30_000, checksum=False, samplers=2)
+            pipe.set_model(model, label_seed=3)
+            recs = pipe.run_batches(order, rng)
+            assert np.all(recs["status"] == 0)
+            out.append((pipe.losses(nb).copy(), pipe.bm_stats()))
+            pipe.close()
+    finally:
+        fd.set_option("bm_split_move", old)
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+
+
 @pytest.mark.parametrize("group", [3, 5, 6, 7])
 def test_pipeline_prefetch_ring_odd_groups(fd, port, group):
     """Group sizes that do not divide the MT prefetch chunk (16): over 320 batches the ring
