@@ -747,6 +747,11 @@ int fdg_set_option(const char* key, int64_t v) {
         g_bm_move_impl = v;
         return FDG_OK;
     }
+    if (k == "hash_ctas") {
+        if (v < 0 || v > 4096) return fail(FDG_INVALID_ARG, "hash_ctas must be in [0, 4096]");
+        g_hash_ctas = v;
+        return FDG_OK;
+    }
     if (k == "hash_ctas_per_sm") {
         if (v < 0 || v > 4) return fail(FDG_INVALID_ARG, "hash_ctas_per_sm must be in [0, 4]");
         g_hash_ctas_per_sm = v;
@@ -827,6 +832,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "tma_cfg") *v = g_tma_cfg;
     else if (k == "hash_dyn") *v = g_hash_dyn;
     else if (k == "hash_ctas_per_sm") *v = g_hash_ctas_per_sm;
+    else if (k == "hash_ctas") *v = g_hash_ctas;
     else if (k == "bm_move_impl") *v = g_bm_move_impl;
     else if (k == "bm_move_grid") *v = g_bm_move_grid;
     else if (k == "bm_fuse_bind") *v = g_bm_fuse_bind;

@@ -635,7 +635,8 @@ int launch_hash_rb(const Ctx& c, cudaStream_t st, uint64_t groups, const uint64_
     const int ch = g_hash_chunk ? int(g_hash_chunk) : (c.row_bytes >= 256 ? 256 : 128);
     const int minb = ch == 128 ? HashRbShape<128>::MINB : HashRbShape<256>::MINB;
     const int per_sm = g_hash_ctas_per_sm > 0 ? int(g_hash_ctas_per_sm) : minb;
-    const int blocks = int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps, uint64_t(c.sm_count) * per_sm));
+    const uint64_t cap = g_hash_ctas > 0 ? uint64_t(g_hash_ctas) : uint64_t(c.sm_count) * per_sm;
+    const int blocks = int(std::min<uint64_t>((groups + kHpWarps - 1) / kHpWarps, cap));
     uint32_t* ctr = g_hash_dyn ? dyn_counter(c) : nullptr;
 #define FDG_HRB(R)                                                                                      \
     case R:                                                                                             \
@@ -906,6 +907,7 @@ int64_t g_hash_dyn = 0;
 // prefetch) fits beside them. One per SM: Papers pipeline with checksum 201.3 vs 204.0 us per
 // batch (products and Friendster unchanged; alone 156 vs 152 us).
 int64_t g_hash_ctas_per_sm = 1;
+int64_t g_hash_ctas = 0;  // option: an absolute CTA count for the fused gather + checksum (0: per SM)
 int64_t g_hash_chunk = 0;  // 0: 256-byte chunks for rows >= 256 B, else 128; or force 128 / 256
 int64_t g_checksum_impl = FDG_GATHER_LDG;
 

@@ -159,6 +159,7 @@ extern int64_t g_gather_pf64;         // 64-byte L2 fetch hint on table reads (0
 extern int g_gather_ctas_per_sm;      // chunk-striped gather: CTAs (512 threads) per SM
 extern int64_t g_rb_ctas_per_sm;      // row-group gather: CTAs (8 warps) per SM
 extern int64_t g_rb_chunk;            // row-group gather: 128- or 256-byte row chunks
+extern int64_t g_hash_ctas;           // fused gather + checksum: absolute CTA count (0: per SM)
 extern int64_t g_hash_ctas_per_sm;    // fused gather + checksum CTAs per SM (0 = min-blocks)
 extern int64_t g_hash_dyn;            // fused gather + checksum: dynamic row-group claims
 extern int64_t g_hash_chunk;          // k_gather_hash_rb staging chunk (0 = by row size)
