@@ -55,7 +55,10 @@ namespace {
 
 constexpr uint32_t kValid = 0x80000000u;
 constexpr uint64_t kNoNode = ~0ull;
-constexpr int kT = 256;        // threads per tile
+#ifndef FDG_BM_THREADS
+#define FDG_BM_THREADS 256
+#endif
+constexpr int kT = FDG_BM_THREADS;  // threads per tile
 constexpr int kI = 8;          // items per thread
 constexpr int kTileN = kT * kI;
 
