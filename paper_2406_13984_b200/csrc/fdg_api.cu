@@ -699,6 +699,11 @@ int fdg_set_option(const char* key, int64_t v) {
         g_early_bloom = v;
         return FDG_OK;
     }
+    if (k == "intern_lean") {
+        if (v < 0 || v > 2) return fail(FDG_INVALID_ARG, "intern_lean must be 0, 1 or 2");
+        g_intern_lean = v;
+        return FDG_OK;
+    }
     if (k == "early_fused") {
         if (v != 0 && v != 1) return fail(FDG_INVALID_ARG, "early_fused must be 0 or 1");
         g_early_fused = v;
@@ -839,6 +844,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "bm_move_hash") *v = g_bm_move_hash;
     else if (k == "hash_early_pct") *v = g_hash_early_pct;
     else if (k == "early_fused") *v = g_early_fused;
+    else if (k == "intern_lean") *v = g_intern_lean;
     else if (k == "early_bloom") *v = g_early_bloom;
     else if (k == "force_idx64") *v = g_force_idx64;
     else if (k == "bm_meta_prio") *v = g_bm_meta_prio;

@@ -184,6 +184,7 @@ extern int64_t g_l2_persist_mb;       // L2 set-aside for the samplers' hash tab
 extern int64_t g_hash_load_pct;       // batch hash sizing (load factor, %)
 extern int64_t g_force_idx64;         // test hook: u64 CSR indices (the N >= 2^32 kernels) for any N
 extern int64_t g_early_bloom;         // sampler: Bloom filter over the early table for the last layer's lookups
+extern int64_t g_intern_lean;         // sampler: lean next-frontier intern passes (0 never, 1 always, 2 pipelines without checksum)
 extern int64_t g_early_fused;         // sampler: seeds + layer 0 in one shared-memory CTA (k_early)
 extern int64_t g_hash_early_pct;      // early batch-hash table load factor (0: hash_load_pct)
 extern int64_t g_sampler_ctas_per_sm; // sampler kernels: CTA cap per SM per launch

@@ -39,6 +39,7 @@ int sampler_sample_group(Sampler* s, cudaStream_t st, uint32_t n, const uint64_t
 void sampler_capacity(const Sampler* s, uint64_t* max_nodes, uint64_t* max_edges);
 void sampler_hash_region(const Sampler* s, void** base, uint64_t* bytes);
 int bm_status_to(fdg_bm* b, cudaStream_t st, uint32_t* dst);
+void sampler_set_lean(Sampler* s, bool lean);
 int bm_extract_meta(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
                     int64_t* alias, uint32_t parity, cudaEvent_t after_acquire = nullptr);
 int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uint32_t* n_dev, uint64_t n_host,
@@ -276,6 +277,7 @@ int pipeline_build(fdg_pipeline* p, fdg_ctx* ctx, const uint32_t* fanouts, uint3
         Sampler* s = nullptr;
         int rc = sampler_create(ctx, cfg->batch_size, fanouts, n_layers, &s, G);
         if (rc) return rc;
+        sampler_set_lean(s, g_intern_lean == 1 || (g_intern_lean == 2 && !cfg->checksum));
         p->samplers.push_back(s);
         // the MT prefetch ring (2 chunks) is sized here: a run never allocates or synchronises
         FDG_TRY(sampler_reserve_ring(s, 2 * p->cfg.prefetch_group));

@@ -415,13 +415,16 @@ __device__ __forceinline__ void intern_tile(const Work<IdT>& W, uint32_t q, uint
 template <typename IdT>
 __device__ __forceinline__ void intern_tile_last(const Work<IdT>& W, uint32_t q, uint32_t epoch, uint32_t tile,
                                                  uint32_t P, uint32_t ntiles);
+template <typename IdT, bool SEEDS>
+__device__ __forceinline__ void intern_tile_next(const Work<IdT>& W, uint32_t q, uint32_t epoch, uint32_t tile,
+                                                 uint32_t P, uint32_t ntiles);
 
 // Persistent: a capped number of CTAs claim tiles in order (keeps SM slots free
 // for the concurrently running gather; look-back needs only claim order).
 // PACK (fanout of the next frontier <= 63): the warp scans carry (first, picks, draws)
 // packed in one u32 (6 + 11 + 11 bits); the last pass (no next frontier) counts first
 // occurrences with ballots alone.
-template <typename IdT, bool SEEDS, bool HAS_NEXT, bool PACK = false>
+template <typename IdT, bool SEEDS, bool HAS_NEXT, bool PACK = false, bool LEAN = false>
 __device__ __forceinline__ void intern_pass(const Work<IdT>& W, uint32_t q, uint32_t epoch) {
     __shared__ uint32_t s_tile;
     fdg_batch_counts* cnt = W.cnt;
@@ -435,6 +438,7 @@ __device__ __forceinline__ void intern_pass(const Work<IdT>& W, uint32_t q, uint
         __syncthreads();
         if (tile >= ntiles) return;
         if constexpr (!HAS_NEXT && !SEEDS) intern_tile_last<IdT>(W, q, epoch, tile, P, ntiles);
+        else if constexpr (HAS_NEXT && PACK && LEAN) intern_tile_next<IdT, SEEDS>(W, q, epoch, tile, P, ntiles);
         else intern_tile<IdT, SEEDS, HAS_NEXT, PACK>(W, q, epoch, tile, P, ntiles);
         __syncthreads();
     }
@@ -446,10 +450,10 @@ __device__ __forceinline__ void intern_pass(const Work<IdT>& W, uint32_t q, uint
 #ifndef FDG_INTERN_LAST_MINB
 #define FDG_INTERN_LAST_MINB 6  // 40 registers with the one-register-per-item last pass (intern_tile_last)
 #endif
-template <typename IdT, bool SEEDS, bool HAS_NEXT, bool PACK>
-__global__ void __launch_bounds__(kScanThreads, HAS_NEXT ? FDG_INTERN_MINB : FDG_INTERN_LAST_MINB) k_intern_s(const __grid_constant__ Group<IdT> G, uint32_t q,
+template <typename IdT, bool SEEDS, bool HAS_NEXT, bool PACK, bool LEAN = false>
+__global__ void __launch_bounds__(kScanThreads, HAS_NEXT ? (LEAN ? 3 : FDG_INTERN_MINB) : FDG_INTERN_LAST_MINB) k_intern_s(const __grid_constant__ Group<IdT> G, uint32_t q,
                                                            uint32_t epoch) {
-    intern_pass<IdT, SEEDS, HAS_NEXT, PACK>(G.w[blockIdx.y], q, epoch);
+    intern_pass<IdT, SEEDS, HAS_NEXT, PACK, LEAN>(G.w[blockIdx.y], q, epoch);
 }
 
 // Per-item scan values. Count-only (no next frontier): the first-occurrence bit, counted
@@ -796,6 +800,164 @@ __device__ __forceinline__ void intern_tile_last(const Work<IdT>& W, uint32_t q,
                 uint32_t bc;
                 if (tf == tile) {
                     bc = base;
+                } else {
+                    while (ld_volatile(W.tile_flag + tf) != (E | 2u)) {
+                    }
+                    __threadfence();
+                    const uint4 in = ld_volatile4(W.tile_incl + tf);
+                    bc = tf == 0 ? 0u : in.x - ld_volatile4(W.tile_agg + tf).x;
+                }
+                src = node_base + bc + ld_volatile_u16(W.rank + ebase + pf);
+            }
+            W.edges[2 * (ebase + p)] = src;
+        }
+    }
+}
+
+// The passes with a next frontier with the packed scan values in shared memory and the hash
+// slot re-read for the outputs (three per-item register arrays instead of six: 80 registers
+// instead of 128). Faster for the device-resident step (Papers 182.4 -> 178.4 us per batch)
+// but not next to the fused checksum gather (190.2 -> 191.3), so the runner picks it for
+// pipelines without the checksum (option intern_lean).
+template <typename IdT, bool SEEDS>
+__device__ __forceinline__ void intern_tile_next(const Work<IdT>& W, uint32_t q, uint32_t epoch, uint32_t tile,
+                                                 uint32_t P, uint32_t ntiles) {
+    using SV = ScanVal<true, true>;
+    __shared__ Tri s_row[kScanItems][kScanThreads / 32];
+    __shared__ Tri s_rowx[kScanItems];
+    __shared__ Tri s_excl, s_agg;
+    __shared__ uint32_t s_xe[kScanItems][kScanThreads];
+    fdg_batch_counts* cnt = W.cnt;
+    const uint32_t ebase = SEEDS ? 0 : cnt->layer_edges[q - 1];
+    const uint32_t node_base = cnt->layer_nodes[q];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t f = W.fan[q];
+    const uint32_t p0 = tile * kTile + tid;
+    IdT kv[kScanItems];
+    uint32_t dg[kScanItems];
+    uint64_t lo[kScanItems];
+    uint32_t first_mask = 0, valid_mask = 0;
+    {
+        uint32_t slot[kScanItems];
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            const uint32_t p = p0 + k * kScanThreads;
+            if (p < P) {
+                valid_mask |= 1u << k;
+                slot[k] = SEEDS ? W.seed_slot[p] : W.edges[2 * (ebase + p)];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k)
+            if (valid_mask & (1u << k)) {
+                IdT key;
+                uint32_t val;
+                W.tab.load(slot[k], key, val);
+                if (val == (kPend | (p0 + k * kScanThreads))) {
+                    first_mask |= 1u << k;
+                    kv[k] = key;
+                } else {
+                    kv[k] = IdT(val);
+                }
+            }
+    }
+    {
+        uint64_t hi[kScanItems];
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k)
+            if (first_mask & (1u << k)) {
+                lo[k] = ld_rand64(W.indptr + uint64_t(kv[k]));
+                hi[k] = ld_rand64(W.indptr + uint64_t(kv[k]) + 1);
+            }
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) dg[k] = (first_mask & (1u << k)) ? uint32_t(hi[k] - lo[k]) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const uint32_t c = (first_mask >> k) & 1u, d = dg[k];
+        const uint32_t v = SV::make(c, d < f ? d : f, d > f ? f : 0u);
+        const uint32_t in = SV::incl(v, lane);
+        s_xe[k][tid] = in - v;
+        if (lane == 31) s_row[k][warp] = SV::tri(in);
+    }
+    __syncthreads();
+    {
+        const int r = warp;
+        const Tri w = lane < kScanThreads / 32 ? s_row[r][lane] : Tri{0, 0, 0};
+        const Tri wi = warp_incl_scan(w, lane);
+        if (lane < kScanThreads / 32) s_row[r][lane] = Tri{wi.c - w.c, wi.p - w.p, wi.d - w.d};
+        if (lane == kScanThreads / 32 - 1) s_rowx[r] = wi;
+    }
+    __syncthreads();
+    const uint32_t E = (epoch & 0x3FFFFFFFu) << 2;
+    if (tid == 0) {
+        Tri run{0, 0, 0};
+        for (int r = 0; r < kScanItems; ++r) {
+            const Tri t = s_rowx[r];
+            s_rowx[r] = run;
+            run = run + t;
+        }
+        s_agg = run;
+        W.tile_agg[tile] = make_uint4(run.c, run.p, run.d, 0);
+        __threadfence();
+        atomicExch(W.tile_flag + tile, E | 1u);
+    }
+    __syncthreads();
+    if (!SEEDS) {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k)
+            if (first_mask & (1u << k))
+                W.rank[ebase + p0 + k * kScanThreads] =
+                    uint16_t(s_rowx[k].c + s_row[k][warp].c + SV::tri(s_xe[k][tid]).c);
+        __threadfence();
+        __syncthreads();
+    }
+    {
+        const Tri agg = s_agg;
+        const Tri excl = tri_lookback_cta(W.tile_flag, W.tile_agg, W.tile_incl, tile, epoch);
+        if (tid == 0) {
+            const Tri tot = excl + agg;
+            W.tile_incl[tile] = make_uint4(tot.c, tot.p, tot.d, 0);
+            __threadfence();
+            atomicExch(W.tile_flag + tile, E | 2u);
+            s_excl = excl;
+            if (tile == ntiles - 1) {
+                cnt->layer_nodes[q + 1] = node_base + tot.c;
+                cnt->n_nodes = node_base + tot.c;
+                cnt->layer_edges[q + 1] = cnt->layer_edges[q] + tot.p;
+                cnt->layer_draws[q + 1] = cnt->layer_draws[q] + tot.d;
+            }
+        }
+    }
+    __syncthreads();
+    const Tri base = s_excl;
+    const FrontierBuf fr = W.fr[q & 1];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (!(valid_mask & (1u << k))) continue;
+        const uint32_t p = p0 + k * kScanThreads;
+        if (first_mask & (1u << k)) {
+            const Tri ex = s_rowx[k] + s_row[k][warp] + SV::tri(s_xe[k][tid]);
+            const uint32_t r = base.c + ex.c;
+            const uint32_t local = node_base + r;
+            const IdT key = kv[k];
+            const uint32_t slot = SEEDS ? W.seed_slot[p] : W.edges[2 * (ebase + p)];
+            W.nodes[local] = uint64_t(key);
+            W.tab.finalize(slot, key, local);
+            W.tab.mark(key);
+            if (!SEEDS) W.edges[2 * (ebase + p)] = local;
+            fr.start[r] = lo[k];
+            fr.deg[r] = dg[k];
+            fr.pick_off[r] = base.p + ex.p;
+            fr.draw_off[r] = base.d + ex.d;
+        } else if (!SEEDS) {
+            uint32_t src = uint32_t(kv[k]);
+            if (src & kPend) {
+                const uint32_t pf = src & ~kPend;
+                const uint32_t tf = pf / kTile;
+                uint32_t bc;
+                if (tf == tile) {
+                    bc = base.c;
                 } else {
                     while (ld_volatile(W.tile_flag + tf) != (E | 2u)) {
                     }
@@ -1481,6 +1643,9 @@ int64_t g_hash_early_pct = 0;
 // 68.0 / 71.6 vs 69.9 / 72.0; products 181.9 vs 176.8): the early layers are latency, not
 // throughput, and 8 samplers in flight hide it. Off by default; parity-tested both ways.
 int64_t g_early_fused = 0;
+// Next-frontier intern passes in the lean form: 0 never, 1 always, 2 (default) in pipelines
+// without the fused checksum (the runner decides; host-API samplers use the general form).
+int64_t g_intern_lean = 2;
 // Bloom filter over the early table's keys for the last layer's lookups (see bloom_hash).
 int64_t g_early_bloom = 1;
 int64_t g_sampler_ctas_per_sm = 16;
@@ -1542,6 +1707,7 @@ struct Sampler {
     uint32_t bloom_bits = 0;  // early-table Bloom filter bits (0: none)
     bool small_f = true;
     bool early_fused = false;  // seeds + layer 0 in one shared-memory CTA per batch (k_early)
+    bool lean_next = false;    // next-frontier intern passes in the lean form (intern_tile_next)
     void* arena = nullptr;
     void* hash_all = nullptr;  // the lanes' last-layer tables, contiguous (one fill per group)
     void* hash_all_a = nullptr;  // the lanes' early tables, contiguous, right before hash_all
@@ -1659,11 +1825,13 @@ void launch_intern(Sampler& s, cudaStream_t st, const Group<IdT>& G, uint32_t n,
     const dim3 grid(uint32_t(std::min(tiles, cap)), n);
     const bool pack = has_next && s.fan[q] <= 63;
     if (seeds) {
-        if (pack) k_intern_s<IdT, true, true, true><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
+        if (pack && s.lean_next) k_intern_s<IdT, true, true, true, true><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
+        else if (pack) k_intern_s<IdT, true, true, true><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
         else if (has_next) k_intern_s<IdT, true, true, false><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
         else k_intern_s<IdT, true, false, false><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
     } else {
-        if (pack) k_intern_s<IdT, false, true, true><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
+        if (pack && s.lean_next) k_intern_s<IdT, false, true, true, true><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
+        else if (pack) k_intern_s<IdT, false, true, true><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
         else if (has_next) k_intern_s<IdT, false, true, false><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
         else k_intern_s<IdT, false, false, false><<<grid, kScanThreads, 0, st>>>(G, q, epoch);
     }
@@ -2071,6 +2239,7 @@ int sampler_debug_zero_word(Sampler* s, cudaStream_t st, uint64_t rng_seed, uint
 }
 
 void sampler_debug_reject(Sampler* s, int lane) { s->debug_reject = lane; }
+void sampler_set_lean(Sampler* s, bool lean) { s->lean_next = lean; }
 
 // A group of n <= gmax batches in one launch chain on `st`. MT words come from the
 // prefetch ring when present, else they are generated inline (one CTA per batch).

@@ -31,7 +31,7 @@ defaults = {"gather_impl": 4, "pipeline_gather_impl": 1, "gather_evict_first": 0
             "hash_clear": 1, "sampler_ctas_per_sm": 16, "gather_ctas_per_sm": 1,
             "extract_streams": 2, "hash_keep": 1,
             "checksum_impl": 1, "hash_chunk": 0, "gather_pf64": 2, "rb_ctas_per_sm": 2, "rb_chunk": 256, "sampler_sms": 0, "tma_cfg": 0,
-            "replay": 1, "mt_adaptive": 1, "hash_dyn": 0, "hash_ctas_per_sm": 1, "bm_move_impl": 2, "bm_move_grid": 0, "bm_meta_prio": 0, "hash_early_pct": 0, "early_fused": 0, "bm_fuse_bind": 1, "bm_move_hash": 1, "bm_move_early": 0, "early_bloom": 1, "extract_prio": 2, "pipe_slots": 0, "bm_split_move": 0, "hash_ctas": 0}
+            "replay": 1, "mt_adaptive": 1, "hash_dyn": 0, "hash_ctas_per_sm": 1, "bm_move_impl": 2, "bm_move_grid": 0, "bm_meta_prio": 0, "hash_early_pct": 0, "early_fused": 0, "bm_fuse_bind": 1, "bm_move_hash": 1, "bm_move_early": 0, "early_bloom": 1, "extract_prio": 2, "pipe_slots": 0, "bm_split_move": 0, "hash_ctas": 0, "intern_lean": 2}
 for spec in sys.argv[1:]:
     kv = dict(x.split("=") for x in spec.split(",") if x)
     S = int(kv.pop("S", 2))

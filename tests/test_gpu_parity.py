@@ -473,9 +473,9 @@ def test_buffer_manager_capacity_and_invariants(fd):
 
 
 # ------------------------------------------------------------ native runner --
-@pytest.mark.parametrize("samplers,group,bm", [(1, 1, False), (2, 1, False), (2, 4, False), (3, 8, False),
-                                               (2, 2, True)])
-def test_pipeline_runner_matches_host_api(fd, samplers, group, bm):
+@pytest.mark.parametrize("samplers,group,bm,lean", [(1, 1, False, 2), (2, 1, False, 1), (2, 4, False, 2),
+                                                    (3, 8, False, 1), (2, 2, True, 1)])
+def test_pipeline_runner_matches_host_api(fd, samplers, group, bm, lean):
     """fdg_pipeline_run (pipelined, grouped, optional buffer manager) produces the same
     per-batch node/edge counts and trainer checksums as sample_khop + gather."""
     n, B, fan = 300_000, 256, [10, 5, 5]
@@ -483,8 +483,13 @@ def test_pipeline_runner_matches_host_api(fd, samplers, group, bm):
     order = np.concatenate(fd.partition_epoch(np.arange(20 * B, dtype=np.uint64), B, 1234))
     nb = 20
     rng = np.array([fd.batch_seed(0, 0, b) for b in range(nb)], np.uint64)
-    pipe = fd.Pipeline(t, fan, B, buffer_slots=(200_000 if bm else None), checksum=True, samplers=samplers,
-                       group_batches=group)
+    old = fd.featdrive.get_option("intern_lean")  # 1: the lean next-frontier passes (option intern_lean)
+    fd.set_option("intern_lean", lean)
+    try:
+        pipe = fd.Pipeline(t, fan, B, buffer_slots=(200_000 if bm else None), checksum=True, samplers=samplers,
+                           group_batches=group)
+    finally:
+        fd.set_option("intern_lean", old)
     recs = pipe.run_batches(order, rng)
     pipe.close()
     assert np.all(recs["status"] == 0)
