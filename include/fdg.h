@@ -215,7 +215,15 @@ int fdg_set_gather_impl(int impl);
  * sizing), "extract_streams" (1/2), "sage_gemm" (1 tcgen05 3xTF32, 0 CUDA cores),
  * "bm_overlap" (buffer-manager row move on its own stream), "sampler_sms" (> 0: pipeline
  * samplers on a green-context SM partition of that size, extraction on the rest; measured
- * slower than sharing, default 0), "tma_cfg" (TMA gather ring shape 0-3). */
+ * slower than sharing, default 0), "tma_cfg" (TMA gather ring shape 0-3).
+ * Round 2: "early_bloom" (Bloom filter before the last layer's early-table lookups, 1),
+ * "intern_lean" (lean next-frontier intern passes: 0 never, 1 always, 2 pipelines without the
+ * checksum), "early_fused" (seeds + layer 0 in one shared-memory CTA, 0), "bm_fuse_bind" (1),
+ * "bm_move_impl" (0 LDG, 1 TMA, 2 row groups), "bm_move_hash" (move + checksum in one pass, 1),
+ * "bm_split_move" (0), "extract_prio" (0, 1, 2 = with the buffer manager), "records_stream" (1),
+ * "hash_ctas_per_sm" (1) / "hash_ctas" (0), "pipe_slots" (0 = 2 x samplers x group),
+ * "tc_write_hi" (read-only: the kind::tf32 truncation check), "force_idx64" (test hook).
+ * Loading the library sets CUDA_DEVICE_MAX_CONNECTIONS=32 unless the process already did. */
 int fdg_set_option(const char* key, int64_t value);
 int fdg_get_option(const char* key, int64_t* value);
 /* Checksum of rows already resident (region slot payloads addressed by alias). */
