@@ -984,7 +984,10 @@ namespace {
 
 uint32_t n_tiles_for(uint64_t n) { return uint32_t(std::max<uint64_t>(1, (n + kTileN - 1) / kTileN)); }
 
-int bm_persistent_grid(const Bm* b) { return b->ctx->sm_count * 2; }
+#ifndef FDG_BM_PERSIST
+#define FDG_BM_PERSIST 2
+#endif
+int bm_persistent_grid(const Bm* b) { return b->ctx->sm_count * FDG_BM_PERSIST; }
 
 }  // namespace
 
