@@ -699,6 +699,11 @@ int fdg_set_option(const char* key, int64_t v) {
         g_early_bloom = v;
         return FDG_OK;
     }
+    if (k == "host_tier_pf") {
+        if (v < 0 || v > 2) return fail(FDG_INVALID_ARG, "host_tier_pf must be 0, 1 or 2");
+        g_host_tier_pf = v;
+        return FDG_OK;
+    }
     if (k == "intern_lean") {
         if (v < 0 || v > 2) return fail(FDG_INVALID_ARG, "intern_lean must be 0, 1 or 2");
         g_intern_lean = v;
@@ -845,6 +850,7 @@ int fdg_get_option(const char* key, int64_t* v) {
     else if (k == "hash_early_pct") *v = g_hash_early_pct;
     else if (k == "early_fused") *v = g_early_fused;
     else if (k == "intern_lean") *v = g_intern_lean;
+    else if (k == "host_tier_pf") *v = g_host_tier_pf;
     else if (k == "early_bloom") *v = g_early_bloom;
     else if (k == "force_idx64") *v = g_force_idx64;
     else if (k == "bm_meta_prio") *v = g_bm_meta_prio;

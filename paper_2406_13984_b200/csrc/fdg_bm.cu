@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(256) k_move_keys(const uint64_t* nodes, const 
 // Chunk-striped over the sorted (position) list: 16-byte chunks, 4 loads in flight per thread.
 __global__ void __launch_bounds__(512) k_move_sorted(BmDev B, const uint32_t* keys, const uint32_t* pos,
                                                      uint64_t bound, const int64_t* alias, const char* table,
-                                                     char* region, uint32_t rb, char* X) {
+                                                     char* region, uint32_t rb, char* X, int pf) {
     if (B.st->status) return;
     const uint32_t cpr = rb / 16;
     const uint64_t total = bound * cpr;
@@ -625,9 +625,19 @@ __global__ void __launch_bounds__(512) k_move_sorted(BmDev B, const uint32_t* ke
             if (k[u] == 0xFFFFFFFFu) continue;  // past the batch
             const char* src = k[u] != 0xFFFFFFFEu ? table + uint64_t(k[u]) * rb : region + uint64_t(alias[p[u]]) * rb;
             if (k[u] == 0xFFFFFFFEu && !X) continue;  // a hit without X: nothing to move
-            asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
-                         : "l"(reinterpret_cast<const uint4*>(src) + col[u]));
+            const uint4* a = reinterpret_cast<const uint4*>(src) + col[u];
+            if (pf == 2)  // larger read requests over PCIe (option host_tier_pf)
+                asm volatile("ld.global.nc.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                             : "l"(a));
+            else if (pf == 1)
+                asm volatile("ld.global.nc.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                             : "l"(a));
+            else
+                asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                             : "l"(a));
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -975,6 +985,7 @@ using namespace fdg;
 
 int64_t fdg::g_bm_eager = 0;
 int64_t fdg::g_bm_sorted_move = 1;
+int64_t fdg::g_host_tier_pf = 0;
 int64_t fdg::g_bm_move_impl = 2;  // row-group move (k_move_hash_rb without the hash): 524.7 -> 514.4 us per batch
 int64_t fdg::g_bm_move_grid = 0;
 int64_t fdg::g_bm_move_hash = 1;
@@ -1222,7 +1233,7 @@ int bm_extract_move(fdg_bm* b, cudaStream_t st, const uint64_t* nodes, const uin
         size_t tb = b->sort_tmp_bytes;
         FDG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, pin, pout, int64_t(n_host), 0, 32, st));
         k_move_sorted<<<blocks, 512, 0, st>>>(d, kout, pout, n_host, alias, table, b->region, rb,
-                                              static_cast<char*>(out));
+                                              static_cast<char*>(out), int(g_host_tier_pf));
     } else if (!host && g_bm_move_impl == 1 && rb <= 4096) {
         FDG_TRACE("bm_move", st);
         constexpr int D = 8, A = 6;

@@ -179,6 +179,7 @@ extern int64_t g_extract_prio;        // pipeline: extraction streams above the 
 extern int64_t g_bm_move_early;       // pipeline: batch j's row move starts after its bind, not after release j-1
 extern int64_t g_bm_meta_prio;        // pipeline: the buffer manager's metadata stream at high priority
 extern int64_t g_bm_move_impl;        // buffer-manager row move: 0 LDG (k_move), 1 TMA bulk copies (k_move_tma)
+extern int64_t g_host_tier_pf;        // host-resident table: prefetch-size hint on the row reads (0, 1 = 128B, 2 = 256B)
 extern int64_t g_bm_sorted_move;      // host-resident table: move the misses in node-id order
 extern int64_t g_l2_persist_mb;       // L2 set-aside for the samplers' hash tables (0 off)
 extern int64_t g_hash_load_pct;       // batch hash sizing (load factor, %)
